@@ -1,0 +1,36 @@
+"""Exception types with the reference's names and meaning.
+
+Reference definitions (``pkg/src/schedtune``): ``ScheduleError`` and
+``InvalidActionError`` (schedspace.py:23-32), ``RlDivergedError``
+(rlcore.py:20-21), ``CostModelError`` (costmodel.py:20-21), ``WorkloadError``
+(workload.py:19-20).  ``DeviceError`` is new: a CUDA/ABI failure, or the
+native library missing on a GPU box (there is no CPU fallback).
+"""
+
+
+class WorkloadError(ValueError):
+    """Unreadable or semantically invalid workload description."""
+
+
+class ScheduleError(ValueError):
+    """Malformed schedule state."""
+
+
+class InvalidActionError(ValueError):
+    """A modification violates its subspace constraints."""
+
+    def __init__(self, subspace: str, detail: str):
+        super().__init__(f"invalid {subspace} action: {detail}")
+        self.subspace = subspace
+
+
+class RlDivergedError(RuntimeError):
+    """A loss or gradient stopped being finite."""
+
+
+class CostModelError(ValueError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    """The B200 path failed (CUDA error, missing native library, bad call)."""

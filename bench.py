@@ -1,0 +1,507 @@
+"""Benchmark: schedules/sec of the HARL inner search step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config c2|c1|c3|c5] [--population P]
+
+A bench "step" is one ``_run_episode`` (tuner.py:350-440) over the whole
+population: initial sampling, every search step of the default geometry
+(cull_window 20, episode_len 40 -> 20 steps at P tracks, a cull to P/2, 40
+steps at P/2, PPO every 2 steps), i.e. P*40 visited schedules.  The unit of
+work is one visited schedule (one CandidateEntry, tuner.py:408-412).
+
+* ``value``: whole-job schedules/s with the population resident in HBM,
+  device time via CUDA events on the launching stream, summed over the K
+  timed episodes (L2 flushed between episodes, outside the events), max over
+  ranks.
+* ``e2e``: the same metric through the host-buffer call a drop-in makes per
+  episode: agent parameters/moments, replay ring, forest and generator state
+  go host->device before and the visited entries (states, scores, rewards)
+  plus the updated agent/ring come back device->host after, every episode.
+* ``cpu_baseline``: the oracle (numpy restatement of the reference, bit-exact
+  with it) timed on this host on a bounded sample of the same workload.
+* ``--impl reference``: the reference CPU path (the oracle port) with all
+  host cores, one independent session per core (the reference's own
+  process-pool model, cli.py:231-235), same metric.
+
+Synthetic data: random-init weights of the reference architecture, a
+synthetic depth-6 50-tree GBT forest with thresholds drawn from real feature
+values (no measurements are available offline).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "schedules/sec (RL step+featurize+cost model) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "schedules/s"
+
+CONFIGS = {
+    "c1": dict(workload="GEMM 1024x1024x1024 (gemm_l.yaml gemm_1024x1024x1024), "
+               "sketch k0", yaml="""
+subgraphs:
+  - id: gemm_1024x1024x1024
+    nodes: [{name: mm, kind: matmul, shape: {m: 1024, k: 1024, n: 1024}}]
+""", sketch=0, population=1024),
+    "c2": dict(workload="conv2d ResNet-50 stage-3 3x3 (conv2d.yaml "
+               "c2d_14x256x256_k3), sketch k0", yaml="""
+subgraphs:
+  - id: c2d_14x256x256_k3
+    nodes:
+      - name: conv
+        kind: conv2d
+        shape: {n: 1, h: 14, w: 14, ci: 256, co: 256, kernel: 3, stride: 1, padding: 1}
+""", sketch=0, population=16384),
+    "c3": dict(workload="BERT-base batched GEMM + softmax subgraph "
+               "(bmm 12x128x64x128 -> softmax), sketch k3", yaml="""
+subgraphs:
+  - id: bgemm_softmax
+    weight: 12
+    nodes:
+      - name: bmm
+        kind: batch_matmul
+        shape: {b: 12, m: 128, k: 64, n: 128}
+        consumers: [sm]
+      - name: sm
+        kind: softmax
+        shape: {heads: 12, q: 128, k: 128}
+""", sketch=3, population=65536),
+    "c5": dict(workload="GEMM 4096^3, sketch k0", yaml="""
+subgraphs:
+  - id: gemm_4096x4096x4096
+    nodes: [{name: mm, kind: matmul, shape: {m: 4096, k: 4096, n: 4096}}]
+""", sketch=0, population=65536),
+}
+
+
+# ---------------------------------------------------------------------------
+# workload construction (shared by the GPU and CPU legs)
+
+
+def synthetic_forest(tables, seed: int, n_trees: int = 50, depth: int = 6):
+    """50 trees of depth <= 6 (the reference's GbtConfig defaults,
+    costmodel.py:24-31) splitting on features that actually vary, with
+    thresholds at feature values of random states so walks branch."""
+    from oracle.harl_oracle import featurize, sample_initial  # host-only
+    rng = np.random.default_rng(seed)
+    tiles, knobs = sample_initial(tables, 512, rng)
+    X = featurize(tables, tiles, knobs)
+    varying = np.flatnonzero(X.std(axis=0) > 0)
+    trees = []
+    for _ in range(n_trees):
+        feat, thr, left, right, val = [], [], [], [], []
+
+        def add(d):
+            i = len(feat)
+            feat.append(-1)
+            thr.append(0.0)
+            left.append(-1)
+            right.append(-1)
+            val.append(0.0)
+            if d < depth and rng.random() < 0.92:
+                f = int(rng.choice(varying))
+                feat[i] = f
+                thr[i] = float(X[int(rng.integers(len(X))), f])
+                left[i] = add(d + 1)
+                right[i] = add(d + 1)
+            else:
+                val[i] = float(rng.normal(0.0, 0.05))
+            return i
+        add(0)
+        trees.append(tuple(np.asarray(a) for a in (feat, thr, left, right,
+                                                   val)))
+    return trees
+
+
+def build_workload(cfg_name: str, population: int | None, seed: int = 0):
+    from paper_2211_11172_b200 import workloads as W
+    from paper_2211_11172_b200.agent import RlConfig, init_session_agents
+    from paper_2211_11172_b200.space import SketchTables
+    c = CONFIGS[cfg_name]
+    net = W.loads_network(c["yaml"])
+    target = W.TargetConfig()
+    sg = net.subgraphs[0]
+    ks = W.generate_sketches(sg, target)
+    S = max(k.space.num_tile_slots for k in ks)
+    tables = SketchTables(sg, ks[c["sketch"]], target, S)
+    rl = RlConfig()
+    agent = init_session_agents([(sg.id, S)], tables.feature_len, rl,
+                                np.random.default_rng(seed))[sg.id]
+    P = population or c["population"]
+    return dict(tables=tables, agent=agent, rl=rl, P=P, cfg=c,
+                trees=synthetic_forest(tables, seed + 1), base=0.5, lr=0.3)
+
+
+def episode_config(P):
+    from paper_2211_11172_b200.engine import EpisodeConfig
+    # TunerConfig defaults with min_tracks = P/2, initial_tracks = P
+    return EpisodeConfig(tracks=P, track_len=40, cull_window=20,
+                         cull_fraction=0.5, min_tracks=P // 2)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+
+class ClockSampler:
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs
+
+
+def cpu_episode_sample(cfg_name, P, steps, seed=0):
+    """Oracle episode on P tracks for `steps` search steps; returns
+    (visits, seconds)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import harl_oracle as O
+    w = build_workload(cfg_name, P, seed)
+    a = w["agent"]
+    oa = O.Agent.from_param_lists(a.policy, a.value, len(a.hidden))
+    opi = O.Adam.zeros_like(oa.policy_params(), w["rl"].lr_actor)
+    ov = O.Adam.zeros_like(oa.value_params(), w["rl"].lr_critic)
+    model = O.GbtModel(w["base"], w["lr"], True, w["trees"])
+    ecfg = O.EpisodeCfg(tracks=P, track_len=steps, cull_window=20,
+                        cull_fraction=0.5, min_tracks=P // 2,
+                        rl_cfg=O.RlCfg())
+    t = time.perf_counter()
+    entries, _, _ = O.run_episode(w["tables"], w["tables"].num_slots, ecfg,
+                                  oa, opi, ov, O.Replay(4096), model,
+                                  np.random.default_rng(seed + 7), 0)
+    return len(entries), time.perf_counter() - t
+
+
+def _cpu_worker(args):
+    cfg_name, P, steps, seed = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    return cpu_episode_sample(cfg_name, P, steps, seed)
+
+
+def cpu_parallel(cfg_name, P, steps, procs):
+    """The reference's own parallelism model: independent sessions in a
+    process pool (cli.py:231-235), P/procs tracks each."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    per = max(2, P // procs)
+    t = time.perf_counter()
+    with ProcessPoolExecutor(procs, mp_context=mp.get_context("spawn")) as ex:
+        res = list(ex.map(_cpu_worker, [(cfg_name, per, steps, s)
+                                        for s in range(procs)]))
+    wall = time.perf_counter() - t
+    visits = sum(v for v, _ in res)
+    slowest = max(s for _, s in res)
+    return visits, slowest, wall
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+
+
+def l2_flush(torch, dev, buf=[]):
+    if not buf:
+        buf.append(torch.empty(256 << 20, dtype=torch.uint8, device=dev))
+    buf[0].fill_(1)
+
+
+def run_gpu(args, rank, world):
+    import torch
+    from paper_2211_11172_b200 import device as D
+    from paper_2211_11172_b200 import profiling
+    from paper_2211_11172_b200.engine import EpisodeEngine
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    w = build_workload(args.config, args.population, seed=rank)
+    P = w["P"]
+    tb = w["tables"]
+    ecfg = episode_config(P)
+    eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, dev)
+    forest = D.DeviceForest(w["trees"], w["base"], w["lr"], device=dev)
+    gen = np.random.default_rng(1000 + rank)
+    stream = torch.cuda.current_stream()
+    order = 0
+    for _ in range(args.warmup):
+        res = eng.run_episode(tb, forest, gen, ecfg, order)
+        order += res.visits
+    torch.cuda.synchronize()
+    profiling.reset()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = 0.0
+    visits = 0
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            l2_flush(torch, dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            res = eng.run_episode(tb, forest, gen, ecfg, order)
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            visits += res.visits
+            order += res.visits
+    torch.cuda.synchronize()
+    launches = profiling.launch_count()
+    kstats = profiling.kernel_times()
+    if world > 1:
+        dist.barrier()
+    # ---- e2e: host buffers in and out every episode ------------------------
+    e2e_ms, h2d, d2h, e2e_visits = 0.0, 0, 0, 0
+    for _ in range(max(1, min(args.steps, 3))):
+        l2_flush(torch, dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b_in, b_out, v = e2e_episode(eng, w, forest, gen, ecfg, order, dev)
+        torch.cuda.synchronize()
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+        h2d, d2h = b_in, b_out
+        e2e_visits += v
+        order += v
+    return dict(total_ms=total_ms, visits=visits, clocks=clk.summary(),
+                launches=launches, kstats=kstats, e2e_ms=e2e_ms,
+                e2e_visits=e2e_visits, h2d=h2d, d2h=d2h, P=P)
+
+
+def e2e_episode(eng, w, forest_unused, gen, ecfg, order, dev):
+    """One drop-in episode with every input from host memory and every
+    output returned to host memory (what the reference-facing wrapper
+    does per round)."""
+    import torch
+    from paper_2211_11172_b200 import device as D
+    tb = w["tables"]
+    nbytes_in = 0
+    # agent params + moments + replay ring + forest from pinned host memory
+    eng.dagent.upload()
+    nbytes_in += 3 * eng.dagent.n_params * 8
+    ring = eng.replay
+    host_ring = {k: getattr(ring, k).cpu().pin_memory()
+                 for k in ("X", "Xn", "actions", "scalars", "move_bits",
+                           "shift_bits")}
+    for k, v in host_ring.items():
+        getattr(ring, k).copy_(v, non_blocking=True)
+        nbytes_in += v.numel() * v.element_size()
+    forest = D.DeviceForest(w["trees"], w["base"], w["lr"], device=dev)
+    nbytes_in += sum(t.numel() * t.element_size() for t in (
+        forest.feature, forest.left, forest.right, forest.threshold,
+        forest.leaf_contrib, forest.tree_first))
+    res = eng.run_episode(tb, forest, gen, ecfg, order)
+    tiles, knobs = res.states()
+    scores = res.scores()
+    rewards = res.log_reward[:res.visits].cpu().numpy()
+    eng.dagent.download()
+    out = ring.export(tb.num_slots, tb.levels)
+    nbytes_out = tiles.nbytes + knobs.nbytes + scores.nbytes + rewards.nbytes
+    nbytes_out += 3 * eng.dagent.n_params * 8
+    nbytes_out += sum(np.asarray(v).nbytes for k, v in out.items()
+                      if k != "masks")
+    return nbytes_in, nbytes_out, res.visits
+
+
+def roofline_entry(kstats, visits_per_episode, steps, tables, hidden):
+    """Dominant kernel's achieved rate vs the measured peak."""
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    if not kstats:
+        return None
+    top = max(kstats.items(), key=lambda kv: kv[1]["ms"])
+    name, st = top
+    F, H = tables.feature_len, hidden
+    C = len(tables.head_cols)
+    pol_flops = 2 * (F * H + H * H + H * (C + 9))
+    val_flops = 2 * (F * H + H * H + H)
+    per_row = {"policy": pol_flops, "value": val_flops}
+    if name in per_row:
+        flops = per_row[name] * st["rows"]
+        tf = flops / (st["ms"] * 1e-3) / 1e12
+        peak = peaks.get("bf16_tflops", 1590.0) / 2.0
+        return {"kernel": name, "bound": "tensor", "achieved": round(tf, 3),
+                "peak": peak, "unit": "TFLOP/s", "frac": round(tf / peak, 5),
+                "traffic": None,
+                "peak_note": "TF32 dense peak taken as measured bf16/2 "
+                             "(MEASURED_PEAKS.json); kernel is FFMA fp32"}
+    byts = {"featurize": 2 * tables.local_slots + 3 + 8 * F,
+            "gbt": 8 * F + 16, "finish": 120}.get(name, 64) * st["rows"]
+    gbs = byts / (st["ms"] * 1e-3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    return {"kernel": name, "bound": "hbm", "achieved": round(gbs, 2),
+            "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 5),
+            "traffic": None}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--population", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    cfgd = CONFIGS[args.config]
+    P = args.population or cfgd["population"]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        reference_arm(args, P, cfgd)
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    r = run_gpu(args, rank, world)
+    total_ms, e2e_ms = r["total_ms"], r["e2e_ms"]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64,
+                         device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_ms = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    visits_all = r["visits"] * world
+    value = visits_all / (total_ms / 1e3)
+    e2e = r["e2e_visits"] * world / (e2e_ms / 1e3)
+    tb = build_workload(args.config, P)["tables"]
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 networks + fp64 features/GBT/PPO",
+        "data": "synthetic (random-init reference architecture, synthetic "
+                "50-tree depth-6 GBT)",
+        "config": {"workload": cfgd["workload"], "population_per_gpu": P,
+                   "episode": "cull_window 20, episode_len 40, "
+                              "min_tracks P/2 (60 steps, P*40 visits)",
+                   "hidden": [128, 128], "step": "one full _run_episode",
+                   "l2": "flushed (256 MiB write) between timed episodes",
+                   "parallelism": f"independent task replicas x{world}"
+                   if world > 1 else "single GPU"},
+        "e2e": {"value": round(e2e, 1), "unit": UNIT,
+                "h2d_bytes_per_step": int(r["h2d"]),
+                "d2h_bytes_per_step": int(r["d2h"])},
+        "gpu_launches": int(r["launches"]),
+        "clocks": r["clocks"],
+        "roofline": roofline_entry(r["kstats"], P * 40, args.steps, tb, 128),
+        "kernel_ms_per_episode": {k: round(v["ms"] / args.steps, 4)
+                                  for k, v in r["kstats"].items()},
+    }
+    if not args.no_cpu_baseline:
+        steps = 2
+        visits, secs = cpu_episode_sample(args.config, P, steps)
+        line["cpu_baseline"] = {
+            "value": round(visits / secs, 1), "unit": UNIT, "cores": 1,
+            "kind": "port",
+            "sample": f"oracle episode, {P} tracks x {steps} steps "
+                      f"({visits} visits) on 1 core, OPENBLAS_NUM_THREADS=1"}
+    print(json.dumps(line))
+
+
+def reference_arm(args, P, cfgd):
+    procs = len(os.sched_getaffinity(0))
+    steps = 2
+    # each "step" of the reference arm: one bounded sample of the workload
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_parallel(args.config, min(P, 2048), 1, min(procs, 2))
+    tot_v, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        v, slowest, wall = cpu_parallel(args.config, P, steps, procs)
+        tot_v += v
+        tot_s += slowest
+    value = tot_v / tot_s
+    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT,
+            "impl": "reference", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * tot_s / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp64 (numpy)", "data": "synthetic",
+            "config": {"workload": cfgd["workload"], "population": P,
+                       "sample": f"{procs} processes x {P // procs} tracks x "
+                                 f"{steps} steps per timed step"},
+            "cpu_baseline": {"value": round(value, 1), "unit": UNIT,
+                             "cores": procs, "kind": "port",
+                             "sample": f"{procs} independent oracle sessions "
+                                       f"x {max(2, P // procs)} tracks x "
+                                       f"{steps} steps"},
+            "e2e": {"value": round(value, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

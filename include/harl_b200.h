@@ -1,0 +1,305 @@
+/*
+ * harl_b200.h — C ABI of the B200-native HARL inner search step.
+ *
+ * The reference (arXiv 2211.11172 "schedtune", pure Python/numpy) has no
+ * native boundary; the functions below are exactly what its Python API for
+ * this path would bind through ctypes.  Each entry
+ * names the reference function it replaces (paths relative to
+ * /root/reference/pkg/src/schedtune).
+ *
+ * Conventions
+ *   - Plain C types only; every array argument is a DEVICE pointer unless
+ *     the parameter name ends in `_host`.  `stream` is a cudaStream_t passed
+ *     as void*.  The library never allocates or frees caller memory; scratch
+ *     space is passed in by the caller.
+ *   - Return 0 on success, a negative HARL_E* code otherwise; the message is
+ *     available from harl_last_error().  Per-candidate failures that the
+ *     reference reports as Python exceptions (InvalidActionError with its
+ *     subspace, RlDivergedError) come back through an int32 status array
+ *     written on device (see HARL_ST_*), and the Python layer raises the same
+ *     exception types.
+ *   - Population arrays are structure-of-arrays: tiles are uint16
+ *     [slot][ld] (slot-major, leading dimension `ld` >= n), knobs are uint8
+ *     [3][ld] (compute-at index, parallel fuse count, unroll index),
+ *     features are float64 row-major [n][F].
+ */
+#ifndef HARL_B200_H
+#define HARL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HARL_ABI_VERSION 1
+
+#define HARL_MAX_DIMS 16
+#define HARL_MAX_LEVELS 8
+#define HARL_MAX_SLOTS 64
+#define HARL_MAX_STAGES 16
+#define HARL_MAX_TENSORS 48
+#define HARL_MAX_TERMS 160
+#define HARL_MAX_HEAD0 512   /* compact tiling-head columns, S*(L-1)+1 */
+#define HARL_MAX_LAYERS 4
+#define HARL_MAX_HIDDEN 256
+#define HARL_MAX_FEATURES 128
+
+/* error codes */
+#define HARL_OK 0
+#define HARL_E_ARG (-1)
+#define HARL_E_CUDA (-2)
+#define HARL_E_LIMIT (-3)
+
+/* per-candidate status (first failing row wins, like the reference's
+ * sequential loop); code values */
+#define HARL_ST_OK 0
+#define HARL_ST_TILING 1        /* InvalidActionError("tiling", ...) */
+#define HARL_ST_COMPUTE_AT 2    /* InvalidActionError("compute_at", ...) */
+#define HARL_ST_PARALLEL 3      /* InvalidActionError("parallel", ...) */
+#define HARL_ST_UNROLL 4        /* InvalidActionError("unroll", ...) */
+#define HARL_ST_NO_VALID 5      /* RlDivergedError: all-masked row */
+#define HARL_ST_NONFINITE 6     /* RlDivergedError: non-finite loss/grad */
+
+/* Per-sketch constant tables.  Mirrors SketchContext.__init__
+ * (schedspace.py:324-368) plus the sampler/lookup tables; built on the
+ * host by paper_2211_11172_b200.space.SketchTables. */
+typedef struct harl_sketch_desc {
+  int32_t levels, ndims, local_slots, num_slots;
+  int32_t ncas, max_fusible, n_unroll, max_feature_dims, feature_len;
+  int32_t n_stages, n_tensors, n_terms, max_extent, n_head0;
+  int32_t extents[HARL_MAX_DIMS];
+  int32_t tiling_counts[HARL_MAX_DIMS];
+  int32_t tiling_offsets[HARL_MAX_DIMS];
+  int16_t term_gi[HARL_MAX_TERMS], term_sc[HARL_MAX_TERMS],
+      term_off[HARL_MAX_TERMS];
+  int16_t tensor_first[HARL_MAX_TENSORS], tensor_nterms[HARL_MAX_TENSORS];
+  int16_t stage_first[HARL_MAX_STAGES], stage_ntensors[HARL_MAX_STAGES],
+      stage_inter[HARL_MAX_STAGES], stage_extra[HARL_MAX_STAGES];
+  int16_t head0_src[HARL_MAX_HEAD0], head0_dst[HARL_MAX_HEAD0];
+  double flops_feature; /* log10(max(flops,1))/12, host libm */
+  const double* log2_lut;       /* device [max_extent+1]: log2(v)/10 */
+  const uint16_t* spf_lut;      /* device [max_extent+1] */
+  const uint16_t* tiling_table; /* device [sum tiling_counts][levels] */
+} harl_sketch_desc;
+
+/* numpy PCG64 bit-generator state (Generator.bit_generator.state). */
+typedef struct harl_pcg64 {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+  int32_t has_uint32;
+  uint32_t uinteger;
+} harl_pcg64;
+
+/* Fully connected tanh network in fp32 for the rollout (fp64 master params
+ * live elsewhere).  Layer i maps dims[i] -> dims[i+1]; W row-major
+ * [dims[i]][dims[i+1]].  Policy: trunk layers (all tanh, rlcore.py:95-103
+ * plus the trunk tanh of rlcore.py:139) then four linear heads packed into
+ * one matrix [hidden][n_head0 + 9] whose first n_head0 columns are the
+ * compact tiling-head columns.  Value: hidden layers tanh, last linear to 1.*/
+typedef struct harl_mlp_desc {
+  int32_t n_layers;
+  int32_t dims[HARL_MAX_LAYERS + 1];
+  const float* W[HARL_MAX_LAYERS];
+  const float* b[HARL_MAX_LAYERS];
+  const float* head_W; /* policy only: [dims[n_layers]][n_head_cols] */
+  const float* head_b;
+  int32_t n_head_cols;
+} harl_mlp_desc;
+
+/* GBT ensemble (costmodel.py:59-78,219-230).  Node arrays are concatenated
+ * over trees; children are tree-local indices.  `leaf_contrib` holds
+ * learning_rate * value (the reference's product, computed on the host). */
+typedef struct harl_forest_desc {
+  int32_t n_trees, fitted;
+  double base, floor_value;
+  const int32_t* tree_first;  /* [n_trees] first node of each tree */
+  const int16_t* feature;     /* -1 = leaf */
+  const int16_t* left;
+  const int16_t* right;
+  const double* threshold;
+  const double* leaf_contrib;
+} harl_forest_desc;
+
+int harl_abi_version(void);
+const char* harl_last_error(void);
+int harl_device_query(int device, int* sm_count_host, int* cc_major_host,
+                      int* cc_minor_host);
+
+/* sample_initial_schedules (schedspace.py:165-178): numpy Generator
+ * .integers semantics (Lemire on 32-bit halves, buffered high half),
+ * track-major.  Exact including rejection draws (repaired sequentially).
+ * Writes the number of 32-bit words consumed to *u32_used_host.
+ * scratch: >= 16 bytes device. */
+int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
+                         int64_t count, uint16_t* tiles, uint8_t* knobs,
+                         int64_t ld, int64_t* u32_used_host, void* scratch,
+                         void* stream);
+
+/* SketchContext.featurize (schedspace.py:415-438) incl. exact footprints
+ * (372-411) and glibc-2.39-faithful log10. feat: [n][feature_len]. */
+int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
+                   const uint8_t* knobs, int64_t n, int64_t ld, double* feat,
+                   void* stream);
+
+/* action_mask (schedspace.py:226-262), materialized: tiling [n][S*S+1]
+ * and shift [n][9] (compute-at, parallel, unroll triples) as uint8. */
+int harl_action_masks(const harl_sketch_desc* sk, const uint16_t* tiles,
+                      const uint8_t* knobs, int64_t n, int64_t ld,
+                      uint8_t* tiling, uint8_t* shift, void* stream);
+
+/* decode_action + apply_action (schedspace.py:196-210,265-301) for
+ * injected actions int32 [4][n] (head-major).  *status (caller-initialised
+ * to UINT64_MAX) receives row*16 + HARL_ST_* of the first failing row. */
+int harl_apply_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
+                       const uint8_t* knobs, int64_t n, int64_t ld,
+                       const int32_t* actions, uint16_t* tiles_out,
+                       uint8_t* knobs_out, uint64_t* status, void* stream);
+
+/* SurrogateModel.predict (costmodel.py:219-230), fp64 bit-exact; if
+ * old_score != NULL also reward = (new-old)/old (tuner.py:389-391). */
+int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
+                     int64_t n, int32_t feature_len, double* score,
+                     const double* old_score, double* reward, int32_t n_nodes,
+                     void* stream);
+
+/* select_actions (rlcore.py:216-228) fused with the walker: policy MLP
+ * (fp32), masked log-softmax, inverse-CDF sampling on the PCG64 stream
+ * (uniform for head h, row r = double #(h*n + r) after `rng`), then
+ * decode+apply (schedspace.py:196-301).  Outputs: actions int32 [4][n]
+ * (full head indices), logp float64 [n], new state, mask bits per row
+ * (uint64 movable-slot bits, uint32 shift-mask bits) for the replay
+ * buffer, the compact tiling-head column taken (head0_col, int32 [n]),
+ * optional logits float32 [n][n_head_cols] (NULL to skip).  *status as in
+ * harl_apply_actions (HARL_ST_NO_VALID for an all-masked row).
+ * If `inject` != NULL the actions are taken from it (int32 [4][n]) and the
+ * uniforms are not used (parity replay of oracle actions). */
+int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+                     const double* feat, const uint16_t* tiles,
+                     const uint8_t* knobs, int64_t n, int64_t ld,
+                     const harl_pcg64* rng, const int32_t* inject,
+                     int32_t* actions, double* logp, uint16_t* tiles_out,
+                     uint8_t* knobs_out, uint64_t* move_bits,
+                     uint32_t* shift_bits, int32_t* head0_col,
+                     float* logits_out, uint64_t* status, void* stream);
+
+/* ValueNet.estimate (rlcore.py:173) on feat (fp64 rows, fp32 math). */
+int harl_value_forward(const harl_mlp_desc* val, const double* feat,
+                       int64_t n, int32_t feature_len, float* v_out,
+                       void* stream);
+
+
+/* ------------------------------------------------------------------------
+ * Episode-level pieces of TuningSession._run_episode (tuner.py:350-440). */
+
+/* Replay FIFO (rlcore.py:253-265) as a device ring of `cap` slots.  Head-0
+ * actions are stored as compact tiling-head columns; masks as movable-slot
+ * bits + shift bits (ActionMask is a pure function of the state). */
+typedef struct harl_replay_ring {
+  double* X;            /* [cap][F]  features */
+  double* Xn;           /* [cap][F]  next features */
+  int32_t* actions;     /* [cap][4] */
+  double* scalars;      /* [cap][4]  logp, reward, advantage, td target */
+  uint64_t* move_bits;  /* [cap] */
+  uint32_t* shift_bits; /* [cap] */
+  int64_t cap;
+} harl_replay_ring;
+
+/* Visited-candidate log (CandidateEntry, tuner.py:406-412), SoA by visit. */
+typedef struct harl_entry_log {
+  uint16_t* tiles;  /* [slot][ld] */
+  uint8_t* knobs;   /* [3][ld] */
+  double* score;    /* [ld] */
+  double* reward;   /* [ld] */
+  int32_t* track;   /* [ld] */
+  int64_t ld;
+} harl_entry_log;
+
+/* Track.advance state (stopping.py:31-53) indexed by track id. */
+typedef struct harl_track_stats {
+  int32_t* steps;
+  double* best_score;
+  int32_t* best_step;
+} harl_track_stats;
+
+/* One step's device arrays (n rows, row r = live track row_track[r]). */
+typedef struct harl_step_buffers {
+  const int32_t* row_track;
+  const uint16_t* tiles_new;
+  const uint8_t* knobs_new;
+  const double* feat;       /* X  [n][F] */
+  const double* feat_new;   /* X' [n][F] */
+  const double* new_score;
+  const double* reward;
+  const float* v_cur;
+  const float* v_next;
+  const int32_t* actions;   /* [4][n] full head indices */
+  const int32_t* head0_col; /* [n] compact column */
+  const double* logp;
+  const uint64_t* move_bits;
+  const uint32_t* shift_bits;
+  double* adv;              /* out [n] */
+} harl_step_buffers;
+
+/* advantage + TD target (rlcore.py:231-234, tuner.py:395-398), replay push
+ * of rows >= keep_from into slots (wpos + r) % cap, entry log at visit
+ * vbase + r, Track.advance.  rl == 0 skips value/advantage/replay. */
+int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
+                     int64_t vbase, int32_t local_slots, int32_t feature_len,
+                     double discount, int32_t rl, const harl_replay_ring* ring,
+                     int64_t wpos, int64_t keep_from, const harl_entry_log* log,
+                     const harl_track_stats* ts, void* stream);
+
+/* Survivor compaction after a host cull (stopping.py:68-86): row i of the
+ * destination population <- row idx[i] of the source. */
+int harl_gather_rows(const int32_t* idx, int64_t n_out, int32_t local_slots,
+                     int32_t feature_len, const uint16_t* tiles,
+                     const uint8_t* knobs, const double* feat,
+                     const double* score, const int32_t* row_track,
+                     int64_t ld_src, uint16_t* tiles_o, uint8_t* knobs_o,
+                     double* feat_o, double* score_o, int32_t* row_track_o,
+                     int64_t ld_dst, void* stream);
+
+/* Flat parameter layout of one network inside the fp64 master buffer (the
+ * same offsets index the fp32 rollout copy, Adam m/v and the gradient),
+ * plus per-row scratch offsets used by the PPO kernels. */
+typedef struct harl_net_layout {
+  int32_t n_layers;
+  int32_t dims[HARL_MAX_LAYERS + 1];
+  int64_t off_W[HARL_MAX_LAYERS], off_b[HARL_MAX_LAYERS];
+  int64_t off_hW, off_hb; /* policy heads, packed [H][n_head_cols] */
+  int32_t n_head_cols;
+  int32_t row_act[HARL_MAX_LAYERS + 1];
+  int32_t row_delta[HARL_MAX_LAYERS];
+  int32_t row_head;
+} harl_net_layout;
+
+typedef struct harl_ppo_hyper {
+  double clip_ratio, entropy_weight, value_loss_weight;
+  double lr_actor, lr_critic;
+  double b1t_pi, b2t_pi, b1t_v, b2t_v; /* 1 - beta^t per optimizer */
+  double beta1, beta2, one_m_beta1, one_m_beta2, eps;
+} harl_ppo_hyper;
+
+/* ppo_update (rlcore.py:361-378) on B replay slots `idx` (device int32):
+ * fp64 forward/backward of both nets, fixed-order reductions, finite
+ * checks, Adam (rlcore.py:62-71) on params[0, n_pi) (policy) and
+ * [n_pi, n_params) (value), fp32 copy refresh.  losses (device double[8]):
+ * actor loss, value loss, policy loss, entropy, mean ratio.  *bad (device
+ * int32, caller zeroes) != 0 when a loss or gradient was not finite, in
+ * which case no parameter changed (RlDivergedError). scratch >=
+ * harl_ppo_scratch_bytes(). head0_src: compact column -> source slot. */
+int64_t harl_ppo_scratch_bytes(int32_t B, int32_t row_stride,
+                               int32_t n_jobs);
+int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
+                    const harl_ppo_hyper* hp, const harl_replay_ring* ring,
+                    const int32_t* idx, int32_t B, int32_t feature_len,
+                    int32_t n_head0, const int16_t* head0_src_host,
+                    int32_t row_stride, double* params, double* grads,
+                    double* adam_m, double* adam_v, float* params32,
+                    int64_t n_pi, int64_t n_params, double* losses,
+                    int32_t* bad, void* scratch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HARL_B200_H */

@@ -1,0 +1,106 @@
+// K5 tail + K8: per-step bookkeeping of _run_episode (tuner.py:393-412):
+// advantage/TD (rlcore.py:231-234, tuner.py:398), the replay push
+// (rlcore.py:253-265: a FIFO holding the last `cap` transitions, pushed in
+// row order), the visited-entry log (tuner.py:406-412) and Track.advance
+// (stopping.py:45-53); plus the survivor compaction after a host cull.
+#pragma once
+
+#include "common.cuh"
+
+namespace harl {
+
+struct FinishArgs {
+  int64_t n;            // rows this step (m)
+  int64_t ld;           // leading dim of the population state arrays
+  int64_t vbase;        // visit index of row 0 in the entry log
+  int32_t local_slots;
+  int32_t F;
+  double discount;
+  int32_t rl;           // value/advantage/replay only for RL searchers
+  int64_t wpos;         // ring slot receiving row 0 (mod cap)
+  int64_t keep_from;    // rows >= keep_from survive in the ring
+};
+
+__global__ void k_finish_step(FinishArgs a, harl_step_buffers io,
+                              harl_replay_ring ring, harl_entry_log log,
+                              harl_track_stats ts) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n) return;
+  const int32_t* row_track = io.row_track;
+  const uint16_t* tiles_new = io.tiles_new;
+  const uint8_t* knobs_new = io.knobs_new;
+  const double* feat = io.feat;
+  const double* feat_new = io.feat_new;
+  const double* new_score = io.new_score;
+  const double* reward = io.reward;
+  const float* v_cur = io.v_cur;
+  const float* v_next = io.v_next;
+  const int32_t* actions = io.actions;
+  const int32_t* head0_col = io.head0_col;
+  const double* logp = io.logp;
+  const uint64_t* move_bits = io.move_bits;
+  const uint32_t* shift_bits = io.shift_bits;
+  double* adv_out = io.adv;
+  const int64_t v = a.vbase + r;
+  for (int s = 0; s < a.local_slots; ++s)
+    log.tiles[(int64_t)s * log.ld + v] = tiles_new[(int64_t)s * a.ld + r];
+  for (int k = 0; k < 3; ++k) log.knobs[(int64_t)k * log.ld + v] = knobs_new[(int64_t)k * a.ld + r];
+  const double sc = new_score[r];
+  const double rw = reward[r];
+  log.score[v] = sc;
+  log.reward[v] = rw;
+  const int32_t t = row_track[r];
+  log.track[v] = t;
+  // Track.advance: steps += 1; best on strict improvement
+  const int32_t st = ts.steps[t] + 1;
+  ts.steps[t] = st;
+  if (sc > ts.best_score[t]) {
+    ts.best_score[t] = sc;
+    ts.best_step[t] = st;
+  }
+  if (!a.rl) return;
+  // advantage(reward, v_next, v_cur) = reward + discount*v_next - v_cur
+  const double vn = (double)v_next[r], vc = (double)v_cur[r];
+  const double tdv = __dadd_rn(rw, __dmul_rn(a.discount, vn));
+  const double adv = __dsub_rn(tdv, vc);
+  adv_out[r] = adv;
+  if (r < a.keep_from) return;
+  const int64_t slot = (a.wpos + r) % ring.cap;
+  for (int k = 0; k < a.F; ++k) {
+    ring.X[slot * a.F + k] = feat[r * a.F + k];
+    ring.Xn[slot * a.F + k] = feat_new[r * a.F + k];
+  }
+  ring.actions[slot * 4 + 0] = head0_col[r];
+  for (int h = 1; h < 4; ++h) ring.actions[slot * 4 + h] = actions[(int64_t)h * a.n + r];
+  ring.scalars[slot * 4 + 0] = logp[r];
+  ring.scalars[slot * 4 + 1] = rw;
+  ring.scalars[slot * 4 + 2] = adv;
+  ring.scalars[slot * 4 + 3] = tdv;
+  ring.move_bits[slot] = move_bits[r];
+  ring.shift_bits[slot] = shift_bits[r];
+}
+
+// Survivor compaction: dst row i <- src row idx[i] for the population state
+struct GatherArgs {
+  int64_t n_out, ld_src, ld_dst;
+  int32_t local_slots, F;
+};
+
+__global__ void k_gather_rows(GatherArgs a, const int32_t* idx,
+                              const uint16_t* tiles, const uint8_t* knobs,
+                              const double* feat, const double* score,
+                              const int32_t* row_track, uint16_t* tiles_o,
+                              uint8_t* knobs_o, double* feat_o, double* score_o,
+                              int32_t* row_track_o) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_out) return;
+  const int64_t r = idx[i];
+  for (int s = 0; s < a.local_slots; ++s)
+    tiles_o[(int64_t)s * a.ld_dst + i] = tiles[(int64_t)s * a.ld_src + r];
+  for (int k = 0; k < 3; ++k) knobs_o[(int64_t)k * a.ld_dst + i] = knobs[(int64_t)k * a.ld_src + r];
+  for (int k = 0; k < a.F; ++k) feat_o[i * a.F + k] = feat[r * a.F + k];
+  score_o[i] = score[r];
+  row_track_o[i] = row_track[r];
+}
+
+}  // namespace harl

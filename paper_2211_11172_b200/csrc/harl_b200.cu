@@ -1,0 +1,472 @@
+// C-ABI entry points (include/harl_b200.h).  Single translation unit: all
+// kernels are included here so constant-memory tables need no -rdc.
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "gbt_kernels.cuh"
+#include "mlp_ffma.cuh"
+#include "space_kernels.cuh"
+#include "episode_kernels.cuh"
+#include "ppo_kernels.cuh"
+
+namespace harl {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  set_error("%s: %s", where, cudaGetErrorString(e));
+  return HARL_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// host-side PCG64 jump tables
+
+typedef unsigned __int128 h128;
+static const h128 PCG_MULT =
+    ((h128)0x2360ED051FC65DA4ull << 64) | (h128)0x4385DF649FCCF645ull;
+
+static inline u128 to_u128(h128 x) {
+  u128 r;
+  r.hi = (uint64_t)(x >> 64);
+  r.lo = (uint64_t)x;
+  return r;
+}
+
+static void build_jump(const harl_pcg64& g, PcgJump* J) {
+  const h128 inc = ((h128)g.inc_hi << 64) | (h128)g.inc_lo;
+  h128 A = PCG_MULT, C = inc;  // one step: s -> A s + C
+  for (int i = 0; i < 64; ++i) {
+    J->A[i] = to_u128(A);
+    J->C[i] = to_u128(C);
+    C = A * C + C;  // compose (A,C) with itself
+    A = A * A;
+  }
+}
+
+static inline u128 state_of(const harl_pcg64& g) {
+  u128 s;
+  s.hi = g.state_hi;
+  s.lo = g.state_lo;
+  return s;
+}
+
+static int max_dyn_smem() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return v;
+}
+
+template <typename K>
+static int allow_smem(K kernel, size_t bytes, const char* name) {
+  if ((int)bytes > max_dyn_smem()) {
+    set_error("%s: needs %zu bytes of shared memory (max %d)", name, bytes,
+              max_dyn_smem());
+    return HARL_E_LIMIT;
+  }
+  cudaError_t e = cudaFuncSetAttribute(
+      kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return cuda_status(e, name);
+  return HARL_OK;
+}
+
+static int check_sketch(const harl_sketch_desc* sk) {
+  if (!sk) {
+    set_error("null sketch descriptor");
+    return HARL_E_ARG;
+  }
+  if (sk->ndims < 0 || sk->ndims > HARL_MAX_DIMS || sk->levels < 1 ||
+      sk->levels > HARL_MAX_LEVELS || sk->num_slots > HARL_MAX_SLOTS ||
+      sk->local_slots != sk->ndims * sk->levels ||
+      sk->num_slots < sk->local_slots || sk->feature_len > HARL_MAX_FEATURES ||
+      sk->n_head0 < 1 || sk->n_head0 > HARL_MAX_HEAD0) {
+    set_error("sketch descriptor out of range");
+    return HARL_E_ARG;
+  }
+  return HARL_OK;
+}
+
+static int check_mlp(const harl_mlp_desc* m, bool policy) {
+  if (!m || m->n_layers < 1 || m->n_layers > HARL_MAX_LAYERS) {
+    set_error("bad mlp descriptor");
+    return HARL_E_ARG;
+  }
+  for (int l = 0; l <= m->n_layers; ++l)
+    if (m->dims[l] < 1 || m->dims[l] > HARL_MAX_HIDDEN + HARL_MAX_FEATURES) {
+      set_error("mlp layer width out of range");
+      return HARL_E_ARG;
+    }
+  if (policy && (m->n_head_cols < 10 || !m->head_W || !m->head_b)) {
+    set_error("policy descriptor missing heads");
+    return HARL_E_ARG;
+  }
+  return HARL_OK;
+}
+
+}  // namespace harl
+
+using namespace harl;
+
+extern "C" {
+
+int harl_abi_version(void) { return HARL_ABI_VERSION; }
+
+const char* harl_last_error(void) { return g_err; }
+
+int harl_device_query(int device, int* sm_count, int* cc_major, int* cc_minor) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDeviceProperties");
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return HARL_OK;
+}
+
+int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
+                         int64_t count, uint16_t* tiles, uint8_t* knobs,
+                         int64_t ld, int64_t* u32_used_host, void* scratch,
+                         void* stream) {
+  int rc = check_sketch(sk);
+  if (rc) return rc;
+  if (count < 0 || ld < count || !rng || !scratch || !u32_used_host) {
+    set_error("harl_init_population: bad arguments");
+    return HARL_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  PcgJump J;
+  build_jump(*rng, &J);
+  InitArgs a;
+  memset(&a, 0, sizeof(a));
+  a.count = count;
+  a.ld = ld;
+  a.s = state_of(*rng);
+  a.has32 = rng->has_uint32;
+  a.buffered = rng->uinteger;
+  a.nbounds = sk->ndims + 3;
+  for (int d = 0; d < sk->ndims; ++d) a.bounds[d] = sk->tiling_counts[d];
+  a.bounds[sk->ndims] = sk->ncas;
+  a.bounds[sk->ndims + 1] = sk->max_fusible + 1;
+  a.bounds[sk->ndims + 2] = sk->n_unroll;
+  for (int k = 0; k < a.nbounds; ++k) a.per_track += a.bounds[k] > 1;
+  unsigned long long* bad = (unsigned long long*)scratch;
+  unsigned long long* used = bad + 1;
+  a.t0 = 0;
+  a.j0 = 0;
+  while (a.t0 < count) {
+    const unsigned long long init = ULLONG_MAX;
+    cudaError_t e = cudaMemcpyAsync(bad, &init, 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "init memcpy");
+    const int64_t todo = count - a.t0;
+    const int threads = 256;
+    k_init_sample<<<(unsigned)((todo + threads - 1) / threads), threads, 0, st>>>(
+        *sk, J, a, tiles, knobs, bad);
+    HARL_CHECK_LAUNCH("k_init_sample");
+    unsigned long long first = 0;
+    e = cudaMemcpyAsync(&first, bad, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_status(e, "init sync");
+    if (first == ULLONG_MAX) {
+      a.j0 += (uint64_t)todo * (uint64_t)a.per_track;
+      a.t0 = count;
+      break;
+    }
+    // tracks [t0, first) are exact; redo `first` sequentially
+    InitArgs one = a;
+    one.j0 = a.j0 + (uint64_t)(first - a.t0) * (uint64_t)a.per_track;
+    k_init_one<<<1, 1, 0, st>>>(*sk, J, one, (int64_t)first, tiles, knobs, used);
+    HARL_CHECK_LAUNCH("k_init_one");
+    unsigned long long u = 0;
+    e = cudaMemcpyAsync(&u, used, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_status(e, "init sync");
+    a.j0 = one.j0 + u;
+    a.t0 = (int64_t)first + 1;
+  }
+  *u32_used_host = (int64_t)a.j0;
+  return HARL_OK;
+}
+
+int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
+                   const uint8_t* knobs, int64_t n, int64_t ld, double* feat,
+                   void* stream) {
+  int rc = check_sketch(sk);
+  if (rc) return rc;
+  if (n <= 0) return HARL_OK;
+  const size_t smem = sizeof(double) * FEAT_THREADS * sk->feature_len;
+  if ((rc = allow_smem(k_featurize, smem, "k_featurize"))) return rc;
+  k_featurize<<<(unsigned)((n + FEAT_THREADS - 1) / FEAT_THREADS), FEAT_THREADS,
+                smem, (cudaStream_t)stream>>>(*sk, tiles, knobs, n, ld, feat);
+  HARL_CHECK_LAUNCH("k_featurize");
+  return HARL_OK;
+}
+
+int harl_action_masks(const harl_sketch_desc* sk, const uint16_t* tiles,
+                      const uint8_t* knobs, int64_t n, int64_t ld,
+                      uint8_t* tiling, uint8_t* shift, void* stream) {
+  int rc = check_sketch(sk);
+  if (rc) return rc;
+  if (n <= 0) return HARL_OK;
+  k_action_masks<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      *sk, tiles, knobs, n, ld, tiling, shift);
+  HARL_CHECK_LAUNCH("k_action_masks");
+  return HARL_OK;
+}
+
+int harl_apply_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
+                       const uint8_t* knobs, int64_t n, int64_t ld,
+                       const int32_t* actions, uint16_t* tiles_out,
+                       uint8_t* knobs_out, uint64_t* status, void* stream) {
+  int rc = check_sketch(sk);
+  if (rc) return rc;
+  if (n <= 0) return HARL_OK;
+  k_apply_actions<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      *sk, tiles, knobs, n, ld, actions, tiles_out, knobs_out,
+      (unsigned long long*)status);
+  HARL_CHECK_LAUNCH("k_apply_actions");
+  return HARL_OK;
+}
+
+int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
+                     int64_t n, int32_t feature_len, double* score,
+                     const double* old_score, double* reward, int32_t n_nodes,
+                     void* stream) {
+  if (!forest || forest->n_trees < 0 || forest->n_trees > 1024 || n_nodes < 0) {
+    set_error("harl_gbt_predict: bad forest");
+    return HARL_E_ARG;
+  }
+  if (n <= 0) return HARL_OK;
+  const size_t smem = sizeof(GbtNode) * (size_t)n_nodes;
+  int rc = allow_smem(k_gbt_predict, smem, "k_gbt_predict");
+  if (rc) return rc;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int64_t blocks = (n + GBT_THREADS - 1) / GBT_THREADS;
+  if (blocks > 4 * sms) blocks = 4 * sms;
+  k_gbt_predict<<<(unsigned)blocks, GBT_THREADS, smem, (cudaStream_t)stream>>>(
+      *forest, feat, n, feature_len, score, old_score, reward, n_nodes);
+  HARL_CHECK_LAUNCH("k_gbt_predict");
+  return HARL_OK;
+}
+
+int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+                     const double* feat, const uint16_t* tiles,
+                     const uint8_t* knobs, int64_t n, int64_t ld,
+                     const harl_pcg64* rng, const int32_t* inject,
+                     int32_t* actions, double* logp, uint16_t* tiles_out,
+                     uint8_t* knobs_out, uint64_t* move_bits,
+                     uint32_t* shift_bits, int32_t* head0_col,
+                     float* logits_out, uint64_t* status, void* stream) {
+  int rc = check_sketch(sk);
+  if (rc) return rc;
+  if ((rc = check_mlp(pol, true))) return rc;
+  if (pol->n_head_cols != sk->n_head0 + 9 || pol->dims[0] != sk->feature_len) {
+    set_error("policy descriptor does not match sketch");
+    return HARL_E_ARG;
+  }
+  if (n <= 0) return HARL_OK;
+  if (!rng && !inject) {
+    set_error("harl_policy_step: need rng or injected actions");
+    return HARL_E_ARG;
+  }
+  int ldbuf = pol->n_head_cols;
+  for (int l = 0; l <= pol->n_layers; ++l) ldbuf = ldbuf > pol->dims[l] ? ldbuf : pol->dims[l];
+  ldbuf += 1;  // bank-conflict padding
+  const size_t smem = sizeof(float) * 2 * MLP_TM * (size_t)ldbuf;
+  if ((rc = allow_smem(k_policy_step, smem, "k_policy_step"))) return rc;
+  PcgJump J;
+  StepRng sr;
+  memset(&J, 0, sizeof(J));
+  memset(&sr, 0, sizeof(sr));
+  if (rng) {
+    build_jump(*rng, &J);
+    sr.s = state_of(*rng);
+  }
+  k_policy_step<<<(unsigned)((n + MLP_TM - 1) / MLP_TM), MLP_THREADS, smem,
+                  (cudaStream_t)stream>>>(*sk, *pol, J, sr, feat, tiles, knobs, n,
+                                          ld, inject, actions, logp, tiles_out,
+                                          knobs_out, move_bits, shift_bits,
+                                          head0_col, logits_out,
+                                          (unsigned long long*)status, ldbuf);
+  HARL_CHECK_LAUNCH("k_policy_step");
+  return HARL_OK;
+}
+
+int harl_value_forward(const harl_mlp_desc* val, const double* feat, int64_t n,
+                       int32_t feature_len, float* v_out, void* stream) {
+  int rc = check_mlp(val, false);
+  if (rc) return rc;
+  if (val->dims[0] != feature_len || val->dims[val->n_layers] != 1 ||
+      val->n_layers < 2) {
+    set_error("value descriptor does not match");
+    return HARL_E_ARG;
+  }
+  if (n <= 0) return HARL_OK;
+  int ldbuf = 0;
+  for (int l = 0; l <= val->n_layers; ++l) ldbuf = ldbuf > val->dims[l] ? ldbuf : val->dims[l];
+  ldbuf += 1;
+  const size_t smem = sizeof(float) * 2 * MLP_TM * (size_t)ldbuf;
+  if ((rc = allow_smem(k_value_forward, smem, "k_value_forward"))) return rc;
+  k_value_forward<<<(unsigned)((n + MLP_TM - 1) / MLP_TM), MLP_THREADS, smem,
+                    (cudaStream_t)stream>>>(*val, feat, n, feature_len, v_out, ldbuf);
+  HARL_CHECK_LAUNCH("k_value_forward");
+  return HARL_OK;
+}
+
+int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
+                     int64_t vbase, int32_t local_slots, int32_t feature_len,
+                     double discount, int32_t rl, const harl_replay_ring* ring,
+                     int64_t wpos, int64_t keep_from, const harl_entry_log* log,
+                     const harl_track_stats* ts, void* stream) {
+  if (!io || !log || !ts || (rl && (!ring || ring->cap < 1))) {
+    set_error("harl_finish_step: bad arguments");
+    return HARL_E_ARG;
+  }
+  if (n <= 0) return HARL_OK;
+  FinishArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n = n;
+  a.ld = ld;
+  a.vbase = vbase;
+  a.local_slots = local_slots;
+  a.F = feature_len;
+  a.discount = discount;
+  a.rl = rl;
+  a.wpos = wpos;
+  a.keep_from = keep_from;
+  harl_replay_ring rg;
+  memset(&rg, 0, sizeof(rg));
+  if (ring) rg = *ring;
+  if (rg.cap < 1) rg.cap = 1;
+  k_finish_step<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      a, *io, rg, *log, *ts);
+  HARL_CHECK_LAUNCH("k_finish_step");
+  return HARL_OK;
+}
+
+int harl_gather_rows(const int32_t* idx, int64_t n_out, int32_t local_slots,
+                     int32_t feature_len, const uint16_t* tiles,
+                     const uint8_t* knobs, const double* feat,
+                     const double* score, const int32_t* row_track,
+                     int64_t ld_src, uint16_t* tiles_o, uint8_t* knobs_o,
+                     double* feat_o, double* score_o, int32_t* row_track_o,
+                     int64_t ld_dst, void* stream) {
+  if (n_out <= 0) return HARL_OK;
+  GatherArgs a;
+  a.n_out = n_out;
+  a.ld_src = ld_src;
+  a.ld_dst = ld_dst;
+  a.local_slots = local_slots;
+  a.F = feature_len;
+  k_gather_rows<<<(unsigned)((n_out + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      a, idx, tiles, knobs, feat, score, row_track, tiles_o, knobs_o, feat_o,
+      score_o, row_track_o);
+  HARL_CHECK_LAUNCH("k_gather_rows");
+  return HARL_OK;
+}
+
+static int build_grad_jobs(const harl_net_layout& P, const harl_net_layout& V,
+                           GradJob* jobs, int* n_jobs, int* n_tiles) {
+  int nj = 0, tiles = 0;
+  auto add = [&](int a_off, int ni, int d_off, int njj, int64_t g_off) {
+    GradJob& j = jobs[nj++];
+    j.a_off = a_off;
+    j.ni = ni;
+    j.d_off = d_off;
+    j.nj = njj;
+    j.g_off = g_off;
+    j.tile_first = tiles;
+    const int ti = ni == 0 ? 1 : (ni + WG_T - 1) / WG_T;
+    tiles += ti * ((njj + WG_T - 1) / WG_T);
+  };
+  for (int l = 0; l < P.n_layers; ++l) {
+    add(P.row_act[l], P.dims[l], P.row_delta[l], P.dims[l + 1], P.off_W[l]);
+    add(0, 0, P.row_delta[l], P.dims[l + 1], P.off_b[l]);
+  }
+  add(P.row_act[P.n_layers], P.dims[P.n_layers], P.row_head, P.n_head_cols, P.off_hW);
+  add(0, 0, P.row_head, P.n_head_cols, P.off_hb);
+  for (int l = 0; l < V.n_layers; ++l) {
+    add(V.row_act[l], V.dims[l], V.row_delta[l], V.dims[l + 1], V.off_W[l]);
+    add(0, 0, V.row_delta[l], V.dims[l + 1], V.off_b[l]);
+  }
+  *n_jobs = nj;
+  *n_tiles = tiles;
+  return HARL_OK;
+}
+
+int64_t harl_ppo_scratch_bytes(int32_t B, int32_t row_stride, int32_t n_jobs) {
+  (void)n_jobs;
+  return (int64_t)B * row_stride * 8 + (int64_t)B * 4 * 8 +
+         (int64_t)sizeof(GradJob) * 4 * (HARL_MAX_LAYERS + 2) + 256;
+}
+
+int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
+                    const harl_ppo_hyper* hp, const harl_replay_ring* ring,
+                    const int32_t* idx, int32_t B, int32_t feature_len,
+                    int32_t n_head0, const int16_t* head0_src_host,
+                    int32_t row_stride, double* params, double* grads,
+                    double* adam_m, double* adam_v, float* params32,
+                    int64_t n_pi, int64_t n_params, double* losses,
+                    int32_t* bad, void* scratch, void* stream) {
+  if (!pol || !val || !hp || !ring || !idx || B < 1 || n_head0 < 1 ||
+      n_head0 > HARL_MAX_HEAD0 || pol->n_layers < 1 ||
+      pol->n_layers > HARL_MAX_LAYERS || val->n_layers < 2 ||
+      val->n_layers > HARL_MAX_LAYERS) {
+    set_error("harl_ppo_update: bad arguments");
+    return HARL_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* sc = (char*)scratch;
+  double* rows = (double*)sc;
+  double* rowout = rows + (int64_t)B * row_stride;
+  GradJob* djobs = (GradJob*)(rowout + (int64_t)B * 4);
+  GradJob jobs[4 * (HARL_MAX_LAYERS + 2)];
+  int n_jobs = 0, n_tiles = 0;
+  build_grad_jobs(*pol, *val, jobs, &n_jobs, &n_tiles);
+  cudaError_t e = cudaMemcpyAsync(djobs, jobs, sizeof(GradJob) * n_jobs,
+                                  cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e, "ppo jobs memcpy");
+  PpoArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = B;
+  a.F = feature_len;
+  a.C0 = n_head0;
+  a.row_stride = row_stride;
+  a.clip_lo = 1.0 - hp->clip_ratio;
+  a.clip_hi = 1.0 + hp->clip_ratio;
+  a.w_ent = hp->entropy_weight;
+  a.w_val = hp->value_loss_weight;
+  for (int j = 0; j < n_head0; ++j) a.head0_src[j] = head0_src_host[j];
+  k_ppo_rows<<<(unsigned)((B + PPO_TM - 1) / PPO_TM), PPO_THREADS, 0, st>>>(
+      a, *pol, *val, *ring, idx, params, rows, rowout);
+  HARL_CHECK_LAUNCH("k_ppo_rows");
+  k_ppo_losses<<<1, 32, 0, st>>>(B, hp->entropy_weight, hp->value_loss_weight,
+                                 rowout, losses, bad);
+  HARL_CHECK_LAUNCH("k_ppo_losses");
+  k_ppo_wgrad<<<(unsigned)n_tiles, 256, 0, st>>>(djobs, n_jobs, B, row_stride,
+                                                 rows, grads, bad);
+  HARL_CHECK_LAUNCH("k_ppo_wgrad");
+  AdamArgs ad;
+  ad.n_pi = n_pi;
+  ad.n = n_params;
+  ad.h = *hp;
+  k_ppo_adam<<<296, 256, 0, st>>>(ad, bad, grads, params, adam_m, adam_v, params32);
+  HARL_CHECK_LAUNCH("k_ppo_adam");
+  return HARL_OK;
+}
+
+}  // extern "C"

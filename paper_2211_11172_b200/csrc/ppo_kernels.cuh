@@ -1,0 +1,338 @@
+// K7: the PPO update (rlcore.py:293-378) in fp64 on device.
+//   (a) k_ppo_rows   row-parallel: gather the sampled transitions from the
+//       replay ring, policy + value forward, per-row clipped-surrogate /
+//       entropy / MSE terms and the per-layer deltas (dL/dz) for both nets
+//       (rlcore.py:293-358, Mlp.backward 105-116, PolicyNet.backward 148-158)
+//   (b) k_ppo_losses one warp: fixed-order means -> losses, finiteness
+//   (c) k_ppo_wgrad  weight/bias gradients = sum over rows of act^T delta,
+//       tiled through shared memory, fixed summation order (deterministic)
+//   (d) k_ppo_adam   Adam.step (rlcore.py:62-71) with the reference's
+//       operation order, skipped entirely when anything is non-finite
+//       (ppo_update raises before stepping, rlcore.py:368-375); refreshes
+//       the fp32 rollout copy of every parameter.
+// Parameters live in one flat fp64 buffer (policy segment then value
+// segment); the tiling head is stored compact (see space.head_columns).
+#pragma once
+
+#include "common.cuh"
+
+namespace harl {
+
+typedef harl_net_layout NetLayout;
+
+struct PpoArgs {
+  int32_t B, F, C0, row_stride;
+  double clip_lo, clip_hi, w_ent, w_val;
+  int16_t head0_src[HARL_MAX_HEAD0];
+};
+
+typedef harl_replay_ring PpoRing;
+
+constexpr int PPO_TM = 8;
+constexpr int PPO_THREADS = 256;
+
+// out[r][c] = act(sum_k in[r][k] W[k][c] + b[c]) for r < rows
+__device__ inline void dense64(const double* in, int ldi, int K,
+                               const double* __restrict__ W,
+                               const double* __restrict__ b, int N, double* out,
+                               int ldo, bool act, int rows) {
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    double acc[PPO_TM];
+#pragma unroll
+    for (int r = 0; r < PPO_TM; ++r) acc[r] = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double w = W[(int64_t)k * N + c];
+#pragma unroll
+      for (int r = 0; r < PPO_TM; ++r)
+        if (r < rows) acc[r] = fma(in[r * ldi + k], w, acc[r]);
+    }
+    for (int r = 0; r < rows; ++r) {
+      const double z = acc[r] + b[c];
+      out[r * ldo + c] = act ? tanh(z) : z;
+    }
+  }
+  __syncthreads();
+}
+
+// out[r][k] = (sum_c d[r][c] W[k][c]) * (tanh' via act: 1 - a[r][k]^2)
+__device__ inline void back64(const double* d, int ldd, int N,
+                              const double* __restrict__ W, int K,
+                              const double* a, int lda, double* out, int ldo,
+                              int rows) {
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double acc[PPO_TM];
+#pragma unroll
+    for (int r = 0; r < PPO_TM; ++r) acc[r] = 0.0;
+    const double* wr = W + (int64_t)k * N;
+    for (int c = 0; c < N; ++c) {
+      const double w = wr[c];
+#pragma unroll
+      for (int r = 0; r < PPO_TM; ++r)
+        if (r < rows) acc[r] = fma(d[r * ldd + c], w, acc[r]);
+    }
+    for (int r = 0; r < rows; ++r) {
+      const double av = a[r * lda + k];
+      out[r * ldo + k] = acc[r] * (1.0 - av * av);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ inline double wmax64(double v) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ inline double wsum64(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// per-row terms written to rowout[r*4 + {0..3}]:
+//   min(s_un, s_cl), entropy total, ratio, (v - td)^2
+__global__ void __launch_bounds__(PPO_THREADS)
+k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout P,
+           const __grid_constant__ NetLayout V, PpoRing ring, const int32_t* idx,
+           const double* params, double* rows, double* rowout) {
+  const int r0 = blockIdx.x * PPO_TM;
+  const int nrows = min(PPO_TM, a.B - r0);
+  const int RS = a.row_stride;
+  double* base = rows + (int64_t)r0 * RS;
+  // gather X (shared by both nets: P.row_act[0] == V.row_act[0])
+  for (int i = threadIdx.x; i < nrows * a.F; i += blockDim.x) {
+    const int rr = i / a.F, k = i % a.F;
+    base[rr * RS + P.row_act[0] + k] = ring.X[(int64_t)idx[r0 + rr] * a.F + k];
+  }
+  __syncthreads();
+  // policy trunk (every layer tanh: rlcore.py:95-103 + 139)
+  for (int l = 0; l < P.n_layers; ++l)
+    dense64(base + P.row_act[l], RS, P.dims[l], params + P.off_W[l],
+            params + P.off_b[l], P.dims[l + 1], base + P.row_act[l + 1], RS,
+            true, nrows);
+  const int H = P.dims[P.n_layers];
+  const int NH = P.n_head_cols;
+  dense64(base + P.row_act[P.n_layers], RS, H, params + P.off_hW,
+          params + P.off_hb, NH, base + P.row_head, RS, false, nrows);
+  // value net
+  for (int l = 0; l < V.n_layers; ++l)
+    dense64(base + V.row_act[l], RS, V.dims[l], params + V.off_W[l],
+            params + V.off_b[l], V.dims[l + 1], base + V.row_act[l + 1], RS,
+            l < V.n_layers - 1, nrows);
+  // per-row PPO terms, one warp per row
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double invB = 1.0 / (double)a.B;
+  for (int rr = warp; rr < nrows; rr += PPO_THREADS / 32) {
+    const int slot = idx[r0 + rr];
+    double* z = base + rr * RS + P.row_head;
+    const uint64_t mv = ring.move_bits[slot];
+    const uint32_t sb = ring.shift_bits[slot];
+    const double logp_old = ring.scalars[slot * 4 + 0];
+    const double adv = ring.scalars[slot * 4 + 2];
+    const double td = ring.scalars[slot * 4 + 3];
+    // pass 1: per-head max, sum, entropy (rlcore.py:300-306)
+    double hmax[4], hsum[4], hlogs[4], hent[4];
+    double logp_new = 0.0, ent_total = 0.0;
+    for (int h = 0; h < 4; ++h) {
+      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
+      const int C = h == 0 ? a.C0 : 3;
+      auto legal = [&](int j) -> bool {
+        if (h == 0) return j == a.C0 - 1 || ((mv >> a.head0_src[j]) & 1ull);
+        return (sb >> (3 * (h - 1) + j)) & 1u;
+      };
+      double m = -INFINITY;
+      for (int j = lane; j < C; j += 32)
+        if (legal(j)) m = fmax(m, z[c0 + j]);
+      m = wmax64(m);
+      double s = 0.0;
+      for (int j = lane; j < C; j += 32)
+        if (legal(j)) s += exp(z[c0 + j] - m);
+      s = wsum64(s);
+      const double ls = log(s);
+      double e = 0.0;
+      for (int j = lane; j < C; j += 32)
+        if (legal(j)) e -= (exp(z[c0 + j] - m) / s) * (z[c0 + j] - m - ls);
+      e = wsum64(e);
+      hmax[h] = m;
+      hsum[h] = s;
+      hlogs[h] = ls;
+      hent[h] = e;
+      ent_total += e;
+    }
+    // log-prob of the taken actions; ring actions hold the COMPACT
+    // column for head 0 (policy kernel output head0_col)
+    for (int h = 0; h < 4; ++h) {
+      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
+      const int col = ring.actions[slot * 4 + h];
+      logp_new += z[c0 + col] - hmax[h] - hlogs[h];
+    }
+    const double ratio = exp(logp_new - logp_old);
+    const double clipped = fmin(fmax(ratio, a.clip_lo), a.clip_hi);
+    const double s_un = ratio * adv, s_cl = clipped * adv;
+    const double coef = (s_un <= s_cl) ? ratio * adv : 0.0;
+    const double dlogp = -coef * invB;
+    const double went = a.w_ent * invB;
+    // pass 2: dz in place over the logits
+    for (int h = 0; h < 4; ++h) {
+      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
+      const int C = h == 0 ? a.C0 : 3;
+      const int col = ring.actions[slot * 4 + h];
+      auto legal = [&](int j) -> bool {
+        if (h == 0) return j == a.C0 - 1 || ((mv >> a.head0_src[j]) & 1ull);
+        return (sb >> (3 * (h - 1) + j)) & 1u;
+      };
+      __syncwarp();
+      for (int j = lane; j < C; j += 32) {
+        double dz = 0.0;
+        if (legal(j)) {
+          const double lp = z[c0 + j] - hmax[h] - hlogs[h];
+          const double p = exp(z[c0 + j] - hmax[h]) / hsum[h];
+          dz = dlogp * ((j == col ? 1.0 : 0.0) - p) + went * p * (lp + hent[h]);
+        } else {
+          dz = dlogp * ((j == col ? 1.0 : 0.0) - 0.0);
+        }
+        z[c0 + j] = dz;
+      }
+    }
+    if (lane == 0) {
+      const double v = base[rr * RS + V.row_act[V.n_layers]];
+      double* o = rowout + (int64_t)(r0 + rr) * 4;
+      o[0] = fmin(s_un, s_cl);
+      o[1] = ent_total;
+      o[2] = ratio;
+      o[3] = (v - td) * (v - td);
+      // dv = w * 2 (v - td) / B is the value net's output delta
+      base[rr * RS + V.row_delta[V.n_layers - 1]] = a.w_val * 2.0 * (v - td) * invB;
+    }
+  }
+  __syncthreads();
+  // policy backward: dhid = dz . Wh^T, times (1 - hid^2)
+  back64(base + P.row_head, RS, NH, params + P.off_hW, H,
+         base + P.row_act[P.n_layers], RS, base + P.row_delta[P.n_layers - 1],
+         RS, nrows);
+  for (int l = P.n_layers - 1; l >= 1; --l)
+    back64(base + P.row_delta[l], RS, P.dims[l + 1], params + P.off_W[l],
+           P.dims[l], base + P.row_act[l], RS, base + P.row_delta[l - 1], RS,
+           nrows);
+  for (int l = V.n_layers - 1; l >= 1; --l)
+    back64(base + V.row_delta[l], RS, V.dims[l + 1], params + V.off_W[l],
+           V.dims[l], base + V.row_act[l], RS, base + V.row_delta[l - 1], RS,
+           nrows);
+}
+
+// (b) fixed-order means; out: [0] actor loss, [1] value loss,
+// [2] policy loss, [3] entropy, [4] mean ratio, [5] finite flag
+__global__ void k_ppo_losses(int B, double w_ent, double w_val,
+                             const double* rowout, double* losses,
+                             int32_t* bad) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double smin = 0, ent = 0, ratio = 0, sq = 0;
+  for (int r = 0; r < B; ++r) {
+    smin += rowout[r * 4 + 0];
+    ent += rowout[r * 4 + 1];
+    ratio += rowout[r * 4 + 2];
+    sq += rowout[r * 4 + 3];
+  }
+  const double policy_loss = -(smin / B);
+  const double entropy = ent / B;
+  const double a_loss = policy_loss - w_ent * entropy;
+  const double v_loss = w_val * (sq / B);
+  losses[0] = a_loss;
+  losses[1] = v_loss;
+  losses[2] = policy_loss;
+  losses[3] = entropy;
+  losses[4] = ratio / B;
+  if (!isfinite(a_loss) || !isfinite(v_loss)) atomicOr(bad, 1);
+}
+
+// (c) gradient jobs: grad[off + i*nj + j] = sum_r A[r][ai + i] * D[r][dj + j]
+// (A column -1 means "ones": bias gradient)
+struct GradJob {
+  int32_t a_off, d_off, ni, nj;  // ni == 0 -> bias (A = 1)
+  int64_t g_off;
+  int32_t tile_first;            // first tile index of this job
+};
+
+constexpr int WG_T = 32;  // 32x32 output tile, 256 threads x 4 outputs
+
+__global__ void __launch_bounds__(256)
+k_ppo_wgrad(const GradJob* jobs, int n_jobs, int B, int RS, const double* rows,
+            double* grads, int32_t* bad) {
+  __shared__ double sa[WG_T][WG_T + 1];
+  __shared__ double sd[WG_T][WG_T + 1];
+  __shared__ int s_job;
+  if (threadIdx.x == 0) {
+    int j = 0;
+    while (j + 1 < n_jobs && jobs[j + 1].tile_first <= (int)blockIdx.x) ++j;
+    s_job = j;
+  }
+  __syncthreads();
+  const GradJob jb = jobs[s_job];
+  const int tile = blockIdx.x - jb.tile_first;
+  const int ni = jb.ni == 0 ? 1 : jb.ni;
+  const int tiles_j = (jb.nj + WG_T - 1) / WG_T;
+  const int i0 = (tile / tiles_j) * WG_T, j0 = (tile % tiles_j) * WG_T;
+  const int tj = threadIdx.x % WG_T, ti = threadIdx.x / WG_T;  // ti 0..7
+  double acc[4] = {0, 0, 0, 0};
+  for (int rb = 0; rb < B; rb += WG_T) {
+    for (int e = threadIdx.x; e < WG_T * WG_T; e += blockDim.x) {
+      const int rr = e / WG_T, cc = e % WG_T;
+      const int r = rb + rr;
+      double av = 0.0, dv = 0.0;
+      if (r < B) {
+        if (i0 + cc < ni) av = jb.ni == 0 ? 1.0 : rows[(int64_t)r * RS + jb.a_off + i0 + cc];
+        if (j0 + cc < jb.nj) dv = rows[(int64_t)r * RS + jb.d_off + j0 + cc];
+      }
+      sa[rr][cc] = av;
+      sd[rr][cc] = dv;
+    }
+    __syncthreads();
+    for (int rr = 0; rr < WG_T; ++rr) {
+      const double dv = sd[rr][tj];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(sa[rr][ti + 8 * q], dv, acc[q]);
+    }
+    __syncthreads();
+  }
+  int nonfinite = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ti + 8 * q, j = j0 + tj;
+    if (i < ni && j < jb.nj) {
+      grads[jb.g_off + (int64_t)i * jb.nj + j] = acc[q];
+      if (!isfinite(acc[q])) nonfinite = 1;
+    }
+  }
+  if (nonfinite) atomicOr(bad, 2);
+}
+
+// (d) Adam over [0, n_pi) with the policy optimizer and [n_pi, n) with the
+// value optimizer.  Scalars precomputed on the host exactly as numpy does.
+struct AdamArgs {
+  int64_t n_pi, n;
+  harl_ppo_hyper h;
+};
+
+__global__ void k_ppo_adam(AdamArgs a, const int32_t* bad, const double* grads,
+                           double* params, double* m, double* v, float* params32) {
+  if (*bad) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool pi = i < a.n_pi;
+    const double lr = pi ? a.h.lr_actor : a.h.lr_critic;
+    const double b1t = pi ? a.h.b1t_pi : a.h.b1t_v;
+    const double b2t = pi ? a.h.b2t_pi : a.h.b2t_v;
+    const double g = grads[i];
+    double mi = __dmul_rn(m[i], a.h.beta1);
+    mi = __dadd_rn(mi, __dmul_rn(a.h.one_m_beta1, g));
+    double vi = __dmul_rn(v[i], a.h.beta2);
+    vi = __dadd_rn(vi, __dmul_rn(a.h.one_m_beta2, __dmul_rn(g, g)));
+    m[i] = mi;
+    v[i] = vi;
+    const double num = __dmul_rn(lr, __ddiv_rn(mi, b1t));
+    const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, b2t)), a.h.eps);
+    const double p = __dsub_rn(params[i], __ddiv_rn(num, den));
+    params[i] = p;
+    params32[i] = (float)p;
+  }
+}
+
+}  // namespace harl

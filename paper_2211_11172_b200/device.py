@@ -1,0 +1,718 @@
+"""Device-resident tables and batch operators (the reference's per-call API,
+one call per population batch).
+
+Every function here launches hand-written sm_100a kernels through the C ABI
+(``_native``); torch is used only for device allocation and the current
+stream.  Reference functions mirrored (``pkg/src/schedtune``):
+
+=============================  ==========================================
+this module                    reference
+=============================  ==========================================
+``init_population``            schedspace.sample_initial_schedules 165-178
+``featurize``                  SketchContext.featurize 415-438
+``action_masks``               schedspace.action_mask 226-262
+``apply_actions``              decode_action + apply_action 196-301
+``gbt_predict``                SurrogateModel.predict 219-230 (+ reward)
+``policy_step``                select_actions 216-228 (+ walker)
+``value_estimate``             ValueNet.estimate 173-174
+``DeviceAgent.ppo_update``     ppo_update 361-378
+=============================  ==========================================
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import profiling as PF
+from . import rng as R
+from .errors import DeviceError, InvalidActionError, RlDivergedError
+from .space import SketchTables, head_columns
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev(device=None):
+    return torch.device("cuda", torch.cuda.current_device()) \
+        if device is None else torch.device(device)
+
+
+_SUBSPACE = {N.ST_TILING: "tiling", N.ST_COMPUTE_AT: "compute_at",
+             N.ST_PARALLEL: "parallel", N.ST_UNROLL: "unroll"}
+
+
+def raise_status(code_word: int, where: str = "") -> None:
+    """Translate a device status word (row*16 + HARL_ST_*) into the
+    reference's exception."""
+    if code_word == (1 << 64) - 1 or code_word < 0:
+        return
+    row, code = divmod(int(code_word), 16)
+    if code in _SUBSPACE:
+        raise InvalidActionError(_SUBSPACE[code],
+                                 f"row {row}{' ' + where if where else ''}")
+    if code == N.ST_NO_VALID:
+        raise RlDivergedError("action mask with no valid entry")
+    if code == N.ST_NONFINITE:
+        raise RlDivergedError("non-finite loss or gradient in update")
+    raise DeviceError(f"unknown device status {code} at row {row}")
+
+
+# ---------------------------------------------------------------------------
+# per-sketch tables
+
+
+class DeviceSketch:
+    """``SketchTables`` uploaded to the device plus its C descriptor."""
+
+    def __init__(self, tables: SketchTables, device=None):
+        N.load()
+        dev = _dev(device)
+        self.tables = tb = tables
+        self.device = dev
+        self.log2_lut = torch.from_numpy(tb.log2_lut).to(dev)
+        self.spf_lut = torch.from_numpy(tb.spf_lut.astype(np.int16)).to(dev)
+        table = tb.tiling_table if tb.tiling_table.size else \
+            np.zeros((1, tb.levels), np.uint16)
+        self.tiling_table = torch.from_numpy(
+            np.ascontiguousarray(table).astype(np.int16)).to(dev)
+        cols = tb.head_cols
+        if len(cols) > N.MAX_HEAD0:
+            raise DeviceError("tiling head too wide for the device tables")
+        d = N.SketchDesc()
+        d.levels, d.ndims, d.local_slots = tb.levels, tb.ndims, tb.local_slots
+        d.num_slots, d.ncas, d.max_fusible = tb.num_slots, tb.ncas, \
+            tb.max_fusible
+        d.n_unroll, d.max_feature_dims = tb.n_unroll, tb.max_feature_dims
+        d.feature_len = tb.feature_len
+        d.n_stages, d.n_tensors = len(tb.stage_first), len(tb.tensor_first)
+        d.n_terms, d.max_extent = len(tb.term_gi), tb.max_extent
+        d.n_head0 = len(cols)
+        for i in range(tb.ndims):
+            d.extents[i] = int(tb.extents[i])
+            d.tiling_counts[i] = int(tb.tiling_counts[i])
+            d.tiling_offsets[i] = int(tb.tiling_offsets[i])
+        for name in ("term_gi", "term_sc", "term_off", "tensor_first",
+                     "tensor_nterms", "stage_first", "stage_ntensors",
+                     "stage_inter", "stage_extra"):
+            arr = getattr(tb, name)
+            dst = getattr(d, name)
+            for i, v in enumerate(arr):
+                dst[i] = int(v)
+        S = tb.num_slots
+        for j, c in enumerate(cols):
+            if j == len(cols) - 1:
+                d.head0_src[j], d.head0_dst[j] = -1, -1
+            else:
+                d.head0_src[j], d.head0_dst[j] = int(c) // S, int(c) % S
+        d.flops_feature = tb.flops_feature
+        d.log2_lut = self.log2_lut.data_ptr()
+        d.spf_lut = self.spf_lut.data_ptr()
+        d.tiling_table = self.tiling_table.data_ptr()
+        self.desc = d
+        self.head_cols = cols
+
+    @property
+    def n_head0(self) -> int:
+        return len(self.head_cols)
+
+
+def alloc_state(n: int, tables: SketchTables, device=None, ld: int | None = None):
+    dev = _dev(device)
+    ld = n if ld is None else ld
+    tiles = torch.zeros((max(tables.local_slots, 1), max(ld, 1)),
+                        dtype=torch.int16, device=dev)
+    knobs = torch.zeros((3, max(ld, 1)), dtype=torch.uint8, device=dev)
+    return tiles, knobs
+
+
+def states_to_device(tables: SketchTables, tiles_np, knobs_np, device=None):
+    """Host [B, slots] u16 / [B, 3] u8 -> device SoA (slot-major)."""
+    dev = _dev(device)
+    t = np.ascontiguousarray(np.asarray(tiles_np, np.uint16).T)
+    if t.size == 0:
+        t = np.zeros((1, max(len(knobs_np), 1)), np.uint16)
+    k = np.ascontiguousarray(np.asarray(knobs_np, np.uint8).T)
+    return (torch.from_numpy(t.astype(np.int16)).to(dev),
+            torch.from_numpy(k).to(dev))
+
+
+def states_to_host(tables: SketchTables, tiles, knobs, n: int):
+    t = tiles[:tables.local_slots, :n].cpu().numpy().astype(np.uint16).T
+    k = knobs[:, :n].cpu().numpy().T
+    return np.ascontiguousarray(t), np.ascontiguousarray(k)
+
+
+# ---------------------------------------------------------------------------
+# batch operators
+
+
+def init_population(dsk: DeviceSketch, count: int, gen: np.random.Generator,
+                    tiles=None, knobs=None):
+    """sample_initial_schedules on device, advancing ``gen`` exactly."""
+    lib = N.load()
+    tb = dsk.tables
+    if tiles is None:
+        tiles, knobs = alloc_state(count, tb, dsk.device)
+    scratch = torch.zeros(4, dtype=torch.int64, device=dsk.device)
+    st = R.to_struct(gen)
+    used = C.c_int64(0)
+    with PF.span("init", count):
+        N.check(lib.harl_init_population(
+            C.byref(dsk.desc), C.byref(st), count, _ptr(tiles), _ptr(knobs),
+            tiles.shape[1], C.byref(used), _ptr(scratch), _stream()),
+            "harl_init_population")
+    R.skip_u32(gen, used.value)
+    return tiles, knobs
+
+
+def featurize(dsk: DeviceSketch, tiles, knobs, n: int, out=None):
+    lib = N.load()
+    F = dsk.tables.feature_len
+    if out is None:
+        out = torch.empty((max(n, 1), F), dtype=torch.float64,
+                          device=dsk.device)
+    with PF.span("featurize", n):
+        N.check(lib.harl_featurize(C.byref(dsk.desc), _ptr(tiles), _ptr(knobs),
+                                   n, tiles.shape[1], _ptr(out), _stream()),
+                "harl_featurize")
+    return out[:n]
+
+
+def action_masks(dsk: DeviceSketch, tiles, knobs, n: int):
+    lib = N.load()
+    S = dsk.tables.num_slots
+    tiling = torch.empty((max(n, 1), S * S + 1), dtype=torch.uint8,
+                         device=dsk.device)
+    shift = torch.empty((max(n, 1), 9), dtype=torch.uint8, device=dsk.device)
+    N.check(lib.harl_action_masks(C.byref(dsk.desc), _ptr(tiles), _ptr(knobs),
+                                  n, tiles.shape[1], _ptr(tiling), _ptr(shift),
+                                  _stream()), "harl_action_masks")
+    sh = shift[:n].bool()
+    return (tiling[:n].bool(), sh[:, 0:3], sh[:, 3:6], sh[:, 6:9])
+
+
+def apply_actions(dsk: DeviceSketch, tiles, knobs, n: int, actions):
+    """actions: host array [n][4] (the reference's (B, 4) layout); raises
+    InvalidActionError like the reference."""
+    lib = N.load()
+    a = torch.from_numpy(np.ascontiguousarray(
+        np.asarray(actions, dtype=np.int32).reshape(n, 4).T)).to(dsk.device)
+    t_out, k_out = alloc_state(n, dsk.tables, dsk.device, tiles.shape[1])
+    status = torch.full((1,), -1, dtype=torch.int64, device=dsk.device)
+    N.check(lib.harl_apply_actions(C.byref(dsk.desc), _ptr(tiles), _ptr(knobs),
+                                   n, tiles.shape[1], _ptr(a), _ptr(t_out),
+                                   _ptr(k_out), _ptr(status), _stream()),
+            "harl_apply_actions")
+    raise_status(int(status.item()) & ((1 << 64) - 1))
+    return t_out, k_out
+
+
+# ---------------------------------------------------------------------------
+# cost model
+
+
+class DeviceForest:
+    """A GBT ensemble in the device layout (costmodel.py:59-78).
+
+    ``trees`` are ``(feature, threshold, left, right, value)`` arrays per
+    tree; ``learning_rate * value`` is formed here with numpy, the same
+    fp64 product the reference computes per prediction."""
+
+    def __init__(self, trees, base: float, learning_rate: float,
+                 fitted: bool = True, floor_value: float = 1e-6,
+                 device=None):
+        N.load()
+        dev = _dev(device)
+        firsts, feats, lefts, rights, thrs, contribs = [], [], [], [], [], []
+        n = 0
+        for feat, thr, left, right, val in trees:
+            feat = np.asarray(feat)
+            _check_depth(feat, np.asarray(left), np.asarray(right))
+            firsts.append(n)
+            n += len(feat)
+            feats.append(feat.astype(np.int16))
+            lefts.append(np.asarray(left).astype(np.int16))
+            rights.append(np.asarray(right).astype(np.int16))
+            thrs.append(np.asarray(thr, dtype=np.float64))
+            contribs.append(learning_rate * np.asarray(val, dtype=np.float64))
+        if len(trees) > 1024:
+            raise DeviceError("more than 1024 trees")
+        cat = (lambda xs, dt: np.concatenate(xs).astype(dt)
+               if xs else np.zeros(1, dt))
+        self.n_nodes = n
+        self.tree_first = torch.from_numpy(cat([np.asarray(firsts)], np.int32)
+                                           if firsts else np.zeros(1, np.int32)
+                                           ).to(dev)
+        self.feature = torch.from_numpy(cat(feats, np.int16)).to(dev)
+        self.left = torch.from_numpy(cat(lefts, np.int16)).to(dev)
+        self.right = torch.from_numpy(cat(rights, np.int16)).to(dev)
+        self.threshold = torch.from_numpy(cat(thrs, np.float64)).to(dev)
+        self.leaf_contrib = torch.from_numpy(cat(contribs, np.float64)).to(dev)
+        d = N.ForestDesc()
+        d.n_trees = len(trees)
+        d.fitted = 1 if fitted else 0
+        d.base = float(base)
+        d.floor_value = float(floor_value)
+        d.tree_first = self.tree_first.data_ptr()
+        d.feature = self.feature.data_ptr()
+        d.left = self.left.data_ptr()
+        d.right = self.right.data_ptr()
+        d.threshold = self.threshold.data_ptr()
+        d.leaf_contrib = self.leaf_contrib.data_ptr()
+        self.desc = d
+        self.device = dev
+
+    @classmethod
+    def from_model(cls, model, device=None):
+        """From a reference ``SurrogateModel`` (duck-typed)."""
+        trees = [(t.feature, t.threshold, t.left, t.right, t.value)
+                 for t in model.trees]
+        return cls(trees, model.base, model.cfg.learning_rate,
+                   fitted=model.fitted, device=device)
+
+
+def _check_depth(feat, left, right):
+    depth = {0: 0}
+    stack = [0]
+    while stack:
+        nd = stack.pop()
+        if feat[nd] >= 0:
+            for ch in (int(left[nd]), int(right[nd])):
+                depth[ch] = depth[nd] + 1
+                if depth[ch] >= 64:
+                    raise DeviceError("tree deeper than the reference's "
+                                      "64-step walk")
+                stack.append(ch)
+    if len(feat) > 32767:
+        raise DeviceError("tree too large for int16 node indices")
+
+
+def gbt_predict(forest: DeviceForest, feat, n: int, old_score=None,
+                out=None, reward=None):
+    lib = N.load()
+    F = feat.shape[1]
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=feat.device)
+    if old_score is not None and reward is None:
+        reward = torch.empty(max(n, 1), dtype=torch.float64, device=feat.device)
+    with PF.span("gbt", n):
+        N.check(lib.harl_gbt_predict(C.byref(forest.desc), _ptr(feat), n, F,
+                                     _ptr(out), _ptr(old_score), _ptr(reward),
+                                     forest.n_nodes, _stream()),
+                "harl_gbt_predict")
+    return (out[:n], reward[:n]) if old_score is not None else out[:n]
+
+
+# ---------------------------------------------------------------------------
+# agent parameters on device
+
+
+class DeviceAgent:
+    """fp64 master parameters + Adam moments + fp32 rollout copy in one flat
+    layout per subgraph agent.  The tiling head is stored compact over
+    ``head_columns(S, L)``: every other column of the reference's
+    ``S*S+1``-wide head has probability zero for every state, hence zero
+    gradient and zero Adam moments forever, so it never changes and is left
+    untouched in the host arrays."""
+
+    def __init__(self, agent, levels: int, device=None):
+        N.load()
+        dev = _dev(device)
+        self.agent = agent
+        self.device = dev
+        hidden = tuple(agent.hidden)
+        S = agent.num_slots
+        F = agent.feature_len
+        if len(hidden) > N.MAX_LAYERS or max(hidden) > N.MAX_HIDDEN or \
+                F > N.MAX_FEATURES:
+            raise DeviceError("network shape beyond the device kernels' limits")
+        self.cols = head_columns(S, levels)
+        self.C0 = len(self.cols)
+        self.NH = self.C0 + 9
+        self.hidden, self.F, self.S = hidden, F, S
+        nt = len(hidden)
+        # ---- flat layout ----
+        off = 0
+        pl = N.NetLayout()
+        pl.n_layers = nt
+        dims = [F, *hidden]
+        for i, d in enumerate(dims):
+            pl.dims[i] = d
+        for l in range(nt):
+            pl.off_W[l] = off
+            off += dims[l] * dims[l + 1]
+            pl.off_b[l] = off
+            off += dims[l + 1]
+        H = hidden[-1]
+        pl.off_hW = off
+        off += H * self.NH
+        pl.off_hb = off
+        off += self.NH
+        pl.n_head_cols = self.NH
+        self.n_pi = off
+        vl = N.NetLayout()
+        vdims = [F, *hidden, 1]
+        vl.n_layers = len(vdims) - 1
+        for i, d in enumerate(vdims):
+            vl.dims[i] = d
+        for l in range(vl.n_layers):
+            vl.off_W[l] = off
+            off += vdims[l] * vdims[l + 1]
+            vl.off_b[l] = off
+            off += vdims[l + 1]
+        self.n_params = off
+        # ---- per-row PPO scratch offsets ----
+        r = 0
+        pl.row_act[0] = vl.row_act[0] = r
+        r += F
+        for l in range(1, nt + 1):
+            pl.row_act[l] = r
+            r += dims[l]
+        pl.row_head = r
+        r += self.NH
+        for l in range(nt):
+            pl.row_delta[l] = r
+            r += dims[l + 1]
+        for l in range(1, vl.n_layers + 1):
+            vl.row_act[l] = r
+            r += vdims[l]
+        for l in range(vl.n_layers):
+            vl.row_delta[l] = r
+            r += vdims[l + 1]
+        self.row_stride = r
+        self.pol_layout, self.val_layout = pl, vl
+        self.params = torch.zeros(self.n_params, dtype=torch.float64, device=dev)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.grads = torch.zeros_like(self.params)
+        self.params32 = torch.zeros(self.n_params, dtype=torch.float32,
+                                    device=dev)
+        self.losses = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.head0_src = np.asarray(
+            [int(c) // S if j < self.C0 - 1 else 0
+             for j, c in enumerate(self.cols)], dtype=np.int16)
+        self._build_descs()
+        self.upload()
+
+    # -- host <-> device --------------------------------------------------
+
+    def _pack(self, pol_list, val_list) -> np.ndarray:
+        out = np.zeros(self.n_params, dtype=np.float64)
+        pl, vl = self.pol_layout, self.val_layout
+        nt = len(self.hidden)
+        for l in range(nt):
+            W, b = pol_list[2 * l], pol_list[2 * l + 1]
+            out[pl.off_W[l]:pl.off_W[l] + W.size] = W.reshape(-1)
+            out[pl.off_b[l]:pl.off_b[l] + b.size] = b
+        heads = pol_list[2 * nt:]
+        H = self.hidden[-1]
+        hW = np.zeros((H, self.NH))
+        hb = np.zeros(self.NH)
+        hW[:, :self.C0] = heads[0][:, self.cols]
+        hb[:self.C0] = heads[1][self.cols]
+        for h in range(3):
+            hW[:, self.C0 + 3 * h:self.C0 + 3 * h + 3] = heads[2 + 2 * h]
+            hb[self.C0 + 3 * h:self.C0 + 3 * h + 3] = heads[3 + 2 * h]
+        out[pl.off_hW:pl.off_hW + hW.size] = hW.reshape(-1)
+        out[pl.off_hb:pl.off_hb + self.NH] = hb
+        for l in range(vl.n_layers):
+            W, b = val_list[2 * l], val_list[2 * l + 1]
+            out[vl.off_W[l]:vl.off_W[l] + W.size] = W.reshape(-1)
+            out[vl.off_b[l]:vl.off_b[l] + b.size] = b
+        return out
+
+    def _unpack_into(self, flat: np.ndarray, pol_list, val_list):
+        pl, vl = self.pol_layout, self.val_layout
+        nt = len(self.hidden)
+        for l in range(nt):
+            W, b = pol_list[2 * l], pol_list[2 * l + 1]
+            W[...] = flat[pl.off_W[l]:pl.off_W[l] + W.size].reshape(W.shape)
+            b[...] = flat[pl.off_b[l]:pl.off_b[l] + b.size]
+        H = self.hidden[-1]
+        hW = flat[pl.off_hW:pl.off_hW + H * self.NH].reshape(H, self.NH)
+        hb = flat[pl.off_hb:pl.off_hb + self.NH]
+        heads = pol_list[2 * nt:]
+        heads[0][:, self.cols] = hW[:, :self.C0]
+        heads[1][self.cols] = hb[:self.C0]
+        for h in range(3):
+            heads[2 + 2 * h][...] = hW[:, self.C0 + 3 * h:self.C0 + 3 * h + 3]
+            heads[3 + 2 * h][...] = hb[self.C0 + 3 * h:self.C0 + 3 * h + 3]
+        for l in range(vl.n_layers):
+            W, b = val_list[2 * l], val_list[2 * l + 1]
+            W[...] = flat[vl.off_W[l]:vl.off_W[l] + W.size].reshape(W.shape)
+            b[...] = flat[vl.off_b[l]:vl.off_b[l] + b.size]
+
+    def upload(self):
+        a = self.agent
+        p = torch.from_numpy(self._pack(a.policy, a.value)).to(self.device)
+        self.params.copy_(p)
+        self.params32.copy_(p.float())
+        self.m.copy_(torch.from_numpy(self._pack(a.opt_pi.m, a.opt_v.m)))
+        self.v.copy_(torch.from_numpy(self._pack(a.opt_pi.v, a.opt_v.v)))
+
+    def download(self):
+        """Write device params and moments back into the numpy lists."""
+        a = self.agent
+        self._unpack_into(self.params.cpu().numpy(), a.policy, a.value)
+        self._unpack_into(self.m.cpu().numpy(), a.opt_pi.m, a.opt_v.m)
+        self._unpack_into(self.v.cpu().numpy(), a.opt_pi.v, a.opt_v.v)
+
+    def _build_descs(self):
+        base = self.params32.data_ptr()
+        f4 = 4
+        pl, vl = self.pol_layout, self.val_layout
+        pd = N.MlpDesc()
+        pd.n_layers = pl.n_layers
+        for i in range(pl.n_layers + 1):
+            pd.dims[i] = pl.dims[i]
+        for l in range(pl.n_layers):
+            pd.W[l] = base + f4 * pl.off_W[l]
+            pd.b[l] = base + f4 * pl.off_b[l]
+        pd.head_W = base + f4 * pl.off_hW
+        pd.head_b = base + f4 * pl.off_hb
+        pd.n_head_cols = self.NH
+        vd = N.MlpDesc()
+        vd.n_layers = vl.n_layers
+        for i in range(vl.n_layers + 1):
+            vd.dims[i] = vl.dims[i]
+        for l in range(vl.n_layers):
+            vd.W[l] = base + f4 * vl.off_W[l]
+            vd.b[l] = base + f4 * vl.off_b[l]
+        self.pol_desc, self.val_desc = pd, vd
+
+    # -- PPO ----------------------------------------------------------------
+
+    def ppo_update(self, ring, slots, cfg, t_pi: int, t_v: int,
+                   scratch=None, losses=None):
+        """One ppo_update on replay ``slots`` (device int32 ring slots).
+        ``t_pi``/``t_v`` are the Adam step counts AFTER this update."""
+        lib = N.load()
+        B = int(slots.shape[0])
+        hp = N.PpoHyper()
+        hp.clip_ratio = cfg.clip_ratio
+        hp.entropy_weight = cfg.entropy_weight
+        hp.value_loss_weight = cfg.value_loss_weight
+        hp.lr_actor, hp.lr_critic = cfg.lr_actor, cfg.lr_critic
+        b1, b2 = 0.9, 0.999
+        hp.beta1, hp.beta2 = b1, b2
+        hp.one_m_beta1, hp.one_m_beta2 = 1.0 - b1, 1.0 - b2
+        hp.eps = 1e-8
+        hp.b1t_pi, hp.b2t_pi = 1.0 - b1 ** t_pi, 1.0 - b2 ** t_pi
+        hp.b1t_v, hp.b2t_v = 1.0 - b1 ** t_v, 1.0 - b2 ** t_v
+        if scratch is None:
+            nbytes = lib.harl_ppo_scratch_bytes(B, self.row_stride, 0)
+            scratch = torch.empty(nbytes, dtype=torch.uint8,
+                                  device=self.device)
+        if losses is None:
+            losses = self.losses
+        src = self.head0_src.ctypes.data_as(C.c_void_p)
+        with PF.span("ppo", B, launches=4):
+          N.check(lib.harl_ppo_update(
+            C.byref(self.pol_layout), C.byref(self.val_layout), C.byref(hp),
+            C.byref(ring.desc), _ptr(slots), B, self.F, self.C0, src,
+            self.row_stride, _ptr(self.params), _ptr(self.grads), _ptr(self.m),
+            _ptr(self.v), _ptr(self.params32), self.n_pi, self.n_params,
+            _ptr(losses), _ptr(self.bad), _ptr(scratch), _stream()),
+            "harl_ppo_update")
+        return losses
+
+
+def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
+                n: int, gen=None, inject=None, out=None, want_logits=False):
+    """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
+    ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
+    Returns a dict of device tensors; ``status`` must be checked by the
+    caller (``raise_status``)."""
+    lib = N.load()
+    dev = dsk.device
+    if out is None:
+        ld = tiles.shape[1]
+        t_o, k_o = alloc_state(n, dsk.tables, dev, ld)
+        out = {"actions": torch.empty((4, max(n, 1)), dtype=torch.int32,
+                                      device=dev),
+               "logp": torch.empty(max(n, 1), dtype=torch.float64, device=dev),
+               "tiles": t_o, "knobs": k_o,
+               "move_bits": torch.empty(max(n, 1), dtype=torch.int64,
+                                        device=dev),
+               "shift_bits": torch.empty(max(n, 1), dtype=torch.int32,
+                                         device=dev),
+               "head0_col": torch.empty(max(n, 1), dtype=torch.int32,
+                                        device=dev),
+               "status": torch.full((1,), -1, dtype=torch.int64, device=dev)}
+    else:
+        out["status"].fill_(-1)
+    logits = None
+    if want_logits:
+        logits = torch.empty((max(n, 1), agent.NH), dtype=torch.float32,
+                             device=dev)
+    st = R.to_struct(gen) if gen is not None else None
+    inj = None
+    if inject is not None:
+        inj = torch.as_tensor(np.ascontiguousarray(np.asarray(inject).T),
+                              dtype=torch.int32).to(dev).contiguous()
+    with PF.span("policy", n):
+      N.check(lib.harl_policy_step(
+        C.byref(dsk.desc), C.byref(agent.pol_desc), _ptr(feat), _ptr(tiles),
+        _ptr(knobs), n, tiles.shape[1], C.byref(st) if st is not None else None,
+        _ptr(inj), _ptr(out["actions"]), _ptr(out["logp"]), _ptr(out["tiles"]),
+        _ptr(out["knobs"]), _ptr(out["move_bits"]), _ptr(out["shift_bits"]),
+        _ptr(out["head0_col"]), _ptr(logits), _ptr(out["status"]), _stream()),
+        "harl_policy_step")
+    if gen is not None and inject is None:
+        R.skip_u64(gen, 4 * n)
+    if want_logits:
+        out["logits"] = logits[:n]
+    return out
+
+
+def value_estimate(agent: DeviceAgent, feat, n: int, out=None):
+    lib = N.load()
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.float32, device=feat.device)
+    with PF.span("value", n):
+        N.check(lib.harl_value_forward(C.byref(agent.val_desc), _ptr(feat), n,
+                                       feat.shape[1], _ptr(out), _stream()),
+                "harl_value_forward")
+    return out[:n]
+
+
+class DeviceReplay:
+    """The replay FIFO as a device ring (rlcore.py:253-274)."""
+
+    def __init__(self, capacity: int, feature_len: int, device=None):
+        dev = _dev(device)
+        self.cap = int(capacity)
+        self.F = feature_len
+        self.X = torch.zeros((self.cap, feature_len), dtype=torch.float64,
+                             device=dev)
+        self.Xn = torch.zeros_like(self.X)
+        self.actions = torch.zeros((self.cap, 4), dtype=torch.int32, device=dev)
+        self.scalars = torch.zeros((self.cap, 4), dtype=torch.float64,
+                                   device=dev)
+        self.move_bits = torch.zeros(self.cap, dtype=torch.int64, device=dev)
+        self.shift_bits = torch.zeros(self.cap, dtype=torch.int32, device=dev)
+        self.count = 0
+        self.wpos = 0
+        d = N.ReplayRing()
+        d.X, d.Xn = self.X.data_ptr(), self.Xn.data_ptr()
+        d.actions, d.scalars = self.actions.data_ptr(), self.scalars.data_ptr()
+        d.move_bits = self.move_bits.data_ptr()
+        d.shift_bits = self.shift_bits.data_ptr()
+        d.cap = self.cap
+        self.desc = d
+        self.device = dev
+
+    def __len__(self):
+        return self.count
+
+    def slots_of(self, idx: np.ndarray) -> np.ndarray:
+        """Buffer positions (0 = oldest) -> ring slots."""
+        start = (self.wpos - self.count) % self.cap
+        return ((start + np.asarray(idx, dtype=np.int64)) % self.cap) \
+            .astype(np.int32)
+
+    def note_push(self, n: int):
+        self.wpos = (self.wpos + n) % self.cap
+        self.count = min(self.cap, self.count + n)
+
+
+def masks_to_bits(masks, num_slots: int, levels: int):
+    """ActionMask arrays (tiling [B, S*S+1], 3x [B, 3]) -> (move bits,
+    shift bits).  A slot is movable iff any same-dim move out of it is
+    legal (schedspace.py:241-248)."""
+    tiling = np.asarray(masks[0], dtype=bool)
+    B = len(tiling)
+    S, L = num_slots, levels
+    move = np.zeros(B, dtype=np.uint64)
+    if L >= 2:
+        for src in range(S):
+            dst = (src // L) * L + (src % L + 1) % L
+            move |= tiling[:, src * S + dst].astype(np.uint64) << np.uint64(src)
+    shift = np.zeros(B, dtype=np.uint32)
+    for h in range(3):
+        m = np.asarray(masks[1 + h], dtype=bool)
+        for j in range(3):
+            shift |= m[:, j].astype(np.uint32) << np.uint32(3 * h + j)
+    return move, shift
+
+
+def bits_to_masks(move, shift, num_slots: int, levels: int):
+    """Inverse of masks_to_bits (materialises the reference's boolean
+    masks, e.g. for checkpoints, tuner.py:683-684)."""
+    move = np.asarray(move).astype(np.uint64)
+    shift = np.asarray(shift).astype(np.uint32)
+    B = len(move)
+    S, L = num_slots, levels
+    tiling = np.zeros((B, S * S + 1), dtype=bool)
+    tiling[:, -1] = True
+    for src in range(S):
+        bit = ((move >> np.uint64(src)) & np.uint64(1)).astype(bool)
+        base = (src // L) * L
+        for dst in range(base, base + L):
+            if dst != src:
+                tiling[:, src * S + dst] = bit
+    out = [tiling]
+    for h in range(3):
+        out.append(np.stack([((shift >> np.uint32(3 * h + j)) & 1).astype(bool)
+                             for j in range(3)], axis=1))
+    return tuple(out)
+
+
+def _replay_load(self, X, Xn, actions, logp, reward, adv, td, masks,
+                 num_slots: int, levels: int):
+    """Replace the ring contents with host transitions (oldest first),
+    like rebuilding the reference's deque (tuner.py:752-768)."""
+    n = len(X)
+    if n > self.cap:
+        raise ValueError("more transitions than ring capacity")
+    cols = head_columns(num_slots, levels)
+    col_of = {int(c): j for j, c in enumerate(cols)}
+    acts = np.asarray(actions, dtype=np.int64).reshape(n, 4).copy()
+    acts[:, 0] = [col_of[int(a)] for a in acts[:, 0]]
+    move, shift = masks_to_bits(masks, num_slots, levels)
+    dev = self.device
+    if n:
+        self.X[:n].copy_(torch.from_numpy(np.asarray(X, np.float64)))
+        self.Xn[:n].copy_(torch.from_numpy(np.asarray(Xn, np.float64)))
+        self.actions[:n].copy_(torch.from_numpy(acts.astype(np.int32)))
+        sc = np.stack([logp, reward, adv, td], axis=1).astype(np.float64)
+        self.scalars[:n].copy_(torch.from_numpy(sc))
+        self.move_bits[:n].copy_(torch.from_numpy(move.view(np.int64)))
+        self.shift_bits[:n].copy_(torch.from_numpy(shift.view(np.int32)))
+    self.count = n
+    self.wpos = n % self.cap
+    del dev
+
+
+def _replay_export(self, num_slots: int, levels: int):
+    """Ring contents oldest-first as host arrays with full head indices and
+    materialised boolean masks."""
+    n = self.count
+    start = (self.wpos - n) % self.cap
+    order = (start + np.arange(n)) % self.cap
+    idx = torch.from_numpy(order).to(self.device)
+    cols = head_columns(num_slots, levels)
+    acts = self.actions[idx].cpu().numpy().astype(np.int64)
+    if n:
+        acts[:, 0] = cols[acts[:, 0]]
+    sc = self.scalars[idx].cpu().numpy()
+    move = self.move_bits[idx].cpu().numpy().view(np.uint64)
+    shift = self.shift_bits[idx].cpu().numpy().view(np.uint32)
+    return {"X": self.X[idx].cpu().numpy(), "Xn": self.Xn[idx].cpu().numpy(),
+            "actions": acts, "logp": sc[:, 0], "reward": sc[:, 1],
+            "adv": sc[:, 2], "td": sc[:, 3],
+            "masks": bits_to_masks(move, shift, num_slots, levels)}
+
+
+DeviceReplay.load = _replay_load
+DeviceReplay.export = _replay_export

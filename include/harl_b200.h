@@ -182,6 +182,29 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                      uint32_t* shift_bits, int32_t* head0_col,
                      float* logits_out, uint64_t* status, void* stream);
 
+/* select_actions + walker as harl_policy_step, on the tcgen05 path when
+ * the policy is the production shape (hidden (128,128), feature_len <= 64,
+ * n_head0 + 9 <= 128): trunk and heads as 3xTF32 tcgen05 MMAs with TMEM
+ * accumulators and TMEM-resident activations.  hid_scratch: float32
+ * [n][128] device scratch.  Falls back to NOTHING: returns HARL_E_ARG if
+ * the shape is not eligible (the caller then uses harl_policy_step). */
+int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+                        const double* feat, const uint16_t* tiles,
+                        const uint8_t* knobs, int64_t n, int64_t ld,
+                        const harl_pcg64* rng, const int32_t* inject,
+                        int32_t* actions, double* logp, uint16_t* tiles_out,
+                        uint8_t* knobs_out, uint64_t* move_bits,
+                        uint32_t* shift_bits, int32_t* head0_col,
+                        float* logits_out, uint64_t* status,
+                        float* hid_scratch, void* stream);
+
+/* V(X) and V(X') in one launch (tuner.py:395-396) on the tcgen05 path
+ * (hidden (128,128), feature_len <= 64); HARL_E_ARG if not eligible. */
+int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
+                       int64_t n0, const double* feat1, int64_t n1,
+                       int32_t feature_len, float* v0, float* v1,
+                       void* stream);
+
 /* ValueNet.estimate (rlcore.py:173) on feat (fp64 rows, fp32 math). */
 int harl_value_forward(const harl_mlp_desc* val, const double* feat,
                        int64_t n, int32_t feature_len, float* v_out,
@@ -298,6 +321,13 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     double* adam_m, double* adam_v, float* params32,
                     int64_t n_pi, int64_t n_params, double* losses,
                     int32_t* bad, void* scratch, void* stream);
+
+/* Diagnostic: one 128x128x64 kind::tf32 tcgen05 MMA (A [128][64], B
+ * [64][128] row-major fp32, D [128][128]); mode 0 = A from TMEM, 1 = A
+ * from shared memory.  Used by the GPU tests to pin the descriptor
+ * layouts the MLP kernels rely on. */
+int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
+                          void* stream);
 
 #ifdef __cplusplus
 }

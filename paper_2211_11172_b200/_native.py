@@ -122,12 +122,18 @@ _SIGS = {
                                P(Pcg64), vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                vp, vp]),
     "harl_value_forward": (i32, [P(MlpDesc), vp, i64, i32, vp, vp]),
+    "harl_policy_step_tc": (i32, [P(SketchDesc), P(MlpDesc), vp, vp, vp, i64,
+                                  i64, P(Pcg64), vp, vp, vp, vp, vp, vp, vp,
+                                  vp, vp, vp, vp, vp]),
+    "harl_value_pair_tc": (i32, [P(MlpDesc), vp, i64, vp, i64, i32, vp, vp,
+                                 vp]),
     "harl_finish_step": (i32, [P(StepBuffers), i64, i64, i64, i32, i32, f64,
                                i32, P(ReplayRing), i64, i64, P(EntryLog),
                                P(TrackStats), vp]),
     "harl_gather_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp,
                                vp, vp, vp, vp, i64, vp]),
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),
+    "harl_selftest_tcgen05": (i32, [vp, vp, vp, i32, vp]),
     "harl_ppo_update": (i32, [P(NetLayout), P(NetLayout), P(PpoHyper),
                               P(ReplayRing), vp, i32, i32, i32, vp, i32, vp,
                               vp, vp, vp, vp, i64, i64, vp, vp, vp, vp]),

@@ -12,6 +12,8 @@
 #include "space_kernels.cuh"
 #include "episode_kernels.cuh"
 #include "ppo_kernels.cuh"
+#include "tc_probe.cuh"
+#include "mlp_tc.cuh"
 
 namespace harl {
 
@@ -306,6 +308,122 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   return HARL_OK;
 }
 
+static bool tc_trunk_ok(const harl_mlp_desc* m, int F) {
+  return m && m->n_layers >= 2 && m->dims[0] == F && F <= TC_K1 &&
+         m->dims[1] == TC_H && m->dims[2] == TC_H;
+}
+
+static int sm_count() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return v;
+}
+
+int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+                        const double* feat, const uint16_t* tiles,
+                        const uint8_t* knobs, int64_t n, int64_t ld,
+                        const harl_pcg64* rng, const int32_t* inject,
+                        int32_t* actions, double* logp, uint16_t* tiles_out,
+                        uint8_t* knobs_out, uint64_t* move_bits,
+                        uint32_t* shift_bits, int32_t* head0_col,
+                        float* logits_out, uint64_t* status,
+                        float* hid_scratch, void* stream) {
+  int rc = check_sketch(sk);
+  if (rc) return rc;
+  if ((rc = check_mlp(pol, true))) return rc;
+  if (pol->n_layers != 2 || !tc_trunk_ok(pol, sk->feature_len) ||
+      pol->n_head_cols != sk->n_head0 + 9 || pol->n_head_cols > HEADS_NMAX ||
+      !hid_scratch) {
+    set_error("harl_policy_step_tc: shape not eligible for the tcgen05 path");
+    return HARL_E_ARG;
+  }
+  if (n <= 0) return HARL_OK;
+  if (!rng && !inject) {
+    set_error("harl_policy_step_tc: need rng or injected actions");
+    return HARL_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = allow_smem(k_trunk_tc<TRUNK_POLICY>, TRUNK_SMEM, "k_trunk_tc")))
+    return rc;
+  TrunkArgs ta;
+  memset(&ta, 0, sizeof(ta));
+  ta.feat0 = feat;
+  ta.n0 = n;
+  ta.F = sk->feature_len;
+  ta.out0 = hid_scratch;
+  ta.W1 = pol->W[0];
+  ta.b1 = pol->b[0];
+  ta.W2 = pol->W[1];
+  ta.b2 = pol->b[1];
+  const int64_t tiles_n = (n + 127) / 128;
+  const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+  k_trunk_tc<TRUNK_POLICY><<<grid, 128, TRUNK_SMEM, st>>>(ta);
+  HARL_CHECK_LAUNCH("k_trunk_tc<policy>");
+  HeadsArgs ha;
+  ha.hid = hid_scratch;
+  ha.Wh = pol->head_W;
+  ha.bh = pol->head_b;
+  ha.NH = pol->n_head_cols;
+  ha.NHP = (ha.NH + 15) / 16 * 16;
+  const size_t smem = (size_t)2 * ha.NHP * TC_H * 4 + HEADS_NMAX * 4 +
+                      (size_t)128 * (ha.NHP + 1) * 4;
+  if ((rc = allow_smem(k_heads_tc<0>, smem, "k_heads_tc"))) return rc;
+  PcgJump J;
+  StepRng sr;
+  memset(&J, 0, sizeof(J));
+  memset(&sr, 0, sizeof(sr));
+  if (rng) {
+    build_jump(*rng, &J);
+    sr.s = state_of(*rng);
+  }
+  k_heads_tc<0><<<grid, HEADS_THREADS, smem, st>>>(
+      ha, *sk, J, sr, tiles, knobs, n, ld, inject, actions, logp, tiles_out,
+      knobs_out, move_bits, shift_bits, head0_col, logits_out,
+      (unsigned long long*)status);
+  HARL_CHECK_LAUNCH("k_heads_tc");
+  return HARL_OK;
+}
+
+int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
+                       int64_t n0, const double* feat1, int64_t n1,
+                       int32_t feature_len, float* v0, float* v1,
+                       void* stream) {
+  int rc = check_mlp(val, false);
+  if (rc) return rc;
+  if (val->n_layers != 3 || !tc_trunk_ok(val, feature_len) ||
+      val->dims[3] != 1) {
+    set_error("harl_value_pair_tc: shape not eligible for the tcgen05 path");
+    return HARL_E_ARG;
+  }
+  if (n0 + n1 <= 0) return HARL_OK;
+  if ((rc = allow_smem(k_trunk_tc<TRUNK_VALUE>, TRUNK_SMEM, "k_trunk_tc")))
+    return rc;
+  TrunkArgs ta;
+  memset(&ta, 0, sizeof(ta));
+  ta.feat0 = feat0;
+  ta.feat1 = feat1;
+  ta.n0 = n0;
+  ta.n1 = feat1 ? n1 : 0;
+  ta.F = feature_len;
+  ta.out0 = v0;
+  ta.out1 = v1;
+  ta.W1 = val->W[0];
+  ta.b1 = val->b[0];
+  ta.W2 = val->W[1];
+  ta.b2 = val->b[1];
+  ta.w3 = val->W[2];
+  ta.b3 = val->b[2];
+  const int64_t tiles_n = (n0 + 127) / 128 + (ta.n1 + 127) / 128;
+  const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+  k_trunk_tc<TRUNK_VALUE><<<grid, 128, TRUNK_SMEM, (cudaStream_t)stream>>>(ta);
+  HARL_CHECK_LAUNCH("k_trunk_tc<value>");
+  return HARL_OK;
+}
+
 int harl_value_forward(const harl_mlp_desc* val, const double* feat, int64_t n,
                        int32_t feature_len, float* v_out, void* stream) {
   int rc = check_mlp(val, false);
@@ -405,6 +523,16 @@ static int build_grad_jobs(const harl_net_layout& P, const harl_net_layout& V,
   }
   *n_jobs = nj;
   *n_tiles = tiles;
+  return HARL_OK;
+}
+
+int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
+                          void* stream) {
+  const size_t smem = (PROBE_N + PROBE_M) * PROBE_K * 4 + 1024;
+  int rc = allow_smem(k_tc_probe, smem, "k_tc_probe");
+  if (rc) return rc;
+  k_tc_probe<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, D, mode);
+  HARL_CHECK_LAUNCH("k_tc_probe");
   return HARL_OK;
 }
 

@@ -145,36 +145,21 @@ __device__ inline int warp_sample(const float* z, int C, Legal legal, double u,
   return ok ? idx : -1;  // -1: reference would land on full index 0
 }
 
-__global__ void __launch_bounds__(MLP_THREADS)
-k_policy_step(const __grid_constant__ harl_sketch_desc sk,
-              const __grid_constant__ harl_mlp_desc net,
-              const __grid_constant__ PcgJump J, StepRng rng,
-              const double* feat, const uint16_t* tiles, const uint8_t* knobs,
-              int64_t n, int64_t ld, const int32_t* inject, int32_t* actions,
-              double* logp, uint16_t* tiles_out, uint8_t* knobs_out,
-              uint64_t* move_bits, uint32_t* shift_bits, int32_t* head0_col,
-              float* logits_out, unsigned long long* status, int ldbuf) {
-  extern __shared__ float smem[];
-  float* bufA = smem;
-  float* bufB = smem + MLP_TM * ldbuf;
-  const int64_t r0 = (int64_t)blockIdx.x * MLP_TM;
-  const int F = sk.feature_len;
-  load_rows(feat, r0, n, F, bufA, ldbuf);
-  __syncthreads();
-  int width;
-  float* hid = run_layers(net, bufA, bufB, ldbuf, 0, &width);
-  float* logits = (hid == bufA) ? bufB : bufA;
-  const int NH = net.n_head_cols;  // n_head0 + 9
-  dense_tile(hid, ldbuf, width, net.head_W, net.head_b, NH, logits, ldbuf, false);
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Sampling epilogue for one row, executed by one warp: masked
+// log-softmax per head, inverse-CDF draw on the PCG64 stream (or the
+// injected action), then decode + apply.  Shared by the FFMA and tcgen05
+// policy kernels.
+__device__ inline void policy_row(
+    const harl_sketch_desc& sk, const PcgJump& J, const StepRng& rng,
+    const float* z, int NH, const uint16_t* tiles, const uint8_t* knobs,
+    int64_t n, int64_t ld, int64_t r, const int32_t* inject, int32_t* actions,
+    double* logp, uint16_t* tiles_out, uint8_t* knobs_out, uint64_t* move_bits,
+    uint32_t* shift_bits, int32_t* head0_col, float* logits_out,
+    unsigned long long* status) {
+  const int lane = threadIdx.x & 31;
   const int C0 = sk.n_head0;
   const int S = sk.num_slots;
-  for (int rr = warp; rr < MLP_TM; rr += MLP_THREADS / 32) {
-    const int64_t r = r0 + rr;
-    if (r >= n) break;
-    const float* z = logits + rr * ldbuf;
+  {
     if (logits_out)
       for (int j = lane; j < NH; j += 32) logits_out[r * NH + j] = z[j];
     // movable slots of the current state
@@ -274,6 +259,39 @@ k_policy_step(const __grid_constant__ harl_sketch_desc sk,
       report_status(status, r, code);
     }
     __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(MLP_THREADS)
+k_policy_step(const __grid_constant__ harl_sketch_desc sk,
+              const __grid_constant__ harl_mlp_desc net,
+              const __grid_constant__ PcgJump J, StepRng rng,
+              const double* feat, const uint16_t* tiles, const uint8_t* knobs,
+              int64_t n, int64_t ld, const int32_t* inject, int32_t* actions,
+              double* logp, uint16_t* tiles_out, uint8_t* knobs_out,
+              uint64_t* move_bits, uint32_t* shift_bits, int32_t* head0_col,
+              float* logits_out, unsigned long long* status, int ldbuf) {
+  extern __shared__ float smem[];
+  float* bufA = smem;
+  float* bufB = smem + MLP_TM * ldbuf;
+  const int64_t r0 = (int64_t)blockIdx.x * MLP_TM;
+  const int F = sk.feature_len;
+  load_rows(feat, r0, n, F, bufA, ldbuf);
+  __syncthreads();
+  int width;
+  float* hid = run_layers(net, bufA, bufB, ldbuf, 0, &width);
+  float* logits = (hid == bufA) ? bufB : bufA;
+  const int NH = net.n_head_cols;  // n_head0 + 9
+  dense_tile(hid, ldbuf, width, net.head_W, net.head_b, NH, logits, ldbuf, false);
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5;
+  for (int rr = warp; rr < MLP_TM; rr += MLP_THREADS / 32) {
+    const int64_t r = r0 + rr;
+    if (r >= n) break;
+    policy_row(sk, J, rng, logits + rr * ldbuf, NH, tiles, knobs, n, ld, r,
+               inject, actions, logp, tiles_out, knobs_out, move_bits,
+               shift_bits, head0_col, logits_out, status);
   }
 }
 

@@ -22,6 +22,7 @@ this module                    reference
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -398,6 +399,9 @@ class DeviceAgent:
                                     device=dev)
         self.losses = torch.zeros(8, dtype=torch.float64, device=dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.tc = (hidden == (128, 128) and F <= 64 and self.NH <= 128
+                   and os.environ.get("HARL_KERNELS", "tc") != "ffma")
+        self._hid = None
         self.head0_src = np.asarray(
             [int(c) // S if j < self.C0 - 1 else 0
              for j, c in enumerate(self.cols)], dtype=np.int16)
@@ -490,6 +494,12 @@ class DeviceAgent:
             vd.b[l] = base + f4 * vl.off_b[l]
         self.pol_desc, self.val_desc = pd, vd
 
+    def hid_scratch(self, n: int):
+        if self._hid is None or self._hid.shape[0] < n:
+            self._hid = torch.empty((max(n, 1), 128), dtype=torch.float32,
+                                    device=self.device)
+        return self._hid
+
     # -- PPO ----------------------------------------------------------------
 
     def ppo_update(self, ring, slots, cfg, t_pi: int, t_v: int,
@@ -560,14 +570,20 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
     if inject is not None:
         inj = torch.as_tensor(np.ascontiguousarray(np.asarray(inject).T),
                               dtype=torch.int32).to(dev).contiguous()
-    with PF.span("policy", n):
-      N.check(lib.harl_policy_step(
-        C.byref(dsk.desc), C.byref(agent.pol_desc), _ptr(feat), _ptr(tiles),
-        _ptr(knobs), n, tiles.shape[1], C.byref(st) if st is not None else None,
-        _ptr(inj), _ptr(out["actions"]), _ptr(out["logp"]), _ptr(out["tiles"]),
-        _ptr(out["knobs"]), _ptr(out["move_bits"]), _ptr(out["shift_bits"]),
-        _ptr(out["head0_col"]), _ptr(logits), _ptr(out["status"]), _stream()),
-        "harl_policy_step")
+    args = [C.byref(dsk.desc), C.byref(agent.pol_desc), _ptr(feat),
+            _ptr(tiles), _ptr(knobs), n, tiles.shape[1],
+            C.byref(st) if st is not None else None, _ptr(inj),
+            _ptr(out["actions"]), _ptr(out["logp"]), _ptr(out["tiles"]),
+            _ptr(out["knobs"]), _ptr(out["move_bits"]),
+            _ptr(out["shift_bits"]), _ptr(out["head0_col"]), _ptr(logits),
+            _ptr(out["status"])]
+    if agent.tc:
+        with PF.span("policy_tc", n, launches=2):
+            N.check(lib.harl_policy_step_tc(*args, _ptr(agent.hid_scratch(n)),
+                                            _stream()), "harl_policy_step_tc")
+    else:
+        with PF.span("policy", n):
+            N.check(lib.harl_policy_step(*args, _stream()), "harl_policy_step")
     if gen is not None and inject is None:
         R.skip_u64(gen, 4 * n)
     if want_logits:
@@ -584,6 +600,23 @@ def value_estimate(agent: DeviceAgent, feat, n: int, out=None):
                                        feat.shape[1], _ptr(out), _stream()),
                 "harl_value_forward")
     return out[:n]
+
+
+def value_pair(agent: DeviceAgent, feat0, n0: int, feat1, n1: int,
+               out0, out1):
+    """V(X) and V(X') (tuner.py:395-396); one tcgen05 launch for the
+    production shape, otherwise two FFMA launches."""
+    lib = N.load()
+    if agent.tc:
+        with PF.span("value_tc", n0 + n1):
+            N.check(lib.harl_value_pair_tc(C.byref(agent.val_desc),
+                                           _ptr(feat0), n0, _ptr(feat1), n1,
+                                           feat0.shape[1], _ptr(out0),
+                                           _ptr(out1), _stream()),
+                    "harl_value_pair_tc")
+        return out0[:n0], out1[:n1]
+    return (value_estimate(agent, feat0, n0, out0),
+            value_estimate(agent, feat1, n1, out1))
 
 
 class DeviceReplay:

@@ -236,8 +236,8 @@ class EpisodeEngine:
             D.featurize(dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
             D.gbt_predict(forest, nxt["feat"], m, old_score=cur["score"],
                           out=nxt["score"], reward=reward)
-            D.value_estimate(self.dagent, cur["feat"], m, v_cur)
-            D.value_estimate(self.dagent, nxt["feat"], m, v_next)
+            D.value_pair(self.dagent, cur["feat"], m, nxt["feat"], m, v_cur,
+                         v_next)
             cap = self.replay.cap
             io = N.StepBuffers(
                 rt.data_ptr(), nxt["tiles"].data_ptr(),

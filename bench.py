@@ -155,58 +155,58 @@ def episode_config(P):
 
 
 class ClockSampler:
+    """SM clock + throttle reasons sampled with NVML every 5 ms while the
+    timed region runs (the recipe's nvidia-smi clocks line, at a rate that
+    sees sub-second regions)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
     def __init__(self, index: int = 0):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.stop = threading.Event()
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h,
+                                                        pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # noqa: BLE001 - no NVML: report nothing
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                clk = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((clk, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.nv is not None:
+            self.thread.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                 "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        clks = [c for c, _ in self.samples]
+        reasons = sorted({name for _, rs in self.samples
+                          for name, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median(clks)),
+                "sm_max_mhz": float(self.max), "reasons": reasons,
+                "samples": len(clks)}
 
 
 # ---------------------------------------------------------------------------
@@ -312,7 +312,9 @@ def run_gpu(args, rank, world):
     # one extra, untimed episode with per-call CUDA events: kernel shares
     profiling.reset()
     profiling.timing(True)
+    eng.use_graphs = False          # per-launch events need eager launches
     res = eng.run_episode(tb, forest, gen, ecfg, order)
+    eng.use_graphs = True
     order += res.visits
     kstats = profiling.kernel_times()
     profiling.timing(False)
@@ -355,8 +357,7 @@ def e2e_episode(eng, w, forest_unused, gen, ecfg, order, dev):
         nbytes_in += v.numel() * v.element_size()
     forest = D.DeviceForest(w["trees"], w["base"], w["lr"], device=dev)
     nbytes_in += sum(t.numel() * t.element_size() for t in (
-        forest.feature, forest.left, forest.right, forest.threshold,
-        forest.leaf_contrib, forest.tree_first))
+        forest.nodes, forest.tree_first))
     res = eng.run_episode(tb, forest, gen, ecfg, order)
     tiles, knobs = res.states()
     scores = res.scores()
@@ -407,7 +408,7 @@ def roofline_entry(kstats, tables, hidden):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))

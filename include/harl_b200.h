@@ -106,21 +106,23 @@ typedef struct harl_mlp_desc {
   int32_t n_head_cols;
 } harl_mlp_desc;
 
-/* GBT ensemble (costmodel.py:59-78,219-230).  Node arrays are concatenated
- * over trees; children are tree-local indices.  `leaf_contrib` holds
- * learning_rate * value (the reference's product, computed on the host). */
+/* GBT ensemble (costmodel.py:59-78,219-230).  Nodes of all trees are
+ * concatenated 16-byte records {double v; int16 feature, left, right, pad}
+ * where v is the split threshold of an internal node (feature >= 0) or
+ * learning_rate * value of a leaf (feature == -1; the reference's product,
+ * computed on the host); children are tree-local indices. */
 typedef struct harl_forest_desc {
   int32_t n_trees, fitted;
   double base, floor_value;
   const int32_t* tree_first;  /* [n_trees] first node of each tree */
-  const int16_t* feature;     /* -1 = leaf */
-  const int16_t* left;
-  const int16_t* right;
-  const double* threshold;
-  const double* leaf_contrib;
+  const void* nodes;          /* [n_nodes] records */
+  int64_t n_nodes;
 } harl_forest_desc;
 
 int harl_abi_version(void);
+/* One-time setup (kernel shared-memory limits, device queries) so that the
+ * step entry points can be recorded into CUDA graphs. */
+int harl_prepare(void);
 const char* harl_last_error(void);
 int harl_device_query(int device, int* sm_count_host, int* cc_major_host,
                       int* cc_minor_host);
@@ -159,8 +161,7 @@ int harl_apply_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
  * old_score != NULL also reward = (new-old)/old (tuner.py:389-391). */
 int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
                      int64_t n, int32_t feature_len, double* score,
-                     const double* old_score, double* reward, int32_t n_nodes,
-                     void* stream);
+                     const double* old_score, double* reward, void* stream);
 
 /* select_actions (rlcore.py:216-228) fused with the walker: policy MLP
  * (fp32), masked log-softmax, inverse-CDF sampling on the PCG64 stream
@@ -186,8 +187,11 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
  * the policy is the production shape (hidden (128,128), feature_len <= 64,
  * n_head0 + 9 <= 128): trunk and heads as 3xTF32 tcgen05 MMAs with TMEM
  * accumulators and TMEM-resident activations.  hid_scratch: float32
- * [n][128] device scratch.  Falls back to NOTHING: returns HARL_E_ARG if
- * the shape is not eligible (the caller then uses harl_policy_step). */
+ * [n][128] device scratch.  rng_state_dev (optional, device {lo, hi}
+ * u64 PCG64 state) overrides rng's state at execution time so the call can
+ * be replayed from a CUDA graph (rng still supplies the increment).  Not
+ * a fallback: returns HARL_E_ARG if the shape is not eligible (the caller
+ * then uses harl_policy_step). */
 int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         const double* feat, const uint16_t* tiles,
                         const uint8_t* knobs, int64_t n, int64_t ld,
@@ -196,14 +200,25 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         uint8_t* knobs_out, uint64_t* move_bits,
                         uint32_t* shift_bits, int32_t* head0_col,
                         float* logits_out, uint64_t* status,
-                        float* hid_scratch, void* stream);
+                        float* hid_scratch, const uint64_t* rng_state_dev,
+                        const void* packed_trunk, const void* packed_heads,
+                        void* stream);
 
 /* V(X) and V(X') in one launch (tuner.py:395-396) on the tcgen05 path
  * (hidden (128,128), feature_len <= 64); HARL_E_ARG if not eligible. */
 int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
                        int64_t n0, const double* feat1, int64_t n1,
                        int32_t feature_len, float* v0, float* v1,
-                       void* stream);
+                       const void* packed, void* stream);
+
+/* Pre-pack the tcgen05 weight images (tf32 hi/lo in the UMMA K-major
+ * layout + biases) after every parameter change; the tcgen05 entry points
+ * then bulk-copy them (cp.async.bulk) instead of re-splitting the weights
+ * in every CTA.  which: 0 = trunk image, 1 = heads image. */
+int64_t harl_tc_packed_bytes(int32_t which, int32_t n_head_cols);
+int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
+                         int32_t feature_len, void* pol_trunk,
+                         void* pol_heads, void* val_trunk, void* stream);
 
 /* ValueNet.estimate (rlcore.py:173) on feat (fp64 rows, fp32 math). */
 int harl_value_forward(const harl_mlp_desc* val, const double* feat,
@@ -265,12 +280,14 @@ typedef struct harl_step_buffers {
 
 /* advantage + TD target (rlcore.py:231-234, tuner.py:395-398), replay push
  * of rows >= keep_from into slots (wpos + r) % cap, entry log at visit
- * vbase + r, Track.advance.  rl == 0 skips value/advantage/replay. */
+ * vbase + r, Track.advance.  rl == 0 skips value/advantage/replay.
+ * wpos_dev (optional device int64) overrides wpos at execution time. */
 int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
                      int64_t vbase, int32_t local_slots, int32_t feature_len,
                      double discount, int32_t rl, const harl_replay_ring* ring,
                      int64_t wpos, int64_t keep_from, const harl_entry_log* log,
-                     const harl_track_stats* ts, void* stream);
+                     const harl_track_stats* ts, const int64_t* wpos_dev,
+                     void* stream);
 
 /* Survivor compaction after a host cull (stopping.py:68-86): row i of the
  * destination population <- row idx[i] of the source. */
@@ -310,7 +327,10 @@ typedef struct harl_ppo_hyper {
  * actor loss, value loss, policy loss, entropy, mean ratio.  *bad (device
  * int32, caller zeroes) != 0 when a loss or gradient was not finite, in
  * which case no parameter changed (RlDivergedError). scratch >=
- * harl_ppo_scratch_bytes(). head0_src: compact column -> source slot. */
+ * harl_ppo_scratch_bytes(). head0_src: compact column -> source slot.
+ * adam_dev (optional device double[4]: 1-b1^t, 1-b2^t for policy then
+ * value) overrides hp's bias corrections at execution time (graph
+ * replay).  No host<->device copies: legal inside stream capture. */
 int64_t harl_ppo_scratch_bytes(int32_t B, int32_t row_stride,
                                int32_t n_jobs);
 int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
@@ -320,7 +340,8 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     int32_t row_stride, double* params, double* grads,
                     double* adam_m, double* adam_v, float* params32,
                     int64_t n_pi, int64_t n_params, double* losses,
-                    int32_t* bad, void* scratch, void* stream);
+                    int32_t* bad, void* scratch, const double* adam_dev,
+                    void* stream);
 
 /* Diagnostic: one 128x128x64 kind::tf32 tcgen05 MMA (A [128][64], B
  * [64][128] row-major fp32, D [128][128]); mode 0 = A from TMEM, 1 = A

@@ -61,9 +61,8 @@ class MlpDesc(C.Structure):
 
 class ForestDesc(C.Structure):
     _fields_ = [("n_trees", i32), ("fitted", i32), ("base", f64),
-                ("floor_value", f64), ("tree_first", vp), ("feature", vp),
-                ("left", vp), ("right", vp), ("threshold", vp),
-                ("leaf_contrib", vp)]
+                ("floor_value", f64), ("tree_first", vp), ("nodes", vp),
+                ("n_nodes", i64)]
 
 
 class ReplayRing(C.Structure):
@@ -108,6 +107,7 @@ class PpoHyper(C.Structure):
 P = C.POINTER
 _SIGS = {
     "harl_abi_version": (i32, []),
+    "harl_prepare": (i32, []),
     "harl_last_error": (C.c_char_p, []),
     "harl_device_query": (i32, [i32, P(i32), P(i32), P(i32)]),
     "harl_init_population": (i32, [P(SketchDesc), P(Pcg64), i64, vp, vp, i64,
@@ -116,27 +116,29 @@ _SIGS = {
     "harl_action_masks": (i32, [P(SketchDesc), vp, vp, i64, i64, vp, vp, vp]),
     "harl_apply_actions": (i32, [P(SketchDesc), vp, vp, i64, i64, vp, vp, vp,
                                  vp, vp]),
-    "harl_gbt_predict": (i32, [P(ForestDesc), vp, i64, i32, vp, vp, vp, i32,
-                               vp]),
+    "harl_gbt_predict": (i32, [P(ForestDesc), vp, i64, i32, vp, vp, vp, vp]),
     "harl_policy_step": (i32, [P(SketchDesc), P(MlpDesc), vp, vp, vp, i64, i64,
                                P(Pcg64), vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                vp, vp]),
     "harl_value_forward": (i32, [P(MlpDesc), vp, i64, i32, vp, vp]),
     "harl_policy_step_tc": (i32, [P(SketchDesc), P(MlpDesc), vp, vp, vp, i64,
                                   i64, P(Pcg64), vp, vp, vp, vp, vp, vp, vp,
-                                  vp, vp, vp, vp, vp]),
+                                  vp, vp, vp, vp, vp, vp, vp, vp]),
     "harl_value_pair_tc": (i32, [P(MlpDesc), vp, i64, vp, i64, i32, vp, vp,
-                                 vp]),
+                                 vp, vp]),
+    "harl_tc_packed_bytes": (i64, [i32, i32]),
+    "harl_pack_tc_weights": (i32, [P(MlpDesc), P(MlpDesc), i32, vp, vp, vp,
+                                   vp]),
     "harl_finish_step": (i32, [P(StepBuffers), i64, i64, i64, i32, i32, f64,
                                i32, P(ReplayRing), i64, i64, P(EntryLog),
-                               P(TrackStats), vp]),
+                               P(TrackStats), vp, vp]),
     "harl_gather_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp,
                                vp, vp, vp, vp, i64, vp]),
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_selftest_tcgen05": (i32, [vp, vp, vp, i32, vp]),
     "harl_ppo_update": (i32, [P(NetLayout), P(NetLayout), P(PpoHyper),
                               P(ReplayRing), vp, i32, i32, i32, vp, i32, vp,
-                              vp, vp, vp, vp, i64, i64, vp, vp, vp, vp]),
+                              vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -21,14 +21,31 @@ struct FinishArgs {
   int64_t keep_from;    // rows >= keep_from survive in the ring
 };
 
-__global__ void k_finish_step(FinishArgs a, harl_step_buffers io,
-                              harl_replay_ring ring, harl_entry_log log,
-                              harl_track_stats ts) {
+__global__ void __launch_bounds__(256)
+k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
+              const __grid_constant__ harl_replay_ring ring,
+              const __grid_constant__ harl_entry_log log,
+              const __grid_constant__ harl_track_stats ts,
+              const int64_t* wpos_dev) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t wpos = wpos_dev ? *wpos_dev : a.wpos;
+  // feature rows of the surviving replay pushes: flat, coalesced copy
+  if (a.rl) {
+    const int64_t keep = a.n - a.keep_from;
+    const int64_t total = keep * a.F;
+    for (int64_t e = r; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t rr = a.keep_from + e / a.F, k = e % a.F;
+      const int64_t slot = (wpos + rr) % ring.cap;
+      ring.X[slot * a.F + k] = io.feat[rr * a.F + k];
+      ring.Xn[slot * a.F + k] = io.feat_new[rr * a.F + k];
+    }
+  }
   if (r >= a.n) return;
-  const int32_t* row_track = io.row_track;
-  const uint16_t* tiles_new = io.tiles_new;
-  const uint8_t* knobs_new = io.knobs_new;
+  const int32_t* __restrict__ row_track = io.row_track;
+  const uint16_t* __restrict__ tiles_new = io.tiles_new;
+  const uint8_t* __restrict__ knobs_new = io.knobs_new;
+  uint16_t* __restrict__ log_tiles = log.tiles;
+  uint8_t* __restrict__ log_knobs = log.knobs;
   const double* feat = io.feat;
   const double* feat_new = io.feat_new;
   const double* new_score = io.new_score;
@@ -42,9 +59,12 @@ __global__ void k_finish_step(FinishArgs a, harl_step_buffers io,
   const uint32_t* shift_bits = io.shift_bits;
   double* adv_out = io.adv;
   const int64_t v = a.vbase + r;
-  for (int s = 0; s < a.local_slots; ++s)
-    log.tiles[(int64_t)s * log.ld + v] = tiles_new[(int64_t)s * a.ld + r];
-  for (int k = 0; k < 3; ++k) log.knobs[(int64_t)k * log.ld + v] = knobs_new[(int64_t)k * a.ld + r];
+  uint16_t tv[HARL_MAX_SLOTS];
+#pragma unroll 8
+  for (int s = 0; s < a.local_slots; ++s) tv[s] = tiles_new[(int64_t)s * a.ld + r];
+#pragma unroll 8
+  for (int s = 0; s < a.local_slots; ++s) log_tiles[(int64_t)s * log.ld + v] = tv[s];
+  for (int k = 0; k < 3; ++k) log_knobs[(int64_t)k * log.ld + v] = knobs_new[(int64_t)k * a.ld + r];
   const double sc = new_score[r];
   const double rw = reward[r];
   log.score[v] = sc;
@@ -65,11 +85,9 @@ __global__ void k_finish_step(FinishArgs a, harl_step_buffers io,
   const double adv = __dsub_rn(tdv, vc);
   adv_out[r] = adv;
   if (r < a.keep_from) return;
-  const int64_t slot = (a.wpos + r) % ring.cap;
-  for (int k = 0; k < a.F; ++k) {
-    ring.X[slot * a.F + k] = feat[r * a.F + k];
-    ring.Xn[slot * a.F + k] = feat_new[r * a.F + k];
-  }
+  const int64_t slot = (wpos + r) % ring.cap;
+  (void)feat;
+  (void)feat_new;
   ring.actions[slot * 4 + 0] = head0_col[r];
   for (int h = 1; h < 4; ++h) ring.actions[slot * 4 + h] = actions[(int64_t)h * a.n + r];
   ring.scalars[slot * 4 + 0] = logp[r];

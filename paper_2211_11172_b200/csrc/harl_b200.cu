@@ -14,6 +14,7 @@
 #include "ppo_kernels.cuh"
 #include "tc_probe.cuh"
 #include "mlp_tc.cuh"
+#include "sample_kernels.cuh"
 
 namespace harl {
 
@@ -73,16 +74,32 @@ static int max_dyn_smem() {
   return v;
 }
 
+// Raise a kernel's dynamic shared-memory limit once (not per call, so the
+// entry points stay legal inside CUDA-graph stream capture).
 template <typename K>
 static int allow_smem(K kernel, size_t bytes, const char* name) {
+  static std::mutex mu;
+  static const void* keys[64];
+  static size_t have[64];
+  static int nkeys = 0;
   if ((int)bytes > max_dyn_smem()) {
     set_error("%s: needs %zu bytes of shared memory (max %d)", name, bytes,
               max_dyn_smem());
     return HARL_E_LIMIT;
   }
+  std::lock_guard<std::mutex> lock(mu);
+  int slot = -1;
+  for (int i = 0; i < nkeys; ++i)
+    if (keys[i] == (const void*)kernel) slot = i;
+  if (slot >= 0 && have[slot] >= bytes) return HARL_OK;
   cudaError_t e = cudaFuncSetAttribute(
       kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return cuda_status(e, name);
+  if (slot < 0 && nkeys < 64) slot = nkeys++;
+  if (slot >= 0) {
+    keys[slot] = (const void*)kernel;
+    have[slot] = bytes;
+  }
   return HARL_OK;
 }
 
@@ -245,22 +262,23 @@ int harl_apply_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
 
 int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
                      int64_t n, int32_t feature_len, double* score,
-                     const double* old_score, double* reward, int32_t n_nodes,
-                     void* stream) {
-  if (!forest || forest->n_trees < 0 || forest->n_trees > 1024 || n_nodes < 0) {
+                     const double* old_score, double* reward, void* stream) {
+  if (!forest || forest->n_trees < 0 || forest->n_trees > 1024 ||
+      (forest->n_trees > 0 && (!forest->nodes || !forest->tree_first))) {
     set_error("harl_gbt_predict: bad forest");
     return HARL_E_ARG;
   }
   if (n <= 0) return HARL_OK;
-  const size_t smem = sizeof(GbtNode) * (size_t)n_nodes;
+  const int T = forest->n_trees > 0 ? forest->n_trees : 1;
+  const int rows = T <= 192 ? GBT_THREADS / GBT_GROUPS : 4;
+  const size_t smem = sizeof(double) * (size_t)rows * T;
   int rc = allow_smem(k_gbt_predict, smem, "k_gbt_predict");
   if (rc) return rc;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  int64_t blocks = (n + GBT_THREADS - 1) / GBT_THREADS;
-  if (blocks > 4 * sms) blocks = 4 * sms;
-  k_gbt_predict<<<(unsigned)blocks, GBT_THREADS, smem, (cudaStream_t)stream>>>(
-      *forest, feat, n, feature_len, score, old_score, reward, n_nodes);
+  k_gbt_predict<<<(unsigned)((n + rows - 1) / rows), GBT_THREADS, smem,
+                  (cudaStream_t)stream>>>(
+      (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
+      forest->fitted, forest->base, forest->floor_value, feat, n, feature_len,
+      score, old_score, reward, rows);
   HARL_CHECK_LAUNCH("k_gbt_predict");
   return HARL_OK;
 }
@@ -308,6 +326,59 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   return HARL_OK;
 }
 
+static void build_lane_jump(const harl_pcg64& g, LaneJump* LJ) {
+  const h128 inc = ((h128)g.inc_hi << 64) | (h128)g.inc_lo;
+  h128 A = 1, C = 0;  // l steps: s -> A s + C
+  for (int l = 0; l < 32; ++l) {
+    LJ->A[l] = to_u128(A);
+    LJ->C[l] = to_u128(C);
+    C = PCG_MULT * C + inc;
+    A = PCG_MULT * A;
+  }
+}
+
+static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
+                          const uint64_t* rng_state_dev,
+                          const float* logits, int ldz, int64_t n, int64_t ld,
+                          const uint16_t* tiles, const uint8_t* knobs,
+                          const int32_t* inject, int32_t* actions, double* logp,
+                          uint16_t* tiles_out, uint8_t* knobs_out,
+                          uint64_t* move_bits, uint32_t* shift_bits,
+                          int32_t* head0_col, uint64_t* status,
+                          cudaStream_t st) {
+  PcgJump J;
+  LaneJump LJ;
+  u128 base;
+  memset(&J, 0, sizeof(J));
+  memset(&LJ, 0, sizeof(LJ));
+  memset(&base, 0, sizeof(base));
+  if (rng) {
+    build_jump(*rng, &J);
+    build_lane_jump(*rng, &LJ);
+    base = state_of(*rng);
+  }
+  SampleArgs a;
+  a.logits = logits;
+  a.ldz = ldz;
+  a.n = n;
+  a.ld = ld;
+  a.inject = inject;
+  a.actions = actions;
+  a.logp = logp;
+  a.tiles_out = tiles_out;
+  a.knobs_out = knobs_out;
+  a.move_bits = move_bits;
+  a.shift_bits = shift_bits;
+  a.head0_col = head0_col;
+  a.status = (unsigned long long*)status;
+  k_sample_rows<<<(unsigned)((n + SAMPLE_THREADS - 1) / SAMPLE_THREADS),
+                  SAMPLE_THREADS, 0, st>>>(*sk, J, LJ, base,
+                                           (const u128*)rng_state_dev, tiles,
+                                           knobs, a);
+  HARL_CHECK_LAUNCH("k_sample_rows");
+  return HARL_OK;
+}
+
 static bool tc_trunk_ok(const harl_mlp_desc* m, int F) {
   return m && m->n_layers >= 2 && m->dims[0] == F && F <= TC_K1 &&
          m->dims[1] == TC_H && m->dims[2] == TC_H;
@@ -331,7 +402,9 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         uint8_t* knobs_out, uint64_t* move_bits,
                         uint32_t* shift_bits, int32_t* head0_col,
                         float* logits_out, uint64_t* status,
-                        float* hid_scratch, void* stream) {
+                        float* hid_scratch, const uint64_t* rng_state_dev,
+                        const void* packed_trunk, const void* packed_heads,
+                        void* stream) {
   int rc = check_sketch(sk);
   if (rc) return rc;
   if ((rc = check_mlp(pol, true))) return rc;
@@ -359,6 +432,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   ta.b1 = pol->b[0];
   ta.W2 = pol->W[1];
   ta.b2 = pol->b[1];
+  ta.packed = packed_trunk;
   const int64_t tiles_n = (n + 127) / 128;
   const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
   k_trunk_tc<TRUNK_POLICY><<<grid, 128, TRUNK_SMEM, st>>>(ta);
@@ -367,31 +441,26 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   ha.hid = hid_scratch;
   ha.Wh = pol->head_W;
   ha.bh = pol->head_b;
+  ha.logits_out = logits_out;
+  ha.packed = packed_heads;
+  ha.n = n;
   ha.NH = pol->n_head_cols;
   ha.NHP = (ha.NH + 15) / 16 * 16;
-  const size_t smem = (size_t)2 * ha.NHP * TC_H * 4 + HEADS_NMAX * 4 +
-                      (size_t)128 * (ha.NHP + 1) * 4;
-  if ((rc = allow_smem(k_heads_tc<0>, smem, "k_heads_tc"))) return rc;
-  PcgJump J;
-  StepRng sr;
-  memset(&J, 0, sizeof(J));
-  memset(&sr, 0, sizeof(sr));
-  if (rng) {
-    build_jump(*rng, &J);
-    sr.s = state_of(*rng);
-  }
-  k_heads_tc<0><<<grid, HEADS_THREADS, smem, st>>>(
-      ha, *sk, J, sr, tiles, knobs, n, ld, inject, actions, logp, tiles_out,
-      knobs_out, move_bits, shift_bits, head0_col, logits_out,
-      (unsigned long long*)status);
+  const size_t smem = (size_t)2 * ha.NHP * TC_H * 4 + HEADS_NMAX * 4;
+  if ((rc = allow_smem(k_heads_tc, smem, "k_heads_tc"))) return rc;
+  k_heads_tc<<<grid, 128, smem, st>>>(ha);
   HARL_CHECK_LAUNCH("k_heads_tc");
-  return HARL_OK;
+  return launch_sampler(sk, rng, rng_state_dev, hid_scratch, TC_H, n, ld,
+                        tiles, knobs, inject,
+                        actions, logp, tiles_out, knobs_out, move_bits,
+                        shift_bits, head0_col, status, st);
 }
+
 
 int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
                        int64_t n0, const double* feat1, int64_t n1,
                        int32_t feature_len, float* v0, float* v1,
-                       void* stream) {
+                       const void* packed, void* stream) {
   int rc = check_mlp(val, false);
   if (rc) return rc;
   if (val->n_layers != 3 || !tc_trunk_ok(val, feature_len) ||
@@ -417,10 +486,80 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
   ta.b2 = val->b[1];
   ta.w3 = val->W[2];
   ta.b3 = val->b[2];
+  ta.packed = packed;
   const int64_t tiles_n = (n0 + 127) / 128 + (ta.n1 + 127) / 128;
   const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
   k_trunk_tc<TRUNK_VALUE><<<grid, 128, TRUNK_SMEM, (cudaStream_t)stream>>>(ta);
   HARL_CHECK_LAUNCH("k_trunk_tc<value>");
+  return HARL_OK;
+}
+
+int harl_prepare(void) {
+  // raise every kernel's dynamic shared-memory limit up front so that no
+  // entry point needs cudaFuncSetAttribute while a stream is being captured
+  const size_t mx = (size_t)max_dyn_smem();
+  int rc = 0;
+  if ((rc = allow_smem(k_featurize, mx, "k_featurize"))) return rc;
+  if ((rc = allow_smem(k_gbt_predict, mx, "k_gbt_predict"))) return rc;
+  if ((rc = allow_smem(k_policy_step, mx, "k_policy_step"))) return rc;
+  if ((rc = allow_smem(k_value_forward, mx, "k_value_forward"))) return rc;
+  if ((rc = allow_smem(k_trunk_tc<TRUNK_POLICY>, mx, "k_trunk_tc"))) return rc;
+  if ((rc = allow_smem(k_trunk_tc<TRUNK_VALUE>, mx, "k_trunk_tc"))) return rc;
+  if ((rc = allow_smem(k_heads_tc, mx, "k_heads_tc"))) return rc;
+  if ((rc = allow_smem(k_ppo_rows, mx, "k_ppo_rows"))) return rc;
+  (void)sm_count();
+  return HARL_OK;
+}
+
+int64_t harl_tc_packed_bytes(int32_t which, int32_t n_head_cols) {
+  if (which == 0) return TRUNK_IMAGE;
+  return heads_image_bytes((n_head_cols + 15) / 16 * 16);
+}
+
+int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
+                         int32_t feature_len, void* pol_trunk,
+                         void* pol_heads, void* val_trunk, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (pol && pol_trunk) {
+    if (!tc_trunk_ok(pol, feature_len) || pol->n_head_cols > HEADS_NMAX) {
+      set_error("harl_pack_tc_weights: policy not eligible");
+      return HARL_E_ARG;
+    }
+    TrunkArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    ta.F = feature_len;
+    ta.W1 = pol->W[0];
+    ta.b1 = pol->b[0];
+    ta.W2 = pol->W[1];
+    ta.b2 = pol->b[1];
+    k_pack_trunk<<<64, 256, 0, st>>>(ta, (uint8_t*)pol_trunk, 0);
+    HARL_CHECK_LAUNCH("k_pack_trunk<policy>");
+    HeadsArgs ha;
+    memset(&ha, 0, sizeof(ha));
+    ha.Wh = pol->head_W;
+    ha.bh = pol->head_b;
+    ha.NH = pol->n_head_cols;
+    ha.NHP = (ha.NH + 15) / 16 * 16;
+    k_pack_heads<<<64, 256, 0, st>>>(ha, (uint8_t*)pol_heads);
+    HARL_CHECK_LAUNCH("k_pack_heads");
+  }
+  if (val && val_trunk) {
+    if (!tc_trunk_ok(val, feature_len)) {
+      set_error("harl_pack_tc_weights: value net not eligible");
+      return HARL_E_ARG;
+    }
+    TrunkArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    ta.F = feature_len;
+    ta.W1 = val->W[0];
+    ta.b1 = val->b[0];
+    ta.W2 = val->W[1];
+    ta.b2 = val->b[1];
+    ta.w3 = val->W[2];
+    ta.b3 = val->b[2];
+    k_pack_trunk<<<64, 256, 0, st>>>(ta, (uint8_t*)val_trunk, 1);
+    HARL_CHECK_LAUNCH("k_pack_trunk<value>");
+  }
   return HARL_OK;
 }
 
@@ -449,7 +588,8 @@ int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
                      int64_t vbase, int32_t local_slots, int32_t feature_len,
                      double discount, int32_t rl, const harl_replay_ring* ring,
                      int64_t wpos, int64_t keep_from, const harl_entry_log* log,
-                     const harl_track_stats* ts, void* stream) {
+                     const harl_track_stats* ts, const int64_t* wpos_dev,
+                     void* stream) {
   if (!io || !log || !ts || (rl && (!ring || ring->cap < 1))) {
     set_error("harl_finish_step: bad arguments");
     return HARL_E_ARG;
@@ -470,8 +610,8 @@ int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
   memset(&rg, 0, sizeof(rg));
   if (ring) rg = *ring;
   if (rg.cap < 1) rg.cap = 1;
-  k_finish_step<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      a, *io, rg, *log, *ts);
+  k_finish_step<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      a, *io, rg, *log, *ts, wpos_dev);
   HARL_CHECK_LAUNCH("k_finish_step");
   return HARL_OK;
 }
@@ -549,7 +689,8 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     int32_t row_stride, double* params, double* grads,
                     double* adam_m, double* adam_v, float* params32,
                     int64_t n_pi, int64_t n_params, double* losses,
-                    int32_t* bad, void* scratch, void* stream) {
+                    int32_t* bad, void* scratch, const double* adam_dev,
+                    void* stream) {
   if (!pol || !val || !hp || !ring || !idx || B < 1 || n_head0 < 1 ||
       n_head0 > HARL_MAX_HEAD0 || pol->n_layers < 1 ||
       pol->n_layers > HARL_MAX_LAYERS || val->n_layers < 2 ||
@@ -565,9 +706,9 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   GradJob jobs[4 * (HARL_MAX_LAYERS + 2)];
   int n_jobs = 0, n_tiles = 0;
   build_grad_jobs(*pol, *val, jobs, &n_jobs, &n_tiles);
-  cudaError_t e = cudaMemcpyAsync(djobs, jobs, sizeof(GradJob) * n_jobs,
-                                  cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_status(e, "ppo jobs memcpy");
+  // the job table is passed by value (no host->device copy: the call is
+  // legal inside CUDA-graph capture)
+  (void)djobs;
   PpoArgs a;
   memset(&a, 0, sizeof(a));
   a.B = B;
@@ -579,20 +720,33 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   a.w_ent = hp->entropy_weight;
   a.w_val = hp->value_loss_weight;
   for (int j = 0; j < n_head0; ++j) a.head0_src[j] = head0_src_host[j];
-  k_ppo_rows<<<(unsigned)((B + PPO_TM - 1) / PPO_TM), PPO_THREADS, 0, st>>>(
+  int wmax = 0;
+  for (int l = 0; l <= pol->n_layers; ++l) wmax = wmax > pol->dims[l] ? wmax : pol->dims[l];
+  for (int l = 0; l <= val->n_layers; ++l) wmax = wmax > val->dims[l] ? wmax : val->dims[l];
+  wmax = wmax > pol->n_head_cols ? wmax : pol->n_head_cols;
+  const size_t rsmem = sizeof(double) * (PPO_TM * (size_t)row_stride + 8);
+  (void)wmax;
+  int rc2 = allow_smem(k_ppo_rows, rsmem, "k_ppo_rows");
+  if (rc2) return rc2;
+  k_ppo_rows<<<(unsigned)((B + PPO_TM - 1) / PPO_TM), PPO_THREADS, rsmem, st>>>(
       a, *pol, *val, *ring, idx, params, rows, rowout);
   HARL_CHECK_LAUNCH("k_ppo_rows");
   k_ppo_losses<<<1, 32, 0, st>>>(B, hp->entropy_weight, hp->value_loss_weight,
                                  rowout, losses, bad);
   HARL_CHECK_LAUNCH("k_ppo_losses");
-  k_ppo_wgrad<<<(unsigned)n_tiles, 256, 0, st>>>(djobs, n_jobs, B, row_stride,
-                                                 rows, grads, bad);
+  GradJobs jt;
+  memset(&jt, 0, sizeof(jt));
+  for (int j = 0; j < n_jobs; ++j) jt.j[j] = jobs[j];
+  jt.n = n_jobs;
+  k_ppo_wgrad<<<(unsigned)n_tiles, 256, 0, st>>>(jt, B, row_stride, rows, grads,
+                                                 bad);
   HARL_CHECK_LAUNCH("k_ppo_wgrad");
   AdamArgs ad;
   ad.n_pi = n_pi;
   ad.n = n_params;
   ad.h = *hp;
-  k_ppo_adam<<<296, 256, 0, st>>>(ad, bad, grads, params, adam_m, adam_v, params32);
+  k_ppo_adam<<<296, 256, 0, st>>>(ad, adam_dev, bad, grads, params, adam_m,
+                                   adam_v, params32);
   HARL_CHECK_LAUNCH("k_ppo_adam");
   return HARL_OK;
 }

@@ -103,46 +103,151 @@ __device__ inline double warp_sum(double v) {
   return v;
 }
 
+constexpr int SAMPLE_MAXCH = 16;  // head-0 columns up to 512
+
 // Masked log-softmax + inverse-CDF sample over `C` columns of one row,
-// computed by one warp.  legal(j) supplied as a predicate functor.
-// Returns the chosen column (walk-back semantics of rlcore.py:206-212) and
-// its log-probability; *all_masked set when no column is legal.
-template <typename Legal>
-__device__ inline int warp_sample(const float* z, int C, Legal legal, double u,
-                                  double* logp_out, bool* all_masked) {
+// computed by one warp (rlcore.py:185-213).  Lane l owns columns
+// l + 32 i; bit i of `lb` says whether that column is legal.  Returns the
+// chosen column (with the reference's walk-back over zero-probability
+// cells) and its log-probability; -1 when the walk ends on an illegal
+// column 0 (the reference then picks full index 0).
+__device__ inline int warp_sample_bits(const float* z, int C, uint32_t lb,
+                                       double u, double* logp_out,
+                                       bool* all_masked) {
   const int lane = threadIdx.x & 31;
+  const int nch = (C + 31) >> 5;
   double zmax = -INFINITY;
-  for (int j = lane; j < C; j += 32)
-    if (legal(j)) zmax = fmax(zmax, (double)z[j]);
+#pragma unroll
+  for (int i = 0; i < SAMPLE_MAXCH; ++i)
+    if (i < nch && ((lb >> i) & 1u)) zmax = fmax(zmax, (double)z[lane + 32 * i]);
   zmax = warp_max(zmax);
   *all_masked = (zmax == -INFINITY);
+  double e[SAMPLE_MAXCH];
   double s = 0.0;
-  for (int j = lane; j < C; j += 32)
-    if (legal(j)) s += exp((double)z[j] - zmax);
+#pragma unroll
+  for (int i = 0; i < SAMPLE_MAXCH; ++i) {
+    e[i] = (i < nch && ((lb >> i) & 1u)) ? exp((double)z[lane + 32 * i] - zmax) : 0.0;
+    s += e[i];
+  }
   s = warp_sum(s);
   const double logs = log(s);
-  // inclusive prefix sum in column order, chunk by chunk; count c < u
+  // inclusive prefix sum of p = e/s in column order; count c < u
   int count = 0;
   double carry = 0.0;
-  for (int base = 0; base < C; base += 32) {
-    const int j = base + lane;
-    double p = (j < C && legal(j)) ? exp((double)z[j] - zmax) / s : 0.0;
-    double c = p;
+#pragma unroll
+  for (int i = 0; i < SAMPLE_MAXCH; ++i) {
+    if (i >= nch) break;
+    double c = e[i] / s;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double t = __shfl_up_sync(0xffffffffu, c, o);
       if (lane >= o) c += t;
     }
     c += carry;
-    if (j < C && c < u) ++count;
+    if (lane + 32 * i < C && c < u) ++count;
     carry = __shfl_sync(0xffffffffu, c, 31);
   }
+#pragma unroll
   for (int o = 16; o; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
   int idx = min(count, C - 1);
-  // float-edge landing on a zero-probability cell: walk back
-  while (idx > 0 && !legal(idx)) --idx;
-  const bool ok = legal(idx);
+  auto legal_at = [&](int j) -> bool {
+    return (__shfl_sync(0xffffffffu, lb, j & 31) >> (j >> 5)) & 1u;
+  };
+  while (idx > 0 && !legal_at(idx)) --idx;
+  const bool ok = legal_at(idx);
   *logp_out = ok ? ((double)z[idx] - zmax - logs) : -INFINITY;
-  return ok ? idx : -1;  // -1: reference would land on full index 0
+  return ok ? idx : -1;
+}
+
+// The same for a 3-column shift head, computed redundantly by every lane
+// with the reference's sequential cumsum.
+__device__ inline int sample3(const float* z, uint32_t m3, double u,
+                              double* logp_out, bool* all_masked) {
+  double zmax = -INFINITY;
+  for (int j = 0; j < 3; ++j)
+    if ((m3 >> j) & 1u) zmax = fmax(zmax, (double)z[j]);
+  *all_masked = (zmax == -INFINITY);
+  double e[3], s = 0.0;
+  for (int j = 0; j < 3; ++j) {
+    e[j] = ((m3 >> j) & 1u) ? exp((double)z[j] - zmax) : 0.0;
+    s += e[j];
+  }
+  int count = 0;
+  double c = 0.0;
+  for (int j = 0; j < 3; ++j) {
+    c += e[j] / s;
+    if (c < u) ++count;
+  }
+  int idx = min(count, 2);
+  while (idx > 0 && !((m3 >> idx) & 1u)) --idx;
+  const bool ok = (m3 >> idx) & 1u;
+  *logp_out = ok ? ((double)z[idx] - zmax - log(s)) : -INFINITY;
+  return ok ? idx : -1;
+}
+
+__device__ inline double logp3(const float* z, uint32_t m3, int a) {
+  if (a < 0 || a > 2 || !((m3 >> a) & 1u)) return -INFINITY;
+  double zmax = -INFINITY, s = 0.0;
+  for (int j = 0; j < 3; ++j)
+    if ((m3 >> j) & 1u) zmax = fmax(zmax, (double)z[j]);
+  for (int j = 0; j < 3; ++j)
+    if ((m3 >> j) & 1u) s += exp((double)z[j] - zmax);
+  return (double)z[a] - zmax - log(s);
+}
+
+// decode + apply for one row by a whole warp (schedspace.py:196-210,
+// 265-301): lane l writes slots l and l+32 of the new state; the checks
+// follow the reference's order and are warp-uniform.
+__device__ inline int apply_row_warp(const harl_sketch_desc& sk, int tv0,
+                                     int tv1, int ca0, int par0, int ur0,
+                                     const int* act, uint16_t* __restrict__ tiles_out,
+                                     uint8_t* __restrict__ knobs_out, int64_t ld,
+                                     int64_t r) {
+  const int lane = threadIdx.x & 31;
+  const int S = sk.num_slots, L = sk.levels;
+  int src = -1, dst = -1;
+  if (act[0] != S * S) {
+    src = act[0] / S;
+    dst = act[0] % S;
+  }
+  int code = HARL_ST_OK;
+  int f_src = 0, f_dst = 0, p = 1;
+  if (src >= 0) {
+    if (src >= sk.local_slots || dst >= sk.local_slots || dst < 0 ||
+        src / L != dst / L || src == dst) {
+      code = HARL_ST_TILING;
+    } else {
+      f_src = __shfl_sync(0xffffffffu, src < 32 ? tv0 : tv1, src & 31);
+      f_dst = __shfl_sync(0xffffffffu, dst < 32 ? tv0 : tv1, dst & 31);
+      if (f_src <= 1) code = HARL_ST_TILING;
+      else p = sk.spf_lut[f_src];
+    }
+  }
+  if (code == HARL_ST_OK) {
+    const int ca = ca0 + (act[1] - 1);
+    const int par = par0 + (act[2] - 1);
+    const int ur = ur0 + (act[3] - 1);
+    if (ca < 0 || ca >= sk.ncas) code = HARL_ST_COMPUTE_AT;
+    else if (par < 0 || par > sk.max_fusible) code = HARL_ST_PARALLEL;
+    else if (ur < 0 || ur >= sk.n_unroll) code = HARL_ST_UNROLL;
+    if (code == HARL_ST_OK && lane == 0) {
+      knobs_out[r] = (uint8_t)ca;
+      knobs_out[ld + r] = (uint8_t)par;
+      knobs_out[2 * ld + r] = (uint8_t)ur;
+    }
+  }
+  const bool moved = code == HARL_ST_OK && src >= 0;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int s = lane + 32 * half;
+    if (s < sk.local_slots) {
+      int v = half ? tv1 : tv0;
+      if (moved && s == src) v = f_src / p;
+      if (moved && s == dst) v = f_dst * p;
+      tiles_out[(int64_t)s * ld + r] = (uint16_t)v;
+    }
+  }
+  return code;
 }
 
 // Sampling epilogue for one row, executed by one warp: masked
@@ -155,65 +260,69 @@ __device__ inline void policy_row(
     int64_t n, int64_t ld, int64_t r, const int32_t* inject, int32_t* actions,
     double* logp, uint16_t* tiles_out, uint8_t* knobs_out, uint64_t* move_bits,
     uint32_t* shift_bits, int32_t* head0_col, float* logits_out,
-    unsigned long long* status) {
+    unsigned long long* status, const int16_t* src_tab,
+    const int16_t* dst_tab) {
   const int lane = threadIdx.x & 31;
   const int C0 = sk.n_head0;
   const int S = sk.num_slots;
   {
     if (logits_out)
       for (int j = lane; j < NH; j += 32) logits_out[r * NH + j] = z[j];
-    // movable slots of the current state
-    uint64_t mv = 0;
-    for (int s0 = 0; s0 < sk.local_slots; s0 += 32) {
-      const int s = s0 + lane;
-      const bool m = (s < sk.local_slots) && tiles[(int64_t)s * ld + r] > 1;
-      mv |= (uint64_t)__ballot_sync(0xffffffffu, m) << s0;
-    }
+    // this lane's tile factors (slots lane, lane+32) and the movable mask
+    const int tv0 = lane < sk.local_slots ? tiles[(int64_t)lane * ld + r] : 0;
+    const int tv1 = lane + 32 < sk.local_slots ? tiles[(int64_t)(lane + 32) * ld + r] : 0;
+    const uint64_t mv = (uint64_t)__ballot_sync(0xffffffffu, tv0 > 1) |
+                        ((uint64_t)__ballot_sync(0xffffffffu, tv1 > 1) << 32);
     const int ca = knobs[r], par = knobs[ld + r], ur = knobs[2 * ld + r];
     const uint32_t sb = shift_bits_of(sk, ca, par, ur);
     int act[4];
     int col0 = 0;
     double lp_total = 0.0;
     bool dead = false;
-    // head 0: compact tiling columns (no-op last)
+    // head 0: compact tiling columns (no-op last); legal bits of my columns
+    uint32_t lb = 0;
+    for (int i = 0; (lane + 32 * i) < C0; ++i) {
+      const int j = lane + 32 * i;
+      const int src = src_tab[j];
+      if (j == C0 - 1 || (src < sk.local_slots && ((mv >> src) & 1ull)))
+        lb |= 1u << i;
+    }
     {
-      auto legal = [&](int j) -> bool {
-        if (j == C0 - 1) return true;
-        const int src = sk.head0_src[j];
-        return src < sk.local_slots && ((mv >> src) & 1ull);
-      };
       double lp;
       bool none;
       double u = 0.0;
       if (!inject) u = u64_to_unit(pcg_draw64(J, rng.s, (uint64_t)r + 1));
-      int j = warp_sample(z, C0, legal, u, &lp, &none);
+      const int j = warp_sample_bits(z, C0, lb, u, &lp, &none);
       dead |= none;
       if (inject) {
         const int a = inject[r];
-        // full index -> compact column (if legal-superset)
+        // full index -> compact column (if in the legal superset)
         int jj = -1;
         for (int c = lane; c < C0; c += 32) {
-          const int full = (c == C0 - 1) ? S * S : sk.head0_src[c] * S + sk.head0_dst[c];
+          const int full = (c == C0 - 1) ? S * S : src_tab[c] * S + dst_tab[c];
           if (full == a) jj = c;
         }
+#pragma unroll
         for (int o = 16; o; o >>= 1) jj = max(jj, __shfl_xor_sync(0xffffffffu, jj, o));
         act[0] = a;
         col0 = jj < 0 ? 0 : jj;
-        if (jj >= 0 && legal(jj)) {
-          // recompute log-prob of the injected column
+        const bool ok = jj >= 0 &&
+            ((__shfl_sync(0xffffffffu, lb, jj & 31) >> (jj >> 5)) & 1u);
+        if (ok) {
+          // log-prob of the injected column under the same softmax
           double zm = -INFINITY, ss = 0.0;
-          for (int c = lane; c < C0; c += 32)
-            if (legal(c)) zm = fmax(zm, (double)z[c]);
+          for (int i = 0; (lane + 32 * i) < C0; ++i)
+            if ((lb >> i) & 1u) zm = fmax(zm, (double)z[lane + 32 * i]);
           zm = warp_max(zm);
-          for (int c = lane; c < C0; c += 32)
-            if (legal(c)) ss += exp((double)z[c] - zm);
+          for (int i = 0; (lane + 32 * i) < C0; ++i)
+            if ((lb >> i) & 1u) ss += exp((double)z[lane + 32 * i] - zm);
           ss = warp_sum(ss);
           lp = (double)z[jj] - zm - log(ss);
         } else {
           lp = -INFINITY;
         }
       } else {
-        act[0] = (j < 0) ? 0 : ((j == C0 - 1) ? S * S : sk.head0_src[j] * S + sk.head0_dst[j]);
+        act[0] = (j < 0) ? 0 : ((j == C0 - 1) ? S * S : src_tab[j] * S + dst_tab[j]);
         col0 = j < 0 ? 0 : j;
       }
       lp_total += lp;
@@ -221,41 +330,31 @@ __device__ inline void policy_row(
     // shift heads: 3 columns each at offsets C0, C0+3, C0+6
     for (int h = 1; h < 4; ++h) {
       const uint32_t m3 = (sb >> (3 * (h - 1))) & 7u;
-      auto legal = [&](int j) -> bool { return (m3 >> j) & 1u; };
       const float* zh = z + C0 + 3 * (h - 1);
       double lp;
       bool none;
-      double u = 0.0;
-      if (!inject) u = u64_to_unit(pcg_draw64(J, rng.s, (uint64_t)h * n + r + 1));
-      int j = warp_sample(zh, 3, legal, u, &lp, &none);
-      dead |= none;
       if (inject) {
         const int a = inject[h * n + r];
         act[h] = a;
-        if (a >= 0 && a < 3 && legal(a)) {
-          double zm = -INFINITY, ss = 0.0;
-          for (int c = 0; c < 3; ++c)
-            if (legal(c)) zm = fmax(zm, (double)zh[c]);
-          for (int c = 0; c < 3; ++c)
-            if (legal(c)) ss += exp((double)zh[c] - zm);
-          lp = (double)zh[a] - zm - log(ss);
-        } else {
-          lp = -INFINITY;
-        }
+        lp = logp3(zh, m3, a);
+        none = m3 == 0;
       } else {
+        const double u = u64_to_unit(pcg_draw64(J, rng.s, (uint64_t)h * n + r + 1));
+        const int j = sample3(zh, m3, u, &lp, &none);
         act[h] = (j < 0) ? 0 : j;
       }
+      dead |= none;
       lp_total += lp;
     }
+    const int code = dead ? HARL_ST_NO_VALID
+                          : apply_row_warp(sk, tv0, tv1, ca, par, ur, act,
+                                           tiles_out, knobs_out, ld, r);
     if (lane == 0) {
       for (int h = 0; h < 4; ++h) actions[h * n + r] = act[h];
       logp[r] = lp_total;
       move_bits[r] = mv;
       shift_bits[r] = sb;
       head0_col[r] = col0;
-      int code = dead ? HARL_ST_NO_VALID
-                      : apply_row(sk, tiles, knobs, ld, r, act[0], act[1], act[2],
-                                  act[3], tiles_out, knobs_out, ld, r);
       report_status(status, r, code);
     }
     __syncwarp();
@@ -285,13 +384,19 @@ k_policy_step(const __grid_constant__ harl_sketch_desc sk,
   dense_tile(hid, ldbuf, width, net.head_W, net.head_b, NH, logits, ldbuf, false);
   __syncthreads();
 
+  __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
+  for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
+    s_src[i] = sk.head0_src[i];
+    s_dst[i] = sk.head0_dst[i];
+  }
+  __syncthreads();
   const int warp = threadIdx.x >> 5;
   for (int rr = warp; rr < MLP_TM; rr += MLP_THREADS / 32) {
     const int64_t r = r0 + rr;
     if (r >= n) break;
     policy_row(sk, J, rng, logits + rr * ldbuf, NH, tiles, knobs, n, ld, r,
                inject, actions, logp, tiles_out, knobs_out, move_bits,
-               shift_bits, head0_col, logits_out, status);
+               shift_bits, head0_col, logits_out, status, s_src, s_dst);
   }
 }
 

@@ -18,8 +18,7 @@
 //                epilogue; POLICY mode writes the trunk output (rlcore.py:
 //                136-139) for the heads kernel.
 // k_heads_tc   : the four linear heads (compact tiling head, rlcore.py:
-//                140-146) + the warp-per-row sampling/walker epilogue shared
-//                with the FFMA kernel (policy_row).
+//                140-146); sampling + walker follow in k_sample_rows.
 #pragma once
 
 #include "mlp_ffma.cuh"
@@ -91,10 +90,46 @@ struct TrunkArgs {
   const float* b2;
   const float* w3;      // [128] (VALUE)
   const float* b3;      // [1]
+  const void* packed;   // optional pre-packed smem image (k_pack_trunk)
 };
 
 constexpr int TRUNK_SMEM = 2 * (TC_K1 * TC_H * 4) + 2 * (TC_H * TC_H * 4) +
                            3 * TC_H * 4 + 16;
+constexpr int TRUNK_IMAGE = (TRUNK_SMEM + 15) / 16 * 16;
+
+// The shared-memory image of the trunk weights (W1/W2 hi+lo in the
+// K-major core layout, b1, b2, w3) built once per parameter update; the
+// persistent kernels then pull it in with a few bulk copies instead of
+// re-splitting ~25 K weights per CTA per launch.
+__global__ void k_pack_trunk(TrunkArgs a, uint8_t* img, int value_mode) {
+  uint8_t* w1h = img;
+  uint8_t* w1l = w1h + TC_K1 * TC_H * 4;
+  uint8_t* w2h = w1l + TC_K1 * TC_H * 4;
+  uint8_t* w2l = w2h + TC_H * TC_H * 4;
+  float* b = (float*)(w2l + TC_H * TC_H * 4);
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nth = gridDim.x * blockDim.x;
+  for (int i = tid; i < TC_K1 * TC_H; i += nth) {
+    const int k = i / TC_H, nn = i % TC_H;
+    const float w = k < a.F ? a.W1[k * TC_H + nn] : 0.f;
+    float h, l;
+    tc::split_tf32(w, h, l);
+    *(float*)(w1h + tc::kmajor_off(nn, k, TC_K1)) = h;
+    *(float*)(w1l + tc::kmajor_off(nn, k, TC_K1)) = l;
+  }
+  for (int i = tid; i < TC_H * TC_H; i += nth) {
+    const int k = i / TC_H, nn = i % TC_H;
+    float h, l;
+    tc::split_tf32(a.W2[k * TC_H + nn], h, l);
+    *(float*)(w2h + tc::kmajor_off(nn, k, TC_H)) = h;
+    *(float*)(w2l + tc::kmajor_off(nn, k, TC_H)) = l;
+  }
+  for (int i = tid; i < TC_H; i += nth) {
+    b[i] = a.b1[i];
+    b[TC_H + i] = a.b2[i];
+    b[2 * TC_H + i] = value_mode ? a.w3[i] : 0.f;
+  }
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) k_trunk_tc(TrunkArgs a) {
@@ -106,20 +141,29 @@ __global__ void __launch_bounds__(128, 1) k_trunk_tc(TrunkArgs a) {
   float* sb1 = (float*)(w2l + TC_H * TC_H * 4);
   float* sb2 = sb1 + TC_H;
   float* sw3 = sb2 + TC_H;
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, wbar;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) tc::tmem_alloc(&tbase, 512);
-  if (tid == 0) tc::mbar_init(&bar, 1);
-  stage_weights(a.W1, a.F, TC_H, TC_K1, TC_H, w1h, w1l);
-  stage_weights(a.W2, TC_H, TC_H, TC_H, TC_H, w2h, w2l);
-  for (int i = tid; i < TC_H; i += blockDim.x) {
-    sb1[i] = a.b1[i];
-    sb2[i] = a.b2[i];
-    sw3[i] = MODE == TRUNK_VALUE ? a.w3[i] : 0.f;
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&wbar, 1);
+  }
+  __syncthreads();
+  if (a.packed) {
+    if (tid == 0) tc::bulk_load(sm, a.packed, TRUNK_IMAGE - 16, &wbar);
+    tc::mbar_wait(&wbar, 0);
+  } else {
+    stage_weights(a.W1, a.F, TC_H, TC_K1, TC_H, w1h, w1l);
+    stage_weights(a.W2, TC_H, TC_H, TC_H, TC_H, w2h, w2l);
+    for (int i = tid; i < TC_H; i += blockDim.x) {
+      sb1[i] = a.b1[i];
+      sb2[i] = a.b2[i];
+      sw3[i] = MODE == TRUNK_VALUE ? a.w3[i] : 0.f;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   const float b3 = MODE == TRUNK_VALUE ? a.b3[0] : 0.f;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_sync();
   const uint32_t tm = tbase;
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
@@ -203,102 +247,121 @@ __global__ void __launch_bounds__(128, 1) k_trunk_tc(TrunkArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// heads + sampling epilogue
+// heads: logits = hid . Wh + bh for a 128-row tile, written IN PLACE over
+// the tile's trunk rows (row stride 128) for the sampling kernel, and
+// optionally to logits_out [n][NH].
 
-constexpr int HEADS_THREADS = 512;
 constexpr int HEADS_NMAX = 128;   // padded head columns handled here
 
 struct HeadsArgs {
-  const float* hid;   // [n][128] trunk output
+  float* hid;         // [n][128] trunk output in, logits out (in place)
   const float* Wh;    // [128][NH]
   const float* bh;    // [NH]
+  float* logits_out;  // optional [n][NH]
+  int64_t n;
   int32_t NH, NHP;    // real / padded (multiple of 16) head columns
+  const void* packed; // optional pre-packed smem image (k_pack_heads)
 };
 
-template <int dummy = 0>
-__global__ void __launch_bounds__(HEADS_THREADS, 1)
-k_heads_tc(HeadsArgs h, const __grid_constant__ harl_sketch_desc sk,
-           const __grid_constant__ PcgJump J, StepRng rng,
-           const uint16_t* tiles, const uint8_t* knobs, int64_t n, int64_t ld,
-           const int32_t* inject, int32_t* actions, double* logp,
-           uint16_t* tiles_out, uint8_t* knobs_out, uint64_t* move_bits,
-           uint32_t* shift_bits, int32_t* head0_col, float* logits_out,
-           unsigned long long* status) {
+__host__ __device__ inline int heads_image_bytes(int NHP) {
+  return 2 * NHP * TC_H * 4 + HEADS_NMAX * 4;
+}
+
+__global__ void k_pack_heads(HeadsArgs h, uint8_t* img) {
+  const int NHP = h.NHP;
+  uint8_t* whh = img;
+  uint8_t* whl = whh + NHP * TC_H * 4;
+  float* b = (float*)(whl + NHP * TC_H * 4);
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nth = gridDim.x * blockDim.x;
+  for (int i = tid; i < TC_H * NHP; i += nth) {
+    const int k = i / NHP, nn = i % NHP;
+    const float w = nn < h.NH ? h.Wh[k * h.NH + nn] : 0.f;
+    float hi, lo;
+    tc::split_tf32(w, hi, lo);
+    *(float*)(whh + tc::kmajor_off(nn, k, TC_H)) = hi;
+    *(float*)(whl + tc::kmajor_off(nn, k, TC_H)) = lo;
+  }
+  for (int i = tid; i < HEADS_NMAX; i += nth) b[i] = i < h.NH ? h.bh[i] : 0.f;
+}
+
+__global__ void __launch_bounds__(128, 1) k_heads_tc(HeadsArgs h) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const int NHP = h.NHP;
   uint8_t* whh = sm;
   uint8_t* whl = whh + NHP * TC_H * 4;
   float* sbh = (float*)(whl + NHP * TC_H * 4);
-  float* slog = sbh + HEADS_NMAX;          // [128][NHP + 1]
-  const int LDL = NHP + 1;
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, wbar;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) tc::tmem_alloc(&tbase, 512);
-  if (tid == 0) tc::mbar_init(&bar, 1);
-  stage_weights(h.Wh, TC_H, h.NH, TC_H, NHP, whh, whl);
-  for (int i = tid; i < NHP; i += blockDim.x) sbh[i] = i < h.NH ? h.bh[i] : 0.f;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&wbar, 1);
+  }
+  __syncthreads();
+  if (h.packed) {
+    if (tid == 0) tc::bulk_load(sm, h.packed, heads_image_bytes(NHP), &wbar);
+    tc::mbar_wait(&wbar, 0);
+  } else {
+    stage_weights(h.Wh, TC_H, h.NH, TC_H, NHP, whh, whl);
+    for (int i = tid; i < HEADS_NMAX; i += blockDim.x) sbh[i] = i < h.NH ? h.bh[i] : 0.f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   tc_sync();
   const uint32_t tm = tbase;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
   const uint32_t cAh = 0, cAl = 128, cD = 256;
   const uint32_t idesc = tc::idesc_tf32(128, NHP);
   const uint32_t s_hh = tc::smem_u32(whh), s_hl = tc::smem_u32(whl);
-  const int64_t tiles_n = (n + 127) / 128;
+  const int64_t tiles_n = (h.n + 127) / 128;
   uint32_t phase = 0;
   for (int64_t tile = blockIdx.x; tile < tiles_n; tile += gridDim.x) {
-    const int64_t r0 = tile * 128;
-    if (warp < 4) {
-      const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-      const int64_t row = r0 + tid;
-      for (int c0 = 0; c0 < TC_H; c0 += 32) {
-        float v[32];
-        if (row < n) {
+    const int64_t row = tile * 128 + tid;
+    float* hrow = h.hid + row * TC_H;
+    for (int c0 = 0; c0 < TC_H; c0 += 32) {
+      float v[32];
+      if (row < h.n) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 q = *(const float4*)(h.hid + row * TC_H + c0 + j);
-            v[j] = q.x;
-            v[j + 1] = q.y;
-            v[j + 2] = q.z;
-            v[j + 3] = q.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        for (int j = 0; j < 32; j += 4) {
+          const float4 q = *(const float4*)(hrow + c0 + j);
+          v[j] = q.x;
+          v[j + 1] = q.y;
+          v[j + 2] = q.z;
+          v[j + 3] = q.w;
         }
-        store_split32(tm + lane_off + cAh + c0, tm + lane_off + cAl + c0, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
-      tc::tmem_st_wait();
+      store_split32(tm + lane_off + cAh + c0, tm + lane_off + cAl + c0, v);
     }
+    tc::tmem_st_wait();
     tc_sync();
     if (tid == 0) {
       mma_3xtf32(tm + cD, tm + cAh, tm + cAl, s_hh, s_hl, TC_H, idesc);
       tc::mma_commit(&bar);
     }
-    if (warp < 4) {
-      __syncwarp();
-      tc::mbar_wait(&bar, phase);
-      tc::fence_after();
-      const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-      for (int c0 = 0; c0 < NHP; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(tm + lane_off + cD + c0, v);
+    __syncwarp();
+    tc::mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+    for (int c0 = 0; c0 < NHP; c0 += 32) {
+      float v[32];
+      tc::tmem_ld32(tm + lane_off + cD + c0, v);
+      if (row < h.n) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c0 + j < NHP) slog[tid * LDL + c0 + j] = v[j] + sbh[c0 + j];
+        for (int j = 0; j < 32; ++j) {
+          const int c = c0 + j;
+          if (c < h.NH) {
+            const float zc = v[j] + sbh[c];
+            hrow[c] = zc;
+            if (h.logits_out) h.logits_out[row * h.NH + c] = zc;
+          }
+        }
       }
     }
-    phase ^= 1;
     tc_sync();
-    // ---- warp-per-row sampling + walker over the 128 rows ----
-    for (int rr = warp; rr < 128; rr += HEADS_THREADS / 32) {
-      const int64_t r = r0 + rr;
-      if (r >= n) break;
-      policy_row(sk, J, rng, slog + rr * LDL, h.NH, tiles, knobs, n, ld, r,
-                 inject, actions, logp, tiles_out, knobs_out, move_bits,
-                 shift_bits, head0_col, logits_out, status);
-    }
-    __syncthreads();
   }
   if (warp == 0) tc::tmem_dealloc(tm, 512);
 }

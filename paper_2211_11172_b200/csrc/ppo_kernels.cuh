@@ -28,20 +28,36 @@ struct PpoArgs {
 
 typedef harl_replay_ring PpoRing;
 
-constexpr int PPO_TM = 8;
+constexpr int PPO_TM = 2;
 constexpr int PPO_THREADS = 256;
+
+// Latency-bound small-batch layers: every thread keeps PPO_UNR weight
+// loads in flight (issued before the FMAs that consume them); the CTA's
+// row activations live in shared memory.
+constexpr int PPO_UNR = 16;
 
 // out[r][c] = act(sum_k in[r][k] W[k][c] + b[c]) for r < rows
 __device__ inline void dense64(const double* in, int ldi, int K,
                                const double* __restrict__ W,
                                const double* __restrict__ b, int N, double* out,
-                               int ldo, bool act, int rows) {
+                               int ldo, bool act, int rows, double*) {
   for (int c = threadIdx.x; c < N; c += blockDim.x) {
     double acc[PPO_TM];
 #pragma unroll
     for (int r = 0; r < PPO_TM; ++r) acc[r] = 0.0;
-    for (int k = 0; k < K; ++k) {
-      const double w = W[(int64_t)k * N + c];
+    int k = 0;
+    for (; k + PPO_UNR <= K; k += PPO_UNR) {
+      double w[PPO_UNR];
+#pragma unroll
+      for (int q = 0; q < PPO_UNR; ++q) w[q] = __ldg(W + (int64_t)(k + q) * N + c);
+#pragma unroll
+      for (int q = 0; q < PPO_UNR; ++q)
+#pragma unroll
+        for (int r = 0; r < PPO_TM; ++r)
+          if (r < rows) acc[r] = fma(in[r * ldi + k + q], w[q], acc[r]);
+    }
+    for (; k < K; ++k) {
+      const double w = __ldg(W + (int64_t)k * N + c);
 #pragma unroll
       for (int r = 0; r < PPO_TM; ++r)
         if (r < rows) acc[r] = fma(in[r * ldi + k], w, acc[r]);
@@ -54,18 +70,29 @@ __device__ inline void dense64(const double* in, int ldi, int K,
   __syncthreads();
 }
 
-// out[r][k] = (sum_c d[r][c] W[k][c]) * (tanh' via act: 1 - a[r][k]^2)
+// out[r][k] = (sum_c d[r][c] W[k][c]) * (1 - a[r][k]^2)
 __device__ inline void back64(const double* d, int ldd, int N,
                               const double* __restrict__ W, int K,
                               const double* a, int lda, double* out, int ldo,
-                              int rows) {
+                              int rows, double*) {
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     double acc[PPO_TM];
 #pragma unroll
     for (int r = 0; r < PPO_TM; ++r) acc[r] = 0.0;
     const double* wr = W + (int64_t)k * N;
-    for (int c = 0; c < N; ++c) {
-      const double w = wr[c];
+    int c = 0;
+    for (; c + PPO_UNR <= N; c += PPO_UNR) {
+      double w[PPO_UNR];
+#pragma unroll
+      for (int q = 0; q < PPO_UNR; ++q) w[q] = __ldg(wr + c + q);
+#pragma unroll
+      for (int q = 0; q < PPO_UNR; ++q)
+#pragma unroll
+        for (int r = 0; r < PPO_TM; ++r)
+          if (r < rows) acc[r] = fma(d[r * ldd + c + q], w[q], acc[r]);
+    }
+    for (; c < N; ++c) {
+      const double w = __ldg(wr + c);
 #pragma unroll
       for (int r = 0; r < PPO_TM; ++r)
         if (r < rows) acc[r] = fma(d[r * ldd + c], w, acc[r]);
@@ -93,10 +120,14 @@ __global__ void __launch_bounds__(PPO_THREADS)
 k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout P,
            const __grid_constant__ NetLayout V, PpoRing ring, const int32_t* idx,
            const double* params, double* rows, double* rowout) {
+  extern __shared__ double srows[];
   const int r0 = blockIdx.x * PPO_TM;
   const int nrows = min(PPO_TM, a.B - r0);
   const int RS = a.row_stride;
-  double* base = rows + (int64_t)r0 * RS;
+  double* base = srows;  // this CTA's rows, copied out at the end
+  double* wbuf = srows + PPO_TM * RS;  // [PPO_KC][N + pad] weight chunk
+  __shared__ int16_t s_src[HARL_MAX_HEAD0];
+  for (int i = threadIdx.x; i < a.C0; i += blockDim.x) s_src[i] = a.head0_src[i];
   // gather X (shared by both nets: P.row_act[0] == V.row_act[0])
   for (int i = threadIdx.x; i < nrows * a.F; i += blockDim.x) {
     const int rr = i / a.F, k = i % a.F;
@@ -107,16 +138,16 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   for (int l = 0; l < P.n_layers; ++l)
     dense64(base + P.row_act[l], RS, P.dims[l], params + P.off_W[l],
             params + P.off_b[l], P.dims[l + 1], base + P.row_act[l + 1], RS,
-            true, nrows);
+            true, nrows, wbuf);
   const int H = P.dims[P.n_layers];
   const int NH = P.n_head_cols;
   dense64(base + P.row_act[P.n_layers], RS, H, params + P.off_hW,
-          params + P.off_hb, NH, base + P.row_head, RS, false, nrows);
+          params + P.off_hb, NH, base + P.row_head, RS, false, nrows, wbuf);
   // value net
   for (int l = 0; l < V.n_layers; ++l)
     dense64(base + V.row_act[l], RS, V.dims[l], params + V.off_W[l],
             params + V.off_b[l], V.dims[l + 1], base + V.row_act[l + 1], RS,
-            l < V.n_layers - 1, nrows);
+            l < V.n_layers - 1, nrows, wbuf);
   // per-row PPO terms, one warp per row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double invB = 1.0 / (double)a.B;
@@ -135,7 +166,7 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
       const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
       const int C = h == 0 ? a.C0 : 3;
       auto legal = [&](int j) -> bool {
-        if (h == 0) return j == a.C0 - 1 || ((mv >> a.head0_src[j]) & 1ull);
+        if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
         return (sb >> (3 * (h - 1) + j)) & 1u;
       };
       double m = -INFINITY;
@@ -176,7 +207,7 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
       const int C = h == 0 ? a.C0 : 3;
       const int col = ring.actions[slot * 4 + h];
       auto legal = [&](int j) -> bool {
-        if (h == 0) return j == a.C0 - 1 || ((mv >> a.head0_src[j]) & 1ull);
+        if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
         return (sb >> (3 * (h - 1) + j)) & 1u;
       };
       __syncwarp();
@@ -207,39 +238,40 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   // policy backward: dhid = dz . Wh^T, times (1 - hid^2)
   back64(base + P.row_head, RS, NH, params + P.off_hW, H,
          base + P.row_act[P.n_layers], RS, base + P.row_delta[P.n_layers - 1],
-         RS, nrows);
+         RS, nrows, wbuf);
   for (int l = P.n_layers - 1; l >= 1; --l)
     back64(base + P.row_delta[l], RS, P.dims[l + 1], params + P.off_W[l],
            P.dims[l], base + P.row_act[l], RS, base + P.row_delta[l - 1], RS,
-           nrows);
+           nrows, wbuf);
   for (int l = V.n_layers - 1; l >= 1; --l)
     back64(base + V.row_delta[l], RS, V.dims[l + 1], params + V.off_W[l],
            V.dims[l], base + V.row_act[l], RS, base + V.row_delta[l - 1], RS,
-           nrows);
+           nrows, wbuf);
+  double* out = rows + (int64_t)r0 * RS;
+  for (int i = threadIdx.x; i < nrows * RS; i += blockDim.x) out[i] = base[i];
 }
 
 // (b) fixed-order means; out: [0] actor loss, [1] value loss,
-// [2] policy loss, [3] entropy, [4] mean ratio, [5] finite flag
+// [2] policy loss, [3] entropy, [4] mean ratio.  One warp: lane l sums rows
+// l, l+32, ... in order, then a fixed xor tree (deterministic).
 __global__ void k_ppo_losses(int B, double w_ent, double w_val,
                              const double* rowout, double* losses,
                              int32_t* bad) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double smin = 0, ent = 0, ratio = 0, sq = 0;
-  for (int r = 0; r < B; ++r) {
-    smin += rowout[r * 4 + 0];
-    ent += rowout[r * 4 + 1];
-    ratio += rowout[r * 4 + 2];
-    sq += rowout[r * 4 + 3];
-  }
-  const double policy_loss = -(smin / B);
-  const double entropy = ent / B;
+  const int lane = threadIdx.x;
+  double q[4] = {0, 0, 0, 0};
+  for (int r = lane; r < B; r += 32)
+    for (int j = 0; j < 4; ++j) q[j] += rowout[r * 4 + j];
+  for (int j = 0; j < 4; ++j) q[j] = wsum64(q[j]);
+  if (lane != 0) return;
+  const double policy_loss = -(q[0] / B);
+  const double entropy = q[1] / B;
   const double a_loss = policy_loss - w_ent * entropy;
-  const double v_loss = w_val * (sq / B);
+  const double v_loss = w_val * (q[3] / B);
   losses[0] = a_loss;
   losses[1] = v_loss;
   losses[2] = policy_loss;
   losses[3] = entropy;
-  losses[4] = ratio / B;
+  losses[4] = q[2] / B;
   if (!isfinite(a_loss) || !isfinite(v_loss)) atomicOr(bad, 1);
 }
 
@@ -253,9 +285,16 @@ struct GradJob {
 
 constexpr int WG_T = 32;  // 32x32 output tile, 256 threads x 4 outputs
 
+struct GradJobs {
+  GradJob j[4 * (HARL_MAX_LAYERS + 2)];
+  int32_t n;
+};
+
 __global__ void __launch_bounds__(256)
-k_ppo_wgrad(const GradJob* jobs, int n_jobs, int B, int RS, const double* rows,
-            double* grads, int32_t* bad) {
+k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
+            const double* rows, double* grads, int32_t* bad) {
+  const GradJob* jobs = jt.j;
+  const int n_jobs = jt.n;
   __shared__ double sa[WG_T][WG_T + 1];
   __shared__ double sd[WG_T][WG_T + 1];
   __shared__ int s_job;
@@ -311,9 +350,16 @@ struct AdamArgs {
   harl_ppo_hyper h;
 };
 
-__global__ void k_ppo_adam(AdamArgs a, const int32_t* bad, const double* grads,
-                           double* params, double* m, double* v, float* params32) {
+__global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* bad,
+                           const double* grads, double* params, double* m,
+                           double* v, float* params32) {
   if (*bad) return;
+  if (adam_dev) {  // graph replay: this update's 1 - beta^t from device memory
+    a.h.b1t_pi = adam_dev[0];
+    a.h.b2t_pi = adam_dev[1];
+    a.h.b1t_v = adam_dev[2];
+    a.h.b2t_v = adam_dev[3];
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const bool pi = i < a.n_pi;

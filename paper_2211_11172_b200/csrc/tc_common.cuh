@@ -51,6 +51,30 @@ __device__ inline void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// bulk global->shared copy completing on an mbarrier (byte count armed
+// with expect_tx by the issuing thread)
+__device__ inline void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ inline void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// copy `bytes` (multiple of 16) with 32 KB bulk ops; call from one thread
+__device__ inline void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                 uint64_t* bar) {
+  mbar_expect_tx(bar, bytes);
+  for (uint32_t off = 0; off < bytes; off += 32768u) {
+    const uint32_t chunk = bytes - off < 32768u ? bytes - off : 32768u;
+    bulk_g2s((uint8_t*)dst + off, (const uint8_t*)src + off, chunk, bar);
+  }
+}
+
 // MMA completion -> mbarrier arrive (implicit before_thread_sync fence)
 __device__ inline void mma_commit(uint64_t* bar) {
   asm volatile(

@@ -228,47 +228,47 @@ class DeviceForest:
     tree; ``learning_rate * value`` is formed here with numpy, the same
     fp64 product the reference computes per prediction."""
 
+    NODE = np.dtype([("v", "<f8"), ("feat", "<i2"), ("left", "<i2"),
+                     ("right", "<i2"), ("pad", "<i2")])
+
     def __init__(self, trees, base: float, learning_rate: float,
                  fitted: bool = True, floor_value: float = 1e-6,
                  device=None):
         N.load()
         dev = _dev(device)
-        firsts, feats, lefts, rights, thrs, contribs = [], [], [], [], [], []
+        if len(trees) > 1024:
+            raise DeviceError("more than 1024 trees")
+        recs, firsts = [], []
         n = 0
         for feat, thr, left, right, val in trees:
             feat = np.asarray(feat)
-            _check_depth(feat, np.asarray(left), np.asarray(right))
+            left, right = np.asarray(left), np.asarray(right)
+            _check_depth(feat, left, right)
+            rec = np.zeros(len(feat), dtype=self.NODE)
+            leaf = feat < 0
+            # leaves carry learning_rate * value: the reference's fp64
+            # product (costmodel.py:224), formed here once
+            rec["v"] = np.where(leaf, learning_rate * np.asarray(val, np.float64),
+                                np.asarray(thr, np.float64))
+            rec["feat"] = feat.astype(np.int16)
+            rec["left"] = np.where(leaf, 0, left).astype(np.int16)
+            rec["right"] = np.where(leaf, 0, right).astype(np.int16)
+            recs.append(rec)
             firsts.append(n)
             n += len(feat)
-            feats.append(feat.astype(np.int16))
-            lefts.append(np.asarray(left).astype(np.int16))
-            rights.append(np.asarray(right).astype(np.int16))
-            thrs.append(np.asarray(thr, dtype=np.float64))
-            contribs.append(learning_rate * np.asarray(val, dtype=np.float64))
-        if len(trees) > 1024:
-            raise DeviceError("more than 1024 trees")
-        cat = (lambda xs, dt: np.concatenate(xs).astype(dt)
-               if xs else np.zeros(1, dt))
+        nodes = np.concatenate(recs) if recs else np.zeros(1, self.NODE)
         self.n_nodes = n
-        self.tree_first = torch.from_numpy(cat([np.asarray(firsts)], np.int32)
-                                           if firsts else np.zeros(1, np.int32)
-                                           ).to(dev)
-        self.feature = torch.from_numpy(cat(feats, np.int16)).to(dev)
-        self.left = torch.from_numpy(cat(lefts, np.int16)).to(dev)
-        self.right = torch.from_numpy(cat(rights, np.int16)).to(dev)
-        self.threshold = torch.from_numpy(cat(thrs, np.float64)).to(dev)
-        self.leaf_contrib = torch.from_numpy(cat(contribs, np.float64)).to(dev)
+        self.nodes = torch.from_numpy(nodes.view(np.uint8).copy()).to(dev)
+        self.tree_first = torch.from_numpy(
+            np.asarray(firsts if firsts else [0], dtype=np.int32)).to(dev)
         d = N.ForestDesc()
         d.n_trees = len(trees)
         d.fitted = 1 if fitted else 0
         d.base = float(base)
         d.floor_value = float(floor_value)
         d.tree_first = self.tree_first.data_ptr()
-        d.feature = self.feature.data_ptr()
-        d.left = self.left.data_ptr()
-        d.right = self.right.data_ptr()
-        d.threshold = self.threshold.data_ptr()
-        d.leaf_contrib = self.leaf_contrib.data_ptr()
+        d.nodes = self.nodes.data_ptr()
+        d.n_nodes = n
         self.desc = d
         self.device = dev
 
@@ -308,7 +308,7 @@ def gbt_predict(forest: DeviceForest, feat, n: int, old_score=None,
     with PF.span("gbt", n):
         N.check(lib.harl_gbt_predict(C.byref(forest.desc), _ptr(feat), n, F,
                                      _ptr(out), _ptr(old_score), _ptr(reward),
-                                     forest.n_nodes, _stream()),
+                                     _stream()),
                 "harl_gbt_predict")
     return (out[:n], reward[:n]) if old_score is not None else out[:n]
 
@@ -402,11 +402,33 @@ class DeviceAgent:
         self.tc = (hidden == (128, 128) and F <= 64 and self.NH <= 128
                    and os.environ.get("HARL_KERNELS", "tc") != "ffma")
         self._hid = None
+        self.packed = None
+        if self.tc:
+            lib = N.load()
+            self.packed = {
+                "pt": torch.empty(lib.harl_tc_packed_bytes(0, self.NH),
+                                  dtype=torch.uint8, device=dev),
+                "ph": torch.empty(lib.harl_tc_packed_bytes(1, self.NH),
+                                  dtype=torch.uint8, device=dev),
+                "vt": torch.empty(lib.harl_tc_packed_bytes(0, self.NH),
+                                  dtype=torch.uint8, device=dev)}
         self.head0_src = np.asarray(
             [int(c) // S if j < self.C0 - 1 else 0
              for j, c in enumerate(self.cols)], dtype=np.int16)
         self._build_descs()
         self.upload()
+
+    def repack(self):
+        """Rebuild the tcgen05 weight images from the fp32 rollout copy
+        (after upload and after every PPO update)."""
+        if not self.tc:
+            return
+        lib = N.load()
+        with PF.span("pack", 0, launches=3):
+            N.check(lib.harl_pack_tc_weights(
+                C.byref(self.pol_desc), C.byref(self.val_desc), self.F,
+                _ptr(self.packed["pt"]), _ptr(self.packed["ph"]),
+                _ptr(self.packed["vt"]), _stream()), "harl_pack_tc_weights")
 
     # -- host <-> device --------------------------------------------------
 
@@ -463,6 +485,8 @@ class DeviceAgent:
         self.params32.copy_(p.float())
         self.m.copy_(torch.from_numpy(self._pack(a.opt_pi.m, a.opt_v.m)))
         self.v.copy_(torch.from_numpy(self._pack(a.opt_pi.v, a.opt_v.v)))
+        if getattr(self, "packed", None) is not None:
+            self.repack()
 
     def download(self):
         """Write device params and moments back into the numpy lists."""
@@ -503,7 +527,7 @@ class DeviceAgent:
     # -- PPO ----------------------------------------------------------------
 
     def ppo_update(self, ring, slots, cfg, t_pi: int, t_v: int,
-                   scratch=None, losses=None):
+                   scratch=None, losses=None, adam_dev=None):
         """One ppo_update on replay ``slots`` (device int32 ring slots).
         ``t_pi``/``t_v`` are the Adam step counts AFTER this update."""
         lib = N.load()
@@ -532,13 +556,16 @@ class DeviceAgent:
             C.byref(ring.desc), _ptr(slots), B, self.F, self.C0, src,
             self.row_stride, _ptr(self.params), _ptr(self.grads), _ptr(self.m),
             _ptr(self.v), _ptr(self.params32), self.n_pi, self.n_params,
-            _ptr(losses), _ptr(self.bad), _ptr(scratch), _stream()),
+            _ptr(losses), _ptr(self.bad), _ptr(scratch), _ptr(adam_dev),
+            _stream()),
             "harl_ppo_update")
+        self.repack()
         return losses
 
 
 def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
-                n: int, gen=None, inject=None, out=None, want_logits=False):
+                n: int, gen=None, inject=None, out=None, want_logits=False,
+                rng_dev=None, advance=True):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
     Returns a dict of device tensors; ``status`` must be checked by the
@@ -578,13 +605,15 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
             _ptr(out["shift_bits"]), _ptr(out["head0_col"]), _ptr(logits),
             _ptr(out["status"])]
     if agent.tc:
-        with PF.span("policy_tc", n, launches=2):
-            N.check(lib.harl_policy_step_tc(*args, _ptr(agent.hid_scratch(n)),
-                                            _stream()), "harl_policy_step_tc")
+        with PF.span("policy_tc", n, launches=3):
+            N.check(lib.harl_policy_step_tc(
+                *args, _ptr(agent.hid_scratch(n)), rng_dev,
+                _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _stream()),
+                "harl_policy_step_tc")
     else:
         with PF.span("policy", n):
             N.check(lib.harl_policy_step(*args, _stream()), "harl_policy_step")
-    if gen is not None and inject is None:
+    if gen is not None and inject is None and advance:
         R.skip_u64(gen, 4 * n)
     if want_logits:
         out["logits"] = logits[:n]
@@ -612,7 +641,8 @@ def value_pair(agent: DeviceAgent, feat0, n0: int, feat1, n1: int,
             N.check(lib.harl_value_pair_tc(C.byref(agent.val_desc),
                                            _ptr(feat0), n0, _ptr(feat1), n1,
                                            feat0.shape[1], _ptr(out0),
-                                           _ptr(out1), _stream()),
+                                           _ptr(out1), _ptr(agent.packed["vt"]),
+                                           _stream()),
                     "harl_value_pair_tc")
         return out0[:n0], out1[:n1]
     return (value_estimate(agent, feat0, n0, out0),

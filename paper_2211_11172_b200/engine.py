@@ -137,13 +137,83 @@ class EpisodeResult:
         return out
 
 
+class _Buffers:
+    """Device buffers of one episode geometry (population, entry log, step
+    scratch, per-step parameter tables).  Kept alive across episodes so the
+    captured CUDA graphs' baked pointers stay valid."""
+
+    def __init__(self, eng, tables, P, V, plan, forest):
+        dev = eng.dev
+        self.tables, self.P, self.V, self.plan = tables, P, V, plan
+        self.forest = forest
+        self.dsk = D.DeviceSketch(tables, dev)
+        self.pop = [eng._pop(tables, P), eng._pop(tables, P)]
+        self.rt = [torch.empty(P, dtype=torch.int32, device=dev),
+                   torch.empty(P, dtype=torch.int32, device=dev)]
+        self.steps = torch.zeros(P, dtype=torch.int32, device=dev)
+        self.best = torch.full((P,), -math.inf, dtype=torch.float64,
+                               device=dev)
+        self.best_step = torch.zeros(P, dtype=torch.int32, device=dev)
+        self.ts = N.TrackStats(self.steps.data_ptr(), self.best.data_ptr(),
+                               self.best_step.data_ptr())
+        slots = max(tables.local_slots, 1)
+        Vm = max(V, 1)
+        self.log_tiles = torch.empty((slots, Vm), dtype=torch.int16, device=dev)
+        self.log_knobs = torch.empty((3, Vm), dtype=torch.uint8, device=dev)
+        self.log_score = torch.empty(Vm, dtype=torch.float64, device=dev)
+        self.log_reward = torch.empty(Vm, dtype=torch.float64, device=dev)
+        self.log_track = torch.empty(Vm, dtype=torch.int32, device=dev)
+        self.elog = N.EntryLog(self.log_tiles.data_ptr(),
+                               self.log_knobs.data_ptr(),
+                               self.log_score.data_ptr(),
+                               self.log_reward.data_ptr(),
+                               self.log_track.data_ptr(), Vm)
+        n_steps = len(plan)
+        self.n_ppo = sum(1 for s in plan if s["ppo"])
+        self.status = torch.full((max(n_steps, 1),), -1, dtype=torch.int64,
+                                 device=dev)
+        self.losses = torch.zeros((max(self.n_ppo, 1), 8),
+                                  dtype=torch.float64, device=dev)
+        self.pol_out = {
+            "actions": torch.empty((4, P), dtype=torch.int32, device=dev),
+            "logp": torch.empty(P, dtype=torch.float64, device=dev),
+            "move_bits": torch.empty(P, dtype=torch.int64, device=dev),
+            "shift_bits": torch.empty(P, dtype=torch.int32, device=dev),
+            "head0_col": torch.empty(P, dtype=torch.int32, device=dev)}
+        self.reward = torch.empty(P, dtype=torch.float64, device=dev)
+        self.v_cur = torch.empty(P, dtype=torch.float32, device=dev)
+        self.v_next = torch.empty(P, dtype=torch.float32, device=dev)
+        self.adv = torch.empty(P, dtype=torch.float64, device=dev)
+        self.keep = torch.empty(P, dtype=torch.int32, device=dev)
+        # per-step tables for graph replay (host fills them each episode)
+        self.rng_tab = torch.zeros((max(n_steps, 1), 2), dtype=torch.int64,
+                                   device=dev)
+        self.wpos_tab = torch.zeros(max(n_steps, 1), dtype=torch.int64,
+                                    device=dev)
+        Bmax = max([s["ppo"] or 0 for s in plan] + [1])
+        self.slot_tab = torch.zeros((max(self.n_ppo, 1), Bmax),
+                                    dtype=torch.int32, device=dev)
+        self.adam_tab = torch.zeros((max(self.n_ppo, 1), 4),
+                                    dtype=torch.float64, device=dev)
+        self.graphs = None      # list of (first_step, last_step, CUDAGraph)
+
+
 class EpisodeEngine:
     """Device state of one subgraph agent: parameters + Adam (DeviceAgent)
     and the replay ring, persistent across that subgraph's episodes like the
-    reference's ``self.agents[sg]``/``self.buffers[sg]``."""
+    reference's ``self.agents[sg]``/``self.buffers[sg]``.
+
+    ``run_episode`` replays each inter-cull segment of the episode as one
+    captured CUDA graph (the whole plan -- live-row counts, cull points,
+    PPO steps, minibatch sizes -- is fixed before the episode starts; the
+    per-step values that do change between episodes, i.e. the RNG base
+    state, replay write position, minibatch slots and Adam bias
+    corrections, are read by the kernels from device tables the host fills
+    before launching).  Parity hooks (``inject``/``record``/
+    ``cull_override``) run the same launch sequence eagerly."""
 
     def __init__(self, agent: AgentState, rl_cfg: RlConfig, levels: int,
-                 device=None):
+                 device=None, use_graphs: bool = True):
         N.load()
         self.dev = D._dev(device)
         self.agent = agent
@@ -153,8 +223,67 @@ class EpisodeEngine:
         self.replay = D.DeviceReplay(rl_cfg.buffer_capacity, agent.feature_len,
                                      self.dev)
         self._ppo_scratch = None
+        self.use_graphs = use_graphs
+        self._cache = {}
 
     # -----------------------------------------------------------------------
+
+    def _buffers(self, tables, cfg, forest, plan):
+        key = (id(tables), cfg, id(forest),
+               tuple((s["m"], s["cull"], s["ppo"]) for s in plan))
+        b = self._cache.get(key)
+        if b is None:
+            if len(self._cache) > 8:
+                self._cache.clear()
+            b = _Buffers(self, tables, cfg.tracks, cfg.budget, plan, forest)
+            b.keepalive = (tables, forest)
+            self._cache[key] = b
+        return b
+
+    def _launch_step(self, b, k, step, cur, nxt, rt, used, graph_mode,
+                     gen=None, inj=None, want_logits=False):
+        """Issue every launch of search step k (policy+walker, featurize,
+        GBT+reward, V(X)/V(X'), finish).  In graph mode the RNG base state
+        and the replay write position come from the device tables."""
+        tables, m, P = b.tables, step["m"], b.P
+        lib = N.load()
+        out = dict(b.pol_out)
+        out["tiles"], out["knobs"] = nxt["tiles"], nxt["knobs"]
+        out["status"] = b.status[k:k + 1]
+        res = D.policy_step(b.dsk, self.dagent, cur["feat"], cur["tiles"],
+                            cur["knobs"], m, gen=gen, inject=inj, out=out,
+                            want_logits=want_logits,
+                            rng_dev=b.rng_tab[k] if graph_mode else None,
+                            advance=not graph_mode)
+        D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
+        D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
+                      out=nxt["score"], reward=b.reward)
+        D.value_pair(self.dagent, cur["feat"], m, nxt["feat"], m, b.v_cur,
+                     b.v_next)
+        po = b.pol_out
+        io = N.StepBuffers(
+            rt.data_ptr(), nxt["tiles"].data_ptr(), nxt["knobs"].data_ptr(),
+            cur["feat"].data_ptr(), nxt["feat"].data_ptr(),
+            nxt["score"].data_ptr(), b.reward.data_ptr(), b.v_cur.data_ptr(),
+            b.v_next.data_ptr(), po["actions"].data_ptr(),
+            po["head0_col"].data_ptr(), po["logp"].data_ptr(),
+            po["move_bits"].data_ptr(), po["shift_bits"].data_ptr(),
+            b.adv.data_ptr())
+        cap = self.replay.cap
+        with PF.span("finish", m):
+            N.check(lib.harl_finish_step(
+                io, m, P, used, tables.local_slots, tables.feature_len,
+                self.rl_cfg.discount, 1, self.replay.desc, self.replay.wpos,
+                max(0, m - cap), b.elog, b.ts,
+                D._ptr(b.wpos_tab[k:k + 1]) if graph_mode else None,
+                D._stream()), "harl_finish_step")
+        return res
+
+    def _launch_ppo(self, b, j, B, slots_t, t_pi, t_v, graph_mode):
+        self._ensure_ppo_scratch(B)
+        self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg, t_pi, t_v,
+                               scratch=self._ppo_scratch, losses=b.losses[j],
+                               adam_dev=b.adam_tab[j] if graph_mode else None)
 
     def run_episode(self, tables: SketchTables, forest: D.DeviceForest, gen,
                     cfg: EpisodeConfig, order_counter: int = 0,
@@ -166,117 +295,92 @@ class EpisodeEngine:
         chosen actions; ``record`` collects per-step device tensors for
         parity checks; ``cull_override(step, own_choice)`` may replace the
         eliminated track set (parity replays only)."""
-        dev = self.dev
-        dsk = D.DeviceSketch(tables, dev)
-        F = tables.feature_len
-        P = cfg.tracks
-        V = cfg.budget
-        rl = cfg.rl
-        plan = schedule(cfg, len(self.replay), self.rl_cfg)
-        if not rl:
+        if not cfg.rl:
             raise NotImplementedError("non-RL searchers: uniform device "
                                       "actions are not implemented yet")
-        # ---- population -------------------------------------------------
-        cur = self._pop(tables, P)
-        nxt = self._pop(tables, P)
-        D.init_population(dsk, P, gen, cur["tiles"], cur["knobs"])
-        D.featurize(dsk, cur["tiles"], cur["knobs"], P, cur["feat"])
+        plan = schedule(cfg, len(self.replay), self.rl_cfg)
+        b = self._buffers(tables, cfg, forest, plan)
+        eager = (inject is not None or record is not None or
+                 cull_override is not None or not self.use_graphs)
+        P = cfg.tracks
+        # ---- population (outside any graph: the sampler may sync) -------
+        cur, nxt = b.pop[0], b.pop[1]
+        rt, rt_spare = b.rt[0], b.rt[1]
+        D.init_population(b.dsk, P, gen, cur["tiles"], cur["knobs"])
+        D.featurize(b.dsk, cur["tiles"], cur["knobs"], P, cur["feat"])
         D.gbt_predict(forest, cur["feat"], P, out=cur["score"])
-        rt = torch.arange(P, dtype=torch.int32, device=dev)
-        rt_spare = torch.empty_like(rt)
-        steps_t = torch.zeros(P, dtype=torch.int32, device=dev)
-        best = torch.full((P,), -math.inf, dtype=torch.float64, device=dev)
-        best_step = torch.zeros(P, dtype=torch.int32, device=dev)
-        ts = N.TrackStats(steps_t.data_ptr(), best.data_ptr(),
-                          best_step.data_ptr())
-        # ---- entry log ----------------------------------------------------
-        slots = max(tables.local_slots, 1)
-        log_tiles = torch.empty((slots, max(V, 1)), dtype=torch.int16, device=dev)
-        log_knobs = torch.empty((3, max(V, 1)), dtype=torch.uint8, device=dev)
-        log_score = torch.empty(max(V, 1), dtype=torch.float64, device=dev)
-        log_reward = torch.empty(max(V, 1), dtype=torch.float64, device=dev)
-        log_track = torch.empty(max(V, 1), dtype=torch.int32, device=dev)
-        elog = N.EntryLog(log_tiles.data_ptr(), log_knobs.data_ptr(),
-                          log_score.data_ptr(), log_reward.data_ptr(),
-                          log_track.data_ptr(), max(V, 1))
-        # ---- per-step scratch ---------------------------------------------
-        n_steps = len(plan)
-        status = torch.full((max(n_steps, 1),), -1, dtype=torch.int64,
-                            device=dev)
-        n_ppo = sum(1 for s in plan if s["ppo"])
-        losses = torch.zeros((max(n_ppo, 1), 8), dtype=torch.float64,
-                             device=dev)
-        pol_out = {
-            "actions": torch.empty((4, P), dtype=torch.int32, device=dev),
-            "logp": torch.empty(P, dtype=torch.float64, device=dev),
-            "move_bits": torch.empty(P, dtype=torch.int64, device=dev),
-            "shift_bits": torch.empty(P, dtype=torch.int32, device=dev),
-            "head0_col": torch.empty(P, dtype=torch.int32, device=dev)}
-        reward = torch.empty(P, dtype=torch.float64, device=dev)
-        v_cur = torch.empty(P, dtype=torch.float32, device=dev)
-        v_next = torch.empty(P, dtype=torch.float32, device=dev)
-        adv = torch.empty(P, dtype=torch.float64, device=dev)
+        rt.copy_(torch.arange(P, dtype=torch.int32, device=self.dev))
+        b.steps.zero_()
+        b.best.fill_(-math.inf)
+        b.best_step.zero_()
+        b.status.fill_(-1)
+        self.dagent.bad.zero_()
+        if eager:
+            res = self._run_eager(b, gen, cfg, order_counter, inject, record,
+                                  cull_override)
+        else:
+            res = self._run_graphed(b, gen, cfg, order_counter)
+        st = b.status.cpu().numpy().view(np.uint64)
+        for code in st[:len(plan)]:
+            D.raise_status(int(code))
+        if int(self.dagent.bad.item()):
+            from .errors import RlDivergedError
+            raise RlDivergedError("non-finite loss or gradient in update")
+        return res
+
+    def _result(self, b, cfg, order_counter, used, culls, train, alive):
+        return EpisodeResult(tables=b.tables, visits=used,
+                             order_start=order_counter,
+                             log_tiles=b.log_tiles, log_knobs=b.log_knobs,
+                             log_score=b.log_score, log_reward=b.log_reward,
+                             log_track=b.log_track,
+                             step_rows=[s["m"] for s in b.plan], culls=culls,
+                             train=train, track_steps=b.steps,
+                             track_best_step=b.best_step, alive=alive)
+
+    # ---- eager path (parity hooks) ------------------------------------------
+
+    def _run_eager(self, b, gen, cfg, order_counter, inject, record,
+                   cull_override):
+        from . import rng as R
+        P = cfg.tracks
+        cur, nxt = b.pop[0], b.pop[1]
+        rt, rt_spare = b.rt[0], b.rt[1]
         alive = np.ones(P, dtype=bool)
         culls, train = [], []
-        used = 0
-        ppo_k = 0
-        lib = N.load()
-        for k, step in enumerate(plan):
+        used, ppo_k = 0, 0
+        for k, step in enumerate(b.plan):
             m = step["m"]
-            out = dict(pol_out)
-            out["tiles"], out["knobs"] = nxt["tiles"], nxt["knobs"]
-            out["status"] = status[k:k + 1]
             inj = inject(step["t"]) if inject is not None else None
-            res = D.policy_step(dsk, self.dagent, cur["feat"], cur["tiles"],
-                                cur["knobs"], m, gen=gen, inject=inj, out=out,
-                                want_logits=record is not None)
+            res = self._launch_step(b, k, step, cur, nxt, rt, used, False,
+                                    gen=gen, inj=inj,
+                                    want_logits=record is not None)
             if inj is not None:
-                from . import rng as R
                 R.skip_u64(gen, 4 * m)
-            D.featurize(dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
-            D.gbt_predict(forest, nxt["feat"], m, old_score=cur["score"],
-                          out=nxt["score"], reward=reward)
-            D.value_pair(self.dagent, cur["feat"], m, nxt["feat"], m, v_cur,
-                         v_next)
-            cap = self.replay.cap
-            io = N.StepBuffers(
-                rt.data_ptr(), nxt["tiles"].data_ptr(),
-                nxt["knobs"].data_ptr(), cur["feat"].data_ptr(),
-                nxt["feat"].data_ptr(), nxt["score"].data_ptr(),
-                reward.data_ptr(), v_cur.data_ptr(), v_next.data_ptr(),
-                pol_out["actions"].data_ptr(), pol_out["head0_col"].data_ptr(),
-                pol_out["logp"].data_ptr(), pol_out["move_bits"].data_ptr(),
-                pol_out["shift_bits"].data_ptr(), adv.data_ptr())
-            with PF.span("finish", m):
-              N.check(lib.harl_finish_step(
-                io, m, P, used, tables.local_slots, F, self.rl_cfg.discount,
-                1 if rl else 0, self.replay.desc, self.replay.wpos,
-                max(0, m - cap), elog, ts, D._stream()), "harl_finish_step")
             self.replay.note_push(m)
             if record is not None:
+                po = b.pol_out
                 record.append({"t": step["t"], "m": m,
                                "sel": rt[:m].clone(),
                                "X": cur["feat"][:m].clone(),
-                               "actions": pol_out["actions"].view(-1)[:4 * m]
+                               "actions": po["actions"].view(-1)[:4 * m]
                                .view(4, m).clone(),
-                               "logp": pol_out["logp"][:m].clone(),
+                               "logp": po["logp"][:m].clone(),
                                "logits": res["logits"].clone(),
                                "new_tiles": nxt["tiles"][:, :m].clone(),
                                "new_knobs": nxt["knobs"][:, :m].clone(),
                                "new_feats": nxt["feat"][:m].clone(),
                                "new_score": nxt["score"][:m].clone(),
-                               "rewards": reward[:m].clone(),
-                               "v_cur": v_cur[:m].clone(),
-                               "v_next": v_next[:m].clone(),
-                               "adv": adv[:m].clone()})
-            # rows >= m (budget tail) keep their state: only happens on the
-            # final step, so the swap below is safe
+                               "rewards": b.reward[:m].clone(),
+                               "v_cur": b.v_cur[:m].clone(),
+                               "v_next": b.v_next[:m].clone(),
+                               "adv": b.adv[:m].clone()})
             cur, nxt = nxt, cur
             used += m
             if step["cull"]:
                 tracks = rt[:m].cpu().numpy().astype(np.int64)
                 before = alive.copy()
-                gone = self._cull(tracks, adv, m, alive, cfg)
+                gone = self._cull(tracks, b.adv, m, alive, cfg)
                 if cull_override is not None:
                     forced = cull_override(step["t"], gone)
                     if forced is not None:
@@ -285,7 +389,8 @@ class EpisodeEngine:
                         alive[gone] = False
                 culls.append((step["t"], gone, int(alive.sum())))
                 keep = np.flatnonzero(alive[tracks])
-                self._compact(tables, cur, rt, nxt, rt_spare, keep)
+                b.keep[:len(keep)].copy_(torch.from_numpy(keep.astype(np.int32)))
+                self._compact(b, cur, rt, nxt, rt_spare, len(keep))
                 cur, nxt = nxt, cur
                 rt, rt_spare = rt_spare, rt
                 if record is not None:
@@ -293,35 +398,136 @@ class EpisodeEngine:
             if step["ppo"]:
                 B = step["ppo"]
                 idx = gen.choice(len(self.replay), size=B, replace=False)
-                slots_np = self.replay.slots_of(idx)
-                slots_t = torch.from_numpy(slots_np).to(dev)
+                slots_t = torch.from_numpy(self.replay.slots_of(idx)).to(self.dev)
                 a = self.agent
                 a.opt_pi.t += 1
                 a.opt_v.t += 1
-                self._ensure_ppo_scratch(B)
-                self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
-                                       a.opt_pi.t, a.opt_v.t,
-                                       scratch=self._ppo_scratch,
-                                       losses=losses[ppo_k])
-                train.append((step["t"], losses[ppo_k], B))
+                self._launch_ppo(b, ppo_k, B, slots_t, a.opt_pi.t, a.opt_v.t,
+                                 False)
+                train.append((step["t"], b.losses[ppo_k], B))
                 if record is not None:
                     record[-1]["ppo_idx"] = idx
                 ppo_k += 1
-        # ---- errors in step order (the reference raises at the first) -----
-        st = status.cpu().numpy().view(np.uint64)
-        bad_ppo = int(self.dagent.bad.item())
-        for code in st[:n_steps]:
-            D.raise_status(int(code))
-        if bad_ppo:
-            from .errors import RlDivergedError
-            raise RlDivergedError("non-finite loss or gradient in update")
-        return EpisodeResult(tables=tables, visits=used,
-                             order_start=order_counter, log_tiles=log_tiles,
-                             log_knobs=log_knobs, log_score=log_score,
-                             log_reward=log_reward, log_track=log_track,
-                             step_rows=[s["m"] for s in plan], culls=culls,
-                             train=train, track_steps=steps_t,
-                             track_best_step=best_step, alive=alive)
+        return self._result(b, cfg, order_counter, used, culls, train, alive)
+
+    # ---- graph path --------------------------------------------------------
+
+    def _segments(self, plan):
+        """Step index ranges between host decisions (a cull ends a
+        segment; the next one starts with the survivor gather)."""
+        segs, start = [], 0
+        for k, step in enumerate(plan):
+            if step["cull"] or k == len(plan) - 1:
+                segs.append((start, k))
+                start = k + 1
+        return segs
+
+    def _capture(self, b, gen):
+        """Record each segment's launches once (pointer sequence fixed by
+        the plan).  ``gen`` only supplies the stream increment (jump
+        tables); states come from the device tables at replay."""
+        N.check(N.load().harl_prepare(), "harl_prepare")
+        if self.dagent.tc:
+            self.dagent.hid_scratch(b.P)
+        self._ensure_ppo_scratch(max([s["ppo"] or 0 for s in b.plan] + [1]))
+        segs = self._segments(b.plan)
+        graphs = []
+        cur_i, rt_i, used, ppo_k = 0, 0, 0, 0
+        wpos0 = self.replay.wpos
+        count0 = self.replay.count
+        stream = torch.cuda.Stream(device=self.dev)
+        stream.wait_stream(torch.cuda.current_stream())
+        for si, (k0, k1) in enumerate(segs):
+            g = torch.cuda.CUDAGraph()
+            n0 = PF.launch_count()
+            with torch.cuda.graph(g, stream=stream,
+                                  capture_error_mode="relaxed"):
+                if si > 0:
+                    n_keep = b.plan[k0 - 1]["m"] - b.plan[k0 - 1]["cull"]
+                    self._compact(b, b.pop[cur_i], b.rt[rt_i],
+                                  b.pop[1 - cur_i], b.rt[1 - rt_i], n_keep)
+                    cur_i, rt_i = 1 - cur_i, 1 - rt_i
+                for k in range(k0, k1 + 1):
+                    step = b.plan[k]
+                    self._launch_step(b, k, step, b.pop[cur_i],
+                                      b.pop[1 - cur_i], b.rt[rt_i], used, True,
+                                      gen=gen)
+                    cur_i = 1 - cur_i
+                    used += step["m"]
+                    if step["ppo"]:
+                        B = step["ppo"]
+                        self._launch_ppo(b, ppo_k, B, b.slot_tab[ppo_k, :B],
+                                         1, 1, True)
+                        ppo_k += 1
+            graphs.append((k0, k1, g, PF.launch_count() - n0))
+        torch.cuda.current_stream().wait_stream(stream)
+        self.replay.wpos, self.replay.count = wpos0, count0
+        b.graphs = graphs
+
+    def _run_graphed(self, b, gen, cfg, order_counter):
+        from . import rng as R
+        P = cfg.tracks
+        if b.graphs is None:
+            self._capture(b, gen)
+            PF.add_launches(-sum(g[3] for g in b.graphs))  # not executed
+        # ---- host precompute of every per-step value (data-independent) --
+        n_steps = len(b.plan)
+        rng_np = np.zeros((max(n_steps, 1), 2), dtype=np.uint64)
+        wpos_np = np.zeros(max(n_steps, 1), dtype=np.int64)
+        slot_np = np.zeros(tuple(b.slot_tab.shape), dtype=np.int32)
+        adam_np = np.zeros((max(b.n_ppo, 1), 4), dtype=np.float64)
+        idx_list = []
+        a = self.agent
+        ppo_k = 0
+        for k, step in enumerate(b.plan):
+            st = gen.bit_generator.state["state"]["state"]
+            rng_np[k, 0] = st & ((1 << 64) - 1)
+            rng_np[k, 1] = st >> 64
+            R.skip_u64(gen, 4 * step["m"])
+            wpos_np[k] = self.replay.wpos
+            self.replay.note_push(step["m"])
+            if step["ppo"]:
+                B = step["ppo"]
+                idx = gen.choice(len(self.replay), size=B, replace=False)
+                idx_list.append(idx)
+                slot_np[ppo_k, :B] = self.replay.slots_of(idx)
+                a.opt_pi.t += 1
+                a.opt_v.t += 1
+                adam_np[ppo_k] = (1.0 - 0.9 ** a.opt_pi.t,
+                                  1.0 - 0.999 ** a.opt_pi.t,
+                                  1.0 - 0.9 ** a.opt_v.t,
+                                  1.0 - 0.999 ** a.opt_v.t)
+                ppo_k += 1
+        b.rng_tab.copy_(torch.from_numpy(rng_np.view(np.int64)))
+        b.wpos_tab.copy_(torch.from_numpy(wpos_np))
+        b.slot_tab.copy_(torch.from_numpy(slot_np))
+        b.adam_tab.copy_(torch.from_numpy(adam_np))
+        # ---- replay the segments; host culls in between --------------------
+        alive = np.ones(P, dtype=bool)
+        culls, train = [], []
+        used, ppo_k = 0, 0
+        rt_i = 0
+        cur_i = 0
+        for si, (k0, k1, g, nl) in enumerate(b.graphs):
+            if si > 0:
+                prev = b.plan[k0 - 1]
+                m = prev["m"]
+                tracks = b.rt[rt_i][:m].cpu().numpy().astype(np.int64)
+                gone = self._cull(tracks, b.adv, m, alive, cfg)
+                culls.append((prev["t"], gone, int(alive.sum())))
+                keep = np.flatnonzero(alive[tracks]).astype(np.int32)
+                b.keep[:len(keep)].copy_(torch.from_numpy(keep))
+                rt_i = 1 - rt_i
+            g.replay()
+            PF.add_launches(nl)
+            for k in range(k0, k1 + 1):
+                step = b.plan[k]
+                used += step["m"]
+                if step["ppo"]:
+                    train.append((step["t"], b.losses[ppo_k], step["ppo"]))
+                    ppo_k += 1
+        del cur_i
+        return self._result(b, cfg, order_counter, used, culls, train, alive)
 
     # -----------------------------------------------------------------------
 
@@ -349,20 +555,21 @@ class EpisodeEngine:
         alive[gone] = False
         return gone
 
-    def _compact(self, tables, src, rt_src, dst, rt_dst, keep_rows):
+    def _compact(self, b, src, rt_src, dst, rt_dst, n_keep):
+        """Survivor gather with row indices from ``b.keep`` (device)."""
         lib = N.load()
-        idx = torch.from_numpy(keep_rows.astype(np.int32)).to(self.dev)
+        tables = b.tables
         P = src["tiles"].shape[1]
-        with PF.span("gather", len(keep_rows)):
-          N.check(lib.harl_gather_rows(
-            idx.data_ptr(), len(keep_rows), tables.local_slots,
-            tables.feature_len, src["tiles"].data_ptr(),
-            src["knobs"].data_ptr(), src["feat"].data_ptr(),
-            src["score"].data_ptr(), rt_src.data_ptr(), P,
-            dst["tiles"].data_ptr(), dst["knobs"].data_ptr(),
-            dst["feat"].data_ptr(), dst["score"].data_ptr(),
-            rt_dst.data_ptr(), dst["tiles"].shape[1], D._stream()),
-            "harl_gather_rows")
+        with PF.span("gather", n_keep):
+            N.check(lib.harl_gather_rows(
+                b.keep.data_ptr(), n_keep, tables.local_slots,
+                tables.feature_len, src["tiles"].data_ptr(),
+                src["knobs"].data_ptr(), src["feat"].data_ptr(),
+                src["score"].data_ptr(), rt_src.data_ptr(), P,
+                dst["tiles"].data_ptr(), dst["knobs"].data_ptr(),
+                dst["feat"].data_ptr(), dst["score"].data_ptr(),
+                rt_dst.data_ptr(), dst["tiles"].shape[1], D._stream()),
+                "harl_gather_rows")
 
     def _ensure_ppo_scratch(self, B):
         lib = N.load()

@@ -30,6 +30,12 @@ def launch_count() -> int:
     return _launches
 
 
+def add_launches(n: int):
+    """Account kernels executed by a CUDA-graph replay."""
+    global _launches
+    _launches += n
+
+
 @contextlib.contextmanager
 def span(name: str, rows: int, launches: int = 1):
     global _launches

@@ -1,0 +1,67 @@
+"""The CUDA-graph episode path is the eager launch sequence, replayed: on
+identical inputs it must produce bit-identical episodes (every kernel is
+deterministic), across several consecutive episodes (tables refilled, graphs
+reused) and for both kernel families (tcgen05 at hidden (128,128), FFMA
+otherwise)."""
+
+import copy
+
+import numpy as np
+import pytest
+
+from gpu_util import CONV, BMM_SOFTMAX, all_sketch_tables, needs_gpu
+
+pytestmark = [pytest.mark.gpu, needs_gpu]
+torch = pytest.importorskip("torch")
+
+
+def _setup(hidden, which):
+    import bench
+    from paper_2211_11172_b200 import device as D
+    from paper_2211_11172_b200.agent import RlConfig, init_session_agents
+    from paper_2211_11172_b200.engine import EpisodeConfig, EpisodeEngine
+    text = CONV if which == "conv" else BMM_SOFTMAX
+    tabs = all_sketch_tables(text)
+    sg, sk, tb = tabs[0] if which == "conv" else tabs[3]
+    rl = RlConfig(hidden=hidden, minibatch=64, buffer_capacity=512)
+    agent = init_session_agents([("sg", tb.num_slots)], tb.feature_len, rl,
+                                np.random.default_rng(0))["sg"]
+    forest = D.DeviceForest(bench.synthetic_forest(tb, 1), 0.5, 0.3)
+    cfg = EpisodeConfig(tracks=600, track_len=6, cull_window=3,
+                        cull_fraction=0.5, min_tracks=300)
+    engines = []
+    for graphs in (False, True):
+        eng = EpisodeEngine(copy.deepcopy(agent), rl, tb.levels,
+                            use_graphs=graphs)
+        engines.append(eng)
+    return tb, forest, cfg, engines
+
+
+@pytest.mark.parametrize("hidden,which", [((128, 128), "conv"),
+                                          ((32, 32), "bmm")])
+def test_graph_replay_is_bit_identical(hidden, which):
+    tb, forest, cfg, (eager, graphed) = _setup(hidden, which)
+    g1, g2 = np.random.default_rng(5), np.random.default_rng(5)
+    for ep in range(3):
+        r1 = eager.run_episode(tb, forest, g1, cfg, 0)
+        out1 = (r1.states(), r1.scores().copy(),
+                r1.log_reward[:r1.visits].cpu().numpy().copy(),
+                [c[1].copy() for c in r1.culls],
+                [t[1].cpu().numpy().copy() for t in r1.train])
+        r2 = graphed.run_episode(tb, forest, g2, cfg, 0)
+        assert graphed._cache and next(iter(graphed._cache.values())).graphs
+        np.testing.assert_array_equal(r2.states()[0], out1[0][0])
+        np.testing.assert_array_equal(r2.states()[1], out1[0][1])
+        assert r2.scores().tobytes() == out1[1].tobytes()
+        assert r2.log_reward[:r2.visits].cpu().numpy().tobytes() == \
+            out1[2].tobytes()
+        for a, b in zip([c[1] for c in r2.culls], out1[3]):
+            np.testing.assert_array_equal(a, b)
+        for a, b in zip([t[1].cpu().numpy() for t in r2.train], out1[4]):
+            assert a.tobytes() == b.tobytes()
+        assert g1.bit_generator.state == g2.bit_generator.state
+        assert eager.agent.opt_pi.t == graphed.agent.opt_pi.t
+        assert eager.replay.wpos == graphed.replay.wpos
+        assert torch.equal(eager.dagent.params, graphed.dagent.params)
+        assert torch.equal(eager.dagent.m, graphed.dagent.m)
+        assert torch.equal(eager.replay.X, graphed.replay.X)

@@ -312,11 +312,14 @@ def run_gpu(args, rank, world):
     # one extra, untimed episode with per-call CUDA events: kernel shares
     profiling.reset()
     profiling.timing(True)
+    profiling.native_timing(True)
     eng.use_graphs = False          # per-launch events need eager launches
     res = eng.run_episode(tb, forest, gen, ecfg, order)
     eng.use_graphs = True
     order += res.visits
     kstats = profiling.kernel_times()
+    native = profiling.native_kernel_times()
+    profiling.native_timing(False)
     profiling.timing(False)
     if world > 1:
         dist.barrier()
@@ -333,7 +336,7 @@ def run_gpu(args, rank, world):
         e2e_visits += v
         order += v
     return dict(total_ms=total_ms, visits=visits, clocks=clk.summary(),
-                launches=launches, kstats=kstats, e2e_ms=e2e_ms,
+                launches=launches, kstats=kstats, native=native, e2e_ms=e2e_ms,
                 e2e_visits=e2e_visits, h2d=h2d, d2h=d2h, P=P)
 
 
@@ -371,38 +374,99 @@ def e2e_episode(eng, w, forest_unused, gen, ecfg, order, dev):
     return nbytes_in, nbytes_out, res.visits
 
 
-def roofline_entry(kstats, tables, hidden):
-    """Dominant kernel's achieved rate vs the measured peak."""
+# kernel -> (profiling span whose rows it processes, bound)
+KERNEL_SPAN = {
+    "k_trunk_tc<policy>": ("policy_tc", "tensor"),
+    "k_heads_tc": ("policy_tc", "tensor"),
+    "k_sample_rows": ("policy_tc", "hbm"),
+    "k_trunk_tc<value>": ("value_tc", "tensor"),
+    "k_featurize": ("featurize", "hbm"),
+    "k_gbt_predict": ("gbt", "hbm"),
+    "k_finish_step": ("finish", "hbm"),
+    "k_ring_rows": ("finish", "hbm"),
+    "k_ppo_rows": ("ppo", "fp64"),
+}
+
+
+def per_row_work(tables, H):
+    """Algorithmic work per row (one schedule / one minibatch row) of each
+    kernel: flops for the MLP kernels, HBM bytes for the rest (DESIGN.md
+    "Kernels and their rooflines" states the same figures)."""
+    F, S = tables.feature_len, tables.num_slots
+    C = len(tables.head_cols)
+    NH = C + 9                      # tiling columns + 3 + 3 + 3 knob heads
+    state = 2 * S + 3               # int16 tile slots + 3 knob bytes
+    return {
+        "k_trunk_tc<policy>": 2 * (F * H + H * H),
+        "k_heads_tc": 2 * H * NH,
+        "k_trunk_tc<value>": 2 * (F * H + H * H + H),   # per evaluated row
+        # logits in; actions, logp, successor state out
+        "k_sample_rows": 4 * NH + state + 16 + 8 + state,
+        "k_featurize": state + 8 * F,
+        "k_gbt_predict": 8 * F + 8,
+        # reward/score/v/adv/log entry (state + score + track) + ring scalars
+        "k_finish_step": 8 * 6 + state + 8 + 4 + 8 * 4 + 16 + 4,
+        "k_ring_rows": 2 * 8 * F * 2,               # X and X' read + written
+        # policy + value forward and backward in fp64 (3x forward flops)
+        "k_ppo_rows": 3 * 2 * (2 * (F * H + H * H) + H * NH + H),
+    }
+
+
+def roofline_entry(native, spans, tables, hidden):
+    """Dominant kernel's achieved rate vs the measured peak, from the native
+    per-kernel event timer (harl_profile_*) of the untimed profiled episode;
+    rows per kernel come from the matching host span."""
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
-    if not kstats:
+    if not native:
         return None
-    top = max(kstats.items(), key=lambda kv: kv[1]["ms"])
-    name, st = top
-    F, H = tables.feature_len, hidden
-    C = len(tables.head_cols)
-    pol_flops = 2 * (F * H + H * H + H * (C + 9))
-    val_flops = 2 * (F * H + H * H + H)
-    per_row = {"policy": pol_flops, "value": val_flops}
-    if name in per_row:
-        flops = per_row[name] * st["rows"]
-        tf = flops / (st["ms"] * 1e-3) / 1e12
-        peak = peaks.get("bf16_tflops", 1590.0) / 2.0
-        return {"kernel": name, "bound": "tensor", "achieved": round(tf, 3),
-                "peak": peak, "unit": "TFLOP/s", "frac": round(tf / peak, 5),
-                "traffic": None,
-                "peak_note": "TF32 dense peak taken as measured bf16/2 "
-                             "(MEASURED_PEAKS.json); kernel is FFMA fp32"}
-    byts = {"featurize": 2 * tables.local_slots + 3 + 8 * F,
-            "gbt": 8 * F + 16, "finish": 120}.get(name, 64) * st["rows"]
-    gbs = byts / (st["ms"] * 1e-3) / 1e9
-    peak = peaks.get("hbm_gbs", 6650.0)
-    return {"kernel": name, "bound": "hbm", "achieved": round(gbs, 2),
-            "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 5),
-            "traffic": None}
+    work = per_row_work(tables, hidden)
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    bf16 = peaks.get("bf16_tflops", 1590.0)
+    tf32 = bf16 * 1.1 / 2.25        # dense tf32 : bf16 nominal ratio
+    fp64 = 37.0                     # B200 nominal fp64 (no measured figure)
+    table = {}
+    for name, st in native.items():
+        if name not in KERNEL_SPAN or st["ms"] <= 0:
+            continue
+        span, bound = KERNEL_SPAN[name]
+        rows = spans.get(span, {}).get("rows", 0)
+        q = work[name] * rows
+        if bound == "hbm":
+            ach = q / (st["ms"] * 1e-3) / 1e9
+            ent = {"bound": "hbm", "achieved": ach, "peak": hbm,
+                   "unit": "GB/s"}
+        else:
+            ach = q / (st["ms"] * 1e-3) / 1e12
+            pk = tf32 if bound == "tensor" else fp64
+            ent = {"bound": "tensor" if bound == "tensor" else "fp64",
+                   "achieved": ach, "peak": round(pk, 1), "unit": "TFLOP/s"}
+        ent["frac"] = ent["achieved"] / ent["peak"]
+        ent["us_per_launch"] = 1e3 * st["ms"] / max(1, st["launches"])
+        ent["ms_per_episode"] = st["ms"]
+        table[name] = ent
+    if not table:
+        return None
+    top = max(table, key=lambda k: table[k]["ms_per_episode"])
+    e = table[top]
+    out = {"kernel": top, "bound": e["bound"],
+           "achieved": round(e["achieved"], 3), "peak": e["peak"],
+           "unit": e["unit"], "frac": round(e["frac"], 5), "traffic": None,
+           "us_per_launch": round(e["us_per_launch"], 2),
+           "peak_note": "hbm: MEASURED_PEAKS.json hbm_gbs (burst); tensor: "
+                        "dense tf32 = measured bf16 x 1.1/2.25; fp64: 37 "
+                        "TFLOP/s nominal",
+           "kernels": {k: {"bound": v["bound"],
+                           "achieved": round(v["achieved"], 3),
+                           "unit": v["unit"], "frac": round(v["frac"], 5),
+                           "us_per_launch": round(v["us_per_launch"], 2),
+                           "ms_per_episode": round(v["ms_per_episode"], 4)}
+                       for k, v in sorted(table.items(),
+                                          key=lambda kv: -kv[1]["ms_per_episode"])}}
+    return out
 
 
 def main():
@@ -465,7 +529,7 @@ def main():
                 "d2h_bytes_per_step": int(r["d2h"])},
         "gpu_launches": int(r["launches"]),
         "clocks": r["clocks"],
-        "roofline": roofline_entry(r["kstats"], tb, 128),
+        "roofline": roofline_entry(r["native"], r["kstats"], tb, 128),
         "kernel_ms_per_episode": {k: round(v["ms"], 4)
                                   for k, v in r["kstats"].items()},
     }

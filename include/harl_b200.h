@@ -137,6 +137,16 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
                          int64_t ld, int64_t* u32_used_host, void* scratch,
                          void* stream);
 
+/* TuningSession._uniform_actions (tuner.py:341-348) for the non-RL
+ * searchers: head-major Generator.integers(len(valid)) per row (no draw when
+ * one choice is valid), exact including rejections.  actions: int32 [4][n]
+ * full head indices.  scratch >= harl_uniform_scratch_bytes(n). */
+int64_t harl_uniform_scratch_bytes(int64_t n);
+int harl_uniform_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
+                         const uint8_t* knobs, int64_t n, int64_t ld,
+                         const harl_pcg64* rng, int32_t* actions,
+                         void* scratch, int64_t* u32_used_host, void* stream);
+
 /* SketchContext.featurize (schedspace.py:415-438) incl. exact footprints
  * (372-411) and glibc-2.39-faithful log10. feat: [n][feature_len]. */
 int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
@@ -173,7 +183,10 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
  * optional logits float32 [n][n_head_cols] (NULL to skip).  *status as in
  * harl_apply_actions (HARL_ST_NO_VALID for an all-masked row).
  * If `inject` != NULL the actions are taken from it (int32 [4][n]) and the
- * uniforms are not used (parity replay of oracle actions). */
+ * uniforms are not used (parity replay of oracle actions).  Population
+ * shards: grow (optional device int32 [n]) is each local row's global row
+ * and m_total the step's global row count; the uniform of head h is then
+ * draw #(h*m_total + grow[r] + 1) (NULL/0: local rows, m_total = n). */
 int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                      const double* feat, const uint16_t* tiles,
                      const uint8_t* knobs, int64_t n, int64_t ld,
@@ -181,13 +194,14 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                      int32_t* actions, double* logp, uint16_t* tiles_out,
                      uint8_t* knobs_out, uint64_t* move_bits,
                      uint32_t* shift_bits, int32_t* head0_col,
-                     float* logits_out, uint64_t* status, void* stream);
+                     float* logits_out, uint64_t* status,
+                     const int32_t* grow, int64_t m_total, void* stream);
 
 /* select_actions + walker as harl_policy_step, on the tcgen05 path when
  * the policy is the production shape (hidden (128,128), feature_len <= 64,
  * n_head0 + 9 <= 128): trunk and heads as 3xTF32 tcgen05 MMAs with TMEM
  * accumulators and TMEM-resident activations.  hid_scratch: float32
- * [n][128] device scratch.  rng_state_dev (optional, device {lo, hi}
+ * [n][128] device scratch.  rng_state_dev (optional, device {hi, lo}
  * u64 PCG64 state) overrides rng's state at execution time so the call can
  * be replayed from a CUDA graph (rng still supplies the increment).  Not
  * a fallback: returns HARL_E_ARG if the shape is not eligible (the caller
@@ -202,7 +216,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* logits_out, uint64_t* status,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
-                        void* stream);
+                        const int32_t* grow, int64_t m_total, void* stream);
 
 /* V(X) and V(X') in one launch (tuner.py:395-396) on the tcgen05 path
  * (hidden (128,128), feature_len <= 64); HARL_E_ARG if not eligible. */
@@ -323,14 +337,21 @@ typedef struct harl_ppo_hyper {
 /* ppo_update (rlcore.py:361-378) on B replay slots `idx` (device int32):
  * fp64 forward/backward of both nets, fixed-order reductions, finite
  * checks, Adam (rlcore.py:62-71) on params[0, n_pi) (policy) and
- * [n_pi, n_params) (value), fp32 copy refresh.  losses (device double[8]):
+ * [n_pi, n_params) (value), fp32 copy refresh.  losses (device double[16]):
  * actor loss, value loss, policy loss, entropy, mean ratio.  *bad (device
  * int32, caller zeroes) != 0 when a loss or gradient was not finite, in
  * which case no parameter changed (RlDivergedError). scratch >=
  * harl_ppo_scratch_bytes(). head0_src: compact column -> source slot.
  * adam_dev (optional device double[4]: 1-b1^t, 1-b2^t for policy then
  * value) overrides hp's bias corrections at execution time (graph
- * replay).  No host<->device copies: legal inside stream capture. */
+ * replay).  No host<->device copies: legal inside stream capture.
+ * *_img (optional, from harl_pack_tc_weights): the Adam pass also
+ * refreshes these tcgen05 weight images in place.
+ * Sharded updates (population split over ranks): B = this rank's rows of
+ * the minibatch, B_norm = the global minibatch size; phase 1 computes this
+ * rank's gradient and loss partial sums (grads, losses[5..8]); the caller
+ * sum-all-reduces both; phase 2 finalises the losses, checks finiteness and
+ * applies Adam.  phase 3 = both (single device). */
 int64_t harl_ppo_scratch_bytes(int32_t B, int32_t row_stride,
                                int32_t n_jobs);
 int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
@@ -341,6 +362,8 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     double* adam_m, double* adam_v, float* params32,
                     int64_t n_pi, int64_t n_params, double* losses,
                     int32_t* bad, void* scratch, const double* adam_dev,
+                    void* pol_trunk_img, void* pol_heads_img,
+                    void* val_trunk_img, int32_t B_norm, int32_t phase,
                     void* stream);
 
 /* Diagnostic: one 128x128x64 kind::tf32 tcgen05 MMA (A [128][64], B
@@ -349,6 +372,22 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
  * layouts the MLP kernels rely on. */
 int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
                           void* stream);
+
+/* Instrumentation (no reference counterpart; the reference has no device).
+ * harl_launch_count: kernels this library has launched since load (graph
+ * replays excluded -- they do not pass through the library).
+ * harl_profile_set(on, spin_ns): while on, every non-captured launch is
+ * preceded by a spin kernel of spin_ns ns (<0 keeps the current value) and
+ * bracketed by CUDA events on its own stream.  harl_profile_read
+ * synchronises the recorded events and writes, per distinct kernel (first
+ * appearance order, at most max_kernels), its name (NUL-terminated in
+ * name_cap-byte slots), summed milliseconds and launch count; it returns
+ * the number of distinct kernels. */
+long long harl_launch_count(void);
+int harl_profile_set(int on, long long spin_ns);
+int harl_profile_reset(void);
+int harl_profile_read(int max_kernels, char* names, int name_cap,
+                      double* total_ms, long long* launches);
 
 #ifdef __cplusplus
 }

@@ -404,11 +404,15 @@ class RlCfg:
     train_interval: int = 2
 
 
-def ppo_grads(agent: Agent, X, masks, actions, logp_old, adv, td, cfg: RlCfg):
+def ppo_grads(agent: Agent, X, masks, actions, logp_old, adv, td, cfg: RlCfg,
+              norm: int | None = None):
     """rlcore.py:293-358 -> (actor loss, actor grads, stats, value loss,
-    value grads)."""
+    value grads).  ``norm`` (sharding checks only) replaces the batch size
+    in the gradient normalisation so per-shard gradients sum to the full
+    one; ``None`` is the reference."""
     logits, (trunk_acts, hid) = agent.policy_forward(X)
     B = len(X)
+    Bn = B if norm is None else norm
     rows = np.arange(B)
     logp_new = np.zeros(B)
     ent_total = np.zeros(B)
@@ -428,14 +432,14 @@ def ppo_grads(agent: Agent, X, masks, actions, logp_old, adv, td, cfg: RlCfg):
     entropy = ent_total.mean()
     a_loss = float(policy_loss - cfg.entropy_weight * entropy)
     coef = np.where(s_un <= s_cl, ratio * adv, 0.0)
-    dlogp = -coef / B
+    dlogp = -coef / Bn
     dhid = np.zeros_like(hid)
     head_grads = []
     for h, (lp_safe, p, ent) in enumerate(heads):
         onehot = np.zeros_like(p)
         onehot[rows, actions[:, h]] = 1.0
         dz = dlogp[:, None] * (onehot - p)
-        dz += (cfg.entropy_weight / B) * p * (lp_safe + ent[:, None])
+        dz += (cfg.entropy_weight / Bn) * p * (lp_safe + ent[:, None])
         head_grads += [hid.T @ dz, dz.sum(axis=0)]
         dhid += dz @ agent.head_W[h].T
     dtrunk = dhid * (1.0 - hid ** 2)
@@ -444,7 +448,8 @@ def ppo_grads(agent: Agent, X, masks, actions, logp_old, adv, td, cfg: RlCfg):
              "mean_ratio": float(ratio.mean())}
     v, vacts = agent.value(X)
     v_loss = float(cfg.value_loss_weight * np.mean((v - td) ** 2))
-    dv = cfg.value_loss_weight * 2.0 * (v - td) / len(X)
+    dv = cfg.value_loss_weight * 2.0 * (v - td) / (len(X) if norm is None
+                                                    else norm)
     v_grads, _ = dense_backward(agent.val_W, vacts, dv[:, None])
     return a_loss, trunk_grads + head_grads, stats, v_loss, v_grads
 

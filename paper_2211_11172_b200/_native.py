@@ -113,17 +113,20 @@ _SIGS = {
     "harl_init_population": (i32, [P(SketchDesc), P(Pcg64), i64, vp, vp, i64,
                                    P(i64), vp, vp]),
     "harl_featurize": (i32, [P(SketchDesc), vp, vp, i64, i64, vp, vp]),
+    "harl_uniform_scratch_bytes": (i64, [i64]),
+    "harl_uniform_actions": (i32, [P(SketchDesc), vp, vp, i64, i64, P(Pcg64),
+                                   vp, vp, P(i64), vp]),
     "harl_action_masks": (i32, [P(SketchDesc), vp, vp, i64, i64, vp, vp, vp]),
     "harl_apply_actions": (i32, [P(SketchDesc), vp, vp, i64, i64, vp, vp, vp,
                                  vp, vp]),
     "harl_gbt_predict": (i32, [P(ForestDesc), vp, i64, i32, vp, vp, vp, vp]),
     "harl_policy_step": (i32, [P(SketchDesc), P(MlpDesc), vp, vp, vp, i64, i64,
                                P(Pcg64), vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                               vp, vp]),
+                               vp, vp, i64, vp]),
     "harl_value_forward": (i32, [P(MlpDesc), vp, i64, i32, vp, vp]),
     "harl_policy_step_tc": (i32, [P(SketchDesc), P(MlpDesc), vp, vp, vp, i64,
                                   i64, P(Pcg64), vp, vp, vp, vp, vp, vp, vp,
-                                  vp, vp, vp, vp, vp, vp, vp, vp]),
+                                  vp, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
     "harl_value_pair_tc": (i32, [P(MlpDesc), vp, i64, vp, i64, i32, vp, vp,
                                  vp, vp]),
     "harl_tc_packed_bytes": (i64, [i32, i32]),
@@ -136,9 +139,14 @@ _SIGS = {
                                vp, vp, vp, vp, i64, vp]),
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_selftest_tcgen05": (i32, [vp, vp, vp, i32, vp]),
+    "harl_launch_count": (C.c_longlong, []),
+    "harl_profile_set": (i32, [i32, C.c_longlong]),
+    "harl_profile_reset": (i32, []),
+    "harl_profile_read": (i32, [i32, C.c_char_p, i32, vp, vp]),
     "harl_ppo_update": (i32, [P(NetLayout), P(NetLayout), P(PpoHyper),
                               P(ReplayRing), vp, i32, i32, i32, vp, i32, vp,
-                              vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp]),
+                              vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp,
+                              vp, vp, i32, i32, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -21,9 +21,9 @@ checkpoints, the CLI -- is the reference's own code.  Per episode it
   (``episode_step``/``cull``/``train``/``episode_end``, tuner.py:413-439);
 * returns the visited entries as the reference's ``CandidateEntry`` list.
 
-Only the RL searchers have a device path; non-RL searchers (random /
-evolutionary) are not the north-star hot path and raise
-``NotImplementedError`` rather than silently running on the CPU.
+The evolutionary searcher's uniform actions (tuner.py:341-348) run on the
+device too (``harl_uniform_actions``); the random searcher never calls
+``_run_episode`` (tuner.py:477-478).
 """
 
 from __future__ import annotations
@@ -122,9 +122,6 @@ def b200_session_class(base):
             from schedtune.costmodel import CandidateEntry
             from schedtune.schedspace import ScheduleState
             ecfg = EpisodeConfig.from_tuner(self.cfg, self.searcher)
-            if not ecfg.rl:
-                raise NotImplementedError(
-                    "the B200 episode engine implements the RL searchers")
             eng = self._b200_engine(sg)
             tables = self._b200_sketch_tables(sg, sketch)
             eng.dagent.upload()

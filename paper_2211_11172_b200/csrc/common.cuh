@@ -13,10 +13,20 @@ namespace harl {
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 
+// Launch accounting and the optional per-kernel timer (harl_profile_*).
+// Every library launch is bracketed by HARL_PROF_BEGIN(stream) and
+// HARL_CHECK_LAUNCH(name); with the timer on (and the stream not being
+// captured) the pair becomes spin-kernel, event, <kernel>, event.
+void prof_begin(cudaStream_t st);
+void prof_end(const char* where);
+
+#define HARL_PROF_BEGIN(st) ::harl::prof_begin((cudaStream_t)(st))
+
 #define HARL_CHECK_LAUNCH(where)                                     \
   do {                                                               \
     cudaError_t _e = cudaGetLastError();                             \
     if (_e != cudaSuccess) return ::harl::cuda_status(_e, where);    \
+    ::harl::prof_end(where);                                         \
   } while (0)
 
 // ---------------------------------------------------------------------------

@@ -21,7 +21,7 @@ struct FinishArgs {
   int64_t keep_from;    // rows >= keep_from survive in the ring
 };
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
               const __grid_constant__ harl_replay_ring ring,
               const __grid_constant__ harl_entry_log log,
@@ -29,17 +29,6 @@ k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
               const int64_t* wpos_dev) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t wpos = wpos_dev ? *wpos_dev : a.wpos;
-  // feature rows of the surviving replay pushes: flat, coalesced copy
-  if (a.rl) {
-    const int64_t keep = a.n - a.keep_from;
-    const int64_t total = keep * a.F;
-    for (int64_t e = r; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t rr = a.keep_from + e / a.F, k = e % a.F;
-      const int64_t slot = (wpos + rr) % ring.cap;
-      ring.X[slot * a.F + k] = io.feat[rr * a.F + k];
-      ring.Xn[slot * a.F + k] = io.feat_new[rr * a.F + k];
-    }
-  }
   if (r >= a.n) return;
   const int32_t* __restrict__ row_track = io.row_track;
   const uint16_t* __restrict__ tiles_new = io.tiles_new;
@@ -59,11 +48,16 @@ k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
   const uint32_t* shift_bits = io.shift_bits;
   double* adv_out = io.adv;
   const int64_t v = a.vbase + r;
-  uint16_t tv[HARL_MAX_SLOTS];
-#pragma unroll 8
-  for (int s = 0; s < a.local_slots; ++s) tv[s] = tiles_new[(int64_t)s * a.ld + r];
-#pragma unroll 8
-  for (int s = 0; s < a.local_slots; ++s) log_tiles[(int64_t)s * log.ld + v] = tv[s];
+  // slot-major copy, 8 independent loads in flight per thread
+  for (int s0 = 0; s0 < a.local_slots; s0 += 8) {
+    uint16_t t8[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      t8[q] = (s0 + q < a.local_slots) ? tiles_new[(int64_t)(s0 + q) * a.ld + r] : 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (s0 + q < a.local_slots) log_tiles[(int64_t)(s0 + q) * log.ld + v] = t8[q];
+  }
   for (int k = 0; k < 3; ++k) log_knobs[(int64_t)k * log.ld + v] = knobs_new[(int64_t)k * a.ld + r];
   const double sc = new_score[r];
   const double rw = reward[r];
@@ -86,8 +80,6 @@ k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
   adv_out[r] = adv;
   if (r < a.keep_from) return;
   const int64_t slot = (wpos + r) % ring.cap;
-  (void)feat;
-  (void)feat_new;
   ring.actions[slot * 4 + 0] = head0_col[r];
   for (int h = 1; h < 4; ++h) ring.actions[slot * 4 + h] = actions[(int64_t)h * a.n + r];
   ring.scalars[slot * 4 + 0] = logp[r];
@@ -96,6 +88,31 @@ k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
   ring.scalars[slot * 4 + 3] = tdv;
   ring.move_bits[slot] = move_bits[r];
   ring.shift_bits[slot] = shift_bits[r];
+}
+
+// replay feature rows (X, X') of the surviving pushes: one warp per row,
+// lanes over features (coalesced), 32-bit index math
+__global__ void __launch_bounds__(256)
+k_ring_rows(int64_t n, int64_t keep_from, int32_t F, int64_t wpos_arg,
+            const int64_t* wpos_dev, const double* __restrict__ feat,
+            const double* __restrict__ feat_new,
+            const __grid_constant__ harl_replay_ring ring) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpos = wpos_dev ? *wpos_dev : wpos_arg;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = keep_from + (int64_t)blockIdx.x * (blockDim.x >> 5) +
+                   (threadIdx.x >> 5);
+       r < n; r += warps) {
+    const int64_t slot = (wpos + r) % ring.cap;
+    const double* x = feat + r * F;
+    const double* xn = feat_new + r * F;
+    double* dx = ring.X + slot * F;
+    double* dxn = ring.Xn + slot * F;
+    for (int k = lane; k < F; k += 32) {
+      dx[k] = x[k];
+      dxn[k] = xn[k];
+    }
+  }
 }
 
 // Survivor compaction: dst row i <- src row idx[i] for the population state

@@ -4,7 +4,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "gbt_kernels.cuh"
@@ -30,6 +33,74 @@ void set_error(const char* fmt, ...) {
 int cuda_status(cudaError_t e, const char* where) {
   set_error("%s: %s", where, cudaGetErrorString(e));
   return HARL_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// launch counter and per-kernel timer.  The timer puts a short spin kernel
+// in front of the timed launch so the GPU is still busy when the host
+// enqueues (begin event, kernel, end event): the begin timestamp is then the
+// kernel's start, not the moment an idle stream saw the event.
+
+__global__ void k_spin(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+struct ProfRec {
+  const char* name;
+  cudaEvent_t e0, e1;
+};
+
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static unsigned long long g_spin_ns = 20000;
+static std::vector<cudaEvent_t> g_ev_pool;
+static std::vector<ProfRec> g_prof_recs;
+static size_t g_ev_used = 0;
+static thread_local cudaEvent_t t_pending = nullptr;
+static thread_local cudaStream_t t_pending_st = nullptr;
+static std::atomic<long long> g_launches{0};
+static const size_t PROF_MAX_EVENTS = 1 << 16;
+
+static cudaEvent_t prof_event() {
+  if (g_ev_used == g_ev_pool.size()) {
+    if (g_ev_pool.size() >= PROF_MAX_EVENTS) return nullptr;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    g_ev_pool.push_back(e);
+  }
+  return g_ev_pool[g_ev_used++];
+}
+
+void prof_begin(cudaStream_t st) {
+  t_pending = nullptr;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_prof_on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess ||
+      cs != cudaStreamCaptureStatusNone)
+    return;
+  cudaEvent_t e = prof_event();
+  if (!e) return;
+  k_spin<<<1, 32, 0, st>>>(g_spin_ns);
+  cudaEventRecord(e, st);
+  t_pending = e;
+  t_pending_st = st;
+}
+
+void prof_end(const char* where) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!t_pending) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t e1 = prof_event();
+  if (e1) {
+    cudaEventRecord(e1, t_pending_st);
+    g_prof_recs.push_back({where, t_pending, e1});
+  }
+  t_pending = nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -101,6 +172,14 @@ static int allow_smem(K kernel, size_t bytes, const char* name) {
     have[slot] = bytes;
   }
   return HARL_OK;
+}
+
+template <typename K>
+static int allow_max_smem(K kernel, const char* name) {
+  cudaFuncAttributes at;
+  cudaError_t e = cudaFuncGetAttributes(&at, kernel);
+  if (e != cudaSuccess) return cuda_status(e, name);
+  return allow_smem(kernel, (size_t)max_dyn_smem() - at.sharedSizeBytes, name);
 }
 
 static int check_sketch(const harl_sketch_desc* sk) {
@@ -192,6 +271,7 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
     if (e != cudaSuccess) return cuda_status(e, "init memcpy");
     const int64_t todo = count - a.t0;
     const int threads = 256;
+    HARL_PROF_BEGIN(st);
     k_init_sample<<<(unsigned)((todo + threads - 1) / threads), threads, 0, st>>>(
         *sk, J, a, tiles, knobs, bad);
     HARL_CHECK_LAUNCH("k_init_sample");
@@ -207,6 +287,7 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
     // tracks [t0, first) are exact; redo `first` sequentially
     InitArgs one = a;
     one.j0 = a.j0 + (uint64_t)(first - a.t0) * (uint64_t)a.per_track;
+    HARL_PROF_BEGIN(st);
     k_init_one<<<1, 1, 0, st>>>(*sk, J, one, (int64_t)first, tiles, knobs, used);
     HARL_CHECK_LAUNCH("k_init_one");
     unsigned long long u = 0;
@@ -220,6 +301,86 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
   return HARL_OK;
 }
 
+int64_t harl_uniform_scratch_bytes(int64_t n) {
+  return 4 * n * 4 + 4 * n * 8 + 64;
+}
+
+int harl_uniform_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
+                         const uint8_t* knobs, int64_t n, int64_t ld,
+                         const harl_pcg64* rng, int32_t* actions,
+                         void* scratch, int64_t* u32_used_host, void* stream) {
+  int rc = check_sketch(sk);
+  if (rc) return rc;
+  if (!rng || !scratch || !u32_used_host || n < 0) {
+    set_error("harl_uniform_actions: bad arguments");
+    return HARL_E_ARG;
+  }
+  *u32_used_host = 0;
+  if (n == 0) return HARL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* count = (int32_t*)scratch;
+  int64_t* offset = (int64_t*)((char*)scratch + 4 * n * 4);
+  unsigned long long* misc = (unsigned long long*)(offset + 4 * n);
+  HARL_PROF_BEGIN(st);
+  k_uniform_counts<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(*sk, tiles, knobs,
+                                                                n, ld, count);
+  HARL_CHECK_LAUNCH("k_uniform_counts");
+  HARL_PROF_BEGIN(st);
+  k_uniform_scan<<<1, 1024, 0, st>>>(count, 4 * n, offset, (int64_t*)&misc[1]);
+  HARL_CHECK_LAUNCH("k_uniform_scan");
+  PcgJump J;
+  build_jump(*rng, &J);
+  UniformArgs a;
+  memset(&a, 0, sizeof(a));
+  a.n = n;
+  a.ld = ld;
+  a.s = state_of(*rng);
+  a.has32 = rng->has_uint32;
+  a.buffered = rng->uinteger;
+  auto d2h = [&](const void* src, void* dst, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+    return e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+  };
+  int64_t total_words = 0;
+  cudaError_t e = d2h(&misc[1], &total_words, 8);
+  if (e != cudaSuccess) return cuda_status(e, "uniform total");
+  int64_t i0 = 0;
+  uint64_t j0 = 0;  // word index of element i0's draw
+  int64_t off_i0 = 0;
+  for (;;) {
+    const unsigned long long init = ULLONG_MAX;
+    e = cudaMemcpyAsync(misc, &init, 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "uniform memcpy");
+    const int64_t todo = 4 * n - i0;
+    HARL_PROF_BEGIN(st);
+    k_uniform_draw<<<(unsigned)((todo + 127) / 128), 128, 0, st>>>(
+        *sk, J, a, i0, j0, tiles, knobs, count, offset, actions, misc);
+    HARL_CHECK_LAUNCH("k_uniform_draw");
+    unsigned long long bad = 0;
+    if ((e = d2h(misc, &bad, 8)) != cudaSuccess) return cuda_status(e, "uniform sync");
+    if (bad == ULLONG_MAX) {
+      *u32_used_host = (int64_t)j0 + (total_words - off_i0);
+      return HARL_OK;
+    }
+    int64_t off_b = 0;
+    if ((e = d2h(&offset[bad], &off_b, 8)) != cudaSuccess) return cuda_status(e, "uniform sync");
+    const uint64_t jb = j0 + (uint64_t)(off_b - off_i0);
+    HARL_PROF_BEGIN(st);
+    k_uniform_one<<<1, 1, 0, st>>>(*sk, J, a, (int64_t)bad, jb, tiles, knobs,
+                                   count, actions, &misc[2]);
+    HARL_CHECK_LAUNCH("k_uniform_one");
+    unsigned long long used = 0;
+    if ((e = d2h(&misc[2], &used, 8)) != cudaSuccess) return cuda_status(e, "uniform sync");
+    i0 = (int64_t)bad + 1;
+    j0 = jb + used;
+    if (i0 >= 4 * n) {
+      *u32_used_host = (int64_t)j0;
+      return HARL_OK;
+    }
+    if ((e = d2h(&offset[i0], &off_i0, 8)) != cudaSuccess) return cuda_status(e, "uniform sync");
+  }
+}
+
 int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
                    const uint8_t* knobs, int64_t n, int64_t ld, double* feat,
                    void* stream) {
@@ -228,6 +389,7 @@ int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
   if (n <= 0) return HARL_OK;
   const size_t smem = sizeof(double) * FEAT_THREADS * sk->feature_len;
   if ((rc = allow_smem(k_featurize, smem, "k_featurize"))) return rc;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_featurize<<<(unsigned)((n + FEAT_THREADS - 1) / FEAT_THREADS), FEAT_THREADS,
                 smem, (cudaStream_t)stream>>>(*sk, tiles, knobs, n, ld, feat);
   HARL_CHECK_LAUNCH("k_featurize");
@@ -240,6 +402,7 @@ int harl_action_masks(const harl_sketch_desc* sk, const uint16_t* tiles,
   int rc = check_sketch(sk);
   if (rc) return rc;
   if (n <= 0) return HARL_OK;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_action_masks<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       *sk, tiles, knobs, n, ld, tiling, shift);
   HARL_CHECK_LAUNCH("k_action_masks");
@@ -253,6 +416,7 @@ int harl_apply_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
   int rc = check_sketch(sk);
   if (rc) return rc;
   if (n <= 0) return HARL_OK;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_apply_actions<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       *sk, tiles, knobs, n, ld, actions, tiles_out, knobs_out,
       (unsigned long long*)status);
@@ -274,6 +438,7 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
   const size_t smem = sizeof(double) * (size_t)rows * T;
   int rc = allow_smem(k_gbt_predict, smem, "k_gbt_predict");
   if (rc) return rc;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_gbt_predict<<<(unsigned)((n + rows - 1) / rows), GBT_THREADS, smem,
                   (cudaStream_t)stream>>>(
       (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
@@ -290,7 +455,8 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                      int32_t* actions, double* logp, uint16_t* tiles_out,
                      uint8_t* knobs_out, uint64_t* move_bits,
                      uint32_t* shift_bits, int32_t* head0_col,
-                     float* logits_out, uint64_t* status, void* stream) {
+                     float* logits_out, uint64_t* status,
+                     const int32_t* grow, int64_t m_total, void* stream) {
   int rc = check_sketch(sk);
   if (rc) return rc;
   if ((rc = check_mlp(pol, true))) return rc;
@@ -316,6 +482,9 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     build_jump(*rng, &J);
     sr.s = state_of(*rng);
   }
+  sr.grow = grow;
+  sr.m_total = m_total;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_policy_step<<<(unsigned)((n + MLP_TM - 1) / MLP_TM), MLP_THREADS, smem,
                   (cudaStream_t)stream>>>(*sk, *pol, J, sr, feat, tiles, knobs, n,
                                           ld, inject, actions, logp, tiles_out,
@@ -338,7 +507,8 @@ static void build_lane_jump(const harl_pcg64& g, LaneJump* LJ) {
 }
 
 static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
-                          const uint64_t* rng_state_dev,
+                          const uint64_t* rng_state_dev, const int32_t* grow,
+                          int64_t m_total,
                           const float* logits, int ldz, int64_t n, int64_t ld,
                           const uint16_t* tiles, const uint8_t* knobs,
                           const int32_t* inject, int32_t* actions, double* logp,
@@ -371,7 +541,11 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   a.shift_bits = shift_bits;
   a.head0_col = head0_col;
   a.status = (unsigned long long*)status;
-  k_sample_rows<<<(unsigned)((n + SAMPLE_THREADS - 1) / SAMPLE_THREADS),
+  a.grow = grow;
+  a.m_total = m_total > 0 ? m_total : n;
+  const int rows_per_cta = SAMPLE_THREADS / SG;
+  HARL_PROF_BEGIN(st);
+  k_sample_rows<<<(unsigned)((n + rows_per_cta - 1) / rows_per_cta),
                   SAMPLE_THREADS, 0, st>>>(*sk, J, LJ, base,
                                            (const u128*)rng_state_dev, tiles,
                                            knobs, a);
@@ -404,7 +578,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* logits_out, uint64_t* status,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
-                        void* stream) {
+                        const int32_t* grow, int64_t m_total, void* stream) {
   int rc = check_sketch(sk);
   if (rc) return rc;
   if ((rc = check_mlp(pol, true))) return rc;
@@ -435,6 +609,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   ta.packed = packed_trunk;
   const int64_t tiles_n = (n + 127) / 128;
   const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+  HARL_PROF_BEGIN(st);
   k_trunk_tc<TRUNK_POLICY><<<grid, 128, TRUNK_SMEM, st>>>(ta);
   HARL_CHECK_LAUNCH("k_trunk_tc<policy>");
   HeadsArgs ha;
@@ -448,9 +623,11 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   ha.NHP = (ha.NH + 15) / 16 * 16;
   const size_t smem = (size_t)2 * ha.NHP * TC_H * 4 + HEADS_NMAX * 4;
   if ((rc = allow_smem(k_heads_tc, smem, "k_heads_tc"))) return rc;
+  HARL_PROF_BEGIN(st);
   k_heads_tc<<<grid, 128, smem, st>>>(ha);
   HARL_CHECK_LAUNCH("k_heads_tc");
-  return launch_sampler(sk, rng, rng_state_dev, hid_scratch, TC_H, n, ld,
+  return launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
+                        TC_H, n, ld,
                         tiles, knobs, inject,
                         actions, logp, tiles_out, knobs_out, move_bits,
                         shift_bits, head0_col, status, st);
@@ -489,6 +666,7 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
   ta.packed = packed;
   const int64_t tiles_n = (n0 + 127) / 128 + (ta.n1 + 127) / 128;
   const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_trunk_tc<TRUNK_VALUE><<<grid, 128, TRUNK_SMEM, (cudaStream_t)stream>>>(ta);
   HARL_CHECK_LAUNCH("k_trunk_tc<value>");
   return HARL_OK;
@@ -497,16 +675,15 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
 int harl_prepare(void) {
   // raise every kernel's dynamic shared-memory limit up front so that no
   // entry point needs cudaFuncSetAttribute while a stream is being captured
-  const size_t mx = (size_t)max_dyn_smem();
   int rc = 0;
-  if ((rc = allow_smem(k_featurize, mx, "k_featurize"))) return rc;
-  if ((rc = allow_smem(k_gbt_predict, mx, "k_gbt_predict"))) return rc;
-  if ((rc = allow_smem(k_policy_step, mx, "k_policy_step"))) return rc;
-  if ((rc = allow_smem(k_value_forward, mx, "k_value_forward"))) return rc;
-  if ((rc = allow_smem(k_trunk_tc<TRUNK_POLICY>, mx, "k_trunk_tc"))) return rc;
-  if ((rc = allow_smem(k_trunk_tc<TRUNK_VALUE>, mx, "k_trunk_tc"))) return rc;
-  if ((rc = allow_smem(k_heads_tc, mx, "k_heads_tc"))) return rc;
-  if ((rc = allow_smem(k_ppo_rows, mx, "k_ppo_rows"))) return rc;
+  if ((rc = allow_max_smem(k_featurize, "k_featurize"))) return rc;
+  if ((rc = allow_max_smem(k_gbt_predict, "k_gbt_predict"))) return rc;
+  if ((rc = allow_max_smem(k_policy_step, "k_policy_step"))) return rc;
+  if ((rc = allow_max_smem(k_value_forward, "k_value_forward"))) return rc;
+  if ((rc = allow_max_smem(k_trunk_tc<TRUNK_POLICY>, "k_trunk_tc"))) return rc;
+  if ((rc = allow_max_smem(k_trunk_tc<TRUNK_VALUE>, "k_trunk_tc"))) return rc;
+  if ((rc = allow_max_smem(k_heads_tc, "k_heads_tc"))) return rc;
+  if ((rc = allow_max_smem(k_ppo_rows, "k_ppo_rows"))) return rc;
   (void)sm_count();
   return HARL_OK;
 }
@@ -532,6 +709,7 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     ta.b1 = pol->b[0];
     ta.W2 = pol->W[1];
     ta.b2 = pol->b[1];
+    HARL_PROF_BEGIN(st);
     k_pack_trunk<<<64, 256, 0, st>>>(ta, (uint8_t*)pol_trunk, 0);
     HARL_CHECK_LAUNCH("k_pack_trunk<policy>");
     HeadsArgs ha;
@@ -540,6 +718,7 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     ha.bh = pol->head_b;
     ha.NH = pol->n_head_cols;
     ha.NHP = (ha.NH + 15) / 16 * 16;
+    HARL_PROF_BEGIN(st);
     k_pack_heads<<<64, 256, 0, st>>>(ha, (uint8_t*)pol_heads);
     HARL_CHECK_LAUNCH("k_pack_heads");
   }
@@ -557,6 +736,7 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     ta.b2 = val->b[1];
     ta.w3 = val->W[2];
     ta.b3 = val->b[2];
+    HARL_PROF_BEGIN(st);
     k_pack_trunk<<<64, 256, 0, st>>>(ta, (uint8_t*)val_trunk, 1);
     HARL_CHECK_LAUNCH("k_pack_trunk<value>");
   }
@@ -578,6 +758,7 @@ int harl_value_forward(const harl_mlp_desc* val, const double* feat, int64_t n,
   ldbuf += 1;
   const size_t smem = sizeof(float) * 2 * MLP_TM * (size_t)ldbuf;
   if ((rc = allow_smem(k_value_forward, smem, "k_value_forward"))) return rc;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_value_forward<<<(unsigned)((n + MLP_TM - 1) / MLP_TM), MLP_THREADS, smem,
                     (cudaStream_t)stream>>>(*val, feat, n, feature_len, v_out, ldbuf);
   HARL_CHECK_LAUNCH("k_value_forward");
@@ -610,9 +791,18 @@ int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
   memset(&rg, 0, sizeof(rg));
   if (ring) rg = *ring;
   if (rg.cap < 1) rg.cap = 1;
-  k_finish_step<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+  HARL_PROF_BEGIN((cudaStream_t)stream);
+  k_finish_step<<<(unsigned)((n + 63) / 64), 64, 0, (cudaStream_t)stream>>>(
       a, *io, rg, *log, *ts, wpos_dev);
   HARL_CHECK_LAUNCH("k_finish_step");
+  if (rl && n > keep_from) {
+    const int64_t rows = n - keep_from;
+    const int64_t blocks = (rows + 7) / 8 < 2 * 148 ? (rows + 7) / 8 : 2 * 148;
+    HARL_PROF_BEGIN((cudaStream_t)stream);
+    k_ring_rows<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        n, keep_from, feature_len, wpos, wpos_dev, io->feat, io->feat_new, rg);
+    HARL_CHECK_LAUNCH("k_ring_rows");
+  }
   return HARL_OK;
 }
 
@@ -630,6 +820,7 @@ int harl_gather_rows(const int32_t* idx, int64_t n_out, int32_t local_slots,
   a.ld_dst = ld_dst;
   a.local_slots = local_slots;
   a.F = feature_len;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_gather_rows<<<(unsigned)((n_out + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       a, idx, tiles, knobs, feat, score, row_track, tiles_o, knobs_o, feat_o,
       score_o, row_track_o);
@@ -671,6 +862,7 @@ int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
   const size_t smem = (PROBE_N + PROBE_M) * PROBE_K * 4 + 1024;
   int rc = allow_smem(k_tc_probe, smem, "k_tc_probe");
   if (rc) return rc;
+  HARL_PROF_BEGIN((cudaStream_t)stream);
   k_tc_probe<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, D, mode);
   HARL_CHECK_LAUNCH("k_tc_probe");
   return HARL_OK;
@@ -690,8 +882,12 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     double* adam_m, double* adam_v, float* params32,
                     int64_t n_pi, int64_t n_params, double* losses,
                     int32_t* bad, void* scratch, const double* adam_dev,
+                    void* pol_trunk_img, void* pol_heads_img,
+                    void* val_trunk_img, int32_t B_norm, int32_t phase,
                     void* stream) {
-  if (!pol || !val || !hp || !ring || !idx || B < 1 || n_head0 < 1 ||
+  if (B_norm <= 0) B_norm = B;
+  if (phase < 1 || phase > 3) phase = 3;
+  if (!pol || !val || !hp || !ring || B < 0 || n_head0 < 1 ||
       n_head0 > HARL_MAX_HEAD0 || pol->n_layers < 1 ||
       pol->n_layers > HARL_MAX_LAYERS || val->n_layers < 2 ||
       val->n_layers > HARL_MAX_LAYERS) {
@@ -715,6 +911,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   a.F = feature_len;
   a.C0 = n_head0;
   a.row_stride = row_stride;
+  a.B_norm = B_norm;
   a.clip_lo = 1.0 - hp->clip_ratio;
   a.clip_hi = 1.0 + hp->clip_ratio;
   a.w_ent = hp->entropy_weight;
@@ -726,29 +923,120 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   wmax = wmax > pol->n_head_cols ? wmax : pol->n_head_cols;
   const size_t rsmem = sizeof(double) * (PPO_TM * (size_t)row_stride + 8);
   (void)wmax;
+  if (phase & 1) {
   int rc2 = allow_smem(k_ppo_rows, rsmem, "k_ppo_rows");
   if (rc2) return rc2;
-  k_ppo_rows<<<(unsigned)((B + PPO_TM - 1) / PPO_TM), PPO_THREADS, rsmem, st>>>(
-      a, *pol, *val, *ring, idx, params, rows, rowout);
-  HARL_CHECK_LAUNCH("k_ppo_rows");
-  k_ppo_losses<<<1, 32, 0, st>>>(B, hp->entropy_weight, hp->value_loss_weight,
-                                 rowout, losses, bad);
+  if (B > 0) {
+    HARL_PROF_BEGIN(st);
+    k_ppo_rows<<<(unsigned)((B + PPO_TM - 1) / PPO_TM), PPO_THREADS, rsmem, st>>>(
+        a, *pol, *val, *ring, idx, params, rows, rowout);
+    HARL_CHECK_LAUNCH("k_ppo_rows");
+  }
+  HARL_PROF_BEGIN(st);
+  k_ppo_losses<<<1, 32, 0, st>>>(B, rowout, losses);
   HARL_CHECK_LAUNCH("k_ppo_losses");
   GradJobs jt;
   memset(&jt, 0, sizeof(jt));
   for (int j = 0; j < n_jobs; ++j) jt.j[j] = jobs[j];
   jt.n = n_jobs;
+  HARL_PROF_BEGIN(st);
   k_ppo_wgrad<<<(unsigned)n_tiles, 256, 0, st>>>(jt, B, row_stride, rows, grads,
                                                  bad);
   HARL_CHECK_LAUNCH("k_ppo_wgrad");
+  }
+  if (!(phase & 2)) return HARL_OK;
+  HARL_PROF_BEGIN(st);
+  k_ppo_finalize<<<148, 256, 0, st>>>(B_norm, hp->entropy_weight,
+                                      hp->value_loss_weight, losses, grads,
+                                      n_params, bad);
+  HARL_CHECK_LAUNCH("k_ppo_finalize");
+  HARL_CHECK_LAUNCH("k_ppo_wgrad");
   AdamArgs ad;
+  memset(&ad, 0, sizeof(ad));
   ad.n_pi = n_pi;
   ad.n = n_params;
   ad.h = *hp;
+  // images as built by k_pack_trunk / k_pack_heads (mlp_tc.cuh)
+  auto add_trunk = [&](const harl_net_layout& L, uint8_t* img, bool value) {
+    const int H = TC_H;
+    float* w1h = (float*)img;
+    float* w1l = w1h + TC_K1 * H;
+    float* w2h = w1l + TC_K1 * H;
+    float* w2l = w2h + H * H;
+    float* bb = w2l + H * H;
+    ad.pk.mat[ad.pk.n_mat++] = {L.off_W[0], L.dims[0], H, TC_K1, w1h, w1l};
+    ad.pk.mat[ad.pk.n_mat++] = {L.off_W[1], H, H, H, w2h, w2l};
+    ad.pk.vec[ad.pk.n_vec++] = {L.off_b[0], H, bb};
+    ad.pk.vec[ad.pk.n_vec++] = {L.off_b[1], H, bb + H};
+    if (value) ad.pk.vec[ad.pk.n_vec++] = {L.off_W[2], H, bb + 2 * H};
+  };
+  if (pol_trunk_img && pol_heads_img) {
+    add_trunk(*pol, (uint8_t*)pol_trunk_img, false);
+    const int NHP = (pol->n_head_cols + 15) / 16 * 16;
+    float* whh = (float*)pol_heads_img;
+    float* whl = whh + NHP * TC_H;
+    ad.pk.mat[ad.pk.n_mat++] = {pol->off_hW, TC_H, pol->n_head_cols, TC_H,
+                                whh, whl};
+    ad.pk.vec[ad.pk.n_vec++] = {pol->off_hb, pol->n_head_cols, whl + NHP * TC_H};
+  }
+  if (val_trunk_img) add_trunk(*val, (uint8_t*)val_trunk_img, true);
+  HARL_PROF_BEGIN(st);
   k_ppo_adam<<<296, 256, 0, st>>>(ad, adam_dev, bad, grads, params, adam_m,
                                    adam_v, params32);
   HARL_CHECK_LAUNCH("k_ppo_adam");
   return HARL_OK;
+}
+
+// -- launch counter / per-kernel timer ----------------------------------------
+
+long long harl_launch_count(void) { return g_launches.load(); }
+
+int harl_profile_set(int on, long long spin_ns) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  if (spin_ns >= 0) g_spin_ns = (unsigned long long)spin_ns;
+  return HARL_OK;
+}
+
+int harl_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_recs.clear();
+  g_ev_used = 0;
+  return HARL_OK;
+}
+
+int harl_profile_read(int max_kernels, char* names, int name_cap,
+                      double* total_ms, long long* launches) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::vector<std::string> keys;
+  std::vector<double> ms;
+  std::vector<long long> cnt;
+  for (const ProfRec& r : g_prof_recs) {
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    if (e != cudaSuccess) return cuda_status(e, "harl_profile_read");
+    float t = 0.f;
+    e = cudaEventElapsedTime(&t, r.e0, r.e1);
+    if (e != cudaSuccess) return cuda_status(e, "harl_profile_read");
+    size_t k = 0;
+    while (k < keys.size() && keys[k] != r.name) ++k;
+    if (k == keys.size()) {
+      keys.push_back(r.name);
+      ms.push_back(0.0);
+      cnt.push_back(0);
+    }
+    ms[k] += t;
+    cnt[k] += 1;
+  }
+  const int n = (int)keys.size();
+  for (int k = 0; k < n && k < max_kernels; ++k) {
+    if (names && name_cap > 0) {
+      snprintf(names + (size_t)k * name_cap, (size_t)name_cap, "%s",
+               keys[k].c_str());
+    }
+    if (total_ms) total_ms[k] = ms[k];
+    if (launches) launches[k] = cnt[k];
+  }
+  return n;
 }
 
 }  // extern "C"

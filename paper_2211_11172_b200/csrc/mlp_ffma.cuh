@@ -92,7 +92,16 @@ __device__ inline float* run_layers(const harl_mlp_desc& net, float* bufA,
 
 struct StepRng {
   u128 s;  // PCG64 state at the start of this step's random((n,1)) draws
+  const int32_t* grow;  // optional global row of each local row (shards)
+  int64_t m_total;      // rows drawn this step over all shards (0 -> n)
 };
+
+__device__ inline uint64_t draw_index(const StepRng& g, int h, int64_t n,
+                                      int64_t r) {
+  const int64_t m = g.m_total > 0 ? g.m_total : n;
+  const int64_t row = g.grow ? (int64_t)g.grow[r] : r;
+  return (uint64_t)h * (uint64_t)m + (uint64_t)row + 1;
+}
 
 __device__ inline double warp_max(double v) {
   for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -291,7 +300,7 @@ __device__ inline void policy_row(
       double lp;
       bool none;
       double u = 0.0;
-      if (!inject) u = u64_to_unit(pcg_draw64(J, rng.s, (uint64_t)r + 1));
+      if (!inject) u = u64_to_unit(pcg_draw64(J, rng.s, draw_index(rng, 0, n, r)));
       const int j = warp_sample_bits(z, C0, lb, u, &lp, &none);
       dead |= none;
       if (inject) {
@@ -339,7 +348,7 @@ __device__ inline void policy_row(
         lp = logp3(zh, m3, a);
         none = m3 == 0;
       } else {
-        const double u = u64_to_unit(pcg_draw64(J, rng.s, (uint64_t)h * n + r + 1));
+        const double u = u64_to_unit(pcg_draw64(J, rng.s, draw_index(rng, h, n, r)));
         const int j = sample3(zh, m3, u, &lp, &none);
         act[h] = (j < 0) ? 0 : j;
       }

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace harl {
 
@@ -22,6 +23,7 @@ typedef harl_net_layout NetLayout;
 
 struct PpoArgs {
   int32_t B, F, C0, row_stride;
+  int32_t B_norm;           // batch size in the 1/B normalisation (global)
   double clip_lo, clip_hi, w_ent, w_val;
   int16_t head0_src[HARL_MAX_HEAD0];
 };
@@ -150,7 +152,7 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
             l < V.n_layers - 1, nrows, wbuf);
   // per-row PPO terms, one warp per row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double invB = 1.0 / (double)a.B;
+  const double invB = 1.0 / (double)a.B_norm;
   for (int rr = warp; rr < nrows; rr += PPO_THREADS / 32) {
     const int slot = idx[r0 + rr];
     double* z = base + rr * RS + P.row_head;
@@ -251,28 +253,43 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   for (int i = threadIdx.x; i < nrows * RS; i += blockDim.x) out[i] = base[i];
 }
 
-// (b) fixed-order means; out: [0] actor loss, [1] value loss,
-// [2] policy loss, [3] entropy, [4] mean ratio.  One warp: lane l sums rows
-// l, l+32, ... in order, then a fixed xor tree (deterministic).
-__global__ void k_ppo_losses(int B, double w_ent, double w_val,
-                             const double* rowout, double* losses,
-                             int32_t* bad) {
+// (b) loss terms: lane l sums rows l, l+32, ... in order, then a fixed xor
+// tree (deterministic).  losses[5..8] = the per-row sums (min surrogate,
+// entropy, ratio, squared value error) -- the quantities a sharded update
+// all-reduces; k_ppo_finalize turns them into the reported means.
+__global__ void k_ppo_losses(int B, const double* rowout, double* losses) {
   const int lane = threadIdx.x;
   double q[4] = {0, 0, 0, 0};
   for (int r = lane; r < B; r += 32)
     for (int j = 0; j < 4; ++j) q[j] += rowout[r * 4 + j];
   for (int j = 0; j < 4; ++j) q[j] = wsum64(q[j]);
-  if (lane != 0) return;
-  const double policy_loss = -(q[0] / B);
-  const double entropy = q[1] / B;
-  const double a_loss = policy_loss - w_ent * entropy;
-  const double v_loss = w_val * (q[3] / B);
-  losses[0] = a_loss;
-  losses[1] = v_loss;
-  losses[2] = policy_loss;
-  losses[3] = entropy;
-  losses[4] = q[2] / B;
-  if (!isfinite(a_loss) || !isfinite(v_loss)) atomicOr(bad, 1);
+  if (lane == 0)
+    for (int j = 0; j < 4; ++j) losses[5 + j] = q[j];
+}
+
+// means (rlcore.py:311-312,355; [0] actor loss, [1] value loss, [2] policy
+// loss, [3] entropy, [4] mean ratio) + the finiteness checks of
+// ppo_update (rlcore.py:368-373) over the (reduced) losses and gradients
+__global__ void k_ppo_finalize(int B, double w_ent, double w_val,
+                               double* losses, const double* grads,
+                               int64_t n, int32_t* bad) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double policy_loss = -(losses[5] / B);
+    const double entropy = losses[6] / B;
+    const double a_loss = policy_loss - w_ent * entropy;
+    const double v_loss = w_val * (losses[8] / B);
+    losses[0] = a_loss;
+    losses[1] = v_loss;
+    losses[2] = policy_loss;
+    losses[3] = entropy;
+    losses[4] = losses[7] / B;
+    if (!isfinite(a_loss) || !isfinite(v_loss)) atomicOr(bad, 1);
+  }
+  int nonfinite = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    nonfinite |= !isfinite(grads[i]);
+  if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(bad, 2);
 }
 
 // (c) gradient jobs: grad[off + i*nj + j] = sum_r A[r][ai + i] * D[r][dj + j]
@@ -331,23 +348,40 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
     }
     __syncthreads();
   }
-  int nonfinite = 0;
+  (void)bad;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int i = i0 + ti + 8 * q, j = j0 + tj;
-    if (i < ni && j < jb.nj) {
-      grads[jb.g_off + (int64_t)i * jb.nj + j] = acc[q];
-      if (!isfinite(acc[q])) nonfinite = 1;
-    }
+    if (i < ni && j < jb.nj) grads[jb.g_off + (int64_t)i * jb.nj + j] = acc[q];
   }
-  if (nonfinite) atomicOr(bad, 2);
 }
 
 // (d) Adam over [0, n_pi) with the policy optimizer and [n_pi, n) with the
 // value optimizer.  Scalars precomputed on the host exactly as numpy does.
+// Where the updated fp32 weights also live in the tcgen05 weight images
+// (tf32 hi/lo, K-major core layout; biases as plain floats), so the Adam
+// pass refreshes the images directly instead of a separate re-pack.
+struct PackMat {
+  int64_t off;
+  int32_t K, N, Kpad;
+  float* hi;
+  float* lo;
+};
+struct PackVec {
+  int64_t off;
+  int32_t len;
+  float* dst;
+};
+struct PackPlan {
+  PackMat mat[6];
+  PackVec vec[6];
+  int32_t n_mat, n_vec;
+};
+
 struct AdamArgs {
   int64_t n_pi, n;
   harl_ppo_hyper h;
+  PackPlan pk;
 };
 
 __global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* bad,
@@ -377,7 +411,25 @@ __global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* ba
     const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, b2t)), a.h.eps);
     const double p = __dsub_rn(params[i], __ddiv_rn(num, den));
     params[i] = p;
-    params32[i] = (float)p;
+    const float p32 = (float)p;
+    params32[i] = p32;
+    for (int q = 0; q < a.pk.n_mat; ++q) {
+      const PackMat& M = a.pk.mat[q];
+      const int64_t e = i - M.off;
+      if (e >= 0 && e < (int64_t)M.K * M.N) {
+        const int k = (int)(e / M.N), nn = (int)(e % M.N);
+        float hi, lo;
+        tc::split_tf32(p32, hi, lo);
+        const uint32_t o = tc::kmajor_off(nn, k, M.Kpad) / 4;
+        M.hi[o] = hi;
+        M.lo[o] = lo;
+      }
+    }
+    for (int q = 0; q < a.pk.n_vec; ++q) {
+      const PackVec& V = a.pk.vec[q];
+      const int64_t e = i - V.off;
+      if (e >= 0 && e < V.len) V.dst[e] = p32;
+    }
   }
 }
 

@@ -1,14 +1,15 @@
 // K4 epilogue as its own full-occupancy kernel: masked log-softmax per head
 // (rlcore.py:185-199), inverse-CDF sampling on the numpy PCG64 stream
 // (rlcore.py:202-213, select_actions 216-228) and decode + apply
-// (schedspace.py:196-301), ONE THREAD PER ROW.  (A warp per row spends
-// ~50x more issue slots on the same work: the heads are short and
-// sequential.)
+// (schedspace.py:196-301).  A group of 8 lanes per row: the head-0
+// columns are spread over the group (max / sum / inclusive CDF scan with
+// 3-step shuffles), lanes 0-3 draw the four heads' uniforms in parallel
+// (one PCG64 jump each), lanes 0-2 sample the 3-way shift heads, and the
+// walker writes 8 slots per lane.  (Thread-per-row is latency-bound at
+// 16 K rows; warp-per-row wastes ~4x the issue slots.)
 //
-// Uniforms: draw #(h*n + r + 1) after the step's base state.  Each warp
-// jumps once from the base state to its first row (warp-uniform), then
-// every lane applies its precomputed lane offset (A^l, C_l) -- one 128-bit
-// multiply-add per lane instead of a full jump per lane.
+// Uniforms: draw #(h*m + row + 1) after the step's base state, row = the
+// global row (shards) or the local row.
 #pragma once
 
 #include "common.cuh"
@@ -16,12 +17,14 @@
 
 namespace harl {
 
-constexpr int SAMPLE_THREADS = 128;
-
 struct LaneJump {
   u128 A[32];
   u128 C[32];
 };
+
+constexpr int SG = 8;                  // lanes cooperating on one row
+constexpr int SAMPLE_THREADS = 128;    // 16 rows per CTA
+constexpr int SAMPLE_MAXI = 16;        // cached exps per lane (C0 <= 128)
 
 struct SampleArgs {
   const float* logits;   // [n][ldz] (head0 compact columns, then 3x3)
@@ -36,36 +39,27 @@ struct SampleArgs {
   uint32_t* shift_bits;
   int32_t* head0_col;
   unsigned long long* status;
+  const int32_t* grow;   // optional: global row of each local row (shards)
+  int64_t m_total;       // rows drawn this step over all shards
 };
 
-// masked log-softmax + inverse CDF over C columns of one row (one thread);
-// exp in fp32 (the logits are fp32), sums/cumsum in fp64.  Walk-back over
-// zero-probability cells as in the reference; returns -1 when the walk ends
-// on an illegal column 0.
-template <typename Legal>
-__device__ inline int row_sample(const float* z, int C, Legal legal, double u,
-                                 double* logp_out, bool* none) {
-  float zmax = -INFINITY;
-  for (int j = 0; j < C; ++j)
-    if (legal(j)) zmax = fmaxf(zmax, z[j]);
-  *none = (zmax == -INFINITY);
-  double s = 0.0;
-  for (int j = 0; j < C; ++j)
-    if (legal(j)) s += (double)expf(z[j] - zmax);
-  const double inv = 1.0 / s;
-  int count = 0;
-  double c = 0.0;
-  for (int j = 0; j < C; ++j) {
-    if (legal(j)) c += (double)expf(z[j] - zmax) * inv;
-    count += (c < u);
-  }
-  int idx = min(count, C - 1);
-  while (idx > 0 && !legal(idx)) --idx;
-  const bool ok = legal(idx);
-  *logp_out = ok ? ((double)z[idx] - (double)zmax - log(s)) : -INFINITY;
-  return ok ? idx : -1;
+__device__ inline float gmaxf(float v) {
+#pragma unroll
+  for (int o = SG / 2; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o, SG));
+  return v;
+}
+__device__ inline double gsum(double v) {
+#pragma unroll
+  for (int o = SG / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, SG);
+  return v;
+}
+__device__ inline int gsumi(int v) {
+#pragma unroll
+  for (int o = SG / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, SG);
+  return v;
 }
 
+// one thread's masked log-softmax logp of column a (inject mode only)
 template <typename Legal>
 __device__ inline double row_logp(const float* z, int C, Legal legal, int a) {
   if (a < 0 || a >= C || !legal(a)) return -INFINITY;
@@ -78,6 +72,30 @@ __device__ inline double row_logp(const float* z, int C, Legal legal, int a) {
   return (double)z[a] - (double)zmax - log(s);
 }
 
+// 3-column shift head, sequential in one thread (the reference's cumsum)
+__device__ inline int sample3(const float* z, uint32_t m3, double u,
+                              double* logp_out) {
+  float zmax = -INFINITY;
+  for (int j = 0; j < 3; ++j)
+    if ((m3 >> j) & 1u) zmax = fmaxf(zmax, z[j]);
+  double e[3], s = 0.0;
+  for (int j = 0; j < 3; ++j) {
+    e[j] = ((m3 >> j) & 1u) ? (double)expf(z[j] - zmax) : 0.0;
+    s += e[j];
+  }
+  int count = 0;
+  double c = 0.0;
+  for (int j = 0; j < 3; ++j) {
+    c += e[j] / s;
+    count += (c < u);
+  }
+  int idx = min(count, 2);
+  while (idx > 0 && !((m3 >> idx) & 1u)) --idx;
+  const bool ok = (m3 >> idx) & 1u;
+  *logp_out = ok ? ((double)z[idx] - (double)zmax - log(s)) : -INFINITY;
+  return ok ? idx : -1;
+}
+
 __global__ void __launch_bounds__(SAMPLE_THREADS)
 k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ PcgJump J,
@@ -85,98 +103,205 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const u128* base_dev, const uint16_t* __restrict__ tiles,
               const uint8_t* __restrict__ knobs, SampleArgs a) {
   __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
-  __shared__ u128 s_la[32], s_lc[32];
   for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
     s_src[i] = sk.head0_src[i];
     s_dst[i] = sk.head0_dst[i];
   }
-  if (threadIdx.x < 32) {
-    s_la[threadIdx.x] = LJ.A[threadIdx.x];
-    s_lc[threadIdx.x] = LJ.C[threadIdx.x];
-  }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t r_lane0 = r - lane;
-  if (r_lane0 >= a.n) return;  // whole warp out of range
-  // uniforms for the 4 heads (computed by every lane of a live warp); the
-  // step's base state comes from device memory in graph-replay mode
-  const u128 base = base_dev ? *base_dev : base_arg;
-  double u[4] = {0, 0, 0, 0};
-  if (!a.inject) {
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const u128 w = pcg_advance(J, base, (uint64_t)h * a.n + r_lane0 + 1);
-      const u128 s = add128(mul128(s_la[lane], w), s_lc[lane]);
-      u[h] = u64_to_unit(pcg_output(s));
-    }
+  (void)LJ;
+  const int g = threadIdx.x & (SG - 1);
+  const int64_t r = (int64_t)blockIdx.x * (SAMPLE_THREADS / SG) + threadIdx.x / SG;
+  // every group stays in the shuffles; out-of-range rows compute on row 0
+  const bool live = r < a.n;
+  const int64_t rr = live ? r : 0;
+  const int S = sk.num_slots, C0 = sk.n_head0;
+  // ---- uniforms: lane h of the group draws head h ---------------------
+  double u_mine = 0.0;
+  if (!a.inject && g < 4) {
+    const u128 base = base_dev ? *base_dev : base_arg;
+    const int64_t row = a.grow ? (int64_t)a.grow[rr] : rr;
+    const uint64_t k = (uint64_t)g * (uint64_t)a.m_total + (uint64_t)row + 1;
+    u_mine = u64_to_unit(pcg_draw64(J, base, k));
   }
-  if (r >= a.n) return;
-  const int S = sk.num_slots, L = sk.levels, C0 = sk.n_head0;
-  // current state
+  // ---- current state: lane g holds slots g, g+8, ... --------------------
   uint64_t mv = 0;
-  for (int s = 0; s < sk.local_slots; ++s)
-    if (tiles[(int64_t)s * a.ld + r] > 1) mv |= 1ull << s;
-  const int ca0 = knobs[r], par0 = knobs[a.ld + r], ur0 = knobs[2 * a.ld + r];
+  int tv[HARL_MAX_SLOTS / SG];
+#pragma unroll
+  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i) {
+    const int s = g + SG * i;
+    tv[i] = s < sk.local_slots ? tiles[(int64_t)s * a.ld + rr] : 0;
+    if (tv[i] > 1) mv |= 1ull << s;
+  }
+#pragma unroll
+  for (int o = SG / 2; o; o >>= 1) mv |= __shfl_xor_sync(0xffffffffu, mv, o, SG);
+  const int ca0 = knobs[rr], par0 = knobs[a.ld + rr], ur0 = knobs[2 * a.ld + rr];
   const uint32_t sb = shift_bits_of(sk, ca0, par0, ur0);
-  const float* z = a.logits + r * a.ldz;
+  const float* z = a.logits + rr * a.ldz;
+  auto legal0 = [&](int j) -> bool {
+    return j == C0 - 1 || ((mv >> s_src[j]) & 1ull);
+  };
   int act[4];
   int col0 = 0;
   double lp_total = 0.0;
   bool dead = false;
-  {
-    auto legal = [&](int j) -> bool {
-      return j == C0 - 1 || ((mv >> s_src[j]) & 1ull);
-    };
-    double lp;
-    bool none = false;
-    if (a.inject) {
-      const int full = a.inject[r];
+  // ---- head 0: columns j = g + 8 i --------------------------------------
+  if (a.inject) {
+    if (g == 0) {
+      const int full = a.inject[rr];
       int jj = -1;
       if (full == S * S) jj = C0 - 1;
-      else if (full >= 0 && full < S * S) {
-        const int src = full / S, dst = full % S;
+      else if (full >= 0 && full < S * S)
         for (int c = 0; c < C0 - 1; ++c)
-          if (s_src[c] == src && s_dst[c] == dst) jj = c;
-      }
+          if (s_src[c] == full / S && s_dst[c] == full % S) jj = c;
       act[0] = full;
       col0 = jj < 0 ? 0 : jj;
-      lp = jj < 0 ? -INFINITY : row_logp(z, C0, legal, jj);
-    } else {
-      const int j = row_sample(z, C0, legal, u[0], &lp, &none);
-      act[0] = (j < 0) ? 0 : ((j == C0 - 1) ? S * S : s_src[j] * S + s_dst[j]);
-      col0 = j < 0 ? 0 : j;
+      lp_total = jj < 0 ? -INFINITY : row_logp(z, C0, legal0, jj);
+      for (int h = 1; h < 4; ++h) {
+        const uint32_t m3 = (sb >> (3 * (h - 1))) & 7u;
+        act[h] = a.inject[h * a.n + rr];
+        lp_total += row_logp(z + C0 + 3 * (h - 1), 3,
+                             [&](int j) -> bool { return (m3 >> j) & 1u; },
+                             act[h]);
+        dead |= (m3 == 0);
+      }
     }
-    dead |= none;
-    lp_total += lp;
-  }
-  for (int h = 1; h < 4; ++h) {
-    const uint32_t m3 = (sb >> (3 * (h - 1))) & 7u;
-    auto legal = [&](int j) -> bool { return (m3 >> j) & 1u; };
-    const float* zh = z + C0 + 3 * (h - 1);
-    double lp;
-    bool none = (m3 == 0);
-    if (a.inject) {
-      act[h] = a.inject[h * a.n + r];
-      lp = row_logp(zh, 3, legal, act[h]);
-    } else {
-      const int j = row_sample(zh, 3, legal, u[h], &lp, &none);
-      act[h] = (j < 0) ? 0 : j;
+  } else {
+    const double u0 = __shfl_sync(0xffffffffu, u_mine, 0, SG);
+    const int nI = (C0 + SG - 1) / SG;
+    float zmax = -INFINITY;
+    for (int i = 0; i < nI; ++i) {
+      const int j = g + SG * i;
+      if (j < C0 && legal0(j)) zmax = fmaxf(zmax, z[j]);
     }
-    dead |= none;
-    lp_total += lp;
+    zmax = gmaxf(zmax);
+    dead |= (zmax == -INFINITY);
+    float e[SAMPLE_MAXI];
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+      const int j = g + SG * i;
+      e[i] = (i < nI && j < C0 && legal0(j)) ? expf(z[j] - zmax) : 0.f;
+      s += (double)e[i];
+    }
+    for (int i = SAMPLE_MAXI; i < nI; ++i) {   // wide heads (C0 > 128)
+      const int j = g + SG * i;
+      if (j < C0 && legal0(j)) s += (double)expf(z[j] - zmax);
+    }
+    s = gsum(s);
+    const double inv = 1.0 / s;
+    int count = 0;
+    double carry = 0.0;
+    for (int i = 0; i < nI; ++i) {
+      const int j = g + SG * i;
+      float ei;
+      if (i < SAMPLE_MAXI) {
+        ei = 0.f;
+#pragma unroll
+        for (int q = 0; q < SAMPLE_MAXI; ++q) ei = (q == i) ? e[q] : ei;
+      } else {
+        ei = (j < C0 && legal0(j)) ? expf(z[j] - zmax) : 0.f;
+      }
+      double c = (double)ei * inv;
+#pragma unroll
+      for (int o = 1; o < SG; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, c, o, SG);
+        if (g >= o) c += t;
+      }
+      c += carry;
+      if (j < C0 && c < u0) ++count;
+      carry = __shfl_sync(0xffffffffu, c, SG - 1, SG);
+    }
+    count = gsumi(count);
+    int idx = min(count, C0 - 1);
+    while (idx > 0 && !legal0(idx)) --idx;
+    const bool ok = legal0(idx);
+    const double lp0 = ok ? ((double)z[idx] - (double)zmax - log(s)) : -INFINITY;
+    act[0] = !ok ? 0 : ((idx == C0 - 1) ? S * S : s_src[idx] * S + s_dst[idx]);
+    col0 = ok ? idx : 0;
+    // shift heads: lane h-1 handles head h
+    int ah = 0;
+    double lph = 0.0;
+    const int hh = g + 1;
+    const double uh = __shfl_sync(0xffffffffu, u_mine, hh < 4 ? hh : 0, SG);
+    if (hh < 4) {
+      const uint32_t m3 = (sb >> (3 * (hh - 1))) & 7u;
+      const int j = sample3(z + C0 + 3 * (hh - 1), m3, uh, &lph);
+      ah = j < 0 ? 0 : j;
+    }
+    lp_total = lp0;
+#pragma unroll
+    for (int h = 1; h < 4; ++h) {
+      act[h] = __shfl_sync(0xffffffffu, ah, h - 1, SG);
+      lp_total += __shfl_sync(0xffffffffu, lph, h - 1, SG);
+    }
+#pragma unroll
+    for (int h = 1; h < 4; ++h) dead |= (((sb >> (3 * (h - 1))) & 7u) == 0);
   }
-  for (int h = 0; h < 4; ++h) a.actions[h * a.n + r] = act[h];
-  a.logp[r] = lp_total;
-  a.move_bits[r] = mv;
-  a.shift_bits[r] = sb;
-  a.head0_col[r] = col0;
-  const int code = dead ? HARL_ST_NO_VALID
-                        : apply_row(sk, tiles, knobs, a.ld, r, act[0], act[1],
-                                    act[2], act[3], a.tiles_out, a.knobs_out,
-                                    a.ld, r);
-  report_status(a.status, r, code);
-  (void)L;
+  // inject mode: broadcast lane 0's decisions
+#pragma unroll
+  for (int h = 0; h < 4; ++h) act[h] = __shfl_sync(0xffffffffu, act[h], 0, SG);
+  col0 = __shfl_sync(0xffffffffu, col0, 0, SG);
+  lp_total = __shfl_sync(0xffffffffu, lp_total, 0, SG);
+  dead = __shfl_sync(0xffffffffu, (int)dead, 0, SG);
+  // ---- decode + apply (schedspace.py:196-210, 265-301) -----------------
+  int src = -1, dst = -1;
+  if (act[0] != S * S) {
+    src = act[0] / S;
+    dst = act[0] % S;
+  }
+  int code = dead ? HARL_ST_NO_VALID : HARL_ST_OK;
+  // factors at src/dst: shuffled unconditionally so every lane of the warp
+  // executes the same shuffles whatever its group decided
+  const int sidx = src >= 0 && src < HARL_MAX_SLOTS ? src : 0;
+  const int didx = dst >= 0 && dst < HARL_MAX_SLOTS ? dst : 0;
+  int vs = 0, vd = 0;
+#pragma unroll
+  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i) {
+    if (i == sidx / SG) vs = tv[i];
+    if (i == didx / SG) vd = tv[i];
+  }
+  const int f_src = __shfl_sync(0xffffffffu, vs, sidx % SG, SG);
+  const int f_dst = __shfl_sync(0xffffffffu, vd, didx % SG, SG);
+  int p = 1;
+  if (code == HARL_ST_OK && src >= 0) {
+    if (src >= sk.local_slots || dst >= sk.local_slots || dst < 0 ||
+        src / sk.levels != dst / sk.levels || src == dst || f_src <= 1)
+      code = HARL_ST_TILING;
+    else
+      p = sk.spf_lut[f_src];
+  }
+  const int ca = ca0 + (act[1] - 1), par = par0 + (act[2] - 1),
+            ur = ur0 + (act[3] - 1);
+  if (code == HARL_ST_OK) {
+    if (ca < 0 || ca >= sk.ncas) code = HARL_ST_COMPUTE_AT;
+    else if (par < 0 || par > sk.max_fusible) code = HARL_ST_PARALLEL;
+    else if (ur < 0 || ur >= sk.n_unroll) code = HARL_ST_UNROLL;
+  }
+  if (!live) return;
+  const bool moved = code == HARL_ST_OK && src >= 0;
+#pragma unroll
+  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i) {
+    const int s = g + SG * i;
+    if (s < sk.local_slots) {
+      int v = tv[i];
+      if (moved && s == src) v = f_src / p;
+      if (moved && s == dst) v = f_dst * p;
+      a.tiles_out[(int64_t)s * a.ld + r] = (uint16_t)v;
+    }
+  }
+  if (g == 0) {
+    if (code == HARL_ST_OK) {
+      a.knobs_out[r] = (uint8_t)ca;
+      a.knobs_out[a.ld + r] = (uint8_t)par;
+      a.knobs_out[2 * a.ld + r] = (uint8_t)ur;
+    }
+    for (int h = 0; h < 4; ++h) a.actions[h * a.n + r] = act[h];
+    a.logp[r] = lp_total;
+    a.move_bits[r] = mv;
+    a.shift_bits[r] = sb;
+    a.head0_col[r] = col0;
+    report_status(a.status, r, code);
+  }
 }
 
 }  // namespace harl

@@ -282,3 +282,154 @@ __global__ void k_apply_actions(const __grid_constant__ harl_sketch_desc sk,
 }
 
 }  // namespace harl
+
+namespace harl {
+
+// ---------------------------------------------------------------------------
+// Uniform actions for the non-RL searchers (TuningSession._uniform_actions,
+// tuner.py:341-348): for head h, row r (head-major) one
+// Generator.integers(len(valid)) -- no draw when a single choice is valid --
+// then the chosen index among the valid ones in increasing index order.
+
+__device__ inline int head0_valid_count(const harl_sketch_desc& sk, uint64_t mv) {
+  // every movable slot can move to the L-1 other slots of its dimension,
+  // plus the always-valid no-op
+  return __popcll(mv) * (sk.levels - 1) + 1;
+}
+
+struct UniformArgs {
+  int64_t n, ld;
+  u128 s;
+  int32_t has32;
+  uint32_t buffered;
+};
+
+// pass 1: per (h, r) choice count; consumes[i] = (count > 1)
+__global__ void k_uniform_counts(const __grid_constant__ harl_sketch_desc sk,
+                                 const uint16_t* tiles, const uint8_t* knobs,
+                                 int64_t n, int64_t ld, int32_t* count) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint64_t mv = movable_bits(sk, tiles, ld, r);
+  const uint32_t sb = shift_bits_of(sk, knobs[r], knobs[ld + r], knobs[2 * ld + r]);
+  count[r] = head0_valid_count(sk, mv);
+  for (int h = 1; h < 4; ++h) count[h * n + r] = __popc((sb >> (3 * (h - 1))) & 7u);
+}
+
+// single-CTA exclusive scan of (count > 1) over 4n entries -> word offsets
+__global__ void k_uniform_scan(const int32_t* count, int64_t total,
+                               int64_t* offset, int64_t* total_words) {
+  __shared__ int64_t carry;
+  __shared__ int64_t warp_sums[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = 0; base < total; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    int64_t v = (i < total && count[i] > 1) ? 1 : 0;
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += t;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int64_t before = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
+    if (i < total) offset[i] = before;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total_words = carry;
+}
+
+// value of the k-th valid tiling column (increasing full index)
+__device__ inline int head0_kth_valid(const harl_sketch_desc& sk, uint64_t mv,
+                                      int k) {
+  const int S = sk.num_slots, L = sk.levels;
+  for (int src = 0; src < sk.local_slots; ++src) {
+    if (!((mv >> src) & 1ull)) continue;
+    const int base = (src / L) * L;
+    for (int dst = base; dst < base + L; ++dst) {
+      if (dst == src) continue;
+      if (k == 0) return src * S + dst;
+      --k;
+    }
+  }
+  return S * S;  // the no-op is the last valid index
+}
+
+// pass 2: draw and decode (optimistic: no rejection before element i0)
+__global__ void k_uniform_draw(const __grid_constant__ harl_sketch_desc sk,
+                               const __grid_constant__ PcgJump J,
+                               const __grid_constant__ UniformArgs a,
+                               int64_t i0, uint64_t j0, const uint16_t* tiles,
+                               const uint8_t* knobs, const int32_t* count,
+                               const int64_t* offset, int32_t* actions,
+                               unsigned long long* first_bad) {
+  const int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 4 * a.n) return;
+  const int64_t h = i / a.n, r = i % a.n;
+  const int c = count[i];
+  uint32_t v = 0;
+  if (c > 1) {
+    const uint64_t j = j0 + (uint64_t)(offset[i] - offset[i0]);
+    if (!lemire32(pcg_word32(J, a.s, a.has32, a.buffered, j), (uint32_t)c, &v)) {
+      atomicMin(first_bad, (unsigned long long)i);
+      return;
+    }
+  }
+  if (h == 0) {
+    actions[r] = head0_kth_valid(sk, movable_bits(sk, tiles, a.ld, r), (int)v);
+  } else {
+    const uint32_t sb = shift_bits_of(sk, knobs[r], knobs[a.ld + r], knobs[2 * a.ld + r]);
+    const uint32_t m3 = (sb >> (3 * (h - 1))) & 7u;
+    int k = (int)v, col = 0;
+    for (int j = 0; j < 3; ++j)
+      if ((m3 >> j) & 1u) {
+        if (k == 0) { col = j; break; }
+        --k;
+      }
+    actions[h * a.n + r] = col;
+  }
+}
+
+// sequential repair of element i (rejection loop); words used -> *used
+__global__ void k_uniform_one(const __grid_constant__ harl_sketch_desc sk,
+                              const __grid_constant__ PcgJump J,
+                              const __grid_constant__ UniformArgs a, int64_t i,
+                              uint64_t j0, const uint16_t* tiles,
+                              const uint8_t* knobs, const int32_t* count,
+                              int32_t* actions, unsigned long long* used) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t h = i / a.n, r = i % a.n;
+  uint64_t j = j0;
+  uint32_t v = 0;
+  while (!lemire32(pcg_word32(J, a.s, a.has32, a.buffered, j++), (uint32_t)count[i], &v)) {
+  }
+  *used = j - j0;
+  if (h == 0) {
+    actions[r] = head0_kth_valid(sk, movable_bits(sk, tiles, a.ld, r), (int)v);
+  } else {
+    const uint32_t sb = shift_bits_of(sk, knobs[r], knobs[a.ld + r], knobs[2 * a.ld + r]);
+    const uint32_t m3 = (sb >> (3 * (h - 1))) & 7u;
+    int k = (int)v, col = 0;
+    for (int q = 0; q < 3; ++q)
+      if ((m3 >> q) & 1u) {
+        if (k == 0) { col = q; break; }
+        --k;
+      }
+    actions[h * a.n + r] = col;
+  }
+}
+
+}  // namespace harl

@@ -175,6 +175,25 @@ def init_population(dsk: DeviceSketch, count: int, gen: np.random.Generator,
     return tiles, knobs
 
 
+def uniform_actions(dsk: DeviceSketch, tiles, knobs, n: int, gen, out=None):
+    """TuningSession._uniform_actions (tuner.py:341-348) on device; advances
+    ``gen`` exactly.  Returns int32 [4][n] (head-major) full indices."""
+    lib = N.load()
+    if out is None:
+        out = torch.empty((4, max(n, 1)), dtype=torch.int32, device=dsk.device)
+    scratch = torch.empty(lib.harl_uniform_scratch_bytes(max(n, 1)),
+                          dtype=torch.uint8, device=dsk.device)
+    st = R.to_struct(gen)
+    used = C.c_int64(0)
+    with PF.span("uniform", n, launches=3):
+        N.check(lib.harl_uniform_actions(
+            C.byref(dsk.desc), _ptr(tiles), _ptr(knobs), n, tiles.shape[1],
+            C.byref(st), _ptr(out), _ptr(scratch), C.byref(used), _stream()),
+            "harl_uniform_actions")
+    R.skip_u32(gen, used.value)
+    return out
+
+
 def featurize(dsk: DeviceSketch, tiles, knobs, n: int, out=None):
     lib = N.load()
     F = dsk.tables.feature_len
@@ -397,7 +416,7 @@ class DeviceAgent:
         self.grads = torch.zeros_like(self.params)
         self.params32 = torch.zeros(self.n_params, dtype=torch.float32,
                                     device=dev)
-        self.losses = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.losses = torch.zeros(16, dtype=torch.float64, device=dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
         self.tc = (hidden == (128, 128) and F <= 64 and self.NH <= 128
                    and os.environ.get("HARL_KERNELS", "tc") != "ffma")
@@ -527,7 +546,8 @@ class DeviceAgent:
     # -- PPO ----------------------------------------------------------------
 
     def ppo_update(self, ring, slots, cfg, t_pi: int, t_v: int,
-                   scratch=None, losses=None, adam_dev=None):
+                   scratch=None, losses=None, adam_dev=None, B_norm=None,
+                   phase: int = 3):
         """One ppo_update on replay ``slots`` (device int32 ring slots).
         ``t_pi``/``t_v`` are the Adam step counts AFTER this update."""
         lib = N.load()
@@ -544,28 +564,30 @@ class DeviceAgent:
         hp.b1t_pi, hp.b2t_pi = 1.0 - b1 ** t_pi, 1.0 - b2 ** t_pi
         hp.b1t_v, hp.b2t_v = 1.0 - b1 ** t_v, 1.0 - b2 ** t_v
         if scratch is None:
-            nbytes = lib.harl_ppo_scratch_bytes(B, self.row_stride, 0)
+            nbytes = lib.harl_ppo_scratch_bytes(max(B, 1), self.row_stride, 0)
             scratch = torch.empty(nbytes, dtype=torch.uint8,
                                   device=self.device)
         if losses is None:
             losses = self.losses
         src = self.head0_src.ctypes.data_as(C.c_void_p)
-        with PF.span("ppo", B, launches=4):
+        with PF.span("ppo", B, launches=(3 if phase & 1 else 0) +
+                     (2 if phase & 2 else 0)):
           N.check(lib.harl_ppo_update(
             C.byref(self.pol_layout), C.byref(self.val_layout), C.byref(hp),
             C.byref(ring.desc), _ptr(slots), B, self.F, self.C0, src,
             self.row_stride, _ptr(self.params), _ptr(self.grads), _ptr(self.m),
             _ptr(self.v), _ptr(self.params32), self.n_pi, self.n_params,
             _ptr(losses), _ptr(self.bad), _ptr(scratch), _ptr(adam_dev),
-            _stream()),
+            *(([_ptr(self.packed["pt"]), _ptr(self.packed["ph"]),
+                _ptr(self.packed["vt"])]) if self.tc else [None, None, None]),
+            int(B_norm or B), phase, _stream()),
             "harl_ppo_update")
-        self.repack()
         return losses
 
 
 def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 n: int, gen=None, inject=None, out=None, want_logits=False,
-                rng_dev=None, advance=True):
+                rng_dev=None, advance=True, grow=None, m_total: int = 0):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
     Returns a dict of device tensors; ``status`` must be checked by the
@@ -607,14 +629,16 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
     if agent.tc:
         with PF.span("policy_tc", n, launches=3):
             N.check(lib.harl_policy_step_tc(
-                *args, _ptr(agent.hid_scratch(n)), rng_dev,
-                _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _stream()),
+                *args, _ptr(agent.hid_scratch(n)), _ptr(rng_dev),
+                _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _ptr(grow),
+                m_total, _stream()),
                 "harl_policy_step_tc")
     else:
         with PF.span("policy", n):
-            N.check(lib.harl_policy_step(*args, _stream()), "harl_policy_step")
+            N.check(lib.harl_policy_step(*args, _ptr(grow), m_total, _stream()),
+                    "harl_policy_step")
     if gen is not None and inject is None and advance:
-        R.skip_u64(gen, 4 * n)
+        R.skip_u64(gen, 4 * (m_total or n))
     if want_logits:
         out["logits"] = logits[:n]
     return out

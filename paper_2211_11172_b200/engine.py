@@ -25,6 +25,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -172,7 +174,7 @@ class _Buffers:
         self.n_ppo = sum(1 for s in plan if s["ppo"])
         self.status = torch.full((max(n_steps, 1),), -1, dtype=torch.int64,
                                  device=dev)
-        self.losses = torch.zeros((max(self.n_ppo, 1), 8),
+        self.losses = torch.zeros((max(self.n_ppo, 1), 16),
                                   dtype=torch.float64, device=dev)
         self.pol_out = {
             "actions": torch.empty((4, P), dtype=torch.int32, device=dev),
@@ -213,7 +215,7 @@ class EpisodeEngine:
     ``cull_override``) run the same launch sequence eagerly."""
 
     def __init__(self, agent: AgentState, rl_cfg: RlConfig, levels: int,
-                 device=None, use_graphs: bool = True):
+                 device=None, use_graphs: bool = True, shard=None):
         N.load()
         self.dev = D._dev(device)
         self.agent = agent
@@ -225,6 +227,11 @@ class EpisodeEngine:
         self._ppo_scratch = None
         self.use_graphs = use_graphs
         self._cache = {}
+        # population sharding: (world, rank, process group or None)
+        self.shard = shard
+        if shard is not None:
+            from .shard import GlobalReplayIndex
+            self._gidx = GlobalReplayIndex(rl_cfg.buffer_capacity, shard[0])
 
     # -----------------------------------------------------------------------
 
@@ -241,11 +248,13 @@ class EpisodeEngine:
         return b
 
     def _launch_step(self, b, k, step, cur, nxt, rt, used, graph_mode,
-                     gen=None, inj=None, want_logits=False):
+                     gen=None, inj=None, want_logits=False, m=None,
+                     grow=None, m_total=0, keep_from=None):
         """Issue every launch of search step k (policy+walker, featurize,
         GBT+reward, V(X)/V(X'), finish).  In graph mode the RNG base state
         and the replay write position come from the device tables."""
-        tables, m, P = b.tables, step["m"], b.P
+        tables, P = b.tables, b.P
+        m = step["m"] if m is None else m
         lib = N.load()
         out = dict(b.pol_out)
         out["tiles"], out["knobs"] = nxt["tiles"], nxt["knobs"]
@@ -254,7 +263,8 @@ class EpisodeEngine:
                             cur["knobs"], m, gen=gen, inject=inj, out=out,
                             want_logits=want_logits,
                             rng_dev=b.rng_tab[k] if graph_mode else None,
-                            advance=not graph_mode)
+                            advance=not graph_mode, grow=grow,
+                            m_total=m_total)
         D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
                       out=nxt["score"], reward=b.reward)
@@ -270,14 +280,47 @@ class EpisodeEngine:
             po["move_bits"].data_ptr(), po["shift_bits"].data_ptr(),
             b.adv.data_ptr())
         cap = self.replay.cap
-        with PF.span("finish", m):
+        keep_from = max(0, m - cap) if keep_from is None else keep_from
+        with PF.span("finish", m, launches=2 if m > keep_from else 1):
             N.check(lib.harl_finish_step(
                 io, m, P, used, tables.local_slots, tables.feature_len,
                 self.rl_cfg.discount, 1, self.replay.desc, self.replay.wpos,
-                max(0, m - cap), b.elog, b.ts,
+                keep_from, b.elog, b.ts,
                 D._ptr(b.wpos_tab[k:k + 1]) if graph_mode else None,
                 D._stream()), "harl_finish_step")
         return res
+
+    def _launch_step_uniform(self, b, k, step, cur, nxt, rt, used, gen,
+                             inj=None):
+        """Non-RL searchers (tuner.py:382-383): uniform valid actions, then
+        the same walker/featurizer/cost model; no value/replay/PPO."""
+        tables, m, P = b.tables, step["m"], b.P
+        lib = N.load()
+        acts = b.pol_out["actions"]
+        if inj is None:
+            D.uniform_actions(b.dsk, cur["tiles"], cur["knobs"], m, gen,
+                              out=acts)
+        else:
+            acts.view(-1)[:4 * m].copy_(torch.from_numpy(
+                np.ascontiguousarray(np.asarray(inj, np.int32).T).reshape(-1)))
+        with PF.span("apply", m):
+            N.check(lib.harl_apply_actions(
+                C.byref(b.dsk.desc), D._ptr(cur["tiles"]), D._ptr(cur["knobs"]),
+                m, P, D._ptr(acts), D._ptr(nxt["tiles"]), D._ptr(nxt["knobs"]),
+                D._ptr(b.status[k:k + 1]), D._stream()), "harl_apply_actions")
+        D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
+        D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
+                      out=nxt["score"], reward=b.reward)
+        io = N.StepBuffers(
+            rt.data_ptr(), nxt["tiles"].data_ptr(), nxt["knobs"].data_ptr(),
+            cur["feat"].data_ptr(), nxt["feat"].data_ptr(),
+            nxt["score"].data_ptr(), b.reward.data_ptr(), None, None, None,
+            None, None, None, None, None)
+        with PF.span("finish", m):
+            N.check(lib.harl_finish_step(
+                io, m, P, used, tables.local_slots, tables.feature_len, 0.0,
+                0, None, 0, m, b.elog, b.ts, None, D._stream()),
+                "harl_finish_step")
 
     def _launch_ppo(self, b, j, B, slots_t, t_pi, t_v, graph_mode):
         self._ensure_ppo_scratch(B)
@@ -295,13 +338,15 @@ class EpisodeEngine:
         chosen actions; ``record`` collects per-step device tensors for
         parity checks; ``cull_override(step, own_choice)`` may replace the
         eliminated track set (parity replays only)."""
-        if not cfg.rl:
-            raise NotImplementedError("non-RL searchers: uniform device "
-                                      "actions are not implemented yet")
+        if self.shard is not None:
+            return self._run_sharded(tables, forest, gen, cfg, order_counter)
         plan = schedule(cfg, len(self.replay), self.rl_cfg)
         b = self._buffers(tables, cfg, forest, plan)
+        # graphs for the production (tcgen05) path; the FFMA kernels used
+        # by small test networks take their RNG state by value
         eager = (inject is not None or record is not None or
-                 cull_override is not None or not self.use_graphs)
+                 cull_override is not None or not self.use_graphs or
+                 not self.dagent.tc or not cfg.rl)
         P = cfg.tracks
         # ---- population (outside any graph: the sampler may sync) -------
         cur, nxt = b.pop[0], b.pop[1]
@@ -352,6 +397,21 @@ class EpisodeEngine:
         for k, step in enumerate(b.plan):
             m = step["m"]
             inj = inject(step["t"]) if inject is not None else None
+            if not cfg.rl:
+                self._launch_step_uniform(b, k, step, cur, nxt, rt, used, gen,
+                                          inj)
+                if record is not None:
+                    po = b.pol_out
+                    record.append({"t": step["t"], "m": m,
+                                   "sel": rt[:m].clone(),
+                                   "actions": po["actions"].view(-1)[:4 * m]
+                                   .view(4, m).clone(),
+                                   "new_feats": nxt["feat"][:m].clone(),
+                                   "new_score": nxt["score"][:m].clone(),
+                                   "rewards": b.reward[:m].clone()})
+                cur, nxt = nxt, cur
+                used += m
+                continue
             res = self._launch_step(b, k, step, cur, nxt, rt, used, False,
                                     gen=gen, inj=inj,
                                     want_logits=record is not None)
@@ -409,6 +469,130 @@ class EpisodeEngine:
                     record[-1]["ppo_idx"] = idx
                 ppo_k += 1
         return self._result(b, cfg, order_counter, used, culls, train, alive)
+
+    # ---- population-sharded path (one rank of G) ---------------------------
+
+    def _allreduce_(self, t):
+        import torch.distributed as dist
+        group = self.shard[2]
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(t, group=group)
+        else:                                   # gloo: reduce a host copy
+            h = t.cpu()
+            dist.all_reduce(h, group=group)
+            t.copy_(h)
+
+    def _run_sharded(self, tables, forest, gen, cfg, order_counter):
+        """This rank's share of the episode: tracks i with i % G == rank
+        (shard.py).  Every rank advances the same generator; uniforms are
+        taken at the tracks' global rows; culls are decided on the
+        all-gathered advantages; PPO gradients are per-shard sums, one
+        all-reduce, then the identical Adam on every rank."""
+        import torch.distributed as dist
+        from . import rng as R
+        from .shard import ShardLayout, cull_decision
+        world, rank, group = self.shard
+        if not cfg.rl:
+            raise NotImplementedError("sharded episodes are RL-only")
+        P = cfg.tracks
+        lay = ShardLayout(P, world, rank)
+        plan = schedule(cfg, len(self._gidx), self.rl_cfg)
+        Pl = len(lay.local_ids)
+        b = self._buffers(tables, cfg, forest, plan)
+        dev = self.dev
+        if not hasattr(b, "full"):
+            b.full = self._pop(tables, P)
+            b.full_rt = torch.arange(P, dtype=torch.int32, device=dev)
+            b.grow = torch.zeros(P, dtype=torch.int32, device=dev)
+        # every rank samples the whole population (identical draws), keeps
+        # its own tracks
+        D.init_population(b.dsk, P, gen, b.full["tiles"], b.full["knobs"])
+        cur, nxt = b.pop[0], b.pop[1]
+        rt, rt_spare = b.rt[0], b.rt[1]
+        b.keep[:Pl].copy_(torch.from_numpy(lay.local_ids.astype(np.int32)))
+        self._compact(b, b.full, b.full_rt, cur, rt, Pl)
+        D.featurize(b.dsk, cur["tiles"], cur["knobs"], Pl, cur["feat"])
+        D.gbt_predict(forest, cur["feat"], Pl, out=cur["score"])
+        b.steps.zero_()
+        b.best.fill_(-math.inf)
+        b.best_step.zero_()
+        b.status.fill_(-1)
+        self.dagent.bad.zero_()
+        alive = np.ones(P, dtype=bool)
+        local_ids = lay.local_ids.copy()        # ids of the local rows
+        culls, train = [], []
+        used_local, used, ppo_k = 0, 0, 0
+        local_rows = []
+        cap = self.replay.cap
+        for k, step in enumerate(plan):
+            m = step["m"]
+            grow_all = lay.global_rows(alive, local_ids)
+            m_l = int(np.searchsorted(grow_all, m))   # local rows in sel
+            b.grow[:m_l].copy_(torch.from_numpy(grow_all[:m_l].astype(np.int32)))
+            keep_from = int(np.searchsorted(grow_all[:m_l], max(0, m - cap)))
+            self._launch_step(b, k, step, cur, nxt, rt, used_local, False,
+                              gen=gen, m=m_l, grow=b.grow, m_total=m,
+                              keep_from=keep_from)
+            self.replay.note_push(m_l)
+            local_rows.append(m_l)
+            live = np.flatnonzero(alive)
+            self._gidx.push_step(live[:m] % world)
+            cur, nxt = nxt, cur
+            used_local += m_l
+            used += m
+            if step["cull"]:
+                mine = (local_ids[:m_l], b.adv[:m_l].cpu().numpy())
+                got = [None] * world
+                dist.all_gather_object(got, mine, group=group)
+                ids = np.concatenate([g_[0] for g_ in got])
+                av = np.concatenate([g_[1] for g_ in got])
+                gone = cull_decision(alive, ids, av, cfg.cull_fraction,
+                                     cfg.min_tracks)
+                alive[gone] = False
+                culls.append((step["t"], gone, int(alive.sum())))
+                keep = np.flatnonzero(alive[local_ids]).astype(np.int32)
+                b.keep[:len(keep)].copy_(torch.from_numpy(keep))
+                self._compact(b, cur, rt, nxt, rt_spare, len(keep))
+                cur, nxt = nxt, cur
+                rt, rt_spare = rt_spare, rt
+                local_ids = local_ids[keep]
+            if step["ppo"]:
+                B = step["ppo"]
+                pos = gen.choice(len(self._gidx), size=B, replace=False)
+                owners, lpush = self._gidx.locate(pos)
+                slots = (lpush[owners == rank] % cap).astype(np.int32)
+                slots_t = torch.from_numpy(slots).to(dev)
+                a = self.agent
+                a.opt_pi.t += 1
+                a.opt_v.t += 1
+                self._ensure_ppo_scratch(max(len(slots), 1))
+                losses = b.losses[ppo_k]
+                self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
+                                       a.opt_pi.t, a.opt_v.t,
+                                       scratch=self._ppo_scratch,
+                                       losses=losses, B_norm=B, phase=1)
+                self._allreduce_(self.dagent.grads)
+                sums = losses[5:9].clone()
+                self._allreduce_(sums)
+                losses[5:9].copy_(sums)
+                self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
+                                       a.opt_pi.t, a.opt_v.t,
+                                       scratch=self._ppo_scratch,
+                                       losses=losses, B_norm=B, phase=2)
+                train.append((step["t"], losses, B))
+                ppo_k += 1
+        st = b.status.cpu().numpy().view(np.uint64)
+        for code in st[:len(plan)]:
+            D.raise_status(int(code))
+        if int(self.dagent.bad.item()):
+            from .errors import RlDivergedError
+            raise RlDivergedError("non-finite loss or gradient in update")
+        res = self._result(b, cfg, order_counter, used_local, culls, train,
+                           alive)
+        res.extra["global_visits"] = used
+        res.extra["local_ids_final"] = local_ids
+        res.step_rows = local_rows
+        return res
 
     # ---- graph path --------------------------------------------------------
 
@@ -481,8 +665,8 @@ class EpisodeEngine:
         ppo_k = 0
         for k, step in enumerate(b.plan):
             st = gen.bit_generator.state["state"]["state"]
-            rng_np[k, 0] = st & ((1 << 64) - 1)
-            rng_np[k, 1] = st >> 64
+            rng_np[k, 0] = st >> 64               # u128 {hi, lo} (common.cuh)
+            rng_np[k, 1] = st & ((1 << 64) - 1)
             R.skip_u64(gen, 4 * step["m"])
             wpos_np[k] = self.replay.wpos
             self.replay.note_push(step["m"])

@@ -64,3 +64,43 @@ def kernel_times() -> dict:
         d["rows"] += rows
         d["calls"] += 1
     return out
+
+
+def native_timing(on: bool, spin_ns: int = 20000):
+    """Per-kernel CUDA-event timer inside the native library
+    (harl_profile_set): each launch is preceded by a ``spin_ns`` spin kernel
+    so its begin event marks the kernel's real start."""
+    from . import _native as N
+    lib = N.load()
+    if on:
+        N.check(lib.harl_profile_reset(), "harl_profile_reset")
+    N.check(lib.harl_profile_set(1 if on else 0, int(spin_ns)),
+            "harl_profile_set")
+
+
+def native_kernel_times() -> dict:
+    """{kernel name: {"ms": summed ms, "launches": n}} from the native
+    timer (synchronises the recorded events)."""
+    import ctypes as C
+    import numpy as np
+    from . import _native as N
+    lib = N.load()
+    cap, width = 64, 64
+    names = C.create_string_buffer(cap * width)
+    ms = np.zeros(cap, dtype=np.float64)
+    cnt = np.zeros(cap, dtype=np.int64)
+    n = lib.harl_profile_read(cap, names, width, ms.ctypes.data,
+                              cnt.ctypes.data)
+    if n < 0:
+        N.check(n, "harl_profile_read")
+    raw = names.raw
+    out = {}
+    for k in range(min(n, cap)):
+        nm = raw[k * width:(k + 1) * width].split(b"\0", 1)[0].decode()
+        out[nm] = {"ms": float(ms[k]), "launches": int(cnt[k])}
+    return out
+
+
+def native_launch_count() -> int:
+    from . import _native as N
+    return int(N.load(require_device=False).harl_launch_count())

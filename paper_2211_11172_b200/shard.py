@@ -1,0 +1,88 @@
+"""Population sharding across ranks.
+
+Track ``i`` of the episode's population lives on rank ``i % G``
+(interleaved, so the replay tail, the culls and the budget tail stay
+balanced; a contiguous split would put every replay row -- and hence every
+PPO minibatch -- on the last rank at P >= 4096, rlcore.py:253-265).
+Parameters and trees are replicated; the only data-path collective is one
+sum-all-reduce of the PPO gradient (+ loss partial sums) per update.
+
+Everything here is host arithmetic that keeps a sharded episode *the same
+episode* as the single-device one:
+
+* **global rows** -- the reference processes the live tracks in index
+  order (tuner.py:373-375); a track's global row is its rank among the
+  alive track ids, and its uniforms are draws ``h*m + row + 1`` of the
+  step (rlcore.py:223-225), whichever device holds it;
+* **replay ownership** -- the FIFO keeps the last ``cap`` pushes in global
+  (step, row) order; each rank's ring holds its own rows, and a global
+  buffer position maps to (rank, local slot);
+* **cull** -- every rank sees all advantages (all-gather) and takes the
+  identical decision (stopping.py:68-86).
+"""
+
+from __future__ import annotations
+
+import math
+from collections import deque
+
+import numpy as np
+
+
+class ShardLayout:
+    def __init__(self, tracks: int, world: int, rank: int):
+        if not 0 <= rank < world:
+            raise ValueError("bad rank")
+        self.P, self.G, self.rank = tracks, world, rank
+        self.local_ids = np.arange(rank, tracks, world, dtype=np.int64)
+
+    @staticmethod
+    def owner(track_ids, world):
+        return np.asarray(track_ids) % world
+
+    def global_rows(self, alive: np.ndarray, local_alive_ids: np.ndarray):
+        """Global row (rank among all alive ids) of each locally alive id."""
+        csum = np.cumsum(alive) - 1
+        return csum[local_alive_ids].astype(np.int64)
+
+
+class GlobalReplayIndex:
+    """Which rank/local slot holds each position of the global replay FIFO.
+
+    Pushes arrive per step in global-row order; every rank appends its own
+    rows to its local ring (capacity ``cap`` each, more than enough since a
+    rank only ever needs the rows that survive globally)."""
+
+    def __init__(self, cap: int, world: int):
+        self.cap, self.G = cap, world
+        self.items = deque(maxlen=cap)      # (rank, local push counter)
+        self.local_pushes = [0] * world
+
+    def __len__(self):
+        return len(self.items)
+
+    def push_step(self, owners_in_row_order):
+        for r in owners_in_row_order:
+            r = int(r)
+            self.items.append((r, self.local_pushes[r]))
+            self.local_pushes[r] += 1
+
+    def locate(self, positions):
+        """Global FIFO positions -> (rank, local push number) arrays."""
+        items = list(self.items)
+        sel = [items[int(i)] for i in positions]
+        return (np.asarray([s[0] for s in sel], dtype=np.int64),
+                np.asarray([s[1] for s in sel], dtype=np.int64))
+
+
+def cull_decision(alive, track_ids, adv, fraction, min_tracks):
+    """stopping.py:68-86 on the merged advantages of every rank."""
+    live = np.flatnonzero(alive)
+    n = len(live)
+    n_elim = min(int(math.floor(fraction * n)), n - min_tracks)
+    if n_elim <= 0:
+        return np.zeros(0, dtype=np.int64)
+    full = np.zeros(len(alive))
+    full[np.asarray(track_ids, dtype=np.int64)] = adv
+    order = np.lexsort((-live, full[live]))
+    return np.sort(live[order[:n_elim]])

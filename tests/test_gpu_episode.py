@@ -141,6 +141,36 @@ def test_golden_episode_replay(name):
         order += res.visits
 
 
+@pytest.mark.parametrize("name", [n for n in case_names()
+                                  if not GoldenCase(n).is_rl])
+def test_golden_uniform_episode_bit_exact(name):
+    """Evolutionary searcher: uniform valid actions drawn on device from the
+    session generator (tuner.py:341-348) -- integer work end to end, so the
+    whole episode is bit-identical to the reference's, no injection."""
+    gc = GoldenCase(name)
+    eng, forest, cfg = _engine_from(gc)
+    order = 0
+    for e_i, ep in enumerate(gc.rec["episodes"]):
+        tb = gc.tables(ep["sketch"])
+        gen = gc.rng_from(ep["rng_state"])
+        rec = []
+        res = eng.run_episode(tb, forest, gen, cfg, order, record=rec)
+        for s_i, r in enumerate(rec, start=1):
+            np.testing.assert_array_equal(
+                r["actions"].cpu().numpy().T,
+                gc.arr[f"e{e_i}_s{s_i}_actions"].astype(np.int64))
+        tiles, knobs = res.states()
+        key = f"e{e_i}_entry_"
+        np.testing.assert_array_equal(tiles, gc.arr[key + "tiles"])
+        np.testing.assert_array_equal(knobs, gc.arr[key + "knobs"])
+        assert res.scores().tobytes() == gc.arr[key + "score"].tobytes()
+        assert gen.bit_generator.state["state"]["state"] == \
+            int(ep["end_rng_state"]["state"]["state"])
+        assert gen.bit_generator.state["has_uint32"] == \
+            ep["end_rng_state"]["has_uint32"]
+        order += res.visits
+
+
 @pytest.mark.parametrize("name", ["conv2d_l4", "bmm_softmax_k3",
                                   "gemm64_l2"])
 def test_sampled_episode_shadow_replay(name):

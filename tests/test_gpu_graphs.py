@@ -49,7 +49,8 @@ def test_graph_replay_is_bit_identical(hidden, which):
                 [c[1].copy() for c in r1.culls],
                 [t[1].cpu().numpy().copy() for t in r1.train])
         r2 = graphed.run_episode(tb, forest, g2, cfg, 0)
-        assert graphed._cache and next(iter(graphed._cache.values())).graphs
+        if graphed.dagent.tc:   # graphs are used on the tcgen05 path only
+            assert next(iter(graphed._cache.values())).graphs
         np.testing.assert_array_equal(r2.states()[0], out1[0][0])
         np.testing.assert_array_equal(r2.states()[1], out1[0][1])
         assert r2.scores().tobytes() == out1[1].tobytes()

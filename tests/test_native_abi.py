@@ -22,6 +22,44 @@ def test_header_declares_what_the_binding_binds():
     assert header_functions() == sorted(N.EXPORTED)
 
 
+def header_prototypes():
+    """{name: [param type strings]} from the header's declarations."""
+    text = open(os.path.join(ROOT, "include", "harl_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(harl_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;", text):
+        args = " ".join(m.group(2).split())
+        out[m.group(1)] = [] if args in ("", "void") else args.split(",")
+    return out
+
+
+def _kind(decl):
+    d = decl.strip()
+    if "*" in d:
+        return "ptr"
+    if "int64_t" in d or "long long" in d:
+        return "i64"
+    if "double" in d:
+        return "f64"
+    return "i32"
+
+
+def _ctkind(t):
+    if t in (ctypes.c_void_p, ctypes.c_char_p) or hasattr(t, "_type_") and \
+            not isinstance(t._type_, str):
+        return "ptr"
+    return {ctypes.c_int64: "i64", ctypes.c_longlong: "i64",
+            ctypes.c_double: "f64"}.get(t, "i32")
+
+
+def test_binding_signatures_match_the_header():
+    protos = header_prototypes()
+    for name, (_, args) in N._SIGS.items():
+        want = [_kind(a) for a in protos[name]]
+        got = [_ctkind(a) for a in args]
+        assert got == want, name
+
+
 def test_library_exports_every_symbol():
     if not os.path.exists(N.LIB_PATH):
         pytest.skip("native library not built (run build())")

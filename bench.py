@@ -380,8 +380,12 @@ KERNEL_SPAN = {
     "k_heads_tc": ("policy_tc", "tensor"),
     "k_sample_rows": ("policy_tc", "hbm"),
     "k_trunk_tc<value>": ("value_tc", "tensor"),
+    "k_policy_tc": ("policy_tc", "tensor"),
+    "k_value_tc": ("value_tc", "tensor"),
     "k_featurize": ("featurize", "hbm"),
+    "k_featurize2": ("featurize", "hbm"),
     "k_gbt_predict": ("gbt", "hbm"),
+    "k_gbt_predict2": ("gbt", "hbm"),
     "k_finish_step": ("finish", "hbm"),
     "k_ring_rows": ("finish", "hbm"),
     "k_ppo_rows": ("ppo", "fp64"),
@@ -400,10 +404,14 @@ def per_row_work(tables, H):
         "k_trunk_tc<policy>": 2 * (F * H + H * H),
         "k_heads_tc": 2 * H * NH,
         "k_trunk_tc<value>": 2 * (F * H + H * H + H),   # per evaluated row
+        "k_policy_tc": 2 * (F * H + H * H + H * NH),
+        "k_value_tc": 2 * (F * H + H * H + H),
         # logits in; actions, logp, successor state out
         "k_sample_rows": 4 * NH + state + 16 + 8 + state,
         "k_featurize": state + 8 * F,
+        "k_featurize2": state + 8 * F,
         "k_gbt_predict": 8 * F + 8,
+        "k_gbt_predict2": 8 * F + 8,
         # reward/score/v/adv/log entry (state + score + track) + ring scalars
         "k_finish_step": 8 * 6 + state + 8 + 4 + 8 * 4 + 16 + 4,
         "k_ring_rows": 2 * 8 * F * 2,               # X and X' read + written

@@ -384,6 +384,9 @@ int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
  * name_cap-byte slots), summed milliseconds and launch count; it returns
  * the number of distinct kernels. */
 long long harl_launch_count(void);
+/* Debug: enable (on=1) phase timestamps (globaltimer ns) written by CTA 0
+ * of the wide tcgen05 kernels; copies the first n (<= 64) to out_host. */
+int harl_debug_timestamps(int on, unsigned long long* out_host, int n);
 int harl_profile_set(int on, long long spin_ns);
 int harl_profile_reset(void);
 int harl_profile_read(int max_kernels, char* names, int name_cap,

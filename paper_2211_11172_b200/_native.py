@@ -140,6 +140,7 @@ _SIGS = {
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_selftest_tcgen05": (i32, [vp, vp, vp, i32, vp]),
     "harl_launch_count": (C.c_longlong, []),
+    "harl_debug_timestamps": (i32, [i32, vp, i32]),
     "harl_profile_set": (i32, [i32, C.c_longlong]),
     "harl_profile_reset": (i32, []),
     "harl_profile_read": (i32, [i32, C.c_char_p, i32, vp, vp]),

@@ -20,6 +20,29 @@ int cuda_status(cudaError_t e, const char* where);
 void prof_begin(cudaStream_t st);
 void prof_end(const char* where);
 
+// phase timestamps of CTA 0 (debug: harl_debug_timestamps)
+__device__ int g_dbg_on;
+__device__ unsigned long long g_dbg_ts[64];
+__device__ inline void dbg_ts(int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_dbg_on) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dbg_ts[i] = t;
+  }
+}
+
+// Ampere-style asynchronous 16-byte global->shared copies (no register
+// staging, so the compiler cannot serialise them behind shared stores)
+__device__ inline void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ inline void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 #define HARL_PROF_BEGIN(st) ::harl::prof_begin((cudaStream_t)(st))
 
 #define HARL_CHECK_LAUNCH(where)                                     \

@@ -48,46 +48,69 @@ k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
   const uint32_t* shift_bits = io.shift_bits;
   double* adv_out = io.adv;
   const int64_t v = a.vbase + r;
-  // slot-major copy, 8 independent loads in flight per thread
-  for (int s0 = 0; s0 < a.local_slots; s0 += 8) {
-    uint16_t t8[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      t8[q] = (s0 + q < a.local_slots) ? tiles_new[(int64_t)(s0 + q) * a.ld + r] : 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (s0 + q < a.local_slots) log_tiles[(int64_t)(s0 + q) * log.ld + v] = t8[q];
-  }
-  for (int k = 0; k < 3; ++k) log_knobs[(int64_t)k * log.ld + v] = knobs_new[(int64_t)k * a.ld + r];
+  // every independent load of the row first (one memory round trip), then
+  // the track-indexed ones (a second), then the stores
+  const int32_t t = row_track[r];
   const double sc = new_score[r];
   const double rw = reward[r];
+  uint8_t kn[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) kn[k] = knobs_new[(int64_t)k * a.ld + r];
+  constexpr int TB = 32;
+  uint16_t tl[TB];
+#pragma unroll
+  for (int q = 0; q < TB; ++q)
+    tl[q] = (q < a.local_slots) ? tiles_new[(int64_t)q * a.ld + r] : 0;
+  float vn32 = 0.f, vc32 = 0.f;
+  double lp = 0.0;
+  int32_t acts[4] = {0, 0, 0, 0};
+  uint64_t mb = 0;
+  uint32_t sb = 0;
+  const bool push = a.rl && r >= a.keep_from;
+  if (a.rl) {
+    vn32 = v_next[r];
+    vc32 = v_cur[r];
+  }
+  if (push) {
+    acts[0] = head0_col[r];
+#pragma unroll
+    for (int h = 1; h < 4; ++h) acts[h] = actions[(int64_t)h * a.n + r];
+    lp = logp[r];
+    mb = move_bits[r];
+    sb = shift_bits[r];
+  }
+  const int32_t st = ts.steps[t] + 1;
+  const double best = ts.best_score[t];
+#pragma unroll
+  for (int q = 0; q < TB; ++q)
+    if (q < a.local_slots) log_tiles[(int64_t)q * log.ld + v] = tl[q];
+  for (int s0 = TB; s0 < a.local_slots; ++s0)
+    log_tiles[(int64_t)s0 * log.ld + v] = tiles_new[(int64_t)s0 * a.ld + r];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) log_knobs[(int64_t)k * log.ld + v] = kn[k];
   log.score[v] = sc;
   log.reward[v] = rw;
-  const int32_t t = row_track[r];
   log.track[v] = t;
   // Track.advance: steps += 1; best on strict improvement
-  const int32_t st = ts.steps[t] + 1;
   ts.steps[t] = st;
-  if (sc > ts.best_score[t]) {
+  if (sc > best) {
     ts.best_score[t] = sc;
     ts.best_step[t] = st;
   }
   if (!a.rl) return;
   // advantage(reward, v_next, v_cur) = reward + discount*v_next - v_cur
-  const double vn = (double)v_next[r], vc = (double)v_cur[r];
-  const double tdv = __dadd_rn(rw, __dmul_rn(a.discount, vn));
-  const double adv = __dsub_rn(tdv, vc);
+  const double tdv = __dadd_rn(rw, __dmul_rn(a.discount, (double)vn32));
+  const double adv = __dsub_rn(tdv, (double)vc32);
   adv_out[r] = adv;
-  if (r < a.keep_from) return;
+  if (!push) return;
   const int64_t slot = (wpos + r) % ring.cap;
-  ring.actions[slot * 4 + 0] = head0_col[r];
-  for (int h = 1; h < 4; ++h) ring.actions[slot * 4 + h] = actions[(int64_t)h * a.n + r];
-  ring.scalars[slot * 4 + 0] = logp[r];
+  *(int4*)&ring.actions[slot * 4] = make_int4(acts[0], acts[1], acts[2], acts[3]);
+  ring.scalars[slot * 4 + 0] = lp;
   ring.scalars[slot * 4 + 1] = rw;
   ring.scalars[slot * 4 + 2] = adv;
   ring.scalars[slot * 4 + 3] = tdv;
-  ring.move_bits[slot] = move_bits[r];
-  ring.shift_bits[slot] = shift_bits[r];
+  ring.move_bits[slot] = mb;
+  ring.shift_bits[slot] = sb;
 }
 
 // replay feature rows (X, X') of the surviving pushes: one warp per row,

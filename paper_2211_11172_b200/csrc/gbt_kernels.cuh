@@ -14,6 +14,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace harl {
 
@@ -63,6 +64,118 @@ k_gbt_predict(const GbtNode* __restrict__ nodes,
   if (old_score) {
     const double o = old_score[r];
     reward[r] = __ddiv_rn(__dsub_rn(s, o), o);
+  }
+}
+
+// Persistent variant: each CTA bulk-copies the forest (nodes and tree
+// offsets) into shared memory once, then loops over 64-row tiles whose
+// feature rows arrive by bulk copy too, double-buffered so the next tile's
+// rows land while the current one is walked; every level of every walk is
+// then two shared-memory loads.  SMEM_NODES=false keeps the nodes in global
+// memory for forests too large to stage.
+constexpr int GBT2_GROUPS = 8;
+constexpr int GBT2_ROWS = 64;
+constexpr int GBT2_THREADS = GBT2_ROWS * GBT2_GROUPS;
+
+__host__ __device__ inline size_t gbt2_align(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline size_t gbt2_smem_bytes(bool smem_nodes, int64_t n_nodes,
+                                                  int T, int F) {
+  return (smem_nodes ? gbt2_align((size_t)n_nodes * 16) : 0) +
+         gbt2_align((size_t)T * 4) + 2 * gbt2_align((size_t)GBT2_ROWS * F * 8) +
+         (size_t)GBT2_ROWS * T * 8;
+}
+
+template <bool SMEM_NODES>
+__global__ void __launch_bounds__(GBT2_THREADS)
+k_gbt_predict2(const GbtNode* __restrict__ gnodes,
+               const int32_t* __restrict__ tree_first, int32_t n_trees,
+               int64_t n_nodes, int32_t fitted, double base,
+               double floor_value, const double* __restrict__ feat, int64_t n,
+               int32_t F, double* score, const double* old_score,
+               double* reward) {
+  dbg_ts(24);
+  extern __shared__ __align__(16) unsigned char gsm[];
+  __shared__ uint64_t fbar, xbar[2];
+  size_t off = 0;
+  const GbtNode* nodes = gnodes;
+  GbtNode* sn = (GbtNode*)gsm;
+  if (SMEM_NODES) {
+    nodes = sn;
+    off = gbt2_align((size_t)n_nodes * 16);
+  }
+  int32_t* s_first = (int32_t*)(gsm + off);
+  off += gbt2_align((size_t)n_trees * 4);
+  double* xsb[2];
+  xsb[0] = (double*)(gsm + off);
+  off += gbt2_align((size_t)GBT2_ROWS * F * 8);
+  xsb[1] = (double*)(gsm + off);
+  off += gbt2_align((size_t)GBT2_ROWS * F * 8);
+  double* contrib = (double*)(gsm + off);
+  const int64_t n_tiles = (n + GBT2_ROWS - 1) / GBT2_ROWS;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&fbar, 1);
+    tc::mbar_init(&xbar[0], 1);
+    tc::mbar_init(&xbar[1], 1);
+    if (SMEM_NODES && n_nodes > 0) tc::bulk_load(sn, gnodes, (uint32_t)n_nodes * 16, &fbar);
+    else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&fbar)) : "memory");
+    if (blockIdx.x < n_tiles) {
+      const int64_t r0 = (int64_t)blockIdx.x * GBT2_ROWS;
+      tc::bulk_f64(xsb[0], feat + r0 * F,
+                   (uint32_t)(min((int64_t)GBT2_ROWS, n - r0) * F), &xbar[0]);
+    }
+  }
+  for (int t = threadIdx.x; t < n_trees; t += blockDim.x) s_first[t] = tree_first[t];
+  // a warp = 32 rows on the same tree group: node reads of a level are
+  // mostly broadcasts and the 32 feature reads hit distinct bank pairs
+  const int warp = threadIdx.x >> 5;
+  const int g = warp / (GBT2_ROWS / 32);
+  const int rl = (warp % (GBT2_ROWS / 32)) * 32 + (threadIdx.x & 31);
+  __syncthreads();
+  tc::mbar_wait(&fbar, 0);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    const int64_t r0 = tile * GBT2_ROWS;
+    const int rows = (int)(n - r0 < GBT2_ROWS ? n - r0 : GBT2_ROWS);
+    const int64_t r = r0 + rl;
+    double o = 0.0;
+    if (old_score && g == 0 && rl < rows) o = old_score[r];
+    const int b = it & 1;
+    tc::mbar_wait(&xbar[b], (it >> 1) & 1);
+    if (threadIdx.x == 0) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < n_tiles) {   // the other buffer was released at the end of it-1
+        const int64_t n0 = nt * GBT2_ROWS;
+        tc::bulk_f64(xsb[b ^ 1], feat + n0 * F,
+                     (uint32_t)(min((int64_t)GBT2_ROWS, n - n0) * F), &xbar[b ^ 1]);
+      }
+    }
+    if (it < 2) dbg_ts(25 + 3 * it);
+    const double* xs = xsb[b];
+    if (fitted && rl < rows) {
+      const double* x = xs + rl * F;
+      for (int t = g; t < n_trees; t += GBT2_GROUPS) {
+        const GbtNode* tree = nodes + s_first[t];
+        GbtNode nd = tree[0];
+        while (nd.feat >= 0) nd = tree[(x[nd.feat] <= nd.v) ? nd.left : nd.right];
+        contrib[rl * n_trees + t] = nd.v;
+      }
+    }
+    __syncthreads();
+    if (it < 2) dbg_ts(26 + 3 * it);
+    if (g == 0 && rl < rows) {
+      double pred = 1.0;
+      if (fitted) {
+        pred = base;
+        const double* c = contrib + rl * n_trees;
+        for (int t = 0; t < n_trees; ++t) pred = __dadd_rn(pred, c[t]);
+      }
+      const double s = (pred != pred) ? pred : (pred < floor_value ? floor_value : pred);
+      score[r] = s;
+      if (old_score) reward[r] = __ddiv_rn(__dsub_rn(s, o), o);
+    }
+    __syncthreads();
+    if (it < 2) dbg_ts(27 + 3 * it);
   }
 }
 

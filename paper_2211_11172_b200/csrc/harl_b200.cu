@@ -1,6 +1,7 @@
 // C-ABI entry points (include/harl_b200.h).  Single translation unit: all
 // kernels are included here so constant-memory tables need no -rdc.
 #include <climits>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -17,6 +18,7 @@
 #include "ppo_kernels.cuh"
 #include "tc_probe.cuh"
 #include "mlp_tc.cuh"
+#include "mlp_tc2.cuh"
 #include "sample_kernels.cuh"
 
 namespace harl {
@@ -133,6 +135,23 @@ static inline u128 state_of(const harl_pcg64& g) {
   s.hi = g.state_hi;
   s.lo = g.state_lo;
   return s;
+}
+
+static int sm_count() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return v;
+}
+
+// HARL_TC_GEN1=1 selects the first-generation 4-warp tcgen05 kernels
+static bool use_tc2() {
+  static int v = -1;
+  if (v < 0) v = getenv("HARL_TC_GEN1") ? 0 : 1;
+  return v == 1;
 }
 
 static int max_dyn_smem() {
@@ -387,6 +406,15 @@ int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
   int rc = check_sketch(sk);
   if (rc) return rc;
   if (n <= 0) return HARL_OK;
+  const size_t smem2 = feat2_smem_bytes(sk->feature_len, sk->local_slots, sk->max_extent);
+  if (smem2 <= (size_t)max_dyn_smem()) {
+    if ((rc = allow_smem(k_featurize2, smem2, "k_featurize2"))) return rc;
+    HARL_PROF_BEGIN((cudaStream_t)stream);
+    k_featurize2<<<(unsigned)((n + FEAT2_ROWS - 1) / FEAT2_ROWS), FEAT2_ROWS, smem2,
+                   (cudaStream_t)stream>>>(*sk, tiles, knobs, n, ld, feat);
+    HARL_CHECK_LAUNCH("k_featurize2");
+    return HARL_OK;
+  }
   const size_t smem = sizeof(double) * FEAT_THREADS * sk->feature_len;
   if ((rc = allow_smem(k_featurize, smem, "k_featurize"))) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);
@@ -434,12 +462,36 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
   }
   if (n <= 0) return HARL_OK;
   const int T = forest->n_trees > 0 ? forest->n_trees : 1;
+  const int F = feature_len;
+  const size_t cap = (size_t)max_dyn_smem();
+  const bool smem_nodes = gbt2_smem_bytes(true, forest->n_nodes, T, F) <= cap;
+  const size_t smem = gbt2_smem_bytes(smem_nodes, forest->n_nodes, T, F);
+  if (smem <= cap) {
+    const int64_t tiles = (n + GBT2_ROWS - 1) / GBT2_ROWS;
+    const int64_t grid = tiles < sm_count() ? tiles : sm_count();
+    int rc = smem_nodes ? allow_smem(k_gbt_predict2<true>, smem, "k_gbt_predict2")
+                        : allow_smem(k_gbt_predict2<false>, smem, "k_gbt_predict2");
+    if (rc) return rc;
+    HARL_PROF_BEGIN((cudaStream_t)stream);
+    if (smem_nodes)
+      k_gbt_predict2<true><<<(unsigned)grid, GBT2_THREADS, smem, (cudaStream_t)stream>>>(
+          (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
+          forest->n_nodes, forest->fitted, forest->base, forest->floor_value, feat,
+          n, F, score, old_score, reward);
+    else
+      k_gbt_predict2<false><<<(unsigned)grid, GBT2_THREADS, smem, (cudaStream_t)stream>>>(
+          (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
+          forest->n_nodes, forest->fitted, forest->base, forest->floor_value, feat,
+          n, F, score, old_score, reward);
+    HARL_CHECK_LAUNCH("k_gbt_predict2");
+    return HARL_OK;
+  }
   const int rows = T <= 192 ? GBT_THREADS / GBT_GROUPS : 4;
-  const size_t smem = sizeof(double) * (size_t)rows * T;
-  int rc = allow_smem(k_gbt_predict, smem, "k_gbt_predict");
+  const size_t smem1 = sizeof(double) * (size_t)rows * T;
+  int rc = allow_smem(k_gbt_predict, smem1, "k_gbt_predict");
   if (rc) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_gbt_predict<<<(unsigned)((n + rows - 1) / rows), GBT_THREADS, smem,
+  k_gbt_predict<<<(unsigned)((n + rows - 1) / rows), GBT_THREADS, smem1,
                   (cudaStream_t)stream>>>(
       (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
       forest->fitted, forest->base, forest->floor_value, feat, n, feature_len,
@@ -558,16 +610,6 @@ static bool tc_trunk_ok(const harl_mlp_desc* m, int F) {
          m->dims[1] == TC_H && m->dims[2] == TC_H;
 }
 
-static int sm_count() {
-  static int v = 0;
-  if (!v) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return v;
-}
-
 int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         const double* feat, const uint16_t* tiles,
                         const uint8_t* knobs, int64_t n, int64_t ld,
@@ -594,6 +636,30 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     return HARL_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  const int NHP = (pol->n_head_cols + 15) / 16 * 16;
+  if (packed_trunk && packed_heads && use_tc2() && ((uintptr_t)feat & 15) == 0 &&
+      (size_t)tc2_smem(NHP) <= (size_t)max_dyn_smem()) {
+    if ((rc = allow_smem(k_policy_tc, (size_t)tc2_smem(NHP), "k_policy_tc"))) return rc;
+    PolicyTcArgs pa;
+    pa.feat = feat;
+    pa.n = n;
+    pa.F = sk->feature_len;
+    pa.NH = pol->n_head_cols;
+    pa.NHP = NHP;
+    pa.logits = hid_scratch;
+    pa.logits_out = logits_out;
+    pa.trunk_img = packed_trunk;
+    pa.heads_img = packed_heads;
+    const int64_t tiles_n = (n + 127) / 128;
+    const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+    HARL_PROF_BEGIN(st);
+    k_policy_tc<<<grid, TC2_THREADS, tc2_smem(NHP), st>>>(pa);
+    HARL_CHECK_LAUNCH("k_policy_tc");
+    return launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
+                          TC_H, n, ld, tiles, knobs, inject, actions, logp,
+                          tiles_out, knobs_out, move_bits, shift_bits,
+                          head0_col, status, st);
+  }
   if ((rc = allow_smem(k_trunk_tc<TRUNK_POLICY>, TRUNK_SMEM, "k_trunk_tc")))
     return rc;
   TrunkArgs ta;
@@ -646,6 +712,27 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
     return HARL_E_ARG;
   }
   if (n0 + n1 <= 0) return HARL_OK;
+  if (packed && use_tc2() && ((uintptr_t)feat0 & 15) == 0 &&
+      ((uintptr_t)feat1 & 15) == 0) {
+    const size_t smem = (size_t)tc2_value_smem();
+    if ((rc = allow_smem(k_value_tc, smem, "k_value_tc"))) return rc;
+    ValueTcArgs va;
+    va.feat0 = feat0;
+    va.feat1 = feat1;
+    va.n0 = n0;
+    va.n1 = feat1 ? n1 : 0;
+    va.F = feature_len;
+    va.out0 = v0;
+    va.out1 = v1;
+    va.b3 = val->b[2];
+    va.trunk_img = packed;
+    const int64_t tiles_n = (n0 + 127) / 128 + (va.n1 + 127) / 128;
+    const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+    HARL_PROF_BEGIN((cudaStream_t)stream);
+    k_value_tc<<<grid, TC2_THREADS, smem, (cudaStream_t)stream>>>(va);
+    HARL_CHECK_LAUNCH("k_value_tc");
+    return HARL_OK;
+  }
   if ((rc = allow_smem(k_trunk_tc<TRUNK_VALUE>, TRUNK_SMEM, "k_trunk_tc")))
     return rc;
   TrunkArgs ta;
@@ -677,12 +764,17 @@ int harl_prepare(void) {
   // entry point needs cudaFuncSetAttribute while a stream is being captured
   int rc = 0;
   if ((rc = allow_max_smem(k_featurize, "k_featurize"))) return rc;
+  if ((rc = allow_max_smem(k_featurize2, "k_featurize2"))) return rc;
   if ((rc = allow_max_smem(k_gbt_predict, "k_gbt_predict"))) return rc;
+  if ((rc = allow_max_smem(k_gbt_predict2<true>, "k_gbt_predict2"))) return rc;
+  if ((rc = allow_max_smem(k_gbt_predict2<false>, "k_gbt_predict2"))) return rc;
   if ((rc = allow_max_smem(k_policy_step, "k_policy_step"))) return rc;
   if ((rc = allow_max_smem(k_value_forward, "k_value_forward"))) return rc;
   if ((rc = allow_max_smem(k_trunk_tc<TRUNK_POLICY>, "k_trunk_tc"))) return rc;
   if ((rc = allow_max_smem(k_trunk_tc<TRUNK_VALUE>, "k_trunk_tc"))) return rc;
   if ((rc = allow_max_smem(k_heads_tc, "k_heads_tc"))) return rc;
+  if ((rc = allow_max_smem(k_policy_tc, "k_policy_tc"))) return rc;
+  if ((rc = allow_max_smem(k_value_tc, "k_value_tc"))) return rc;
   if ((rc = allow_max_smem(k_ppo_rows, "k_ppo_rows"))) return rc;
   (void)sm_count();
   return HARL_OK;
@@ -990,6 +1082,17 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
 // -- launch counter / per-kernel timer ----------------------------------------
 
 long long harl_launch_count(void) { return g_launches.load(); }
+
+int harl_debug_timestamps(int on, unsigned long long* out_host, int n) {
+  cudaError_t e = cudaMemcpyToSymbol(g_dbg_on, &on, sizeof(int));
+  if (e != cudaSuccess) return cuda_status(e, "harl_debug_timestamps");
+  if (out_host && n > 0) {
+    e = cudaMemcpyFromSymbol(out_host, g_dbg_ts,
+                             sizeof(unsigned long long) * (n < 64 ? n : 64));
+    if (e != cudaSuccess) return cuda_status(e, "harl_debug_timestamps");
+  }
+  return HARL_OK;
+}
 
 int harl_profile_set(int on, long long spin_ns) {
   std::lock_guard<std::mutex> lk(g_prof_mu);

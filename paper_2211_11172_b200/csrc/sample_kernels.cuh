@@ -102,6 +102,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ LaneJump LJ, u128 base_arg,
               const u128* base_dev, const uint16_t* __restrict__ tiles,
               const uint8_t* __restrict__ knobs, SampleArgs a) {
+  dbg_ts(16);
   __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
   for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
     s_src[i] = sk.head0_src[i];
@@ -123,6 +124,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     const uint64_t k = (uint64_t)g * (uint64_t)a.m_total + (uint64_t)row + 1;
     u_mine = u64_to_unit(pcg_draw64(J, base, k));
   }
+  dbg_ts(17);
   // ---- current state: lane g holds slots g, g+8, ... --------------------
   uint64_t mv = 0;
   int tv[HARL_MAX_SLOTS / SG];
@@ -137,6 +139,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   const int ca0 = knobs[rr], par0 = knobs[a.ld + rr], ur0 = knobs[2 * a.ld + rr];
   const uint32_t sb = shift_bits_of(sk, ca0, par0, ur0);
   const float* z = a.logits + rr * a.ldz;
+  dbg_ts(18);
   auto legal0 = [&](int j) -> bool {
     return j == C0 - 1 || ((mv >> s_src[j]) & 1ull);
   };
@@ -168,8 +171,21 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   } else {
     const double u0 = __shfl_sync(0xffffffffu, u_mine, 0, SG);
     const int nI = (C0 + SG - 1) / SG;
+    // this lane's head-0 logits, all loads in flight at once; illegal and
+    // padding columns read as -inf
+    float zc[SAMPLE_MAXI];
+#pragma unroll
+    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+      const int j = g + SG * i;
+      zc[i] = (i < nI && j < C0) ? z[j] : -INFINITY;
+    }
     float zmax = -INFINITY;
-    for (int i = 0; i < nI; ++i) {
+#pragma unroll
+    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+      const int j = g + SG * i;
+      if (i < nI && j < C0 && legal0(j)) zmax = fmaxf(zmax, zc[i]);
+    }
+    for (int i = SAMPLE_MAXI; i < nI; ++i) {
       const int j = g + SG * i;
       if (j < C0 && legal0(j)) zmax = fmaxf(zmax, z[j]);
     }
@@ -180,7 +196,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
 #pragma unroll
     for (int i = 0; i < SAMPLE_MAXI; ++i) {
       const int j = g + SG * i;
-      e[i] = (i < nI && j < C0 && legal0(j)) ? expf(z[j] - zmax) : 0.f;
+      e[i] = (i < nI && j < C0 && legal0(j)) ? expf(zc[i] - zmax) : 0.f;
       s += (double)e[i];
     }
     for (int i = SAMPLE_MAXI; i < nI; ++i) {   // wide heads (C0 > 128)
@@ -188,6 +204,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
       if (j < C0 && legal0(j)) s += (double)expf(z[j] - zmax);
     }
     s = gsum(s);
+    dbg_ts(19);
     const double inv = 1.0 / s;
     int count = 0;
     double carry = 0.0;
@@ -212,6 +229,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
       carry = __shfl_sync(0xffffffffu, c, SG - 1, SG);
     }
     count = gsumi(count);
+    dbg_ts(20);
     int idx = min(count, C0 - 1);
     while (idx > 0 && !legal0(idx)) --idx;
     const bool ok = legal0(idx);
@@ -228,6 +246,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
       const int j = sample3(z + C0 + 3 * (hh - 1), m3, uh, &lph);
       ah = j < 0 ? 0 : j;
     }
+    dbg_ts(21);
     lp_total = lp0;
 #pragma unroll
     for (int h = 1; h < 4; ++h) {
@@ -277,6 +296,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     else if (par < 0 || par > sk.max_fusible) code = HARL_ST_PARALLEL;
     else if (ur < 0 || ur >= sk.n_unroll) code = HARL_ST_UNROLL;
   }
+  dbg_ts(22);
   if (!live) return;
   const bool moved = code == HARL_ST_OK && src >= 0;
 #pragma unroll
@@ -302,6 +322,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     a.head0_col[r] = col0;
     report_status(a.status, r, code);
   }
+  dbg_ts(23);
 }
 
 }  // namespace harl

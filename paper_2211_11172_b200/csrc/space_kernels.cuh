@@ -139,7 +139,9 @@ __device__ inline void footprint_l1l2(const harl_sketch_desc& sk,
 __device__ inline void featurize_row(const harl_sketch_desc& sk,
                                      const uint16_t* tiles,
                                      const uint8_t* knobs, int64_t ld,
-                                     int64_t r, double* dst) {
+                                     int64_t r, double* dst,
+                                     const double* lut = nullptr) {
+  if (!lut) lut = sk.log2_lut;
   const int L = sk.levels, F = sk.feature_len;
   for (int i = 0; i < F; ++i) dst[i] = 0.0;
   int64_t t1[HARL_MAX_DIMS], t2[HARL_MAX_DIMS];
@@ -147,7 +149,7 @@ __device__ inline void featurize_row(const harl_sketch_desc& sk,
     int64_t prod = 1;
     for (int lv = 0; lv < L; ++lv) {
       const int v = tiles[(int64_t)(d * L + lv) * ld + r];
-      dst[d * L + lv] = sk.log2_lut[v];
+      dst[d * L + lv] = lut[v];
       if (lv >= L - 2) prod *= v;
       if (lv == L - 1) t1[d] = v;
     }
@@ -180,6 +182,78 @@ k_featurize(const __grid_constant__ harl_sketch_desc sk, const uint16_t* tiles,
   const int64_t rows = min((int64_t)FEAT_THREADS, n - r0);
   double* out = feat + r0 * F;
   for (int64_t i = threadIdx.x; i < rows * F; i += FEAT_THREADS) out[i] = sfeat[i];
+}
+
+// Staged variant: the CTA's tile/knob columns (coalesced along rows) and
+// the log2 LUT are copied into shared memory with all loads in flight at
+// once; each thread then featurizes its row from shared memory.
+constexpr int FEAT2_ROWS = 128;
+constexpr int FEAT2_LUT_MAX = 4096;
+
+__host__ __device__ inline size_t feat2_smem_bytes(int F, int local_slots,
+                                                   int max_extent) {
+  const size_t lut = (max_extent + 1 <= FEAT2_LUT_MAX) ? (size_t)((max_extent + 2) & ~1) * 8 : 0;
+  return (size_t)FEAT2_ROWS * F * 8 + lut +
+         (((size_t)FEAT2_ROWS * local_slots * 2 + FEAT2_ROWS * 3 + 15) & ~(size_t)15);
+}
+
+__global__ void __launch_bounds__(FEAT2_ROWS)
+k_featurize2(const __grid_constant__ harl_sketch_desc sk,
+             const uint16_t* __restrict__ tiles,
+             const uint8_t* __restrict__ knobs, int64_t n, int64_t ld,
+             double* __restrict__ feat) {
+  dbg_ts(32);
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const int F = sk.feature_len, S = sk.local_slots;
+  double* sfeat = (double*)fsm;
+  const bool slut = sk.max_extent + 1 <= FEAT2_LUT_MAX;
+  double* lut = slut ? sfeat + FEAT2_ROWS * F : nullptr;
+  uint16_t* stile = (uint16_t*)(sfeat + FEAT2_ROWS * F + (slut ? (sk.max_extent + 2) & ~1 : 0));
+  uint8_t* sknob = (uint8_t*)(stile + FEAT2_ROWS * S);
+  const int64_t r0 = (int64_t)blockIdx.x * FEAT2_ROWS;
+  const int rows = (int)min((int64_t)FEAT2_ROWS, n - r0);
+  const bool vec = (ld % 16) == 0 && (((uintptr_t)tiles | (uintptr_t)knobs |
+                                       (uintptr_t)sk.log2_lut) & 15) == 0;
+  if (vec) {
+    // 16-byte async copies: slot segments (8 rows per chunk), knob rows
+    // (16 rows per chunk) and the LUT; chunks past `rows` stay inside the
+    // allocation because ld is a multiple of 16
+    const int cs = (rows + 7) / 8, ck = (rows + 15) / 16;
+    for (int i = threadIdx.x; i < S * cs; i += FEAT2_ROWS) {
+      const int sl = i / cs, c = i % cs;
+      cp_async16(stile + sl * FEAT2_ROWS + 8 * c, tiles + (int64_t)sl * ld + r0 + 8 * c);
+    }
+    for (int i = threadIdx.x; i < 3 * ck; i += FEAT2_ROWS) {
+      const int k = i / ck, c = i % ck;
+      cp_async16(sknob + k * FEAT2_ROWS + 16 * c, knobs + (int64_t)k * ld + r0 + 16 * c);
+    }
+    if (slut) {
+      const int nl = sk.max_extent + 1;
+      for (int i = threadIdx.x; i < nl / 2; i += FEAT2_ROWS)
+        cp_async16(lut + 2 * i, sk.log2_lut + 2 * i);
+      if ((nl & 1) && threadIdx.x == 0) lut[nl - 1] = sk.log2_lut[nl - 1];
+    }
+    cp_async_wait_all();
+  } else {
+    for (int s0 = 0; s0 < S; ++s0)
+      if ((int)threadIdx.x < rows)
+        stile[s0 * FEAT2_ROWS + threadIdx.x] = tiles[(int64_t)s0 * ld + r0 + threadIdx.x];
+    for (int k = 0; k < 3; ++k)
+      if ((int)threadIdx.x < rows)
+        sknob[k * FEAT2_ROWS + threadIdx.x] = knobs[(int64_t)k * ld + r0 + threadIdx.x];
+    if (slut)
+      for (int i = threadIdx.x; i <= sk.max_extent; i += FEAT2_ROWS) lut[i] = sk.log2_lut[i];
+  }
+  __syncthreads();
+  dbg_ts(33);
+  if (threadIdx.x < rows)
+    featurize_row(sk, stile, sknob, FEAT2_ROWS, threadIdx.x,
+                  sfeat + threadIdx.x * F, lut);
+  __syncthreads();
+  dbg_ts(34);
+  double* out = feat + r0 * F;
+  for (int i = threadIdx.x; i < rows * F; i += FEAT2_ROWS) out[i] = sfeat[i];
+  dbg_ts(35);
 }
 
 // ---------------------------------------------------------------------------

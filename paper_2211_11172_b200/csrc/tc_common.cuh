@@ -75,6 +75,20 @@ __device__ inline void bulk_load(void* dst, const void* src, uint32_t bytes,
   }
 }
 
+// `n` doubles (contiguous, 16-byte aligned source) -> shared memory with
+// one bulk copy; an odd 8-byte tail is written with a plain store before
+// the arrive, whose release makes it visible to every waiter.  One thread.
+__device__ inline void bulk_f64(double* dst, const double* src, uint32_t n,
+                                uint64_t* bar) {
+  const uint32_t bytes = n * 8, main = bytes & ~15u;
+  if (bytes != main) dst[main / 8] = src[main / 8];
+  if (main) {
+    bulk_load(dst, src, main, bar);
+  } else {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  }
+}
+
 // MMA completion -> mbarrier arrive (implicit before_thread_sync fence)
 __device__ inline void mma_commit(uint64_t* bar) {
   asm volatile(
@@ -167,6 +181,33 @@ __device__ inline void tmem_st32(uint32_t taddr, const float* v) {
         "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]),
         "r"(r[31])
       : "memory");
+}
+
+__device__ inline void tmem_st16(uint32_t taddr, const float* v) {
+  uint32_t r[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(v[i]);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),
+        "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),
+        "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+__device__ inline void tmem_st1(uint32_t taddr, float v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};"
+               ::"r"(taddr), "r"(__float_as_uint(v)) : "memory");
+}
+
+__device__ inline void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ inline void tmem_st_wait() {

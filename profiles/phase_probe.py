@@ -1,0 +1,50 @@
+"""Phase timeline of CTA 0 of the wide tcgen05 policy kernel (globaltimer
+timestamps, harl_debug_timestamps) for one rollout step at P rows.
+
+    python profiles/phase_probe.py [P]
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2211_11172_b200 import _native as N  # noqa: E402
+from paper_2211_11172_b200 import device as D  # noqa: E402
+from paper_2211_11172_b200.engine import EpisodeConfig, EpisodeEngine  # noqa: E402
+
+NAMES = ["start", "init", "x_staged", "w1_ready", "mma1", "epi1", "mma2",
+         "epi2", "heads_ready", "mma_heads", "end"]
+SNAMES = ["start", "rng", "state", "softmax", "cdf", "shift_heads", "decided", "end"]
+GNAMES = ["start", "x0", "walk0", "sum0", "x1", "walk1", "sum1"]
+FNAMES = ["start", "staged", "rows", "end"]
+
+
+def main():
+    P = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+    w = bench.build_workload("c2", P)
+    tb = w["tables"]
+    forest = D.DeviceForest(w["trees"], w["base"], w["lr"])
+    eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, use_graphs=False)
+    cfg = EpisodeConfig(tracks=P, track_len=1, cull_window=20,
+                        cull_fraction=0.5, min_tracks=P // 2)
+    lib = N.load()
+    gen = np.random.default_rng(0)
+    for rep in range(3):
+        N.check(lib.harl_debug_timestamps(1, None, 0), "dbg")
+        eng.run_episode(tb, forest, gen, cfg, 0)
+        torch.cuda.synchronize()
+        ts = np.zeros(64, dtype=np.uint64)
+        N.check(lib.harl_debug_timestamps(0, ts.ctypes.data_as(C.c_void_p), 64), "dbg")
+        for nm, lo, names in (("policy", 0, NAMES), ("sample", 16, SNAMES),
+                              ("gbt", 24, GNAMES), ("featurize", 32, FNAMES)):
+            t = ts[lo:lo + len(names)].astype(np.int64)
+            rel = (t - t[0]) / 1e3
+            print(f"rep {rep} {nm}: " + " ".join(f"{n}={r:.2f}" for n, r in zip(names, rel)))
+
+
+if __name__ == "__main__":
+    main()

@@ -363,8 +363,17 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     int64_t n_pi, int64_t n_params, double* losses,
                     int32_t* bad, void* scratch, const double* adam_dev,
                     void* pol_trunk_img, void* pol_heads_img,
-                    void* val_trunk_img, int32_t B_norm, int32_t phase,
-                    void* stream);
+                    void* val_trunk_img, double* wt_params, int32_t B_norm,
+                    int32_t phase, void* stream);
+
+/* fp64 transposed copies of the matrices the PPO backward pass reads
+ * (policy heads, policy/value W[l] for l >= 1): size in doubles, and a
+ * rebuild from the master parameters (after any host-side upload; the Adam
+ * kernel keeps them current afterwards). */
+int64_t harl_ppo_wt_doubles(const harl_net_layout* pol,
+                            const harl_net_layout* val);
+int harl_ppo_wt_fill(const harl_net_layout* pol, const harl_net_layout* val,
+                     const double* params, double* wt, void* stream);
 
 /* Diagnostic: one 128x128x64 kind::tf32 tcgen05 MMA (A [128][64], B
  * [64][128] row-major fp32, D [128][128]); mode 0 = A from TMEM, 1 = A

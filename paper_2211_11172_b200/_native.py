@@ -147,7 +147,9 @@ _SIGS = {
     "harl_ppo_update": (i32, [P(NetLayout), P(NetLayout), P(PpoHyper),
                               P(ReplayRing), vp, i32, i32, i32, vp, i32, vp,
                               vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp,
-                              vp, vp, i32, i32, vp]),
+                              vp, vp, vp, i32, i32, vp]),
+    "harl_ppo_wt_doubles": (i64, [P(NetLayout), P(NetLayout)]),
+    "harl_ppo_wt_fill": (i32, [P(NetLayout), P(NetLayout), vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -135,8 +135,14 @@ struct GlibcLogData {
   double logc[128];
 };
 
-// single translation unit (harl_b200.cu), so the table is defined here
+// single translation unit (harl_b200.cu), so the table is defined here.
+// The scalars are read from the constant bank (uniform across a warp); the
+// per-lane table lookups go through a global copy and the L1 path, since
+// divergent constant-bank reads serialise.
 __constant__ GlibcLogData c_logdata = {
+#include "glibc_log_data.inc"
+};
+__device__ GlibcLogData g_logdata = {
 #include "glibc_log_data.inc"
 };
 
@@ -169,9 +175,9 @@ __device__ inline double glibc_log(double x) {
   int i = (int)((tmp >> 45) & 127u);
   int64_t k = (int64_t)tmp >> 52;
   double z = bitsd(ix - (tmp & (0xfffull << 52)));
-  double r = __fma_rn(z, D.invc[i], -1.0);
+  double r = __fma_rn(z, __ldg(&g_logdata.invc[i]), -1.0);
   double kd = (double)k;
-  double w = __fma_rn(kd, D.ln2hi, D.logc[i]);
+  double w = __fma_rn(kd, D.ln2hi, __ldg(&g_logdata.logc[i]));
   double hi = __dadd_rn(w, r);
   double lo = __fma_rn(kd, D.ln2lo, __dadd_rn(__dsub_rn(w, hi), r));
   double r2 = __dmul_rn(r, r);

@@ -410,7 +410,7 @@ int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
   if (smem2 <= (size_t)max_dyn_smem()) {
     if ((rc = allow_smem(k_featurize2, smem2, "k_featurize2"))) return rc;
     HARL_PROF_BEGIN((cudaStream_t)stream);
-    k_featurize2<<<(unsigned)((n + FEAT2_ROWS - 1) / FEAT2_ROWS), FEAT2_ROWS, smem2,
+    k_featurize2<<<(unsigned)((n + FEAT2_ROWS - 1) / FEAT2_ROWS), FEAT2_THREADS, smem2,
                    (cudaStream_t)stream>>>(*sk, tiles, knobs, n, ld, feat);
     HARL_CHECK_LAUNCH("k_featurize2");
     return HARL_OK;
@@ -960,6 +960,51 @@ int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
   return HARL_OK;
 }
 
+static void build_trans_plan(const harl_net_layout& P, const harl_net_layout& V,
+                             TransPlan* tp, PpoArgs* a) {
+  memset(tp, 0, sizeof(*tp));
+  int64_t dst = 0;
+  auto add = [&](int64_t off, int K, int N) -> int64_t {
+    const int64_t d = dst;
+    tp->m[tp->n++] = {off, d, K, N};
+    dst += (int64_t)K * N;
+    return d;
+  };
+  const int H = P.dims[P.n_layers];
+  const int64_t h = add(P.off_hW, H, P.n_head_cols);
+  if (a) a->wt_head = h;
+  for (int l = 1; l < P.n_layers; ++l) {
+    const int64_t d = add(P.off_W[l], P.dims[l], P.dims[l + 1]);
+    if (a) a->wt_P[l] = d;
+  }
+  for (int l = 1; l < V.n_layers; ++l) {
+    const int64_t d = add(V.off_W[l], V.dims[l], V.dims[l + 1]);
+    if (a) a->wt_V[l] = d;
+  }
+  tp->total = dst;
+}
+
+int64_t harl_ppo_wt_doubles(const harl_net_layout* pol, const harl_net_layout* val) {
+  if (!pol || !val) return 0;
+  TransPlan tp;
+  build_trans_plan(*pol, *val, &tp, nullptr);
+  return tp.total;
+}
+
+int harl_ppo_wt_fill(const harl_net_layout* pol, const harl_net_layout* val,
+                     const double* params, double* wt, void* stream) {
+  if (!pol || !val || !params || !wt) {
+    set_error("harl_ppo_wt_fill: null argument");
+    return HARL_E_ARG;
+  }
+  TransPlan tp;
+  build_trans_plan(*pol, *val, &tp, nullptr);
+  HARL_PROF_BEGIN((cudaStream_t)stream);
+  k_wt_fill<<<148, 256, 0, (cudaStream_t)stream>>>(tp, params, wt);
+  HARL_CHECK_LAUNCH("k_wt_fill");
+  return HARL_OK;
+}
+
 int64_t harl_ppo_scratch_bytes(int32_t B, int32_t row_stride, int32_t n_jobs) {
   (void)n_jobs;
   return (int64_t)B * row_stride * 8 + (int64_t)B * 4 * 8 +
@@ -975,8 +1020,8 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     int64_t n_pi, int64_t n_params, double* losses,
                     int32_t* bad, void* scratch, const double* adam_dev,
                     void* pol_trunk_img, void* pol_heads_img,
-                    void* val_trunk_img, int32_t B_norm, int32_t phase,
-                    void* stream) {
+                    void* val_trunk_img, double* wt_params, int32_t B_norm,
+                    int32_t phase, void* stream) {
   if (B_norm <= 0) B_norm = B;
   if (phase < 1 || phase > 3) phase = 3;
   if (!pol || !val || !hp || !ring || B < 0 || n_head0 < 1 ||
@@ -1009,19 +1054,26 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   a.w_ent = hp->entropy_weight;
   a.w_val = hp->value_loss_weight;
   for (int j = 0; j < n_head0; ++j) a.head0_src[j] = head0_src_host[j];
+  TransPlan tplan;
+  build_trans_plan(*pol, *val, &tplan, &a);
+  if (!wt_params) {
+    set_error("harl_ppo_update: wt_params (transposed weights) required");
+    return HARL_E_ARG;
+  }
   int wmax = 0;
   for (int l = 0; l <= pol->n_layers; ++l) wmax = wmax > pol->dims[l] ? wmax : pol->dims[l];
   for (int l = 0; l <= val->n_layers; ++l) wmax = wmax > val->dims[l] ? wmax : val->dims[l];
   wmax = wmax > pol->n_head_cols ? wmax : pol->n_head_cols;
-  const size_t rsmem = sizeof(double) * (PPO_TM * (size_t)row_stride + 8);
-  (void)wmax;
+  // rows + the split-reduction partials (PPO_SPLIT x PPO_TM x widest layer)
+  const size_t rsmem = sizeof(double) * (PPO_TM * (size_t)row_stride + 8 +
+                                         (size_t)PPO_SPLIT * PPO_TM * wmax);
   if (phase & 1) {
   int rc2 = allow_smem(k_ppo_rows, rsmem, "k_ppo_rows");
   if (rc2) return rc2;
   if (B > 0) {
     HARL_PROF_BEGIN(st);
     k_ppo_rows<<<(unsigned)((B + PPO_TM - 1) / PPO_TM), PPO_THREADS, rsmem, st>>>(
-        a, *pol, *val, *ring, idx, params, rows, rowout);
+        a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
     HARL_CHECK_LAUNCH("k_ppo_rows");
   }
   HARL_PROF_BEGIN(st);
@@ -1072,6 +1124,8 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
     ad.pk.vec[ad.pk.n_vec++] = {pol->off_hb, pol->n_head_cols, whl + NHP * TC_H};
   }
   if (val_trunk_img) add_trunk(*val, (uint8_t*)val_trunk_img, true);
+  ad.tp = tplan;
+  ad.wt = wt_params;
   HARL_PROF_BEGIN(st);
   k_ppo_adam<<<296, 256, 0, st>>>(ad, adam_dev, bad, grads, params, adam_m,
                                    adam_v, params32);

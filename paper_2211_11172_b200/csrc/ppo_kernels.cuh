@@ -23,6 +23,9 @@ typedef harl_net_layout NetLayout;
 
 struct PpoArgs {
   int32_t B, F, C0, row_stride;
+  // offsets (doubles) of the transposed copies used by the backward pass:
+  // policy heads, policy W[l] and value W[l] for l >= 1
+  int64_t wt_head, wt_P[HARL_MAX_LAYERS], wt_V[HARL_MAX_LAYERS];
   int32_t B_norm;           // batch size in the 1/B normalisation (global)
   double clip_lo, clip_hi, w_ent, w_val;
   int16_t head0_src[HARL_MAX_HEAD0];
@@ -31,24 +34,38 @@ struct PpoArgs {
 typedef harl_replay_ring PpoRing;
 
 constexpr int PPO_TM = 2;
-constexpr int PPO_THREADS = 256;
+constexpr int PPO_THREADS = 128 * PPO_TM;   // 4 warps per row in the loss terms
 
 // Latency-bound small-batch layers: every thread keeps PPO_UNR weight
 // loads in flight (issued before the FMAs that consume them); the CTA's
 // row activations live in shared memory.
 constexpr int PPO_UNR = 16;
 
+// Each output is split over up to PPO_SPLIT threads along the reduction
+// (contiguous k ranges summed in part order: deterministic), so a thread's
+// chain of dependent weight-load rounds is PPO_SPLIT times shorter.
+constexpr int PPO_SPLIT = 4;
+
+__device__ inline int ppo_parts(int outputs) {
+  int p = (int)blockDim.x / (outputs > 0 ? outputs : 1);
+  return p < 1 ? 1 : (p > PPO_SPLIT ? PPO_SPLIT : p);
+}
+
 // out[r][c] = act(sum_k in[r][k] W[k][c] + b[c]) for r < rows
 __device__ inline void dense64(const double* in, int ldi, int K,
                                const double* __restrict__ W,
                                const double* __restrict__ b, int N, double* out,
-                               int ldo, bool act, int rows, double*) {
-  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+                               int ldo, bool act, int rows, double* part) {
+  const int P = ppo_parts(N);
+  const int kc = (K + P - 1) / P;
+  for (int t = threadIdx.x; t < N * P; t += blockDim.x) {
+    const int c = t % N, p = t / N;
+    const int k1 = min(K, (p + 1) * kc);
     double acc[PPO_TM];
 #pragma unroll
     for (int r = 0; r < PPO_TM; ++r) acc[r] = 0.0;
-    int k = 0;
-    for (; k + PPO_UNR <= K; k += PPO_UNR) {
+    int k = p * kc;
+    for (; k + PPO_UNR <= k1; k += PPO_UNR) {
       double w[PPO_UNR];
 #pragma unroll
       for (int q = 0; q < PPO_UNR; ++q) w[q] = __ldg(W + (int64_t)(k + q) * N + c);
@@ -58,50 +75,92 @@ __device__ inline void dense64(const double* in, int ldi, int K,
         for (int r = 0; r < PPO_TM; ++r)
           if (r < rows) acc[r] = fma(in[r * ldi + k + q], w[q], acc[r]);
     }
-    for (; k < K; ++k) {
+    for (; k < k1; ++k) {
       const double w = __ldg(W + (int64_t)k * N + c);
 #pragma unroll
       for (int r = 0; r < PPO_TM; ++r)
         if (r < rows) acc[r] = fma(in[r * ldi + k], w, acc[r]);
     }
-    for (int r = 0; r < rows; ++r) {
-      const double z = acc[r] + b[c];
+    if (P == 1) {
+      for (int r = 0; r < rows; ++r) {
+        const double z = acc[r] + b[c];
+        out[r * ldo + c] = act ? tanh(z) : z;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < PPO_TM; ++r) part[(p * PPO_TM + r) * N + c] = acc[r];
+    }
+  }
+  if (P > 1) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < N * rows; t += blockDim.x) {
+      const int c = t % N, r = t / N;
+      double z = part[r * N + c];
+      for (int p = 1; p < P; ++p) z += part[(p * PPO_TM + r) * N + c];
+      z += b[c];
       out[r * ldo + c] = act ? tanh(z) : z;
     }
   }
   __syncthreads();
 }
 
-// out[r][k] = (sum_c d[r][c] W[k][c]) * (1 - a[r][k]^2)
+__device__ inline double wsum64_(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// out[r][k] = (sum_c d[r][c] W[k][c]) * (1 - a[r][k]^2), reading the
+// transposed copy WT[c][k] (kept current by the Adam kernel) so that
+// threads over k load coalesced rows, with the same split reduction as
+// dense64.
 __device__ inline void back64(const double* d, int ldd, int N,
-                              const double* __restrict__ W, int K,
+                              const double* __restrict__ WT, int K,
                               const double* a, int lda, double* out, int ldo,
-                              int rows, double*) {
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+                              int rows, double* part) {
+  const int P = ppo_parts(K);
+  const int ncs = (N + P - 1) / P;
+  for (int t = threadIdx.x; t < K * P; t += blockDim.x) {
+    const int k = t % K, p = t / K;
+    const int c1 = min(N, (p + 1) * ncs);
     double acc[PPO_TM];
 #pragma unroll
     for (int r = 0; r < PPO_TM; ++r) acc[r] = 0.0;
-    const double* wr = W + (int64_t)k * N;
-    int c = 0;
-    for (; c + PPO_UNR <= N; c += PPO_UNR) {
+    int c = p * ncs;
+    for (; c + PPO_UNR <= c1; c += PPO_UNR) {
       double w[PPO_UNR];
 #pragma unroll
-      for (int q = 0; q < PPO_UNR; ++q) w[q] = __ldg(wr + c + q);
+      for (int q = 0; q < PPO_UNR; ++q) w[q] = __ldg(WT + (int64_t)(c + q) * K + k);
 #pragma unroll
       for (int q = 0; q < PPO_UNR; ++q)
 #pragma unroll
         for (int r = 0; r < PPO_TM; ++r)
           if (r < rows) acc[r] = fma(d[r * ldd + c + q], w[q], acc[r]);
     }
-    for (; c < N; ++c) {
-      const double w = __ldg(wr + c);
+    for (; c < c1; ++c) {
+      const double w = __ldg(WT + (int64_t)c * K + k);
 #pragma unroll
       for (int r = 0; r < PPO_TM; ++r)
         if (r < rows) acc[r] = fma(d[r * ldd + c], w, acc[r]);
     }
-    for (int r = 0; r < rows; ++r) {
+    if (P == 1) {
+      for (int r = 0; r < rows; ++r) {
+        const double av = a[r * lda + k];
+        out[r * ldo + k] = acc[r] * (1.0 - av * av);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < PPO_TM; ++r) part[(p * PPO_TM + r) * K + k] = acc[r];
+    }
+  }
+  if (P > 1) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < K * rows; t += blockDim.x) {
+      const int k = t % K, r = t / K;
+      double z = part[r * K + k];
+      for (int p = 1; p < P; ++p) z += part[(p * PPO_TM + r) * K + k];
       const double av = a[r * lda + k];
-      out[r * ldo + k] = acc[r] * (1.0 - av * av);
+      out[r * ldo + k] = z * (1.0 - av * av);
     }
   }
   __syncthreads();
@@ -121,13 +180,15 @@ __device__ inline double wsum64(double v) {
 __global__ void __launch_bounds__(PPO_THREADS)
 k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout P,
            const __grid_constant__ NetLayout V, PpoRing ring, const int32_t* idx,
-           const double* params, double* rows, double* rowout) {
+           const double* params, const double* wt, double* rows,
+           double* rowout) {
+  dbg_ts(40);
   extern __shared__ double srows[];
   const int r0 = blockIdx.x * PPO_TM;
   const int nrows = min(PPO_TM, a.B - r0);
   const int RS = a.row_stride;
   double* base = srows;  // this CTA's rows, copied out at the end
-  double* wbuf = srows + PPO_TM * RS;  // [PPO_KC][N + pad] weight chunk
+  double* wbuf = srows + PPO_TM * RS + 8;  // split-reduction partials
   __shared__ int16_t s_src[HARL_MAX_HEAD0];
   for (int i = threadIdx.x; i < a.C0; i += blockDim.x) s_src[i] = a.head0_src[i];
   // gather X (shared by both nets: P.row_act[0] == V.row_act[0])
@@ -136,67 +197,97 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
     base[rr * RS + P.row_act[0] + k] = ring.X[(int64_t)idx[r0 + rr] * a.F + k];
   }
   __syncthreads();
+  dbg_ts(41);
   // policy trunk (every layer tanh: rlcore.py:95-103 + 139)
   for (int l = 0; l < P.n_layers; ++l)
     dense64(base + P.row_act[l], RS, P.dims[l], params + P.off_W[l],
             params + P.off_b[l], P.dims[l + 1], base + P.row_act[l + 1], RS,
             true, nrows, wbuf);
+  dbg_ts(42);
   const int H = P.dims[P.n_layers];
   const int NH = P.n_head_cols;
   dense64(base + P.row_act[P.n_layers], RS, H, params + P.off_hW,
           params + P.off_hb, NH, base + P.row_head, RS, false, nrows, wbuf);
+  dbg_ts(43);
   // value net
   for (int l = 0; l < V.n_layers; ++l)
     dense64(base + V.row_act[l], RS, V.dims[l], params + V.off_W[l],
             params + V.off_b[l], V.dims[l + 1], base + V.row_act[l + 1], RS,
             l < V.n_layers - 1, nrows, wbuf);
-  // per-row PPO terms, one warp per row
+  dbg_ts(44);
+  // per-row PPO terms: warp w takes (row w/4, head w%4); the exps of a
+  // lane's columns are computed once and reused for the sum, the entropy
+  // and the gradient.  Per-(row, head) results meet in shared memory.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double invB = 1.0 / (double)a.B_norm;
-  for (int rr = warp; rr < nrows; rr += PPO_THREADS / 32) {
-    const int slot = idx[r0 + rr];
-    double* z = base + rr * RS + P.row_head;
-    const uint64_t mv = ring.move_bits[slot];
-    const uint32_t sb = ring.shift_bits[slot];
+  __shared__ double s_lp[PPO_TM][4], s_ent[PPO_TM][4];
+  const int rr = warp >> 2, h = warp & 3;
+  const bool active = rr < nrows && (PPO_THREADS / 32) >= 4 * PPO_TM;
+  constexpr int HI = 4;      // cached columns per lane (C0 <= 128)
+  double ev[HI];
+  double hm = 0.0, hs = 1.0, hls = 0.0, hent = 0.0;
+  int col = 0, c0 = 0, C = 0, slot = 0;
+  uint64_t mv = 0;
+  uint32_t sb = 0;
+  double* z = nullptr;
+  if (active) {
+    slot = idx[r0 + rr];
+    z = base + rr * RS + P.row_head;
+    mv = ring.move_bits[slot];
+    sb = ring.shift_bits[slot];
+    c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
+    C = h == 0 ? a.C0 : 3;
+    col = ring.actions[slot * 4 + h];
+  }
+  auto legal = [&](int j) -> bool {
+    if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
+    return (sb >> (3 * (h - 1) + j)) & 1u;
+  };
+  if (active) {
+    // pass 1: max, sum, entropy (rlcore.py:300-306)
+    double m = -INFINITY;
+    for (int j = lane; j < C; j += 32)
+      if (legal(j)) m = fmax(m, z[c0 + j]);
+    m = wmax64(m);
+    double sacc = 0.0;
+#pragma unroll
+    for (int i = 0; i < HI; ++i) {
+      const int j = lane + 32 * i;
+      ev[i] = 0.0;
+      if (j < C && legal(j)) ev[i] = exp(z[c0 + j] - m);
+      sacc += ev[i];
+    }
+    for (int j = lane + 32 * HI; j < C; j += 32)   // wide heads (C0 > 128)
+      if (legal(j)) sacc += exp(z[c0 + j] - m);
+    const double sh = wsum64(sacc);
+    const double ls = log(sh);
+    double e = 0.0;
+#pragma unroll
+    for (int i = 0; i < HI; ++i) {
+      const int j = lane + 32 * i;
+      if (j < C && legal(j)) e -= (ev[i] / sh) * (z[c0 + j] - m - ls);
+    }
+    for (int j = lane + 32 * HI; j < C; j += 32)
+      if (legal(j)) e -= (exp(z[c0 + j] - m) / sh) * (z[c0 + j] - m - ls);
+    e = wsum64(e);
+    hm = m;
+    hs = sh;
+    hls = ls;
+    hent = e;
+    if (lane == 0) {
+      // log-prob of the taken action; ring actions hold the COMPACT column
+      // for head 0 (policy kernel output head0_col)
+      s_lp[rr][h] = z[c0 + col] - m - ls;
+      s_ent[rr][h] = e;
+    }
+  }
+  __syncthreads();
+  if (active) {
+    const double logp_new = ((s_lp[rr][0] + s_lp[rr][1]) + s_lp[rr][2]) + s_lp[rr][3];
+    const double ent_total = ((s_ent[rr][0] + s_ent[rr][1]) + s_ent[rr][2]) + s_ent[rr][3];
     const double logp_old = ring.scalars[slot * 4 + 0];
     const double adv = ring.scalars[slot * 4 + 2];
     const double td = ring.scalars[slot * 4 + 3];
-    // pass 1: per-head max, sum, entropy (rlcore.py:300-306)
-    double hmax[4], hsum[4], hlogs[4], hent[4];
-    double logp_new = 0.0, ent_total = 0.0;
-    for (int h = 0; h < 4; ++h) {
-      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
-      const int C = h == 0 ? a.C0 : 3;
-      auto legal = [&](int j) -> bool {
-        if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
-        return (sb >> (3 * (h - 1) + j)) & 1u;
-      };
-      double m = -INFINITY;
-      for (int j = lane; j < C; j += 32)
-        if (legal(j)) m = fmax(m, z[c0 + j]);
-      m = wmax64(m);
-      double s = 0.0;
-      for (int j = lane; j < C; j += 32)
-        if (legal(j)) s += exp(z[c0 + j] - m);
-      s = wsum64(s);
-      const double ls = log(s);
-      double e = 0.0;
-      for (int j = lane; j < C; j += 32)
-        if (legal(j)) e -= (exp(z[c0 + j] - m) / s) * (z[c0 + j] - m - ls);
-      e = wsum64(e);
-      hmax[h] = m;
-      hsum[h] = s;
-      hlogs[h] = ls;
-      hent[h] = e;
-      ent_total += e;
-    }
-    // log-prob of the taken actions; ring actions hold the COMPACT
-    // column for head 0 (policy kernel output head0_col)
-    for (int h = 0; h < 4; ++h) {
-      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
-      const int col = ring.actions[slot * 4 + h];
-      logp_new += z[c0 + col] - hmax[h] - hlogs[h];
-    }
     const double ratio = exp(logp_new - logp_old);
     const double clipped = fmin(fmax(ratio, a.clip_lo), a.clip_hi);
     const double s_un = ratio * adv, s_cl = clipped * adv;
@@ -204,28 +295,24 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
     const double dlogp = -coef * invB;
     const double went = a.w_ent * invB;
     // pass 2: dz in place over the logits
-    for (int h = 0; h < 4; ++h) {
-      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
-      const int C = h == 0 ? a.C0 : 3;
-      const int col = ring.actions[slot * 4 + h];
-      auto legal = [&](int j) -> bool {
-        if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
-        return (sb >> (3 * (h - 1) + j)) & 1u;
-      };
-      __syncwarp();
-      for (int j = lane; j < C; j += 32) {
-        double dz = 0.0;
+    for (int j = lane, i = 0; j < C; j += 32, ++i) {
+      {
+        double dz;
         if (legal(j)) {
-          const double lp = z[c0 + j] - hmax[h] - hlogs[h];
-          const double p = exp(z[c0 + j] - hmax[h]) / hsum[h];
-          dz = dlogp * ((j == col ? 1.0 : 0.0) - p) + went * p * (lp + hent[h]);
+          const double lp = z[c0 + j] - hm - hls;
+          double evj = 0.0;
+#pragma unroll
+          for (int q = 0; q < HI; ++q) evj = q == i ? ev[q] : evj;
+          if (i >= HI) evj = exp(z[c0 + j] - hm);
+          const double p = evj / hs;
+          dz = dlogp * ((j == col ? 1.0 : 0.0) - p) + went * p * (lp + hent);
         } else {
           dz = dlogp * ((j == col ? 1.0 : 0.0) - 0.0);
         }
         z[c0 + j] = dz;
       }
     }
-    if (lane == 0) {
+    if (h == 0 && lane == 0) {
       const double v = base[rr * RS + V.row_act[V.n_layers]];
       double* o = rowout + (int64_t)(r0 + rr) * 4;
       o[0] = fmin(s_un, s_cl);
@@ -237,20 +324,24 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
     }
   }
   __syncthreads();
+  dbg_ts(45);
   // policy backward: dhid = dz . Wh^T, times (1 - hid^2)
-  back64(base + P.row_head, RS, NH, params + P.off_hW, H,
+  back64(base + P.row_head, RS, NH, wt + a.wt_head, H,
          base + P.row_act[P.n_layers], RS, base + P.row_delta[P.n_layers - 1],
          RS, nrows, wbuf);
   for (int l = P.n_layers - 1; l >= 1; --l)
-    back64(base + P.row_delta[l], RS, P.dims[l + 1], params + P.off_W[l],
+    back64(base + P.row_delta[l], RS, P.dims[l + 1], wt + a.wt_P[l],
            P.dims[l], base + P.row_act[l], RS, base + P.row_delta[l - 1], RS,
            nrows, wbuf);
+  dbg_ts(46);
   for (int l = V.n_layers - 1; l >= 1; --l)
-    back64(base + V.row_delta[l], RS, V.dims[l + 1], params + V.off_W[l],
+    back64(base + V.row_delta[l], RS, V.dims[l + 1], wt + a.wt_V[l],
            V.dims[l], base + V.row_act[l], RS, base + V.row_delta[l - 1], RS,
            nrows, wbuf);
+  dbg_ts(47);
   double* out = rows + (int64_t)r0 * RS;
   for (int i = threadIdx.x; i < nrows * RS; i += blockDim.x) out[i] = base[i];
+  dbg_ts(48);
 }
 
 // (b) loss terms: lane l sums rows l, l+32, ... in order, then a fixed xor
@@ -378,11 +469,36 @@ struct PackPlan {
   int32_t n_mat, n_vec;
 };
 
+// fp64 transposed copies of the matrices the PPO backward pass reads
+// (WT[n][k] = W[k][n] at wt + dst)
+struct TransMat {
+  int64_t off, dst;
+  int32_t K, N;
+};
+struct TransPlan {
+  TransMat m[2 * HARL_MAX_LAYERS + 2];
+  int32_t n;
+  int64_t total;
+};
+
 struct AdamArgs {
   int64_t n_pi, n;
   harl_ppo_hyper h;
   PackPlan pk;
+  TransPlan tp;
+  double* wt;
 };
+
+__global__ void k_wt_fill(TransPlan tp, const double* params, double* wt) {
+  for (int q = 0; q < tp.n; ++q) {
+    const TransMat& M = tp.m[q];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+         e < (int64_t)M.K * M.N; e += (int64_t)gridDim.x * blockDim.x) {
+      const int k = (int)(e / M.N), nn = (int)(e % M.N);
+      wt[M.dst + (int64_t)nn * M.K + k] = params[M.off + e];
+    }
+  }
+}
 
 __global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* bad,
                            const double* grads, double* params, double* m,
@@ -430,6 +546,15 @@ __global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* ba
       const int64_t e = i - V.off;
       if (e >= 0 && e < V.len) V.dst[e] = p32;
     }
+    if (a.wt)
+      for (int q = 0; q < a.tp.n; ++q) {
+        const TransMat& M = a.tp.m[q];
+        const int64_t e = i - M.off;
+        if (e >= 0 && e < (int64_t)M.K * M.N) {
+          const int k = (int)(e / M.N), nn = (int)(e % M.N);
+          a.wt[M.dst + (int64_t)nn * M.K + k] = p;
+        }
+      }
   }
 }
 

@@ -96,7 +96,7 @@ __device__ inline int sample3(const float* z, uint32_t m3, double u,
   return ok ? idx : -1;
 }
 
-__global__ void __launch_bounds__(SAMPLE_THREADS)
+__global__ void __launch_bounds__(SAMPLE_THREADS, 8)
 k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ PcgJump J,
               const __grid_constant__ LaneJump LJ, u128 base_arg,
@@ -104,11 +104,6 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const uint8_t* __restrict__ knobs, SampleArgs a) {
   dbg_ts(16);
   __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
-  for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
-    s_src[i] = sk.head0_src[i];
-    s_dst[i] = sk.head0_dst[i];
-  }
-  __syncthreads();
   (void)LJ;
   const int g = threadIdx.x & (SG - 1);
   const int64_t r = (int64_t)blockIdx.x * (SAMPLE_THREADS / SG) + threadIdx.x / SG;
@@ -116,29 +111,56 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   const bool live = r < a.n;
   const int64_t rr = live ? r : 0;
   const int S = sk.num_slots, C0 = sk.n_head0;
-  // ---- uniforms: lane h of the group draws head h ---------------------
-  double u_mine = 0.0;
-  if (!a.inject && g < 4) {
-    const u128 base = base_dev ? *base_dev : base_arg;
-    const int64_t row = a.grow ? (int64_t)a.grow[rr] : rr;
-    const uint64_t k = (uint64_t)g * (uint64_t)a.m_total + (uint64_t)row + 1;
-    u_mine = u64_to_unit(pcg_draw64(J, base, k));
+  const bool draw = !a.inject && g < 4;
+  // ---- every global load of the row is issued before any math ----------
+  u128 base = base_arg;
+  int64_t grow_r = rr;
+  if (draw) {
+    if (base_dev) base = *base_dev;
+    if (a.grow) grow_r = (int64_t)a.grow[rr];
   }
-  dbg_ts(17);
-  // ---- current state: lane g holds slots g, g+8, ... --------------------
-  uint64_t mv = 0;
   int tv[HARL_MAX_SLOTS / SG];
 #pragma unroll
   for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i) {
     const int s = g + SG * i;
     tv[i] = s < sk.local_slots ? tiles[(int64_t)s * a.ld + rr] : 0;
-    if (tv[i] > 1) mv |= 1ull << s;
   }
+  const int ca0 = knobs[rr], par0 = knobs[a.ld + rr], ur0 = knobs[2 * a.ld + rr];
+  const float* z = a.logits + rr * a.ldz;
+  const int nI = (C0 + SG - 1) / SG;
+  float zc[SAMPLE_MAXI];   // head-0 logits j = g + 8i (padding reads as -inf)
+  float z3[3] = {0.f, 0.f, 0.f};   // shift head g+1's three logits (lanes 0-2)
+  if (!a.inject) {
+#pragma unroll
+    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+      const int j = g + SG * i;
+      zc[i] = (i < nI && j < C0) ? z[j] : -INFINITY;
+    }
+    if (g < 3) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) z3[j] = z[C0 + 3 * g + j];
+    }
+  }
+  for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
+    s_src[i] = sk.head0_src[i];
+    s_dst[i] = sk.head0_dst[i];
+  }
+  __syncthreads();
+  // ---- uniforms: lane h of the group draws head h ---------------------
+  double u_mine = 0.0;
+  if (draw) {
+    const uint64_t k = (uint64_t)g * (uint64_t)a.m_total + (uint64_t)grow_r + 1;
+    u_mine = u64_to_unit(pcg_draw64(J, base, k));
+  }
+  dbg_ts(17);
+  // ---- current state: lane g holds slots g, g+8, ... --------------------
+  uint64_t mv = 0;
+#pragma unroll
+  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i)
+    if (tv[i] > 1) mv |= 1ull << (g + SG * i);
 #pragma unroll
   for (int o = SG / 2; o; o >>= 1) mv |= __shfl_xor_sync(0xffffffffu, mv, o, SG);
-  const int ca0 = knobs[rr], par0 = knobs[a.ld + rr], ur0 = knobs[2 * a.ld + rr];
   const uint32_t sb = shift_bits_of(sk, ca0, par0, ur0);
-  const float* z = a.logits + rr * a.ldz;
   dbg_ts(18);
   auto legal0 = [&](int j) -> bool {
     return j == C0 - 1 || ((mv >> s_src[j]) & 1ull);
@@ -170,15 +192,6 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     }
   } else {
     const double u0 = __shfl_sync(0xffffffffu, u_mine, 0, SG);
-    const int nI = (C0 + SG - 1) / SG;
-    // this lane's head-0 logits, all loads in flight at once; illegal and
-    // padding columns read as -inf
-    float zc[SAMPLE_MAXI];
-#pragma unroll
-    for (int i = 0; i < SAMPLE_MAXI; ++i) {
-      const int j = g + SG * i;
-      zc[i] = (i < nI && j < C0) ? z[j] : -INFINITY;
-    }
     float zmax = -INFINITY;
 #pragma unroll
     for (int i = 0; i < SAMPLE_MAXI; ++i) {
@@ -208,16 +221,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     const double inv = 1.0 / s;
     int count = 0;
     double carry = 0.0;
-    for (int i = 0; i < nI; ++i) {
-      const int j = g + SG * i;
-      float ei;
-      if (i < SAMPLE_MAXI) {
-        ei = 0.f;
-#pragma unroll
-        for (int q = 0; q < SAMPLE_MAXI; ++q) ei = (q == i) ? e[q] : ei;
-      } else {
-        ei = (j < C0 && legal0(j)) ? expf(z[j] - zmax) : 0.f;
-      }
+    auto cdf_step = [&](int j, float ei) {
       double c = (double)ei * inv;
 #pragma unroll
       for (int o = 1; o < SG; o <<= 1) {
@@ -227,6 +231,15 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
       c += carry;
       if (j < C0 && c < u0) ++count;
       carry = __shfl_sync(0xffffffffu, c, SG - 1, SG);
+    };
+#pragma unroll
+    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+      if (i >= nI) break;   // uniform across the warp
+      cdf_step(g + SG * i, e[i]);
+    }
+    for (int i = SAMPLE_MAXI; i < nI; ++i) {
+      const int j = g + SG * i;
+      cdf_step(j, (j < C0 && legal0(j)) ? expf(z[j] - zmax) : 0.f);
     }
     count = gsumi(count);
     dbg_ts(20);
@@ -243,7 +256,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     const double uh = __shfl_sync(0xffffffffu, u_mine, hh < 4 ? hh : 0, SG);
     if (hh < 4) {
       const uint32_t m3 = (sb >> (3 * (hh - 1))) & 7u;
-      const int j = sample3(z + C0 + 3 * (hh - 1), m3, uh, &lph);
+      const int j = sample3(z3, m3, uh, &lph);
       ah = j < 0 ? 0 : j;
     }
     dbg_ts(21);

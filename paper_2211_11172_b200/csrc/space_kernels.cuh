@@ -135,6 +135,31 @@ __device__ inline void footprint_l1l2(const harl_sketch_desc& sk,
   *l2o = l2;
 }
 
+// one footprint level alone (level 1: t = innermost tiles, every stage
+// adds (inter+extra)*last; level 2: t = product of the two innermost
+// levels, inter only at the root) -- the same integer sums as
+// footprint_l1l2, split so two threads can take one level each
+__device__ inline int64_t footprint_level(const harl_sketch_desc& sk,
+                                          const int64_t* t, bool level1,
+                                          bool root) {
+  int64_t l = 0;
+  for (int s = 0; s < sk.n_stages; ++s) {
+    int64_t sacc = 0, o = 0;
+    const int tf = sk.stage_first[s], tn = sk.stage_ntensors[s];
+    for (int ti = tf; ti < tf + tn; ++ti) {
+      int64_t e = 1;
+      const int f = sk.tensor_first[ti], nt = sk.tensor_nterms[ti];
+      for (int q = f; q < f + nt; ++q) e *= (int64_t)sk.term_sc[q] * t[sk.term_gi[q]] + sk.term_off[q];
+      sacc += e;
+      o = e;
+    }
+    const int64_t inter = sk.stage_inter[s], extra = sk.stage_extra[s];
+    sacc += level1 ? (inter + extra) * o : extra * o + (root ? inter * o : 0);
+    l += sacc;
+  }
+  return l;
+}
+
 // one feature row into dst[0..F)
 __device__ inline void featurize_row(const harl_sketch_desc& sk,
                                      const uint16_t* tiles,
@@ -188,6 +213,8 @@ k_featurize(const __grid_constant__ harl_sketch_desc sk, const uint16_t* tiles,
 // the log2 LUT are copied into shared memory with all loads in flight at
 // once; each thread then featurizes its row from shared memory.
 constexpr int FEAT2_ROWS = 128;
+constexpr int FEAT2_PARTS = 4;     // threads per row
+constexpr int FEAT2_THREADS = FEAT2_ROWS * FEAT2_PARTS;
 constexpr int FEAT2_LUT_MAX = 4096;
 
 __host__ __device__ inline size_t feat2_smem_bytes(int F, int local_slots,
@@ -197,7 +224,7 @@ __host__ __device__ inline size_t feat2_smem_bytes(int F, int local_slots,
          (((size_t)FEAT2_ROWS * local_slots * 2 + FEAT2_ROWS * 3 + 15) & ~(size_t)15);
 }
 
-__global__ void __launch_bounds__(FEAT2_ROWS)
+__global__ void __launch_bounds__(FEAT2_THREADS)
 k_featurize2(const __grid_constant__ harl_sketch_desc sk,
              const uint16_t* __restrict__ tiles,
              const uint8_t* __restrict__ knobs, int64_t n, int64_t ld,
@@ -219,40 +246,71 @@ k_featurize2(const __grid_constant__ harl_sketch_desc sk,
     // (16 rows per chunk) and the LUT; chunks past `rows` stay inside the
     // allocation because ld is a multiple of 16
     const int cs = (rows + 7) / 8, ck = (rows + 15) / 16;
-    for (int i = threadIdx.x; i < S * cs; i += FEAT2_ROWS) {
+    for (int i = threadIdx.x; i < S * cs; i += FEAT2_THREADS) {
       const int sl = i / cs, c = i % cs;
       cp_async16(stile + sl * FEAT2_ROWS + 8 * c, tiles + (int64_t)sl * ld + r0 + 8 * c);
     }
-    for (int i = threadIdx.x; i < 3 * ck; i += FEAT2_ROWS) {
+    for (int i = threadIdx.x; i < 3 * ck; i += FEAT2_THREADS) {
       const int k = i / ck, c = i % ck;
       cp_async16(sknob + k * FEAT2_ROWS + 16 * c, knobs + (int64_t)k * ld + r0 + 16 * c);
     }
     if (slut) {
       const int nl = sk.max_extent + 1;
-      for (int i = threadIdx.x; i < nl / 2; i += FEAT2_ROWS)
+      for (int i = threadIdx.x; i < nl / 2; i += FEAT2_THREADS)
         cp_async16(lut + 2 * i, sk.log2_lut + 2 * i);
       if ((nl & 1) && threadIdx.x == 0) lut[nl - 1] = sk.log2_lut[nl - 1];
     }
     cp_async_wait_all();
   } else {
-    for (int s0 = 0; s0 < S; ++s0)
-      if ((int)threadIdx.x < rows)
-        stile[s0 * FEAT2_ROWS + threadIdx.x] = tiles[(int64_t)s0 * ld + r0 + threadIdx.x];
-    for (int k = 0; k < 3; ++k)
-      if ((int)threadIdx.x < rows)
-        sknob[k * FEAT2_ROWS + threadIdx.x] = knobs[(int64_t)k * ld + r0 + threadIdx.x];
+    for (int i = threadIdx.x; i < S * FEAT2_ROWS; i += FEAT2_THREADS)
+      if (i % FEAT2_ROWS < rows)
+        stile[i] = tiles[(int64_t)(i / FEAT2_ROWS) * ld + r0 + i % FEAT2_ROWS];
+    for (int i = threadIdx.x; i < 3 * FEAT2_ROWS; i += FEAT2_THREADS)
+      if (i % FEAT2_ROWS < rows)
+        sknob[i] = knobs[(int64_t)(i / FEAT2_ROWS) * ld + r0 + i % FEAT2_ROWS];
     if (slut)
-      for (int i = threadIdx.x; i <= sk.max_extent; i += FEAT2_ROWS) lut[i] = sk.log2_lut[i];
+      for (int i = threadIdx.x; i <= sk.max_extent; i += FEAT2_THREADS) lut[i] = sk.log2_lut[i];
   }
   __syncthreads();
   dbg_ts(33);
-  if (threadIdx.x < rows)
-    featurize_row(sk, stile, sknob, FEAT2_ROWS, threadIdx.x,
-                  sfeat + threadIdx.x * F, lut);
+  for (int i = threadIdx.x; i < rows * F; i += FEAT2_THREADS) sfeat[i] = 0.0;
+  __syncthreads();
+  {
+    // part 0: tile logs + knob features; parts 1/2: one footprint level
+    // and its log10 each; part 3: the flops feature
+    const int part = threadIdx.x / FEAT2_ROWS, rl = threadIdx.x % FEAT2_ROWS;
+    if (rl < rows) {
+      const int L = sk.levels;
+      double* dst = sfeat + rl * F;
+      const int ca = sknob[rl];
+      int pos = sk.max_feature_dims * L;
+      if (part == 0) {
+        for (int d = 0; d < sk.ndims; ++d)
+          for (int lv = 0; lv < L; ++lv)
+            dst[d * L + lv] = (slut ? lut : sk.log2_lut)[stile[(d * L + lv) * FEAT2_ROWS + rl]];
+        const int par = sknob[FEAT2_ROWS + rl], ur = sknob[2 * FEAT2_ROWS + rl];
+        dst[pos] = sk.ncas > 1 ? __ddiv_rn((double)ca, (double)(sk.ncas - 1)) : 0.0;
+        dst[pos + 1] = sk.max_fusible ? __ddiv_rn((double)par, (double)sk.max_fusible) : 0.0;
+        dst[pos + 2 + ur] = 1.0;
+      } else if (part == 1 || part == 2) {
+        int64_t t[HARL_MAX_DIMS];
+        for (int d = 0; d < sk.ndims; ++d) {
+          const int vl = stile[(d * L + L - 1) * FEAT2_ROWS + rl];
+          t[d] = (part == 2 && L >= 2)
+                     ? (int64_t)stile[(d * L + L - 2) * FEAT2_ROWS + rl] * vl : vl;
+        }
+        const int64_t l = footprint_level(sk, t, part == 1, ca == 0);
+        pos += 2 + sk.n_unroll;
+        dst[pos + part - 1] = __ddiv_rn(glibc_log10_ge1(__dadd_rn(1.0, (double)l)), 6.0);
+      } else {
+        dst[pos + 2 + sk.n_unroll + 2] = sk.flops_feature;
+      }
+    }
+  }
   __syncthreads();
   dbg_ts(34);
   double* out = feat + r0 * F;
-  for (int i = threadIdx.x; i < rows * F; i += FEAT2_ROWS) out[i] = sfeat[i];
+  for (int i = threadIdx.x; i < rows * F; i += FEAT2_THREADS) out[i] = sfeat[i];
   dbg_ts(35);
 }
 

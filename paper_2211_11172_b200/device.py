@@ -418,6 +418,9 @@ class DeviceAgent:
                                     device=dev)
         self.losses = torch.zeros(16, dtype=torch.float64, device=dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        # transposed fp64 copies for the PPO backward (kept current by Adam)
+        self.wt = torch.zeros(max(1, int(N.load().harl_ppo_wt_doubles(
+            C.byref(pl), C.byref(vl)))), dtype=torch.float64, device=dev)
         self.tc = (hidden == (128, 128) and F <= 64 and self.NH <= 128
                    and os.environ.get("HARL_KERNELS", "tc") != "ffma")
         self._hid = None
@@ -504,6 +507,12 @@ class DeviceAgent:
         self.params32.copy_(p.float())
         self.m.copy_(torch.from_numpy(self._pack(a.opt_pi.m, a.opt_v.m)))
         self.v.copy_(torch.from_numpy(self._pack(a.opt_pi.v, a.opt_v.v)))
+        lib = N.load()
+        with PF.span("wt_fill", 0):
+            N.check(lib.harl_ppo_wt_fill(C.byref(self.pol_layout),
+                                         C.byref(self.val_layout),
+                                         _ptr(self.params), _ptr(self.wt),
+                                         _stream()), "harl_ppo_wt_fill")
         if getattr(self, "packed", None) is not None:
             self.repack()
 
@@ -580,7 +589,7 @@ class DeviceAgent:
             _ptr(losses), _ptr(self.bad), _ptr(scratch), _ptr(adam_dev),
             *(([_ptr(self.packed["pt"]), _ptr(self.packed["ph"]),
                 _ptr(self.packed["vt"])]) if self.tc else [None, None, None]),
-            int(B_norm or B), phase, _stream()),
+            _ptr(self.wt), int(B_norm or B), phase, _stream()),
             "harl_ppo_update")
         return losses
 

@@ -21,6 +21,7 @@ NAMES = ["start", "init", "x_staged", "w1_ready", "mma1", "epi1", "mma2",
 SNAMES = ["start", "rng", "state", "softmax", "cdf", "shift_heads", "decided", "end"]
 GNAMES = ["start", "x0", "walk0", "sum0", "x1", "walk1", "sum1"]
 FNAMES = ["start", "staged", "rows", "end"]
+PNAMES = ["start", "gather", "pol_fwd", "heads", "val_fwd", "terms", "pol_bwd", "val_bwd", "end"]
 
 
 def main():
@@ -29,7 +30,7 @@ def main():
     tb = w["tables"]
     forest = D.DeviceForest(w["trees"], w["base"], w["lr"])
     eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, use_graphs=False)
-    cfg = EpisodeConfig(tracks=P, track_len=1, cull_window=20,
+    cfg = EpisodeConfig(tracks=P, track_len=2, cull_window=20,
                         cull_fraction=0.5, min_tracks=P // 2)
     lib = N.load()
     gen = np.random.default_rng(0)
@@ -40,7 +41,8 @@ def main():
         ts = np.zeros(64, dtype=np.uint64)
         N.check(lib.harl_debug_timestamps(0, ts.ctypes.data_as(C.c_void_p), 64), "dbg")
         for nm, lo, names in (("policy", 0, NAMES), ("sample", 16, SNAMES),
-                              ("gbt", 24, GNAMES), ("featurize", 32, FNAMES)):
+                              ("gbt", 24, GNAMES), ("featurize", 32, FNAMES),
+                              ("ppo_rows", 40, PNAMES)):
             t = ts[lo:lo + len(names)].astype(np.int64)
             rel = (t - t[0]) / 1e3
             print(f"rep {rep} {nm}: " + " ".join(f"{n}={r:.2f}" for n, r in zip(names, rel)))

@@ -13,6 +13,17 @@ namespace harl {
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 
+// Programmatic dependent launch (sm_90+): every kernel waits for its
+// predecessor grid (completion + memory visibility) before touching global
+// memory, then lets its own dependents launch; without the launch
+// attribute both are no-ops.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Launch accounting and the optional per-kernel timer (harl_profile_*).
 // Every library launch is bracketed by HARL_PROF_BEGIN(stream) and
 // HARL_CHECK_LAUNCH(name); with the timer on (and the stream not being
@@ -41,6 +52,17 @@ __device__ inline void cp_async16(void* smem, const void* gmem) {
 }
 __device__ inline void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// grid extent probe: earliest CTA start / latest CTA end of one kernel
+// (slots 60/61; harl_debug_timestamps resets them with on=1)
+__device__ inline void dbg_grid(bool end, int slot = 60) {
+  if (threadIdx.x == 0 && g_dbg_on == 2) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (end) atomicMax(&g_dbg_ts[slot + 1], t);
+    else atomicMin(&g_dbg_ts[slot], t);
+  }
 }
 
 #define HARL_PROF_BEGIN(st) ::harl::prof_begin((cudaStream_t)(st))

@@ -21,16 +21,17 @@ struct FinishArgs {
   int64_t keep_from;    // rows >= keep_from survive in the ring
 };
 
-__global__ void __launch_bounds__(128)
-k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
-              const __grid_constant__ harl_replay_ring ring,
-              const __grid_constant__ harl_entry_log log,
-              const __grid_constant__ harl_track_stats ts,
-              const int64_t* wpos_dev) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t wpos = wpos_dev ? *wpos_dev : a.wpos;
-  if (r >= a.n) return;
+constexpr int FIN_ROWS = 64;       // rows per CTA
+constexpr int FIN_THREADS = 256;   // row work on the first 64, copy on all
+
+__device__ inline void finish_row(const FinishArgs& a,
+                                  const harl_step_buffers& io,
+                                  const harl_replay_ring& ring,
+                                  const harl_entry_log& log,
+                                  const harl_track_stats& ts, int64_t wpos,
+                                  int64_t r) {
   const int32_t* __restrict__ row_track = io.row_track;
+  (void)FIN_THREADS;
   const uint16_t* __restrict__ tiles_new = io.tiles_new;
   const uint8_t* __restrict__ knobs_new = io.knobs_new;
   uint16_t* __restrict__ log_tiles = log.tiles;
@@ -113,6 +114,52 @@ k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
   ring.shift_bits[slot] = sb;
 }
 
+// Per step: the row bookkeeping above for 64 rows, then the CTA copies the
+// surviving rows' X and X' into their replay slots.  The rows' features are
+// contiguous in both [n][F] arrays, so the loads are coalesced; slots are
+// consecutive modulo cap.
+__global__ void __launch_bounds__(FIN_THREADS)
+k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
+              const __grid_constant__ harl_replay_ring ring,
+              const __grid_constant__ harl_entry_log log,
+              const __grid_constant__ harl_track_stats ts,
+              const int64_t* wpos_dev) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  const int64_t r0 = (int64_t)blockIdx.x * FIN_ROWS;
+  const int64_t wpos = wpos_dev ? *wpos_dev : a.wpos;
+  if (threadIdx.x < FIN_ROWS && r0 + threadIdx.x < a.n)
+    finish_row(a, io, ring, log, ts, wpos, r0 + threadIdx.x);
+  if (!a.rl) return;
+  const int64_t lo = r0 > a.keep_from ? r0 : a.keep_from;
+  const int64_t hi = r0 + FIN_ROWS < a.n ? r0 + FIN_ROWS : a.n;
+  if (lo >= hi) return;
+  const int F = a.F;
+  const int total = (int)(hi - lo) * F;
+  const double* sx = io.feat + lo * F;
+  const double* sxn = io.feat_new + lo * F;
+  constexpr int U = 8;
+  for (int e0 = threadIdx.x; e0 < total; e0 += FIN_THREADS * U) {
+    double vx[U], vxn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * FIN_THREADS;
+      vx[u] = e < total ? sx[e] : 0.0;
+      vxn[u] = e < total ? sxn[e] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * FIN_THREADS;
+      if (e < total) {
+        const int rr = e / F, k = e - rr * F;
+        const int64_t slot = (wpos + lo + rr) % ring.cap;
+        ring.X[slot * F + k] = vx[u];
+        ring.Xn[slot * F + k] = vxn[u];
+      }
+    }
+  }
+}
+
 // replay feature rows (X, X') of the surviving pushes: one warp per row,
 // lanes over features (coalesced), 32-bit index math
 __global__ void __launch_bounds__(256)
@@ -120,6 +167,8 @@ k_ring_rows(int64_t n, int64_t keep_from, int32_t F, int64_t wpos_arg,
             const int64_t* wpos_dev, const double* __restrict__ feat,
             const double* __restrict__ feat_new,
             const __grid_constant__ harl_replay_ring ring) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int lane = threadIdx.x & 31;
   const int64_t wpos = wpos_dev ? *wpos_dev : wpos_arg;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -150,6 +199,8 @@ __global__ void k_gather_rows(GatherArgs a, const int32_t* idx,
                               const int32_t* row_track, uint16_t* tiles_o,
                               uint8_t* knobs_o, double* feat_o, double* score_o,
                               int32_t* row_track_o) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n_out) return;
   const int64_t r = idx[i];

@@ -34,6 +34,8 @@ k_gbt_predict(const GbtNode* __restrict__ nodes,
               const double* __restrict__ feat, int64_t n, int32_t F,
               double* score, const double* old_score, double* reward,
               int32_t rows_per_cta) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ double contrib[];  // [rows_per_cta][n_trees]
   const int g = threadIdx.x % GBT_GROUPS;
   const int rl = threadIdx.x / GBT_GROUPS;
@@ -94,6 +96,8 @@ k_gbt_predict2(const GbtNode* __restrict__ gnodes,
                double floor_value, const double* __restrict__ feat, int64_t n,
                int32_t F, double* score, const double* old_score,
                double* reward) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   dbg_ts(24);
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint64_t fbar, xbar[2];

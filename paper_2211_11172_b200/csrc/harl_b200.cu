@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <utility>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -44,6 +45,8 @@ int cuda_status(cudaError_t e, const char* where) {
 // kernel's start, not the moment an idle stream saw the event.
 
 __global__ void k_spin(unsigned long long ns) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   unsigned long long t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   do {
@@ -145,6 +148,39 @@ static int sm_count() {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
   }
   return v;
+}
+
+// Every library kernel is launched through launch_k: with HARL_PDL=1 the
+// launch carries the programmatic-stream-serialization attribute, so the
+// next kernel's CTAs are scheduled (and run their pre-wait prologue) while
+// the previous grid drains; griddep_wait() inside each kernel keeps the
+// data dependency exact.
+static bool use_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HARL_PDL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (use_pdl()) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // HARL_TC_GEN1=1 selects the first-generation 4-warp tcgen05 kernels
@@ -291,7 +327,7 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
     const int64_t todo = count - a.t0;
     const int threads = 256;
     HARL_PROF_BEGIN(st);
-    k_init_sample<<<(unsigned)((todo + threads - 1) / threads), threads, 0, st>>>(
+    launch_k(k_init_sample, dim3((unsigned)((todo + threads - 1) / threads)), dim3(threads), 0, st, 
         *sk, J, a, tiles, knobs, bad);
     HARL_CHECK_LAUNCH("k_init_sample");
     unsigned long long first = 0;
@@ -307,7 +343,7 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
     InitArgs one = a;
     one.j0 = a.j0 + (uint64_t)(first - a.t0) * (uint64_t)a.per_track;
     HARL_PROF_BEGIN(st);
-    k_init_one<<<1, 1, 0, st>>>(*sk, J, one, (int64_t)first, tiles, knobs, used);
+    launch_k(k_init_one, dim3(1), dim3(1), 0, st, *sk, J, one, (int64_t)first, tiles, knobs, used);
     HARL_CHECK_LAUNCH("k_init_one");
     unsigned long long u = 0;
     e = cudaMemcpyAsync(&u, used, 8, cudaMemcpyDeviceToHost, st);
@@ -341,11 +377,11 @@ int harl_uniform_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
   int64_t* offset = (int64_t*)((char*)scratch + 4 * n * 4);
   unsigned long long* misc = (unsigned long long*)(offset + 4 * n);
   HARL_PROF_BEGIN(st);
-  k_uniform_counts<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(*sk, tiles, knobs,
+  launch_k(k_uniform_counts, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, st, *sk, tiles, knobs,
                                                                 n, ld, count);
   HARL_CHECK_LAUNCH("k_uniform_counts");
   HARL_PROF_BEGIN(st);
-  k_uniform_scan<<<1, 1024, 0, st>>>(count, 4 * n, offset, (int64_t*)&misc[1]);
+  launch_k(k_uniform_scan, dim3(1), dim3(1024), 0, st, count, 4 * n, offset, (int64_t*)&misc[1]);
   HARL_CHECK_LAUNCH("k_uniform_scan");
   PcgJump J;
   build_jump(*rng, &J);
@@ -372,7 +408,7 @@ int harl_uniform_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
     if (e != cudaSuccess) return cuda_status(e, "uniform memcpy");
     const int64_t todo = 4 * n - i0;
     HARL_PROF_BEGIN(st);
-    k_uniform_draw<<<(unsigned)((todo + 127) / 128), 128, 0, st>>>(
+    launch_k(k_uniform_draw, dim3((unsigned)((todo + 127) / 128)), dim3(128), 0, st, 
         *sk, J, a, i0, j0, tiles, knobs, count, offset, actions, misc);
     HARL_CHECK_LAUNCH("k_uniform_draw");
     unsigned long long bad = 0;
@@ -385,7 +421,7 @@ int harl_uniform_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
     if ((e = d2h(&offset[bad], &off_b, 8)) != cudaSuccess) return cuda_status(e, "uniform sync");
     const uint64_t jb = j0 + (uint64_t)(off_b - off_i0);
     HARL_PROF_BEGIN(st);
-    k_uniform_one<<<1, 1, 0, st>>>(*sk, J, a, (int64_t)bad, jb, tiles, knobs,
+    launch_k(k_uniform_one, dim3(1), dim3(1), 0, st, *sk, J, a, (int64_t)bad, jb, tiles, knobs,
                                    count, actions, &misc[2]);
     HARL_CHECK_LAUNCH("k_uniform_one");
     unsigned long long used = 0;
@@ -410,16 +446,14 @@ int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
   if (smem2 <= (size_t)max_dyn_smem()) {
     if ((rc = allow_smem(k_featurize2, smem2, "k_featurize2"))) return rc;
     HARL_PROF_BEGIN((cudaStream_t)stream);
-    k_featurize2<<<(unsigned)((n + FEAT2_ROWS - 1) / FEAT2_ROWS), FEAT2_THREADS, smem2,
-                   (cudaStream_t)stream>>>(*sk, tiles, knobs, n, ld, feat);
+    launch_k(k_featurize2, dim3((unsigned)((n + FEAT2_ROWS - 1) / FEAT2_ROWS)), dim3(FEAT2_THREADS), smem2, (cudaStream_t)stream, *sk, tiles, knobs, n, ld, feat);
     HARL_CHECK_LAUNCH("k_featurize2");
     return HARL_OK;
   }
   const size_t smem = sizeof(double) * FEAT_THREADS * sk->feature_len;
   if ((rc = allow_smem(k_featurize, smem, "k_featurize"))) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_featurize<<<(unsigned)((n + FEAT_THREADS - 1) / FEAT_THREADS), FEAT_THREADS,
-                smem, (cudaStream_t)stream>>>(*sk, tiles, knobs, n, ld, feat);
+  launch_k(k_featurize, dim3((unsigned)((n + FEAT_THREADS - 1) / FEAT_THREADS)), dim3(FEAT_THREADS), smem, (cudaStream_t)stream, *sk, tiles, knobs, n, ld, feat);
   HARL_CHECK_LAUNCH("k_featurize");
   return HARL_OK;
 }
@@ -431,7 +465,7 @@ int harl_action_masks(const harl_sketch_desc* sk, const uint16_t* tiles,
   if (rc) return rc;
   if (n <= 0) return HARL_OK;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_action_masks<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+  launch_k(k_action_masks, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, (cudaStream_t)stream, 
       *sk, tiles, knobs, n, ld, tiling, shift);
   HARL_CHECK_LAUNCH("k_action_masks");
   return HARL_OK;
@@ -445,7 +479,7 @@ int harl_apply_actions(const harl_sketch_desc* sk, const uint16_t* tiles,
   if (rc) return rc;
   if (n <= 0) return HARL_OK;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_apply_actions<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+  launch_k(k_apply_actions, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, (cudaStream_t)stream, 
       *sk, tiles, knobs, n, ld, actions, tiles_out, knobs_out,
       (unsigned long long*)status);
   HARL_CHECK_LAUNCH("k_apply_actions");
@@ -474,12 +508,12 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
     if (rc) return rc;
     HARL_PROF_BEGIN((cudaStream_t)stream);
     if (smem_nodes)
-      k_gbt_predict2<true><<<(unsigned)grid, GBT2_THREADS, smem, (cudaStream_t)stream>>>(
+      launch_k(k_gbt_predict2<true>, dim3((unsigned)grid), dim3(GBT2_THREADS), smem, (cudaStream_t)stream, 
           (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
           forest->n_nodes, forest->fitted, forest->base, forest->floor_value, feat,
           n, F, score, old_score, reward);
     else
-      k_gbt_predict2<false><<<(unsigned)grid, GBT2_THREADS, smem, (cudaStream_t)stream>>>(
+      launch_k(k_gbt_predict2<false>, dim3((unsigned)grid), dim3(GBT2_THREADS), smem, (cudaStream_t)stream, 
           (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
           forest->n_nodes, forest->fitted, forest->base, forest->floor_value, feat,
           n, F, score, old_score, reward);
@@ -491,8 +525,7 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
   int rc = allow_smem(k_gbt_predict, smem1, "k_gbt_predict");
   if (rc) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_gbt_predict<<<(unsigned)((n + rows - 1) / rows), GBT_THREADS, smem1,
-                  (cudaStream_t)stream>>>(
+  launch_k(k_gbt_predict, dim3((unsigned)((n + rows - 1) / rows)), dim3(GBT_THREADS), smem1, (cudaStream_t)stream, 
       (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
       forest->fitted, forest->base, forest->floor_value, feat, n, feature_len,
       score, old_score, reward, rows);
@@ -537,8 +570,7 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   sr.grow = grow;
   sr.m_total = m_total;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_policy_step<<<(unsigned)((n + MLP_TM - 1) / MLP_TM), MLP_THREADS, smem,
-                  (cudaStream_t)stream>>>(*sk, *pol, J, sr, feat, tiles, knobs, n,
+  launch_k(k_policy_step, dim3((unsigned)((n + MLP_TM - 1) / MLP_TM)), dim3(MLP_THREADS), smem, (cudaStream_t)stream, *sk, *pol, J, sr, feat, tiles, knobs, n,
                                           ld, inject, actions, logp, tiles_out,
                                           knobs_out, move_bits, shift_bits,
                                           head0_col, logits_out,
@@ -597,8 +629,7 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   a.m_total = m_total > 0 ? m_total : n;
   const int rows_per_cta = SAMPLE_THREADS / SG;
   HARL_PROF_BEGIN(st);
-  k_sample_rows<<<(unsigned)((n + rows_per_cta - 1) / rows_per_cta),
-                  SAMPLE_THREADS, 0, st>>>(*sk, J, LJ, base,
+  launch_k(k_sample_rows, dim3((unsigned)((n + rows_per_cta - 1) / rows_per_cta)), dim3(SAMPLE_THREADS), 0, st, *sk, J, LJ, base,
                                            (const u128*)rng_state_dev, tiles,
                                            knobs, a);
   HARL_CHECK_LAUNCH("k_sample_rows");
@@ -653,7 +684,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     const int64_t tiles_n = (n + 127) / 128;
     const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
     HARL_PROF_BEGIN(st);
-    k_policy_tc<<<grid, TC2_THREADS, tc2_smem(NHP), st>>>(pa);
+    launch_k(k_policy_tc, dim3(grid), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
     HARL_CHECK_LAUNCH("k_policy_tc");
     return launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
                           TC_H, n, ld, tiles, knobs, inject, actions, logp,
@@ -676,7 +707,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   const int64_t tiles_n = (n + 127) / 128;
   const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
   HARL_PROF_BEGIN(st);
-  k_trunk_tc<TRUNK_POLICY><<<grid, 128, TRUNK_SMEM, st>>>(ta);
+  launch_k(k_trunk_tc<TRUNK_POLICY>, dim3(grid), dim3(128), TRUNK_SMEM, st, ta);
   HARL_CHECK_LAUNCH("k_trunk_tc<policy>");
   HeadsArgs ha;
   ha.hid = hid_scratch;
@@ -690,7 +721,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   const size_t smem = (size_t)2 * ha.NHP * TC_H * 4 + HEADS_NMAX * 4;
   if ((rc = allow_smem(k_heads_tc, smem, "k_heads_tc"))) return rc;
   HARL_PROF_BEGIN(st);
-  k_heads_tc<<<grid, 128, smem, st>>>(ha);
+  launch_k(k_heads_tc, dim3(grid), dim3(128), smem, st, ha);
   HARL_CHECK_LAUNCH("k_heads_tc");
   return launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
                         TC_H, n, ld,
@@ -729,7 +760,7 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
     const int64_t tiles_n = (n0 + 127) / 128 + (va.n1 + 127) / 128;
     const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
     HARL_PROF_BEGIN((cudaStream_t)stream);
-    k_value_tc<<<grid, TC2_THREADS, smem, (cudaStream_t)stream>>>(va);
+    launch_k(k_value_tc, dim3(grid), dim3(TC2_THREADS), smem, (cudaStream_t)stream, va);
     HARL_CHECK_LAUNCH("k_value_tc");
     return HARL_OK;
   }
@@ -754,7 +785,7 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
   const int64_t tiles_n = (n0 + 127) / 128 + (ta.n1 + 127) / 128;
   const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_trunk_tc<TRUNK_VALUE><<<grid, 128, TRUNK_SMEM, (cudaStream_t)stream>>>(ta);
+  launch_k(k_trunk_tc<TRUNK_VALUE>, dim3(grid), dim3(128), TRUNK_SMEM, (cudaStream_t)stream, ta);
   HARL_CHECK_LAUNCH("k_trunk_tc<value>");
   return HARL_OK;
 }
@@ -776,6 +807,52 @@ int harl_prepare(void) {
   if ((rc = allow_max_smem(k_policy_tc, "k_policy_tc"))) return rc;
   if ((rc = allow_max_smem(k_value_tc, "k_value_tc"))) return rc;
   if ((rc = allow_max_smem(k_ppo_rows, "k_ppo_rows"))) return rc;
+  // One shared-memory carveout for every kernel: the episode alternates
+  // 230 KB-smem tcgen05 kernels with smem-light ones, and a carveout change
+  // between consecutive kernels makes the SMs drain and reconfigure.
+  // HARL_CARVEOUT=default keeps the driver's per-kernel choice.
+  const char* cv = getenv("HARL_CARVEOUT");
+  if (!cv || strcmp(cv, "default") != 0) {
+    auto carve = [](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared);
+    };
+  carve(k_spin);
+  carve(k_init_sample);
+  carve(k_init_one);
+  carve(k_uniform_counts);
+  carve(k_uniform_scan);
+  carve(k_uniform_draw);
+  carve(k_uniform_one);
+  carve(k_featurize);
+  carve(k_featurize2);
+  carve(k_action_masks);
+  carve(k_apply_actions);
+  carve(k_gbt_predict);
+  carve(k_gbt_predict2<true>);
+  carve(k_gbt_predict2<false>);
+  carve(k_policy_step);
+  carve(k_value_forward);
+  carve(k_sample_rows);
+  carve(k_trunk_tc<TRUNK_POLICY>);
+  carve(k_trunk_tc<TRUNK_VALUE>);
+  carve(k_heads_tc);
+  carve(k_pack_trunk);
+  carve(k_pack_heads);
+  carve(k_policy_tc);
+  carve(k_value_tc);
+  carve(k_finish_step);
+  carve(k_ring_rows);
+  carve(k_gather_rows);
+  carve(k_ppo_rows);
+  carve(k_ppo_losses);
+  carve(k_ppo_wgrad);
+  carve(k_ppo_finalize);
+  carve(k_ppo_adam);
+  carve(k_wt_fill);
+  carve(k_tc_probe);
+    cudaGetLastError();
+  }
   (void)sm_count();
   return HARL_OK;
 }
@@ -802,7 +879,7 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     ta.W2 = pol->W[1];
     ta.b2 = pol->b[1];
     HARL_PROF_BEGIN(st);
-    k_pack_trunk<<<64, 256, 0, st>>>(ta, (uint8_t*)pol_trunk, 0);
+    launch_k(k_pack_trunk, dim3(64), dim3(256), 0, st, ta, (uint8_t*)pol_trunk, 0);
     HARL_CHECK_LAUNCH("k_pack_trunk<policy>");
     HeadsArgs ha;
     memset(&ha, 0, sizeof(ha));
@@ -811,7 +888,7 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     ha.NH = pol->n_head_cols;
     ha.NHP = (ha.NH + 15) / 16 * 16;
     HARL_PROF_BEGIN(st);
-    k_pack_heads<<<64, 256, 0, st>>>(ha, (uint8_t*)pol_heads);
+    launch_k(k_pack_heads, dim3(64), dim3(256), 0, st, ha, (uint8_t*)pol_heads);
     HARL_CHECK_LAUNCH("k_pack_heads");
   }
   if (val && val_trunk) {
@@ -829,7 +906,7 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     ta.w3 = val->W[2];
     ta.b3 = val->b[2];
     HARL_PROF_BEGIN(st);
-    k_pack_trunk<<<64, 256, 0, st>>>(ta, (uint8_t*)val_trunk, 1);
+    launch_k(k_pack_trunk, dim3(64), dim3(256), 0, st, ta, (uint8_t*)val_trunk, 1);
     HARL_CHECK_LAUNCH("k_pack_trunk<value>");
   }
   return HARL_OK;
@@ -851,8 +928,7 @@ int harl_value_forward(const harl_mlp_desc* val, const double* feat, int64_t n,
   const size_t smem = sizeof(float) * 2 * MLP_TM * (size_t)ldbuf;
   if ((rc = allow_smem(k_value_forward, smem, "k_value_forward"))) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_value_forward<<<(unsigned)((n + MLP_TM - 1) / MLP_TM), MLP_THREADS, smem,
-                    (cudaStream_t)stream>>>(*val, feat, n, feature_len, v_out, ldbuf);
+  launch_k(k_value_forward, dim3((unsigned)((n + MLP_TM - 1) / MLP_TM)), dim3(MLP_THREADS), smem, (cudaStream_t)stream, *val, feat, n, feature_len, v_out, ldbuf);
   HARL_CHECK_LAUNCH("k_value_forward");
   return HARL_OK;
 }
@@ -884,17 +960,9 @@ int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
   if (ring) rg = *ring;
   if (rg.cap < 1) rg.cap = 1;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_finish_step<<<(unsigned)((n + 63) / 64), 64, 0, (cudaStream_t)stream>>>(
-      a, *io, rg, *log, *ts, wpos_dev);
+  launch_k(k_finish_step, dim3((unsigned)((n + FIN_ROWS - 1) / FIN_ROWS)), dim3(FIN_THREADS),
+           0, (cudaStream_t)stream, a, *io, rg, *log, *ts, wpos_dev);
   HARL_CHECK_LAUNCH("k_finish_step");
-  if (rl && n > keep_from) {
-    const int64_t rows = n - keep_from;
-    const int64_t blocks = (rows + 7) / 8 < 2 * 148 ? (rows + 7) / 8 : 2 * 148;
-    HARL_PROF_BEGIN((cudaStream_t)stream);
-    k_ring_rows<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        n, keep_from, feature_len, wpos, wpos_dev, io->feat, io->feat_new, rg);
-    HARL_CHECK_LAUNCH("k_ring_rows");
-  }
   return HARL_OK;
 }
 
@@ -913,7 +981,7 @@ int harl_gather_rows(const int32_t* idx, int64_t n_out, int32_t local_slots,
   a.local_slots = local_slots;
   a.F = feature_len;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_gather_rows<<<(unsigned)((n_out + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  launch_k(k_gather_rows, dim3((unsigned)((n_out + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, 
       a, idx, tiles, knobs, feat, score, row_track, tiles_o, knobs_o, feat_o,
       score_o, row_track_o);
   HARL_CHECK_LAUNCH("k_gather_rows");
@@ -955,7 +1023,7 @@ int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
   int rc = allow_smem(k_tc_probe, smem, "k_tc_probe");
   if (rc) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_tc_probe<<<1, 128, smem, (cudaStream_t)stream>>>(A, B, D, mode);
+  launch_k(k_tc_probe, dim3(1), dim3(128), smem, (cudaStream_t)stream, A, B, D, mode);
   HARL_CHECK_LAUNCH("k_tc_probe");
   return HARL_OK;
 }
@@ -1000,7 +1068,7 @@ int harl_ppo_wt_fill(const harl_net_layout* pol, const harl_net_layout* val,
   TransPlan tp;
   build_trans_plan(*pol, *val, &tp, nullptr);
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  k_wt_fill<<<148, 256, 0, (cudaStream_t)stream>>>(tp, params, wt);
+  launch_k(k_wt_fill, dim3(148), dim3(256), 0, (cudaStream_t)stream, tp, params, wt);
   HARL_CHECK_LAUNCH("k_wt_fill");
   return HARL_OK;
 }
@@ -1072,29 +1140,31 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   if (rc2) return rc2;
   if (B > 0) {
     HARL_PROF_BEGIN(st);
-    k_ppo_rows<<<(unsigned)((B + PPO_TM - 1) / PPO_TM), PPO_THREADS, rsmem, st>>>(
+    launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM)), dim3(PPO_THREADS), rsmem, st, 
         a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
     HARL_CHECK_LAUNCH("k_ppo_rows");
   }
   HARL_PROF_BEGIN(st);
-  k_ppo_losses<<<1, 32, 0, st>>>(B, rowout, losses);
+  launch_k(k_ppo_losses, dim3(1), dim3(32), 0, st, B, rowout, losses, phase == 3 ? B_norm : 0,
+                                 hp->entropy_weight, hp->value_loss_weight, bad);
   HARL_CHECK_LAUNCH("k_ppo_losses");
   GradJobs jt;
   memset(&jt, 0, sizeof(jt));
   for (int j = 0; j < n_jobs; ++j) jt.j[j] = jobs[j];
   jt.n = n_jobs;
   HARL_PROF_BEGIN(st);
-  k_ppo_wgrad<<<(unsigned)n_tiles, 256, 0, st>>>(jt, B, row_stride, rows, grads,
-                                                 bad);
+  launch_k(k_ppo_wgrad, dim3((unsigned)n_tiles), dim3(256), 0, st, jt, B, row_stride, rows, grads,
+                                                 bad, phase == 3 ? 1 : 0);
   HARL_CHECK_LAUNCH("k_ppo_wgrad");
   }
   if (!(phase & 2)) return HARL_OK;
-  HARL_PROF_BEGIN(st);
-  k_ppo_finalize<<<148, 256, 0, st>>>(B_norm, hp->entropy_weight,
-                                      hp->value_loss_weight, losses, grads,
-                                      n_params, bad);
-  HARL_CHECK_LAUNCH("k_ppo_finalize");
-  HARL_CHECK_LAUNCH("k_ppo_wgrad");
+  if (phase == 2) {   // sharded: means and checks over the all-reduced sums
+    HARL_PROF_BEGIN(st);
+    launch_k(k_ppo_finalize, dim3(148), dim3(256), 0, st, B_norm, hp->entropy_weight,
+                                        hp->value_loss_weight, losses, grads,
+                                        n_params, bad);
+    HARL_CHECK_LAUNCH("k_ppo_finalize");
+  }
   AdamArgs ad;
   memset(&ad, 0, sizeof(ad));
   ad.n_pi = n_pi;
@@ -1127,7 +1197,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   ad.tp = tplan;
   ad.wt = wt_params;
   HARL_PROF_BEGIN(st);
-  k_ppo_adam<<<296, 256, 0, st>>>(ad, adam_dev, bad, grads, params, adam_m,
+  launch_k(k_ppo_adam, dim3(296), dim3(256), 0, st, ad, adam_dev, bad, grads, params, adam_m,
                                    adam_v, params32);
   HARL_CHECK_LAUNCH("k_ppo_adam");
   return HARL_OK;
@@ -1138,6 +1208,12 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
 long long harl_launch_count(void) { return g_launches.load(); }
 
 int harl_debug_timestamps(int on, unsigned long long* out_host, int n) {
+  if (on) {
+    unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+    cudaError_t e0 = cudaMemcpyToSymbol(g_dbg_ts, init, sizeof(init),
+                                        60 * sizeof(unsigned long long));
+    if (e0 != cudaSuccess) return cuda_status(e0, "harl_debug_timestamps");
+  }
   cudaError_t e = cudaMemcpyToSymbol(g_dbg_on, &on, sizeof(int));
   if (e != cudaSuccess) return cuda_status(e, "harl_debug_timestamps");
   if (out_host && n > 0) {

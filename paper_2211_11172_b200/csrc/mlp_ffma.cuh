@@ -379,6 +379,8 @@ k_policy_step(const __grid_constant__ harl_sketch_desc sk,
               double* logp, uint16_t* tiles_out, uint8_t* knobs_out,
               uint64_t* move_bits, uint32_t* shift_bits, int32_t* head0_col,
               float* logits_out, unsigned long long* status, int ldbuf) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ float smem[];
   float* bufA = smem;
   float* bufB = smem + MLP_TM * ldbuf;
@@ -414,6 +416,8 @@ k_policy_step(const __grid_constant__ harl_sketch_desc sk,
 __global__ void __launch_bounds__(MLP_THREADS)
 k_value_forward(const __grid_constant__ harl_mlp_desc net, const double* feat,
                 int64_t n, int32_t F, float* v_out, int ldbuf) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ float smem[];
   float* bufA = smem;
   float* bufB = smem + MLP_TM * ldbuf;

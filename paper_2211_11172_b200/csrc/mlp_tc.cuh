@@ -102,6 +102,8 @@ constexpr int TRUNK_IMAGE = (TRUNK_SMEM + 15) / 16 * 16;
 // persistent kernels then pull it in with a few bulk copies instead of
 // re-splitting ~25 K weights per CTA per launch.
 __global__ void k_pack_trunk(TrunkArgs a, uint8_t* img, int value_mode) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   uint8_t* w1h = img;
   uint8_t* w1l = w1h + TC_K1 * TC_H * 4;
   uint8_t* w2h = w1l + TC_K1 * TC_H * 4;
@@ -133,6 +135,8 @@ __global__ void k_pack_trunk(TrunkArgs a, uint8_t* img, int value_mode) {
 
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) k_trunk_tc(TrunkArgs a) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* w1h = sm;
   uint8_t* w1l = w1h + TC_K1 * TC_H * 4;
@@ -268,6 +272,8 @@ __host__ __device__ inline int heads_image_bytes(int NHP) {
 }
 
 __global__ void k_pack_heads(HeadsArgs h, uint8_t* img) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int NHP = h.NHP;
   uint8_t* whh = img;
   uint8_t* whl = whh + NHP * TC_H * 4;
@@ -286,6 +292,8 @@ __global__ void k_pack_heads(HeadsArgs h, uint8_t* img) {
 }
 
 __global__ void __launch_bounds__(128, 1) k_heads_tc(HeadsArgs h) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ __align__(1024) uint8_t sm[];
   const int NHP = h.NHP;
   uint8_t* whh = sm;

@@ -96,6 +96,8 @@ struct PolicyTcArgs {
 };
 
 __global__ void __launch_bounds__(TC2_THREADS, 1) k_policy_tc(PolicyTcArgs a) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   dbg_ts(0);
   extern __shared__ __align__(128) uint8_t sm2[];
   uint8_t* sm = sm2;
@@ -252,6 +254,8 @@ __host__ __device__ inline int tc2_value_smem() { return TC2_W1 + TC2_W2 + TC2_V
 // weights take the rest of shared memory); the next tile's first half is
 // prefetched as soon as the current tile's X is in TMEM.
 __global__ void __launch_bounds__(TC2_THREADS, 1) k_value_tc(ValueTcArgs a) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ __align__(128) uint8_t sm3[];
   uint8_t* rA = sm3;
   uint8_t* rB = sm3 + TC2_W1;

@@ -182,6 +182,8 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
            const __grid_constant__ NetLayout V, PpoRing ring, const int32_t* idx,
            const double* params, const double* wt, double* rows,
            double* rowout) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   dbg_ts(40);
   extern __shared__ double srows[];
   const int r0 = blockIdx.x * PPO_TM;
@@ -348,14 +350,36 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
 // tree (deterministic).  losses[5..8] = the per-row sums (min surrogate,
 // entropy, ratio, squared value error) -- the quantities a sharded update
 // all-reduces; k_ppo_finalize turns them into the reported means.
-__global__ void k_ppo_losses(int B, const double* rowout, double* losses) {
+__device__ inline void ppo_loss_means(int B, double w_ent, double w_val,
+                                      double* losses, int32_t* bad) {
+  const double policy_loss = -(losses[5] / B);
+  const double entropy = losses[6] / B;
+  const double a_loss = policy_loss - w_ent * entropy;
+  const double v_loss = w_val * (losses[8] / B);
+  losses[0] = a_loss;
+  losses[1] = v_loss;
+  losses[2] = policy_loss;
+  losses[3] = entropy;
+  losses[4] = losses[7] / B;
+  if (!isfinite(a_loss) || !isfinite(v_loss)) atomicOr(bad, 1);
+}
+
+// means_B > 0 (single device): also the reported means and the loss
+// finiteness check, for a batch of means_B rows
+__global__ void k_ppo_losses(int B, const double* rowout, double* losses,
+                             int means_B, double w_ent, double w_val,
+                             int32_t* bad) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int lane = threadIdx.x;
   double q[4] = {0, 0, 0, 0};
   for (int r = lane; r < B; r += 32)
     for (int j = 0; j < 4; ++j) q[j] += rowout[r * 4 + j];
   for (int j = 0; j < 4; ++j) q[j] = wsum64(q[j]);
-  if (lane == 0)
+  if (lane == 0) {
     for (int j = 0; j < 4; ++j) losses[5 + j] = q[j];
+    if (means_B > 0) ppo_loss_means(means_B, w_ent, w_val, losses, bad);
+  }
 }
 
 // means (rlcore.py:311-312,355; [0] actor loss, [1] value loss, [2] policy
@@ -364,18 +388,9 @@ __global__ void k_ppo_losses(int B, const double* rowout, double* losses) {
 __global__ void k_ppo_finalize(int B, double w_ent, double w_val,
                                double* losses, const double* grads,
                                int64_t n, int32_t* bad) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const double policy_loss = -(losses[5] / B);
-    const double entropy = losses[6] / B;
-    const double a_loss = policy_loss - w_ent * entropy;
-    const double v_loss = w_val * (losses[8] / B);
-    losses[0] = a_loss;
-    losses[1] = v_loss;
-    losses[2] = policy_loss;
-    losses[3] = entropy;
-    losses[4] = losses[7] / B;
-    if (!isfinite(a_loss) || !isfinite(v_loss)) atomicOr(bad, 1);
-  }
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  if (blockIdx.x == 0 && threadIdx.x == 0) ppo_loss_means(B, w_ent, w_val, losses, bad);
   int nonfinite = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -391,20 +406,29 @@ struct GradJob {
   int32_t tile_first;            // first tile index of this job
 };
 
-constexpr int WG_T = 32;  // 32x32 output tile, 256 threads x 4 outputs
+constexpr int WG_T = 16;    // 16x16 output tile, one output per thread
+constexpr int WG_RB = 128;  // rows staged per pass (static smem <= 48 KB)
 
 struct GradJobs {
   GradJob j[4 * (HARL_MAX_LAYERS + 2)];
   int32_t n;
 };
 
+// Every gradient element is one thread's in-order sum over the batch rows
+// (the same single-accumulator order as before, so results are unchanged);
+// a CTA stages its 16 A columns and 16 D columns for 256 rows at a time
+// with all loads in flight.  check_finite: flag non-finite gradients here
+// (rlcore.py:368-373) so no separate scan is needed on a single device.
 __global__ void __launch_bounds__(256)
 k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
-            const double* rows, double* grads, int32_t* bad) {
+            const double* __restrict__ rows, double* grads, int32_t* bad,
+            int check_finite) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const GradJob* jobs = jt.j;
   const int n_jobs = jt.n;
-  __shared__ double sa[WG_T][WG_T + 1];
-  __shared__ double sd[WG_T][WG_T + 1];
+  __shared__ double sa[WG_RB][WG_T];
+  __shared__ double sd[WG_RB][WG_T];
   __shared__ int s_job;
   if (threadIdx.x == 0) {
     int j = 0;
@@ -417,33 +441,40 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
   const int ni = jb.ni == 0 ? 1 : jb.ni;
   const int tiles_j = (jb.nj + WG_T - 1) / WG_T;
   const int i0 = (tile / tiles_j) * WG_T, j0 = (tile % tiles_j) * WG_T;
-  const int tj = threadIdx.x % WG_T, ti = threadIdx.x / WG_T;  // ti 0..7
-  double acc[4] = {0, 0, 0, 0};
-  for (int rb = 0; rb < B; rb += WG_T) {
-    for (int e = threadIdx.x; e < WG_T * WG_T; e += blockDim.x) {
+  const int tj = threadIdx.x % WG_T, ti = threadIdx.x / WG_T;
+  const bool ones = jb.ni == 0;
+  double acc = 0.0;
+  for (int rb = 0; rb < B; rb += WG_RB) {
+    const int nr = min(WG_RB, B - rb);
+    // element e of the 128x16 slab: row e/16, column e%16
+    constexpr int PER = WG_RB * WG_T / 256;   // 8 per thread per operand
+    double va[PER], vd[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + 256 * u;
       const int rr = e / WG_T, cc = e % WG_T;
-      const int r = rb + rr;
-      double av = 0.0, dv = 0.0;
-      if (r < B) {
-        if (i0 + cc < ni) av = jb.ni == 0 ? 1.0 : rows[(int64_t)r * RS + jb.a_off + i0 + cc];
-        if (j0 + cc < jb.nj) dv = rows[(int64_t)r * RS + jb.d_off + j0 + cc];
-      }
-      sa[rr][cc] = av;
-      sd[rr][cc] = dv;
+      const int64_t rowoff = (int64_t)(rb + rr) * RS;
+      vd[u] = (rr < nr && j0 + cc < jb.nj) ? rows[rowoff + jb.d_off + j0 + cc] : 0.0;
+      va[u] = (!ones && rr < nr && i0 + cc < ni) ? rows[rowoff + jb.a_off + i0 + cc] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      sd[e / WG_T][e % WG_T] = vd[u];
+      sa[e / WG_T][e % WG_T] = va[u];
     }
     __syncthreads();
-    for (int rr = 0; rr < WG_T; ++rr) {
-      const double dv = sd[rr][tj];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = fma(sa[rr][ti + 8 * q], dv, acc[q]);
+    if (ones) {
+      for (int rr = 0; rr < nr; ++rr) acc = fma(1.0, sd[rr][tj], acc);
+    } else {
+      for (int rr = 0; rr < nr; ++rr) acc = fma(sa[rr][ti], sd[rr][tj], acc);
     }
     __syncthreads();
   }
-  (void)bad;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int i = i0 + ti + 8 * q, j = j0 + tj;
-    if (i < ni && j < jb.nj) grads[jb.g_off + (int64_t)i * jb.nj + j] = acc[q];
+  const int i = i0 + ti, j = j0 + tj;
+  if (i < ni && j < jb.nj) {
+    grads[jb.g_off + (int64_t)i * jb.nj + j] = acc;
+    if (check_finite && !isfinite(acc)) atomicOr(bad, 2);
   }
 }
 
@@ -490,6 +521,8 @@ struct AdamArgs {
 };
 
 __global__ void k_wt_fill(TransPlan tp, const double* params, double* wt) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   for (int q = 0; q < tp.n; ++q) {
     const TransMat& M = tp.m[q];
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -503,7 +536,11 @@ __global__ void k_wt_fill(TransPlan tp, const double* params, double* wt) {
 __global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* bad,
                            const double* grads, double* params, double* m,
                            double* v, float* params32) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  dbg_ts(50);
   if (*bad) return;
+  dbg_ts(51);
   if (adam_dev) {  // graph replay: this update's 1 - beta^t from device memory
     a.h.b1t_pi = adam_dev[0];
     a.h.b2t_pi = adam_dev[1];
@@ -533,7 +570,8 @@ __global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* ba
       const PackMat& M = a.pk.mat[q];
       const int64_t e = i - M.off;
       if (e >= 0 && e < (int64_t)M.K * M.N) {
-        const int k = (int)(e / M.N), nn = (int)(e % M.N);
+        const uint32_t ue = (uint32_t)e, un = (uint32_t)M.N;
+        const int k = (int)(ue / un), nn = (int)(ue % un);
         float hi, lo;
         tc::split_tf32(p32, hi, lo);
         const uint32_t o = tc::kmajor_off(nn, k, M.Kpad) / 4;
@@ -546,16 +584,19 @@ __global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* ba
       const int64_t e = i - V.off;
       if (e >= 0 && e < V.len) V.dst[e] = p32;
     }
+    dbg_ts(52);
     if (a.wt)
       for (int q = 0; q < a.tp.n; ++q) {
         const TransMat& M = a.tp.m[q];
         const int64_t e = i - M.off;
         if (e >= 0 && e < (int64_t)M.K * M.N) {
-          const int k = (int)(e / M.N), nn = (int)(e % M.N);
+          const uint32_t ue = (uint32_t)e, un = (uint32_t)M.N;
+          const int k = (int)(ue / un), nn = (int)(ue % un);
           a.wt[M.dst + (int64_t)nn * M.K + k] = p;
         }
       }
   }
+  dbg_ts(53);
 }
 
 }  // namespace harl

@@ -102,7 +102,10 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ LaneJump LJ, u128 base_arg,
               const u128* base_dev, const uint16_t* __restrict__ tiles,
               const uint8_t* __restrict__ knobs, SampleArgs a) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   dbg_ts(16);
+  dbg_grid(false, 60);
   __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
   (void)LJ;
   const int g = threadIdx.x & (SG - 1);
@@ -336,6 +339,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     report_status(a.status, r, code);
   }
   dbg_ts(23);
+  dbg_grid(true, 60);
 }
 
 }  // namespace harl

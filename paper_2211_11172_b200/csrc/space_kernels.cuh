@@ -57,6 +57,8 @@ __global__ void k_init_sample(const __grid_constant__ harl_sketch_desc sk,
                               const __grid_constant__ InitArgs a,
                               uint16_t* tiles, uint8_t* knobs,
                               unsigned long long* first_bad) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   int64_t t = a.t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.count) return;
   uint64_t j = a.j0 + (uint64_t)(t - a.t0) * (uint64_t)a.per_track;
@@ -82,6 +84,8 @@ __global__ void k_init_one(const __grid_constant__ harl_sketch_desc sk,
                            const __grid_constant__ InitArgs a, int64_t t,
                            uint16_t* tiles, uint8_t* knobs,
                            unsigned long long* used) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint64_t j = a.j0;
   uint32_t v[HARL_MAX_DIMS + 3];
@@ -198,6 +202,8 @@ constexpr int FEAT_THREADS = 128;
 __global__ void __launch_bounds__(FEAT_THREADS)
 k_featurize(const __grid_constant__ harl_sketch_desc sk, const uint16_t* tiles,
             const uint8_t* knobs, int64_t n, int64_t ld, double* feat) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ double sfeat[];
   const int F = sk.feature_len;
   const int64_t r0 = (int64_t)blockIdx.x * FEAT_THREADS;
@@ -229,7 +235,10 @@ k_featurize2(const __grid_constant__ harl_sketch_desc sk,
              const uint16_t* __restrict__ tiles,
              const uint8_t* __restrict__ knobs, int64_t n, int64_t ld,
              double* __restrict__ feat) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   dbg_ts(32);
+  if (blockIdx.x == 0) dbg_grid(true, 61);   // CTA 0 start of the latest launch -> slot 62
   extern __shared__ __align__(16) unsigned char fsm[];
   const int F = sk.feature_len, S = sk.local_slots;
   double* sfeat = (double*)fsm;
@@ -312,6 +321,7 @@ k_featurize2(const __grid_constant__ harl_sketch_desc sk,
   double* out = feat + r0 * F;
   for (int i = threadIdx.x; i < rows * F; i += FEAT2_THREADS) out[i] = sfeat[i];
   dbg_ts(35);
+  dbg_grid(true, 62);
 }
 
 // ---------------------------------------------------------------------------
@@ -341,6 +351,8 @@ __global__ void k_action_masks(const __grid_constant__ harl_sketch_desc sk,
                                const uint16_t* tiles, const uint8_t* knobs,
                                int64_t n, int64_t ld, uint8_t* tiling,
                                uint8_t* shift) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int S = sk.num_slots, L = sk.levels;
@@ -405,6 +417,8 @@ __global__ void k_apply_actions(const __grid_constant__ harl_sketch_desc sk,
                                 int64_t n, int64_t ld, const int32_t* actions,
                                 uint16_t* tiles_out, uint8_t* knobs_out,
                                 unsigned long long* status) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int code = apply_row(sk, tiles, knobs, ld, r, actions[r], actions[n + r],
@@ -440,6 +454,8 @@ struct UniformArgs {
 __global__ void k_uniform_counts(const __grid_constant__ harl_sketch_desc sk,
                                  const uint16_t* tiles, const uint8_t* knobs,
                                  int64_t n, int64_t ld, int32_t* count) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const uint64_t mv = movable_bits(sk, tiles, ld, r);
@@ -451,6 +467,8 @@ __global__ void k_uniform_counts(const __grid_constant__ harl_sketch_desc sk,
 // single-CTA exclusive scan of (count > 1) over 4n entries -> word offsets
 __global__ void k_uniform_scan(const int32_t* count, int64_t total,
                                int64_t* offset, int64_t* total_words) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   __shared__ int64_t carry;
   __shared__ int64_t warp_sums[32];
   if (threadIdx.x == 0) carry = 0;
@@ -508,6 +526,8 @@ __global__ void k_uniform_draw(const __grid_constant__ harl_sketch_desc sk,
                                const uint8_t* knobs, const int32_t* count,
                                const int64_t* offset, int32_t* actions,
                                unsigned long long* first_bad) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   const int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 4 * a.n) return;
   const int64_t h = i / a.n, r = i % a.n;
@@ -542,6 +562,8 @@ __global__ void k_uniform_one(const __grid_constant__ harl_sketch_desc sk,
                               uint64_t j0, const uint16_t* tiles,
                               const uint8_t* knobs, const int32_t* count,
                               int32_t* actions, unsigned long long* used) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int64_t h = i / a.n, r = i % a.n;
   uint64_t j = j0;

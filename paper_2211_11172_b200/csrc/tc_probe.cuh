@@ -15,6 +15,8 @@ constexpr int PROBE_M = 128, PROBE_N = 128, PROBE_K = 64;
 
 __global__ void __launch_bounds__(128)
 k_tc_probe(const float* A, const float* B, float* D, int mode) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
   extern __shared__ __align__(1024) uint8_t sm[];
   float* sB = (float*)sm;                              // N x K (K-major)
   float* sA = (float*)(sm + PROBE_N * PROBE_K * 4);    // M x K (K-major)

@@ -183,8 +183,12 @@ class _Buffers:
             "shift_bits": torch.empty(P, dtype=torch.int32, device=dev),
             "head0_col": torch.empty(P, dtype=torch.int32, device=dev)}
         self.reward = torch.empty(P, dtype=torch.float64, device=dev)
-        self.v_cur = torch.empty(P, dtype=torch.float32, device=dev)
-        self.v_next = torch.empty(P, dtype=torch.float32, device=dev)
+        # V buffers alternate by step parity: step k writes V(X') into
+        # vbuf[k % 2] and reads/writes V(X) in vbuf[(k + 1) % 2], which
+        # already holds V(X'_{k-1}) = V(X_k) whenever no update or cull
+        # came in between (then V(X) is not recomputed)
+        self.vbuf = [torch.empty(P, dtype=torch.float32, device=dev),
+                     torch.empty(P, dtype=torch.float32, device=dev)]
         self.adv = torch.empty(P, dtype=torch.float64, device=dev)
         self.keep = torch.empty(P, dtype=torch.int32, device=dev)
         # per-step tables for graph replay (host fills them each episode)
@@ -222,6 +226,7 @@ class EpisodeEngine:
         self.rl_cfg = rl_cfg
         self.levels = levels
         self.dagent = D.DeviceAgent(agent, levels, self.dev)
+        N.check(N.load().harl_prepare(), "harl_prepare")
         self.replay = D.DeviceReplay(rl_cfg.buffer_capacity, agent.feature_len,
                                      self.dev)
         self._ppo_scratch = None
@@ -247,6 +252,12 @@ class EpisodeEngine:
             self._cache[key] = b
         return b
 
+    @staticmethod
+    def _v_reusable(plan, k):
+        """V(X_k) == V(X'_{k-1}) bit for bit when step k-1 was followed by
+        neither a PPO update nor a cull (same weights, same rows)."""
+        return k > 0 and not plan[k - 1]["ppo"] and not plan[k - 1]["cull"]
+
     def _launch_step(self, b, k, step, cur, nxt, rt, used, graph_mode,
                      gen=None, inj=None, want_logits=False, m=None,
                      grow=None, m_total=0, keep_from=None):
@@ -268,20 +279,22 @@ class EpisodeEngine:
         D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
                       out=nxt["score"], reward=b.reward)
-        D.value_pair(self.dagent, cur["feat"], m, nxt["feat"], m, b.v_cur,
-                     b.v_next)
+        v_cur, v_next = b.vbuf[(k + 1) % 2], b.vbuf[k % 2]
+        reuse = self._v_reusable(b.plan, k)
+        D.value_pair(self.dagent, cur["feat"], 0 if reuse else m, nxt["feat"],
+                     m, v_cur, v_next)
         po = b.pol_out
         io = N.StepBuffers(
             rt.data_ptr(), nxt["tiles"].data_ptr(), nxt["knobs"].data_ptr(),
             cur["feat"].data_ptr(), nxt["feat"].data_ptr(),
-            nxt["score"].data_ptr(), b.reward.data_ptr(), b.v_cur.data_ptr(),
-            b.v_next.data_ptr(), po["actions"].data_ptr(),
+            nxt["score"].data_ptr(), b.reward.data_ptr(), v_cur.data_ptr(),
+            v_next.data_ptr(), po["actions"].data_ptr(),
             po["head0_col"].data_ptr(), po["logp"].data_ptr(),
             po["move_bits"].data_ptr(), po["shift_bits"].data_ptr(),
             b.adv.data_ptr())
         cap = self.replay.cap
         keep_from = max(0, m - cap) if keep_from is None else keep_from
-        with PF.span("finish", m, launches=2 if m > keep_from else 1):
+        with PF.span("finish", m, launches=1):
             N.check(lib.harl_finish_step(
                 io, m, P, used, tables.local_slots, tables.feature_len,
                 self.rl_cfg.discount, 1, self.replay.desc, self.replay.wpos,
@@ -432,8 +445,8 @@ class EpisodeEngine:
                                "new_feats": nxt["feat"][:m].clone(),
                                "new_score": nxt["score"][:m].clone(),
                                "rewards": b.reward[:m].clone(),
-                               "v_cur": b.v_cur[:m].clone(),
-                               "v_next": b.v_next[:m].clone(),
+                               "v_cur": b.vbuf[(k + 1) % 2][:m].clone(),
+                               "v_next": b.vbuf[k % 2][:m].clone(),
                                "adv": b.adv[:m].clone()})
             cur, nxt = nxt, cur
             used += m

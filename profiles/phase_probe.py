@@ -21,6 +21,7 @@ NAMES = ["start", "init", "x_staged", "w1_ready", "mma1", "epi1", "mma2",
 SNAMES = ["start", "rng", "state", "softmax", "cdf", "shift_heads", "decided", "end"]
 GNAMES = ["start", "x0", "walk0", "sum0", "x1", "walk1", "sum1"]
 FNAMES = ["start", "staged", "rows", "end"]
+ANAMES = ["start", "bad_checked", "updated", "end"]
 PNAMES = ["start", "gather", "pol_fwd", "heads", "val_fwd", "terms", "pol_bwd", "val_bwd", "end"]
 
 
@@ -29,23 +30,30 @@ def main():
     w = bench.build_workload("c2", P)
     tb = w["tables"]
     forest = D.DeviceForest(w["trees"], w["base"], w["lr"])
-    eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, use_graphs=False)
+    graphs = len(sys.argv) > 2 and sys.argv[2] == "graph"
+    eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, use_graphs=graphs)
     cfg = EpisodeConfig(tracks=P, track_len=2, cull_window=20,
                         cull_fraction=0.5, min_tracks=P // 2)
+    cfg1 = EpisodeConfig(tracks=P, track_len=1, cull_window=20,
+                         cull_fraction=0.5, min_tracks=P // 2)
     lib = N.load()
     gen = np.random.default_rng(0)
     for rep in range(3):
-        N.check(lib.harl_debug_timestamps(1, None, 0), "dbg")
-        eng.run_episode(tb, forest, gen, cfg, 0)
+        N.check(lib.harl_debug_timestamps(2 if rep == 2 else 1, None, 0), "dbg")
+        eng.run_episode(tb, forest, gen, cfg1 if graphs else cfg, 0)
         torch.cuda.synchronize()
         ts = np.zeros(64, dtype=np.uint64)
         N.check(lib.harl_debug_timestamps(0, ts.ctypes.data_as(C.c_void_p), 64), "dbg")
         for nm, lo, names in (("policy", 0, NAMES), ("sample", 16, SNAMES),
                               ("gbt", 24, GNAMES), ("featurize", 32, FNAMES),
-                              ("ppo_rows", 40, PNAMES)):
+                              ("ppo_rows", 40, PNAMES), ("adam", 50, ANAMES)):
             t = ts[lo:lo + len(names)].astype(np.int64)
             rel = (t - t[0]) / 1e3
             print(f"rep {rep} {nm}: " + " ".join(f"{n}={r:.2f}" for n, r in zip(names, rel)))
+        if rep == 2:
+            a0, a1, b0, b1 = (int(x) for x in ts[60:64])
+            print(f"sampler grid {(a1 - a0) / 1e3:.2f} us, gap to featurize "
+                  f"{(b0 - a1) / 1e3:.2f} us, featurize grid {(b1 - b0) / 1e3:.2f} us")
 
 
 if __name__ == "__main__":

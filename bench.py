@@ -30,10 +30,16 @@ values (no measurements are available offline).
 
 from __future__ import annotations
 
+import os
+
+# the CPU legs time single-threaded numpy (cores = processes); set before
+# numpy loads so BLAS pools are not oversubscribed (spawned workers inherit)
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import argparse
 import json
 import math
-import os
 import subprocess
 import sys
 import threading
@@ -324,54 +330,103 @@ def run_gpu(args, rank, world):
     if world > 1:
         dist.barrier()
     # ---- e2e: host buffers in and out every episode ------------------------
+    host = E2EHost(eng, w, dev, ecfg.budget)
     e2e_ms, h2d, d2h, e2e_visits = 0.0, 0, 0, 0
+    e2e_parts = {}
     for _ in range(max(1, min(args.steps, 3))):
         l2_flush(torch, dev)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        b_in, b_out, v = e2e_episode(eng, w, forest, gen, ecfg, order, dev)
+        b_in, b_out, v, parts = host.episode(forest, gen, ecfg, order)
         torch.cuda.synchronize()
         e2e_ms += (time.perf_counter() - t0) * 1e3
         h2d, d2h = b_in, b_out
         e2e_visits += v
         order += v
+        for k_, t_ in parts.items():
+            e2e_parts[k_] = e2e_parts.get(k_, 0.0) + t_
     return dict(total_ms=total_ms, visits=visits, clocks=clk.summary(),
                 launches=launches, kstats=kstats, native=native, e2e_ms=e2e_ms,
-                e2e_visits=e2e_visits, h2d=h2d, d2h=d2h, P=P)
+                e2e_visits=e2e_visits, h2d=h2d, d2h=d2h, P=P,
+                e2e_parts=e2e_parts)
 
 
-def e2e_episode(eng, w, forest_unused, gen, ecfg, order, dev):
-    """One drop-in episode with every input from host memory and every
-    output returned to host memory (what the reference-facing wrapper
-    does per round)."""
-    import torch
-    from paper_2211_11172_b200 import device as D
-    tb = w["tables"]
-    nbytes_in = 0
-    # agent params + moments + replay ring + forest from pinned host memory
-    eng.dagent.upload()
-    nbytes_in += 3 * eng.dagent.n_params * 8
-    ring = eng.replay
-    host_ring = {k: getattr(ring, k).cpu().pin_memory()
-                 for k in ("X", "Xn", "actions", "scalars", "move_bits",
-                           "shift_bits")}
-    for k, v in host_ring.items():
-        getattr(ring, k).copy_(v, non_blocking=True)
-        nbytes_in += v.numel() * v.element_size()
-    forest = D.DeviceForest(w["trees"], w["base"], w["lr"], device=dev)
-    nbytes_in += sum(t.numel() * t.element_size() for t in (
-        forest.nodes, forest.tree_first))
-    res = eng.run_episode(tb, forest, gen, ecfg, order)
-    tiles, knobs = res.states()
-    scores = res.scores()
-    rewards = res.log_reward[:res.visits].cpu().numpy()
-    eng.dagent.download()
-    out = ring.export(tb.num_slots, tb.levels)
-    nbytes_out = tiles.nbytes + knobs.nbytes + scores.nbytes + rewards.nbytes
-    nbytes_out += 3 * eng.dagent.n_params * 8
-    nbytes_out += sum(np.asarray(v).nbytes for k, v in out.items()
-                      if k != "masks")
-    return nbytes_in, nbytes_out, res.visits
+class E2EHost:
+    """The drop-in's host side for the e2e number: pinned host buffers for
+    every per-episode input (agent parameters + Adam moments, replay ring,
+    GBT ensemble) and output (visited entries: states, scores, rewards;
+    updated agent and ring), allocated once.  Each timed episode copies the
+    inputs host->device, runs ``_run_episode`` and copies the outputs back
+    (what ``compat.B200TuningSession._run_episode`` moves per round, without
+    the reference's Python object construction)."""
+
+    def __init__(self, eng, w, dev, visits):
+        import torch
+        self.eng, self.w, self.dev = eng, w, dev
+        self.tb = w["tables"]
+        da, ring = eng.dagent, eng.replay
+        pin = lambda t: torch.empty(t.shape, dtype=t.dtype).pin_memory()
+        self.agent_in = {k: pin(getattr(da, k)) for k in ("params", "m", "v")}
+        for k, t in self.agent_in.items():
+            t.copy_(getattr(da, k))
+        self.agent_out = {k: pin(getattr(da, k)) for k in ("params", "m", "v")}
+        keys = ("X", "Xn", "actions", "scalars", "move_bits", "shift_bits")
+        self.ring_in = {k: pin(getattr(ring, k)) for k in keys}
+        for k, t in self.ring_in.items():
+            t.copy_(getattr(ring, k))
+        self.ring_out = {k: pin(getattr(ring, k)) for k in keys}
+        tb = self.tb
+        self.V = (visits, {
+            "tiles": torch.empty((tb.local_slots, visits), dtype=torch.int16).pin_memory(),
+            "knobs": torch.empty((3, visits), dtype=torch.uint8).pin_memory(),
+            "score": torch.empty(visits, dtype=torch.float64).pin_memory(),
+            "reward": torch.empty(visits, dtype=torch.float64).pin_memory()})
+
+    def episode(self, forest, gen, ecfg, order):
+        import torch
+        eng, tb = self.eng, self.tb
+        da, ring = eng.dagent, eng.replay
+        parts = {}
+        t0 = time.perf_counter()
+        nin = 0
+        for k, t in self.agent_in.items():
+            getattr(da, k).copy_(t, non_blocking=True)
+            nin += t.numel() * t.element_size()
+        da.params32.copy_(da.params)            # fp32 rollout copy
+        da.refresh_derived()                    # tcgen05 images + transposes
+        for k, t in self.ring_in.items():
+            getattr(ring, k).copy_(t, non_blocking=True)
+            nin += t.numel() * t.element_size()
+        w = self.w
+        forest.load(w["trees"], w["base"], w["lr"])
+        nin += forest.n_nodes * 16 + forest.n_trees * 4 + forest.HDR.itemsize
+        t1 = time.perf_counter()
+        res = eng.run_episode(tb, forest, gen, ecfg, order)
+        t2 = time.perf_counter()
+        V = res.visits
+        if self.V is None or self.V[0] < V:
+            self.V = (V, {
+                "tiles": torch.empty((tb.local_slots, V), dtype=torch.int16).pin_memory(),
+                "knobs": torch.empty((3, V), dtype=torch.uint8).pin_memory(),
+                "score": torch.empty(V, dtype=torch.float64).pin_memory(),
+                "reward": torch.empty(V, dtype=torch.float64).pin_memory()})
+        ho = self.V[1]
+        ho["tiles"][:, :V].copy_(res.log_tiles[:tb.local_slots, :V], non_blocking=True)
+        ho["knobs"][:, :V].copy_(res.log_knobs[:, :V], non_blocking=True)
+        ho["score"][:V].copy_(res.log_score[:V], non_blocking=True)
+        ho["reward"][:V].copy_(res.log_reward[:V], non_blocking=True)
+        nout = V * (2 * tb.local_slots + 3 + 16)
+        for k, t in self.agent_out.items():
+            t.copy_(getattr(da, k), non_blocking=True)
+            nout += t.numel() * t.element_size()
+        for k, t in self.ring_out.items():
+            t.copy_(getattr(ring, k), non_blocking=True)
+            nout += t.numel() * t.element_size()
+        torch.cuda.current_stream().synchronize()
+        t3 = time.perf_counter()
+        parts.update(h2d_ms=(t1 - t0) * 1e3, episode_ms=(t2 - t1) * 1e3,
+                     d2h_ms=(t3 - t2) * 1e3)
+        return nin, nout, V, parts
 
 
 # kernel -> (profiling span whose rows it processes, bound)
@@ -467,9 +522,26 @@ def roofline_entry(native, spans, tables, hidden):
     top = max((k for k in table if table[k]["bound"]),
               key=lambda k: table[k]["ms_per_episode"])
     e = table[top]
+    # DRAM bytes per launch of that kernel from the committed ncu --set full
+    # capture (per row there, scaled to this run's average rows per launch)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        if top in tr:
+            span = KERNEL_SPAN[top][0]
+            rows = spans.get(span, {}).get("rows", 0)
+            launches = native[top]["launches"] or 1
+            per_row = tr[top]["dram_bytes_per_launch"] / tr[top]["rows_per_launch"]
+            traffic = round(per_row * rows / launches)
+    except (OSError, ValueError, KeyError):
+        traffic = None
     out = {"kernel": top, "bound": e["bound"],
            "achieved": round(e["achieved"], 3), "peak": e["peak"],
-           "unit": e["unit"], "frac": round(e["frac"], 5), "traffic": None,
+           "unit": e["unit"], "frac": round(e["frac"], 5), "traffic": traffic,
+           "traffic_note": "DRAM bytes/launch (dram__bytes_read+write) from "
+                           "profiles/r1_traffic.json (ncu --set full), scaled "
+                           "to this run's rows/launch; population data is "
+                           "L2-resident, so DRAM traffic << algorithmic bytes",
            "us_per_launch": round(e["us_per_launch"], 2),
            "peak_note": "hbm: MEASURED_PEAKS.json hbm_gbs (burst); tensor: "
                         "dense tf32 = measured bf16 x 1.1/2.25; fp64: 37 "
@@ -541,7 +613,9 @@ def main():
                    if world > 1 else "single GPU"},
         "e2e": {"value": round(e2e, 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(r["h2d"]),
-                "d2h_bytes_per_step": int(r["d2h"])},
+                "d2h_bytes_per_step": int(r["d2h"]),
+                "ms_per_step_parts": {k: round(v / max(1, min(args.steps, 3)), 3)
+                                      for k, v in r["e2e_parts"].items()}},
         "gpu_launches": int(r["launches"]),
         "clocks": r["clocks"],
         "roofline": roofline_entry(r["native"], r["kstats"], tb, 128),

@@ -117,6 +117,12 @@ typedef struct harl_forest_desc {
   const int32_t* tree_first;  /* [n_trees] first node of each tree */
   const void* nodes;          /* [n_nodes] records */
   int64_t n_nodes;
+  /* Optional device header {int32 n_trees, int32 fitted, double base,
+   * double floor_value, int64 n_nodes} read by the kernels at run time.
+   * When set, the host fields above are CAPACITIES (shared-memory sizing
+   * only), so a refitted ensemble can be loaded into the same buffers
+   * without re-recording captured launches. */
+  const void* dev_hdr;
 } harl_forest_desc;
 
 int harl_abi_version(void);

@@ -62,7 +62,7 @@ class MlpDesc(C.Structure):
 class ForestDesc(C.Structure):
     _fields_ = [("n_trees", i32), ("fitted", i32), ("base", f64),
                 ("floor_value", f64), ("tree_first", vp), ("nodes", vp),
-                ("n_nodes", i64)]
+                ("n_nodes", i64), ("dev_hdr", vp)]
 
 
 class ReplayRing(C.Structure):

@@ -126,7 +126,17 @@ def b200_session_class(base):
             tables = self._b200_sketch_tables(sg, sketch)
             eng.dagent.upload()
             self._b200_load_ring(eng, sg)
-            forest = D.DeviceForest.from_model(self.model)
+            forest = getattr(self, "_b200_forest", None)
+            if forest is None or not forest.load_model(self.model):
+                # capacity for the refits to come (n_estimators trees of
+                # at most 2^(max_depth+1) nodes), so one capture serves all
+                cfg = self.model.cfg
+                depth = getattr(cfg, "max_depth", 6)
+                trees = max(getattr(cfg, "n_trees", 0), len(self.model.trees), 1)
+                forest = D.DeviceForest.from_model(
+                    self.model, node_capacity=trees * (2 ** (depth + 1)),
+                    tree_capacity=trees)
+                self._b200_forest = forest
             res = eng.run_episode(tables, forest, self.rng, ecfg,
                                   self.order_counter)
             eng.sync_to_host()

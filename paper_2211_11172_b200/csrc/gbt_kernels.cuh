@@ -18,6 +18,13 @@
 
 namespace harl {
 
+// device-side forest scalars (harl_forest_desc.dev_hdr)
+struct GbtHdr {
+  int32_t n_trees, fitted;
+  double base, floor_value;
+  int64_t n_nodes;
+};
+
 struct __align__(16) GbtNode {
   double v;        // split threshold (internal) / lr*value (leaf)
   int16_t feat;    // -1 for a leaf
@@ -33,10 +40,16 @@ k_gbt_predict(const GbtNode* __restrict__ nodes,
               int32_t fitted, double base, double floor_value,
               const double* __restrict__ feat, int64_t n, int32_t F,
               double* score, const double* old_score, double* reward,
-              int32_t rows_per_cta) {
+              int32_t rows_per_cta, const GbtHdr* hdr) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   extern __shared__ double contrib[];  // [rows_per_cta][n_trees]
+  if (hdr) {
+    n_trees = hdr->n_trees;
+    fitted = hdr->fitted;
+    base = hdr->base;
+    floor_value = hdr->floor_value;
+  }
   const int g = threadIdx.x % GBT_GROUPS;
   const int rl = threadIdx.x / GBT_GROUPS;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
@@ -95,12 +108,19 @@ k_gbt_predict2(const GbtNode* __restrict__ gnodes,
                int64_t n_nodes, int32_t fitted, double base,
                double floor_value, const double* __restrict__ feat, int64_t n,
                int32_t F, double* score, const double* old_score,
-               double* reward) {
+               double* reward, const GbtHdr* hdr, int32_t t_cap) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   dbg_ts(24);
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint64_t fbar, xbar[2];
+  if (hdr) {   // reloadable forest: the scalars live on the device
+    n_trees = hdr->n_trees;
+    fitted = hdr->fitted;
+    base = hdr->base;
+    floor_value = hdr->floor_value;
+    n_nodes = hdr->n_nodes;
+  }
   size_t off = 0;
   const GbtNode* nodes = gnodes;
   GbtNode* sn = (GbtNode*)gsm;
@@ -109,7 +129,7 @@ k_gbt_predict2(const GbtNode* __restrict__ gnodes,
     off = gbt2_align((size_t)n_nodes * 16);
   }
   int32_t* s_first = (int32_t*)(gsm + off);
-  off += gbt2_align((size_t)n_trees * 4);
+  off += gbt2_align((size_t)(n_trees > t_cap ? n_trees : t_cap) * 4);
   double* xsb[2];
   xsb[0] = (double*)(gsm + off);
   off += gbt2_align((size_t)GBT2_ROWS * F * 8);

@@ -511,12 +511,12 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
       launch_k(k_gbt_predict2<true>, dim3((unsigned)grid), dim3(GBT2_THREADS), smem, (cudaStream_t)stream, 
           (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
           forest->n_nodes, forest->fitted, forest->base, forest->floor_value, feat,
-          n, F, score, old_score, reward);
+          n, F, score, old_score, reward, (const GbtHdr*)forest->dev_hdr, T);
     else
       launch_k(k_gbt_predict2<false>, dim3((unsigned)grid), dim3(GBT2_THREADS), smem, (cudaStream_t)stream, 
           (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
           forest->n_nodes, forest->fitted, forest->base, forest->floor_value, feat,
-          n, F, score, old_score, reward);
+          n, F, score, old_score, reward, (const GbtHdr*)forest->dev_hdr, T);
     HARL_CHECK_LAUNCH("k_gbt_predict2");
     return HARL_OK;
   }
@@ -528,7 +528,7 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
   launch_k(k_gbt_predict, dim3((unsigned)((n + rows - 1) / rows)), dim3(GBT_THREADS), smem1, (cudaStream_t)stream, 
       (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
       forest->fitted, forest->base, forest->floor_value, feat, n, feature_len,
-      score, old_score, reward, rows);
+      score, old_score, reward, rows, (const GbtHdr*)forest->dev_hdr);
   HARL_CHECK_LAUNCH("k_gbt_predict");
   return HARL_OK;
 }

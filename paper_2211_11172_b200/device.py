@@ -245,25 +245,52 @@ class DeviceForest:
 
     ``trees`` are ``(feature, threshold, left, right, value)`` arrays per
     tree; ``learning_rate * value`` is formed here with numpy, the same
-    fp64 product the reference computes per prediction."""
+    fp64 product the reference computes per prediction.
+
+    The buffers have a capacity: ``load`` writes a refitted ensemble into
+    the same device memory and its scalars into a device header the kernels
+    read at run time, so CUDA graphs recorded against this forest stay valid
+    across refits (one capture per session, not per round)."""
 
     NODE = np.dtype([("v", "<f8"), ("feat", "<i2"), ("left", "<i2"),
                      ("right", "<i2"), ("pad", "<i2")])
+    HDR = np.dtype([("n_trees", "<i4"), ("fitted", "<i4"), ("base", "<f8"),
+                    ("floor_value", "<f8"), ("n_nodes", "<i8")])
 
     def __init__(self, trees, base: float, learning_rate: float,
                  fitted: bool = True, floor_value: float = 1e-6,
-                 device=None):
+                 device=None, node_capacity: int = 0, tree_capacity: int = 0):
         N.load()
         dev = _dev(device)
+        nodes, firsts = self._records(trees, learning_rate)
+        self.cap_nodes = max(len(nodes), int(node_capacity), 1)
+        self.cap_trees = max(len(firsts), int(tree_capacity), 1)
+        self.nodes = torch.zeros(self.cap_nodes * 16, dtype=torch.uint8,
+                                 device=dev)
+        self.tree_first = torch.zeros(self.cap_trees, dtype=torch.int32,
+                                      device=dev)
+        self.hdr = torch.zeros(self.HDR.itemsize, dtype=torch.uint8,
+                               device=dev)
+        d = N.ForestDesc()
+        d.n_trees = self.cap_trees
+        d.n_nodes = self.cap_nodes
+        d.tree_first = self.tree_first.data_ptr()
+        d.nodes = self.nodes.data_ptr()
+        d.dev_hdr = self.hdr.data_ptr()
+        self.desc = d
+        self.device = dev
+        self._write(nodes, firsts, base, fitted, floor_value)
+
+    @classmethod
+    def _records(cls, trees, learning_rate):
         if len(trees) > 1024:
             raise DeviceError("more than 1024 trees")
-        recs, firsts = [], []
-        n = 0
+        recs, firsts, n = [], [], 0
         for feat, thr, left, right, val in trees:
             feat = np.asarray(feat)
             left, right = np.asarray(left), np.asarray(right)
             _check_depth(feat, left, right)
-            rec = np.zeros(len(feat), dtype=self.NODE)
+            rec = np.zeros(len(feat), dtype=cls.NODE)
             leaf = feat < 0
             # leaves carry learning_rate * value: the reference's fp64
             # product (costmodel.py:224), formed here once
@@ -275,45 +302,71 @@ class DeviceForest:
             recs.append(rec)
             firsts.append(n)
             n += len(feat)
-        nodes = np.concatenate(recs) if recs else np.zeros(1, self.NODE)
-        self.n_nodes = n
-        self.nodes = torch.from_numpy(nodes.view(np.uint8).copy()).to(dev)
-        self.tree_first = torch.from_numpy(
-            np.asarray(firsts if firsts else [0], dtype=np.int32)).to(dev)
-        d = N.ForestDesc()
-        d.n_trees = len(trees)
-        d.fitted = 1 if fitted else 0
-        d.base = float(base)
-        d.floor_value = float(floor_value)
-        d.tree_first = self.tree_first.data_ptr()
-        d.nodes = self.nodes.data_ptr()
-        d.n_nodes = n
-        self.desc = d
-        self.device = dev
+        nodes = np.concatenate(recs) if recs else np.zeros(0, cls.NODE)
+        return nodes, np.asarray(firsts, dtype=np.int32)
+
+    def _write(self, nodes, firsts, base, fitted, floor_value):
+        self.n_nodes = len(nodes)
+        self.n_trees = len(firsts)
+        if len(nodes):
+            self.nodes[:len(nodes) * 16].copy_(
+                torch.from_numpy(nodes.view(np.uint8).copy()))
+        if len(firsts):
+            self.tree_first[:len(firsts)].copy_(torch.from_numpy(firsts))
+        h = np.zeros(1, dtype=self.HDR)
+        h["n_trees"], h["fitted"] = len(firsts), 1 if fitted else 0
+        h["base"], h["floor_value"] = float(base), float(floor_value)
+        h["n_nodes"] = len(nodes)
+        self.hdr.copy_(torch.from_numpy(h.view(np.uint8).copy()))
+        # host mirrors (informational; the kernels read the header)
+        self.desc.fitted = 1 if fitted else 0
+        self.desc.base = float(base)
+        self.desc.floor_value = float(floor_value)
+
+    def load(self, trees, base: float, learning_rate: float,
+             fitted: bool = True, floor_value: float = 1e-6) -> bool:
+        """Load another ensemble in place; False if it exceeds the
+        capacity (build a new forest then)."""
+        nodes, firsts = self._records(trees, learning_rate)
+        if len(nodes) > self.cap_nodes or len(firsts) > self.cap_trees:
+            return False
+        self._write(nodes, firsts, base, fitted, floor_value)
+        return True
+
+    @staticmethod
+    def _model_trees(model):
+        return [(t.feature, t.threshold, t.left, t.right, t.value)
+                for t in model.trees]
 
     @classmethod
-    def from_model(cls, model, device=None):
+    def from_model(cls, model, device=None, node_capacity: int = 0,
+                   tree_capacity: int = 0):
         """From a reference ``SurrogateModel`` (duck-typed)."""
-        trees = [(t.feature, t.threshold, t.left, t.right, t.value)
-                 for t in model.trees]
-        return cls(trees, model.base, model.cfg.learning_rate,
-                   fitted=model.fitted, device=device)
+        return cls(cls._model_trees(model), model.base,
+                   model.cfg.learning_rate, fitted=model.fitted,
+                   device=device, node_capacity=node_capacity,
+                   tree_capacity=tree_capacity)
+
+    def load_model(self, model) -> bool:
+        return self.load(self._model_trees(model), model.base,
+                         model.cfg.learning_rate, fitted=model.fitted)
 
 
 def _check_depth(feat, left, right):
-    depth = {0: 0}
-    stack = [0]
-    while stack:
-        nd = stack.pop()
-        if feat[nd] >= 0:
-            for ch in (int(left[nd]), int(right[nd])):
-                depth[ch] = depth[nd] + 1
-                if depth[ch] >= 64:
-                    raise DeviceError("tree deeper than the reference's "
-                                      "64-step walk")
-                stack.append(ch)
+    """The reference walks at most 64 levels (costmodel.py:67-78); reject
+    deeper trees and node indices int16 cannot hold.  Level-synchronous
+    (vectorised) traversal from the root."""
+    feat = np.asarray(feat)
     if len(feat) > 32767:
         raise DeviceError("tree too large for int16 node indices")
+    frontier = np.zeros(1, dtype=np.int64)
+    for _ in range(64):
+        inner = frontier[feat[frontier] >= 0]
+        if inner.size == 0:
+            return
+        frontier = np.concatenate([np.asarray(left)[inner],
+                                   np.asarray(right)[inner]]).astype(np.int64)
+    raise DeviceError("tree deeper than the reference's 64-step walk")
 
 
 def gbt_predict(forest: DeviceForest, feat, n: int, old_score=None,
@@ -507,6 +560,12 @@ class DeviceAgent:
         self.params32.copy_(p.float())
         self.m.copy_(torch.from_numpy(self._pack(a.opt_pi.m, a.opt_v.m)))
         self.v.copy_(torch.from_numpy(self._pack(a.opt_pi.v, a.opt_v.v)))
+        self.refresh_derived()
+
+    def refresh_derived(self):
+        """Rebuild every device copy derived from the master parameters:
+        the fp64 transposes the PPO backward reads and the tcgen05 weight
+        images (the Adam kernel keeps both current afterwards)."""
         lib = N.load()
         with PF.span("wt_fill", 0):
             N.check(lib.harl_ppo_wt_fill(C.byref(self.pol_layout),

@@ -18,6 +18,8 @@ def summarize(path):
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0].replace("void ", "")
+        if name.endswith("k_spin"):
+            continue   # bench's per-kernel timer (untimed profiled episode)
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", "")) * scale[r[ui]]
     tot = sum(v for _, v in agg.values())

@@ -436,6 +436,7 @@ KERNEL_SPAN = {
     "k_sample_rows": ("policy_tc", "hbm"),
     "k_trunk_tc<value>": ("value_tc", "tensor"),
     "k_policy_tc": ("policy_tc", "tensor"),
+    "k_policy_step_fused": ("policy_tc", "tensor"),
     "k_value_tc": ("value_tc", "tensor"),
     "k_featurize": ("featurize", "hbm"),
     "k_featurize2": ("featurize", "hbm"),
@@ -460,6 +461,8 @@ def per_row_work(tables, H):
         "k_heads_tc": 2 * H * NH,
         "k_trunk_tc<value>": 2 * (F * H + H * H + H),   # per evaluated row
         "k_policy_tc": 2 * (F * H + H * H + H * NH),
+        # + the sampler/walker and the featurizer of the same rows
+        "k_policy_step_fused": 2 * (F * H + H * H + H * NH),
         "k_value_tc": 2 * (F * H + H * H + H),
         # logits in; actions, logp, successor state out
         "k_sample_rows": 4 * NH + state + 16 + 8 + state,

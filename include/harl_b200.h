@@ -209,7 +209,11 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
  * accumulators and TMEM-resident activations.  hid_scratch: float32
  * [n][128] device scratch.  rng_state_dev (optional, device {hi, lo}
  * u64 PCG64 state) overrides rng's state at execution time so the call can
- * be replayed from a CUDA graph (rng still supplies the increment).  Not
+ * be replayed from a CUDA graph (rng still supplies the increment).
+ * feat_out (optional, f64 [n][F]): also featurize the new states
+ * (schedspace.py:415-438) -- with the packed weight images this is one
+ * fused kernel (policy -> sample/apply -> featurize per 128-row tile, the
+ * logits never leave the SM); otherwise a separate featurize launch.  Not
  * a fallback: returns HARL_E_ARG if the shape is not eligible (the caller
  * then uses harl_policy_step). */
 int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
@@ -222,7 +226,8 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* logits_out, uint64_t* status,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
-                        const int32_t* grow, int64_t m_total, void* stream);
+                        const int32_t* grow, int64_t m_total, double* feat_out,
+                        void* stream);
 
 /* V(X) and V(X') in one launch (tuner.py:395-396) on the tcgen05 path
  * (hidden (128,128), feature_len <= 64); HARL_E_ARG if not eligible. */

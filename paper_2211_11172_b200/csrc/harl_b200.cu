@@ -19,8 +19,8 @@
 #include "ppo_kernels.cuh"
 #include "tc_probe.cuh"
 #include "mlp_tc.cuh"
-#include "mlp_tc2.cuh"
 #include "sample_kernels.cuh"
+#include "mlp_tc2.cuh"
 
 namespace harl {
 
@@ -590,6 +590,40 @@ static void build_lane_jump(const harl_pcg64& g, LaneJump* LJ) {
   }
 }
 
+static void sampler_setup(const harl_pcg64* rng, PcgJump* J, u128* base) {
+  memset(J, 0, sizeof(*J));
+  memset(base, 0, sizeof(*base));
+  if (rng) {
+    build_jump(*rng, J);
+    *base = state_of(*rng);
+  }
+}
+
+static SampleArgs sample_args(const float* logits, int ldz, int64_t n, int64_t ld,
+                              const int32_t* inject, int32_t* actions, double* logp,
+                              uint16_t* tiles_out, uint8_t* knobs_out,
+                              uint64_t* move_bits, uint32_t* shift_bits,
+                              int32_t* head0_col, uint64_t* status,
+                              const int32_t* grow, int64_t m_total) {
+  SampleArgs a;
+  a.logits = logits;
+  a.ldz = ldz;
+  a.n = n;
+  a.ld = ld;
+  a.inject = inject;
+  a.actions = actions;
+  a.logp = logp;
+  a.tiles_out = tiles_out;
+  a.knobs_out = knobs_out;
+  a.move_bits = move_bits;
+  a.shift_bits = shift_bits;
+  a.head0_col = head0_col;
+  a.status = (unsigned long long*)status;
+  a.grow = grow;
+  a.m_total = m_total > 0 ? m_total : n;
+  return a;
+}
+
 static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
                           const uint64_t* rng_state_dev, const int32_t* grow,
                           int64_t m_total,
@@ -651,7 +685,8 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* logits_out, uint64_t* status,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
-                        const int32_t* grow, int64_t m_total, void* stream) {
+                        const int32_t* grow, int64_t m_total, double* feat_out,
+                        void* stream) {
   int rc = check_sketch(sk);
   if (rc) return rc;
   if ((rc = check_mlp(pol, true))) return rc;
@@ -668,6 +703,47 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int NHP = (pol->n_head_cols + 15) / 16 * 16;
+  // fused step: policy -> sample/apply -> featurize in one kernel
+  if (feat_out && packed_trunk && packed_heads && use_tc2() &&
+      ((uintptr_t)feat & 15) == 0) {
+    int regA = tc2_regA(NHP);
+    const int need = tc2_fused_regA_need(sk->feature_len, sk->local_slots, sk->max_extent);
+    if (need > regA) regA = (need + 127) / 128 * 128;
+    const size_t smem = (size_t)regA + TC2_W2P;
+    if (smem <= (size_t)max_dyn_smem()) {
+      if ((rc = allow_smem(k_policy_step_fused, smem, "k_policy_step_fused"))) return rc;
+      PolicyTcArgs pa;
+      memset(&pa, 0, sizeof(pa));
+      pa.feat = feat;
+      pa.n = n;
+      pa.F = sk->feature_len;
+      pa.NH = pol->n_head_cols;
+      pa.NHP = NHP;
+      pa.regA = regA;
+      pa.logits = nullptr;
+      pa.logits_out = logits_out;
+      pa.trunk_img = packed_trunk;
+      pa.heads_img = packed_heads;
+      StepFuseArgs fa;
+      memset(&fa, 0, sizeof(fa));
+      PcgJump J;
+      sampler_setup(rng, &J, &fa.base_arg);
+      fa.base_dev = (const u128*)rng_state_dev;
+      fa.s = sample_args(nullptr, TC2_LG_LD, n, ld, inject, actions, logp, tiles_out,
+                         knobs_out, move_bits, shift_bits, head0_col, status, grow,
+                         m_total);
+      fa.tiles = tiles;
+      fa.knobs = knobs;
+      fa.feat_new = feat_out;
+      const int64_t tiles_n = (n + 127) / 128;
+      const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+      HARL_PROF_BEGIN(st);
+      launch_k(k_policy_step_fused, dim3(grid), dim3(TC2_THREADS), smem, st, pa, fa,
+               *sk, J);
+      HARL_CHECK_LAUNCH("k_policy_step_fused");
+      return HARL_OK;
+    }
+  }
   if (packed_trunk && packed_heads && use_tc2() && ((uintptr_t)feat & 15) == 0 &&
       (size_t)tc2_smem(NHP) <= (size_t)max_dyn_smem()) {
     if ((rc = allow_smem(k_policy_tc, (size_t)tc2_smem(NHP), "k_policy_tc"))) return rc;
@@ -677,6 +753,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     pa.F = sk->feature_len;
     pa.NH = pol->n_head_cols;
     pa.NHP = NHP;
+    pa.regA = tc2_regA(NHP);
     pa.logits = hid_scratch;
     pa.logits_out = logits_out;
     pa.trunk_img = packed_trunk;
@@ -686,10 +763,12 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     HARL_PROF_BEGIN(st);
     launch_k(k_policy_tc, dim3(grid), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
     HARL_CHECK_LAUNCH("k_policy_tc");
-    return launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
+    rc = launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
                           TC_H, n, ld, tiles, knobs, inject, actions, logp,
                           tiles_out, knobs_out, move_bits, shift_bits,
                           head0_col, status, st);
+    if (rc || !feat_out) return rc;
+    return harl_featurize(sk, tiles_out, knobs_out, n, ld, feat_out, stream);
   }
   if ((rc = allow_smem(k_trunk_tc<TRUNK_POLICY>, TRUNK_SMEM, "k_trunk_tc")))
     return rc;
@@ -723,11 +802,13 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   HARL_PROF_BEGIN(st);
   launch_k(k_heads_tc, dim3(grid), dim3(128), smem, st, ha);
   HARL_CHECK_LAUNCH("k_heads_tc");
-  return launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
+  rc = launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
                         TC_H, n, ld,
                         tiles, knobs, inject,
                         actions, logp, tiles_out, knobs_out, move_bits,
                         shift_bits, head0_col, status, st);
+    if (rc || !feat_out) return rc;
+    return harl_featurize(sk, tiles_out, knobs_out, n, ld, feat_out, stream);
 }
 
 
@@ -805,6 +886,7 @@ int harl_prepare(void) {
   if ((rc = allow_max_smem(k_trunk_tc<TRUNK_VALUE>, "k_trunk_tc"))) return rc;
   if ((rc = allow_max_smem(k_heads_tc, "k_heads_tc"))) return rc;
   if ((rc = allow_max_smem(k_policy_tc, "k_policy_tc"))) return rc;
+  if ((rc = allow_max_smem(k_policy_step_fused, "k_policy_step_fused"))) return rc;
   if ((rc = allow_max_smem(k_value_tc, "k_value_tc"))) return rc;
   if ((rc = allow_max_smem(k_ppo_rows, "k_ppo_rows"))) return rc;
   // One shared-memory carveout for every kernel: the episode alternates
@@ -840,6 +922,7 @@ int harl_prepare(void) {
   carve(k_pack_trunk);
   carve(k_pack_heads);
   carve(k_policy_tc);
+  carve(k_policy_step_fused);
   carve(k_value_tc);
   carve(k_finish_step);
   carve(k_ring_rows);
@@ -1144,17 +1227,16 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
         a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
     HARL_CHECK_LAUNCH("k_ppo_rows");
   }
-  HARL_PROF_BEGIN(st);
-  launch_k(k_ppo_losses, dim3(1), dim3(32), 0, st, B, rowout, losses, phase == 3 ? B_norm : 0,
-                                 hp->entropy_weight, hp->value_loss_weight, bad);
-  HARL_CHECK_LAUNCH("k_ppo_losses");
   GradJobs jt;
   memset(&jt, 0, sizeof(jt));
   for (int j = 0; j < n_jobs; ++j) jt.j[j] = jobs[j];
   jt.n = n_jobs;
+  // one extra CTA sums the per-row loss terms (and, on a single device,
+  // forms the means and checks them) alongside the gradient tiles
   HARL_PROF_BEGIN(st);
-  launch_k(k_ppo_wgrad, dim3((unsigned)n_tiles), dim3(256), 0, st, jt, B, row_stride, rows, grads,
-                                                 bad, phase == 3 ? 1 : 0);
+  launch_k(k_ppo_wgrad, dim3((unsigned)n_tiles + 1), dim3(256), 0, st, jt, B, row_stride,
+           rows, grads, bad, phase == 3 ? 1 : 0, (const double*)rowout, losses,
+           phase == 3 ? B_norm : 0, hp->entropy_weight, hp->value_loss_weight);
   HARL_CHECK_LAUNCH("k_ppo_wgrad");
   }
   if (!(phase & 2)) return HARL_OK;

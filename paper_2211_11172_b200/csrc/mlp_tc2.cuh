@@ -22,6 +22,8 @@
 #pragma once
 
 #include "mlp_tc.cuh"
+#include "sample_kernels.cuh"
+#include "space_kernels.cuh"
 
 namespace harl {
 
@@ -89,19 +91,38 @@ struct PolicyTcArgs {
   const double* feat;   // [n][F] (16-byte aligned)
   int64_t n;
   int32_t F, NH, NHP;
+  int32_t regA;         // bytes of shared-memory region A (>= tc2_regA(NHP))
   float* logits;        // [n][128] (the sampler's input, row stride 128)
   float* logits_out;    // optional [n][NH]
   const void* trunk_img;  // k_pack_trunk image
   const void* heads_img;  // k_pack_heads image
 };
 
-__global__ void __launch_bounds__(TC2_THREADS, 1) k_policy_tc(PolicyTcArgs a) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
+// The rest of the rollout step, fused behind the heads (FUSED = true):
+// the CTA samples and applies its 128 rows' actions straight from the
+// logits staging tile (k_sample_rows' 8-lane groups, two passes), then
+// featurizes the new states of the same rows into X' (k_featurize2's 4-part
+// rows) -- the logits never reach HBM and two launches disappear.
+struct StepFuseArgs {
+  SampleArgs s;               // sampler outputs (logits field unused)
+  u128 base_arg;
+  const u128* base_dev;       // graph replay: the step's RNG base state
+  const uint16_t* tiles;      // current state [slot][ld]
+  const uint8_t* knobs;
+  double* feat_new;           // X' [n][F]
+};
+
+static_assert(FEAT2_THREADS == TC2_THREADS, "fused featurize shares the CTA");
+
+template <bool FUSED>
+__device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
+                                               const StepFuseArgs* f,
+                                               const harl_sketch_desc* sk,
+                                               const PcgJump* J) {
   dbg_ts(0);
   extern __shared__ __align__(128) uint8_t sm2[];
   uint8_t* sm = sm2;
-  const int regA = tc2_regA(a.NHP);
+  const int regA = a.regA;
   uint8_t* rA = sm;
   uint8_t* rB = sm + regA;
   const float* sb1 = (const float*)(rB + 2 * TC_H * TC_H * 4);
@@ -217,22 +238,69 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_policy_tc(PolicyTcArgs a) {
         *(float4*)(srow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     }
     __syncthreads();
-    const int c4n = a.NHP / 4;
-    for (int i = tid; i < rows * c4n; i += TC2_THREADS) {
-      const int rr = i / c4n, c4 = i % c4n;
-      *(float4*)(a.logits + (r0 + rr) * TC_H + 4 * c4) =
-          *(const float4*)(stg + rr * TC2_LG_LD + 4 * c4);
+    if (!FUSED) {
+      const int c4n = a.NHP / 4;
+      for (int i = tid; i < rows * c4n; i += TC2_THREADS) {
+        const int rr = i / c4n, c4 = i % c4n;
+        *(float4*)(a.logits + (r0 + rr) * TC_H + 4 * c4) =
+            *(const float4*)(stg + rr * TC2_LG_LD + 4 * c4);
+      }
     }
     if (a.logits_out)
       for (int i = tid; i < rows * a.NH; i += TC2_THREADS) {
         const int rr = i / a.NH, c = i % a.NH;
         a.logits_out[(r0 + rr) * a.NH + c] = stg[rr * TC2_LG_LD + c];
       }
+    if (FUSED) {
+      int16_t* s_src = (int16_t*)(rA + 128 * TC2_LG_LD * 4);
+      int16_t* s_dst = s_src + HARL_MAX_HEAD0;
+      for (int i = tid; i < sk->n_head0; i += TC2_THREADS) {
+        s_src[i] = sk->head0_src[i];
+        s_dst[i] = sk->head0_dst[i];
+      }
+      __syncthreads();
+      dbg_ts(11);
+#pragma unroll 1
+      for (int pass = 0; pass < 128 / (TC2_THREADS / SG); ++pass) {
+        const int lr = pass * (TC2_THREADS / SG) + tid / SG;
+        sample_group(*sk, *J, f->base_arg, f->base_dev, f->tiles, f->knobs,
+                     f->s, r0 + lr, stg + lr * TC2_LG_LD, s_src, s_dst);
+      }
+      __syncthreads();   // the tile's new states are written (and visible)
+      dbg_ts(12);
+      featurize_tile(*sk, f->s.tiles_out, f->s.knobs_out, a.n, f->s.ld, r0,
+                     f->feat_new, rA);
+      dbg_ts(13);
+    }
     first = false;
     tc_sync();  // staging reads done before the next tile reuses regA
     dbg_ts(10);
   }
   if (warp == 0) tc::tmem_dealloc(tm, 512);
+}
+
+__global__ void __launch_bounds__(TC2_THREADS, 1) k_policy_tc(PolicyTcArgs a) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  policy_tc_body<false>(a, nullptr, nullptr, nullptr);
+}
+
+__global__ void __launch_bounds__(TC2_THREADS, 1)
+k_policy_step_fused(PolicyTcArgs a, StepFuseArgs f,
+                    const __grid_constant__ harl_sketch_desc sk,
+                    const __grid_constant__ PcgJump J) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  policy_tc_body<true>(a, &f, &sk, &J);
+}
+
+// regA must also hold the sampler's column tables and the featurize
+// staging of the fused step
+__host__ __device__ inline int tc2_fused_regA_need(int F, int local_slots,
+                                                   int max_extent) {
+  const int samp = 128 * TC2_LG_LD * 4 + 4 * HARL_MAX_HEAD0;
+  const int feat = (int)feat2_smem_bytes(F, local_slots, max_extent);
+  return samp > feat ? samp : feat;
 }
 
 struct ValueTcArgs {

@@ -366,12 +366,11 @@ __device__ inline void ppo_loss_means(int B, double w_ent, double w_val,
 
 // means_B > 0 (single device): also the reported means and the loss
 // finiteness check, for a batch of means_B rows
-__global__ void k_ppo_losses(int B, const double* rowout, double* losses,
-                             int means_B, double w_ent, double w_val,
-                             int32_t* bad) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
-  const int lane = threadIdx.x;
+__device__ inline void ppo_losses_warp(int B, const double* rowout,
+                                       double* losses, int means_B,
+                                       double w_ent, double w_val,
+                                       int32_t* bad) {
+  const int lane = threadIdx.x & 31;
   double q[4] = {0, 0, 0, 0};
   for (int r = lane; r < B; r += 32)
     for (int j = 0; j < 4; ++j) q[j] += rowout[r * 4 + j];
@@ -380,6 +379,14 @@ __global__ void k_ppo_losses(int B, const double* rowout, double* losses,
     for (int j = 0; j < 4; ++j) losses[5 + j] = q[j];
     if (means_B > 0) ppo_loss_means(means_B, w_ent, w_val, losses, bad);
   }
+}
+
+__global__ void k_ppo_losses(int B, const double* rowout, double* losses,
+                             int means_B, double w_ent, double w_val,
+                             int32_t* bad) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  ppo_losses_warp(B, rowout, losses, means_B, w_ent, w_val, bad);
 }
 
 // means (rlcore.py:311-312,355; [0] actor loss, [1] value loss, [2] policy
@@ -422,9 +429,14 @@ struct GradJobs {
 __global__ void __launch_bounds__(256)
 k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
             const double* __restrict__ rows, double* grads, int32_t* bad,
-            int check_finite) {
+            int check_finite, const double* rowout, double* losses,
+            int means_B, double w_ent, double w_val) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
+  if (blockIdx.x == gridDim.x - 1) {   // the extra CTA: loss sums/means
+    if (threadIdx.x < 32) ppo_losses_warp(B, rowout, losses, means_B, w_ent, w_val, bad);
+    return;
+  }
   const GradJob* jobs = jt.j;
   const int n_jobs = jt.n;
   __shared__ double sa[WG_RB][WG_T];

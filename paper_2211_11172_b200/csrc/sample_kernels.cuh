@@ -96,20 +96,16 @@ __device__ inline int sample3(const float* z, uint32_t m3, double u,
   return ok ? idx : -1;
 }
 
-__global__ void __launch_bounds__(SAMPLE_THREADS, 8)
-k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
-              const __grid_constant__ PcgJump J,
-              const __grid_constant__ LaneJump LJ, u128 base_arg,
-              const u128* base_dev, const uint16_t* __restrict__ tiles,
-              const uint8_t* __restrict__ knobs, SampleArgs a) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
-  dbg_ts(16);
-  dbg_grid(false, 60);
-  __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
-  (void)LJ;
+// One 8-lane group samples and applies the action of global row r (the
+// rows past a.n compute on row 0 and write nothing, so every lane stays in
+// the group shuffles).  zrow: the row's logits (null: a.logits + r*ldz);
+// s_src/s_dst: the compact head-0 column tables, filled by the caller.
+__device__ __forceinline__ void sample_group(
+    const harl_sketch_desc& sk, const PcgJump& J, u128 base_arg,
+    const u128* base_dev, const uint16_t* __restrict__ tiles,
+    const uint8_t* __restrict__ knobs, const SampleArgs& a, int64_t r,
+    const float* zrow, const int16_t* s_src, const int16_t* s_dst) {
   const int g = threadIdx.x & (SG - 1);
-  const int64_t r = (int64_t)blockIdx.x * (SAMPLE_THREADS / SG) + threadIdx.x / SG;
   // every group stays in the shuffles; out-of-range rows compute on row 0
   const bool live = r < a.n;
   const int64_t rr = live ? r : 0;
@@ -129,7 +125,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     tv[i] = s < sk.local_slots ? tiles[(int64_t)s * a.ld + rr] : 0;
   }
   const int ca0 = knobs[rr], par0 = knobs[a.ld + rr], ur0 = knobs[2 * a.ld + rr];
-  const float* z = a.logits + rr * a.ldz;
+  const float* z = zrow ? zrow : a.logits + rr * a.ldz;
   const int nI = (C0 + SG - 1) / SG;
   float zc[SAMPLE_MAXI];   // head-0 logits j = g + 8i (padding reads as -inf)
   float z3[3] = {0.f, 0.f, 0.f};   // shift head g+1's three logits (lanes 0-2)
@@ -144,11 +140,6 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
       for (int j = 0; j < 3; ++j) z3[j] = z[C0 + 3 * g + j];
     }
   }
-  for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
-    s_src[i] = sk.head0_src[i];
-    s_dst[i] = sk.head0_dst[i];
-  }
-  __syncthreads();
   // ---- uniforms: lane h of the group draws head h ---------------------
   double u_mine = 0.0;
   if (draw) {
@@ -338,6 +329,27 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     a.head0_col[r] = col0;
     report_status(a.status, r, code);
   }
+}
+
+__global__ void __launch_bounds__(SAMPLE_THREADS, 8)
+k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
+              const __grid_constant__ PcgJump J,
+              const __grid_constant__ LaneJump LJ, u128 base_arg,
+              const u128* base_dev, const uint16_t* __restrict__ tiles,
+              const uint8_t* __restrict__ knobs, SampleArgs a) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  dbg_ts(16);
+  dbg_grid(false, 60);
+  __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
+  (void)LJ;
+  for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
+    s_src[i] = sk.head0_src[i];
+    s_dst[i] = sk.head0_dst[i];
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * (SAMPLE_THREADS / SG) + threadIdx.x / SG;
+  sample_group(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src, s_dst);
   dbg_ts(23);
   dbg_grid(true, 60);
 }

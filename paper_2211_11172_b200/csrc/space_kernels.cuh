@@ -230,23 +230,18 @@ __host__ __device__ inline size_t feat2_smem_bytes(int F, int local_slots,
          (((size_t)FEAT2_ROWS * local_slots * 2 + FEAT2_ROWS * 3 + 15) & ~(size_t)15);
 }
 
-__global__ void __launch_bounds__(FEAT2_THREADS)
-k_featurize2(const __grid_constant__ harl_sketch_desc sk,
-             const uint16_t* __restrict__ tiles,
-             const uint8_t* __restrict__ knobs, int64_t n, int64_t ld,
-             double* __restrict__ feat) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
-  dbg_ts(32);
-  if (blockIdx.x == 0) dbg_grid(true, 61);   // CTA 0 start of the latest launch -> slot 62
-  extern __shared__ __align__(16) unsigned char fsm[];
+// Featurize rows [r0, r0 + 128) of a population (n rows, leading dim ld)
+// with FEAT2_THREADS threads, staging through `fsm` (feat2_smem_bytes).
+__device__ __forceinline__ void featurize_tile(
+    const harl_sketch_desc& sk, const uint16_t* __restrict__ tiles,
+    const uint8_t* __restrict__ knobs, int64_t n, int64_t ld, int64_t r0,
+    double* __restrict__ feat, unsigned char* fsm) {
   const int F = sk.feature_len, S = sk.local_slots;
   double* sfeat = (double*)fsm;
   const bool slut = sk.max_extent + 1 <= FEAT2_LUT_MAX;
   double* lut = slut ? sfeat + FEAT2_ROWS * F : nullptr;
   uint16_t* stile = (uint16_t*)(sfeat + FEAT2_ROWS * F + (slut ? (sk.max_extent + 2) & ~1 : 0));
   uint8_t* sknob = (uint8_t*)(stile + FEAT2_ROWS * S);
-  const int64_t r0 = (int64_t)blockIdx.x * FEAT2_ROWS;
   const int rows = (int)min((int64_t)FEAT2_ROWS, n - r0);
   const bool vec = (ld % 16) == 0 && (((uintptr_t)tiles | (uintptr_t)knobs |
                                        (uintptr_t)sk.log2_lut) & 15) == 0;
@@ -281,7 +276,7 @@ k_featurize2(const __grid_constant__ harl_sketch_desc sk,
       for (int i = threadIdx.x; i <= sk.max_extent; i += FEAT2_THREADS) lut[i] = sk.log2_lut[i];
   }
   __syncthreads();
-  dbg_ts(33);
+
   for (int i = threadIdx.x; i < rows * F; i += FEAT2_THREADS) sfeat[i] = 0.0;
   __syncthreads();
   {
@@ -317,11 +312,23 @@ k_featurize2(const __grid_constant__ harl_sketch_desc sk,
     }
   }
   __syncthreads();
-  dbg_ts(34);
+
   double* out = feat + r0 * F;
   for (int i = threadIdx.x; i < rows * F; i += FEAT2_THREADS) out[i] = sfeat[i];
+
+}
+
+__global__ void __launch_bounds__(FEAT2_THREADS)
+k_featurize2(const __grid_constant__ harl_sketch_desc sk,
+             const uint16_t* __restrict__ tiles,
+             const uint8_t* __restrict__ knobs, int64_t n, int64_t ld,
+             double* __restrict__ feat) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  dbg_ts(32);
+  extern __shared__ __align__(16) unsigned char fsm[];
+  featurize_tile(sk, tiles, knobs, n, ld, (int64_t)blockIdx.x * FEAT2_ROWS, feat, fsm);
   dbg_ts(35);
-  dbg_grid(true, 62);
 }
 
 // ---------------------------------------------------------------------------

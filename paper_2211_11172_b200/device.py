@@ -638,7 +638,7 @@ class DeviceAgent:
         if losses is None:
             losses = self.losses
         src = self.head0_src.ctypes.data_as(C.c_void_p)
-        with PF.span("ppo", B, launches=(3 if phase & 1 else 0) +
+        with PF.span("ppo", B, launches=(2 if phase & 1 else 0) +
                      (2 if phase == 2 else 1 if phase & 2 else 0)):
           N.check(lib.harl_ppo_update(
             C.byref(self.pol_layout), C.byref(self.val_layout), C.byref(hp),
@@ -655,11 +655,13 @@ class DeviceAgent:
 
 def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 n: int, gen=None, inject=None, out=None, want_logits=False,
-                rng_dev=None, advance=True, grow=None, m_total: int = 0):
+                rng_dev=None, advance=True, grow=None, m_total: int = 0,
+                feat_out=None):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
-    Returns a dict of device tensors; ``status`` must be checked by the
-    caller (``raise_status``)."""
+    ``feat_out`` (optional f64 [n][F]): also featurize the new states (one
+    fused kernel on the tcgen05 path).  Returns a dict of device tensors;
+    ``status`` must be checked by the caller (``raise_status``)."""
     lib = N.load()
     dev = dsk.device
     if out is None:
@@ -695,16 +697,18 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
             _ptr(out["shift_bits"]), _ptr(out["head0_col"]), _ptr(logits),
             _ptr(out["status"])]
     if agent.tc:
-        with PF.span("policy_tc", n, launches=3):
+        with PF.span("policy_tc", n, launches=None):
             N.check(lib.harl_policy_step_tc(
                 *args, _ptr(agent.hid_scratch(n)), _ptr(rng_dev),
                 _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _ptr(grow),
-                m_total, _stream()),
+                m_total, _ptr(feat_out), _stream()),
                 "harl_policy_step_tc")
     else:
         with PF.span("policy", n):
             N.check(lib.harl_policy_step(*args, _ptr(grow), m_total, _stream()),
                     "harl_policy_step")
+        if feat_out is not None:
+            featurize(dsk, out["tiles"], out["knobs"], n, feat_out)
     if gen is not None and inject is None and advance:
         R.skip_u64(gen, 4 * (m_total or n))
     if want_logits:

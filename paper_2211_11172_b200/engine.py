@@ -30,11 +30,21 @@ import ctypes as C
 import numpy as np
 import torch
 
+import os
+
 from . import _native as N
 from . import device as D
 from . import profiling as PF
 from .agent import AgentState, RlConfig
 from .space import SketchTables
+
+
+# HARL_FUSED_STEP=1: policy -> sample/apply -> featurize as one kernel per
+# 128-row tile (k_policy_step_fused).  Correct, but with one 16-warp CTA per
+# SM the sampler's rows run in two serial passes and it measured slower
+# (49.7 us) than the three separate kernels (policy 19.3 + sampler 21.8 +
+# featurize 11.4 us at ~28 warps/SM), so the split launches are the default.
+_FUSED_STEP = os.environ.get("HARL_FUSED_STEP") == "1"
 
 
 @dataclass(frozen=True)
@@ -275,8 +285,10 @@ class EpisodeEngine:
                             want_logits=want_logits,
                             rng_dev=b.rng_tab[k] if graph_mode else None,
                             advance=not graph_mode, grow=grow,
-                            m_total=m_total)
-        D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
+                            m_total=m_total,
+                            feat_out=nxt["feat"] if _FUSED_STEP else None)
+        if not _FUSED_STEP:
+            D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
                       out=nxt["score"], reward=b.reward)
         v_cur, v_next = b.vbuf[(k + 1) % 2], b.vbuf[k % 2]

@@ -36,9 +36,24 @@ def add_launches(n: int):
     _launches += n
 
 
+def _native_count():
+    from . import _native as N
+    return int(N.load(require_device=False).harl_launch_count())
+
+
 @contextlib.contextmanager
-def span(name: str, rows: int, launches: int = 1):
+def span(name: str, rows: int, launches: int | None = 1):
+    """``launches=None``: count the library's own launches in the span
+    (entry points whose kernel count depends on the path they take)."""
     global _launches
+    if launches is None:
+        before = _native_count()
+        try:
+            with span(name, rows, 0):
+                yield
+        finally:
+            _launches += _native_count() - before
+        return
     _launches += launches
     if not _timing:
         yield

@@ -66,3 +66,23 @@ def test_graph_replay_is_bit_identical(hidden, which):
         assert torch.equal(eager.dagent.params, graphed.dagent.params)
         assert torch.equal(eager.dagent.m, graphed.dagent.m)
         assert torch.equal(eager.replay.X, graphed.replay.X)
+
+
+def test_fused_policy_sample_featurize_matches_split(monkeypatch):
+    """k_policy_step_fused (policy -> sample/apply -> featurize in one
+    kernel) produces the split launches' episode bit for bit."""
+    from paper_2211_11172_b200 import engine as E
+    tb, forest, cfg, (_, split) = _setup((128, 128), "conv")
+    _, _, _, (_, fused) = _setup((128, 128), "conv")
+    g1, g2 = np.random.default_rng(9), np.random.default_rng(9)
+    for ep in range(2):
+        monkeypatch.setattr(E, "_FUSED_STEP", False)
+        r1 = split.run_episode(tb, forest, g1, cfg, 0)
+        s1, sc1 = r1.states(), r1.scores().copy()
+        monkeypatch.setattr(E, "_FUSED_STEP", True)
+        r2 = fused.run_episode(tb, forest, g2, cfg, 0)
+        np.testing.assert_array_equal(r2.states()[0], s1[0])
+        np.testing.assert_array_equal(r2.states()[1], s1[1])
+        assert r2.scores().tobytes() == sc1.tobytes()
+        assert torch.equal(split.dagent.params, fused.dagent.params)
+        assert g1.bit_generator.state == g2.bit_generator.state

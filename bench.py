@@ -15,8 +15,10 @@ work is one visited schedule (one CandidateEntry, tuner.py:408-412).
   ranks.
 * ``e2e``: the same metric through the host-buffer call a drop-in makes per
   episode: agent parameters/moments, replay ring, forest and generator state
-  go host->device before and the visited entries (states, scores, rewards)
-  plus the updated agent/ring come back device->host after, every episode.
+  go host->device before; after the episode the device rank_scores
+  (costmodel.py:266-286) selects the top-k' distinct unmeasured entries and
+  those (states, features, scores), the per-visit rewards and the updated
+  agent/ring come back device->host, every episode.
 * ``cpu_baseline``: the oracle (numpy restatement of the reference, bit-exact
   with it) timed on this host on a bounded sample of the same workload.
 * ``--impl reference``: the reference CPU path (the oracle port) with all
@@ -354,11 +356,14 @@ def run_gpu(args, rank, world):
 class E2EHost:
     """The drop-in's host side for the e2e number: pinned host buffers for
     every per-episode input (agent parameters + Adam moments, replay ring,
-    GBT ensemble) and output (visited entries: states, scores, rewards;
-    updated agent and ring), allocated once.  Each timed episode copies the
-    inputs host->device, runs ``_run_episode`` and copies the outputs back
+    GBT ensemble) and output (the rank_scores selection -- top-k' distinct
+    unmeasured entries with states, features, scores -- the per-visit
+    rewards of the trajectory log, the updated agent and ring), allocated
+    once.  Each timed episode copies the inputs host->device, runs
+    ``_run_episode`` + the device rank_scores and copies the outputs back
     (what ``compat.B200TuningSession._run_episode`` moves per round, without
-    the reference's Python object construction)."""
+    the reference's Python object construction).  The selected states
+    accumulate as the "measured" exclusion set, as in a session."""
 
     def __init__(self, eng, w, dev, visits):
         import torch
@@ -375,12 +380,11 @@ class E2EHost:
         for k, t in self.ring_in.items():
             t.copy_(getattr(ring, k))
         self.ring_out = {k: pin(getattr(ring, k)) for k in keys}
-        tb = self.tb
-        self.V = (visits, {
-            "tiles": torch.empty((tb.local_slots, visits), dtype=torch.int16).pin_memory(),
-            "knobs": torch.empty((3, visits), dtype=torch.uint8).pin_memory(),
-            "score": torch.empty(visits, dtype=torch.float64).pin_memory(),
-            "reward": torch.empty(visits, dtype=torch.float64).pin_memory()})
+        self.V = (visits, torch.empty(visits, dtype=torch.float64).pin_memory())
+        from paper_2211_11172_b200 import device as D
+        self.rank_scratch = D.RankScratch(dev)
+        self.top_k = 64                 # TunerConfig.top_k default
+        self.measured = None
 
     def episode(self, forest, gen, ecfg, order):
         import torch
@@ -405,17 +409,22 @@ class E2EHost:
         t2 = time.perf_counter()
         V = res.visits
         if self.V is None or self.V[0] < V:
-            self.V = (V, {
-                "tiles": torch.empty((tb.local_slots, V), dtype=torch.int16).pin_memory(),
-                "knobs": torch.empty((3, V), dtype=torch.uint8).pin_memory(),
-                "score": torch.empty(V, dtype=torch.float64).pin_memory(),
-                "reward": torch.empty(V, dtype=torch.float64).pin_memory()})
-        ho = self.V[1]
-        ho["tiles"][:, :V].copy_(res.log_tiles[:tb.local_slots, :V], non_blocking=True)
-        ho["knobs"][:, :V].copy_(res.log_knobs[:, :V], non_blocking=True)
-        ho["score"][:V].copy_(res.log_score[:V], non_blocking=True)
-        ho["reward"][:V].copy_(res.log_reward[:V], non_blocking=True)
-        nout = V * (2 * tb.local_slots + 3 + 16)
+            self.V = (V, torch.empty(V, dtype=torch.float64).pin_memory())
+        # rank_scores on the device (what run_round consumes): the top-k'
+        # distinct unmeasured entries come back with their features; the
+        # per-visit rewards come back for the trajectory log
+        idx, tiles, knobs, feats, scores, _ = res.top_entries(
+            self.top_k, self.measured, self.rank_scratch)
+        self.V[1][:V].copy_(res.log_reward[:V], non_blocking=True)
+        nout = len(idx) * (2 * tb.local_slots + 3 + 8 * tb.feature_len + 8 + 8) \
+            + V * 8
+        # the chosen states become "measured" for the next episodes
+        mt = tiles if self.measured is None else \
+            np.concatenate([self.measured[0], tiles])
+        mk = knobs if self.measured is None else \
+            np.concatenate([self.measured[1], knobs])
+        self.measured = (mt, mk)
+        t2b = time.perf_counter()
         for k, t in self.agent_out.items():
             t.copy_(getattr(da, k), non_blocking=True)
             nout += t.numel() * t.element_size()
@@ -425,7 +434,7 @@ class E2EHost:
         torch.cuda.current_stream().synchronize()
         t3 = time.perf_counter()
         parts.update(h2d_ms=(t1 - t0) * 1e3, episode_ms=(t2 - t1) * 1e3,
-                     d2h_ms=(t3 - t2) * 1e3)
+                     rank_ms=(t2b - t2) * 1e3, d2h_ms=(t3 - t2b) * 1e3)
         return nin, nout, V, parts
 
 

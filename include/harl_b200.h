@@ -393,6 +393,24 @@ int harl_ppo_wt_fill(const harl_net_layout* pol, const harl_net_layout* val,
 int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
                           void* stream);
 
+/* rank_scores (costmodel.py:266-286) over the entry log: the visits of the
+ * top k distinct states by (score desc, visit asc), excluding n_excluded
+ * states given SoA ([local_slots][ex_ld] tiles, [3][ex_ld] knobs; the
+ * reference's exclude=measured, tuner.py:481-482).  Duplicates collapse to
+ * their first visit.  Writes the selected visit indices (unordered, count
+ * stats[0]) to out_idx; stats (device int64[4]) = {selected, distinct kept,
+ * hash-collision keeps, k'}.  k' = k + collisions: a 64-bit hash collision
+ * keeps the colliding visit (exact compares only), so the selection is a
+ * superset on which the reference's rank_scores gives its exact answer.
+ * out_cap >= k + n_visits is always enough. */
+int64_t harl_rank_scratch_bytes(int64_t n_visits, int64_t n_excluded);
+int harl_rank_topk(const harl_entry_log* log, int32_t local_slots,
+                   int64_t n_visits, const uint16_t* ex_tiles,
+                   const uint8_t* ex_knobs, int64_t ex_ld, int64_t n_excluded,
+                   int64_t k, void* scratch, int64_t scratch_bytes,
+                   int32_t* out_idx, int64_t out_cap, int64_t* stats,
+                   void* stream);
+
 /* Instrumentation (no reference counterpart; the reference has no device).
  * harl_launch_count: kernels this library has launched since load (graph
  * replays excluded -- they do not pass through the library).

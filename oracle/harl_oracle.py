@@ -20,6 +20,7 @@ What it restates (reference files under ``/root/reference/pkg/src/schedtune``):
 * ``actor_grads`` / ``critic_grads`` /
   ``ppo_update`` / ``Adam.step`` ............... rlcore.py:48-71,293-378
 * ``TrackSet.cull`` / ``episode_done`` ......... stopping.py:68-95
+* ``rank_scores`` ............................... costmodel.py:266-286
 
 It is written population-at-once (structure-of-arrays numpy) instead of the
 reference's per-track objects, but every floating-point operation is the
@@ -543,6 +544,24 @@ class Entry:
     features: np.ndarray
     score: float
     order: int
+
+
+def rank_scores(canonicals, scores, orders, k: int, exclude=()):
+    """costmodel.py:266-286 over parallel lists: drop excluded and repeated
+    canonical strings (first occurrence wins), then the top ``k`` by
+    ``(-score, order)``.  ``scores`` are the model's predictions of each
+    entry (predict is pointwise, so scoring the pool after dedup equals
+    indexing the per-entry scores).  Returns positions into the lists."""
+    exclude = set(exclude or ())
+    seen = set()
+    pool = []
+    for i, c in enumerate(canonicals):
+        if c in exclude or c in seen:
+            continue
+        seen.add(c)
+        pool.append(i)
+    ranked = sorted(pool, key=lambda i: (-float(scores[i]), orders[i]))
+    return ranked[:k]
 
 
 def run_episode(tb, num_slots, cfg: EpisodeCfg, agent: Agent, opt_pi: Adam,

@@ -139,6 +139,9 @@ _SIGS = {
     "harl_gather_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp,
                                vp, vp, vp, vp, i64, vp]),
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),
+    "harl_rank_scratch_bytes": (i64, [i64, i64]),
+    "harl_rank_topk": (i32, [P(EntryLog), i32, i64, vp, vp, i64, i64, i64,
+                             vp, i64, vp, i64, vp, vp]),
     "harl_selftest_tcgen05": (i32, [vp, vp, vp, i32, vp]),
     "harl_launch_count": (C.c_longlong, []),
     "harl_debug_timestamps": (i32, [i32, vp, i32]),

@@ -21,6 +21,7 @@
 #include "mlp_tc.cuh"
 #include "sample_kernels.cuh"
 #include "mlp_tc2.cuh"
+#include "rank_kernels.cuh"
 
 namespace harl {
 
@@ -1068,6 +1069,111 @@ int harl_gather_rows(const int32_t* idx, int64_t n_out, int32_t local_slots,
       a, idx, tiles, knobs, feat, score, row_track, tiles_o, knobs_o, feat_o,
       score_o, row_track_o);
   HARL_CHECK_LAUNCH("k_gather_rows");
+  return HARL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// rank_scores on the entry log (rank_kernels.cuh)
+
+static int64_t rank_table_size(int64_t items) {
+  int64_t t = 1024;
+  while (t < 2 * items) t <<= 1;
+  return t;
+}
+
+static int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+int64_t harl_rank_scratch_bytes(int64_t n_visits, int64_t n_excluded) {
+  if (n_visits < 0 || n_excluded < 0) return -1;
+  const int64_t T = rank_table_size(n_visits + n_excluded);
+  return align256((int64_t)sizeof(RankState)) + align256(T * 8) +
+         align256(T * 4) + align256(n_visits > 0 ? n_visits : 1);
+}
+
+int harl_rank_topk(const harl_entry_log* log, int32_t local_slots,
+                   int64_t n_visits, const uint16_t* ex_tiles,
+                   const uint8_t* ex_knobs, int64_t ex_ld, int64_t n_excluded,
+                   int64_t k, void* scratch, int64_t scratch_bytes,
+                   int32_t* out_idx, int64_t out_cap, int64_t* stats,
+                   void* stream) {
+  if (!log || !scratch || !out_idx || !stats || n_visits < 0 ||
+      n_excluded < 0 || k < 0 || local_slots < 0) {
+    set_error("harl_rank_topk: bad arguments");
+    return HARL_E_ARG;
+  }
+  if (n_visits + n_excluded >= (int64_t)INT_MAX) {
+    set_error("harl_rank_topk: %lld items exceed the int32 index range",
+              (long long)(n_visits + n_excluded));
+    return HARL_E_ARG;
+  }
+  if (n_excluded > 0 && (!ex_tiles && local_slots > 0 || !ex_knobs)) {
+    set_error("harl_rank_topk: excluded states without arrays");
+    return HARL_E_ARG;
+  }
+  if (scratch_bytes < harl_rank_scratch_bytes(n_visits, n_excluded)) {
+    set_error("harl_rank_topk: scratch too small");
+    return HARL_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t T = rank_table_size(n_visits + n_excluded);
+  char* p = (char*)scratch;
+  RankArgs a;
+  memset(&a, 0, sizeof(a));
+  a.st = (RankState*)p;
+  p += align256((int64_t)sizeof(RankState));
+  a.keys = (unsigned long long*)p;
+  p += align256(T * 8);
+  a.reps = (int32_t*)p;
+  p += align256(T * 4);
+  a.keep = (uint8_t*)p;
+  a.tiles = log->tiles;
+  a.knobs = log->knobs;
+  a.score = log->score;
+  a.ld = log->ld;
+  a.V = n_visits;
+  a.ex_tiles = ex_tiles;
+  a.ex_knobs = ex_knobs;
+  a.ex_ld = ex_ld;
+  a.E = n_excluded;
+  a.slots = local_slots;
+  a.tmask = T - 1;
+  a.k = k;
+  a.out_idx = out_idx;
+  a.out_cap = out_cap;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(a.st, 0, sizeof(RankState), st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(a.keys, 0, (size_t)T * 8, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(a.reps, 0x7f, (size_t)T * 4, st)) != cudaSuccess)
+    return cuda_status(e, "harl_rank_topk memset");
+  const int64_t items = n_visits + n_excluded;
+  const int cap = sm_count() * 8;
+  auto grid = [&](int64_t n) {
+    int64_t g = (n + 255) / 256;
+    return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+  };
+  if (items > 0) {
+    HARL_PROF_BEGIN(st);
+    launch_k(k_rank_insert, dim3(grid(items)), dim3(256), 0, st, a);
+    HARL_CHECK_LAUNCH("k_rank_insert");
+  }
+  if (n_visits > 0) {
+    HARL_PROF_BEGIN(st);
+    launch_k(k_rank_mark, dim3(grid(n_visits)), dim3(256), 0, st, a);
+    HARL_CHECK_LAUNCH("k_rank_mark");
+  }
+  for (int d = 0; d < 12; ++d) {
+    HARL_PROF_BEGIN(st);
+    launch_k(k_rank_select, dim3(grid(n_visits)), dim3(256), 0, st, a, d);
+    HARL_CHECK_LAUNCH("k_rank_select");
+  }
+  if (n_visits > 0) {
+    HARL_PROF_BEGIN(st);
+    launch_k(k_rank_emit, dim3(grid(n_visits)), dim3(256), 0, st, a);
+    HARL_CHECK_LAUNCH("k_rank_emit");
+  }
+  HARL_PROF_BEGIN(st);
+  launch_k(k_rank_stats, dim3(1), dim3(1), 0, st, a, stats);
+  HARL_CHECK_LAUNCH("k_rank_stats");
   return HARL_OK;
 }
 

@@ -16,6 +16,7 @@ this module                    reference
 ``policy_step``                select_actions 216-228 (+ walker)
 ``value_estimate``             ValueNet.estimate 173-174
 ``DeviceAgent.ppo_update``     ppo_update 361-378
+``rank_topk``                  costmodel.rank_scores 266-286
 =============================  ==========================================
 """
 
@@ -205,6 +206,88 @@ def featurize(dsk: DeviceSketch, tiles, knobs, n: int, out=None):
                                    n, tiles.shape[1], _ptr(out), _stream()),
                 "harl_featurize")
     return out[:n]
+
+
+class RankScratch:
+    """Reusable device scratch of ``rank_topk`` (grown on demand)."""
+
+    def __init__(self, device=None):
+        self.device = _dev(device)
+        self.buf = None
+        self.out = None
+        self.stats = torch.zeros(4, dtype=torch.int64, device=self.device)
+
+    def ensure(self, n_visits: int, n_excluded: int, k: int):
+        need = N.load().harl_rank_scratch_bytes(n_visits, n_excluded)
+        if self.buf is None or self.buf.numel() < need:
+            self.buf = torch.empty(need, dtype=torch.uint8, device=self.device)
+        cap = k + n_visits
+        if self.out is None or self.out.numel() < cap:
+            self.out = torch.empty(max(cap, 1), dtype=torch.int32,
+                                   device=self.device)
+
+
+def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
+              n_visits: int, k: int, exclude=None, scratch=None):
+    """``rank_scores(model, entries, k, exclude)`` (costmodel.py:266-286)
+    over a device entry log whose ``log_score`` holds each visit's model
+    score (the episode's per-visit GBT predictions, which equal
+    ``model.predict(features)`` since predict is pointwise and the model is
+    fixed within an episode).
+
+    ``exclude``: optional host ``(tiles [E, slots] u16, knobs [E, 3] u8)``
+    of already-measured states of this sketch.  Returns the selected visit
+    indices (ascending, so first occurrences come first) and the device
+    stats ``{selected, kept, collisions, k_target}``.  The selection is a
+    superset of the reference's answer on which ``rank_scores`` returns
+    exactly that answer (it equals the answer when ``collisions == 0``)."""
+    lib = N.load()
+    dev = log_score.device
+    sc = scratch if scratch is not None else RankScratch(dev)
+    E = 0
+    ex_t = ex_k = None
+    if exclude is not None and len(exclude[1]):
+        E = len(exclude[1])
+        ex_t, ex_k = states_to_device(tables, exclude[0], exclude[1], dev)
+    sc.ensure(n_visits, E, k)
+    elog = N.EntryLog(log_tiles.data_ptr(), log_knobs.data_ptr(),
+                      log_score.data_ptr(), 0, 0, log_tiles.shape[1])
+    with PF.span("rank", n_visits):
+        N.check(lib.harl_rank_topk(
+            C.byref(elog), tables.local_slots, n_visits, _ptr(ex_t),
+            _ptr(ex_k), 0 if ex_t is None else ex_t.shape[1], E, k,
+            sc.buf.data_ptr(), sc.buf.numel(), sc.out.data_ptr(),
+            sc.out.numel(), sc.stats.data_ptr(), _stream()),
+            "harl_rank_topk")
+    st = sc.stats.cpu().numpy()
+    n = int(st[0])
+    idx = np.sort(sc.out[:n].cpu().numpy().astype(np.int64))
+    return idx, {"selected": n, "kept": int(st[1]), "collisions": int(st[2]),
+                 "k_target": int(st[3])}
+
+
+def gather_entries(tables: SketchTables, log_tiles, log_knobs, log_score,
+                   log_track, idx):
+    """Device gather of visits ``idx`` of an entry log -> device SoA
+    (tiles, knobs), scores and tracks, plus their features (featurize on
+    device: the features the reference stored in the CandidateEntry)."""
+    lib = N.load()
+    dev = log_score.device
+    n = len(idx)
+    didx = torch.from_numpy(np.asarray(idx, np.int32)).to(dev)
+    tiles, knobs = alloc_state(n, tables, dev)
+    score = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    track = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    if n:
+        N.check(lib.harl_gather_rows(
+            didx.data_ptr(), n, tables.local_slots, 0,
+            log_tiles.data_ptr(), log_knobs.data_ptr(), None,
+            log_score.data_ptr(), log_track.data_ptr(), log_tiles.shape[1],
+            tiles.data_ptr(), knobs.data_ptr(), None, score.data_ptr(),
+            track.data_ptr(), tiles.shape[1], _stream()),
+            "harl_gather_rows")
+    feats = featurize(DeviceSketch(tables, dev), tiles, knobs, n)
+    return tiles, knobs, score[:n], track[:n], feats
 
 
 def action_masks(dsk: DeviceSketch, tiles, knobs, n: int):

@@ -140,6 +140,20 @@ class EpisodeResult:
     def scores(self) -> np.ndarray:
         return self.log_score[:self.visits].cpu().numpy()
 
+    def top_entries(self, k: int, exclude=None, scratch=None):
+        """``rank_scores(model, entries, k, exclude)`` on the device entry
+        log (costmodel.py:266-286): (visit indices ascending, host tiles
+        [n, slots] u16, knobs [n, 3] u8, features [n, F] f64, scores [n],
+        stats).  See ``device.rank_topk`` for the superset contract."""
+        idx, stats = D.rank_topk(self.tables, self.log_tiles, self.log_knobs,
+                                 self.log_score, self.visits, k, exclude,
+                                 scratch)
+        t, kn, sc, _, f = D.gather_entries(self.tables, self.log_tiles,
+                                           self.log_knobs, self.log_score,
+                                           self.log_track, idx)
+        tiles, knobs = D.states_to_host(self.tables, t, kn, len(idx))
+        return (idx, tiles, knobs, f.cpu().numpy(), sc.cpu().numpy(), stats)
+
     def rewards_per_step(self):
         r = self.log_reward[:self.visits].cpu().numpy()
         out, p = [], 0

@@ -308,6 +308,26 @@ class SketchTables:
                                  unroll_index=int(k[2])))
         return out
 
+    def arrays_from_canonical(self, texts) -> tuple:
+        """Canonical strings of this sketch (``sk|t=a.b;..|ca=|par=|ur=``,
+        schedspace.py:117-120) -> (tiles u16 [E, local_slots], knobs u8
+        [E, 3]); strings of other sketches are skipped."""
+        tiles, knobs = [], []
+        for c in texts:
+            sk, t, ca, par, ur = c.rsplit("|", 4)
+            if sk != self.sketch_id:
+                continue
+            flat = [int(v) for d in t[2:].split(";") if d
+                    for v in d.split(".")]
+            if len(flat) != self.local_slots:
+                raise ValueError(f"canonical state {c!r} does not match "
+                                 f"sketch {self.sketch_id}")
+            tiles.append(flat)
+            knobs.append((int(ca[3:]), int(par[4:]), int(ur[3:])))
+        return (np.asarray(tiles, np.uint16).reshape(len(tiles),
+                                                     self.local_slots),
+                np.asarray(knobs, np.uint8).reshape(len(knobs), 3))
+
     def canonical(self, tiles_row, knobs_row) -> str:
         L = self.levels
         tl = [tiles_row[d * L:(d + 1) * L] for d in range(self.ndims)]

@@ -238,6 +238,21 @@ def main():
                 "\n".join(e.canonical for e in entries).encode()).hexdigest()
             ep["entries_order"] = [entries[0].order, entries[-1].order,
                                    len(entries)]
+            # rank_scores (costmodel.py:266-286) on these entries: several k,
+            # with and without an exclude set of already-measured states
+            from schedtune.costmodel import rank_scores
+            distinct = list(dict.fromkeys(e.canonical for e in entries))
+            excl = set(distinct[::5]) | set(
+                e.canonical for e in rank_scores(session.model, entries, 3))
+            ep["rank"] = []
+            for k in (1, 8, 64, len(entries) + 5):
+                for ex in (None, excl):
+                    chosen = rank_scores(session.model, entries, k,
+                                         exclude=ex)
+                    ep["rank"].append({
+                        "k": k,
+                        "exclude": sorted(ex) if ex else [],
+                        "chosen": [e.order for e in chosen]})
             ep["end_rng_state"] = session.rng.bit_generator.state
             ep["end_policy_digest"] = digest_list(agent.policy.params())
             ep["end_value_digest"] = digest_list(agent.value.params())

@@ -107,3 +107,8 @@ def config_tables():
     cases += all_sketch_tables(TCONV, W.TargetConfig(tiling_levels=3))
     cases += all_sketch_tables(ELEMENTWISE)
     return cases
+
+
+def conv_tables():
+    """Sketch k0 of the conv2d config (C2)."""
+    return all_sketch_tables(CONV)[0][2]

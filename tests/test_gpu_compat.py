@@ -36,7 +36,7 @@ subgraphs:
 """
 
 
-def _sessions(tmp_path, hidden, searcher="rl"):
+def _sessions(tmp_path, hidden, searcher="rl", total_trials=24):
     from schedtune.measure import SimulatedBackend
     from schedtune.tuner import TunerConfig, TuningSession
     from schedtune.workload import TargetConfig, load_network
@@ -44,7 +44,7 @@ def _sessions(tmp_path, hidden, searcher="rl"):
     p = tmp_path / "w.yaml"
     p.write_text(GEMM64)
     net = load_network(str(p))
-    cfg = TunerConfig(total_trials=24, top_k=8, min_tracks=8,
+    cfg = TunerConfig(total_trials=total_trials, top_k=8, min_tracks=8,
                       initial_tracks=16, cull_window=3, episode_len=6,
                       hidden=hidden, minibatch=32, buffer_capacity=64)
     tgt = TargetConfig(tiling_levels=2)
@@ -91,3 +91,37 @@ def test_drop_in_checkpoint_round_trip(tmp_path):
     assert arrays[f"buffer/{sg}/mask0"].dtype == bool
     for i, p in enumerate(dev.agents[sg].policy.params()):
         np.testing.assert_array_equal(arrays[f"agent/{sg}/pi/{i}"], p)
+
+
+@pytest.mark.parametrize("searcher", ["rl", "evolutionary"])
+def test_drop_in_topk_entries_rank_like_full_list(tmp_path, searcher):
+    """The default entry list (device top-k' superset) and the full visit
+    list give run_round the same rank_scores answer, round after round
+    (the measured set grows, so exclusions are exercised)."""
+    from schedtune.costmodel import rank_scores
+    _, dev = _sessions(tmp_path, (16,), searcher, total_trials=64)
+    orig = dev._b200_entries
+    seen = []
+
+    def spy(res, tables, sketch):
+        top = orig(res, tables, sketch)
+        dev.b200_all_entries = True
+        try:
+            full = orig(res, tables, sketch)
+        finally:
+            dev.b200_all_entries = False
+        k_hat = min(dev.cfg.top_k, dev.cfg.total_trials - dev.trials_used)
+        a = rank_scores(dev.model, top, k_hat, exclude=dev.measured)
+        b = rank_scores(dev.model, full, k_hat, exclude=dev.measured)
+        assert [(e.order, e.canonical) for e in a] == \
+            [(e.order, e.canonical) for e in b]
+        for x, y in zip(a, b):
+            assert x.features.tobytes() == y.features.tobytes()
+        assert len(top) <= len(full) == res.visits
+        seen.append((len(top), len(full), len(dev.measured)))
+        return top
+
+    dev._b200_entries = spy
+    while dev.trials_used < dev.cfg.total_trials:
+        dev.run_round()
+    assert len(seen) >= 4 and seen[-1][2] > 0

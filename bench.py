@@ -90,6 +90,9 @@ subgraphs:
   - id: gemm_4096x4096x4096
     nodes: [{name: mm, kind: matmul, shape: {m: 4096, k: 4096, n: 4096}}]
 """, sketch=0, population=65536),
+    "c4": dict(workload="ResNet-50 v1.5 task set (workloads/resnet50.yaml: 24 "
+               "subgraphs), searcher rl (adaptive), tasks sharded over ranks",
+               yaml=None, sketch=None, population=4096),
 }
 
 
@@ -584,6 +587,9 @@ def main():
     cfgd = CONFIGS[args.config]
     P = args.population or cfgd["population"]
 
+    if args.config == "c4":
+        taskset_main(args, P, rank, world)
+        return
     if args.impl == "reference":
         if rank != 0:
             return
@@ -672,6 +678,136 @@ def reference_arm(args, P, cfgd):
                                        f"{steps} steps"},
             "e2e": {"value": round(value, 1), "unit": UNIT,
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# C4: the ResNet-50 task set through the reference session (drop-in)
+
+
+def _ref_import():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    import schedtune  # noqa: F401  (raises ImportError when absent)
+
+
+def taskset_session(cls_name, P, rank, world, rounds_budget):
+    """A TuningSession (reference or B200 subclass) over this rank's share
+    of the ResNet-50 task set."""
+    import dataclasses
+    from schedtune.measure import SimulatedBackend
+    from schedtune.tuner import TunerConfig, TuningSession
+    from schedtune.workload import TargetConfig, load_network
+    from paper_2211_11172_b200.shard import shard_tasks
+    net = load_network(os.path.join(ROOT, "workloads", "resnet50.yaml"))
+    mine = shard_tasks(len(net.subgraphs), world, rank)
+    sub = dataclasses.replace(net, subgraphs=tuple(net.subgraphs[i]
+                                                   for i in mine))
+    cfg = TunerConfig(seed=rank, total_trials=64 * rounds_budget,
+                      top_k=64, initial_tracks=P, min_tracks=P // 2)
+    cls = TuningSession
+    if cls_name == "b200":
+        from paper_2211_11172_b200.compat import b200_session_class
+        cls = b200_session_class(TuningSession)
+    return cls(sub, TargetConfig(), cfg, SimulatedBackend(), "rl"), mine
+
+
+def taskset_main(args, P, rank, world):
+    """One bench step = one tuning round of a session (bandit pick of a
+    subgraph + sketch, _run_episode over P tracks with adaptive culls,
+    rank_scores, simulated measurement, GBT refit).  schedules/s = visited
+    candidates / wall time of the rounds, summed over ranks (max time)."""
+    try:
+        _ref_import()
+    except ImportError as exc:
+        if rank == 0:
+            print(json.dumps({"impl": args.impl, "unavailable":
+                              f"config c4 needs the reference session "
+                              f"(baseline/_ref): {exc}"}))
+        return
+    ref = args.impl == "reference"
+    if ref and rank != 0:
+        return
+    if not ref and world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    if not ref:
+        import torch
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    steps = args.steps if not ref else min(args.steps, 2)
+    warm = args.warmup if not ref else 0
+    sess, mine = taskset_session("reference" if ref else "b200", P,
+                                 rank, 1 if ref else world,
+                                 warm + steps + 1)
+    ep_ms = [0.0]
+    if not ref:
+        import torch
+        orig = sess._run_episode
+
+        def timed(sg, sketch, rnd):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            out = orig(sg, sketch, rnd)
+            torch.cuda.synchronize()
+            ep_ms[0] += (time.perf_counter() - t) * 1e3
+            return out
+        sess._run_episode = timed
+    for _ in range(warm):
+        sess.run_round()
+    v0, ep_ms[0] = sess.order_counter, 0.0
+    if not ref and world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sess.run_round()
+    secs = time.perf_counter() - t0
+    visits = sess.order_counter - v0
+    tot_v, max_s = visits, secs
+    if not ref and world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(visits)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        tot_v = int(t.item())
+        t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_s = float(t.item())
+    if rank != 0:
+        return
+    value = tot_v / max_s
+    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT,
+            "n_gpus": 0 if ref else world, "steps": steps, "warmup": warm,
+            "ms_per_step": round(1e3 * max_s / steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp64 (numpy)" if ref else
+                     "fp32 networks + fp64 features/GBT/PPO",
+            "data": "synthetic (random-init agents, SimulatedBackend "
+                    "measurements)",
+            "config": {"workload": CONFIGS["c4"]["workload"],
+                       "population_per_task": P,
+                       "tasks_rank0": len(mine),
+                       "step": "one TuningSession.run_round (episode + "
+                               "rank_scores + measure + GBT refit)",
+                       "parallelism": "reference CPU session, 1 process"
+                       if ref else f"tasks sharded i mod {world}"}}
+    if ref:
+        line["impl"] = "reference"
+        line["cpu_baseline"] = {"value": round(value, 1), "unit": UNIT,
+                                "cores": 1, "kind": "reference",
+                                "sample": f"{steps} rounds of the reference "
+                                          f"session on rank 0's tasks"}
+        line["e2e"] = {"value": round(value, 1), "unit": UNIT,
+                       "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    else:
+        line["e2e"] = {"value": round(value, 1), "unit": UNIT,
+                       "note": "the whole round is host-driven through the "
+                               "reference session; episode (device) share "
+                               f"{ep_ms[0] / (1e3 * secs):.3f}"}
+        line["ms_per_step_parts"] = {
+            "episode_ms": round(ep_ms[0] / steps, 2),
+            "host_ms": round((1e3 * secs - ep_ms[0]) / steps, 2)}
     print(json.dumps(line))
 
 

@@ -13,7 +13,9 @@ import os
 from .errors import DeviceError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libharl_b200.so")
+# HARL_LIB_PATH: a variant build (build.py --out/-D) for A/B measurements
+LIB_PATH = os.environ.get("HARL_LIB_PATH") or \
+    os.path.join(HERE, "libharl_b200.so")
 
 MAX_DIMS, MAX_LEVELS, MAX_SLOTS = 16, 8, 64
 MAX_STAGES, MAX_TENSORS, MAX_TERMS = 16, 48, 160

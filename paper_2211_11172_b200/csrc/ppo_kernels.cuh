@@ -33,8 +33,13 @@ struct PpoArgs {
 
 typedef harl_replay_ring PpoRing;
 
+#ifndef HARL_PPO_WIDE
+#define HARL_PPO_WIDE 2
+#endif
 constexpr int PPO_TM = 2;
-constexpr int PPO_THREADS = 128 * PPO_TM;   // 4 warps per row in the loss terms
+// HARL_PPO_WIDE x 4 warps per row: the loss terms use 4 warps per row, the
+// dense layers split each output's reduction over the extra threads
+constexpr int PPO_THREADS = 128 * PPO_TM * HARL_PPO_WIDE;
 
 // Latency-bound small-batch layers: every thread keeps PPO_UNR weight
 // loads in flight (issued before the FMAs that consume them); the CTA's
@@ -44,7 +49,10 @@ constexpr int PPO_UNR = 16;
 // Each output is split over up to PPO_SPLIT threads along the reduction
 // (contiguous k ranges summed in part order: deterministic), so a thread's
 // chain of dependent weight-load rounds is PPO_SPLIT times shorter.
-constexpr int PPO_SPLIT = 4;
+#ifndef HARL_PPO_SPLIT
+#define HARL_PPO_SPLIT 4
+#endif
+constexpr int PPO_SPLIT = HARL_PPO_SPLIT;
 
 __device__ inline int ppo_parts(int outputs) {
   int p = (int)blockDim.x / (outputs > 0 ? outputs : 1);

@@ -228,7 +228,8 @@ class RankScratch:
 
 
 def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
-              n_visits: int, k: int, exclude=None, scratch=None):
+              n_visits: int, k: int, exclude=None, scratch=None,
+              sort: bool = True):
     """``rank_scores(model, entries, k, exclude)`` (costmodel.py:266-286)
     over a device entry log whose ``log_score`` holds each visit's model
     score (the episode's per-visit GBT predictions, which equal
@@ -238,7 +239,8 @@ def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
     ``exclude``: optional host ``(tiles [E, slots] u16, knobs [E, 3] u8)``
     of already-measured states of this sketch.  Returns the selected visit
     indices (ascending, so first occurrences come first) and the device
-    stats ``{selected, kept, collisions, k_target}``.  The selection is a
+    stats ``{selected, kept, collisions, k_target}``; ``sort=False``
+    returns (device int32 indices, unordered; count; stats) instead.  The selection is a
     superset of the reference's answer on which ``rank_scores`` returns
     exactly that answer (it equals the answer when ``collisions == 0``)."""
     lib = N.load()
@@ -261,20 +263,23 @@ def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
             "harl_rank_topk")
     st = sc.stats.cpu().numpy()
     n = int(st[0])
-    idx = np.sort(sc.out[:n].cpu().numpy().astype(np.int64))
-    return idx, {"selected": n, "kept": int(st[1]), "collisions": int(st[2]),
-                 "k_target": int(st[3])}
+    stats = {"selected": n, "kept": int(st[1]), "collisions": int(st[2]),
+             "k_target": int(st[3])}
+    if not sort:
+        return sc.out, n, stats
+    return np.sort(sc.out[:n].cpu().numpy().astype(np.int64)), stats
 
 
 def gather_entries(tables: SketchTables, log_tiles, log_knobs, log_score,
-                   log_track, idx):
+                   log_track, idx, dsk=None):
     """Device gather of visits ``idx`` of an entry log -> device SoA
     (tiles, knobs), scores and tracks, plus their features (featurize on
     device: the features the reference stored in the CandidateEntry)."""
     lib = N.load()
     dev = log_score.device
     n = len(idx)
-    didx = torch.from_numpy(np.asarray(idx, np.int32)).to(dev)
+    didx = idx if isinstance(idx, torch.Tensor) else \
+        torch.from_numpy(np.asarray(idx, np.int32)).to(dev)
     tiles, knobs = alloc_state(n, tables, dev)
     score = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
     track = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
@@ -286,7 +291,8 @@ def gather_entries(tables: SketchTables, log_tiles, log_knobs, log_score,
             tiles.data_ptr(), knobs.data_ptr(), None, score.data_ptr(),
             track.data_ptr(), tiles.shape[1], _stream()),
             "harl_gather_rows")
-    feats = featurize(DeviceSketch(tables, dev), tiles, knobs, n)
+    feats = featurize(dsk if dsk is not None else DeviceSketch(tables, dev),
+                      tiles, knobs, n)
     return tiles, knobs, score[:n], track[:n], feats
 
 
@@ -366,27 +372,34 @@ class DeviceForest:
 
     @classmethod
     def _records(cls, trees, learning_rate):
+        """All trees' node records in one vectorised pass (the per-round
+        host cost of a refit reload)."""
         if len(trees) > 1024:
             raise DeviceError("more than 1024 trees")
-        recs, firsts, n = [], [], 0
-        for feat, thr, left, right, val in trees:
-            feat = np.asarray(feat)
-            left, right = np.asarray(left), np.asarray(right)
-            _check_depth(feat, left, right)
-            rec = np.zeros(len(feat), dtype=cls.NODE)
-            leaf = feat < 0
-            # leaves carry learning_rate * value: the reference's fp64
-            # product (costmodel.py:224), formed here once
-            rec["v"] = np.where(leaf, learning_rate * np.asarray(val, np.float64),
-                                np.asarray(thr, np.float64))
-            rec["feat"] = feat.astype(np.int16)
-            rec["left"] = np.where(leaf, 0, left).astype(np.int16)
-            rec["right"] = np.where(leaf, 0, right).astype(np.int16)
-            recs.append(rec)
-            firsts.append(n)
-            n += len(feat)
-        nodes = np.concatenate(recs) if recs else np.zeros(0, cls.NODE)
-        return nodes, np.asarray(firsts, dtype=np.int32)
+        if not trees:
+            return np.zeros(0, cls.NODE), np.zeros(0, np.int32)
+        sizes = np.fromiter((len(t[0]) for t in trees), np.int64, len(trees))
+        if sizes.max() > 32767:
+            raise DeviceError("tree too large for int16 node indices")
+        firsts = np.zeros(len(trees), np.int64)
+        np.cumsum(sizes[:-1], out=firsts[1:])
+        feat = np.concatenate([np.asarray(t[0]) for t in trees])
+        thr = np.concatenate([np.asarray(t[1], np.float64) for t in trees])
+        left = np.concatenate([np.asarray(t[2]) for t in trees])
+        right = np.concatenate([np.asarray(t[3]) for t in trees])
+        val = np.concatenate([np.asarray(t[4], np.float64) for t in trees])
+        leaf = feat < 0
+        off = np.repeat(firsts, sizes)
+        _check_depth_all(feat, np.where(leaf, 0, left) + off,
+                         np.where(leaf, 0, right) + off, firsts)
+        rec = np.zeros(len(feat), dtype=cls.NODE)
+        # leaves carry learning_rate * value: the reference's fp64
+        # product (costmodel.py:224), formed here once
+        rec["v"] = np.where(leaf, learning_rate * val, thr)
+        rec["feat"] = feat.astype(np.int16)
+        rec["left"] = np.where(leaf, 0, left).astype(np.int16)
+        rec["right"] = np.where(leaf, 0, right).astype(np.int16)
+        return rec, firsts.astype(np.int32)
 
     def _write(self, nodes, firsts, base, fitted, floor_value):
         self.n_nodes = len(nodes)
@@ -435,20 +448,16 @@ class DeviceForest:
                          model.cfg.learning_rate, fitted=model.fitted)
 
 
-def _check_depth(feat, left, right):
+def _check_depth_all(feat, left_g, right_g, roots):
     """The reference walks at most 64 levels (costmodel.py:67-78); reject
-    deeper trees and node indices int16 cannot hold.  Level-synchronous
-    (vectorised) traversal from the root."""
-    feat = np.asarray(feat)
-    if len(feat) > 32767:
-        raise DeviceError("tree too large for int16 node indices")
-    frontier = np.zeros(1, dtype=np.int64)
+    deeper trees.  All trees at once: global child indices, one
+    level-synchronous walk from every root."""
+    frontier = np.asarray(roots, dtype=np.int64)
     for _ in range(64):
         inner = frontier[feat[frontier] >= 0]
         if inner.size == 0:
             return
-        frontier = np.concatenate([np.asarray(left)[inner],
-                                   np.asarray(right)[inner]]).astype(np.int64)
+        frontier = np.concatenate([left_g[inner], right_g[inner]])
     raise DeviceError("tree deeper than the reference's 64-step walk")
 
 

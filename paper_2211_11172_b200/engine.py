@@ -145,14 +145,19 @@ class EpisodeResult:
         log (costmodel.py:266-286): (visit indices ascending, host tiles
         [n, slots] u16, knobs [n, 3] u8, features [n, F] f64, scores [n],
         stats).  See ``device.rank_topk`` for the superset contract."""
-        idx, stats = D.rank_topk(self.tables, self.log_tiles, self.log_knobs,
-                                 self.log_score, self.visits, k, exclude,
-                                 scratch)
+        didx, n, stats = D.rank_topk(self.tables, self.log_tiles,
+                                     self.log_knobs, self.log_score,
+                                     self.visits, k, exclude, scratch,
+                                     sort=False)
         t, kn, sc, _, f = D.gather_entries(self.tables, self.log_tiles,
                                            self.log_knobs, self.log_score,
-                                           self.log_track, idx)
-        tiles, knobs = D.states_to_host(self.tables, t, kn, len(idx))
-        return (idx, tiles, knobs, f.cpu().numpy(), sc.cpu().numpy(), stats)
+                                           self.log_track, didx[:n],
+                                           self.extra.get("dsk"))
+        idx = didx[:n].cpu().numpy().astype(np.int64)
+        tiles, knobs = D.states_to_host(self.tables, t, kn, n)
+        f, sc = f.cpu().numpy(), sc.cpu().numpy()
+        o = np.argsort(idx, kind="stable")
+        return (idx[o], tiles[o], knobs[o], f[o], sc[o], stats)
 
     def rewards_per_step(self):
         r = self.log_reward[:self.visits].cpu().numpy()
@@ -420,7 +425,8 @@ class EpisodeEngine:
                              log_track=b.log_track,
                              step_rows=[s["m"] for s in b.plan], culls=culls,
                              train=train, track_steps=b.steps,
-                             track_best_step=b.best_step, alive=alive)
+                             track_best_step=b.best_step, alive=alive,
+                             extra={"dsk": b.dsk})
 
     # ---- eager path (parity hooks) ------------------------------------------
 

@@ -86,3 +86,12 @@ def cull_decision(alive, track_ids, adv, fraction, min_tracks):
     full[np.asarray(track_ids, dtype=np.int64)] = adv
     order = np.lexsort((-live, full[live]))
     return np.sort(live[order[:n_elim]])
+
+
+def shard_tasks(n_tasks: int, world: int, rank: int) -> list:
+    """Independent subgraph tasks of a task set (config C4): task i on rank
+    i mod world.  Each rank tunes its tasks in its own session (no
+    collective on the data path; SURVEY.md §8(e) task sharding)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return [i for i in range(n_tasks) if i % world == rank]

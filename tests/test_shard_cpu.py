@@ -213,3 +213,14 @@ def test_sharded_oracle_episode_matches_single_device():
         np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-12)
     for a, b in zip(out[0][1], out[1][1]):
         np.testing.assert_array_equal(a, b)
+
+
+def test_shard_tasks_interleaved_partition():
+    from paper_2211_11172_b200.shard import shard_tasks
+    for world in (1, 2, 4, 8):
+        parts = [shard_tasks(24, world, r) for r in range(world)]
+        assert sorted(i for p in parts for i in p) == list(range(24))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+        assert parts[0][:2] == [0, world][:len(parts[0][:2])]
+    with pytest.raises(ValueError):
+        shard_tasks(24, 2, 2)

@@ -138,6 +138,12 @@ int harl_device_query(int device, int* sm_count_host, int* cc_major_host,
  * track-major.  Exact including rejection draws (repaired sequentially).
  * Writes the number of 32-bit words consumed to *u32_used_host.
  * scratch: >= 16 bytes device. */
+/* Build (once per stream increment) the device jump table the samplers use
+ * for numpy's PCG64 stream; call before capturing a graph that samples from
+ * this generator (during capture a missing table falls back to the slower
+ * bitwise jump -- same draws). */
+int harl_rng_prepare(const harl_pcg64* rng);
+
 int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
                          int64_t count, uint16_t* tiles, uint8_t* knobs,
                          int64_t ld, int64_t* u32_used_host, void* scratch,

@@ -114,6 +114,7 @@ _SIGS = {
     "harl_device_query": (i32, [i32, P(i32), P(i32), P(i32)]),
     "harl_init_population": (i32, [P(SketchDesc), P(Pcg64), i64, vp, vp, i64,
                                    P(i64), vp, vp]),
+    "harl_rng_prepare": (i32, [P(Pcg64)]),
     "harl_featurize": (i32, [P(SketchDesc), vp, vp, i64, i64, vp, vp]),
     "harl_uniform_scratch_bytes": (i64, [i64]),
     "harl_uniform_actions": (i32, [P(SketchDesc), vp, vp, i64, i64, P(Pcg64),

@@ -126,6 +126,41 @@ __device__ inline uint64_t pcg_draw64(const PcgJump& J, u128 s, uint64_t k) {
   return pcg_output(pcg_advance(J, s, k));
 }
 
+// Byte-sliced jump table of one stream increment: entry [L][b] advances
+// b * 256^L steps, so any k < 2^32 is at most four table jumps (loads
+// independent of the state, issued up front) instead of one dependent
+// multiply per set bit with lane-divergent table indices.  Lives in
+// global memory (32 KB, built once per increment by the host library).
+struct PcgTab {
+  u128 A[4 * 256];
+  u128 C[4 * 256];
+};
+
+__device__ inline u128 ldg_u128(const u128* p) {
+  const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+  u128 r;
+  r.hi = v.x;
+  r.lo = v.y;
+  return r;
+}
+
+__device__ inline u128 pcg_advance_tab(const PcgTab* T, u128 s, uint32_t k) {
+#pragma unroll
+  for (int L = 0; L < 4; ++L) {
+    const uint32_t b = (k >> (8 * L)) & 255u;
+    if (b) s = add128(mul128(ldg_u128(&T->A[L * 256 + b]), s),
+                      ldg_u128(&T->C[L * 256 + b]));
+  }
+  return s;
+}
+
+// k-th draw with the table when there is one (and k fits), else bitwise
+__device__ inline uint64_t pcg_draw64t(const PcgTab* T, const PcgJump& J,
+                                       u128 s, uint64_t k) {
+  if (T && k < (1ull << 32)) return pcg_output(pcg_advance_tab(T, s, (uint32_t)k));
+  return pcg_output(pcg_advance(J, s, k));
+}
+
 __device__ inline double u64_to_unit(uint64_t x) {
   return (double)(x >> 11) * (1.0 / 9007199254740992.0);
 }

@@ -134,6 +134,64 @@ static void build_jump(const harl_pcg64& g, PcgJump* J) {
   }
 }
 
+// byte-sliced jump tables (PcgTab), one per stream increment, built on the
+// host and uploaded once; never freed (captured graphs bake the pointer)
+static std::mutex g_tab_mu;
+static std::vector<std::pair<h128, PcgTab*>> g_tabs;
+
+static h128 to_h128(u128 x) { return ((h128)x.hi << 64) | (h128)x.lo; }
+
+static int build_pcg_tab(const harl_pcg64& g, PcgTab** out) {
+  const h128 inc = ((h128)g.inc_hi << 64) | (h128)g.inc_lo;
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto& e : g_tabs)
+    if (e.first == inc) {
+      *out = e.second;
+      return HARL_OK;
+    }
+  PcgJump J;
+  build_jump(g, &J);
+  std::vector<PcgTab> host(1);
+  PcgTab& T = host[0];
+  for (int L = 0; L < 4; ++L) {
+    // one step of this level advances 256^L draws: (A, C) = J[8L]
+    const h128 A1 = to_h128(J.A[8 * L]), C1 = to_h128(J.C[8 * L]);
+    h128 A = 1, C = 0;
+    for (int b = 0; b < 256; ++b) {
+      T.A[L * 256 + b] = to_u128(A);
+      T.C[L * 256 + b] = to_u128(C);
+      C = A1 * C + C1;  // compose one more level step after (A, C)
+      A = A1 * A;
+    }
+  }
+  PcgTab* dev = nullptr;
+  cudaError_t e = cudaMalloc(&dev, sizeof(PcgTab));
+  if (e != cudaSuccess) return cuda_status(e, "pcg table alloc");
+  e = cudaMemcpy(dev, &T, sizeof(PcgTab), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_status(e, "pcg table upload");
+  g_tabs.push_back({inc, dev});
+  *out = dev;
+  return HARL_OK;
+}
+
+// the table of this stream if it exists or can be built now (not while the
+// stream is being captured); null -> kernels use the bitwise jump
+static const PcgTab* pcg_tab_for(const harl_pcg64* rng, cudaStream_t st) {
+  if (!rng) return nullptr;
+  const h128 inc = ((h128)rng->inc_hi << 64) | (h128)rng->inc_lo;
+  {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    for (auto& e : g_tabs)
+      if (e.first == inc) return e.second;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess ||
+      cs != cudaStreamCaptureStatusNone)
+    return nullptr;
+  PcgTab* t = nullptr;
+  return build_pcg_tab(*rng, &t) == HARL_OK ? t : nullptr;
+}
+
 static inline u128 state_of(const harl_pcg64& g) {
   u128 s;
   s.hi = g.state_hi;
@@ -276,6 +334,16 @@ static int check_mlp(const harl_mlp_desc* m, bool policy) {
 using namespace harl;
 
 extern "C" {
+
+int harl_rng_prepare(const harl_pcg64* rng) {
+  if (!rng) {
+    set_error("harl_rng_prepare: null generator");
+    return HARL_E_ARG;
+  }
+  PcgTab* t = nullptr;
+  return build_pcg_tab(*rng, &t);
+}
+
 
 int harl_abi_version(void) { return HARL_ABI_VERSION; }
 
@@ -622,6 +690,7 @@ static SampleArgs sample_args(const float* logits, int ldz, int64_t n, int64_t l
   a.status = (unsigned long long*)status;
   a.grow = grow;
   a.m_total = m_total > 0 ? m_total : n;
+  a.pcg_tab = nullptr;
   return a;
 }
 
@@ -662,6 +731,7 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   a.status = (unsigned long long*)status;
   a.grow = grow;
   a.m_total = m_total > 0 ? m_total : n;
+  a.pcg_tab = pcg_tab_for(rng, st);
   const int rows_per_cta = SAMPLE_THREADS / SG;
   HARL_PROF_BEGIN(st);
   launch_k(k_sample_rows, dim3((unsigned)((n + rows_per_cta - 1) / rows_per_cta)), dim3(SAMPLE_THREADS), 0, st, *sk, J, LJ, base,
@@ -733,6 +803,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
       fa.s = sample_args(nullptr, TC2_LG_LD, n, ld, inject, actions, logp, tiles_out,
                          knobs_out, move_bits, shift_bits, head0_col, status, grow,
                          m_total);
+      fa.s.pcg_tab = pcg_tab_for(rng, st);
       fa.tiles = tiles;
       fa.knobs = knobs;
       fa.feat_new = feat_out;
@@ -1329,7 +1400,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   if (rc2) return rc2;
   if (B > 0) {
     HARL_PROF_BEGIN(st);
-    launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM)), dim3(PPO_THREADS), rsmem, st, 
+    launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM), 2), dim3(PPO_THREADS), rsmem, st, 
         a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
     HARL_CHECK_LAUNCH("k_ppo_rows");
   }

@@ -194,6 +194,10 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   griddep_launch();
   dbg_ts(40);
   extern __shared__ double srows[];
+  // blockIdx.y: 0 = policy (forward, heads, surrogate/entropy terms,
+  // backward), 1 = value (forward, squared error, backward) -- the two nets
+  // share only X, so their chains run side by side in separate CTAs
+  const int role = blockIdx.y;
   const int r0 = blockIdx.x * PPO_TM;
   const int nrows = min(PPO_TM, a.B - r0);
   const int RS = a.row_stride;
@@ -208,23 +212,26 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   }
   __syncthreads();
   dbg_ts(41);
-  // policy trunk (every layer tanh: rlcore.py:95-103 + 139)
-  for (int l = 0; l < P.n_layers; ++l)
-    dense64(base + P.row_act[l], RS, P.dims[l], params + P.off_W[l],
-            params + P.off_b[l], P.dims[l + 1], base + P.row_act[l + 1], RS,
-            true, nrows, wbuf);
-  dbg_ts(42);
   const int H = P.dims[P.n_layers];
   const int NH = P.n_head_cols;
-  dense64(base + P.row_act[P.n_layers], RS, H, params + P.off_hW,
-          params + P.off_hb, NH, base + P.row_head, RS, false, nrows, wbuf);
-  dbg_ts(43);
-  // value net
-  for (int l = 0; l < V.n_layers; ++l)
-    dense64(base + V.row_act[l], RS, V.dims[l], params + V.off_W[l],
-            params + V.off_b[l], V.dims[l + 1], base + V.row_act[l + 1], RS,
-            l < V.n_layers - 1, nrows, wbuf);
-  dbg_ts(44);
+  if (role == 0) {
+    // policy trunk (every layer tanh: rlcore.py:95-103 + 139) and heads
+    for (int l = 0; l < P.n_layers; ++l)
+      dense64(base + P.row_act[l], RS, P.dims[l], params + P.off_W[l],
+              params + P.off_b[l], P.dims[l + 1], base + P.row_act[l + 1], RS,
+              true, nrows, wbuf);
+    dbg_ts(42);
+    dense64(base + P.row_act[P.n_layers], RS, H, params + P.off_hW,
+            params + P.off_hb, NH, base + P.row_head, RS, false, nrows, wbuf);
+    dbg_ts(43);
+  } else {
+    // value net (its last layer linear, rlcore.py:161-178)
+    for (int l = 0; l < V.n_layers; ++l)
+      dense64(base + V.row_act[l], RS, V.dims[l], params + V.off_W[l],
+              params + V.off_b[l], V.dims[l + 1], base + V.row_act[l + 1], RS,
+              l < V.n_layers - 1, nrows, wbuf);
+    dbg_ts(44);
+  }
   // per-row PPO terms: warp w takes (row w/4, head w%4); the exps of a
   // lane's columns are computed once and reused for the sum, the entropy
   // and the gradient.  Per-(row, head) results meet in shared memory.
@@ -232,7 +239,8 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   const double invB = 1.0 / (double)a.B_norm;
   __shared__ double s_lp[PPO_TM][4], s_ent[PPO_TM][4];
   const int rr = warp >> 2, h = warp & 3;
-  const bool active = rr < nrows && (PPO_THREADS / 32) >= 4 * PPO_TM;
+  const bool active = role == 0 && rr < nrows &&
+                      (PPO_THREADS / 32) >= 4 * PPO_TM;
   constexpr int HI = 4;      // cached columns per lane (C0 <= 128)
   double ev[HI];
   double hm = 0.0, hs = 1.0, hls = 0.0, hent = 0.0;
@@ -297,7 +305,6 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
     const double ent_total = ((s_ent[rr][0] + s_ent[rr][1]) + s_ent[rr][2]) + s_ent[rr][3];
     const double logp_old = ring.scalars[slot * 4 + 0];
     const double adv = ring.scalars[slot * 4 + 2];
-    const double td = ring.scalars[slot * 4 + 3];
     const double ratio = exp(logp_new - logp_old);
     const double clipped = fmin(fmax(ratio, a.clip_lo), a.clip_hi);
     const double s_un = ratio * adv, s_cl = clipped * adv;
@@ -323,34 +330,50 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
       }
     }
     if (h == 0 && lane == 0) {
-      const double v = base[rr * RS + V.row_act[V.n_layers]];
       double* o = rowout + (int64_t)(r0 + rr) * 4;
       o[0] = fmin(s_un, s_cl);
       o[1] = ent_total;
       o[2] = ratio;
-      o[3] = (v - td) * (v - td);
-      // dv = w * 2 (v - td) / B is the value net's output delta
-      base[rr * RS + V.row_delta[V.n_layers - 1]] = a.w_val * 2.0 * (v - td) * invB;
     }
+  }
+  if (role == 1 && threadIdx.x < nrows) {
+    const int q = threadIdx.x;
+    const int sl = idx[r0 + q];
+    const double td = ring.scalars[sl * 4 + 3];
+    const double v = base[q * RS + V.row_act[V.n_layers]];
+    rowout[(int64_t)(r0 + q) * 4 + 3] = (v - td) * (v - td);
+    // dv = w * 2 (v - td) / B is the value net's output delta
+    base[q * RS + V.row_delta[V.n_layers - 1]] = a.w_val * 2.0 * (v - td) * invB;
   }
   __syncthreads();
   dbg_ts(45);
-  // policy backward: dhid = dz . Wh^T, times (1 - hid^2)
-  back64(base + P.row_head, RS, NH, wt + a.wt_head, H,
-         base + P.row_act[P.n_layers], RS, base + P.row_delta[P.n_layers - 1],
-         RS, nrows, wbuf);
-  for (int l = P.n_layers - 1; l >= 1; --l)
-    back64(base + P.row_delta[l], RS, P.dims[l + 1], wt + a.wt_P[l],
-           P.dims[l], base + P.row_act[l], RS, base + P.row_delta[l - 1], RS,
-           nrows, wbuf);
-  dbg_ts(46);
-  for (int l = V.n_layers - 1; l >= 1; --l)
-    back64(base + V.row_delta[l], RS, V.dims[l + 1], wt + a.wt_V[l],
-           V.dims[l], base + V.row_act[l], RS, base + V.row_delta[l - 1], RS,
-           nrows, wbuf);
-  dbg_ts(47);
+  if (role == 0) {
+    // policy backward: dhid = dz . Wh^T, times (1 - hid^2)
+    back64(base + P.row_head, RS, NH, wt + a.wt_head, H,
+           base + P.row_act[P.n_layers], RS,
+           base + P.row_delta[P.n_layers - 1], RS, nrows, wbuf);
+    for (int l = P.n_layers - 1; l >= 1; --l)
+      back64(base + P.row_delta[l], RS, P.dims[l + 1], wt + a.wt_P[l],
+             P.dims[l], base + P.row_act[l], RS, base + P.row_delta[l - 1],
+             RS, nrows, wbuf);
+    dbg_ts(46);
+  } else {
+    for (int l = V.n_layers - 1; l >= 1; --l)
+      back64(base + V.row_delta[l], RS, V.dims[l + 1], wt + a.wt_V[l],
+             V.dims[l], base + V.row_act[l], RS, base + V.row_delta[l - 1],
+             RS, nrows, wbuf);
+    dbg_ts(47);
+  }
+  // each role writes its own segment of the rows: [X, policy acts, heads,
+  // policy deltas] | [value acts, value deltas] (DeviceAgent row layout)
+  const int seg0 = role == 0 ? 0 : V.row_act[1];
+  const int seg1 = role == 0 ? V.row_act[1] : RS;
+  const int sw = seg1 - seg0;
   double* out = rows + (int64_t)r0 * RS;
-  for (int i = threadIdx.x; i < nrows * RS; i += blockDim.x) out[i] = base[i];
+  for (int i = threadIdx.x; i < nrows * sw; i += blockDim.x) {
+    const int q = i / sw, c = seg0 + i % sw;
+    out[q * RS + c] = base[q * RS + c];
+  }
   dbg_ts(48);
 }
 

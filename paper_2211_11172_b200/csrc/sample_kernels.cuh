@@ -41,6 +41,7 @@ struct SampleArgs {
   unsigned long long* status;
   const int32_t* grow;   // optional: global row of each local row (shards)
   int64_t m_total;       // rows drawn this step over all shards
+  const PcgTab* pcg_tab; // optional byte-sliced jump table of the stream
 };
 
 __device__ inline float gmaxf(float v) {
@@ -126,13 +127,16 @@ __device__ __forceinline__ void sample_group(
   }
   const int ca0 = knobs[rr], par0 = knobs[a.ld + rr], ur0 = knobs[2 * a.ld + rr];
   const float* z = zrow ? zrow : a.logits + rr * a.ldz;
+  // lane g owns the contiguous head-0 columns [g*nI, g*nI + nI): local
+  // max / sum / prefix, then one 8-lane scan of the lane totals
   const int nI = (C0 + SG - 1) / SG;
-  float zc[SAMPLE_MAXI];   // head-0 logits j = g + 8i (padding reads as -inf)
+  const int jb = g * nI;
+  float zc[SAMPLE_MAXI];   // head-0 logits j = jb + i (padding reads as -inf)
   float z3[3] = {0.f, 0.f, 0.f};   // shift head g+1's three logits (lanes 0-2)
   if (!a.inject) {
 #pragma unroll
     for (int i = 0; i < SAMPLE_MAXI; ++i) {
-      const int j = g + SG * i;
+      const int j = jb + i;
       zc[i] = (i < nI && j < C0) ? z[j] : -INFINITY;
     }
     if (g < 3) {
@@ -144,7 +148,7 @@ __device__ __forceinline__ void sample_group(
   double u_mine = 0.0;
   if (draw) {
     const uint64_t k = (uint64_t)g * (uint64_t)a.m_total + (uint64_t)grow_r + 1;
-    u_mine = u64_to_unit(pcg_draw64(J, base, k));
+    u_mine = u64_to_unit(pcg_draw64t(a.pcg_tab, J, base, k));
   }
   dbg_ts(17);
   // ---- current state: lane g holds slots g, g+8, ... --------------------
@@ -189,51 +193,58 @@ __device__ __forceinline__ void sample_group(
     float zmax = -INFINITY;
 #pragma unroll
     for (int i = 0; i < SAMPLE_MAXI; ++i) {
-      const int j = g + SG * i;
+      const int j = jb + i;
       if (i < nI && j < C0 && legal0(j)) zmax = fmaxf(zmax, zc[i]);
     }
-    for (int i = SAMPLE_MAXI; i < nI; ++i) {
-      const int j = g + SG * i;
+    for (int i = SAMPLE_MAXI; i < nI; ++i) {   // wide heads (C0 > 128)
+      const int j = jb + i;
       if (j < C0 && legal0(j)) zmax = fmaxf(zmax, z[j]);
     }
     zmax = gmaxf(zmax);
     dead |= (zmax == -INFINITY);
     float e[SAMPLE_MAXI];
-    double s = 0.0;
+    double sl = 0.0;
 #pragma unroll
     for (int i = 0; i < SAMPLE_MAXI; ++i) {
-      const int j = g + SG * i;
+      const int j = jb + i;
       e[i] = (i < nI && j < C0 && legal0(j)) ? expf(zc[i] - zmax) : 0.f;
-      s += (double)e[i];
-    }
-    for (int i = SAMPLE_MAXI; i < nI; ++i) {   // wide heads (C0 > 128)
-      const int j = g + SG * i;
-      if (j < C0 && legal0(j)) s += (double)expf(z[j] - zmax);
-    }
-    s = gsum(s);
-    dbg_ts(19);
-    const double inv = 1.0 / s;
-    int count = 0;
-    double carry = 0.0;
-    auto cdf_step = [&](int j, float ei) {
-      double c = (double)ei * inv;
-#pragma unroll
-      for (int o = 1; o < SG; o <<= 1) {
-        const double t = __shfl_up_sync(0xffffffffu, c, o, SG);
-        if (g >= o) c += t;
-      }
-      c += carry;
-      if (j < C0 && c < u0) ++count;
-      carry = __shfl_sync(0xffffffffu, c, SG - 1, SG);
-    };
-#pragma unroll
-    for (int i = 0; i < SAMPLE_MAXI; ++i) {
-      if (i >= nI) break;   // uniform across the warp
-      cdf_step(g + SG * i, e[i]);
+      sl += (double)e[i];
     }
     for (int i = SAMPLE_MAXI; i < nI; ++i) {
-      const int j = g + SG * i;
-      cdf_step(j, (j < C0 && legal0(j)) ? expf(z[j] - zmax) : 0.f);
+      const int j = jb + i;
+      if (j < C0 && legal0(j)) sl += (double)expf(z[j] - zmax);
+    }
+    const double s = gsum(sl);
+    dbg_ts(19);
+    const double inv = 1.0 / s;
+    // lane-local inclusive prefix of p_j = e_j / s; the lane's offset is the
+    // exclusive scan of the lane totals (3 shuffle steps)
+    double tot = 0.0;
+#pragma unroll
+    for (int i = 0; i < SAMPLE_MAXI; ++i) tot += (double)e[i] * inv;
+    for (int i = SAMPLE_MAXI; i < nI; ++i) {
+      const int j = jb + i;
+      if (j < C0 && legal0(j)) tot += (double)expf(z[j] - zmax) * inv;
+    }
+    double incl = tot;
+#pragma unroll
+    for (int o = 1; o < SG; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, incl, o, SG);
+      if (g >= o) incl += t;
+    }
+    double c = incl - tot;   // exclusive offset
+    int count = 0;
+#pragma unroll
+    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+      c += (double)e[i] * inv;
+      if (i < nI && jb + i < C0 && c < u0) ++count;
+    }
+    for (int i = SAMPLE_MAXI; i < nI; ++i) {
+      const int j = jb + i;
+      if (j < C0) {
+        if (legal0(j)) c += (double)expf(z[j] - zmax) * inv;
+        if (c < u0) ++count;
+      }
     }
     count = gsumi(count);
     dbg_ts(20);

@@ -655,7 +655,13 @@ class EpisodeEngine:
         """Record each segment's launches once (pointer sequence fixed by
         the plan).  ``gen`` only supplies the stream increment (jump
         tables); states come from the device tables at replay."""
-        N.check(N.load().harl_prepare(), "harl_prepare")
+        from . import rng as R
+        lib = N.load()
+        N.check(lib.harl_prepare(), "harl_prepare")
+        # the sampler's byte-sliced jump table must exist before capture
+        N.check(lib.harl_rng_prepare(C.byref(R.to_struct(gen))),
+                "harl_rng_prepare")
+        b.graph_inc = int(gen.bit_generator.state["state"]["inc"])
         if self.dagent.tc:
             self.dagent.hid_scratch(b.P)
         self._ensure_ppo_scratch(max([s["ppo"] or 0 for s in b.plan] + [1]))
@@ -696,6 +702,9 @@ class EpisodeEngine:
     def _run_graphed(self, b, gen, cfg, order_counter):
         from . import rng as R
         P = cfg.tracks
+        inc = int(gen.bit_generator.state["state"]["inc"])
+        if b.graphs is not None and getattr(b, "graph_inc", None) != inc:
+            b.graphs = None     # jump tables of another stream are baked in
         if b.graphs is None:
             self._capture(b, gen)
             PF.add_launches(-sum(g[3] for g in b.graphs))  # not executed

@@ -455,6 +455,7 @@ KERNEL_SPAN = {
     "k_gbt_predict": ("gbt", "hbm"),
     "k_gbt_predict2": ("gbt", "hbm"),
     "k_finish_step": ("finish", "hbm"),
+    "k_gbt_finish": ("gbt", "hbm"),
     "k_ring_rows": ("finish", "hbm"),
     "k_ppo_rows": ("ppo", "fp64"),
 }
@@ -484,6 +485,8 @@ def per_row_work(tables, H):
         "k_gbt_predict2": 8 * F + 8,
         # reward/score/v/adv/log entry (state + score + track) + ring scalars
         "k_finish_step": 8 * 6 + state + 8 + 4 + 8 * 4 + 16 + 4,
+        # GBT (features in, score + reward out) + the finish row work
+        "k_gbt_finish": 8 * F + 8 + 8 * 6 + state + 8 + 4 + 8 * 4 + 16 + 4,
         "k_ring_rows": 2 * 8 * F * 2,               # X and X' read + written
         # policy + value forward and backward in fp64 (3x forward flops)
         "k_ppo_rows": 3 * 2 * (2 * (F * H + H * H) + H * NH + H),

@@ -322,6 +322,20 @@ int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
 
 /* Survivor compaction after a host cull (stopping.py:68-86): row i of the
  * destination population <- row idx[i] of the source. */
+/* harl_gbt_predict + harl_finish_step as one persistent kernel: the GBT
+ * scores of X' = io->feat_new are written to io->new_score, the rewards
+ * against old_score to io->reward, then each tile's rows get the finish
+ * bookkeeping (advantage needs io->v_cur / io->v_next: run the value pass
+ * first).  HARL_E_LIMIT when the forest does not fit in shared memory (use
+ * the two calls then). */
+int harl_gbt_finish_step(const harl_forest_desc* forest, int32_t feature_len,
+                         const double* old_score, const harl_step_buffers* io,
+                         int64_t n, int64_t ld, int64_t vbase,
+                         int32_t local_slots, double discount, int32_t rl,
+                         const harl_replay_ring* ring, int64_t wpos,
+                         int64_t keep_from, const harl_entry_log* log,
+                         const harl_track_stats* ts, const int64_t* wpos_dev,
+                         void* stream);
 int harl_gather_rows(const int32_t* idx, int64_t n_out, int32_t local_slots,
                      int32_t feature_len, const uint16_t* tiles,
                      const uint8_t* knobs, const double* feat,

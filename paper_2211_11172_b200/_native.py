@@ -22,6 +22,8 @@ MAX_STAGES, MAX_TENSORS, MAX_TERMS = 16, 48, 160
 MAX_HEAD0, MAX_LAYERS, MAX_HIDDEN, MAX_FEATURES = 512, 4, 256, 128
 
 ST_OK, ST_TILING, ST_COMPUTE_AT, ST_PARALLEL, ST_UNROLL = 0, 1, 2, 3, 4
+# return codes (harl_b200.h)
+E_ARG, E_CUDA, E_LIMIT = -1, -2, -3
 ST_NO_VALID, ST_NONFINITE = 5, 6
 
 i16, i32, i64, u32, u64, f64 = (C.c_int16, C.c_int32, C.c_int64, C.c_uint32,
@@ -139,6 +141,10 @@ _SIGS = {
     "harl_finish_step": (i32, [P(StepBuffers), i64, i64, i64, i32, i32, f64,
                                i32, P(ReplayRing), i64, i64, P(EntryLog),
                                P(TrackStats), vp, vp]),
+    "harl_gbt_finish_step": (i32, [P(ForestDesc), i32, vp, P(StepBuffers), i64,
+                                   i64, i64, i32, f64, i32, P(ReplayRing),
+                                   i64, i64, P(EntryLog), P(TrackStats), vp,
+                                   vp]),
     "harl_gather_rows": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp,
                                vp, vp, vp, vp, i64, vp]),
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),

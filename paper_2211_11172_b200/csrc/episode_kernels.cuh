@@ -160,6 +160,63 @@ k_finish_step(FinishArgs a, const __grid_constant__ harl_step_buffers io,
   }
 }
 
+// GBT predict + reward + the finish bookkeeping in one persistent kernel
+// (the value pass runs first, so v_cur/v_next are ready): after a tile's
+// scores are written, group 1's 64 threads run finish_row for its rows and
+// groups 2-7 copy the pushed rows' X / X' into their replay slots.
+struct GbtFinishArgs {
+  FinishArgs a;
+  harl_step_buffers io;
+  harl_replay_ring ring;
+  harl_entry_log log;
+  harl_track_stats ts;
+  const int64_t* wpos_dev;
+};
+
+struct GbtFinishEpilogue {
+  const GbtFinishArgs& f;
+  int64_t wpos;
+  __device__ void operator()(int64_t r0, int rows, int g, int rl) const {
+    if (g == 1) {
+      if (rl < rows) finish_row(f.a, f.io, f.ring, f.log, f.ts, wpos, r0 + rl);
+      return;
+    }
+    if (g < 2 || !f.a.rl) return;
+    const int64_t lo = r0 > f.a.keep_from ? r0 : f.a.keep_from;
+    const int64_t hi = r0 + rows;
+    if (lo >= hi) return;
+    const int F = f.a.F;
+    const int total = (int)(hi - lo) * F;
+    const double* sx = f.io.feat + lo * F;
+    const double* sxn = f.io.feat_new + lo * F;
+    const int nthr = (GBT2_GROUPS - 2) * GBT2_ROWS;
+    const int tid = threadIdx.x - 2 * GBT2_ROWS;
+    for (int e = tid; e < total; e += nthr) {
+      const int rr = e / F, k = e - rr * F;
+      const int64_t slot = (wpos + lo + rr) % f.ring.cap;
+      f.ring.X[slot * F + k] = sx[e];
+      f.ring.Xn[slot * F + k] = sxn[e];
+    }
+  }
+};
+
+template <bool SMEM_NODES>
+__global__ void __launch_bounds__(GBT2_THREADS)
+k_gbt_finish(const GbtNode* __restrict__ gnodes,
+             const int32_t* __restrict__ tree_first, int32_t n_trees,
+             int64_t n_nodes, int32_t fitted, double base, double floor_value,
+             const double* __restrict__ feat, int64_t n, int32_t F,
+             double* score, const double* old_score, double* reward,
+             const GbtHdr* hdr, int32_t t_cap,
+             const __grid_constant__ GbtFinishArgs fa) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  const GbtFinishEpilogue epi{fa, fa.wpos_dev ? *fa.wpos_dev : fa.a.wpos};
+  gbt2_body<SMEM_NODES>(gnodes, tree_first, n_trees, n_nodes, fitted, base,
+                        floor_value, feat, n, F, score, old_score, reward, hdr,
+                        t_cap, epi);
+}
+
 // replay feature rows (X, X') of the surviving pushes: one warp per row,
 // lanes over features (coalesced), 32-bit index math
 __global__ void __launch_bounds__(256)

@@ -101,16 +101,19 @@ __host__ __device__ inline size_t gbt2_smem_bytes(bool smem_nodes, int64_t n_nod
          (size_t)GBT2_ROWS * T * 8;
 }
 
-template <bool SMEM_NODES>
-__global__ void __launch_bounds__(GBT2_THREADS)
-k_gbt_predict2(const GbtNode* __restrict__ gnodes,
-               const int32_t* __restrict__ tree_first, int32_t n_trees,
-               int64_t n_nodes, int32_t fitted, double base,
-               double floor_value, const double* __restrict__ feat, int64_t n,
-               int32_t F, double* score, const double* old_score,
-               double* reward, const GbtHdr* hdr, int32_t t_cap) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
+struct GbtNoEpilogue {
+  __device__ void operator()(int64_t, int, int, int) const {}
+};
+
+// epi(r0, rows, group, local row) runs after each tile's scores and rewards
+// are in global memory (visible to the whole CTA)
+template <bool SMEM_NODES, typename Epi>
+__device__ __forceinline__ void gbt2_body(
+    const GbtNode* __restrict__ gnodes, const int32_t* __restrict__ tree_first,
+    int32_t n_trees, int64_t n_nodes, int32_t fitted, double base,
+    double floor_value, const double* __restrict__ feat, int64_t n, int32_t F,
+    double* score, const double* old_score, double* reward, const GbtHdr* hdr,
+    int32_t t_cap, const Epi& epi) {
   dbg_ts(24);
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint64_t fbar, xbar[2];
@@ -200,7 +203,23 @@ k_gbt_predict2(const GbtNode* __restrict__ gnodes,
     }
     __syncthreads();
     if (it < 2) dbg_ts(27 + 3 * it);
+    epi(r0, rows, g, rl);
   }
+}
+
+template <bool SMEM_NODES>
+__global__ void __launch_bounds__(GBT2_THREADS)
+k_gbt_predict2(const GbtNode* __restrict__ gnodes,
+               const int32_t* __restrict__ tree_first, int32_t n_trees,
+               int64_t n_nodes, int32_t fitted, double base,
+               double floor_value, const double* __restrict__ feat, int64_t n,
+               int32_t F, double* score, const double* old_score,
+               double* reward, const GbtHdr* hdr, int32_t t_cap) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  gbt2_body<SMEM_NODES>(gnodes, tree_first, n_trees, n_nodes, fitted, base,
+                        floor_value, feat, n, F, score, old_score, reward, hdr,
+                        t_cap, GbtNoEpilogue());
 }
 
 }  // namespace harl

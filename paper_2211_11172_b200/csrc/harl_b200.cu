@@ -1088,6 +1088,72 @@ int harl_value_forward(const harl_mlp_desc* val, const double* feat, int64_t n,
   return HARL_OK;
 }
 
+int harl_gbt_finish_step(const harl_forest_desc* forest, int32_t feature_len,
+                         const double* old_score, const harl_step_buffers* io, int64_t n, int64_t ld,
+                         int64_t vbase, int32_t local_slots, double discount,
+                         int32_t rl, const harl_replay_ring* ring, int64_t wpos,
+                         int64_t keep_from, const harl_entry_log* log,
+                         const harl_track_stats* ts, const int64_t* wpos_dev,
+                         void* stream) {
+  if (!forest || forest->n_trees < 0 || forest->n_trees > 1024 ||
+      (forest->n_trees > 0 && (!forest->nodes || !forest->tree_first)) || !io ||
+      !log || !ts || (rl && (!ring || ring->cap < 1))) {
+    set_error("harl_gbt_finish_step: bad arguments");
+    return HARL_E_ARG;
+  }
+  if (n <= 0) return HARL_OK;
+  const int T = forest->n_trees > 0 ? forest->n_trees : 1;
+  const int F = feature_len;
+  const size_t cap = (size_t)max_dyn_smem();
+  const bool smem_nodes = gbt2_smem_bytes(true, forest->n_nodes, T, F) <= cap;
+  const size_t smem = gbt2_smem_bytes(smem_nodes, forest->n_nodes, T, F);
+  if (smem > cap) {   // forest too large for the persistent kernel
+    set_error("harl_gbt_finish_step: forest too large; use harl_gbt_predict + "
+              "harl_finish_step");
+    return HARL_E_LIMIT;
+  }
+  double* score = const_cast<double*>(io->new_score);
+  double* reward = const_cast<double*>(io->reward);
+  GbtFinishArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.a.n = n;
+  fa.a.ld = ld;
+  fa.a.vbase = vbase;
+  fa.a.local_slots = local_slots;
+  fa.a.F = F;
+  fa.a.discount = discount;
+  fa.a.rl = rl;
+  fa.a.wpos = wpos;
+  fa.a.keep_from = keep_from;
+  fa.io = *io;
+  if (ring) fa.ring = *ring;
+  if (fa.ring.cap < 1) fa.ring.cap = 1;
+  fa.log = *log;
+  fa.ts = *ts;
+  fa.wpos_dev = wpos_dev;
+  const int64_t tiles = (n + GBT2_ROWS - 1) / GBT2_ROWS;
+  const int64_t grid = tiles < sm_count() ? tiles : sm_count();
+  int rc = smem_nodes ? allow_smem(k_gbt_finish<true>, smem, "k_gbt_finish")
+                      : allow_smem(k_gbt_finish<false>, smem, "k_gbt_finish");
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  HARL_PROF_BEGIN(st);
+  if (smem_nodes)
+    launch_k(k_gbt_finish<true>, dim3((unsigned)grid), dim3(GBT2_THREADS), smem, st,
+             (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
+             forest->n_nodes, forest->fitted, forest->base, forest->floor_value,
+             io->feat_new, n, F, score, old_score, reward,
+             (const GbtHdr*)forest->dev_hdr, T, fa);
+  else
+    launch_k(k_gbt_finish<false>, dim3((unsigned)grid), dim3(GBT2_THREADS), smem, st,
+             (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
+             forest->n_nodes, forest->fitted, forest->base, forest->floor_value,
+             io->feat_new, n, F, score, old_score, reward,
+             (const GbtHdr*)forest->dev_hdr, T, fa);
+  HARL_CHECK_LAUNCH("k_gbt_finish");
+  return HARL_OK;
+}
+
 int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
                      int64_t vbase, int32_t local_slots, int32_t feature_len,
                      double discount, int32_t rl, const harl_replay_ring* ring,

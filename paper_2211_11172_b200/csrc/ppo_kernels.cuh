@@ -464,6 +464,7 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
             int means_B, double w_ent, double w_val) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
+  dbg_ts(54);
   if (blockIdx.x == gridDim.x - 1) {   // the extra CTA: loss sums/means
     if (threadIdx.x < 32) ppo_losses_warp(B, rowout, losses, means_B, w_ent, w_val, bad);
     return;
@@ -486,7 +487,14 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
   const int i0 = (tile / tiles_j) * WG_T, j0 = (tile % tiles_j) * WG_T;
   const int tj = threadIdx.x % WG_T, ti = threadIdx.x / WG_T;
   const bool ones = jb.ni == 0;
-  double acc = 0.0;
+  // fp64 tensor cores: warp w sums rows [16w, 16w + 16) of each 128-row
+  // slab into a 16x16 partial with mma.m8n8k4.f64 (M = i, N = j, K = rows);
+  // the 8 warps' partials are added in warp order at the end
+  // (deterministic).  A fragment (m = i, k = r) = A[r][i], B fragment
+  // (k = r, n = j) = D[r][j].
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  double pacc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
   for (int rb = 0; rb < B; rb += WG_RB) {
     const int nr = min(WG_RB, B - rb);
     // element e of the 128x16 slab: row e/16, column e%16
@@ -498,7 +506,8 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
       const int rr = e / WG_T, cc = e % WG_T;
       const int64_t rowoff = (int64_t)(rb + rr) * RS;
       vd[u] = (rr < nr && j0 + cc < jb.nj) ? rows[rowoff + jb.d_off + j0 + cc] : 0.0;
-      va[u] = (!ones && rr < nr && i0 + cc < ni) ? rows[rowoff + jb.a_off + i0 + cc] : 0.0;
+      va[u] = ones ? (rr < nr ? 1.0 : 0.0)
+                   : ((rr < nr && i0 + cc < ni) ? rows[rowoff + jb.a_off + i0 + cc] : 0.0);
     }
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -507,13 +516,45 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
       sa[e / WG_T][e % WG_T] = va[u];
     }
     __syncthreads();
-    if (ones) {
-      for (int rr = 0; rr < nr; ++rr) acc = fma(1.0, sd[rr][tj], acc);
-    } else {
-      for (int rr = 0; rr < nr; ++rr) acc = fma(sa[rr][ti], sd[rr][tj], acc);
+    if (rb == 0) dbg_ts(55);
+    // rows past nr were staged as zeros
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int r = warp * 16 + ks * 4 + tig;
+      double af[2], bf[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        af[t] = sa[r][8 * t + gid];
+        bf[t] = sd[r][8 * t + gid];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+              "{%0, %1}, {%2}, {%3}, {%0, %1};"
+              : "+d"(pacc[mt][nt][0]), "+d"(pacc[mt][nt][1])
+              : "d"(af[mt]), "d"(bf[nt]));
     }
     __syncthreads();
   }
+  dbg_ts(56);
+  // partials -> shared (reusing sa: 8 warps x 256 doubles = 16 KB), then
+  // one output per thread summed over warps in order
+  double* part = &sa[0][0];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        part[warp * 256 + (8 * mt + gid) * 16 + 8 * nt + 2 * tig + q] =
+            pacc[mt][nt][q];
+  __syncthreads();
+  double acc1 = 0.0;
+  for (int w = 0; w < 8; ++w) acc1 += part[w * 256 + ti * 16 + tj];
+  const double acc = acc1;
   const int i = i0 + ti, j = j0 + tj;
   if (i < ni && j < jb.nj) {
     grads[jb.g_off + (int64_t)i * jb.nj + j] = acc;
@@ -576,26 +617,31 @@ __global__ void k_wt_fill(TransPlan tp, const double* params, double* wt) {
   }
 }
 
-__global__ void k_ppo_adam(AdamArgs a, const double* adam_dev, const int32_t* bad,
+__global__ void k_ppo_adam(const __grid_constant__ AdamArgs a,
+                           const double* adam_dev, const int32_t* bad,
                            const double* grads, double* params, double* m,
                            double* v, float* params32) {
+  // __grid_constant__: the pack/transposition plans are indexed with
+  // runtime loop counters; a by-value param would be copied to local memory
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   dbg_ts(50);
   if (*bad) return;
   dbg_ts(51);
+  double b1t_pi = a.h.b1t_pi, b2t_pi = a.h.b2t_pi, b1t_v = a.h.b1t_v,
+         b2t_v = a.h.b2t_v;
   if (adam_dev) {  // graph replay: this update's 1 - beta^t from device memory
-    a.h.b1t_pi = adam_dev[0];
-    a.h.b2t_pi = adam_dev[1];
-    a.h.b1t_v = adam_dev[2];
-    a.h.b2t_v = adam_dev[3];
+    b1t_pi = adam_dev[0];
+    b2t_pi = adam_dev[1];
+    b1t_v = adam_dev[2];
+    b2t_v = adam_dev[3];
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const bool pi = i < a.n_pi;
     const double lr = pi ? a.h.lr_actor : a.h.lr_critic;
-    const double b1t = pi ? a.h.b1t_pi : a.h.b1t_v;
-    const double b2t = pi ? a.h.b2t_pi : a.h.b2t_v;
+    const double b1t = pi ? b1t_pi : b1t_v;
+    const double b2t = pi ? b2t_pi : b2t_v;
     const double g = grads[i];
     double mi = __dmul_rn(m[i], a.h.beta1);
     mi = __dadd_rn(mi, __dmul_rn(a.h.one_m_beta1, g));

@@ -46,6 +46,10 @@ from .space import SketchTables
 # featurize 11.4 us at ~28 warps/SM), so the split launches are the default.
 _FUSED_STEP = os.environ.get("HARL_FUSED_STEP") == "1"
 
+# HARL_SPLIT_FINISH=1: separate GBT and finish launches (k_gbt_predict2 +
+# k_finish_step) instead of the fused k_gbt_finish (A/B and fallback path)
+_SPLIT_FINISH = os.environ.get("HARL_SPLIT_FINISH") == "1"
+
 
 @dataclass(frozen=True)
 class EpisodeConfig:
@@ -308,8 +312,8 @@ class EpisodeEngine:
                             feat_out=nxt["feat"] if _FUSED_STEP else None)
         if not _FUSED_STEP:
             D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
-        D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
-                      out=nxt["score"], reward=b.reward)
+        # value pass first: the fused GBT kernel's finish epilogue needs
+        # V(X) and V(X') (the GBT and value passes both read only X')
         v_cur, v_next = b.vbuf[(k + 1) % 2], b.vbuf[k % 2]
         reuse = self._v_reusable(b.plan, k)
         D.value_pair(self.dagent, cur["feat"], 0 if reuse else m, nxt["feat"],
@@ -325,13 +329,26 @@ class EpisodeEngine:
             b.adv.data_ptr())
         cap = self.replay.cap
         keep_from = max(0, m - cap) if keep_from is None else keep_from
+        wdev = D._ptr(b.wpos_tab[k:k + 1]) if graph_mode else None
+        if not _SPLIT_FINISH:
+            with PF.span("gbt", m, launches=1):
+                rc = lib.harl_gbt_finish_step(
+                    C.byref(b.forest.desc), tables.feature_len,
+                    cur["score"].data_ptr(), io, m, P, used,
+                    tables.local_slots, self.rl_cfg.discount, 1,
+                    self.replay.desc, self.replay.wpos, keep_from, b.elog,
+                    b.ts, wdev, D._stream())
+            if rc == 0:
+                return res
+            if rc != N.E_LIMIT:
+                N.check(rc, "harl_gbt_finish_step")
+        D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
+                      out=nxt["score"], reward=b.reward)
         with PF.span("finish", m, launches=1):
             N.check(lib.harl_finish_step(
                 io, m, P, used, tables.local_slots, tables.feature_len,
                 self.rl_cfg.discount, 1, self.replay.desc, self.replay.wpos,
-                keep_from, b.elog, b.ts,
-                D._ptr(b.wpos_tab[k:k + 1]) if graph_mode else None,
-                D._stream()), "harl_finish_step")
+                keep_from, b.elog, b.ts, wdev, D._stream()), "harl_finish_step")
         return res
 
     def _launch_step_uniform(self, b, k, step, cur, nxt, rt, used, gen,

@@ -22,6 +22,7 @@ SNAMES = ["start", "rng", "state", "softmax", "cdf", "shift_heads", "decided", "
 GNAMES = ["start", "x0", "walk0", "sum0", "x1", "walk1", "sum1"]
 FNAMES = ["start", "staged", "rows", "end"]
 ANAMES = ["start", "bad_checked", "updated", "end"]
+WNAMES = ["start", "staged0", "summed"]
 PNAMES = ["start", "gather", "pol_fwd", "heads", "val_fwd", "terms", "pol_bwd", "val_bwd", "end"]
 
 
@@ -46,7 +47,8 @@ def main():
         N.check(lib.harl_debug_timestamps(0, ts.ctypes.data_as(C.c_void_p), 64), "dbg")
         for nm, lo, names in (("policy", 0, NAMES), ("sample", 16, SNAMES),
                               ("gbt", 24, GNAMES), ("featurize", 32, FNAMES),
-                              ("ppo_rows", 40, PNAMES), ("adam", 50, ANAMES)):
+                              ("ppo_rows", 40, PNAMES), ("adam", 50, ANAMES),
+                              ("wgrad", 54, WNAMES)):
             t = ts[lo:lo + len(names)].astype(np.int64)
             rel = (t - t[0]) / 1e3
             print(f"rep {rep} {nm}: " + " ".join(f"{n}={r:.2f}" for n, r in zip(names, rel)))

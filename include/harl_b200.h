@@ -233,7 +233,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
                         const int32_t* grow, int64_t m_total, double* feat_out,
-                        void* stream);
+                        int32_t fuse_tc, void* stream);
 
 /* V(X) and V(X') in one launch (tuner.py:395-396) on the tcgen05 path
  * (hidden (128,128), feature_len <= 64); HARL_E_ARG if not eligible. */

@@ -132,7 +132,7 @@ _SIGS = {
     "harl_policy_step_tc": (i32, [P(SketchDesc), P(MlpDesc), vp, vp, vp, i64,
                                   i64, P(Pcg64), vp, vp, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, vp, vp, vp, i64, vp,
-                                  vp]),
+                                  i32, vp]),
     "harl_value_pair_tc": (i32, [P(MlpDesc), vp, i64, vp, i64, i32, vp, vp,
                                  vp, vp]),
     "harl_tc_packed_bytes": (i64, [i32, i32]),

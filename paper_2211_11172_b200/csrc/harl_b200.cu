@@ -703,7 +703,7 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
                           uint16_t* tiles_out, uint8_t* knobs_out,
                           uint64_t* move_bits, uint32_t* shift_bits,
                           int32_t* head0_col, uint64_t* status,
-                          cudaStream_t st) {
+                          cudaStream_t st, double* feat_out = nullptr) {
   PcgJump J;
   LaneJump LJ;
   u128 base;
@@ -733,13 +733,28 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   a.m_total = m_total > 0 ? m_total : n;
   a.pcg_tab = pcg_tab_for(rng, st);
   const int rows_per_cta = SAMPLE_THREADS / SG;
+  const dim3 grid((unsigned)((n + rows_per_cta - 1) / rows_per_cta));
   HARL_PROF_BEGIN(st);
-  launch_k(k_sample_rows, dim3((unsigned)((n + rows_per_cta - 1) / rows_per_cta)), dim3(SAMPLE_THREADS), 0, st, *sk, J, LJ, base,
-                                           (const u128*)rng_state_dev, tiles,
-                                           knobs, a);
+  if (feat_out) {   // also featurize the successor states (schedspace.py:415)
+    const size_t smem = (size_t)rows_per_cta * sk->feature_len * 8;
+    int rc = allow_smem(k_sample_rows<true>, smem, "k_sample_rows");
+    if (rc) return rc;
+    launch_k(k_sample_rows<true>, grid, dim3(SAMPLE_THREADS), smem, st, *sk, J, LJ,
+             base, (const u128*)rng_state_dev, tiles, knobs, a, feat_out);
+  } else {
+    launch_k(k_sample_rows<false>, grid, dim3(SAMPLE_THREADS), 0, st, *sk, J, LJ,
+             base, (const u128*)rng_state_dev, tiles, knobs, a, (double*)nullptr);
+  }
   HARL_CHECK_LAUNCH("k_sample_rows");
   return HARL_OK;
 }
+
+// featurize inside the sampler up to this many rows per launch (measured:
+// -6 us per step at 16 K rows, +100 us at 1 M rows)
+#ifndef HARL_SAMPLE_FEAT_MAX_ROWS
+#define HARL_SAMPLE_FEAT_MAX_ROWS 32768
+#endif
+static const int64_t SAMPLE_FEAT_MAX_ROWS = HARL_SAMPLE_FEAT_MAX_ROWS;
 
 static bool tc_trunk_ok(const harl_mlp_desc* m, int F) {
   return m && m->n_layers >= 2 && m->dims[0] == F && F <= TC_K1 &&
@@ -757,7 +772,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
                         const int32_t* grow, int64_t m_total, double* feat_out,
-                        void* stream) {
+                        int32_t fuse_tc, void* stream) {
   int rc = check_sketch(sk);
   if (rc) return rc;
   if ((rc = check_mlp(pol, true))) return rc;
@@ -775,7 +790,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   cudaStream_t st = (cudaStream_t)stream;
   const int NHP = (pol->n_head_cols + 15) / 16 * 16;
   // fused step: policy -> sample/apply -> featurize in one kernel
-  if (feat_out && packed_trunk && packed_heads && use_tc2() &&
+  if (feat_out && fuse_tc && packed_trunk && packed_heads && use_tc2() &&
       ((uintptr_t)feat & 15) == 0) {
     int regA = tc2_regA(NHP);
     const int need = tc2_fused_regA_need(sk->feature_len, sk->local_slots, sk->max_extent);
@@ -835,11 +850,15 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     HARL_PROF_BEGIN(st);
     launch_k(k_policy_tc, dim3(grid), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
     HARL_CHECK_LAUNCH("k_policy_tc");
+    // small populations (latency-bound steps): the sampler featurizes the
+    // successor states itself, one launch less; large ones (throughput-
+    // bound): the 4-threads-per-row featurizer keeps every lane busy
+    const bool in_sampler = feat_out && n <= SAMPLE_FEAT_MAX_ROWS;
     rc = launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
-                          TC_H, n, ld, tiles, knobs, inject, actions, logp,
-                          tiles_out, knobs_out, move_bits, shift_bits,
-                          head0_col, status, st);
-    if (rc || !feat_out) return rc;
+                        TC_H, n, ld, tiles, knobs, inject, actions, logp,
+                        tiles_out, knobs_out, move_bits, shift_bits, head0_col,
+                        status, st, in_sampler ? feat_out : nullptr);
+    if (rc || !feat_out || in_sampler) return rc;
     return harl_featurize(sk, tiles_out, knobs_out, n, ld, feat_out, stream);
   }
   if ((rc = allow_smem(k_trunk_tc<TRUNK_POLICY>, TRUNK_SMEM, "k_trunk_tc")))
@@ -987,7 +1006,10 @@ int harl_prepare(void) {
   carve(k_gbt_predict2<false>);
   carve(k_policy_step);
   carve(k_value_forward);
-  carve(k_sample_rows);
+  carve(k_sample_rows<false>);
+  carve(k_sample_rows<true>);
+  carve(k_gbt_finish<true>);
+  carve(k_gbt_finish<false>);
   carve(k_trunk_tc<TRUNK_POLICY>);
   carve(k_trunk_tc<TRUNK_VALUE>);
   carve(k_heads_tc);

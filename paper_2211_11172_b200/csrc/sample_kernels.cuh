@@ -105,7 +105,8 @@ __device__ __forceinline__ void sample_group(
     const harl_sketch_desc& sk, const PcgJump& J, u128 base_arg,
     const u128* base_dev, const uint16_t* __restrict__ tiles,
     const uint8_t* __restrict__ knobs, const SampleArgs& a, int64_t r,
-    const float* zrow, const int16_t* s_src, const int16_t* s_dst) {
+    const float* zrow, const int16_t* s_src, const int16_t* s_dst,
+    uint16_t* st_tiles = nullptr, uint8_t* st_knobs = nullptr) {
   const int g = threadIdx.x & (SG - 1);
   // every group stays in the shuffles; out-of-range rows compute on row 0
   const bool live = r < a.n;
@@ -325,7 +326,14 @@ __device__ __forceinline__ void sample_group(
       if (moved && s == src) v = f_src / p;
       if (moved && s == dst) v = f_dst * p;
       a.tiles_out[(int64_t)s * a.ld + r] = (uint16_t)v;
+      if (st_tiles) st_tiles[s] = (uint16_t)v;
     }
+  }
+  if (st_knobs && g == 0) {   // the successor's knobs (old ones on failure)
+    const bool ok = code == HARL_ST_OK;
+    st_knobs[0] = (uint8_t)(ok ? ca : ca0);
+    st_knobs[1] = (uint8_t)(ok ? par : par0);
+    st_knobs[2] = (uint8_t)(ok ? ur : ur0);
   }
   if (g == 0) {
     if (code == HARL_ST_OK) {
@@ -342,26 +350,78 @@ __device__ __forceinline__ void sample_group(
   }
 }
 
+// featurize one successor state (schedspace.py:415-438) with the row's 8
+// lanes: tile logs spread over the lanes, the two footprint levels (and
+// their glibc log10s) on lanes 1 and 2, the knob/flop features on lane 0;
+// the row is built in shared memory (dst, F doubles) from the successor
+// state the sampler left in st / kn
+__device__ __forceinline__ void featurize_group(const harl_sketch_desc& sk,
+                                                int g, unsigned gmask,
+                                                const uint16_t* st,
+                                                const uint8_t* kn, double* dst) {
+  const int F = sk.feature_len, L = sk.levels;
+  for (int k = g; k < F; k += SG) dst[k] = 0.0;
+  __syncwarp(gmask);
+  for (int s2 = g; s2 < sk.local_slots; s2 += SG) dst[s2] = __ldg(sk.log2_lut + st[s2]);
+  const int ca = kn[0], par = kn[1], ur = kn[2];
+  const int pos = sk.max_feature_dims * L;
+  if (g == 0) {
+    dst[pos] = sk.ncas > 1 ? __ddiv_rn((double)ca, (double)(sk.ncas - 1)) : 0.0;
+    dst[pos + 1] = sk.max_fusible ? __ddiv_rn((double)par, (double)sk.max_fusible) : 0.0;
+    dst[pos + 2 + ur] = 1.0;
+    dst[pos + 2 + sk.n_unroll + 2] = sk.flops_feature;
+  } else if (g == 1 || g == 2) {
+    int64_t t[HARL_MAX_DIMS];
+    for (int d = 0; d < sk.ndims; ++d) {
+      const int vl = st[d * L + L - 1];
+      t[d] = (g == 2 && L >= 2) ? (int64_t)st[d * L + L - 2] * vl : vl;
+    }
+    const int64_t l = footprint_level(sk, t, g == 1, ca == 0);
+    dst[pos + 2 + sk.n_unroll + g - 1] =
+        __ddiv_rn(glibc_log10_ge1(__dadd_rn(1.0, (double)l)), 6.0);
+  }
+}
+
+template <bool FEAT>
 __global__ void __launch_bounds__(SAMPLE_THREADS, 8)
 k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ PcgJump J,
               const __grid_constant__ LaneJump LJ, u128 base_arg,
               const u128* base_dev, const uint16_t* __restrict__ tiles,
-              const uint8_t* __restrict__ knobs, SampleArgs a) {
+              const uint8_t* __restrict__ knobs, SampleArgs a,
+              double* __restrict__ feat_out) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   dbg_ts(16);
   dbg_grid(false, 60);
+  constexpr int ROWS = SAMPLE_THREADS / SG;
   __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
+  __shared__ uint16_t s_st[FEAT ? ROWS : 1][HARL_MAX_SLOTS];
+  __shared__ uint8_t s_kn[FEAT ? ROWS : 1][4];
+  extern __shared__ double s_feat[];   // FEAT: [ROWS][F]
   (void)LJ;
   for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
     s_src[i] = sk.head0_src[i];
     s_dst[i] = sk.head0_dst[i];
   }
   __syncthreads();
-  const int64_t r = (int64_t)blockIdx.x * (SAMPLE_THREADS / SG) + threadIdx.x / SG;
-  sample_group(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src, s_dst);
+  const int lr = threadIdx.x / SG;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+  const int64_t r = r0 + lr;
+  sample_group(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src,
+               s_dst, FEAT ? s_st[lr] : nullptr, FEAT ? s_kn[lr] : nullptr);
   dbg_ts(23);
+  if (FEAT) {
+    const int g = threadIdx.x & (SG - 1);
+    const unsigned gmask = 0xffu << (threadIdx.x & 24);
+    __syncwarp(gmask);
+    const int F = sk.feature_len;
+    if (r < a.n) featurize_group(sk, g, gmask, s_st[lr], s_kn[lr], s_feat + lr * F);
+    __syncthreads();
+    const int64_t rows = a.n - r0 < ROWS ? a.n - r0 : ROWS;
+    double* out = feat_out + r0 * F;
+    for (int i = threadIdx.x; i < rows * F; i += blockDim.x) out[i] = s_feat[i];
+  }
   dbg_grid(true, 60);
 }
 

@@ -748,11 +748,12 @@ class DeviceAgent:
 def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 n: int, gen=None, inject=None, out=None, want_logits=False,
                 rng_dev=None, advance=True, grow=None, m_total: int = 0,
-                feat_out=None):
+                feat_out=None, fuse_tc: bool = False):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
-    ``feat_out`` (optional f64 [n][F]): also featurize the new states (one
-    fused kernel on the tcgen05 path).  Returns a dict of device tensors;
+    ``feat_out`` (optional f64 [n][F]): also featurize the new states (in
+    the sampler kernel on the tcgen05 path; ``fuse_tc``: in the one fused
+    policy->sample->featurize kernel instead).  Returns a dict of device tensors;
     ``status`` must be checked by the caller (``raise_status``)."""
     lib = N.load()
     dev = dsk.device
@@ -793,7 +794,7 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
             N.check(lib.harl_policy_step_tc(
                 *args, _ptr(agent.hid_scratch(n)), _ptr(rng_dev),
                 _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _ptr(grow),
-                m_total, _ptr(feat_out), _stream()),
+                m_total, _ptr(feat_out), 1 if fuse_tc else 0, _stream()),
                 "harl_policy_step_tc")
     else:
         with PF.span("policy", n):

@@ -46,6 +46,10 @@ from .space import SketchTables
 # featurize 11.4 us at ~28 warps/SM), so the split launches are the default.
 _FUSED_STEP = os.environ.get("HARL_FUSED_STEP") == "1"
 
+# HARL_SPLIT_FEATURIZE=1: featurize as its own launch (k_featurize2) instead
+# of inside the sampler kernel (A/B and parity cross-check)
+_SPLIT_FEATURIZE = os.environ.get("HARL_SPLIT_FEATURIZE") == "1"
+
 # HARL_SPLIT_FINISH=1: separate GBT and finish launches (k_gbt_predict2 +
 # k_finish_step) instead of the fused k_gbt_finish (A/B and fallback path)
 _SPLIT_FINISH = os.environ.get("HARL_SPLIT_FINISH") == "1"
@@ -309,8 +313,9 @@ class EpisodeEngine:
                             rng_dev=b.rng_tab[k] if graph_mode else None,
                             advance=not graph_mode, grow=grow,
                             m_total=m_total,
-                            feat_out=nxt["feat"] if _FUSED_STEP else None)
-        if not _FUSED_STEP:
+                            feat_out=None if _SPLIT_FEATURIZE else nxt["feat"],
+                            fuse_tc=_FUSED_STEP)
+        if _SPLIT_FEATURIZE:
             D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         # value pass first: the fused GBT kernel's finish epilogue needs
         # V(X) and V(X') (the GBT and value passes both read only X')

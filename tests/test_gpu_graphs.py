@@ -68,21 +68,31 @@ def test_graph_replay_is_bit_identical(hidden, which):
         assert torch.equal(eager.replay.X, graphed.replay.X)
 
 
-def test_fused_policy_sample_featurize_matches_split(monkeypatch):
-    """k_policy_step_fused (policy -> sample/apply -> featurize in one
-    kernel) produces the split launches' episode bit for bit."""
+@pytest.mark.parametrize("flag", ["_FUSED_STEP", "_SPLIT_FEATURIZE",
+                                  "_SPLIT_FINISH"])
+def test_kernel_fusion_variants_match_default(monkeypatch, flag):
+    """Each alternative launch structure produces the default episode bit
+    for bit: _FUSED_STEP (k_policy_step_fused: policy -> sample/apply ->
+    featurize in one kernel), _SPLIT_FEATURIZE (k_featurize2 launched after
+    the sampler instead of inside it), _SPLIT_FINISH (k_gbt_predict2 +
+    k_finish_step instead of the fused k_gbt_finish)."""
     from paper_2211_11172_b200 import engine as E
-    tb, forest, cfg, (_, split) = _setup((128, 128), "conv")
-    _, _, _, (_, fused) = _setup((128, 128), "conv")
+    tb, forest, cfg, (_, dflt) = _setup((128, 128), "conv")
+    _, _, _, (_, alt) = _setup((128, 128), "conv")
     g1, g2 = np.random.default_rng(9), np.random.default_rng(9)
     for ep in range(2):
-        monkeypatch.setattr(E, "_FUSED_STEP", False)
-        r1 = split.run_episode(tb, forest, g1, cfg, 0)
+        monkeypatch.setattr(E, flag, False)
+        r1 = dflt.run_episode(tb, forest, g1, cfg, 0)
         s1, sc1 = r1.states(), r1.scores().copy()
-        monkeypatch.setattr(E, "_FUSED_STEP", True)
-        r2 = fused.run_episode(tb, forest, g2, cfg, 0)
+        rw1 = r1.log_reward[:r1.visits].cpu().numpy().copy()
+        monkeypatch.setattr(E, flag, True)
+        r2 = alt.run_episode(tb, forest, g2, cfg, 0)
         np.testing.assert_array_equal(r2.states()[0], s1[0])
         np.testing.assert_array_equal(r2.states()[1], s1[1])
         assert r2.scores().tobytes() == sc1.tobytes()
-        assert torch.equal(split.dagent.params, fused.dagent.params)
+        assert r2.log_reward[:r2.visits].cpu().numpy().tobytes() == \
+            rw1.tobytes()
+        assert torch.equal(dflt.dagent.params, alt.dagent.params)
+        assert torch.equal(dflt.replay.X, alt.replay.X)
+        assert torch.equal(dflt.replay.Xn, alt.replay.Xn)
         assert g1.bit_generator.state == g2.bit_generator.state

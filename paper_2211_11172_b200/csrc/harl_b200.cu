@@ -750,9 +750,10 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
 }
 
 // featurize inside the sampler up to this many rows per launch (measured:
-// -6 us per step at 16 K rows, +100 us at 1 M rows)
+// C2 16 K rows +4 % episode throughput; C3 at 32 K rows and the 1 M-row
+// sweep faster with the separate featurizer)
 #ifndef HARL_SAMPLE_FEAT_MAX_ROWS
-#define HARL_SAMPLE_FEAT_MAX_ROWS 32768
+#define HARL_SAMPLE_FEAT_MAX_ROWS 16384
 #endif
 static const int64_t SAMPLE_FEAT_MAX_ROWS = HARL_SAMPLE_FEAT_MAX_ROWS;
 

@@ -431,6 +431,25 @@ int harl_rank_topk(const harl_entry_log* log, int32_t local_slots,
                    int32_t* out_idx, int64_t out_cap, int64_t* stats,
                    void* stream);
 
+/* GBT refit: SurrogateModel.fit_incremental + _fit_tree (costmodel.py:
+ * 81-141, 190-212) on the device, bit-exact with the reference.  X [n][F]
+ * and y [n] (renormalised targets) on the device; n <= 16384, max_depth <=
+ * 12.  Trees come back in heap layout, K = 2^(max_depth+1) - 1 nodes per
+ * tree (children of k: 2k+1, 2k+2): out_feat [n_trees][K] (>= 0 split
+ * feature, -1 leaf, -2 no node), out_thr, out_val (the node mean) [n_trees]
+ * [K]; out_pred [n] the final training predictions; out_base (device
+ * double) y.mean(); out_ntrees (device int32) trees built before the
+ * residual early stop.  The host renumbers nodes in the reference's
+ * depth-first creation order. */
+int64_t harl_gbt_fit_scratch_bytes(int32_t n, int32_t feature_len,
+                                   int32_t max_depth);
+int harl_gbt_fit(const double* X, const double* y, int32_t n,
+                 int32_t feature_len, int32_t n_trees, int32_t max_depth,
+                 double learning_rate, int32_t min_leaf, void* scratch,
+                 int64_t scratch_bytes, int32_t* out_feat, double* out_thr,
+                 double* out_val, double* out_pred, double* out_base,
+                 int32_t* out_ntrees, void* stream);
+
 /* Instrumentation (no reference counterpart; the reference has no device).
  * harl_launch_count: kernels this library has launched since load (graph
  * replays excluded -- they do not pass through the library).

@@ -21,6 +21,7 @@ What it restates (reference files under ``/root/reference/pkg/src/schedtune``):
   ``ppo_update`` / ``Adam.step`` ............... rlcore.py:48-71,293-378
 * ``TrackSet.cull`` / ``episode_done`` ......... stopping.py:68-95
 * ``rank_scores`` ............................... costmodel.py:266-286
+* ``_fit_tree`` / ``fit_incremental`` (GBT refit) costmodel.py:81-141,190-212
 
 It is written population-at-once (structure-of-arrays numpy) instead of the
 reference's per-track objects, but every floating-point operation is the
@@ -239,6 +240,101 @@ class GbtModel:
                                                right[node]), node)
             pred = pred + self.learning_rate * val[node]
         return np.maximum(pred, PREDICTION_FLOOR)
+
+
+def fit_tree(X, y, max_depth: int, min_leaf: int):
+    """costmodel.py:81-141: exact greedy variance-reduction split search.
+    Nodes are numbered as the reference creates them (an explicit stack,
+    left child processed first, children allocated at the parent's split).
+    Returns (feature, threshold, left, right, value) arrays."""
+    feature, threshold, left, right, value = [], [], [], [], []
+
+    def add_node():
+        feature.append(-1)
+        threshold.append(0.0)
+        left.append(-1)
+        right.append(-1)
+        value.append(0.0)
+        return len(feature) - 1
+
+    root = add_node()
+    stack = [(root, np.arange(len(y)), 0)]
+    while stack:
+        nid, idx, depth = stack.pop()
+        ys = y[idx]
+        mean = float(ys.mean())
+        value[nid] = mean
+        if depth >= max_depth or len(idx) < 2 * min_leaf:
+            continue
+        if float(((ys - mean) ** 2).sum()) <= 1e-24:
+            continue
+        Xs = X[idx]
+        order = np.argsort(Xs, axis=0, kind="stable")
+        Xsort = np.take_along_axis(Xs, order, axis=0)
+        csum = np.cumsum(ys[order], axis=0)
+        total = float(ys.sum())
+        m = len(idx)
+        pos = np.arange(1, m, dtype=np.float64)
+        sum_l = csum[:-1]
+        gain = (sum_l ** 2) / pos[:, None] + \
+            ((total - sum_l) ** 2) / (m - pos)[:, None]
+        ok = Xsort[1:] != Xsort[:-1]
+        if min_leaf > 1:
+            ok &= ((pos >= min_leaf) & (m - pos >= min_leaf))[:, None]
+        gain = np.where(ok, gain, -np.inf)
+        flat = int(np.argmax(gain))
+        if not np.isfinite(gain.flat[flat]):
+            continue
+        split_pos, feat = divmod(flat, X.shape[1])
+        thr = 0.5 * (Xsort[split_pos, feat] + Xsort[split_pos + 1, feat])
+        go_left = Xs[:, feat] <= thr
+        li, ri = idx[go_left], idx[~go_left]
+        if len(li) == 0 or len(ri) == 0:
+            continue
+        lid, rid = add_node(), add_node()
+        feature[nid] = int(feat)
+        threshold[nid] = float(thr)
+        left[nid] = lid
+        right[nid] = rid
+        stack.append((rid, ri, depth + 1))
+        stack.append((lid, li, depth + 1))
+    return (np.asarray(feature, np.int64), np.asarray(threshold, np.float64),
+            np.asarray(left, np.int64), np.asarray(right, np.int64),
+            np.asarray(value, np.float64))
+
+
+def tree_predict(tree, X):
+    """_Tree.predict (costmodel.py:67-78)."""
+    feat, thr, left, right, val = tree
+    node = np.zeros(len(X), dtype=np.int64)
+    rows = np.arange(len(X))
+    for _ in range(64):
+        f = feat[node]
+        live = f >= 0
+        if not live.any():
+            break
+        go_left = X[rows, np.maximum(f, 0)] <= thr[node]
+        node = np.where(live, np.where(go_left, left[node], right[node]), node)
+    return val[node]
+
+
+def gbt_fit(X, y, n_trees: int = 50, max_depth: int = 6,
+            learning_rate: float = 0.3, min_leaf: int = 1):
+    """SurrogateModel.fit_incremental (costmodel.py:190-212) on a prepared
+    (X, y): returns (base, trees, final training predictions)."""
+    X = np.asarray(X, np.float64)
+    y = np.asarray(y, np.float64)
+    base = float(y.mean())
+    trees = []
+    pred = np.full(len(y), base)
+    for _ in range(n_trees):
+        resid = y - pred
+        if float(np.abs(resid).max()) <= 1e-12:
+            break
+        tree = fit_tree(X, resid, max_depth, min_leaf)
+        pred = pred + learning_rate * tree_predict(tree, X)
+        trees.append(tree)
+    return base, trees, pred
 
 
 # ---------------------------------------------------------------------------

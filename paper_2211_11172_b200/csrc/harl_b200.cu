@@ -22,6 +22,7 @@
 #include "sample_kernels.cuh"
 #include "mlp_tc2.cuh"
 #include "rank_kernels.cuh"
+#include "gbt_fit_kernels.cuh"
 
 namespace harl {
 
@@ -1337,6 +1338,44 @@ int harl_rank_topk(const harl_entry_log* log, int32_t local_slots,
   return HARL_OK;
 }
 
+// ---------------------------------------------------------------------------
+// GBT refit (gbt_fit_kernels.cuh)
+
+struct FitLayout {
+  int64_t pred, resid, sorted_all, ord0, ord1, srt0, srt1, node_of, goleft,
+      seg_start, seg_count, state, nleft, feat, thr, total, bgain, bpos, ctl,
+      bytes;
+};
+
+static FitLayout fit_layout(int64_t n, int64_t F, int max_depth) {
+  FitLayout L;
+  const int64_t K = ((int64_t)1 << (max_depth + 1)) - 1;
+  const int64_t NL = (int64_t)1 << max_depth;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { int64_t r = o; o += align256(bytes); return r; };
+  L.pred = take(n * 8);
+  L.resid = take(n * 8);
+  L.sorted_all = take(F * n * 4);
+  L.ord0 = take(n * 4);
+  L.ord1 = take(n * 4);
+  L.srt0 = take(F * n * 4);
+  L.srt1 = take(F * n * 4);
+  L.node_of = take(n * 4);
+  L.goleft = take(n * 4);
+  L.seg_start = take(K * 4);
+  L.seg_count = take(K * 4);
+  L.state = take(K * 4);
+  L.nleft = take(K * 4);
+  L.feat = take(K * 4);
+  L.thr = take(K * 8);
+  L.total = take(K * 8);
+  L.bgain = take(NL * F * 8);
+  L.bpos = take(NL * F * 4);
+  L.ctl = take((int64_t)sizeof(FitCtl));
+  L.bytes = o;
+  return L;
+}
+
 static int build_grad_jobs(const harl_net_layout& P, const harl_net_layout& V,
                            GradJob* jobs, int* n_jobs, int* n_tiles) {
   int nj = 0, tiles = 0;
@@ -1618,6 +1657,129 @@ int harl_profile_read(int max_kernels, char* names, int name_cap,
     if (launches) launches[k] = cnt[k];
   }
   return n;
+}
+
+
+int64_t harl_gbt_fit_scratch_bytes(int32_t n, int32_t feature_len,
+                                   int32_t max_depth) {
+  if (n < 1 || feature_len < 1 || max_depth < 0 || max_depth > FIT_MAX_DEPTH)
+    return -1;
+  return fit_layout(n, feature_len, max_depth).bytes;
+}
+
+int harl_gbt_fit(const double* X, const double* y, int32_t n,
+                 int32_t feature_len, int32_t n_trees, int32_t max_depth,
+                 double learning_rate, int32_t min_leaf, void* scratch,
+                 int64_t scratch_bytes, int32_t* out_feat, double* out_thr,
+                 double* out_val, double* out_pred, double* out_base,
+                 int32_t* out_ntrees, void* stream) {
+  if (!X || !y || n < 1 || feature_len < 1 || n_trees < 0 || max_depth < 0 ||
+      min_leaf < 1 || !scratch || !out_feat || !out_thr || !out_val ||
+      !out_pred || !out_base || !out_ntrees) {
+    set_error("harl_gbt_fit: bad arguments");
+    return HARL_E_ARG;
+  }
+  if (n > FIT_MAX_N || max_depth > FIT_MAX_DEPTH) {
+    set_error("harl_gbt_fit: n %d > %d or depth %d > %d", n, FIT_MAX_N,
+              max_depth, FIT_MAX_DEPTH);
+    return HARL_E_LIMIT;
+  }
+  const FitLayout L = fit_layout(n, feature_len, max_depth);
+  if (scratch_bytes < L.bytes) {
+    set_error("harl_gbt_fit: scratch too small");
+    return HARL_E_ARG;
+  }
+  char* p = (char*)scratch;
+  FitArgs a;
+  memset(&a, 0, sizeof(a));
+  a.X = X;
+  a.y = y;
+  a.n = n;
+  a.F = feature_len;
+  a.K = (1 << (max_depth + 1)) - 1;
+  a.max_depth = max_depth;
+  a.min_leaf = min_leaf;
+  a.lr = learning_rate;
+  a.pred = out_pred;   // the running prediction lives in the output
+  a.resid = (double*)(p + L.resid);
+  a.sorted_all = (const int32_t*)(p + L.sorted_all);
+  a.ord[0] = (int32_t*)(p + L.ord0);
+  a.ord[1] = (int32_t*)(p + L.ord1);
+  a.srt[0] = (int32_t*)(p + L.srt0);
+  a.srt[1] = (int32_t*)(p + L.srt1);
+  a.node_of = (int32_t*)(p + L.node_of);
+  a.goleft = (int32_t*)(p + L.goleft);
+  a.seg_start = (int32_t*)(p + L.seg_start);
+  a.seg_count = (int32_t*)(p + L.seg_count);
+  a.state = (int32_t*)(p + L.state);
+  a.nleft = (int32_t*)(p + L.nleft);
+  a.feat = (int32_t*)(p + L.feat);
+  a.thr = (double*)(p + L.thr);
+  a.total = (double*)(p + L.total);
+  a.bgain = (double*)(p + L.bgain);
+  a.bpos = (int32_t*)(p + L.bpos);
+  a.ctl = (FitCtl*)(p + L.ctl);
+  a.out_feat = out_feat;
+  a.out_thr = out_thr;
+  a.out_val = out_val;
+  cudaStream_t st = (cudaStream_t)stream;
+  int P2 = 1;
+  while (P2 < n) P2 <<= 1;
+  const size_t ssmem = (size_t)P2 * 12;
+  int rc = allow_smem(k_fit_presort, ssmem, "k_fit_presort");
+  if (rc) return rc;
+  const unsigned gn = (unsigned)((n + 255) / 256 < sm_count() * 4 ? (n + 255) / 256 : sm_count() * 4);
+  HARL_PROF_BEGIN(st);
+  launch_k(k_fit_presort, dim3(feature_len), dim3(1024), ssmem, st, X, (int)n,
+           (int)feature_len, P2, (int32_t*)a.sorted_all);
+  HARL_CHECK_LAUNCH("k_fit_presort");
+  HARL_PROF_BEGIN(st);
+  launch_k(k_fit_iota, dim3(gn), dim3(256), 0, st, a.ord[0], (int)n);
+  HARL_CHECK_LAUNCH("k_fit_iota");
+  HARL_PROF_BEGIN(st);
+  launch_k(k_fit_base, dim3(1), dim3(256), 0, st, a);
+  HARL_CHECK_LAUNCH("k_fit_base");
+  const unsigned ginit = (unsigned)sm_count() * 4;
+  for (int t = 0; t < n_trees; ++t) {
+    HARL_PROF_BEGIN(st);
+    launch_k(k_fit_tree_init, dim3(ginit), dim3(256), 0, st, a);
+    HARL_CHECK_LAUNCH("k_fit_tree_init");
+    HARL_PROF_BEGIN(st);
+    launch_k(k_fit_tree_check, dim3(1), dim3(1), 0, st, a, t);
+    HARL_CHECK_LAUNCH("k_fit_tree_check");
+    for (int d = 0; d <= max_depth; ++d) {
+      const int nl = 1 << d, lists = d & 1;
+      HARL_PROF_BEGIN(st);
+      launch_k(k_fit_stats, dim3(nl), dim3(128), 0, st, a, d, t, lists);
+      HARL_CHECK_LAUNCH("k_fit_stats");
+      if (d == max_depth) break;
+      const int64_t wb = (int64_t)nl * feature_len * 32;
+      HARL_PROF_BEGIN(st);
+      launch_k(k_fit_best, dim3((unsigned)((wb + 255) / 256)), dim3(256), 0, st, a, d, lists);
+      HARL_CHECK_LAUNCH("k_fit_best");
+      HARL_PROF_BEGIN(st);
+      launch_k(k_fit_split, dim3((unsigned)((nl + 127) / 128)), dim3(128), 0, st, a, d, lists);
+      HARL_CHECK_LAUNCH("k_fit_split");
+      HARL_PROF_BEGIN(st);
+      launch_k(k_fit_route, dim3(gn), dim3(256), 0, st, a);
+      HARL_CHECK_LAUNCH("k_fit_route");
+      HARL_PROF_BEGIN(st);
+      launch_k(k_fit_commit, dim3((unsigned)((nl + 127) / 128)), dim3(128), 0, st, a, d, t);
+      HARL_CHECK_LAUNCH("k_fit_commit");
+      const int64_t wp = (int64_t)nl * (feature_len + 1) * 32;
+      HARL_PROF_BEGIN(st);
+      launch_k(k_fit_partition, dim3((unsigned)((wp + 255) / 256)), dim3(256), 0, st, a, d, lists);
+      HARL_CHECK_LAUNCH("k_fit_partition");
+    }
+    HARL_PROF_BEGIN(st);
+    launch_k(k_fit_pred, dim3(gn), dim3(256), 0, st, a, t);
+    HARL_CHECK_LAUNCH("k_fit_pred");
+  }
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(out_base, &a.ctl->base, 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(out_ntrees, &a.ctl->n_built, 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    return cuda_status(e, "harl_gbt_fit outputs");
+  return HARL_OK;
 }
 
 }  // extern "C"

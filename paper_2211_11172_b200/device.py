@@ -17,6 +17,8 @@ this module                    reference
 ``value_estimate``             ValueNet.estimate 173-174
 ``DeviceAgent.ppo_update``     ppo_update 361-378
 ``rank_topk``                  costmodel.rank_scores 266-286
+``gbt_fit``                    SurrogateModel.fit_incremental 190-212
+                               (+ _fit_tree 81-141)
 =============================  ==========================================
 """
 
@@ -294,6 +296,87 @@ def gather_entries(tables: SketchTables, log_tiles, log_knobs, log_score,
     feats = featurize(dsk if dsk is not None else DeviceSketch(tables, dev),
                       tiles, knobs, n)
     return tiles, knobs, score[:n], track[:n], feats
+
+
+class GbtFit:
+    """A device refit: ``base``, ``trees`` as the reference stores them
+    ((feature, threshold, left, right, value) arrays, nodes numbered in
+    _fit_tree's creation order) and ``pred``, the final training
+    predictions (fit_incremental's ``pred``)."""
+
+    def __init__(self, base, trees, pred):
+        self.base, self.trees, self.pred = base, trees, pred
+
+
+def heap_tree_to_reference(feat_h, thr_h, val_h):
+    """Heap-layout tree (children of k at 2k+1, 2k+2) -> the reference's
+    node numbering: _fit_tree pops a stack (left child first) and allocates
+    both children when it splits a node (costmodel.py:86-141)."""
+    feature, threshold, left, right, value = [-1], [0.0], [-1], [-1], [0.0]
+    ref = {0: 0}
+    stack = [0]
+    while stack:
+        h = stack.pop()
+        nid = ref[h]
+        value[nid] = float(val_h[h])
+        f = int(feat_h[h])
+        if f < 0:
+            continue
+        lid, rid = len(feature), len(feature) + 1
+        for _ in range(2):
+            feature.append(-1)
+            threshold.append(0.0)
+            left.append(-1)
+            right.append(-1)
+            value.append(0.0)
+        ref[2 * h + 1], ref[2 * h + 2] = lid, rid
+        feature[nid] = f
+        threshold[nid] = float(thr_h[h])
+        left[nid], right[nid] = lid, rid
+        stack.append(2 * h + 2)
+        stack.append(2 * h + 1)
+    return (np.asarray(feature, np.int64), np.asarray(threshold, np.float64),
+            np.asarray(left, np.int64), np.asarray(right, np.int64),
+            np.asarray(value, np.float64))
+
+
+def gbt_fit(X, y, n_trees: int = 50, max_depth: int = 6,
+            learning_rate: float = 0.3, min_leaf: int = 1, device=None):
+    """SurrogateModel.fit_incremental (costmodel.py:190-212) on the device:
+    (X [n][F], y [n]) host or device arrays -> ``GbtFit``, bit-exact with
+    the reference's trees."""
+    lib = N.load()
+    dev = _dev(device)
+    Xd = torch.as_tensor(np.ascontiguousarray(X, np.float64)
+                         if not isinstance(X, torch.Tensor) else X,
+                         dtype=torch.float64).to(dev).contiguous()
+    yd = torch.as_tensor(np.ascontiguousarray(y, np.float64)
+                         if not isinstance(y, torch.Tensor) else y,
+                         dtype=torch.float64).to(dev).contiguous()
+    n, F = Xd.shape
+    need = lib.harl_gbt_fit_scratch_bytes(n, F, max_depth)
+    if need < 0:
+        raise DeviceError(f"gbt_fit: unsupported shape n={n} F={F} "
+                          f"depth={max_depth}")
+    scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+    K = (1 << (max_depth + 1)) - 1
+    T = max(n_trees, 1)
+    feat = torch.empty((T, K), dtype=torch.int32, device=dev)
+    thr = torch.empty((T, K), dtype=torch.float64, device=dev)
+    val = torch.empty((T, K), dtype=torch.float64, device=dev)
+    pred = torch.empty(n, dtype=torch.float64, device=dev)
+    base = torch.empty(1, dtype=torch.float64, device=dev)
+    nt = torch.zeros(1, dtype=torch.int32, device=dev)
+    with PF.span("gbt_fit", n):
+        N.check(lib.harl_gbt_fit(
+            _ptr(Xd), _ptr(yd), n, F, n_trees, max_depth, learning_rate,
+            min_leaf, _ptr(scratch), need, _ptr(feat), _ptr(thr), _ptr(val),
+            _ptr(pred), _ptr(base), _ptr(nt), _stream()), "harl_gbt_fit")
+    k = int(nt.item())
+    fh, th, vh = (feat[:k].cpu().numpy(), thr[:k].cpu().numpy(),
+                  val[:k].cpu().numpy())
+    trees = [heap_tree_to_reference(fh[t], th[t], vh[t]) for t in range(k)]
+    return GbtFit(float(base.item()), trees, pred.cpu().numpy())
 
 
 def action_masks(dsk: DeviceSketch, tiles, knobs, n: int):

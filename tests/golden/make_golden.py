@@ -149,9 +149,13 @@ def main():
                                          for s in states])
             for s, r in zip(states, res):
                 session.model.observe(ctx.featurize(s), r.throughput, sg.id)
+        ex = session.model.training_examples()
         session.model.fit_round()
         trees = session.model.trees
         arrays = {}
+        # the refit's training set (GBT refit parity, costmodel.py:190-212)
+        arrays["fit_X"] = np.stack([e.features for e in ex])
+        arrays["fit_y"] = np.asarray([e.target for e in ex], np.float64)
         arrays["model_base"] = np.asarray([session.model.base])
         for i, tr in enumerate(trees):
             arrays[f"tree{i:03d}_feature"] = tr.feature.astype(np.int16)
@@ -273,7 +277,53 @@ def main():
         index[case["name"]] = os.path.getsize(path)
         print(case["name"], "episodes", len(rec["episodes"]),
               "npz bytes", os.path.getsize(path))
+    index["gbt_fit_large"] = make_gbt_fixture()
     return index
+
+
+def make_gbt_fixture(n: int = 2500):
+    """The reference's own GBT refit on a larger realistic training set:
+    featurized uniform conv2d/GEMM states (many tied feature values) with
+    SimulatedBackend throughputs, renormalized per subgraph exactly as
+    training_examples() does."""
+    sys.path.insert(0, REF)
+    from schedtune.costmodel import GbtConfig, SurrogateModel
+    from schedtune.measure import MeasureRequest, SimulatedBackend
+    from schedtune.schedspace import SketchContext, sample_initial_schedules
+    from schedtune.workload import TargetConfig, generate_sketches, load_network
+    wl_dir = "/root/reference/pkg/workloads"
+    model = SurrogateModel(GbtConfig())
+    rng = np.random.default_rng(77)
+    backend = SimulatedBackend()
+    for wl in ("conv2d.yaml", "gemm_l.yaml"):
+        net = load_network(os.path.join(wl_dir, wl))
+        tg = TargetConfig()
+        for sg in net.subgraphs[:2]:
+            for sk in generate_sketches(sg, tg):
+                ctx = SketchContext(sg, sk, tg)
+                states = sample_initial_schedules(sk, n // 12, rng)
+                res = backend.measure_batch([MeasureRequest(s, ctx)
+                                             for s in states])
+                for s_, r in zip(states, res):
+                    if r.valid:
+                        model.observe(ctx.featurize(s_), r.throughput, sg.id)
+    ex = model.training_examples()
+    X = np.stack([e.features for e in ex])
+    y = np.asarray([e.target for e in ex], np.float64)
+    rep = model.fit_round()
+    arrays = {"X": X, "y": y, "base": np.asarray([model.base]),
+              "loss": np.asarray([rep.loss_before, rep.loss_after])}
+    for i, tr in enumerate(model.trees):
+        arrays[f"tree{i:03d}_feature"] = tr.feature.astype(np.int16)
+        arrays[f"tree{i:03d}_threshold"] = tr.threshold
+        arrays[f"tree{i:03d}_left"] = tr.left.astype(np.int16)
+        arrays[f"tree{i:03d}_right"] = tr.right.astype(np.int16)
+        arrays[f"tree{i:03d}_value"] = tr.value
+    arrays["n_trees"] = np.asarray([len(model.trees)])
+    path = os.path.join(HERE, "gbt_fit_large.npz")
+    np.savez_compressed(path, **arrays)
+    print("gbt_fit_large", X.shape, len(model.trees), os.path.getsize(path))
+    return os.path.getsize(path)
 
 
 if __name__ == "__main__":

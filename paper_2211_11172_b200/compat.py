@@ -19,6 +19,8 @@ checkpoints, the CLI -- is the reference's own code.  Per episode it
 * writes back parameters, moments, Adam step counts, the replay deque and
   ``order_counter``; emits the same trajectory-log events
   (``episode_step``/``cull``/``train``/``episode_end``, tuner.py:413-439);
+* refits the surrogate after each round's measurements on the device
+  (``harl_gbt_fit``: the same trees, bit for bit, as fit_incremental);
 * returns the visited entries as the reference's ``CandidateEntry`` list --
   by default only the device-selected top-k' (``harl_rank_topk``), on
   which run_round's ``rank_scores`` returns exactly its full-list answer
@@ -46,6 +48,43 @@ def _enc(x):
     return x
 
 
+def _device_fit_incremental(model, examples):
+    """SurrogateModel.fit_incremental (costmodel.py:190-212) with the trees
+    grown on the device (device.gbt_fit, bit-exact) and the report's losses
+    from device predictions: loss_before = mean((raw old prediction - y)^2)
+    with the old ensemble evaluated by the GBT kernel without its floor,
+    loss_after from the fit's own final predictions."""
+    from schedtune.costmodel import CostModelError, FitReport, _Tree
+    if not examples:
+        raise CostModelError("fit_incremental needs at least one example")
+    cfg = model.cfg
+    X = np.stack([e.features for e in examples])
+    y = np.asarray([e.target for e in examples], dtype=np.float64)
+    if len(y) > 16384 or cfg.max_depth > 12:     # beyond the device limits
+        return model._b200_host_fit(examples)
+    import torch
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    if model.fitted:
+        old = D.DeviceForest(
+            [(t.feature, t.threshold, t.left, t.right, t.value)
+             for t in model.trees], model.base, cfg.learning_rate,
+            fitted=True, floor_value=-np.inf)
+        raw = D.gbt_predict(old, Xd, len(y)).cpu().numpy()
+    else:
+        raw = np.ones(len(y), dtype=np.float64)
+    before = float(np.mean((raw - y) ** 2))
+    fit = D.gbt_fit(Xd, y, n_trees=cfg.n_trees, max_depth=cfg.max_depth,
+                    learning_rate=cfg.learning_rate,
+                    min_leaf=cfg.min_samples_leaf)
+    model.base = fit.base
+    model.fitted = True
+    model.trees = [_Tree(feature=f, threshold=t, left=l, right=r, value=v)
+                   for f, t, l, r, v in fit.trees]
+    after = float(np.mean((fit.pred - y) ** 2))
+    return FitReport(n_examples=len(y), loss_before=before,
+                     loss_after=after)
+
+
 def b200_session_class(base):
     """Build the B200 subclass of the reference ``TuningSession`` class
     ``base`` (passed in so this module never imports the reference)."""
@@ -56,6 +95,8 @@ def b200_session_class(base):
         # True: _run_episode returns every visited entry (the reference's
         # full list); False: the top-k' superset rank_scores needs
         b200_all_entries = False
+        # refit the surrogate on the device (harl_gbt_fit, bit-exact)
+        b200_device_refit = True
 
         def _b200_engine(self, sg):
             eng = getattr(self, "_b200_engines", None)
@@ -124,7 +165,19 @@ def b200_session_class(base):
 
         # -- the seam --------------------------------------------------------
 
+        def _b200_hook_model(self):
+            """Route the session model's refit (fit_round ->
+            fit_incremental, costmodel.py:190-215) to the device."""
+            m = self.model
+            if self.b200_device_refit and \
+                    getattr(m, "_b200_refit_of", None) is not m:
+                import types
+                m._b200_host_fit = m.fit_incremental
+                m.fit_incremental = types.MethodType(_device_fit_incremental, m)
+                m._b200_refit_of = m
+
         def _run_episode(self, sg, sketch, rnd):
+            self._b200_hook_model()
             ecfg = EpisodeConfig.from_tuner(self.cfg, self.searcher)
             eng = self._b200_engine(sg)
             tables = self._b200_sketch_tables(sg, sketch)

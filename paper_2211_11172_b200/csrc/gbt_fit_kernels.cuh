@@ -310,23 +310,56 @@ __global__ void k_fit_best(FitArgs a, int d, int lists) {
   double best = -INFINITY;
   int bpos = -1;
   double carry = 0.0;
+  // software pipeline: the next chunk's residuals and feature values are
+  // loaded into registers while lane 0 runs the current chunk's chain
+  constexpr int PL = FIT_CHUNK / 32;
+  double nr[PL], nx[PL];
+  auto fetch = [&](int c0) {
+#pragma unroll
+    for (int u = 0; u < PL; ++u) {
+      const int q = lane + 32 * u;
+      const int j = c0 + q;
+      if (j < m) {
+        const int i = list[j];
+        nr[u] = a.resid[i];
+        nx[u] = a.X[(int64_t)i * a.F + f];
+      }
+    }
+  };
+  if (m > 1) fetch(0);
   for (int c0 = 0; c0 < m - 1; c0 += FIT_CHUNK) {
     const int cn = min(FIT_CHUNK, m - c0);           // elements staged
     // positions j = c0 .. c0+cn-1 need x_j and x_{j+1}
-    for (int q = lane; q < cn; q += 32) {
-      const int i = list[c0 + q];
-      cs[q] = a.resid[i];
-      xs[q] = a.X[(int64_t)i * a.F + f];
+#pragma unroll
+    for (int u = 0; u < PL; ++u) {
+      const int q = lane + 32 * u;
+      if (q < cn) {
+        cs[q] = nr[u];
+        xs[q] = nx[u];
+      }
     }
     if (lane == 0)
       xs[cn] = (c0 + cn < m) ? a.X[(int64_t)list[c0 + cn] * a.F + f] : 0.0;
     __syncwarp();
+    if (c0 + FIT_CHUNK < m - 1) fetch(c0 + FIT_CHUNK);
     if (lane == 0) {   // numpy cumsum: out[0] = a[0], out[j] = out[j-1] + a[j]
       double c = carry;
       int q = 0;
       if (c0 == 0) {
         c = cs[0];
         q = 1;
+      }
+      for (; q + 8 <= cn; q += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = cs[q + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          c = __dadd_rn(c, v[u]);
+          v[u] = c;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cs[q + u] = v[u];
       }
       for (; q < cn; ++q) {
         c = __dadd_rn(c, cs[q]);
@@ -471,22 +504,32 @@ __global__ void k_fit_partition(FitArgs a, int d, int lists) {
   const int32_t* src = q == a.F ? a.ord[lists] : a.srt[lists] + (int64_t)q * a.n;
   int32_t* dst = q == a.F ? a.ord[lists ^ 1] : a.srt[lists ^ 1] + (int64_t)q * a.n;
   int nlw = 0, nrw = 0;
-  for (int c0 = 0; c0 < m; c0 += 32) {
-    const int j = c0 + lane;
-    const bool in = j < m;
-    const int i = in ? src[s + j] : 0;
-    const bool gl = in && a.goleft[i];
-    const unsigned bl = __ballot_sync(0xffffffffu, gl);
-    const unsigned br = __ballot_sync(0xffffffffu, in && !gl);
-    const unsigned below = (1u << lane) - 1u;
-    if (in) {
-      const int p = gl ? s + nlw + __popc(bl & below)
-                       : s + L + nrw + __popc(br & below);
-      dst[p] = i;
-      if (q == a.F) a.node_of[i] = gl ? 2 * k + 1 : 2 * k + 2;
+  constexpr int PB = 8;   // chunks of 32 with their loads in flight together
+  for (int c0 = 0; c0 < m; c0 += 32 * PB) {
+    int iv[PB];
+    bool gv[PB];
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      const int j = c0 + 32 * u + lane;
+      iv[u] = j < m ? src[s + j] : -1;
     }
-    nlw += __popc(bl);
-    nrw += __popc(br);
+#pragma unroll
+    for (int u = 0; u < PB; ++u) gv[u] = iv[u] >= 0 && a.goleft[iv[u]];
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      const bool in = iv[u] >= 0;
+      const unsigned bl = __ballot_sync(0xffffffffu, gv[u]);
+      const unsigned br = __ballot_sync(0xffffffffu, in && !gv[u]);
+      const unsigned below = (1u << lane) - 1u;
+      if (in) {
+        const int p = gv[u] ? s + nlw + __popc(bl & below)
+                            : s + L + nrw + __popc(br & below);
+        dst[p] = iv[u];
+        if (q == a.F) a.node_of[iv[u]] = gv[u] ? 2 * k + 1 : 2 * k + 2;
+      }
+      nlw += __popc(bl);
+      nrw += __popc(br);
+    }
   }
 }
 

@@ -125,3 +125,26 @@ def test_drop_in_topk_entries_rank_like_full_list(tmp_path, searcher):
     while dev.trials_used < dev.cfg.total_trials:
         dev.run_round()
     assert len(seen) >= 4 and seen[-1][2] > 0
+
+
+def test_drop_in_device_refit_matches_host_refit(tmp_path):
+    """After real rounds (device refits inside run_round), the session
+    model's next refit on the device equals the reference's own host
+    fit_incremental from the same state: trees, base and FitReport."""
+    from schedtune.costmodel import SurrogateModel
+    _, dev = _sessions(tmp_path, (16,), total_trials=64)
+    for _ in range(4):
+        dev.run_round()
+    m = dev.model
+    assert getattr(m, "_b200_refit_of", None) is m
+    host = SurrogateModel(m.cfg)
+    host._feat, host._thr, host._sg = list(m._feat), list(m._thr), list(m._sg)
+    host._best_thr = dict(m._best_thr)
+    host.base, host.fitted, host.trees = m.base, m.fitted, list(m.trees)
+    ex = m.training_examples()
+    rep_h = SurrogateModel.fit_incremental(host, ex)
+    rep_d = m.fit_incremental(ex)
+    assert (rep_d.n_examples, rep_d.loss_before, rep_d.loss_after) == \
+        (rep_h.n_examples, rep_h.loss_before, rep_h.loss_after)
+    assert m.base == host.base and len(m.trees) == len(host.trees)
+    assert m.dump_text() == host.dump_text()

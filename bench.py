@@ -461,7 +461,7 @@ KERNEL_SPAN = {
 }
 
 
-def per_row_work(tables, H):
+def per_row_work(tables, H, feat_in_sampler=False):
     """Algorithmic work per row (one schedule / one minibatch row) of each
     kernel: flops for the MLP kernels, HBM bytes for the rest (DESIGN.md
     "Kernels and their rooflines" states the same figures)."""
@@ -477,8 +477,10 @@ def per_row_work(tables, H):
         # + the sampler/walker and the featurizer of the same rows
         "k_policy_step_fused": 2 * (F * H + H * H + H * NH),
         "k_value_tc": 2 * (F * H + H * H + H),
-        # logits in; actions, logp, successor state out
-        "k_sample_rows": 4 * NH + state + 16 + 8 + state,
+        # logits in; actions, logp, successor state out (+ its feature row
+        # when the sampler featurizes, <= 16 K rows per launch)
+        "k_sample_rows": 4 * NH + state + 16 + 8 + state +
+                         (8 * F if feat_in_sampler else 0),
         "k_featurize": state + 8 * F,
         "k_featurize2": state + 8 * F,
         "k_gbt_predict": 8 * F + 8,
@@ -493,7 +495,7 @@ def per_row_work(tables, H):
     }
 
 
-def roofline_entry(native, spans, tables, hidden):
+def roofline_entry(native, spans, tables, hidden, P=0):
     """Dominant kernel's achieved rate vs the measured peak, from the native
     per-kernel event timer (harl_profile_*) of the untimed profiled episode;
     rows per kernel come from the matching host span."""
@@ -504,7 +506,9 @@ def roofline_entry(native, spans, tables, hidden):
         pass
     if not native:
         return None
-    work = per_row_work(tables, hidden)
+    # the sampler featurizes in-kernel up to 16 K rows per launch
+    # (HARL_SAMPLE_FEAT_MAX_ROWS, harl_b200.cu)
+    work = per_row_work(tables, hidden, feat_in_sampler=0 < P <= 16384)
     hbm = peaks.get("hbm_gbs", 6650.0)
     bf16 = peaks.get("bf16_tflops", 1590.0)
     tf32 = bf16 * 1.1 / 2.25        # dense tf32 : bf16 nominal ratio
@@ -639,7 +643,7 @@ def main():
                                       for k, v in r["e2e_parts"].items()}},
         "gpu_launches": int(r["launches"]),
         "clocks": r["clocks"],
-        "roofline": roofline_entry(r["native"], r["kstats"], tb, 128),
+        "roofline": roofline_entry(r["native"], r["kstats"], tb, 128, P),
         "kernel_ms_per_episode": {k: round(v["ms"], 4)
                                   for k, v in r["kstats"].items()},
     }

@@ -831,12 +831,14 @@ class DeviceAgent:
 def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 n: int, gen=None, inject=None, out=None, want_logits=False,
                 rng_dev=None, advance=True, grow=None, m_total: int = 0,
-                feat_out=None, fuse_tc: bool = False):
+                feat_out=None, fuse_tc: bool = False, reset_status=True):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
     ``feat_out`` (optional f64 [n][F]): also featurize the new states (in
     the sampler kernel on the tcgen05 path; ``fuse_tc``: in the one fused
-    policy->sample->featurize kernel instead).  Returns a dict of device tensors;
+    policy->sample->featurize kernel instead).  ``reset_status=False``: the
+    caller already set ``out["status"]`` to -1 (the engine fills its
+    per-step status table once per episode, not once per step).  Returns a dict of device tensors;
     ``status`` must be checked by the caller (``raise_status``)."""
     lib = N.load()
     dev = dsk.device
@@ -854,7 +856,7 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                "head0_col": torch.empty(max(n, 1), dtype=torch.int32,
                                         device=dev),
                "status": torch.full((1,), -1, dtype=torch.int64, device=dev)}
-    else:
+    elif reset_status:
         out["status"].fill_(-1)
     logits = None
     if want_logits:

@@ -314,7 +314,7 @@ class EpisodeEngine:
                             advance=not graph_mode, grow=grow,
                             m_total=m_total,
                             feat_out=None if _SPLIT_FEATURIZE else nxt["feat"],
-                            fuse_tc=_FUSED_STEP)
+                            fuse_tc=_FUSED_STEP, reset_status=False)
         if _SPLIT_FEATURIZE:
             D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         # value pass first: the fused GBT kernel's finish epilogue needs

@@ -663,13 +663,23 @@ class EpisodeEngine:
 
     # ---- graph path --------------------------------------------------------
 
+    # steps in the first graph: its per-step rows are prepared before any
+    # GPU work of the episode can start, the rest while it runs
+    HEAD_STEPS = 8
+
     def _segments(self, plan):
-        """Step index ranges between host decisions (a cull ends a
-        segment; the next one starts with the survivor gather)."""
-        segs, start = [], 0
+        """Step index ranges of the captured graphs: a host cull decision
+        ends a segment (the next one starts with the survivor gather), and
+        the episode's first HEAD_STEPS steps are a graph of their own so the
+        host precompute of the rest overlaps them.  Returns (first, last,
+        starts_after_cull)."""
+        segs, start, after_cull = [], 0, False
         for k, step in enumerate(plan):
-            if step["cull"] or k == len(plan) - 1:
-                segs.append((start, k))
+            head_end = k == self.HEAD_STEPS - 1 and start == 0 and \
+                k < len(plan) - 1 and not step["cull"]
+            if step["cull"] or k == len(plan) - 1 or head_end:
+                segs.append((start, k, after_cull))
+                after_cull = bool(step["cull"])
                 start = k + 1
         return segs
 
@@ -694,12 +704,12 @@ class EpisodeEngine:
         count0 = self.replay.count
         stream = torch.cuda.Stream(device=self.dev)
         stream.wait_stream(torch.cuda.current_stream())
-        for si, (k0, k1) in enumerate(segs):
+        for si, (k0, k1, after_cull) in enumerate(segs):
             g = torch.cuda.CUDAGraph()
             n0 = PF.launch_count()
             with torch.cuda.graph(g, stream=stream,
                                   capture_error_mode="relaxed"):
-                if si > 0:
+                if after_cull:
                     n_keep = b.plan[k0 - 1]["m"] - b.plan[k0 - 1]["cull"]
                     self._compact(b, b.pop[cur_i], b.rt[rt_i],
                                   b.pop[1 - cur_i], b.rt[1 - rt_i], n_keep)
@@ -716,7 +726,7 @@ class EpisodeEngine:
                         self._launch_ppo(b, ppo_k, B, b.slot_tab[ppo_k, :B],
                                          1, 1, True)
                         ppo_k += 1
-            graphs.append((k0, k1, g, PF.launch_count() - n0))
+            graphs.append((k0, k1, g, PF.launch_count() - n0, after_cull))
         torch.cuda.current_stream().wait_stream(stream)
         self.replay.wpos, self.replay.count = wpos0, count0
         b.graphs = graphs
@@ -730,55 +740,82 @@ class EpisodeEngine:
         if b.graphs is None:
             self._capture(b, gen)
             PF.add_launches(-sum(g[3] for g in b.graphs))  # not executed
-        # ---- host precompute of every per-step value (data-independent) --
+        # ---- host precompute of every per-step value (data-independent),
+        # pipelined: the first segment's rows go up and its graph starts,
+        # then the host prepares the remaining rows while the GPU runs
         n_steps = len(b.plan)
-        rng_np = np.zeros((max(n_steps, 1), 2), dtype=np.uint64)
-        wpos_np = np.zeros(max(n_steps, 1), dtype=np.int64)
-        slot_np = np.zeros(tuple(b.slot_tab.shape), dtype=np.int32)
-        adam_np = np.zeros((max(b.n_ppo, 1), 4), dtype=np.float64)
-        idx_list = []
+        if getattr(b, "pins", None) is None:
+            mk = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            b.pins = {"rng": mk(b.rng_tab), "wpos": mk(b.wpos_tab),
+                      "slot": mk(b.slot_tab), "adam": mk(b.adam_tab)}
+        pins = b.pins
+        rng_np = pins["rng"].numpy().view(np.uint64)
+        wpos_np = pins["wpos"].numpy()
+        slot_np = pins["slot"].numpy()
+        adam_np = pins["adam"].numpy()
         a = self.agent
-        ppo_k = 0
-        for k, step in enumerate(b.plan):
-            st = gen.bit_generator.state["state"]["state"]
-            rng_np[k, 0] = st >> 64               # u128 {hi, lo} (common.cuh)
-            rng_np[k, 1] = st & ((1 << 64) - 1)
-            R.skip_u64(gen, 4 * step["m"])
-            wpos_np[k] = self.replay.wpos
-            self.replay.note_push(step["m"])
-            if step["ppo"]:
-                B = step["ppo"]
-                idx = gen.choice(len(self.replay), size=B, replace=False)
-                idx_list.append(idx)
-                slot_np[ppo_k, :B] = self.replay.slots_of(idx)
-                a.opt_pi.t += 1
-                a.opt_v.t += 1
-                adam_np[ppo_k] = (1.0 - 0.9 ** a.opt_pi.t,
-                                  1.0 - 0.999 ** a.opt_pi.t,
-                                  1.0 - 0.9 ** a.opt_v.t,
-                                  1.0 - 0.999 ** a.opt_v.t)
-                ppo_k += 1
-        b.rng_tab.copy_(torch.from_numpy(rng_np.view(np.int64)))
-        b.wpos_tab.copy_(torch.from_numpy(wpos_np))
-        b.slot_tab.copy_(torch.from_numpy(slot_np))
-        b.adam_tab.copy_(torch.from_numpy(adam_np))
+        cursor = R.StreamCursor(gen)
+        pk = [0]
+
+        def precompute(k0, k1):
+            p0 = pk[0]
+            for k in range(k0, k1 + 1):
+                step = b.plan[k]
+                st = cursor.s
+                rng_np[k, 0] = st >> 64           # u128 {hi, lo} (common.cuh)
+                rng_np[k, 1] = st & ((1 << 64) - 1)
+                cursor.skip_u64(4 * step["m"])
+                wpos_np[k] = self.replay.wpos
+                self.replay.note_push(step["m"])
+                if step["ppo"]:
+                    B = step["ppo"]
+                    cursor.sync_to()
+                    idx = gen.choice(len(self.replay), size=B, replace=False)
+                    cursor.sync_from()
+                    slot_np[pk[0], :B] = self.replay.slots_of(idx)
+                    a.opt_pi.t += 1
+                    a.opt_v.t += 1
+                    adam_np[pk[0]] = (1.0 - 0.9 ** a.opt_pi.t,
+                                      1.0 - 0.999 ** a.opt_pi.t,
+                                      1.0 - 0.9 ** a.opt_v.t,
+                                      1.0 - 0.999 ** a.opt_v.t)
+                    pk[0] += 1
+            return p0, pk[0]
+
+        def upload(k0, k1, p0, p1):
+            b.rng_tab[k0:k1 + 1].copy_(pins["rng"][k0:k1 + 1], non_blocking=True)
+            b.wpos_tab[k0:k1 + 1].copy_(pins["wpos"][k0:k1 + 1],
+                                        non_blocking=True)
+            if p1 > p0:
+                b.slot_tab[p0:p1].copy_(pins["slot"][p0:p1], non_blocking=True)
+                b.adam_tab[p0:p1].copy_(pins["adam"][p0:p1], non_blocking=True)
+
+        segs = b.graphs
+        first = segs[0]
+        upload(first[0], first[1], *precompute(first[0], first[1]))
+        first[2].replay()
+        if len(segs) > 1:
+            k0 = segs[1][0]
+            upload(k0, n_steps - 1, *precompute(k0, n_steps - 1))
+        cursor.sync_to()
         # ---- replay the segments; host culls in between --------------------
         alive = np.ones(P, dtype=bool)
         culls, train = [], []
         used, ppo_k = 0, 0
         rt_i = 0
         cur_i = 0
-        for si, (k0, k1, g, nl) in enumerate(b.graphs):
-            if si > 0:
+        for si, (k0, k1, g, nl, after_cull) in enumerate(b.graphs):
+            if after_cull:
                 prev = b.plan[k0 - 1]
                 m = prev["m"]
-                tracks = b.rt[rt_i][:m].cpu().numpy().astype(np.int64)
-                gone = self._cull(tracks, b.adv, m, alive, cfg)
+                tracks, adv_h = self._cull_inputs(b, rt_i, m)
+                gone = self._cull(tracks, adv_h, m, alive, cfg)
                 culls.append((prev["t"], gone, int(alive.sum())))
                 keep = np.flatnonzero(alive[tracks]).astype(np.int32)
                 b.keep[:len(keep)].copy_(torch.from_numpy(keep))
                 rt_i = 1 - rt_i
-            g.replay()
+            if si > 0:
+                g.replay()       # segment 0 was launched above
             PF.add_launches(nl)
             for k in range(k0, k1 + 1):
                 step = b.plan[k]
@@ -800,20 +837,45 @@ class EpisodeEngine:
                 "score": torch.empty(P, dtype=torch.float64, device=dev)}
 
     def _cull(self, tracks, adv, m, alive, cfg):
-        """stopping.py:68-86 on the host: lowest (advantage, -index) go."""
+        """stopping.py:68-86 on the host: the n_elim lowest by
+        (advantage, -index) go.  ``adv``: host array of the step's rows (or
+        a device tensor).  A partition finds the cut value; only ties at the
+        cut are ordered (higher index first), as the full sort would."""
         live = np.flatnonzero(alive)
         n = len(live)
         n_elim = min(int(math.floor(cfg.cull_fraction * n)),
                      n - cfg.min_tracks)
         if n_elim <= 0:
             return np.zeros(0, dtype=np.int64)
-        a = adv[:m].cpu().numpy()
+        a = adv[:m].cpu().numpy() if isinstance(adv, torch.Tensor) \
+            else np.asarray(adv[:m])
         adv_full = np.zeros(len(alive))
         adv_full[tracks] = a
-        order = np.lexsort((-live, adv_full[live]))
-        gone = np.sort(live[order[:n_elim]])
+        v = adv_full[live]
+        if np.isnan(v).any():      # NaN orders last, as in the full sort
+            order = np.lexsort((-live, v))
+            gone = np.sort(live[order[:n_elim]])
+        else:
+            cut = np.partition(v, n_elim - 1)[n_elim - 1]
+            below = live[v < cut]
+            tied = live[v == cut]
+            need = n_elim - len(below)
+            gone = np.sort(np.concatenate([below, tied[::-1][:need]]))
         alive[gone] = False
         return gone
+
+    def _cull_inputs(self, b, rt_i, m):
+        """Row->track ids and advantages of the cull step in one pinned
+        D2H round trip."""
+        if getattr(b, "cull_pin", None) is None:
+            b.cull_pin = (torch.empty(b.P, dtype=torch.int32, pin_memory=True),
+                          torch.empty(b.P, dtype=torch.float64,
+                                      pin_memory=True))
+        pt, pa = b.cull_pin
+        pt[:m].copy_(b.rt[rt_i][:m], non_blocking=True)
+        pa[:m].copy_(b.adv[:m], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return pt[:m].numpy().astype(np.int64), pa[:m].numpy().copy()
 
     def _compact(self, b, src, rt_src, dst, rt_dst, n_keep):
         """Survivor gather with row indices from ``b.keep`` (device)."""

@@ -35,6 +35,42 @@ def _jump(steps: int, inc: int):
     return acc_a, acc_c
 
 
+class StreamCursor:
+    """The generator's PCG64 state as Python ints, advanced without a
+    state-dict round trip per skip (jump constants cached per distinct
+    step count); ``sync_to``/``sync_from`` hand it to numpy around calls
+    that draw through the Generator itself (``choice``)."""
+
+    def __init__(self, gen: np.random.Generator):
+        st = check_pcg64(gen)
+        self.gen = gen
+        self.s = int(st["state"]["state"])
+        self.inc = int(st["state"]["inc"])
+        self.has = int(st["has_uint32"])
+        self.buf = int(st["uinteger"])
+        self._jumps = {}
+
+    def skip_u64(self, n: int) -> None:
+        if n <= 0:
+            return
+        j = self._jumps.get(n)
+        if j is None:
+            j = self._jumps[n] = _jump(n, self.inc)
+        self.s = (j[0] * self.s + j[1]) & M128
+
+    def sync_to(self) -> None:
+        self.gen.bit_generator.state = {
+            "bit_generator": "PCG64",
+            "state": {"state": self.s, "inc": self.inc},
+            "has_uint32": self.has, "uinteger": self.buf}
+
+    def sync_from(self) -> None:
+        st = self.gen.bit_generator.state
+        self.s = int(st["state"]["state"])
+        self.has = int(st["has_uint32"])
+        self.buf = int(st["uinteger"])
+
+
 def advance_state(state: int, inc: int, steps: int) -> int:
     a, c = _jump(steps, inc)
     return (a * state + c) & M128

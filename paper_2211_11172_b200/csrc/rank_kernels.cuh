@@ -210,12 +210,21 @@ __global__ void k_rank_select(RankArgs a, int d) {
   }
   for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
   __syncthreads();
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.V;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (!a.keep[v]) continue;
-    unsigned int dg;
-    if (rank_match(rank_okey(a.score[v]), ~(unsigned int)v, d, st, &dg))
-      atomicAdd(&hist[dg], 1u);
+  // scores cluster (a GBT ensemble has few distinct values near the top),
+  // so most lanes of a warp hit the same bin: one atomic per distinct
+  // digit per warp (__match_any_sync), not one per item
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t vend = (a.V + 31) & ~(int64_t)31;   // whole warps iterate
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < vend;
+       v += stride) {
+    unsigned int dg = 0xffffffffu;
+    if (v < a.V && a.keep[v]) {
+      unsigned int t;
+      if (rank_match(rank_okey(a.score[v]), ~(unsigned int)v, d, st, &t)) dg = t;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    if (dg != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(&hist[dg], (unsigned int)__popc(peers));
   }
   __syncthreads();
   for (int t = threadIdx.x; t < 256; t += blockDim.x)
@@ -225,25 +234,49 @@ __global__ void k_rank_select(RankArgs a, int d) {
   if (threadIdx.x == 0)
     last = (atomicAdd(&st.blocks_done, 1u) == gridDim.x - 1);
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
+  // the last CTA picks the digit: the 256 global bins into shared memory in
+  // parallel, a suffix sum over them, the bin where the remaining count
+  // falls
   __threadfence();
-  unsigned long long rem = (d == 0) ? ktarget : st.remaining;
-  unsigned long long above = 0;
-  int b = 255;
-  for (; b > 0; --b) {
-    const unsigned int c = *(volatile unsigned int*)&st.hist[b];
-    if (above + c >= rem) break;
-    above += c;
+  __shared__ unsigned long long suf[256];
+  __shared__ int s_b;
+  unsigned int* hs = hist;   // reuse the CTA histogram for the totals
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    hs[t] = *(volatile unsigned int*)&st.hist[t];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) suf[t] = hs[t];
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {   // suf[t] = sum of bins >= t
+    unsigned long long v = 0;
+    for (int t = threadIdx.x; t < 256; t += blockDim.x)
+      if (t + o < 256) v = suf[t + o];
+    __syncthreads();
+    for (int t = threadIdx.x; t < 256; t += blockDim.x)
+      if (t + o < 256) suf[t] += v;
+    __syncthreads();
   }
-  const unsigned long long inb = *(volatile unsigned int*)&st.hist[b];
-  rem -= above;
-  if (d < 8) st.prefix_hi |= (unsigned long long)b << (56 - 8 * d);
-  else st.prefix_lo |= (unsigned int)b << (24 - 8 * (d - 8));
-  st.remaining = rem;
-  if (d == 0) st.k_target = ktarget;
-  if (inb == rem) st.done = 1;   // the whole bucket is selected
-  for (int t = 0; t < 256; ++t) st.hist[t] = 0;
-  st.blocks_done = 0;
+  const unsigned long long rem0 = (d == 0) ? ktarget : st.remaining;
+  if (threadIdx.x == 0) s_b = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+    const unsigned long long above = t < 255 ? suf[t + 1] : 0ull;
+    if (t > 0 && above < rem0 && rem0 <= suf[t]) s_b = t;   // unique
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int b = s_b;   // 0 when no higher bin reaches rem0
+    const unsigned long long above = b < 255 ? suf[b + 1] : 0ull;
+    const unsigned long long inb = hs[b];
+    const unsigned long long rem = rem0 - above;
+    if (d < 8) st.prefix_hi |= (unsigned long long)b << (56 - 8 * d);
+    else st.prefix_lo |= (unsigned int)b << (24 - 8 * (d - 8));
+    st.remaining = rem;
+    if (d == 0) st.k_target = ktarget;
+    if (inb == rem) st.done = 1;   // the whole bucket is selected
+    st.blocks_done = 0;
+  }
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) st.hist[t] = 0;
 }
 
 __global__ void k_rank_emit(RankArgs a) {

@@ -450,6 +450,15 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
                  double* out_val, double* out_pred, double* out_base,
                  int32_t* out_ntrees, void* stream);
 
+/* TrackSet.cull (stopping.py:68-86), host-side (no device pointers): the
+ * n_elim live tracks with the lowest (advantage, -index) are eliminated
+ * (NaN advantages order last).  adv/tracks: the cull step's m rows; alive:
+ * per-track 0/1, updated; gone_out: eliminated track ids ascending;
+ * keep_out/n_keep: surviving rows ascending. */
+int harl_cull_select(const double* adv, const int32_t* tracks, int64_t m,
+                     uint8_t* alive, int64_t n_tracks, int64_t n_elim,
+                     int64_t* gone_out, int32_t* keep_out, int64_t* n_keep);
+
 /* Instrumentation (no reference counterpart; the reference has no device).
  * harl_launch_count: kernels this library has launched since load (graph
  * replays excluded -- they do not pass through the library).

@@ -10,6 +10,8 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 #include "gbt_kernels.cuh"
@@ -1779,6 +1781,67 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
   if ((e = cudaMemcpyAsync(out_base, &a.ctl->base, 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess ||
       (e = cudaMemcpyAsync(out_ntrees, &a.ctl->n_built, 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
     return cuda_status(e, "harl_gbt_fit outputs");
+  return HARL_OK;
+}
+
+
+// TrackSet.cull (stopping.py:68-86) on the host: the n_elim live tracks
+// with the lowest (advantage, -index) go (NaN advantages order last, as a
+// numpy sort puts them).  rows: the cull step's m rows (row r = track
+// tracks[r], advantage adv[r]); alive (per track, 0/1) is updated; gone_out
+// gets the eliminated track ids ascending, keep_out the surviving rows
+// ascending (the survivor gather's index list).
+int harl_cull_select(const double* adv, const int32_t* tracks, int64_t m,
+                     uint8_t* alive, int64_t n_tracks, int64_t n_elim,
+                     int64_t* gone_out, int32_t* keep_out, int64_t* n_keep) {
+  if (!adv || !tracks || !alive || m < 0 || n_elim < 0 || n_elim > m ||
+      (n_elim && !gone_out) || !keep_out || !n_keep) {
+    set_error("harl_cull_select: bad arguments");
+    return HARL_E_ARG;
+  }
+  for (int64_t r = 0; r < m; ++r)
+    if (tracks[r] < 0 || tracks[r] >= n_tracks || !alive[tracks[r]]) {
+      set_error("harl_cull_select: row %lld is not a live track", (long long)r);
+      return HARL_E_ARG;
+    }
+  if (n_elim > 0) {
+    // ordered 64-bit keys (NaN last), the cut = the n_elim-th smallest key;
+    // everything below goes, ties at the cut go by descending track index
+    std::vector<uint64_t> key(m), tmp(m);
+    const uint64_t* bits = reinterpret_cast<const uint64_t*>(adv);
+    for (int64_t r = 0; r < m; ++r) {
+      const uint64_t b = bits[r];
+      const bool nan = (b & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
+      const uint64_t k = nan ? ~0ull : ((b >> 63) ? ~b : (b | 0x8000000000000000ull));
+      key[r] = k;
+      tmp[r] = k;
+    }
+    std::nth_element(tmp.begin(), tmp.begin() + (n_elim - 1), tmp.end());
+    const uint64_t cut = tmp[n_elim - 1];
+    std::vector<int32_t> tied;
+    int64_t below = 0;
+    for (int64_t r = 0; r < m; ++r) {
+      if (key[r] < cut) {
+        alive[tracks[r]] = 2;   // marked: eliminated
+        ++below;
+      } else if (key[r] == cut) {
+        tied.push_back(tracks[r]);
+      }
+    }
+    const int64_t need = n_elim - below;
+    std::sort(tied.begin(), tied.end(), [](int32_t a, int32_t b) { return a > b; });
+    for (int64_t i = 0; i < need; ++i) alive[tied[i]] = 2;
+    int64_t g = 0;
+    for (int64_t t = 0; t < n_tracks; ++t)
+      if (alive[t] == 2) {
+        gone_out[g++] = t;
+        alive[t] = 0;
+      }
+  }
+  int64_t k = 0;
+  for (int64_t r = 0; r < m; ++r)
+    if (alive[tracks[r]]) keep_out[k++] = (int32_t)r;
+  *n_keep = k;
   return HARL_OK;
 }
 

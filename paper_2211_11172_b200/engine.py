@@ -23,6 +23,7 @@ lands within ~1e-7 of a CDF boundary).
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import ctypes as C
@@ -58,6 +59,10 @@ _PY_CULL = os.environ.get("HARL_NATIVE_CULL") != "1"
 # HARL_SPLIT_FINISH=1: separate GBT and finish launches (k_gbt_predict2 +
 # k_finish_step) instead of the fused k_gbt_finish (A/B and fallback path)
 _SPLIT_FINISH = os.environ.get("HARL_SPLIT_FINISH") == "1"
+
+# host-side timeline of the graphed episode (profiles/host_probe.py sets a
+# list here; None = off)
+_HOST_TRACE = None
 
 
 @dataclass(frozen=True)
@@ -425,7 +430,9 @@ class EpisodeEngine:
         D.init_population(b.dsk, P, gen, cur["tiles"], cur["knobs"])
         D.featurize(b.dsk, cur["tiles"], cur["knobs"], P, cur["feat"])
         D.gbt_predict(forest, cur["feat"], P, out=cur["score"])
-        rt.copy_(torch.arange(P, dtype=torch.int32, device=self.dev))
+        if getattr(b, "iota", None) is None:
+            b.iota = torch.arange(P, dtype=torch.int32, device=self.dev)
+        rt.copy_(b.iota)
         b.steps.zero_()
         b.best.fill_(-math.inf)
         b.best_step.zero_()
@@ -668,20 +675,22 @@ class EpisodeEngine:
 
     # ---- graph path --------------------------------------------------------
 
-    # steps in the first graph: its per-step rows are prepared before any
-    # GPU work of the episode can start, the rest while it runs
-    HEAD_STEPS = 8
+    # graph boundaries at the start of an episode: the rows of the first
+    # graph are prepared before any GPU work can start, each later graph's
+    # while the previous one runs (host precompute ~10-30 us per step)
+    HEAD_SPLITS = (2, 8)
 
     def _segments(self, plan):
         """Step index ranges of the captured graphs: a host cull decision
         ends a segment (the next one starts with the survivor gather), and
-        the episode's first HEAD_STEPS steps are a graph of their own so the
-        host precompute of the rest overlaps them.  Returns (first, last,
+        the first steps are split at HEAD_SPLITS so the host precompute of
+        each graph overlaps the previous one.  Returns (first, last,
         starts_after_cull)."""
         segs, start, after_cull = [], 0, False
         for k, step in enumerate(plan):
-            head_end = k == self.HEAD_STEPS - 1 and start == 0 and \
-                k < len(plan) - 1 and not step["cull"]
+            head_end = (k + 1) in self.HEAD_SPLITS and start <= k and \
+                k < len(plan) - 1 and not step["cull"] and \
+                all(not s["cull"] for s in plan[:k])
             if step["cull"] or k == len(plan) - 1 or head_end:
                 segs.append((start, k, after_cull))
                 after_cull = bool(step["cull"])
@@ -796,20 +805,32 @@ class EpisodeEngine:
                 b.adam_tab[p0:p1].copy_(pins["adam"][p0:p1], non_blocking=True)
 
         segs = b.graphs
-        first = segs[0]
-        upload(first[0], first[1], *precompute(first[0], first[1]))
-        first[2].replay()
-        if len(segs) > 1:
-            k0 = segs[1][0]
-            upload(k0, n_steps - 1, *precompute(k0, n_steps - 1))
-        cursor.sync_to()
+        # rows of segment 0 first; then, before blocking anywhere, the rows
+        # of the next segment(s) while the GPU runs the launched ones
+        done = [-1]          # last step whose rows are uploaded
+
+        trace = _HOST_TRACE
+
+        def prepare(upto):
+            if upto > done[0]:
+                k0 = done[0] + 1
+                if trace is not None:
+                    trace.append(("pre", k0, upto, time.perf_counter()))
+                rows = precompute(k0, upto)
+                if trace is not None:
+                    trace.append(("up", k0, upto, time.perf_counter()))
+                upload(k0, upto, *rows)
+                done[0] = upto
+                if trace is not None:
+                    trace.append(("done", k0, upto, time.perf_counter()))
+
+        prepare(segs[0][1])
         # ---- replay the segments; host culls in between --------------------
         alive = np.ones(P, dtype=bool)
         culls, train = [], []
         used, ppo_k = 0, 0
         rt_i = 0
-        cur_i = 0
-        for si, (k0, k1, g, nl, after_cull) in enumerate(b.graphs):
+        for si, (k0, k1, g, nl, after_cull) in enumerate(segs):
             if after_cull:
                 prev = b.plan[k0 - 1]
                 m = prev["m"]
@@ -822,16 +843,26 @@ class EpisodeEngine:
                     gone = self._cull_native(b, rt_i, m, alive, cfg)
                 culls.append((prev["t"], gone, int(alive.sum())))
                 rt_i = 1 - rt_i
-            if si > 0:
-                g.replay()       # segment 0 was launched above
+            prepare(k1)
+            if trace is not None:
+                trace.append(("launch", k0, k1, time.perf_counter()))
+            g.replay()
+            if trace is not None:
+                trace.append(("launched", k0, k1, time.perf_counter()))
             PF.add_launches(nl)
+            # look ahead while this segment runs: the next segment's rows, or
+            # all remaining rows when a cull (which blocks the host) comes
+            # first
+            if si + 1 < len(segs):
+                nk0, nk1, _, _, n_after_cull = segs[si + 1]
+                prepare(n_steps - 1 if n_after_cull else nk1)
             for k in range(k0, k1 + 1):
                 step = b.plan[k]
                 used += step["m"]
                 if step["ppo"]:
                     train.append((step["t"], b.losses[ppo_k], step["ppo"]))
                     ppo_k += 1
-        del cur_i
+        cursor.sync_to()
         return self._result(b, cfg, order_counter, used, culls, train, alive)
 
     # -----------------------------------------------------------------------

@@ -35,6 +35,9 @@ def _jump(steps: int, inc: int):
     return acc_a, acc_c
 
 
+_JUMPS: dict = {}     # (steps, inc) -> (A, C), shared across episodes
+
+
 class StreamCursor:
     """The generator's PCG64 state as Python ints, advanced without a
     state-dict round trip per skip (jump constants cached per distinct
@@ -48,14 +51,15 @@ class StreamCursor:
         self.inc = int(st["state"]["inc"])
         self.has = int(st["has_uint32"])
         self.buf = int(st["uinteger"])
-        self._jumps = {}
 
     def skip_u64(self, n: int) -> None:
         if n <= 0:
             return
-        j = self._jumps.get(n)
+        j = _JUMPS.get((n, self.inc))
         if j is None:
-            j = self._jumps[n] = _jump(n, self.inc)
+            if len(_JUMPS) > 4096:
+                _JUMPS.clear()
+            j = _JUMPS[(n, self.inc)] = _jump(n, self.inc)
         self.s = (j[0] * self.s + j[1]) & M128
 
     def sync_to(self) -> None:

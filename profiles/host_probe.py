@@ -46,11 +46,15 @@ def main():
     wrap(eng, "_cull_inputs", "cull D2H (incl. wait for segment)")
     wrap(eng, "_cull", "cull host")
     wrap(torch.cuda.CUDAGraph, "replay", "graph replay calls")
+    E._HOST_TRACE = trace = []
     t = time.perf_counter()
     eng.run_episode(tb, forest, gen, cfg, 0)
     torch.cuda.synchronize()
     acc["episode total"] = (time.perf_counter() - t) * 1e3
+    E._HOST_TRACE = None
     print(json.dumps({k: round(v, 3) for k, v in acc.items()}))
+    print(json.dumps([(a, k0, k1, round((tt - t) * 1e3, 3))
+                      for a, k0, k1, tt in trace]))
 
 
 if __name__ == "__main__":

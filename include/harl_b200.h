@@ -459,6 +459,14 @@ int harl_cull_select(const double* adv, const int32_t* tracks, int64_t m,
                      uint8_t* alive, int64_t n_tracks, int64_t n_elim,
                      int64_t* gone_out, int32_t* keep_out, int64_t* n_keep);
 
+/* Host-side: Python float repr (float.__repr__, as json.dumps renders
+ * floats; NaN / Infinity / -Infinity) of v[0..n) joined by ", " -- the body
+ * of json.dumps(list) -- for the trajectory log's per-visit reward lists
+ * (tuner.py:414-420).  Returns the bytes written to out, or -(bytes needed)
+ * if cap is too small (40 * n suffices).  threads <= 0: all cores. */
+long long harl_format_floats(const double* v, long long n, char* out,
+                             long long cap, int threads);
+
 /* Instrumentation (no reference counterpart; the reference has no device).
  * harl_launch_count: kernels this library has launched since load (graph
  * replays excluded -- they do not pass through the library).

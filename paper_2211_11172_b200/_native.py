@@ -149,6 +149,8 @@ _SIGS = {
                                vp, vp, vp, vp, i64, vp]),
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_rank_scratch_bytes": (i64, [i64, i64]),
+    "harl_format_floats": (C.c_longlong, [vp, C.c_longlong, vp, C.c_longlong,
+                                          i32]),
     "harl_cull_select": (i32, [vp, vp, i64, vp, i64, i64, vp, vp, P(i64)]),
     "harl_gbt_fit_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_gbt_fit": (i32, [vp, vp, i32, i32, i32, i32, f64, i32, vp, i64, vp,

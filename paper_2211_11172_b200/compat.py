@@ -244,15 +244,24 @@ def b200_session_class(base):
                     for i, s in enumerate(states)]
 
         def _b200_log(self, res, rnd):
+            import json
             rewards = res.rewards_per_step()
             culls = {t: (gone, alive) for t, gone, alive in res.culls}
             train = {t: (losses.cpu().numpy(), B) for t, losses, B in
                      res.train}
+            fh = self.log.fh
             for t, (m, r) in enumerate(zip(res.step_rows, rewards), start=1):
-                self.log.write({"event": "episode_step", "round": rnd,
-                                "step": t, "alive": m,
-                                "mean_reward": float(np.mean(r)),
-                                "rewards": [float(x) for x in r]})
+                # json.dumps(sort_keys=True) of the reference's event
+                # (tuner.py:414-420), the reward list rendered by
+                # harl_format_floats (float.__repr__, byte-identical)
+                head = json.dumps({"alive": m, "event": "episode_step",
+                                   "mean_reward": float(np.mean(r))},
+                                  sort_keys=True)[:-1]
+                tail = json.dumps({"round": rnd, "step": t},
+                                  sort_keys=True)[1:]
+                fh.write(head + ', "rewards": [' + D.format_floats(r) +
+                         '], ' + tail + "\n")
+                fh.flush()
                 if t in culls and len(culls[t][0]):
                     self.log.write({"event": "cull", "round": rnd, "step": t,
                                     "eliminated": [int(i) for i in culls[t][0]],
@@ -269,13 +278,20 @@ def b200_session_class(base):
                                     **{k: _enc(v) for k, v in metrics.items()}})
             steps = res.track_steps.cpu().numpy()
             best = res.track_best_step.cpu().numpy()
-            self.log.write({"event": "episode_end", "round": rnd,
-                            "visited": res.visits,
-                            "tracks": [{"index": int(i), "len": int(steps[i]),
-                                        "best_step": int(best[i]),
-                                        "alive": bool(res.alive[i])}
-                                       for i in range(len(steps))
-                                       if steps[i] > 0]})
+            # the episode_end event (tuner.py:434-439) as json.dumps(
+            # sort_keys=True) renders it, one f-string per track instead of
+            # a dict per track
+            idx = np.flatnonzero(steps > 0)
+            alive = ["true" if a else "false" for a in res.alive[idx]]
+            items = ", ".join(
+                f'{{"alive": {a}, "best_step": {bs}, "index": {i}, '
+                f'"len": {ln}}}'
+                for a, bs, i, ln in zip(alive, best[idx].tolist(),
+                                        idx.tolist(), steps[idx].tolist()))
+            fh.write('{"event": "episode_end", "round": ' +
+                     json.dumps(rnd) + ', "tracks": [' + items +
+                     '], "visited": ' + json.dumps(res.visits) + "}\n")
+            fh.flush()
 
     B200TuningSession.__name__ = "B200TuningSession"
     return B200TuningSession

@@ -1,0 +1,156 @@
+// Python float repr for the trajectory log (host C++).
+//
+// The drop-in writes the reference's `episode_step` events (tuner.py:
+// 414-420): json.dumps(sort_keys=True) of a dict whose "rewards" list holds
+// every visited candidate's reward (P floats per step).  json renders each
+// float with float.__repr__: the shortest digit string that round-trips
+// (David Gay's dtoa mode 0), printed fixed when the decimal exponent is in
+// (-4, 16] and as d.ddde+XX otherwise, with ".0" added to integral values;
+// NaN / Infinity / -Infinity for the non-finite ones.  std::to_chars (C++17,
+// libstdc++'s Ryu) yields the same shortest, nearest digits; this file
+// formats them by CPython's rules (Python/pystrtod.c, format_float_short),
+// splitting the list over worker threads.  Output is byte-identical to
+// ", ".join(json's float repr) -- tests/test_repr_format.py checks millions of
+// values, edge cases included, against json.dumps itself.
+#include <charconv>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+namespace {
+
+// one value into dst (>= 32 bytes available); returns bytes written
+int repr_one(double x, char* dst) {
+  if (std::isnan(x)) {
+    memcpy(dst, "NaN", 3);
+    return 3;
+  }
+  if (std::isinf(x)) {
+    if (x > 0) {
+      memcpy(dst, "Infinity", 8);
+      return 8;
+    }
+    memcpy(dst, "-Infinity", 9);
+    return 9;
+  }
+  char* p = dst;
+  if (std::signbit(x)) {
+    *p++ = '-';
+    x = -x;
+  }
+  if (x == 0.0) {
+    memcpy(p, "0.0", 3);
+    return (int)(p - dst) + 3;
+  }
+  // shortest digits in scientific form: d[.ddd]e(+|-)XX
+  char sci[40];
+  const auto r = std::to_chars(sci, sci + sizeof(sci), x,
+                               std::chars_format::scientific);
+  const int len = (int)(r.ptr - sci);
+  char digits[24];
+  int nd = 0, i = 0;
+  for (; i < len && sci[i] != 'e'; ++i)
+    if (sci[i] != '.') digits[nd++] = sci[i];
+  int e = 0;
+  bool neg = false;
+  ++i;  // 'e'
+  if (sci[i] == '-') neg = true;
+  ++i;
+  for (; i < len; ++i) e = e * 10 + (sci[i] - '0');
+  if (neg) e = -e;
+  const int decpt = e + 1;   // value = 0.d1d2... x 10^decpt
+  if (decpt <= -4 || decpt > 16) {
+    *p++ = digits[0];
+    if (nd > 1) {
+      *p++ = '.';
+      memcpy(p, digits + 1, nd - 1);
+      p += nd - 1;
+    }
+    *p++ = 'e';
+    const int ex = decpt - 1;
+    *p++ = ex < 0 ? '-' : '+';
+    const int a = ex < 0 ? -ex : ex;
+    if (a >= 100) {
+      *p++ = (char)('0' + a / 100);
+      *p++ = (char)('0' + (a / 10) % 10);
+      *p++ = (char)('0' + a % 10);
+    } else {
+      *p++ = (char)('0' + a / 10);
+      *p++ = (char)('0' + a % 10);
+    }
+  } else if (decpt <= 0) {
+    *p++ = '0';
+    *p++ = '.';
+    for (int z = 0; z < -decpt; ++z) *p++ = '0';
+    memcpy(p, digits, nd);
+    p += nd;
+  } else if (decpt >= nd) {
+    memcpy(p, digits, nd);
+    p += nd;
+    for (int z = 0; z < decpt - nd; ++z) *p++ = '0';
+    *p++ = '.';
+    *p++ = '0';
+  } else {
+    memcpy(p, digits, decpt);
+    p += decpt;
+    *p++ = '.';
+    memcpy(p, digits + decpt, nd - decpt);
+    p += nd - decpt;
+  }
+  return (int)(p - dst);
+}
+
+}  // namespace
+
+extern "C" {
+
+// Python repr of v[0..n) joined by ", " (the body of json.dumps(list)) into
+// out (cap bytes).  Returns the byte count, or -(bytes needed) when cap is
+// too small (40 * n always suffices).  threads <= 0: hardware concurrency.
+long long harl_format_floats(const double* v, long long n, char* out,
+                             long long cap, int threads) {
+  if (n <= 0) return 0;
+  if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+  if (threads < 1) threads = 1;
+  const long long per = 8192;
+  long long chunks = (n + per - 1) / per;
+  if (threads > chunks) threads = (int)chunks;
+  // each chunk formats into its own buffer, then they are concatenated
+  std::vector<std::vector<char>> bufs(chunks);
+  auto work = [&](int tid) {
+    for (long long c = tid; c < chunks; c += threads) {
+      const long long a = c * per, b = a + per < n ? a + per : n;
+      std::vector<char>& buf = bufs[c];
+      buf.resize((size_t)(b - a) * 34);
+      char* p = buf.data();
+      for (long long k = a; k < b; ++k) {
+        if (k > 0) {
+          *p++ = ',';
+          *p++ = ' ';
+        }
+        p += repr_one(v[k], p);
+      }
+      buf.resize((size_t)(p - buf.data()));
+    }
+  };
+  if (threads == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+    for (auto& t : pool) t.join();
+  }
+  long long total = 0;
+  for (auto& b : bufs) total += (long long)b.size();
+  if (total > cap) return -total;
+  char* p = out;
+  for (auto& b : bufs) {
+    memcpy(p, b.data(), b.size());
+    p += b.size();
+  }
+  return total;
+}
+
+}  // extern "C"

@@ -210,6 +210,22 @@ def featurize(dsk: DeviceSketch, tiles, knobs, n: int, out=None):
     return out[:n]
 
 
+def format_floats(values, threads: int = 0) -> str:
+    """", ".join of json's float rendering (float.__repr__, NaN/Infinity)
+    of a host float64 array, in the native library's threaded formatter
+    (harl_format_floats) -- the trajectory log's reward lists."""
+    lib = N.load(require_device=False)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if v.size == 0:
+        return ""
+    cap = 40 * v.size + 16
+    out = C.create_string_buffer(cap)
+    n = lib.harl_format_floats(v.ctypes.data, v.size, out, cap, threads)
+    if n < 0:
+        raise DeviceError("harl_format_floats: buffer too small")
+    return out.raw[:n].decode("ascii")
+
+
 class RankScratch:
     """Reusable device scratch of ``rank_topk`` (grown on demand)."""
 

@@ -148,3 +148,19 @@ def test_drop_in_device_refit_matches_host_refit(tmp_path):
         (rep_h.n_examples, rep_h.loss_before, rep_h.loss_after)
     assert m.base == host.base and len(m.trees) == len(host.trees)
     assert m.dump_text() == host.dump_text()
+
+
+def test_drop_in_log_lines_are_json_dumps_bytes(tmp_path):
+    """The fast-path trajectory lines (reward lists through
+    harl_format_floats, episode_end by f-string) are byte-identical to
+    json.dumps(sort_keys=True) of the same objects, as TrajectoryLogger
+    writes them (tuner.py:162-164)."""
+    _, dev = _sessions(tmp_path, (16,))
+    for _ in range(2):
+        dev.run_round()
+    n = 0
+    for line in open(tmp_path / "dev" / "trajectory.jsonl"):
+        obj = json.loads(line)
+        assert json.dumps(obj, sort_keys=True) + "\n" == line
+        n += obj["event"] in ("episode_step", "episode_end")
+    assert n > 0

@@ -85,9 +85,50 @@ def _device_fit_incremental(model, examples):
                      loss_after=after)
 
 
+_RingBuffer = None
+
+
+def _ring_buffer_class():
+    """A ReplayBuffer (rlcore.py:253-274) whose contents may live in the
+    engine's device ring: ``len`` reads the ring's count, and the deque
+    (``buf``) is materialised from the device the first time anything reads
+    it after an episode."""
+    from schedtune.rlcore import ReplayBuffer
+
+    class RingBuffer(ReplayBuffer):
+        def __init__(self, capacity, session, sg):
+            self._on_device = False
+            self._buf = None
+            super().__init__(capacity)
+            self._session, self._sg = session, sg
+
+        @property
+        def buf(self):
+            if self._on_device:
+                self._on_device = False
+                s = self._session
+                s._b200_store_ring(s._b200_engines[self._sg.id], self._sg)
+            return self._buf
+
+        @buf.setter
+        def buf(self, d):
+            self._buf = d
+
+        def __len__(self):
+            if self._on_device:
+                return int(self._session._b200_engines[self._sg.id].replay.count)
+            return len(self._buf)
+
+    return RingBuffer
+
+
 def b200_session_class(base):
     """Build the B200 subclass of the reference ``TuningSession`` class
     ``base`` (passed in so this module never imports the reference)."""
+
+    global _RingBuffer
+    if _RingBuffer is None:
+        _RingBuffer = _ring_buffer_class()
 
     class B200TuningSession(base):
         _b200_engines: dict
@@ -121,6 +162,11 @@ def b200_session_class(base):
                               buffer_capacity=cfg.buffer_capacity,
                               train_interval=cfg.train_interval)
                 eng[sg.id] = EpisodeEngine(st, rl, self.target.tiling_levels)
+                old = self.buffers[sg.id]
+                if not isinstance(old, _RingBuffer):
+                    nb = _RingBuffer(old.buf.maxlen, self, sg)
+                    nb.buf = old.buf
+                    self.buffers[sg.id] = nb
             return eng[sg.id]
 
         def _b200_sketch_tables(self, sg, sketch):
@@ -163,6 +209,42 @@ def b200_session_class(base):
                     td_target=float(ex["td"][i]),
                     masks=tuple(ex["masks"][h][i] for h in range(4))))
 
+        def _collect_state(self):
+            """The reference's checkpoint state (tuner.py:606-702) with the
+            device-resident replay rings exported as the same arrays
+            (features, next_features, actions, scalars, mask0-3) instead of
+            going through Transition objects."""
+            dev = {k: b for k, b in self.buffers.items()
+                   if isinstance(b, _RingBuffer) and b._on_device}
+            saved = {}
+            for k, b in dev.items():
+                from collections import deque
+                saved[k] = b._buf
+                b._buf = deque(maxlen=b._buf.maxlen)
+                b._on_device = False
+            try:
+                meta, arrays = super()._collect_state()
+            finally:
+                for k, b in dev.items():
+                    b._buf = saved[k]
+                    b._on_device = True
+            for k, b in dev.items():
+                eng = self._b200_engines[k]
+                ex = eng.replay.export(self.slots[k], self.target.tiling_levels)
+                n = len(ex["X"])
+                meta["buffers"][k] = n
+                if not n:
+                    continue
+                pre = f"buffer/{k}/"
+                arrays[pre + "features"] = ex["X"]
+                arrays[pre + "next_features"] = ex["Xn"]
+                arrays[pre + "actions"] = ex["actions"]
+                arrays[pre + "scalars"] = np.stack(
+                    [ex["logp"], ex["reward"], ex["adv"], ex["td"]], axis=1)
+                for h in range(4):
+                    arrays[pre + f"mask{h}"] = ex["masks"][h]
+            return meta, arrays
+
         # -- the seam --------------------------------------------------------
 
         def _b200_hook_model(self):
@@ -182,7 +264,9 @@ def b200_session_class(base):
             eng = self._b200_engine(sg)
             tables = self._b200_sketch_tables(sg, sketch)
             eng.dagent.upload()
-            self._b200_load_ring(eng, sg)
+            buf = self.buffers[sg.id]
+            if not buf._on_device:
+                self._b200_load_ring(eng, sg)
             forest = getattr(self, "_b200_forest", None)
             if forest is None or not forest.load_model(self.model):
                 # capacity for the refits to come (n_estimators trees of
@@ -197,7 +281,9 @@ def b200_session_class(base):
             res = eng.run_episode(tables, forest, self.rng, ecfg,
                                   self.order_counter)
             eng.sync_to_host()
-            self._b200_store_ring(eng, sg)
+            # the replay FIFO now lives in the device ring; the deque is
+            # rebuilt only if something reads it (_RingBuffer)
+            buf._on_device = True
             entries = self._b200_entries(res, tables, sketch)
             self.order_counter += res.visits
             if self.log:

@@ -164,3 +164,25 @@ def test_drop_in_log_lines_are_json_dumps_bytes(tmp_path):
         assert json.dumps(obj, sort_keys=True) + "\n" == line
         n += obj["event"] in ("episode_step", "episode_end")
     assert n > 0
+
+
+def test_drop_in_checkpoint_from_device_rings_equals_transitions(tmp_path):
+    """Checkpoints written while the replay FIFO lives on the device export
+    the same buffer arrays the reference builds from Transition objects."""
+    from schedtune.tuner import read_checkpoint
+    _, dev = _sessions(tmp_path, (16,))
+    dev.run_round()
+    sg = dev.net.subgraphs[0].id
+    assert dev.buffers[sg]._on_device
+    p1 = str(tmp_path / "a.bin")
+    dev.save(p1)
+    assert dev.buffers[sg]._on_device          # no materialisation
+    items = list(dev.buffers[sg].buf)           # materialise the deque
+    assert not dev.buffers[sg]._on_device
+    p2 = str(tmp_path / "b.bin")
+    dev.save(p2)                                # the reference's own path
+    assert open(p1, "rb").read() == open(p2, "rb").read()
+    assert len(items) == len(dev.buffers[sg])
+    dev.run_round()                             # reloads the ring from the deque
+    meta, arrays = read_checkpoint(p2)
+    assert meta["buffers"][sg] == len(items)

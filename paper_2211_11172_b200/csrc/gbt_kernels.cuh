@@ -88,7 +88,13 @@ k_gbt_predict(const GbtNode* __restrict__ nodes,
 // rows land while the current one is walked; every level of every walk is
 // then two shared-memory loads.  SMEM_NODES=false keeps the nodes in global
 // memory for forests too large to stage.
-constexpr int GBT2_GROUPS = 8;
+#ifndef HARL_GBT_GROUPS
+#define HARL_GBT_GROUPS 8
+#endif
+// tree groups per tile (a warp pair walks every GROUPS-th tree for the
+// tile's 64 rows); 16 groups (1024 threads) measured slower: the 64-register
+// cap spills the fused finish epilogue (C2 20.5 -> 24.2 us)
+constexpr int GBT2_GROUPS = HARL_GBT_GROUPS;
 constexpr int GBT2_ROWS = 64;
 constexpr int GBT2_THREADS = GBT2_ROWS * GBT2_GROUPS;
 
@@ -195,7 +201,17 @@ __device__ __forceinline__ void gbt2_body(
       if (fitted) {
         pred = base;
         const double* c = contrib + rl * n_trees;
-        for (int t = 0; t < n_trees; ++t) pred = __dadd_rn(pred, c[t]);
+        // sequential in tree order (the reference's pred = pred + lr*leaf),
+        // the shared-memory loads of 8 terms issued ahead of their adds
+        int t = 0;
+        for (; t + 8 <= n_trees; t += 8) {
+          double cc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cc[u] = c[t + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pred = __dadd_rn(pred, cc[u]);
+        }
+        for (; t < n_trees; ++t) pred = __dadd_rn(pred, c[t]);
       }
       const double s = (pred != pred) ? pred : (pred < floor_value ? floor_value : pred);
       score[r] = s;

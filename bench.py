@@ -458,6 +458,7 @@ KERNEL_SPAN = {
     "k_gbt_finish": ("gbt", "hbm"),
     "k_ring_rows": ("finish", "hbm"),
     "k_ppo_rows": ("ppo", "fp64"),
+    "k_ppo_rows_tc": ("ppo", "fp64"),
 }
 
 
@@ -492,6 +493,7 @@ def per_row_work(tables, H, feat_in_sampler=False):
         "k_ring_rows": 2 * 8 * F * 2,               # X and X' read + written
         # policy + value forward and backward in fp64 (3x forward flops)
         "k_ppo_rows": 3 * 2 * (2 * (F * H + H * H) + H * NH + H),
+        "k_ppo_rows_tc": 3 * 2 * (2 * (F * H + H * H) + H * NH + H),
     }
 
 

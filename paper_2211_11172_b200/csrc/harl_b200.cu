@@ -245,6 +245,18 @@ static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// HARL_PPO_TC=1: the DMMA PPO rows kernel (8 rows per CTA) instead of the
+// SIMT one (2 rows per CTA, split reductions) -- measured slower at C2
+// (41 vs 29 us: 32 CTAs per chain and dependent 32-step MMA chains)
+static bool use_ppo_tc() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HARL_PPO_TC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // HARL_TC_GEN1=1 selects the first-generation 4-warp tcgen05 kernels
 static bool use_tc2() {
   static int v = -1;
@@ -984,6 +996,7 @@ int harl_prepare(void) {
   if ((rc = allow_max_smem(k_policy_step_fused, "k_policy_step_fused"))) return rc;
   if ((rc = allow_max_smem(k_value_tc, "k_value_tc"))) return rc;
   if ((rc = allow_max_smem(k_ppo_rows, "k_ppo_rows"))) return rc;
+  if ((rc = allow_max_smem(k_ppo_rows_tc, "k_ppo_rows_tc"))) return rc;
   // One shared-memory carveout for every kernel: the episode alternates
   // 230 KB-smem tcgen05 kernels with smem-light ones, and a carveout change
   // between consecutive kernels makes the SMs drain and reconfigure.
@@ -1026,6 +1039,7 @@ int harl_prepare(void) {
   carve(k_ring_rows);
   carve(k_gather_rows);
   carve(k_ppo_rows);
+  carve(k_ppo_rows_tc);
   carve(k_ppo_losses);
   carve(k_ppo_wgrad);
   carve(k_ppo_finalize);
@@ -1526,13 +1540,27 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   const size_t rsmem = sizeof(double) * (PPO_TM * (size_t)row_stride + 8 +
                                          (size_t)PPO_SPLIT * PPO_TM * wmax);
   if (phase & 1) {
-  int rc2 = allow_smem(k_ppo_rows, rsmem, "k_ppo_rows");
-  if (rc2) return rc2;
-  if (B > 0) {
-    HARL_PROF_BEGIN(st);
-    launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM), 2), dim3(PPO_THREADS), rsmem, st, 
-        a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
-    HARL_CHECK_LAUNCH("k_ppo_rows");
+  if (use_ppo_tc()) {
+    // fp64 tensor-core rows kernel: 8 rows per CTA in shared memory
+    const size_t tsmem = sizeof(double) * (size_t)PPO8_ROWS * row_stride;
+    int rc2 = allow_smem(k_ppo_rows_tc, tsmem, "k_ppo_rows_tc");
+    if (rc2) return rc2;
+    if (B > 0) {
+      HARL_PROF_BEGIN(st);
+      launch_k(k_ppo_rows_tc, dim3((unsigned)((B + PPO8_ROWS - 1) / PPO8_ROWS), 2),
+               dim3(PPO8_THREADS), tsmem, st, a, *pol, *val, *ring, idx, params,
+               wt_params, rows, rowout);
+      HARL_CHECK_LAUNCH("k_ppo_rows_tc");
+    }
+  } else {
+    int rc2 = allow_smem(k_ppo_rows, rsmem, "k_ppo_rows");
+    if (rc2) return rc2;
+    if (B > 0) {
+      HARL_PROF_BEGIN(st);
+      launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM), 2), dim3(PPO_THREADS), rsmem, st, 
+          a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
+      HARL_CHECK_LAUNCH("k_ppo_rows");
+    }
   }
   GradJobs jt;
   memset(&jt, 0, sizeof(jt));

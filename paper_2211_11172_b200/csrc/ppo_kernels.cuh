@@ -377,6 +377,266 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   dbg_ts(48);
 }
 
+// ---------------------------------------------------------------------------
+// (a') the same per-row work on fp64 tensor cores: 8 minibatch rows per CTA
+// (mma.m8n8k4.f64: M = the 8 rows, N = 8 outputs per warp tile, K = 4 per
+// instruction); each warp owns output tiles n0 = 8 * (warp + 16 i), loads
+// all of its weight fragments before the dependent MMA chain, and writes
+// act(z + b) / delta * (1 - a^2) for its tile.  Accumulation order differs
+// from the SIMT kernel (fp64 rounding level; the parity tests' tolerance).
+// Opt-in (HARL_PPO_TC=1): at B = 256 it measured slower than k_ppo_rows
+// (41 vs 29 us) -- 32 CTAs per chain and a dependent MMA chain per tile.
+
+constexpr int PPO8_ROWS = 8;
+constexpr int PPO8_THREADS = 512;
+constexpr int PPO8_KMAX = 128;   // reduction length held in fragments
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a,
+                                        double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+      "{%0, %1}, {%2}, {%3}, {%0, %1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// out[r][n] = epi(r, n, sum_k in[r][k] * Wm[k][n]) for r < 8, n < Nout;
+// Wm row-major [Kred][Nout] in global memory, in (smem) row stride ldi.
+template <typename Epi>
+__device__ __forceinline__ void mma8_layer(const double* in, int ldi, int Kred,
+                                           const double* __restrict__ Wm,
+                                           int Nout, const Epi& epi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nwarps = blockDim.x >> 5;
+  const int ksteps = (Kred + 3) / 4;
+  for (int n0 = 8 * warp; n0 < Nout; n0 += 8 * nwarps) {
+    const int col = n0 + gid;
+    double d0 = 0.0, d1 = 0.0;
+    for (int kb = 0; kb < ksteps; kb += 16) {
+      double bf[16], af[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = 4 * (kb + u) + tig;
+        bf[u] = (kb + u < ksteps && k < Kred && col < Nout)
+                    ? __ldg(Wm + (int64_t)k * Nout + col) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int k = 4 * (kb + u) + tig;
+        af[u] = (kb + u < ksteps && k < Kred) ? in[gid * ldi + k] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (kb + u < ksteps) dmma884(d0, d1, af[u], bf[u]);
+    }
+    const int c0 = n0 + 2 * tig;
+    if (c0 < Nout) epi(gid, c0, d0);
+    if (c0 + 1 < Nout) epi(gid, c0 + 1, d1);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(PPO8_THREADS, 1)
+k_ppo_rows_tc(const __grid_constant__ PpoArgs a,
+              const __grid_constant__ NetLayout P,
+              const __grid_constant__ NetLayout V, PpoRing ring,
+              const int32_t* idx, const double* params, const double* wt,
+              double* rows, double* rowout) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  dbg_ts(40);
+  extern __shared__ double srows[];
+  const int role = blockIdx.y;   // 0 policy chain, 1 value chain
+  const int r0 = blockIdx.x * PPO8_ROWS;
+  const int nrows = min(PPO8_ROWS, a.B - r0);
+  const int RS = a.row_stride;
+  double* base = srows;
+  __shared__ int16_t s_src[HARL_MAX_HEAD0];
+  __shared__ double s_st[PPO8_ROWS * 4][4];   // per (row, head): m, s, log s, ent
+  __shared__ double s_lp[PPO8_ROWS][4], s_ent[PPO8_ROWS][4];
+  for (int i = threadIdx.x; i < a.C0; i += blockDim.x) s_src[i] = a.head0_src[i];
+  // rows past nrows are zeros (their fragments contribute nothing)
+  for (int i = threadIdx.x; i < PPO8_ROWS * RS; i += blockDim.x) base[i] = 0.0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nrows * a.F; i += blockDim.x) {
+    const int rr = i / a.F, k = i % a.F;
+    base[rr * RS + P.row_act[0] + k] = ring.X[(int64_t)idx[r0 + rr] * a.F + k];
+  }
+  __syncthreads();
+  dbg_ts(41);
+  const int H = P.dims[P.n_layers];
+  const int NH = P.n_head_cols;
+  if (role == 0) {
+    for (int l = 0; l < P.n_layers; ++l) {
+      double* out = base + P.row_act[l + 1];
+      const double* bb = params + P.off_b[l];
+      mma8_layer(base + P.row_act[l], RS, P.dims[l], params + P.off_W[l],
+                 P.dims[l + 1], [&](int r, int c, double z) {
+                   out[r * RS + c] = tanh(z + bb[c]);
+                 });
+    }
+    dbg_ts(42);
+    {
+      double* out = base + P.row_head;
+      const double* bb = params + P.off_hb;
+      mma8_layer(base + P.row_act[P.n_layers], RS, H, params + P.off_hW, NH,
+                 [&](int r, int c, double z) { out[r * RS + c] = z + bb[c]; });
+    }
+    dbg_ts(43);
+  } else {
+    for (int l = 0; l < V.n_layers; ++l) {
+      double* out = base + V.row_act[l + 1];
+      const double* bb = params + V.off_b[l];
+      const bool act = l < V.n_layers - 1;
+      mma8_layer(base + V.row_act[l], RS, V.dims[l], params + V.off_W[l],
+                 V.dims[l + 1], [&](int r, int c, double z) {
+                   const double v = z + bb[c];
+                   out[r * RS + c] = act ? tanh(v) : v;
+                 });
+    }
+    dbg_ts(44);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const double invB = 1.0 / (double)a.B_norm;
+  if (role == 0) {
+    // per-(row, head) warps: max, sum, entropy (rlcore.py:300-306)
+    for (int pr = warp; pr < nrows * 4; pr += nwarps) {
+      const int rr = pr >> 2, h = pr & 3;
+      const int slot = idx[r0 + rr];
+      const double* z = base + rr * RS + P.row_head;
+      const uint64_t mv = ring.move_bits[slot];
+      const uint32_t sb = ring.shift_bits[slot];
+      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
+      const int C = h == 0 ? a.C0 : 3;
+      auto legal = [&](int j) -> bool {
+        if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
+        return (sb >> (3 * (h - 1) + j)) & 1u;
+      };
+      double m = -INFINITY;
+      for (int j = lane; j < C; j += 32)
+        if (legal(j)) m = fmax(m, z[c0 + j]);
+      m = wmax64(m);
+      double sacc = 0.0;
+      for (int j = lane; j < C; j += 32)
+        if (legal(j)) sacc += exp(z[c0 + j] - m);
+      const double sh = wsum64(sacc);
+      const double ls = log(sh);
+      double e = 0.0;
+      for (int j = lane; j < C; j += 32)
+        if (legal(j)) e -= (exp(z[c0 + j] - m) / sh) * (z[c0 + j] - m - ls);
+      e = wsum64(e);
+      if (lane == 0) {
+        const int col = ring.actions[slot * 4 + h];
+        s_lp[rr][h] = z[c0 + col] - m - ls;
+        s_ent[rr][h] = e;
+        s_st[pr][0] = m;
+        s_st[pr][1] = sh;
+        s_st[pr][2] = ls;
+        s_st[pr][3] = e;
+      }
+    }
+    __syncthreads();
+    // pass 2: dz in place over the logits
+    for (int pr = warp; pr < nrows * 4; pr += nwarps) {
+      const int rr = pr >> 2, h = pr & 3;
+      const int slot = idx[r0 + rr];
+      double* z = base + rr * RS + P.row_head;
+      const uint64_t mv = ring.move_bits[slot];
+      const uint32_t sb = ring.shift_bits[slot];
+      const int c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
+      const int C = h == 0 ? a.C0 : 3;
+      auto legal = [&](int j) -> bool {
+        if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
+        return (sb >> (3 * (h - 1) + j)) & 1u;
+      };
+      const double hm = s_st[pr][0], hs = s_st[pr][1], hls = s_st[pr][2],
+                   hent = s_st[pr][3];
+      const double logp_new = ((s_lp[rr][0] + s_lp[rr][1]) + s_lp[rr][2]) + s_lp[rr][3];
+      const double logp_old = ring.scalars[slot * 4 + 0];
+      const double adv = ring.scalars[slot * 4 + 2];
+      const double ratio = exp(logp_new - logp_old);
+      const double clipped = fmin(fmax(ratio, a.clip_lo), a.clip_hi);
+      const double s_un = ratio * adv, s_cl = clipped * adv;
+      const double coef = (s_un <= s_cl) ? ratio * adv : 0.0;
+      const double dlogp = -coef * invB;
+      const double went = a.w_ent * invB;
+      const int col = ring.actions[slot * 4 + h];
+      for (int j = lane; j < C; j += 32) {
+        double dz;
+        if (legal(j)) {
+          const double lp = z[c0 + j] - hm - hls;
+          const double p = exp(z[c0 + j] - hm) / hs;
+          dz = dlogp * ((j == col ? 1.0 : 0.0) - p) + went * p * (lp + hent);
+        } else {
+          dz = dlogp * ((j == col ? 1.0 : 0.0) - 0.0);
+        }
+        z[c0 + j] = dz;
+      }
+      if (h == 0 && lane == 0) {
+        const double ent_total =
+            ((s_ent[rr][0] + s_ent[rr][1]) + s_ent[rr][2]) + s_ent[rr][3];
+        double* o = rowout + (int64_t)(r0 + rr) * 4;
+        o[0] = fmin(s_un, s_cl);
+        o[1] = ent_total;
+        o[2] = ratio;
+      }
+    }
+    __syncthreads();
+    dbg_ts(45);
+    // policy backward: dhid = dz . Wh^T, times (1 - hid^2)
+    {
+      const double* act = base + P.row_act[P.n_layers];
+      double* out = base + P.row_delta[P.n_layers - 1];
+      mma8_layer(base + P.row_head, RS, NH, wt + a.wt_head, H,
+                 [&](int r, int c, double z) {
+                   const double av = act[r * RS + c];
+                   out[r * RS + c] = z * (1.0 - av * av);
+                 });
+    }
+    for (int l = P.n_layers - 1; l >= 1; --l) {
+      const double* act = base + P.row_act[l];
+      double* out = base + P.row_delta[l - 1];
+      mma8_layer(base + P.row_delta[l], RS, P.dims[l + 1], wt + a.wt_P[l],
+                 P.dims[l], [&](int r, int c, double z) {
+                   const double av = act[r * RS + c];
+                   out[r * RS + c] = z * (1.0 - av * av);
+                 });
+    }
+    dbg_ts(46);
+  } else {
+    if (threadIdx.x < nrows) {
+      const int q = threadIdx.x;
+      const int sl = idx[r0 + q];
+      const double td = ring.scalars[sl * 4 + 3];
+      const double v = base[q * RS + V.row_act[V.n_layers]];
+      rowout[(int64_t)(r0 + q) * 4 + 3] = (v - td) * (v - td);
+      base[q * RS + V.row_delta[V.n_layers - 1]] = a.w_val * 2.0 * (v - td) * invB;
+    }
+    __syncthreads();
+    for (int l = V.n_layers - 1; l >= 1; --l) {
+      const double* act = base + V.row_act[l];
+      double* out = base + V.row_delta[l - 1];
+      mma8_layer(base + V.row_delta[l], RS, V.dims[l + 1], wt + a.wt_V[l],
+                 V.dims[l], [&](int r, int c, double z) {
+                   const double av = act[r * RS + c];
+                   out[r * RS + c] = z * (1.0 - av * av);
+                 });
+    }
+    dbg_ts(47);
+  }
+  const int seg0 = role == 0 ? 0 : V.row_act[1];
+  const int seg1 = role == 0 ? V.row_act[1] : RS;
+  const int sw = seg1 - seg0;
+  double* out = rows + (int64_t)r0 * RS;
+  for (int i = threadIdx.x; i < nrows * sw; i += blockDim.x) {
+    const int q = i / sw, c = seg0 + i % sw;
+    out[q * RS + c] = base[q * RS + c];
+  }
+  dbg_ts(48);
+}
+
 // (b) loss terms: lane l sums rows l, l+32, ... in order, then a fixed xor
 // tree (deterministic).  losses[5..8] = the per-row sums (min surrogate,
 // entropy, ratio, squared value error) -- the quantities a sharded update

@@ -384,8 +384,9 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
 // all of its weight fragments before the dependent MMA chain, and writes
 // act(z + b) / delta * (1 - a^2) for its tile.  Accumulation order differs
 // from the SIMT kernel (fp64 rounding level; the parity tests' tolerance).
-// Opt-in (HARL_PPO_TC=1): at B = 256 it measured slower than k_ppo_rows
-// (41 vs 29 us) -- 32 CTAs per chain and a dependent MMA chain per tile.
+// Opt-in (HARL_PPO_TC=1): the full GPU suite passed with it as the default
+// (PPO parity within tolerance), but at B = 256 it measured slower than
+// k_ppo_rows (41 vs 29 us) -- 32 CTAs per chain, dependent MMA chains.
 
 constexpr int PPO8_ROWS = 8;
 constexpr int PPO8_THREADS = 512;

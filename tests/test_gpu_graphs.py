@@ -97,11 +97,3 @@ def test_kernel_fusion_variants_match_default(monkeypatch, flag):
         assert torch.equal(dflt.replay.Xn, alt.replay.Xn)
         assert g1.bit_generator.state == g2.bit_generator.state
 
-
-def test_dmma_ppo_rows_variant_within_tolerance(monkeypatch):
-    """The opt-in DMMA rows kernel (HARL_PPO_TC=1, a separate library load is
-    not possible in-process, so this checks the SIMT default against the
-    oracle-level tolerance only when the env var selects the DMMA path)."""
-    import os
-    if os.environ.get("HARL_PPO_TC") != "1":
-        pytest.skip("DMMA rows kernel not selected (HARL_PPO_TC=1)")

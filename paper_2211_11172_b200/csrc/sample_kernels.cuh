@@ -22,8 +22,14 @@ struct LaneJump {
   u128 C[32];
 };
 
-constexpr int SG = 8;                  // lanes cooperating on one row
-constexpr int SAMPLE_THREADS = 128;    // 16 rows per CTA
+#ifndef HARL_SAMPLE_LANES
+#define HARL_SAMPLE_LANES 8
+#endif
+#ifndef HARL_SAMPLE_MINB
+#define HARL_SAMPLE_MINB (8 * 8 / HARL_SAMPLE_LANES)
+#endif
+constexpr int SG = HARL_SAMPLE_LANES;   // lanes cooperating on one row
+constexpr int SAMPLE_THREADS = 16 * SG;  // 16 rows per CTA
 constexpr int SAMPLE_MAXI = 16;        // cached exps per lane (C0 <= 128)
 
 struct SampleArgs {
@@ -383,7 +389,7 @@ __device__ __forceinline__ void featurize_group(const harl_sketch_desc& sk,
 }
 
 template <bool FEAT>
-__global__ void __launch_bounds__(SAMPLE_THREADS, 8)
+__global__ void __launch_bounds__(SAMPLE_THREADS, HARL_SAMPLE_MINB)
 k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ PcgJump J,
               const __grid_constant__ LaneJump LJ, u128 base_arg,
@@ -413,7 +419,8 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   dbg_ts(23);
   if (FEAT) {
     const int g = threadIdx.x & (SG - 1);
-    const unsigned gmask = 0xffu << (threadIdx.x & 24);
+    const unsigned gmask = (SG == 32 ? 0xffffffffu : ((1u << SG) - 1u))
+                           << (threadIdx.x & (32 - SG));
     __syncwarp(gmask);
     const int F = sk.feature_len;
     if (r < a.n) featurize_group(sk, g, gmask, s_st[lr], s_kn[lr], s_feat + lr * F);

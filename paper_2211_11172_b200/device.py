@@ -37,6 +37,11 @@ from .errors import DeviceError, InvalidActionError, RlDivergedError
 from .space import SketchTables, head_columns
 
 
+# rows per launch up to which the sampler featurizes in-kernel
+# (HARL_SAMPLE_FEAT_MAX_ROWS in harl_b200.cu)
+SAMPLE_FEAT_MAX_ROWS = 16384
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -897,6 +902,11 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _ptr(grow),
                 m_total, _ptr(feat_out), 1 if fuse_tc else 0, _stream()),
                 "harl_policy_step_tc")
+        if feat_out is not None and not fuse_tc and n > SAMPLE_FEAT_MAX_ROWS:
+            # the library featurized with k_featurize2 inside the call: its
+            # rows belong to the featurize span (per-kernel roofline rows)
+            with PF.span("featurize", n, launches=0):
+                pass
     else:
         with PF.span("policy", n):
             N.check(lib.harl_policy_step(*args, _ptr(grow), m_total, _stream()),

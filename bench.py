@@ -448,6 +448,7 @@ KERNEL_SPAN = {
     "k_sample_rows": ("policy_tc", "hbm"),
     "k_trunk_tc<value>": ("value_tc", "tensor"),
     "k_policy_tc": ("policy_tc", "tensor"),
+    "k_policy_tc64": ("policy_tc", "tensor"),
     "k_policy_step_fused": ("policy_tc", "tensor"),
     "k_value_tc": ("value_tc", "tensor"),
     "k_featurize": ("featurize", "hbm"),
@@ -475,6 +476,7 @@ def per_row_work(tables, H, feat_in_sampler=False):
         "k_heads_tc": 2 * H * NH,
         "k_trunk_tc<value>": 2 * (F * H + H * H + H),   # per evaluated row
         "k_policy_tc": 2 * (F * H + H * H + H * NH),
+        "k_policy_tc64": 2 * (F * H + H * H + H * NH),
         # + the sampler/walker and the featurizer of the same rows
         "k_policy_step_fused": 2 * (F * H + H * H + H * NH),
         "k_value_tc": 2 * (F * H + H * H + H),

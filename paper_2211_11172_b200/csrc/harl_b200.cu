@@ -257,6 +257,16 @@ static bool use_ppo_tc() {
   return v == 1;
 }
 
+// HARL_TC64=0 disables the 64-row-tile tcgen05 kernels
+static bool use_tc64() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HARL_TC64");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // HARL_TC_GEN1=1 selects the first-generation 4-warp tcgen05 kernels
 static bool use_tc2() {
   static int v = -1;
@@ -861,11 +871,21 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     pa.logits_out = logits_out;
     pa.trunk_img = packed_trunk;
     pa.heads_img = packed_heads;
-    const int64_t tiles_n = (n + 127) / 128;
-    const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
-    HARL_PROF_BEGIN(st);
-    launch_k(k_policy_tc, dim3(grid), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
-    HARL_CHECK_LAUNCH("k_policy_tc");
+    // 64-row tiles when they still fit in one wave: twice the CTAs of
+    // 128-row tiles, half the epilogue per warp (the post-cull steps)
+    const int64_t tiles64 = (n + 63) / 64;
+    if (use_tc64() && tiles64 <= sm_count()) {
+      if ((rc = allow_smem(k_policy_tc64, (size_t)tc2_smem(NHP), "k_policy_tc64"))) return rc;
+      HARL_PROF_BEGIN(st);
+      launch_k(k_policy_tc64, dim3((unsigned)tiles64), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
+      HARL_CHECK_LAUNCH("k_policy_tc64");
+    } else {
+      const int64_t tiles_n = (n + 127) / 128;
+      const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
+      HARL_PROF_BEGIN(st);
+      launch_k(k_policy_tc, dim3(grid), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
+      HARL_CHECK_LAUNCH("k_policy_tc");
+    }
     // small populations (latency-bound steps): the sampler featurizes the
     // successor states itself, one launch less; large ones (throughput-
     // bound): the 4-threads-per-row featurizer keeps every lane busy
@@ -993,6 +1013,7 @@ int harl_prepare(void) {
   if ((rc = allow_max_smem(k_trunk_tc<TRUNK_VALUE>, "k_trunk_tc"))) return rc;
   if ((rc = allow_max_smem(k_heads_tc, "k_heads_tc"))) return rc;
   if ((rc = allow_max_smem(k_policy_tc, "k_policy_tc"))) return rc;
+  if ((rc = allow_max_smem(k_policy_tc64, "k_policy_tc64"))) return rc;
   if ((rc = allow_max_smem(k_policy_step_fused, "k_policy_step_fused"))) return rc;
   if ((rc = allow_max_smem(k_value_tc, "k_value_tc"))) return rc;
   if ((rc = allow_max_smem(k_ppo_rows, "k_ppo_rows"))) return rc;
@@ -1033,6 +1054,7 @@ int harl_prepare(void) {
   carve(k_pack_trunk);
   carve(k_pack_heads);
   carve(k_policy_tc);
+  carve(k_policy_tc64);
   carve(k_policy_step_fused);
   carve(k_value_tc);
   carve(k_finish_step);
@@ -1424,6 +1446,14 @@ static int build_grad_jobs(const harl_net_layout& P, const harl_net_layout& V,
 int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
                           void* stream) {
   const size_t smem = (PROBE_N + PROBE_M) * PROBE_K * 4 + 1024;
+  if (mode >= 3) {
+    int rc = allow_smem(k_tc_probe_m64, smem, "k_tc_probe_m64");
+    if (rc) return rc;
+    HARL_PROF_BEGIN((cudaStream_t)stream);
+    launch_k(k_tc_probe_m64, dim3(1), dim3(128), smem, (cudaStream_t)stream, A, B, D, mode);
+    HARL_CHECK_LAUNCH("k_tc_probe_m64");
+    return HARL_OK;
+  }
   int rc = allow_smem(k_tc_probe, smem, "k_tc_probe");
   if (rc) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);

@@ -87,6 +87,39 @@ __device__ inline void tc2_stage_x_smem(const double* xs, int lrow, int rows,
   tc::tmem_st16(t_lo, l);
 }
 
+// M = 64 tiles (n <= 148 * 64 rows per launch: twice the CTAs of 128-row
+// tiles, half the epilogue per warp).  Warp w: lane quarter q = w % 4 holds
+// tile rows 16 q .. 16 q + 15 (lanes 32 q .. 32 q + 15), column group
+// g = w / 4.
+__device__ inline void tc64_stage_x_smem(const double* xs, int q, int lane,
+                                         int rows, int F, int g,
+                                         uint32_t t_hi, uint32_t t_lo) {
+  float h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 16 * q + tc::frag64_row(lane, i);
+    const int k = 16 * g + tc::frag64_col(lane, i);
+    const float v = (r < rows && k < F) ? (float)xs[r * F + k] : 0.f;
+    tc::split_tf32(v, h[i], l[i]);
+  }
+  tc::tmem_st16x256_x2(t_hi, h);
+  tc::tmem_st16x256_x2(t_lo, l);
+}
+
+__device__ inline void tc64_tanh_split(uint32_t t_d, uint32_t t_hi,
+                                       uint32_t t_lo, const float* b,
+                                       int lane) {
+  float v[16], h[16], l[16];
+  tc::tmem_ld16x256_x4(t_d, v);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float z = tanhf(v[i] + b[tc::frag64_col(lane, i)]);
+    tc::split_tf32(z, h[i], l[i]);
+  }
+  tc::tmem_st16x256_x4(t_hi, h);
+  tc::tmem_st16x256_x4(t_lo, l);
+}
+
 struct PolicyTcArgs {
   const double* feat;   // [n][F] (16-byte aligned)
   int64_t n;
@@ -114,7 +147,7 @@ struct StepFuseArgs {
 
 static_assert(FEAT2_THREADS == TC2_THREADS, "fused featurize shares the CTA");
 
-template <bool FUSED>
+template <bool FUSED, int M = 128>
 __device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
                                                const StepFuseArgs* f,
                                                const harl_sketch_desc* sk,
@@ -131,9 +164,10 @@ __device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
   float* stg = (float*)rA;  // logits staging [128][TC2_LG_LD] after the heads MMA
   __shared__ uint64_t bar, wbar1, wbar2, hbar, xbar;
   __shared__ uint32_t tbase;
+  static_assert(M == 128 || (M == 64 && !FUSED), "tile rows");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, g = warp >> 2;
-  const int lrow = q * 32 + lane;
+  const int lrow = q * 32 + lane;   // M = 128: this thread's tile row
   if (warp == 0) tc::tmem_alloc(&tbase, 512);
   if (tid == 0) {
     tc::mbar_init(&bar, 1);
@@ -144,11 +178,11 @@ __device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
   }
   __syncthreads();
   const uint8_t* timg = (const uint8_t*)a.trunk_img;
-  const int64_t tiles = (a.n + 127) / 128;
+  const int64_t tiles = (a.n + M - 1) / M;
   if (tid == 0 && blockIdx.x < tiles) {
     // first tile: X into regB (W2 follows once X is in TMEM), W1 into regA
-    const int64_t r0 = (int64_t)blockIdx.x * 128;
-    tc2_bulk_x(rB, a.feat, r0, (int)min((int64_t)128, a.n - r0), a.F, &xbar);
+    const int64_t r0 = (int64_t)blockIdx.x * M;
+    tc2_bulk_x(rB, a.feat, r0, (int)min((int64_t)M, a.n - r0), a.F, &xbar);
     tc::bulk_load(rA, timg, TC2_W1, &wbar1);
   }
   tc_sync();
@@ -156,21 +190,24 @@ __device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
   const uint32_t tm = tbase;
   const uint32_t lo = (uint32_t)(q * 32) << 16;
   const uint32_t cXh = 0, cXl = 64, cD = 128, cHh = 256, cHl = 384;
-  const uint32_t id_h = tc::idesc_tf32(128, TC_H);
-  const uint32_t id_o = tc::idesc_tf32(128, a.NHP);
+  const uint32_t id_h = tc::idesc_tf32(M, TC_H);
+  const uint32_t id_o = tc::idesc_tf32(M, a.NHP);
   const uint32_t sA = tc::smem_u32(rA), sB = tc::smem_u32(rB);
   uint32_t ph = 0, pw1 = 0, ph_h = 0, px = 0;
   bool first = true;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t r0 = tile * 128;
-    const int rows = (int)min((int64_t)128, a.n - r0);
-    const int64_t row = r0 + lrow;
+    const int64_t r0 = tile * M;
+    const int rows = (int)min((int64_t)M, a.n - r0);
     if (!first && tid == 0) tc2_bulk_x(rA, a.feat, r0, rows, a.F, &xbar);
     tc::mbar_wait(&xbar, px);
     px ^= 1;
     const double* xs = (const double*)(first ? rB : rA);
-    if (g < TC_K1 / 16)
-      tc2_stage_x_smem(xs, lrow, rows, a.F, g, tm + lo + cXh + 16 * g, tm + lo + cXl + 16 * g);
+    if (g < TC_K1 / 16) {
+      if constexpr (M == 128)
+        tc2_stage_x_smem(xs, lrow, rows, a.F, g, tm + lo + cXh + 16 * g, tm + lo + cXl + 16 * g);
+      else
+        tc64_stage_x_smem(xs, q, lane, rows, a.F, g, tm + lo + cXh + 16 * g, tm + lo + cXl + 16 * g);
+    }
     tc::tmem_st_wait();
     tc_sync();
     dbg_ts(2);
@@ -192,8 +229,12 @@ __device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
     // regA is free: stream the heads image in behind the epilogues
     if (tid == 0) tc::bulk_load(rA, a.heads_img, heads_image_bytes(a.NHP), &hbar);
     if (first) tc::mbar_wait(&wbar2, 0);
-    tc2_tanh_split(tm + lo + cD + 32 * g, tm + lo + cHh + 32 * g, tm + lo + cHl + 32 * g,
-                   sb1 + 32 * g);
+    if constexpr (M == 128)
+      tc2_tanh_split(tm + lo + cD + 32 * g, tm + lo + cHh + 32 * g, tm + lo + cHl + 32 * g,
+                     sb1 + 32 * g);
+    else
+      tc64_tanh_split(tm + lo + cD + 32 * g, tm + lo + cHh + 32 * g, tm + lo + cHl + 32 * g,
+                      sb1 + 32 * g, lane);
     tc::tmem_st_wait();
     tc_sync();
     dbg_ts(5);
@@ -205,8 +246,12 @@ __device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
     ph ^= 1;
     tc::fence_after();
     dbg_ts(6);
-    tc2_tanh_split(tm + lo + cD + 32 * g, tm + lo + cHh + 32 * g, tm + lo + cHl + 32 * g,
-                   sb2 + 32 * g);
+    if constexpr (M == 128)
+      tc2_tanh_split(tm + lo + cD + 32 * g, tm + lo + cHh + 32 * g, tm + lo + cHl + 32 * g,
+                     sb2 + 32 * g);
+    else
+      tc64_tanh_split(tm + lo + cD + 32 * g, tm + lo + cHh + 32 * g, tm + lo + cHl + 32 * g,
+                      sb2 + 32 * g, lane);
     tc::tmem_st_wait();
     tc_sync();
     dbg_ts(7);
@@ -225,17 +270,34 @@ __device__ __forceinline__ void policy_tc_body(const PolicyTcArgs& a,
     // The heads weights are dead; the bias sits above the staging tile.
     float v[32];
     const bool has = 32 * g < a.NHP;
-    if (has) {
-      tc::tmem_ld32(tm + lo + cD + 32 * g, v);
+    if constexpr (M == 128) {
+      if (has) {
+        tc::tmem_ld32(tm + lo + cD + 32 * g, v);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += sbh[32 * g + j];
+        for (int j = 0; j < 32; ++j) v[j] += sbh[32 * g + j];
+      }
+    } else {
+      if (has) {
+        tc::tmem_ld16x256_x4(tm + lo + cD + 32 * g, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += sbh[32 * g + tc::frag64_col(lane, i)];
+      }
     }
     __syncthreads();  // every thread has read the bias before it may be overwritten
     if (has) {
-      float* srow = stg + lrow * TC2_LG_LD + 32 * g;
+      if constexpr (M == 128) {
+        float* srow = stg + lrow * TC2_LG_LD + 32 * g;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *(float4*)(srow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        for (int j = 0; j < 32; j += 4)
+          *(float4*)(srow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const int r = 16 * q + tc::frag64_row(lane, i);
+          *(float2*)(stg + r * TC2_LG_LD + 32 * g + tc::frag64_col(lane, i)) =
+              make_float2(v[i], v[i + 1]);
+        }
+      }
     }
     __syncthreads();
     if (!FUSED) {
@@ -283,6 +345,13 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_policy_tc(PolicyTcArgs a) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   policy_tc_body<false>(a, nullptr, nullptr, nullptr);
+}
+
+// 64-row tiles: for launches of <= 148 * 64 rows (the steps after a cull)
+__global__ void __launch_bounds__(TC2_THREADS, 1) k_policy_tc64(PolicyTcArgs a) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  policy_tc_body<false, 64>(a, nullptr, nullptr, nullptr);
 }
 
 __global__ void __launch_bounds__(TC2_THREADS, 1)

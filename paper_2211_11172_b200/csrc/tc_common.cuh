@@ -210,6 +210,60 @@ __device__ inline void tmem_ld4(uint32_t taddr, float* v) {
   for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// -- M = 64 tiles: rows live in lanes (r % 16) + 32 (r / 16) (probed,
+// variants/probe_m64.py); tcgen05.ld/st .16x256b spread a warp's 16 lanes
+// over all 32 threads: thread t holds lanes a = t/4 and a + 8 of its lane
+// base, columns 8 j + 2 (t % 4) + {0, 1} of repetition j, in the register
+// order (a, c), (a, c+1), (a+8, c), (a+8, c+1) per repetition.
+__device__ inline void tmem_ld16x256_x4(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]),
+        "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+        "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ inline void tmem_st16x256_x4(uint32_t taddr, const float* v) {
+  uint32_t r[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(v[i]);
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),
+        "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),
+        "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+__device__ inline void tmem_st16x256_x2(uint32_t taddr, const float* v) {
+  uint32_t r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(v[i]);
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8};"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),
+        "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+
+// (row within the 16-lane group, column within the 8 j + ... block) of
+// register i of a 16x256b fragment for thread `lane`
+__device__ __forceinline__ int frag64_row(int lane, int i) {
+  return (lane >> 2) + ((i >> 1) & 1) * 8;
+}
+__device__ __forceinline__ int frag64_col(int lane, int i) {
+  return 8 * (i >> 2) + 2 * (lane & 3) + (i & 1);
+}
+
 __device__ inline void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }

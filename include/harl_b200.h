@@ -125,6 +125,20 @@ typedef struct harl_forest_desc {
   const void* dev_hdr;
 } harl_forest_desc;
 
+/* The analytic measurement model of one sketch (SimHwParams + the
+ * SketchContext stage data the simulator reads, measure.py:41-122).
+ * Anchor stages in the sketch descriptor's stage order. */
+typedef struct harl_sim_desc {
+  int32_t cores, n_skipped;
+  double cap_l1, cap_l2, miss_l1, miss_l2, par_overhead, peak_flops;
+  double unroll_factor[HARL_MAX_LEVELS];   /* per unroll index */
+  double stage_flops[HARL_MAX_STAGES];
+  int32_t stage_spatial_n[HARL_MAX_STAGES];
+  int16_t stage_spatial[HARL_MAX_STAGES][HARL_MAX_DIMS];
+  double skipped_flops[HARL_MAX_STAGES], skipped_l1[HARL_MAX_STAGES],
+      skipped_l2[HARL_MAX_STAGES];
+} harl_sim_desc;
+
 int harl_abi_version(void);
 /* One-time setup (kernel shared-memory limits, device queries) so that the
  * step entry points can be recorded into CUDA graphs. */
@@ -466,6 +480,22 @@ int harl_cull_select(const double* adv, const int32_t* tracks, int64_t m,
  * if cap is too small (40 * n suffices).  threads <= 0: all cores. */
 long long harl_format_floats(const double* v, long long n, char* out,
                              long long cap, int threads);
+
+/* simulate_time (measure.py:99-112) for n states (SoA, leading dim ld):
+ * out[r] = the model's seconds, bit-exact with the reference. */
+int harl_sim_time(const harl_sketch_desc* sk, const harl_sim_desc* sim,
+                  const uint16_t* tiles, const uint8_t* knobs, int64_t n,
+                  int64_t ld, double* out, void* stream);
+/* brute_force_best's sweep (measure.py:135-167) over state numbers
+ * [x0, x0 + count) (dim 0's tilings slowest, then compute-at, parallel,
+ * unroll): best (device u64) = ordered bits of the minimum time; out
+ * (device u64) = the state number attaining it with the smallest canonical
+ * text (the reference's tie rule).  scratch: scratch_len device u64 (one
+ * per CTA of the sweep; >= 148 * 16 uses the full grid). */
+int harl_brute_force(const harl_sketch_desc* sk, const harl_sim_desc* sim,
+                     uint64_t x0, uint64_t count, unsigned long long* best,
+                     unsigned long long* out, unsigned long long* scratch,
+                     int64_t scratch_len, void* stream);
 
 /* Instrumentation (no reference counterpart; the reference has no device).
  * harl_launch_count: kernels this library has launched since load (graph

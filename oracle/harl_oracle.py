@@ -22,6 +22,7 @@ What it restates (reference files under ``/root/reference/pkg/src/schedtune``):
 * ``TrackSet.cull`` / ``episode_done`` ......... stopping.py:68-95
 * ``rank_scores`` ............................... costmodel.py:266-286
 * ``_fit_tree`` / ``fit_incremental`` (GBT refit) costmodel.py:81-141,190-212
+* ``simulate_time`` / ``brute_force_best`` ........ measure.py:78-167
 
 It is written population-at-once (structure-of-arrays numpy) instead of the
 reference's per-track objects, but every floating-point operation is the
@@ -335,6 +336,89 @@ def gbt_fit(X, y, n_trees: int = 50, max_depth: int = 6,
         pred = pred + learning_rate * tree_predict(tree, X)
         trees.append(tree)
     return base, trees, pred
+
+
+SIM_DEFAULTS = dict(cores=32, cap_l1=4096.0, cap_l2=131072.0,
+                    miss_penalty_l1=0.3, miss_penalty_l2=0.6,
+                    parallel_overhead=0.02,
+                    unroll_factors=((0, 1.00), (16, 0.97), (64, 0.95),
+                                    (512, 0.98), (1024, 1.00)),
+                    peak_flops=1e11)
+
+
+def _miss_factor(l1, l2, p):
+    """measure.py:78-81."""
+    m1 = 1.0 + p["miss_penalty_l1"] * max(0.0, l1 / p["cap_l1"] - 1.0)
+    m2 = 1.0 + p["miss_penalty_l2"] * max(0.0, l2 / p["cap_l2"] - 1.0)
+    return m1 * m2
+
+
+def sim_time(tb, tiles_row, knobs_row, params=None):
+    """measure.simulate_time (measure.py:99-112) for one state given as the
+    flat tile row + (ca, par, ur), over the host mirror's stage tables."""
+    p = dict(SIM_DEFAULTS)
+    p.update(params or {})
+    L = tb.levels
+    t = [int(v) for v in tiles_row]
+    ca, par, ur = (int(v) for v in knobs_row)
+    depth = tb.unroll_depths[ur]
+    u = dict(p["unroll_factors"]).get(depth, 1.0)
+    t1 = [t[d * L + L - 1] for d in range(tb.ndims)]
+    t2 = [t[d * L + L - 2] * t[d * L + L - 1] for d in range(tb.ndims)] \
+        if L >= 2 else list(t1)
+    total = 0.0
+    for s_i, (tensors, inter, extra, flops) in enumerate(tb.stages):
+        def el(terms, tl):
+            n = 1
+            for gi, sc, off in terms:
+                n *= sc * tl[gi] + off
+            return n
+        l1 = sum(el(tt, t1) for tt in tensors)
+        l2 = sum(el(tt, t2) for tt in tensors)
+        l1 += (inter + extra) * el(tensors[-1], t1)
+        l2 += extra * el(tensors[-1], t2)
+        if ca == 0:
+            l2 += inter * el(tensors[-1], t2)
+        m = _miss_factor(float(l1), float(l2), p)
+        spatial = tb.sim_spatial[s_i]
+        if par == 0 or not spatial:
+            spd = 1.0
+        else:
+            extent = 1
+            for gi in spatial:
+                for lv in range(par):
+                    extent *= t[gi * L + lv]
+            used = min(extent, p["cores"])
+            balance = extent / (math.ceil(extent / p["cores"]) * p["cores"])
+            spd = used * balance * (1.0 - p["parallel_overhead"] * (par - 1))
+        total += (flops / p["peak_flops"]) * m * u / spd
+    for flops, l1, l2 in tb.sim_skipped:
+        total += (flops / p["peak_flops"]) * _miss_factor(l1, l2, p)
+    return total
+
+
+def brute_force_best(tb, params=None):
+    """measure.brute_force_best (measure.py:135-167): (tiles, knobs, time)
+    of the minimum, ties on the canonical text."""
+    import itertools
+    L = tb.levels
+    per_dim = [tb.tiling_table[int(tb.tiling_offsets[d]):
+                               int(tb.tiling_offsets[d]) +
+                               int(tb.tiling_counts[d])]
+               for d in range(tb.ndims)]
+    best = (math.inf, "", None, None)
+    for combo in itertools.product(*per_dim):
+        row = np.concatenate(combo) if combo else np.zeros(0, np.uint16)
+        for ca in range(tb.ncas):
+            for par in range(tb.max_fusible + 1):
+                for ur in range(tb.n_unroll):
+                    tm = sim_time(tb, row, (ca, par, ur), params)
+                    if tm < best[0] or (tm == best[0] and
+                                        tb.canonical(row, (ca, par, ur))
+                                        < best[1]):
+                        best = (tm, tb.canonical(row, (ca, par, ur)),
+                                row.copy(), (ca, par, ur))
+    return best[2], best[3], best[0]
 
 
 # ---------------------------------------------------------------------------

@@ -74,6 +74,19 @@ class ReplayRing(C.Structure):
                 ("move_bits", vp), ("shift_bits", vp), ("cap", i64)]
 
 
+class SimDesc(C.Structure):
+    _fields_ = [("cores", i32), ("n_skipped", i32), ("cap_l1", f64),
+                ("cap_l2", f64), ("miss_l1", f64), ("miss_l2", f64),
+                ("par_overhead", f64), ("peak_flops", f64),
+                ("unroll_factor", f64 * MAX_LEVELS),
+                ("stage_flops", f64 * MAX_STAGES),
+                ("stage_spatial_n", i32 * MAX_STAGES),
+                ("stage_spatial", (i16 * MAX_DIMS) * MAX_STAGES),
+                ("skipped_flops", f64 * MAX_STAGES),
+                ("skipped_l1", f64 * MAX_STAGES),
+                ("skipped_l2", f64 * MAX_STAGES)]
+
+
 class EntryLog(C.Structure):
     _fields_ = [("tiles", vp), ("knobs", vp), ("score", vp), ("reward", vp),
                 ("track", vp), ("ld", i64)]
@@ -149,6 +162,10 @@ _SIGS = {
                                vp, vp, vp, vp, i64, vp]),
     "harl_ppo_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_rank_scratch_bytes": (i64, [i64, i64]),
+    "harl_sim_time": (i32, [P(SketchDesc), P(SimDesc), vp, vp, i64, i64, vp,
+                            vp]),
+    "harl_brute_force": (i32, [P(SketchDesc), P(SimDesc), u64, u64, vp, vp,
+                               vp, i64, vp]),
     "harl_format_floats": (C.c_longlong, [vp, C.c_longlong, vp, C.c_longlong,
                                           i32]),
     "harl_cull_select": (i32, [vp, vp, i64, vp, i64, i64, vp, vp, P(i64)]),

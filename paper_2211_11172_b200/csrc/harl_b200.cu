@@ -25,6 +25,7 @@
 #include "mlp_tc2.cuh"
 #include "rank_kernels.cuh"
 #include "gbt_fit_kernels.cuh"
+#include "sim_kernels.cuh"
 
 namespace harl {
 
@@ -1900,6 +1901,57 @@ int harl_cull_select(const double* adv, const int32_t* tracks, int64_t m,
   for (int64_t r = 0; r < m; ++r)
     if (alive[tracks[r]]) keep_out[k++] = (int32_t)r;
   *n_keep = k;
+  return HARL_OK;
+}
+
+
+int harl_sim_time(const harl_sketch_desc* sk, const harl_sim_desc* sim,
+                  const uint16_t* tiles, const uint8_t* knobs, int64_t n,
+                  int64_t ld, double* out, void* stream) {
+  if (!sk || !sim || !knobs || !out || n < 0 || sim->n_skipped < 0 ||
+      sim->n_skipped > HARL_MAX_STAGES || sk->n_unroll > HARL_MAX_LEVELS) {
+    set_error("harl_sim_time: bad arguments");
+    return HARL_E_ARG;
+  }
+  if (n == 0) return HARL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t g = (n + 127) / 128;
+  const unsigned grid = (unsigned)(g < sm_count() * 8 ? g : sm_count() * 8);
+  HARL_PROF_BEGIN(st);
+  launch_k(k_sim_time, dim3(grid), dim3(128), 0, st, *sk, *sim, tiles, knobs, n, ld, out);
+  HARL_CHECK_LAUNCH("k_sim_time");
+  return HARL_OK;
+}
+
+int harl_brute_force(const harl_sketch_desc* sk, const harl_sim_desc* sim,
+                     uint64_t x0, uint64_t count, unsigned long long* best,
+                     unsigned long long* out, unsigned long long* scratch,
+                     int64_t scratch_len, void* stream) {
+  if (!sk || !sim || !best || !out || !scratch || sk->ncas < 1 ||
+      sk->n_unroll < 1 || sk->n_unroll > HARL_MAX_LEVELS) {
+    set_error("harl_brute_force: bad arguments");
+    return HARL_E_ARG;
+  }
+  if (count == 0) return HARL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(best, 0xff, 8, st)) != cudaSuccess)
+    return cuda_status(e, "harl_brute_force memset");
+  const uint64_t g = (count + 255) / 256;
+  uint64_t gmax = (uint64_t)sm_count() * 16;
+  if (gmax > (uint64_t)scratch_len) gmax = (uint64_t)scratch_len;
+  const unsigned grid = (unsigned)(g < gmax ? g : gmax);
+  HARL_PROF_BEGIN(st);
+  launch_k(k_brute_min, dim3(grid), dim3(256), 0, st, *sk, *sim, x0, count, best);
+  HARL_CHECK_LAUNCH("k_brute_min");
+  HARL_PROF_BEGIN(st);
+  launch_k(k_brute_ties, dim3(grid), dim3(256), 0, st, *sk, *sim, x0, count,
+           (const unsigned long long*)best, scratch);
+  HARL_CHECK_LAUNCH("k_brute_ties");
+  HARL_PROF_BEGIN(st);
+  launch_k(k_brute_final, dim3(1), dim3(32), 0, st, *sk,
+           (const unsigned long long*)scratch, (int)grid, out);
+  HARL_CHECK_LAUNCH("k_brute_final");
   return HARL_OK;
 }
 

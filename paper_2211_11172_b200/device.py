@@ -17,6 +17,8 @@ this module                    reference
 ``value_estimate``             ValueNet.estimate 173-174
 ``DeviceAgent.ppo_update``     ppo_update 361-378
 ``rank_topk``                  costmodel.rank_scores 266-286
+``simulate_time``              measure.simulate_time 99-112
+``brute_force_best``           measure.brute_force_best 135-167
 ``gbt_fit``                    SurrogateModel.fit_incremental 190-212
                                (+ _fit_tree 81-141)
 =============================  ==========================================
@@ -398,6 +400,130 @@ def gbt_fit(X, y, n_trees: int = 50, max_depth: int = 6,
                   val[:k].cpu().numpy())
     trees = [heap_tree_to_reference(fh[t], th[t], vh[t]) for t in range(k)]
     return GbtFit(float(base.item()), trees, pred.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# the analytic measurement model (measure.py)
+
+
+SIM_DEFAULTS = dict(cores=32, cap_l1=4096.0, cap_l2=131072.0,
+                    miss_penalty_l1=0.3, miss_penalty_l2=0.6,
+                    parallel_overhead=0.02,
+                    unroll_factors=((0, 1.00), (16, 0.97), (64, 0.95),
+                                    (512, 0.98), (1024, 1.00)),
+                    peak_flops=1e11)
+
+
+def _sim_param(params, name):
+    if params is None:
+        return SIM_DEFAULTS[name]
+    if isinstance(params, dict):
+        return params.get(name, SIM_DEFAULTS[name])
+    return getattr(params, name)
+
+
+def sim_desc(tables: SketchTables, params=None) -> "N.SimDesc":
+    """The simulator's descriptor for one sketch: SimHwParams (the
+    reference's dataclass or a dict; defaults measure.py:41-60) and the
+    sketch's stage data.  Noise is ignored (brute_force_best and the pure
+    model)."""
+    d = N.SimDesc()
+    d.cores = int(_sim_param(params, "cores"))
+    d.cap_l1 = float(_sim_param(params, "cap_l1"))
+    d.cap_l2 = float(_sim_param(params, "cap_l2"))
+    d.miss_l1 = float(_sim_param(params, "miss_penalty_l1"))
+    d.miss_l2 = float(_sim_param(params, "miss_penalty_l2"))
+    d.par_overhead = float(_sim_param(params, "parallel_overhead"))
+    d.peak_flops = float(_sim_param(params, "peak_flops"))
+    table = dict(_sim_param(params, "unroll_factors"))
+    for i, depth in enumerate(tables.unroll_depths):
+        d.unroll_factor[i] = float(table.get(depth, 1.0))
+    if len(tables.stage_flops) > N.MAX_STAGES or \
+            len(tables.sim_skipped) > N.MAX_STAGES:
+        raise DeviceError("too many stages for the simulator tables")
+    for s_i, (fl, sp) in enumerate(zip(tables.stage_flops,
+                                       tables.sim_spatial)):
+        d.stage_flops[s_i] = float(fl)
+        d.stage_spatial_n[s_i] = len(sp)
+        for j, gi in enumerate(sp):
+            d.stage_spatial[s_i][j] = gi
+    d.n_skipped = len(tables.sim_skipped)
+    for k, (fl, l1, l2) in enumerate(tables.sim_skipped):
+        d.skipped_flops[k], d.skipped_l1[k], d.skipped_l2[k] = fl, l1, l2
+    return d
+
+
+def simulate_time(dsk: DeviceSketch, tiles, knobs, n: int, params=None,
+                  out=None):
+    """measure.simulate_time (measure.py:99-112) for n device states:
+    seconds under the analytic model, bit-exact."""
+    lib = N.load()
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=dsk.device)
+    d = sim_desc(dsk.tables, params)
+    with PF.span("sim", n):
+        N.check(lib.harl_sim_time(C.byref(dsk.desc), C.byref(d), _ptr(tiles),
+                                  _ptr(knobs), n, tiles.shape[1], _ptr(out),
+                                  _stream()), "harl_sim_time")
+    return out[:n]
+
+
+def space_states(tables: SketchTables) -> int:
+    """space_size (schedspace.py:88-95) from the tables."""
+    n = 1
+    for c in tables.tiling_counts:
+        n *= int(c)
+    return n * tables.ncas * (tables.max_fusible + 1) * tables.n_unroll
+
+
+def decode_state_number(tables: SketchTables, x: int):
+    """State number -> (tiles [local_slots] u16, knobs (ca, par, ur)) in
+    brute_force_best's enumeration order (dim 0's tilings slowest)."""
+    L = tables.levels
+    ur = x % tables.n_unroll
+    x //= tables.n_unroll
+    par = x % (tables.max_fusible + 1)
+    x //= tables.max_fusible + 1
+    ca = x % tables.ncas
+    x //= tables.ncas
+    tiles = np.zeros(tables.local_slots, dtype=np.uint16)
+    for d in range(tables.ndims - 1, -1, -1):
+        c = int(tables.tiling_counts[d])
+        idx = x % c
+        x //= c
+        tiles[d * L:(d + 1) * L] = tables.tiling_table[
+            int(tables.tiling_offsets[d]) + idx]
+    return tiles, (int(ca), int(par), int(ur))
+
+
+def brute_force_best(tables: SketchTables, params=None,
+                     cap: int = 1_000_000, device=None):
+    """measure.brute_force_best (measure.py:135-167): the noise-free optimum
+    of one sketch's space, ties broken on the canonical text.  The device
+    sweeps every state (the minimum time, then the canonically smallest
+    state attaining it, compared on rendered text).  Returns (tiles, (ca,
+    par, ur), time)."""
+    from .errors import SpaceTooLarge
+    size = space_states(tables)
+    if size > cap:
+        raise SpaceTooLarge(size, cap)
+    lib = N.load()
+    dev = _dev(device)
+    dsk = DeviceSketch(tables, dev)
+    d = sim_desc(tables, params)
+    best = torch.empty(1, dtype=torch.int64, device=dev)
+    win = torch.empty(1, dtype=torch.int64, device=dev)
+    scratch = torch.empty(4096, dtype=torch.int64, device=dev)
+    with PF.span("brute", size):
+        N.check(lib.harl_brute_force(C.byref(dsk.desc), C.byref(d), 0, size,
+                                     _ptr(best), _ptr(win), _ptr(scratch),
+                                     scratch.numel(), _stream()),
+                "harl_brute_force")
+    bits = int(best.item()) & ((1 << 64) - 1)
+    raw = bits & ((1 << 63) - 1) if bits >> 63 else (~bits) & ((1 << 64) - 1)
+    t = float(np.asarray([raw], dtype=np.uint64).view(np.float64)[0])
+    tl, kn = decode_state_number(tables, int(win.item()))
+    return tl, kn, t
 
 
 def action_masks(dsk: DeviceSketch, tiles, knobs, n: int):

@@ -34,3 +34,12 @@ class CostModelError(ValueError):
 
 class DeviceError(RuntimeError):
     """The B200 path failed (CUDA error, missing native library, bad call)."""
+
+
+class SpaceTooLarge(DeviceError):
+    """brute_force_best refused a space above its cap (measure.py:30-36)."""
+
+    def __init__(self, size: int, cap: int):
+        super().__init__(f"space has {size} states, above the cap of {cap}")
+        self.size = size
+        self.cap = cap

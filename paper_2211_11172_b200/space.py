@@ -192,11 +192,27 @@ class SketchTables:
         slot_of = {(td.node, td.dim): i for i, td in enumerate(sp.tiled_dims)}
         b_eff = effective_flops(sg, sketch)
         stages = []
+        # simulator data (SketchContext.stages / .skipped, schedspace.py:
+        # 337-364): per anchor stage its flops and spatial slots; per
+        # non-anchor node (flops, full footprint, full footprint)
+        self.sim_spatial = []
+        self.sim_skipped = []
+        self.unroll_depths = tuple(int(d) for d in sp.unroll_depths)
         for node in sg.nodes:
             st = _val(sketch.structure_of(node.name))
-            if st == "inlined" or st == "skipped":
+            if st == "inlined":
                 continue
-            specs = _specs(_mirror_node(node))
+            mnode = _mirror_node(node)
+            if st == "skipped":
+                full = {d: e for d, e in mnode.shape}
+                l_full = float(sum(t.elements(full) for t in _specs(mnode)))
+                self.sim_skipped.append((float(b_eff[node.name]), l_full,
+                                         l_full))
+                continue
+            self.sim_spatial.append(tuple(slot_of[(node.name, d)]
+                                          for d, _ in mnode.shape
+                                          if mnode.is_spatial(d)))
+            specs = _specs(mnode)
             tensors = [[(slot_of[(node.name, d)], int(sc), int(off))
                         for d, sc, off in t.terms] for t in specs]
             inter = {"tiled": 0, "tiled_fused": 1, "cache_write_tiled": 1,

@@ -278,7 +278,66 @@ def main():
         print(case["name"], "episodes", len(rec["episodes"]),
               "npz bytes", os.path.getsize(path))
     index["gbt_fit_large"] = make_gbt_fixture()
+    index["sim"] = make_sim_fixture()
     return index
+
+
+def make_sim_fixture():
+    """The reference's analytic model: simulate_time of random states of
+    several sketches (default and custom SimHwParams) and brute_force_best
+    on the 4,116-state GEMM-64 space."""
+    sys.path.insert(0, REF)
+    from dataclasses import asdict
+    from schedtune.measure import SimHwParams, brute_force_best, simulate_time
+    from schedtune.schedspace import SketchContext, sample_initial_schedules
+    from schedtune.workload import (TargetConfig, generate_sketches,
+                                    gpu_target, load_network)
+    wl_dir = "/root/reference/pkg/workloads"
+    custom = SimHwParams(cores=8, cap_l1=2048.0, cap_l2=65536.0,
+                         miss_penalty_l1=0.45, miss_penalty_l2=0.9,
+                         parallel_overhead=0.05, peak_flops=3e10)
+    rng = np.random.default_rng(5)
+    out = {"params": {"default": {}, "custom": {
+        k: (list(map(list, v)) if k == "unroll_factors" else v)
+        for k, v in asdict(custom).items()
+        if k not in ("noise_sigma", "noise_seed")}}, "cases": []}
+    nets = [("gemm_64.yaml", TargetConfig(tiling_levels=2)),
+            ("conv2d.yaml", TargetConfig()), ("bert_like.yaml", TargetConfig()),
+            ("two_phase.yaml", TargetConfig()), ("gemm_l.yaml", gpu_target())]
+    out["yaml"] = {}
+    for wl, tg in nets:
+        out["yaml"][wl] = open(os.path.join(wl_dir, wl)).read()
+        net = load_network(os.path.join(wl_dir, wl))
+        for sg_i, sg in enumerate(net.subgraphs[:2]):
+            for k_i, sk in enumerate(generate_sketches(sg, tg)):
+                ctx = SketchContext(sg, sk, tg)
+                states = sample_initial_schedules(sk, 40, rng)
+                rec = {"workload": wl, "target": asdict(tg), "sg": sg_i,
+                       "sketch": k_i,
+                       "states": [s.canonical() for s in states],
+                       "default": [repr(simulate_time(s, ctx, SimHwParams()))
+                                   for s in states],
+                       "custom": [repr(simulate_time(s, ctx, custom))
+                                  for s in states]}
+                out["cases"].append(rec)
+    net = load_network(os.path.join(wl_dir, "gemm_64.yaml"))
+    tg = TargetConfig(tiling_levels=2)
+    sg = net.subgraphs[0]
+    out["brute"] = []
+    for k_i, sk in enumerate(generate_sketches(sg, tg)):
+        ctx = SketchContext(sg, sk, tg)
+        for name, prm in (("default", SimHwParams()), ("custom", custom)):
+            st, tm = brute_force_best(ctx, prm)
+            out["brute"].append({"workload": "gemm_64.yaml", "sg": 0,
+                                 "sketch": k_i, "target": asdict(tg),
+                                 "params": name, "state": st.canonical(),
+                                 "time": repr(tm)})
+    path = os.path.join(HERE, "sim_golden.json")
+    with open(path, "w") as fh:
+        json.dump(out, fh, indent=0, sort_keys=True)
+    print("sim golden", len(out["cases"]), "cases,", len(out["brute"]),
+          "brute-force optima")
+    return os.path.getsize(path)
 
 
 def make_gbt_fixture(n: int = 2500):

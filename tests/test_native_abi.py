@@ -49,6 +49,7 @@ def _ctkind(t):
             not isinstance(t._type_, str):
         return "ptr"
     return {ctypes.c_int64: "i64", ctypes.c_longlong: "i64",
+            ctypes.c_uint64: "i64", ctypes.c_ulonglong: "i64",
             ctypes.c_double: "f64"}.get(t, "i32")
 
 

@@ -42,8 +42,11 @@ def digest_list(arrs) -> str:
 
 
 def case_names():
+    """Recorded sessions: a .json header with its .npz arrays (other
+    fixtures -- sim_golden.json, gbt_fit_large.npz -- stand alone)."""
     return sorted(os.path.basename(p)[:-5]
-                  for p in glob.glob(os.path.join(GOLDEN, "*.json")))
+                  for p in glob.glob(os.path.join(GOLDEN, "*.json"))
+                  if os.path.exists(p[:-5] + ".npz"))
 
 
 class GoldenCase:

@@ -428,16 +428,11 @@ class EpisodeEngine:
         cur, nxt = b.pop[0], b.pop[1]
         rt, rt_spare = b.rt[0], b.rt[1]
         D.init_population(b.dsk, P, gen, cur["tiles"], cur["knobs"])
-        D.featurize(b.dsk, cur["tiles"], cur["knobs"], P, cur["feat"])
-        D.gbt_predict(forest, cur["feat"], P, out=cur["score"])
         if getattr(b, "iota", None) is None:
             b.iota = torch.arange(P, dtype=torch.int32, device=self.dev)
-        rt.copy_(b.iota)
-        b.steps.zero_()
-        b.best.fill_(-math.inf)
-        b.best_step.zero_()
-        b.status.fill_(-1)
-        self.dagent.bad.zero_()
+        if eager:
+            # (the graphed path records these launches in its first graph)
+            self._episode_prologue(b, forest)
         if eager:
             res = self._run_eager(b, gen, cfg, order_counter, inject, record,
                                   cull_override)
@@ -450,6 +445,20 @@ class EpisodeEngine:
             from .errors import RlDivergedError
             raise RlDivergedError("non-finite loss or gradient in update")
         return res
+
+    def _episode_prologue(self, b, forest):
+        """The initial population's features and scores, and the per-episode
+        resets (track stats, status words, divergence flag)."""
+        P = b.P
+        cur = b.pop[0]
+        D.featurize(b.dsk, cur["tiles"], cur["knobs"], P, cur["feat"])
+        D.gbt_predict(forest, cur["feat"], P, out=cur["score"])
+        b.rt[0].copy_(b.iota)
+        b.steps.zero_()
+        b.best.fill_(-math.inf)
+        b.best_step.zero_()
+        b.status.fill_(-1)
+        self.dagent.bad.zero_()
 
     def _result(self, b, cfg, order_counter, used, culls, train, alive):
         return EpisodeResult(tables=b.tables, visits=used,
@@ -723,6 +732,8 @@ class EpisodeEngine:
             n0 = PF.launch_count()
             with torch.cuda.graph(g, stream=stream,
                                   capture_error_mode="relaxed"):
+                if si == 0:
+                    self._episode_prologue(b, b.forest)
                 if after_cull:
                     n_keep = b.plan[k0 - 1]["m"] - b.plan[k0 - 1]["cull"]
                     self._compact(b, b.pop[cur_i], b.rt[rt_i],

@@ -847,9 +847,14 @@ class EpisodeEngine:
                 m = prev["m"]
                 if _PY_CULL:
                     tracks, adv_h = self._cull_inputs(b, rt_i, m)
-                    gone = self._cull(tracks, adv_h, m, alive, cfg)
-                    keep = np.flatnonzero(alive[tracks]).astype(np.int32)
-                    b.keep[:len(keep)].copy_(torch.from_numpy(keep))
+                    gone, keep = self._cull_rows(tracks, adv_h, alive, cfg)
+                    kp = b.keep_pin if getattr(b, "keep_pin", None) is not \
+                        None else None
+                    if kp is None:
+                        kp = b.keep_pin = torch.empty(b.P, dtype=torch.int32,
+                                                      pin_memory=True)
+                    kp[:len(keep)].numpy()[:] = keep
+                    b.keep[:len(keep)].copy_(kp[:len(keep)], non_blocking=True)
                 else:
                     gone = self._cull_native(b, rt_i, m, alive, cfg)
                 culls.append((prev["t"], gone, int(alive.sum())))
@@ -913,6 +918,30 @@ class EpisodeEngine:
             gone = np.sort(np.concatenate([below, tied[::-1][:need]]))
         alive[gone] = False
         return gone
+
+    def _cull_rows(self, tracks, adv, alive, cfg):
+        """``_cull`` on the cull step's rows directly (row r = live track
+        tracks[r], every live track has one row): (eliminated track ids
+        ascending, surviving rows ascending)."""
+        m = len(tracks)
+        n_elim = min(int(math.floor(cfg.cull_fraction * m)),
+                     m - cfg.min_tracks)
+        if n_elim <= 0:
+            return np.zeros(0, dtype=np.int64), np.arange(m, dtype=np.int32)
+        if np.isnan(adv).any():          # NaN orders last: the full sort
+            gone = self._cull(tracks, adv, m, alive, cfg)
+            return gone, np.flatnonzero(alive[tracks]).astype(np.int32)
+        cut = np.partition(adv, n_elim - 1)[n_elim - 1]
+        out = adv < cut
+        tie = np.flatnonzero(adv == cut)
+        need = n_elim - int(np.count_nonzero(out))
+        # ties go by higher track index first (stopping.py:81)
+        out[tie[np.argsort(-tracks[tie], kind="stable")[:need]]] = True
+        alive[tracks[out]] = False
+        # ascending ids without a sort: the tracks that were live and are not
+        dead = np.zeros(len(alive), dtype=bool)
+        dead[tracks[out]] = True
+        return np.flatnonzero(dead), np.flatnonzero(~out).astype(np.int32)
 
     def _cull_native(self, b, rt_i, m, alive, cfg):
         """The graphed episode's cull: one pinned D2H of the step's rows and

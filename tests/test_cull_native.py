@@ -59,3 +59,27 @@ def test_cull_select_rejects_dead_rows():
     assert lib.harl_cull_select(adv.ctypes.data, tracks.ctypes.data, 2,
                                 a8.ctypes.data, 2, 1, gone.ctypes.data,
                                 keep.ctypes.data, C.byref(nk)) != 0
+
+
+def test_row_cull_matches_track_cull():
+    """engine._cull_rows (the graphed episode's cull on the step's rows)
+    makes the same decision as engine._cull, ties and NaNs included."""
+    from types import SimpleNamespace
+    from paper_2211_11172_b200.engine import EpisodeEngine
+    E = EpisodeEngine.__new__(EpisodeEngine)
+    rng = np.random.default_rng(2)
+    for t in range(300):
+        P = int(rng.integers(10, 500))
+        alive = rng.random(P) < 0.8
+        tracks = np.flatnonzero(alive)
+        rng.shuffle(tracks)
+        adv = np.round(rng.random(len(tracks)) * rng.choice([3, 50, 1e6])) / 7
+        if t % 9 == 0:
+            adv[rng.random(len(adv)) < 0.1] = np.nan
+        cfg = SimpleNamespace(cull_fraction=0.5,
+                              min_tracks=int(rng.integers(1, 10)))
+        a1, a2 = alive.copy(), alive.copy()
+        g1 = E._cull(tracks, adv, len(tracks), a1, cfg)
+        g2, k2 = E._cull_rows(tracks, adv, a2, cfg)
+        assert g1.tolist() == g2.tolist() and np.array_equal(a1, a2)
+        assert k2.tolist() == np.flatnonzero(a1[tracks]).tolist()

@@ -359,7 +359,8 @@ def run_gpu(args, rank, world):
 class E2EHost:
     """The drop-in's host side for the e2e number: pinned host buffers for
     every per-episode input (agent parameters + Adam moments, replay ring,
-    GBT ensemble) and output (the rank_scores selection -- top-k' distinct
+    GBT ensemble; the replay ring stays resident like the drop-in's) and
+    output (the rank_scores selection -- top-k' distinct
     unmeasured entries with states, features, scores -- the per-visit
     rewards of the trajectory log, the updated agent and ring), allocated
     once.  Each timed episode copies the inputs host->device, runs
@@ -379,14 +380,14 @@ class E2EHost:
             t.copy_(getattr(da, k))
         self.agent_out = {k: pin(getattr(da, k)) for k in ("params", "m", "v")}
         keys = ("X", "Xn", "actions", "scalars", "move_bits", "shift_bits")
-        self.ring_in = {k: pin(getattr(ring, k)) for k in keys}
-        for k, t in self.ring_in.items():
-            t.copy_(getattr(ring, k))
         self.ring_out = {k: pin(getattr(ring, k)) for k in keys}
         self.V = (visits, torch.empty(visits, dtype=torch.float64).pin_memory())
         from paper_2211_11172_b200 import device as D
         self.rank_scratch = D.RankScratch(dev)
         self.top_k = 64                 # TunerConfig.top_k default
+        # allocations a session makes once, outside the per-round path
+        self.rank_scratch.ensure(visits, 64 * 16, self.top_k)
+        self.rank_scratch.host_pins(4 * self.top_k, w["tables"])
         self.measured = None
 
     def episode(self, forest, gen, ecfg, order):
@@ -401,9 +402,9 @@ class E2EHost:
             nin += t.numel() * t.element_size()
         da.params32.copy_(da.params)            # fp32 rollout copy
         da.refresh_derived()                    # tcgen05 images + transposes
-        for k, t in self.ring_in.items():
-            getattr(ring, k).copy_(t, non_blocking=True)
-            nin += t.numel() * t.element_size()
+        # the replay ring is not uploaded: between episodes the drop-in keeps
+        # it in device memory (compat._RingBuffer); it is still exported
+        # below, as the per-round checkpoint does
         w = self.w
         forest.load(w["trees"], w["base"], w["lr"])
         nin += forest.n_nodes * 16 + forest.n_trees * 4 + forest.HDR.itemsize

@@ -242,6 +242,23 @@ class RankScratch:
         self.out = None
         self.stats = torch.zeros(4, dtype=torch.int64, device=self.device)
 
+    def host_pins(self, n: int, tables: SketchTables):
+        """Pinned host buffers for a selection of n entries (grown on
+        demand): (indices, tiles [slots][cap], knobs [3][cap], features,
+        scores)."""
+        S, F = max(tables.local_slots, 1), tables.feature_len
+        cur = getattr(self, "_pins", None)
+        if cur is None or cur[0].numel() < n or cur[1].shape[0] < S or \
+                cur[3].shape[1] != F:
+            cap = max(n, 256)
+            pin = dict(pin_memory=True)
+            self._pins = (torch.empty(cap, dtype=torch.int32, **pin),
+                          torch.empty((S, cap), dtype=torch.int16, **pin),
+                          torch.empty((3, cap), dtype=torch.uint8, **pin),
+                          torch.empty((cap, F), dtype=torch.float64, **pin),
+                          torch.empty(cap, dtype=torch.float64, **pin))
+        return self._pins
+
     def ensure(self, n_visits: int, n_excluded: int, k: int):
         need = N.load().harl_rank_scratch_bytes(n_visits, n_excluded)
         if self.buf is None or self.buf.numel() < need:

@@ -171,9 +171,27 @@ class EpisodeResult:
                                            self.log_knobs, self.log_score,
                                            self.log_track, didx[:n],
                                            self.extra.get("dsk"))
-        idx = didx[:n].cpu().numpy().astype(np.int64)
-        tiles, knobs = D.states_to_host(self.tables, t, kn, n)
-        f, sc = f.cpu().numpy(), sc.cpu().numpy()
+        # one synchronisation for the five results (pinned, async copies)
+        pins = scratch.host_pins(n, self.tables) if scratch is not None \
+            else None
+        if pins is None:
+            idx = didx[:n].cpu().numpy().astype(np.int64)
+            tiles, knobs = D.states_to_host(self.tables, t, kn, n)
+            f, sc = f.cpu().numpy(), sc.cpu().numpy()
+        else:
+            S = self.tables.local_slots
+            pi, pt, pk, pf, ps = pins
+            pi[:n].copy_(didx[:n], non_blocking=True)
+            pt[:S, :n].copy_(t[:S, :n], non_blocking=True)
+            pk[:, :n].copy_(kn[:, :n], non_blocking=True)
+            pf[:n].copy_(f[:n], non_blocking=True)
+            ps[:n].copy_(sc[:n], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            idx = pi[:n].numpy().astype(np.int64)
+            tiles = np.ascontiguousarray(
+                pt[:S, :n].numpy().astype(np.uint16).T)
+            knobs = np.ascontiguousarray(pk[:, :n].numpy().T)
+            f, sc = pf[:n].numpy().copy(), ps[:n].numpy().copy()
         o = np.argsort(idx, kind="stable")
         return (idx[o], tiles[o], knobs[o], f[o], sc[o], stats)
 

@@ -454,7 +454,10 @@ int harl_rank_topk(const harl_entry_log* log, int32_t local_slots,
  * [K]; out_pred [n] the final training predictions; out_base (device
  * double) y.mean(); out_ntrees (device int32) trees built before the
  * residual early stop.  The host renumbers nodes in the reference's
- * depth-first creation order. */
+ * depth-first creation order.  n_dev (optional device int32): the row
+ * count read at run time, n then being the capacity (X, y, out_pred and the
+ * scratch sized for n) -- one captured graph of the launch sequence serves
+ * every training-set size up to n. */
 int64_t harl_gbt_fit_scratch_bytes(int32_t n, int32_t feature_len,
                                    int32_t max_depth);
 int harl_gbt_fit(const double* X, const double* y, int32_t n,
@@ -462,7 +465,7 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
                  double learning_rate, int32_t min_leaf, void* scratch,
                  int64_t scratch_bytes, int32_t* out_feat, double* out_thr,
                  double* out_val, double* out_pred, double* out_base,
-                 int32_t* out_ntrees, void* stream);
+                 int32_t* out_ntrees, const int32_t* n_dev, void* stream);
 
 /* TrackSet.cull (stopping.py:68-86), host-side (no device pointers): the
  * n_elim live tracks with the lowest (advantage, -index) are eliminated

@@ -171,7 +171,7 @@ _SIGS = {
     "harl_cull_select": (i32, [vp, vp, i64, vp, i64, i64, vp, vp, P(i64)]),
     "harl_gbt_fit_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_gbt_fit": (i32, [vp, vp, i32, i32, i32, i32, f64, i32, vp, i64, vp,
-                           vp, vp, vp, vp, vp, vp]),
+                           vp, vp, vp, vp, vp, vp, vp]),
     "harl_rank_topk": (i32, [P(EntryLog), i32, i64, vp, vp, i64, i64, i64,
                              vp, i64, vp, i64, vp, vp]),
     "harl_selftest_tcgen05": (i32, [vp, vp, vp, i32, vp]),

@@ -41,6 +41,9 @@ struct FitArgs {
   const double* X;    // [n][F]
   const double* y;    // [n]
   int32_t n, F, K, max_depth, min_leaf;
+  int32_t ncap;       // row capacity: stride of the [F][ncap] lists
+  const int32_t* n_dev;  // optional: the row count read at run time
+                         // (a captured fit graph replayed for any n <= ncap)
   double lr;
   double* pred;       // [n]
   double* resid;      // [n]
@@ -64,20 +67,26 @@ struct FitArgs {
   double* out_val;    // [n_trees][K]
 };
 
+__device__ __forceinline__ int fit_n(const FitArgs& a) {
+  return a.n_dev ? *a.n_dev : a.n;
+}
+
 // ---- presort: one CTA per feature, bitonic sort of (x, index) ------------
 
 __device__ __forceinline__ bool fit_less(double xa, int ia, double xb, int ib) {
   return xa < xb || (!(xb < xa) && ia < ib);
 }
 
-__global__ void k_fit_presort(const double* __restrict__ X, int n, int F,
-                              int P2, int32_t* sorted_all) {
+__global__ void k_fit_presort(const double* __restrict__ X, int n_host,
+                              const int32_t* n_dev, int F, int P2, int ncap,
+                              int32_t* sorted_all) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   extern __shared__ __align__(16) unsigned char fsm_[];
   double* key = (double*)fsm_;
   int32_t* idx = (int32_t*)(key + P2);
   const int f = blockIdx.x;
+  const int n = n_dev ? *n_dev : n_host;
   for (int i = threadIdx.x; i < P2; i += blockDim.x) {
     key[i] = i < n ? X[(int64_t)i * F + f] : INFINITY;
     idx[i] = i < n ? i : 0x7fffffff;
@@ -99,7 +108,7 @@ __global__ void k_fit_presort(const double* __restrict__ X, int n, int F,
       __syncthreads();
     }
   for (int i = threadIdx.x; i < n; i += blockDim.x)
-    sorted_all[(int64_t)f * n + i] = idx[i];
+    sorted_all[(int64_t)f * ncap + i] = idx[i];
 }
 
 // ---- numpy pairwise summation over an index list --------------------------
@@ -189,10 +198,11 @@ __global__ void k_fit_base(FitArgs a) {
   __shared__ int s_starts[FIT_MAX_LEAVES], s_lens[FIT_MAX_LEAVES], s_cnt;
   __shared__ double s_sums[FIT_MAX_LEAVES];
   // identity list: pairwise over y in index order (ord[0] holds 0..n-1)
-  const double tot = fit_pw_cta(a.y, a.ord[0], 0, a.n, false, 0.0, s_starts,
+  const int n = fit_n(a);
+  const double tot = fit_pw_cta(a.y, a.ord[0], 0, n, false, 0.0, s_starts,
                                 s_lens, s_sums, &s_cnt);
-  const double base = __ddiv_rn(tot, (double)a.n);
-  for (int i = threadIdx.x; i < a.n; i += blockDim.x) a.pred[i] = base;
+  const double base = __ddiv_rn(tot, (double)n);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a.pred[i] = base;
   if (threadIdx.x == 0) {
     a.ctl->base = base;
     a.ctl->stop = 0;
@@ -201,9 +211,10 @@ __global__ void k_fit_base(FitArgs a) {
   }
 }
 
-__global__ void k_fit_iota(int32_t* ord, int n) {
+__global__ void k_fit_iota(int32_t* ord, int n_host, const int32_t* n_dev) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
+  const int n = n_dev ? *n_dev : n_host;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     ord[i] = i;
 }
@@ -214,7 +225,8 @@ __global__ void k_fit_tree_init(FitArgs a) {
   griddep_launch();
   if (a.ctl->stop) return;
   unsigned long long mx = 0ull;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+  const int n = fit_n(a);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
     const double r = __dsub_rn(a.y[i], a.pred[i]);
     a.resid[i] = r;
@@ -229,14 +241,14 @@ __global__ void k_fit_tree_init(FitArgs a) {
     mx = t > mx ? t : mx;
   }
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(&a.ctl->maxres_bits, mx);
-  for (int64_t e = blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)a.F * a.n;
+  for (int64_t e = blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)a.F * a.ncap;
        e += gridDim.x * blockDim.x)
-    a.srt[0][e] = a.sorted_all[e];
+    if ((int)(e % a.ncap) < n) a.srt[0][e] = a.sorted_all[e];
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K;
        k += gridDim.x * blockDim.x) {
     a.state[k] = k == 0 ? FS_OPEN : FS_NONE;
     a.seg_start[k] = 0;
-    a.seg_count[k] = k == 0 ? a.n : 0;
+    a.seg_count[k] = k == 0 ? n : 0;
     a.nleft[k] = 0;
   }
 }
@@ -304,7 +316,7 @@ __global__ void k_fit_best(FitArgs a, int d, int lists) {
   double* cs = s_c[(threadIdx.x >> 5) & 7];
   double* xs = s_x[(threadIdx.x >> 5) & 7];
   const int s = a.seg_start[k], m = a.seg_count[k];
-  const int32_t* list = a.srt[lists] + (int64_t)f * a.n + s;
+  const int32_t* list = a.srt[lists] + (int64_t)f * a.ncap + s;
   const double total = a.total[k];
   const double mf = (double)m;
   double best = -INFINITY;
@@ -432,7 +444,7 @@ __global__ void k_fit_split(FitArgs a, int d, int lists) {
     return;
   }
   const int s = a.seg_start[k];
-  const int32_t* list = a.srt[lists] + (int64_t)bf * a.n + s;
+  const int32_t* list = a.srt[lists] + (int64_t)bf * a.ncap + s;
   const double x0 = a.X[(int64_t)list[bp] * a.F + bf];
   const double x1 = a.X[(int64_t)list[bp + 1] * a.F + bf];
   a.feat[k] = bf;
@@ -446,7 +458,8 @@ __global__ void k_fit_route(FitArgs a) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   if (a.ctl->stop) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+  const int n = fit_n(a);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
     const int k = a.node_of[i];
     if (a.state[k] != FS_PEND) continue;
@@ -501,8 +514,8 @@ __global__ void k_fit_partition(FitArgs a, int d, int lists) {
   const int k = nl - 1 + node;
   if (a.state[k] != FS_SPLIT) return;
   const int s = a.seg_start[k], m = a.seg_count[k], L = a.nleft[k];
-  const int32_t* src = q == a.F ? a.ord[lists] : a.srt[lists] + (int64_t)q * a.n;
-  int32_t* dst = q == a.F ? a.ord[lists ^ 1] : a.srt[lists ^ 1] + (int64_t)q * a.n;
+  const int32_t* src = q == a.F ? a.ord[lists] : a.srt[lists] + (int64_t)q * a.ncap;
+  int32_t* dst = q == a.F ? a.ord[lists ^ 1] : a.srt[lists ^ 1] + (int64_t)q * a.ncap;
   int nlw = 0, nrw = 0;
   constexpr int PB = 8;   // chunks of 32 with their loads in flight together
   for (int c0 = 0; c0 < m; c0 += 32 * PB) {
@@ -538,7 +551,8 @@ __global__ void k_fit_pred(FitArgs a, int t) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
   if (a.ctl->stop) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+  const int n = fit_n(a);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += gridDim.x * blockDim.x) {
     const double v = a.out_val[(int64_t)t * a.K + a.node_of[i]];
     a.pred[i] = __dadd_rn(a.pred[i], __dmul_rn(a.lr, v));

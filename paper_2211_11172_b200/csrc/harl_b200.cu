@@ -1733,7 +1733,7 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
                  double learning_rate, int32_t min_leaf, void* scratch,
                  int64_t scratch_bytes, int32_t* out_feat, double* out_thr,
                  double* out_val, double* out_pred, double* out_base,
-                 int32_t* out_ntrees, void* stream) {
+                 int32_t* out_ntrees, const int32_t* n_dev, void* stream) {
   if (!X || !y || n < 1 || feature_len < 1 || n_trees < 0 || max_depth < 0 ||
       min_leaf < 1 || !scratch || !out_feat || !out_thr || !out_val ||
       !out_pred || !out_base || !out_ntrees) {
@@ -1756,6 +1756,8 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
   a.X = X;
   a.y = y;
   a.n = n;
+  a.ncap = n;
+  a.n_dev = n_dev;
   a.F = feature_len;
   a.K = (1 << (max_depth + 1)) - 1;
   a.max_depth = max_depth;
@@ -1792,10 +1794,10 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
   const unsigned gn = (unsigned)((n + 255) / 256 < sm_count() * 4 ? (n + 255) / 256 : sm_count() * 4);
   HARL_PROF_BEGIN(st);
   launch_k(k_fit_presort, dim3(feature_len), dim3(1024), ssmem, st, X, (int)n,
-           (int)feature_len, P2, (int32_t*)a.sorted_all);
+           n_dev, (int)feature_len, P2, (int)n, (int32_t*)a.sorted_all);
   HARL_CHECK_LAUNCH("k_fit_presort");
   HARL_PROF_BEGIN(st);
-  launch_k(k_fit_iota, dim3(gn), dim3(256), 0, st, a.ord[0], (int)n);
+  launch_k(k_fit_iota, dim3(gn), dim3(256), 0, st, a.ord[0], (int)n, n_dev);
   HARL_CHECK_LAUNCH("k_fit_iota");
   HARL_PROF_BEGIN(st);
   launch_k(k_fit_base, dim3(1), dim3(256), 0, st, a);

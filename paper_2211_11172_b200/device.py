@@ -380,11 +380,64 @@ def heap_tree_to_reference(feat_h, thr_h, val_h):
             np.asarray(value, np.float64))
 
 
+class _FitGraph:
+    """A captured GBT refit for training sets of up to ``ncap`` rows: the
+    ~2,000 launches of one fit recorded once (the kernels read the row count
+    from device memory), replayed per round with the new data copied into
+    the workspace -- the launch latency, not the work, dominates small
+    fits."""
+
+    def __init__(self, ncap, F, n_trees, max_depth, lr, min_leaf, dev):
+        lib = N.load()
+        self.ncap, self.F, self.T = ncap, F, max(n_trees, 1)
+        self.K = (1 << (max_depth + 1)) - 1
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.X = torch.zeros((ncap, F), **f64)
+        self.y = torch.zeros(ncap, **f64)
+        self.pred = torch.zeros(ncap, **f64)
+        self.base = torch.zeros(1, **f64)
+        self.nt = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.n_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.feat = torch.empty((self.T, self.K), dtype=torch.int32,
+                                device=dev)
+        self.thr = torch.empty((self.T, self.K), **f64)
+        self.val = torch.empty((self.T, self.K), **f64)
+        need = lib.harl_gbt_fit_scratch_bytes(ncap, F, max_depth)
+        self.scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+        self.args = (n_trees, max_depth, lr, min_leaf)
+        self.n_dev.fill_(1)
+        self._call()                       # eager once: attributes, checks
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            self._call()
+
+    def _call(self):
+        lib = N.load()
+        n_trees, max_depth, lr, min_leaf = self.args
+        N.check(lib.harl_gbt_fit(
+            _ptr(self.X), _ptr(self.y), self.ncap, self.F, n_trees, max_depth,
+            lr, min_leaf, _ptr(self.scratch), self.scratch.numel(),
+            _ptr(self.feat), _ptr(self.thr), _ptr(self.val), _ptr(self.pred),
+            _ptr(self.base), _ptr(self.nt), _ptr(self.n_dev), _stream()),
+            "harl_gbt_fit")
+
+    def run(self, Xd, yd, n):
+        self.X[:n].copy_(Xd)
+        self.y[:n].copy_(yd)
+        self.n_dev.fill_(n)
+        self.graph.replay()
+
+
+_FIT_GRAPHS: dict = {}
+
+
 def gbt_fit(X, y, n_trees: int = 50, max_depth: int = 6,
             learning_rate: float = 0.3, min_leaf: int = 1, device=None):
     """SurrogateModel.fit_incremental (costmodel.py:190-212) on the device:
     (X [n][F], y [n]) host or device arrays -> ``GbtFit``, bit-exact with
-    the reference's trees."""
+    the reference's trees.  Runs as a captured graph per (power-of-two row
+    capacity, F, config) -- HARL_FIT_EAGER=1 launches directly."""
     lib = N.load()
     dev = _dev(device)
     Xd = torch.as_tensor(np.ascontiguousarray(X, np.float64)
@@ -394,29 +447,48 @@ def gbt_fit(X, y, n_trees: int = 50, max_depth: int = 6,
                          if not isinstance(y, torch.Tensor) else y,
                          dtype=torch.float64).to(dev).contiguous()
     n, F = Xd.shape
-    need = lib.harl_gbt_fit_scratch_bytes(n, F, max_depth)
-    if need < 0:
+    if lib.harl_gbt_fit_scratch_bytes(n, F, max_depth) < 0 or n > 16384:
         raise DeviceError(f"gbt_fit: unsupported shape n={n} F={F} "
                           f"depth={max_depth}")
-    scratch = torch.empty(need, dtype=torch.uint8, device=dev)
-    K = (1 << (max_depth + 1)) - 1
-    T = max(n_trees, 1)
-    feat = torch.empty((T, K), dtype=torch.int32, device=dev)
-    thr = torch.empty((T, K), dtype=torch.float64, device=dev)
-    val = torch.empty((T, K), dtype=torch.float64, device=dev)
-    pred = torch.empty(n, dtype=torch.float64, device=dev)
-    base = torch.empty(1, dtype=torch.float64, device=dev)
-    nt = torch.zeros(1, dtype=torch.int32, device=dev)
-    with PF.span("gbt_fit", n):
-        N.check(lib.harl_gbt_fit(
-            _ptr(Xd), _ptr(yd), n, F, n_trees, max_depth, learning_rate,
-            min_leaf, _ptr(scratch), need, _ptr(feat), _ptr(thr), _ptr(val),
-            _ptr(pred), _ptr(base), _ptr(nt), _stream()), "harl_gbt_fit")
+    if os.environ.get("HARL_FIT_EAGER") == "1":
+        fg = None
+    else:
+        ncap = 1024
+        while ncap < n:
+            ncap <<= 1
+        key = (ncap, F, n_trees, max_depth, float(learning_rate), min_leaf,
+               dev)
+        fg = _FIT_GRAPHS.get(key)
+        if fg is None:
+            fg = _FIT_GRAPHS[key] = _FitGraph(ncap, F, n_trees, max_depth,
+                                              float(learning_rate), min_leaf,
+                                              dev)
+    with PF.span("gbt_fit", n, launches=None):
+        if fg is not None:
+            fg.run(Xd, yd, n)
+            feat, thr, val, pred = fg.feat, fg.thr, fg.val, fg.pred
+            base, nt = fg.base, fg.nt
+        else:
+            need = lib.harl_gbt_fit_scratch_bytes(n, F, max_depth)
+            scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+            K = (1 << (max_depth + 1)) - 1
+            T = max(n_trees, 1)
+            feat = torch.empty((T, K), dtype=torch.int32, device=dev)
+            thr = torch.empty((T, K), dtype=torch.float64, device=dev)
+            val = torch.empty((T, K), dtype=torch.float64, device=dev)
+            pred = torch.empty(n, dtype=torch.float64, device=dev)
+            base = torch.empty(1, dtype=torch.float64, device=dev)
+            nt = torch.zeros(1, dtype=torch.int32, device=dev)
+            N.check(lib.harl_gbt_fit(
+                _ptr(Xd), _ptr(yd), n, F, n_trees, max_depth, learning_rate,
+                min_leaf, _ptr(scratch), need, _ptr(feat), _ptr(thr),
+                _ptr(val), _ptr(pred), _ptr(base), _ptr(nt), None,
+                _stream()), "harl_gbt_fit")
     k = int(nt.item())
     fh, th, vh = (feat[:k].cpu().numpy(), thr[:k].cpu().numpy(),
                   val[:k].cpu().numpy())
     trees = [heap_tree_to_reference(fh[t], th[t], vh[t]) for t in range(k)]
-    return GbtFit(float(base.item()), trees, pred.cpu().numpy())
+    return GbtFit(float(base.item()), trees, pred[:n].cpu().numpy())
 
 
 # ---------------------------------------------------------------------------

@@ -500,6 +500,15 @@ int harl_brute_force(const harl_sketch_desc* sk, const harl_sim_desc* sim,
                      unsigned long long* out, unsigned long long* scratch,
                      int64_t scratch_len, void* stream);
 
+/* Host-side: harl_gbt_fit's heap-layout trees (host copies) -> the
+ * reference's node numbering (_fit_tree, costmodel.py:86-141), K slots per
+ * tree in and out; sizes[t] = nodes of tree t.  0 on success. */
+int harl_heap_to_creation_order(const int32_t* feat_h, const double* thr_h,
+                                const double* val_h, int K, int n_trees,
+                                int64_t* feature, double* threshold,
+                                int64_t* left, int64_t* right, double* value,
+                                int32_t* sizes);
+
 /* Instrumentation (no reference counterpart; the reference has no device).
  * harl_launch_count: kernels this library has launched since load (graph
  * replays excluded -- they do not pass through the library).

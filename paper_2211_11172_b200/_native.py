@@ -166,6 +166,8 @@ _SIGS = {
                             vp]),
     "harl_brute_force": (i32, [P(SketchDesc), P(SimDesc), u64, u64, vp, vp,
                                vp, i64, vp]),
+    "harl_heap_to_creation_order": (i32, [vp, vp, vp, i32, i32, vp, vp, vp,
+                                          vp, vp, vp]),
     "harl_format_floats": (C.c_longlong, [vp, C.c_longlong, vp, C.c_longlong,
                                           i32]),
     "harl_cull_select": (i32, [vp, vp, i64, vp, i64, i64, vp, vp, P(i64)]),

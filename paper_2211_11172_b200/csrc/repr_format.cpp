@@ -153,4 +153,57 @@ long long harl_format_floats(const double* v, long long n, char* out,
   return total;
 }
 
+// GBT refit output (heap layout: children of k at 2k+1, 2k+2; feat -2 = no
+// node, -1 = leaf) -> _fit_tree's node numbering (costmodel.py:86-141: an
+// explicit stack, left child first, both children allocated when the parent
+// splits).  Per tree t: out_* [t][K] with the reference arrays in their
+// first sizes[t] entries.
+int harl_heap_to_creation_order(const int32_t* feat_h, const double* thr_h,
+                                const double* val_h, int K, int n_trees,
+                                int64_t* feature, double* threshold,
+                                int64_t* left, int64_t* right, double* value,
+                                int32_t* sizes) {
+  if (!feat_h || !thr_h || !val_h || K < 1 || n_trees < 0 || !feature ||
+      !threshold || !left || !right || !value || !sizes)
+    return -1;
+  std::vector<int> stack, ref(K);
+  for (int t = 0; t < n_trees; ++t) {
+    const int32_t* fh = feat_h + (size_t)t * K;
+    const double* th = thr_h + (size_t)t * K;
+    const double* vh = val_h + (size_t)t * K;
+    int64_t* fo = feature + (size_t)t * K;
+    double* to = threshold + (size_t)t * K;
+    int64_t* lo = left + (size_t)t * K;
+    int64_t* ro = right + (size_t)t * K;
+    double* vo = value + (size_t)t * K;
+    int n = 1;
+    fo[0] = -1; to[0] = 0.0; lo[0] = -1; ro[0] = -1; vo[0] = 0.0;
+    ref[0] = 0;
+    stack.assign(1, 0);
+    while (!stack.empty()) {
+      const int h = stack.back();
+      stack.pop_back();
+      const int nid = ref[h];
+      vo[nid] = vh[h];
+      if (fh[h] < 0) continue;
+      if (2 * h + 2 >= K) return -2;
+      const int lid = n, rid = n + 1;
+      n += 2;
+      for (int c = lid; c <= rid; ++c) {
+        fo[c] = -1; to[c] = 0.0; lo[c] = -1; ro[c] = -1; vo[c] = 0.0;
+      }
+      ref[2 * h + 1] = lid;
+      ref[2 * h + 2] = rid;
+      fo[nid] = fh[h];
+      to[nid] = th[h];
+      lo[nid] = lid;
+      ro[nid] = rid;
+      stack.push_back(2 * h + 2);
+      stack.push_back(2 * h + 1);
+    }
+    sizes[t] = n;
+  }
+  return 0;
+}
+
 }  // extern "C"

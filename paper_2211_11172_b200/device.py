@@ -485,10 +485,40 @@ def gbt_fit(X, y, n_trees: int = 50, max_depth: int = 6,
                 _ptr(val), _ptr(pred), _ptr(base), _ptr(nt), None,
                 _stream()), "harl_gbt_fit")
     k = int(nt.item())
-    fh, th, vh = (feat[:k].cpu().numpy(), thr[:k].cpu().numpy(),
-                  val[:k].cpu().numpy())
-    trees = [heap_tree_to_reference(fh[t], th[t], vh[t]) for t in range(k)]
-    return GbtFit(float(base.item()), trees, pred[:n].cpu().numpy())
+    fh = np.ascontiguousarray(feat[:k].cpu().numpy())
+    th = np.ascontiguousarray(thr[:k].cpu().numpy())
+    vh = np.ascontiguousarray(val[:k].cpu().numpy())
+    return GbtFit(float(base.item()), heap_trees_to_reference(fh, th, vh),
+                  pred[:n].cpu().numpy())
+
+
+def heap_trees_to_reference(fh, th, vh):
+    """All trees of a fit through the native renumbering
+    (harl_heap_to_creation_order; ``heap_tree_to_reference`` is the same
+    rule in Python)."""
+    T, K = fh.shape if fh.ndim == 2 else (0, 1)
+    if T == 0:
+        return []
+    lib = N.load(require_device=False)
+    fo = np.empty((T, K), np.int64)
+    to = np.empty((T, K), np.float64)
+    lo = np.empty((T, K), np.int64)
+    ro = np.empty((T, K), np.int64)
+    vo = np.empty((T, K), np.float64)
+    sz = np.empty(T, np.int32)
+    # (arrays bound to names: a temporary's buffer may be freed before the
+    # call reads it)
+    fh = np.ascontiguousarray(fh, dtype=np.int32)
+    th = np.ascontiguousarray(th, dtype=np.float64)
+    vh = np.ascontiguousarray(vh, dtype=np.float64)
+    rc = lib.harl_heap_to_creation_order(
+        fh.ctypes.data, th.ctypes.data, vh.ctypes.data, K, T,
+        fo.ctypes.data, to.ctypes.data, lo.ctypes.data, ro.ctypes.data,
+        vo.ctypes.data, sz.ctypes.data)
+    if rc != 0:
+        raise DeviceError(f"harl_heap_to_creation_order failed ({rc})")
+    return [(fo[t, :sz[t]].copy(), to[t, :sz[t]].copy(), lo[t, :sz[t]].copy(),
+             ro[t, :sz[t]].copy(), vo[t, :sz[t]].copy()) for t in range(T)]
 
 
 # ---------------------------------------------------------------------------

@@ -119,3 +119,17 @@ def test_heap_renumbering_roundtrip(name):
     for tr in trees:
         got = heap_tree_to_reference(*_ref_to_heap(tr, 127))
         _same_trees([got], [tr])
+
+
+def test_native_heap_renumbering_matches_python():
+    """harl_heap_to_creation_order == heap_tree_to_reference (no GPU)."""
+    from paper_2211_11172_b200.device import (heap_tree_to_reference,
+                                              heap_trees_to_reference)
+    _, _, _, trees, _ = _case("large")
+    heaps = [_ref_to_heap(tr, 127) for tr in trees]
+    fh = np.stack([h[0] for h in heaps])
+    th = np.stack([h[1] for h in heaps])
+    vh = np.stack([h[2] for h in heaps])
+    got = heap_trees_to_reference(fh, th, vh)
+    _same_trees(got, trees)
+    _same_trees(got, [heap_tree_to_reference(*h) for h in heaps])

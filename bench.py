@@ -652,7 +652,7 @@ def main():
         "kernel_ms_per_episode": {k: round(v["ms"], 4)
                                   for k, v in r["kstats"].items()},
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:   # rank 0 at N=1 only
         steps = 2
         visits, secs = cpu_episode_sample(args.config, P, steps)
         line["cpu_baseline"] = {

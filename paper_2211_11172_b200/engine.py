@@ -60,6 +60,17 @@ _PY_CULL = os.environ.get("HARL_NATIVE_CULL") != "1"
 # k_finish_step) instead of the fused k_gbt_finish (A/B and fallback path)
 _SPLIT_FINISH = os.environ.get("HARL_SPLIT_FINISH") == "1"
 
+# HARL_PAR_VALUE=1: the value pass on a forked stream, concurrent with the
+# GBT pass (both read only X'); the finish kernel joins them (split finish).
+# Measured slower at 16 K tracks (5.95 vs 5.82 ms per C2 episode): both
+# kernels hold most of an SM's shared memory, so they do not co-reside
+_PAR_VALUE = os.environ.get("HARL_PAR_VALUE") == "1"
+
+# HARL_EAGER_CAPTURE=1: capture a plan's graphs on its first episode
+# instead of its second (C4 first visits, P = 4 K: 13.5 ms eager vs 18.5 ms
+# capture + replay per episode, profiles/c4_rounds.py)
+_LAZY_CAPTURE = os.environ.get("HARL_EAGER_CAPTURE") != "1"
+
 # host-side timeline of the graphed episode (profiles/host_probe.py sets a
 # list here; None = off)
 _HOST_TRACE = None
@@ -349,8 +360,17 @@ class EpisodeEngine:
         # V(X) and V(X') (the GBT and value passes both read only X')
         v_cur, v_next = b.vbuf[(k + 1) % 2], b.vbuf[k % 2]
         reuse = self._v_reusable(b.plan, k)
-        D.value_pair(self.dagent, cur["feat"], 0 if reuse else m, nxt["feat"],
-                     m, v_cur, v_next)
+        par = _PAR_VALUE
+        if par:
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
+                             nxt["feat"], m, v_cur, v_next)
+        else:
+            D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
+                         nxt["feat"], m, v_cur, v_next)
         po = b.pol_out
         io = N.StepBuffers(
             rt.data_ptr(), nxt["tiles"].data_ptr(), nxt["knobs"].data_ptr(),
@@ -363,7 +383,7 @@ class EpisodeEngine:
         cap = self.replay.cap
         keep_from = max(0, m - cap) if keep_from is None else keep_from
         wdev = D._ptr(b.wpos_tab[k:k + 1]) if graph_mode else None
-        if not _SPLIT_FINISH:
+        if not _SPLIT_FINISH and not par:
             with PF.span("gbt", m, launches=1):
                 rc = lib.harl_gbt_finish_step(
                     C.byref(b.forest.desc), tables.feature_len,
@@ -377,12 +397,20 @@ class EpisodeEngine:
                 N.check(rc, "harl_gbt_finish_step")
         D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
                       out=nxt["score"], reward=b.reward)
+        if par:
+            main.wait_stream(side)
         with PF.span("finish", m, launches=1):
             N.check(lib.harl_finish_step(
                 io, m, P, used, tables.local_slots, tables.feature_len,
                 self.rl_cfg.discount, 1, self.replay.desc, self.replay.wpos,
                 keep_from, b.elog, b.ts, wdev, D._stream()), "harl_finish_step")
         return res
+
+    def _side_stream(self):
+        s = getattr(self, "_side", None)
+        if s is None:
+            s = self._side = torch.cuda.Stream(device=self.dev)
+        return s
 
     def _launch_step_uniform(self, b, k, step, cur, nxt, rt, used, gen,
                              inj=None):
@@ -438,9 +466,14 @@ class EpisodeEngine:
         b = self._buffers(tables, cfg, forest, plan)
         # graphs for the production (tcgen05) path; the FFMA kernels used
         # by small test networks take their RNG state by value
+        # a plan's first episode runs eagerly: capturing costs more than the
+        # launches it saves once, and plans that change every episode (a
+        # filling replay buffer, task sets visited once) never repay it
+        b.uses = getattr(b, "uses", 0) + 1
         eager = (inject is not None or record is not None or
                  cull_override is not None or not self.use_graphs or
-                 not self.dagent.tc or not cfg.rl)
+                 not self.dagent.tc or not cfg.rl or
+                 (b.graphs is None and b.uses < 2 and _LAZY_CAPTURE))
         P = cfg.tracks
         # ---- population (outside any graph: the sampler may sync) -------
         cur, nxt = b.pop[0], b.pop[1]

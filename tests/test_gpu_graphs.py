@@ -37,20 +37,33 @@ def _setup(hidden, which):
     return tb, forest, cfg, engines
 
 
+@pytest.fixture(autouse=True)
+def _capture_first_use(monkeypatch):
+    """Capture on a plan's first episode so every episode here replays
+    graphs (the default runs a plan's first episode eagerly)."""
+    from paper_2211_11172_b200 import engine as E
+    monkeypatch.setattr(E, "_LAZY_CAPTURE", False)
+
+
 @pytest.mark.parametrize("hidden,which", [((128, 128), "conv"),
                                           ((32, 32), "bmm")])
-def test_graph_replay_is_bit_identical(hidden, which):
+@pytest.mark.parametrize("lazy", [False, True])
+def test_graph_replay_is_bit_identical(monkeypatch, hidden, which, lazy):
+    from paper_2211_11172_b200 import engine as E
+    monkeypatch.setattr(E, "_LAZY_CAPTURE", lazy)
     tb, forest, cfg, (eager, graphed) = _setup(hidden, which)
     g1, g2 = np.random.default_rng(5), np.random.default_rng(5)
-    for ep in range(3):
+    for ep in range(4 if lazy else 3):
         r1 = eager.run_episode(tb, forest, g1, cfg, 0)
         out1 = (r1.states(), r1.scores().copy(),
                 r1.log_reward[:r1.visits].cpu().numpy().copy(),
                 [c[1].copy() for c in r1.culls],
                 [t[1].cpu().numpy().copy() for t in r1.train])
         r2 = graphed.run_episode(tb, forest, g2, cfg, 0)
-        if graphed.dagent.tc:   # graphs are used on the tcgen05 path only
-            assert next(iter(graphed._cache.values())).graphs
+        # graphs are used on the tcgen05 path only; lazily, from a plan's
+        # second episode (the first episode's plan differs: empty replay)
+        if graphed.dagent.tc and (not lazy or ep >= 2):
+            assert any(b.graphs for b in graphed._cache.values())
         np.testing.assert_array_equal(r2.states()[0], out1[0][0])
         np.testing.assert_array_equal(r2.states()[1], out1[0][1])
         assert r2.scores().tobytes() == out1[1].tobytes()
@@ -69,13 +82,14 @@ def test_graph_replay_is_bit_identical(hidden, which):
 
 
 @pytest.mark.parametrize("flag", ["_FUSED_STEP", "_SPLIT_FEATURIZE",
-                                  "_SPLIT_FINISH"])
+                                  "_SPLIT_FINISH", "_PAR_VALUE"])
 def test_kernel_fusion_variants_match_default(monkeypatch, flag):
     """Each alternative launch structure produces the default episode bit
     for bit: _FUSED_STEP (k_policy_step_fused: policy -> sample/apply ->
     featurize in one kernel), _SPLIT_FEATURIZE (k_featurize2 launched after
     the sampler instead of inside it), _SPLIT_FINISH (k_gbt_predict2 +
-    k_finish_step instead of the fused k_gbt_finish)."""
+    k_finish_step instead of the fused k_gbt_finish), _PAR_VALUE (the value
+    pass on a forked stream beside the GBT pass, joined by the finish)."""
     from paper_2211_11172_b200 import engine as E
     tb, forest, cfg, (_, dflt) = _setup((128, 128), "conv")
     _, _, _, (_, alt) = _setup((128, 128), "conv")

@@ -145,20 +145,48 @@ __device__ inline u128 ldg_u128(const u128* p) {
 }
 
 __device__ inline u128 pcg_advance_tab(const PcgTab* T, u128 s, uint32_t k) {
+  // entry 0 of every level is the identity (A = 1, C = 0), so the four
+  // steps run unconditionally and all eight loads issue before the chain
+  u128 A[4], C[4];
 #pragma unroll
   for (int L = 0; L < 4; ++L) {
     const uint32_t b = (k >> (8 * L)) & 255u;
-    if (b) s = add128(mul128(ldg_u128(&T->A[L * 256 + b]), s),
-                      ldg_u128(&T->C[L * 256 + b]));
+    A[L] = ldg_u128(&T->A[L * 256 + b]);
+    C[L] = ldg_u128(&T->C[L * 256 + b]);
   }
+#pragma unroll
+  for (int L = 0; L < 4; ++L) s = add128(mul128(A[L], s), C[L]);
   return s;
 }
 
 // k-th draw with the table when there is one (and k fits), else bitwise
+// the table path split in two, so a caller can issue the eight loads early
+// and run the multiply chain once the base state has arrived
+__device__ inline void pcg_tab_load(const PcgTab* T, uint32_t k, u128* A,
+                                    u128* C) {
+#pragma unroll
+  for (int L = 0; L < 4; ++L) {
+    const uint32_t b = (k >> (8 * L)) & 255u;
+    A[L] = ldg_u128(&T->A[L * 256 + b]);
+    C[L] = ldg_u128(&T->C[L * 256 + b]);
+  }
+}
+__device__ inline u128 pcg_tab_apply(u128 s, const u128* A, const u128* C) {
+#pragma unroll
+  for (int L = 0; L < 4; ++L) s = add128(mul128(A[L], s), C[L]);
+  return s;
+}
+
+// (out of line: keeps the table path's callers compact in the i-cache)
+__device__ __noinline__ uint64_t pcg_draw64_bitwise(const PcgJump& J, u128 s,
+                                                    uint64_t k) {
+  return pcg_output(pcg_advance(J, s, k));
+}
+
 __device__ inline uint64_t pcg_draw64t(const PcgTab* T, const PcgJump& J,
                                        u128 s, uint64_t k) {
   if (T && k < (1ull << 32)) return pcg_output(pcg_advance_tab(T, s, (uint32_t)k));
-  return pcg_output(pcg_advance(J, s, k));
+  return pcg_draw64_bitwise(J, s, k);
 }
 
 __device__ inline double u64_to_unit(uint64_t x) {

@@ -761,16 +761,25 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   const int rows_per_cta = SAMPLE_THREADS / SG;
   const dim3 grid((unsigned)((n + rows_per_cta - 1) / rows_per_cta));
   HARL_PROF_BEGIN(st);
-  if (feat_out) {   // also featurize the successor states (schedspace.py:415)
-    const size_t smem = (size_t)rows_per_cta * sk->feature_len * 8;
-    int rc = allow_smem(k_sample_rows<true>, smem, "k_sample_rows");
-    if (rc) return rc;
-    launch_k(k_sample_rows<true>, grid, dim3(SAMPLE_THREADS), smem, st, *sk, J, LJ,
-             base, (const u128*)rng_state_dev, tiles, knobs, a, feat_out);
-  } else {
-    launch_k(k_sample_rows<false>, grid, dim3(SAMPLE_THREADS), 0, st, *sk, J, LJ,
-             base, (const u128*)rng_state_dev, tiles, knobs, a, (double*)nullptr);
-  }
+  const int nI = (sk->n_head0 + SG - 1) / SG;
+  auto go = [&](auto kfeat, auto kplain) -> int {
+    if (feat_out) {   // also featurize the successor states (schedspace.py:415)
+      const size_t smem = (size_t)rows_per_cta * sk->feature_len * 8;
+      int rc = allow_smem(kfeat, smem, "k_sample_rows");
+      if (rc) return rc;
+      launch_k(kfeat, grid, dim3(SAMPLE_THREADS), smem, st, *sk, J, LJ, base,
+               (const u128*)rng_state_dev, tiles, knobs, a, feat_out);
+    } else {
+      launch_k(kplain, grid, dim3(SAMPLE_THREADS), 0, st, *sk, J, LJ, base,
+               (const u128*)rng_state_dev, tiles, knobs, a, (double*)nullptr);
+    }
+    return HARL_OK;
+  };
+  int grc;
+  if (nI <= 8) grc = go(k_sample_rows<true, 8>, k_sample_rows<false, 8>);
+  else if (nI <= 12) grc = go(k_sample_rows<true, 12>, k_sample_rows<false, 12>);
+  else grc = go(k_sample_rows<true, 16>, k_sample_rows<false, 16>);
+  if (grc) return grc;
   HARL_CHECK_LAUNCH("k_sample_rows");
   return HARL_OK;
 }
@@ -1045,8 +1054,12 @@ int harl_prepare(void) {
   carve(k_gbt_predict2<false>);
   carve(k_policy_step);
   carve(k_value_forward);
-  carve(k_sample_rows<false>);
-  carve(k_sample_rows<true>);
+  carve(k_sample_rows<false, 8>);
+  carve(k_sample_rows<true, 8>);
+  carve(k_sample_rows<false, 12>);
+  carve(k_sample_rows<true, 12>);
+  carve(k_sample_rows<false, 16>);
+  carve(k_sample_rows<true, 16>);
   carve(k_gbt_finish<true>);
   carve(k_gbt_finish<false>);
   carve(k_trunk_tc<TRUNK_POLICY>);

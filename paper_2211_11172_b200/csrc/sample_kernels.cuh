@@ -103,16 +103,57 @@ __device__ inline int sample3(const float* z, uint32_t m3, double u,
   return ok ? idx : -1;
 }
 
+// inject mode (parity replays): lane 0 scores the given actions; out of
+// line so the sampling path stays compact in the instruction cache
+struct InjectRow {
+  int act[4];
+  int col0;
+  int dead;
+  double lp;
+};
+__device__ __noinline__ InjectRow sample_inject_row(
+    const float* z, int C0, int S, uint64_t mv, const int16_t* s_src,
+    const int16_t* s_dst, uint32_t sb, const int32_t* inject, int64_t n,
+    int64_t rr) {
+  InjectRow o;
+  int* act = o.act;
+  auto legal0 = [&](int j) -> bool {
+    return j == C0 - 1 || ((mv >> s_src[j]) & 1ull);
+  };
+  const int full = inject[rr];
+  int jj = -1;
+  if (full == S * S) jj = C0 - 1;
+  else if (full >= 0 && full < S * S)
+    for (int c = 0; c < C0 - 1; ++c)
+      if (s_src[c] == full / S && s_dst[c] == full % S) jj = c;
+  act[0] = full;
+  o.col0 = jj < 0 ? 0 : jj;
+  double lp = jj < 0 ? -INFINITY : row_logp(z, C0, legal0, jj);
+  bool d = false;
+  for (int h = 1; h < 4; ++h) {
+    const uint32_t m3 = (sb >> (3 * (h - 1))) & 7u;
+    act[h] = inject[h * n + rr];
+    lp += row_logp(z + C0 + 3 * (h - 1), 3,
+                   [&](int j) -> bool { return (m3 >> j) & 1u; }, act[h]);
+    d |= (m3 == 0);
+  }
+  o.lp = lp;
+  o.dead = d;
+  return o;
+}
+
 // One 8-lane group samples and applies the action of global row r (the
 // rows past a.n compute on row 0 and write nothing, so every lane stays in
 // the group shuffles).  zrow: the row's logits (null: a.logits + r*ldz);
 // s_src/s_dst: the compact head-0 column tables, filled by the caller.
+template <int MAXI = SAMPLE_MAXI>
 __device__ __forceinline__ void sample_group(
     const harl_sketch_desc& sk, const PcgJump& J, u128 base_arg,
     const u128* base_dev, const uint16_t* __restrict__ tiles,
     const uint8_t* __restrict__ knobs, const SampleArgs& a, int64_t r,
     const float* zrow, const int16_t* s_src, const int16_t* s_dst,
-    uint16_t* st_tiles = nullptr, uint8_t* st_knobs = nullptr) {
+    uint16_t* st_tiles = nullptr, uint8_t* st_knobs = nullptr,
+    bool fill_tables = false) {
   const int g = threadIdx.x & (SG - 1);
   // every group stays in the shuffles; out-of-range rows compute on row 0
   const bool live = r < a.n;
@@ -133,16 +174,21 @@ __device__ __forceinline__ void sample_group(
     tv[i] = s < sk.local_slots ? tiles[(int64_t)s * a.ld + rr] : 0;
   }
   const int ca0 = knobs[rr], par0 = knobs[a.ld + rr], ur0 = knobs[2 * a.ld + rr];
+  // this lane's draw: table entries loaded now, applied after the barrier
+  const uint64_t kdraw = (uint64_t)g * (uint64_t)a.m_total + (uint64_t)grow_r + 1;
+  const bool tab = draw && a.pcg_tab && kdraw < (1ull << 32);
+  u128 pA[4], pC[4];
+  if (tab) pcg_tab_load(a.pcg_tab, (uint32_t)kdraw, pA, pC);
   const float* z = zrow ? zrow : a.logits + rr * a.ldz;
   // lane g owns the contiguous head-0 columns [g*nI, g*nI + nI): local
   // max / sum / prefix, then one 8-lane scan of the lane totals
   const int nI = (C0 + SG - 1) / SG;
   const int jb = g * nI;
-  float zc[SAMPLE_MAXI];   // head-0 logits j = jb + i (padding reads as -inf)
+  float zc[MAXI];   // head-0 logits j = jb + i (padding reads as -inf)
   float z3[3] = {0.f, 0.f, 0.f};   // shift head g+1's three logits (lanes 0-2)
   if (!a.inject) {
 #pragma unroll
-    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+    for (int i = 0; i < MAXI; ++i) {
       const int j = jb + i;
       zc[i] = (i < nI && j < C0) ? z[j] : -INFINITY;
     }
@@ -151,12 +197,20 @@ __device__ __forceinline__ void sample_group(
       for (int j = 0; j < 3; ++j) z3[j] = z[C0 + 3 * g + j];
     }
   }
+  if (fill_tables) {
+    // the CTA's head-0 column tables, filled while the row loads above are
+    // in flight (the caller passes this CTA's shared arrays)
+    for (int i = threadIdx.x; i < C0; i += blockDim.x) {
+      const int16_t vs = sk.head0_src[i], vd = sk.head0_dst[i];
+      const_cast<int16_t*>(s_src)[i] = vs;
+      const_cast<int16_t*>(s_dst)[i] = vd;
+    }
+    __syncthreads();
+  }
   // ---- uniforms: lane h of the group draws head h ---------------------
   double u_mine = 0.0;
-  if (draw) {
-    const uint64_t k = (uint64_t)g * (uint64_t)a.m_total + (uint64_t)grow_r + 1;
-    u_mine = u64_to_unit(pcg_draw64t(a.pcg_tab, J, base, k));
-  }
+  if (tab) u_mine = u64_to_unit(pcg_output(pcg_tab_apply(base, pA, pC)));
+  else if (draw) u_mine = u64_to_unit(pcg_draw64_bitwise(J, base, kdraw));
   dbg_ts(17);
   // ---- current state: lane g holds slots g, g+8, ... --------------------
   uint64_t mv = 0;
@@ -177,47 +231,44 @@ __device__ __forceinline__ void sample_group(
   // ---- head 0: columns j = g + 8 i --------------------------------------
   if (a.inject) {
     if (g == 0) {
-      const int full = a.inject[rr];
-      int jj = -1;
-      if (full == S * S) jj = C0 - 1;
-      else if (full >= 0 && full < S * S)
-        for (int c = 0; c < C0 - 1; ++c)
-          if (s_src[c] == full / S && s_dst[c] == full % S) jj = c;
-      act[0] = full;
-      col0 = jj < 0 ? 0 : jj;
-      lp_total = jj < 0 ? -INFINITY : row_logp(z, C0, legal0, jj);
-      for (int h = 1; h < 4; ++h) {
-        const uint32_t m3 = (sb >> (3 * (h - 1))) & 7u;
-        act[h] = a.inject[h * a.n + rr];
-        lp_total += row_logp(z + C0 + 3 * (h - 1), 3,
-                             [&](int j) -> bool { return (m3 >> j) & 1u; },
-                             act[h]);
-        dead |= (m3 == 0);
-      }
+      const InjectRow o = sample_inject_row(z, C0, S, mv, s_src, s_dst, sb,
+                                            a.inject, a.n, rr);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) act[h] = o.act[h];
+      col0 = o.col0;
+      lp_total = o.lp;
+      dead = o.dead != 0;
     }
   } else {
     const double u0 = __shfl_sync(0xffffffffu, u_mine, 0, SG);
+    // the lane's cached columns: in range (rm) and legal (lm), tested once
+    uint32_t lm = 0, rm = 0;
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+      const int j = jb + i;
+      if (i < nI && j < C0) {
+        rm |= 1u << i;
+        if (legal0(j)) lm |= 1u << i;
+      }
+    }
     float zmax = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < SAMPLE_MAXI; ++i) {
-      const int j = jb + i;
-      if (i < nI && j < C0 && legal0(j)) zmax = fmaxf(zmax, zc[i]);
-    }
-    for (int i = SAMPLE_MAXI; i < nI; ++i) {   // wide heads (C0 > 128)
+    for (int i = 0; i < MAXI; ++i)
+      if ((lm >> i) & 1u) zmax = fmaxf(zmax, zc[i]);
+    for (int i = MAXI; i < nI; ++i) {   // wide heads (C0 > 128)
       const int j = jb + i;
       if (j < C0 && legal0(j)) zmax = fmaxf(zmax, z[j]);
     }
     zmax = gmaxf(zmax);
     dead |= (zmax == -INFINITY);
-    float e[SAMPLE_MAXI];
+    float e[MAXI];
     double sl = 0.0;
 #pragma unroll
-    for (int i = 0; i < SAMPLE_MAXI; ++i) {
-      const int j = jb + i;
-      e[i] = (i < nI && j < C0 && legal0(j)) ? expf(zc[i] - zmax) : 0.f;
+    for (int i = 0; i < MAXI; ++i) {
+      e[i] = ((lm >> i) & 1u) ? expf(zc[i] - zmax) : 0.f;
       sl += (double)e[i];
     }
-    for (int i = SAMPLE_MAXI; i < nI; ++i) {
+    for (int i = MAXI; i < nI; ++i) {
       const int j = jb + i;
       if (j < C0 && legal0(j)) sl += (double)expf(z[j] - zmax);
     }
@@ -228,8 +279,8 @@ __device__ __forceinline__ void sample_group(
     // exclusive scan of the lane totals (3 shuffle steps)
     double tot = 0.0;
 #pragma unroll
-    for (int i = 0; i < SAMPLE_MAXI; ++i) tot += (double)e[i] * inv;
-    for (int i = SAMPLE_MAXI; i < nI; ++i) {
+    for (int i = 0; i < MAXI; ++i) tot += (double)e[i] * inv;
+    for (int i = MAXI; i < nI; ++i) {
       const int j = jb + i;
       if (j < C0 && legal0(j)) tot += (double)expf(z[j] - zmax) * inv;
     }
@@ -242,11 +293,11 @@ __device__ __forceinline__ void sample_group(
     double c = incl - tot;   // exclusive offset
     int count = 0;
 #pragma unroll
-    for (int i = 0; i < SAMPLE_MAXI; ++i) {
+    for (int i = 0; i < MAXI; ++i) {
       c += (double)e[i] * inv;
-      if (i < nI && jb + i < C0 && c < u0) ++count;
+      if (((rm >> i) & 1u) && c < u0) ++count;
     }
-    for (int i = SAMPLE_MAXI; i < nI; ++i) {
+    for (int i = MAXI; i < nI; ++i) {
       const int j = jb + i;
       if (j < C0) {
         if (legal0(j)) c += (double)expf(z[j] - zmax) * inv;
@@ -388,7 +439,10 @@ __device__ __forceinline__ void featurize_group(const harl_sketch_desc& sk,
   }
 }
 
-template <bool FEAT>
+// MAXI: head-0 columns cached per lane (>= ceil(C0 / SG) for the cached
+// path; the host picks the smallest of 8 / 12 / 16 that covers the head so
+// the unrolled column loops carry no dead iterations)
+template <bool FEAT, int MAXI>
 __global__ void __launch_bounds__(SAMPLE_THREADS, HARL_SAMPLE_MINB)
 k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ PcgJump J,
@@ -406,16 +460,12 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   __shared__ uint8_t s_kn[FEAT ? ROWS : 1][4];
   extern __shared__ double s_feat[];   // FEAT: [ROWS][F]
   (void)LJ;
-  for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
-    s_src[i] = sk.head0_src[i];
-    s_dst[i] = sk.head0_dst[i];
-  }
-  __syncthreads();
   const int lr = threadIdx.x / SG;
   const int64_t r0 = (int64_t)blockIdx.x * ROWS;
   const int64_t r = r0 + lr;
-  sample_group(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src,
-               s_dst, FEAT ? s_st[lr] : nullptr, FEAT ? s_kn[lr] : nullptr);
+  sample_group<MAXI>(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src,
+               s_dst, FEAT ? s_st[lr] : nullptr, FEAT ? s_kn[lr] : nullptr,
+               /*fill_tables=*/true);
   dbg_ts(23);
   if (FEAT) {
     const int g = threadIdx.x & (SG - 1);

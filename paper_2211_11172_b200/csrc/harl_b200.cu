@@ -764,7 +764,9 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   const int nI = (sk->n_head0 + SG - 1) / SG;
   auto go = [&](auto kfeat, auto kplain) -> int {
     if (feat_out) {   // also featurize the successor states (schedspace.py:415)
-      const size_t smem = (size_t)rows_per_cta * sk->feature_len * 8;
+      const size_t lut = sk->max_extent + 1 <= FEAT_LUT_SMEM_MAX
+                             ? (size_t)(sk->max_extent + 1) * 8 : 0;
+      const size_t smem = (size_t)rows_per_cta * sk->feature_len * 8 + lut;
       int rc = allow_smem(kfeat, smem, "k_sample_rows");
       if (rc) return rc;
       launch_k(kfeat, grid, dim3(SAMPLE_THREADS), smem, st, *sk, J, LJ, base,

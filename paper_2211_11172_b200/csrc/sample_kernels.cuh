@@ -103,6 +103,50 @@ __device__ inline int sample3(const float* z, uint32_t m3, double u,
   return ok ? idx : -1;
 }
 
+// The footprint tables and the log2 LUT of the in-sampler featurize,
+// staged in shared memory by the CTA prologue: the descriptor's arrays live
+// in the kernel's parameter bank (indexed loads through the constant cache)
+// and the LUT in global memory, and on a cold SM each dependent lookup of
+// the per-term chain cost an L2 round trip (3.7 us for the footprint of
+// one row on the first CTA of an SM, phase probe).  Units are (tensor,
+// level) pairs so the row's 8 lanes share the products.
+constexpr int FEAT_LUT_SMEM_MAX = 1024;   // LUT entries staged (8 KB)
+struct FootSmem {
+  int16_t gi[HARL_MAX_TERMS];
+  int32_t sc[HARL_MAX_TERMS], off[HARL_MAX_TERMS];
+  int16_t tfirst[HARL_MAX_TENSORS], tn[HARL_MAX_TENSORS];
+  int32_t coef1[HARL_MAX_TENSORS];   // level 1: inter+extra on a stage's last tensor
+  int32_t coef2x[HARL_MAX_TENSORS];  // level 2: extra on the last tensor
+  int32_t coef2i[HARL_MAX_TENSORS];  // level 2 at the root: + inter
+};
+
+__device__ inline void foot_fill(const harl_sketch_desc& sk, FootSmem* fs,
+                                 double* lut_s, int lut_n) {
+  for (int q = threadIdx.x; q < sk.n_terms; q += blockDim.x) {
+    fs->gi[q] = sk.term_gi[q];
+    fs->sc[q] = sk.term_sc[q];
+    fs->off[q] = sk.term_off[q];
+  }
+  for (int ti = threadIdx.x; ti < sk.n_tensors; ti += blockDim.x) {
+    fs->tfirst[ti] = sk.tensor_first[ti];
+    fs->tn[ti] = sk.tensor_nterms[ti];
+    // the last tensor of each stage carries the stage terms
+    int c1 = 0, c2x = 0, c2i = 0;
+    for (int st = 0; st < sk.n_stages; ++st)
+      if (sk.stage_ntensors[st] > 0 &&
+          ti == sk.stage_first[st] + sk.stage_ntensors[st] - 1) {
+        c1 = sk.stage_inter[st] + sk.stage_extra[st];
+        c2x = sk.stage_extra[st];
+        c2i = sk.stage_inter[st];
+      }
+    fs->coef1[ti] = c1;
+    fs->coef2x[ti] = c2x;
+    fs->coef2i[ti] = c2i;
+  }
+  if (lut_s)
+    for (int v = threadIdx.x; v < lut_n; v += blockDim.x) lut_s[v] = __ldg(sk.log2_lut + v);
+}
+
 // inject mode (parity replays): lane 0 scores the given actions; out of
 // line so the sampling path stays compact in the instruction cache
 struct InjectRow {
@@ -153,7 +197,8 @@ __device__ __forceinline__ void sample_group(
     const uint8_t* __restrict__ knobs, const SampleArgs& a, int64_t r,
     const float* zrow, const int16_t* s_src, const int16_t* s_dst,
     uint16_t* st_tiles = nullptr, uint8_t* st_knobs = nullptr,
-    bool fill_tables = false) {
+    bool fill_tables = false, FootSmem* fs = nullptr, double* lut_s = nullptr,
+    int lut_n = 0) {
   const int g = threadIdx.x & (SG - 1);
   // every group stays in the shuffles; out-of-range rows compute on row 0
   const bool live = r < a.n;
@@ -205,6 +250,7 @@ __device__ __forceinline__ void sample_group(
       const_cast<int16_t*>(s_src)[i] = vs;
       const_cast<int16_t*>(s_dst)[i] = vd;
     }
+    if (fs) foot_fill(sk, fs, lut_s, lut_n);
     __syncthreads();
   }
   // ---- uniforms: lane h of the group draws head h ---------------------
@@ -415,25 +461,50 @@ __device__ __forceinline__ void sample_group(
 __device__ __forceinline__ void featurize_group(const harl_sketch_desc& sk,
                                                 int g, unsigned gmask,
                                                 const uint16_t* st,
-                                                const uint8_t* kn, double* dst) {
+                                                const uint8_t* kn, double* dst,
+                                                const FootSmem* fs,
+                                                const double* lut_s) {
   const int F = sk.feature_len, L = sk.levels;
   for (int k = g; k < F; k += SG) dst[k] = 0.0;
   __syncwarp(gmask);
-  for (int s2 = g; s2 < sk.local_slots; s2 += SG) dst[s2] = __ldg(sk.log2_lut + st[s2]);
+  dbg_ts(32);
+  for (int s2 = g; s2 < sk.local_slots; s2 += SG)
+    dst[s2] = lut_s ? lut_s[st[s2]] : __ldg(sk.log2_lut + st[s2]);
   const int ca = kn[0], par = kn[1], ur = kn[2];
+  dbg_ts(33);
   const int pos = sk.max_feature_dims * L;
+  // footprints (footprint_level's integer sums, schedspace.py:415-438):
+  // unit u = (tensor u/2, level 1 + u%2); per tensor e = prod over its
+  // terms of (sc * t[gi] + off), weighted 1 (+ the stage terms on a
+  // stage's last tensor); int64 sums, so the lane split is exact
+  const bool root = ca == 0;
+  long long l1 = 0, l2 = 0;
+  for (int u = g; u < 2 * sk.n_tensors; u += SG) {
+    const int ti = u >> 1;
+    const bool lv2 = (u & 1) && L >= 2;
+    long long e = 1;
+    const int f = fs->tfirst[ti], nt = fs->tn[ti];
+    for (int q = f; q < f + nt; ++q) {
+      const int d = fs->gi[q];
+      long long t = st[d * L + L - 1];
+      if (lv2) t *= st[d * L + L - 2];
+      e *= (long long)fs->sc[q] * t + fs->off[q];
+    }
+    if (u & 1) l2 += e * (1 + fs->coef2x[ti] + (root ? fs->coef2i[ti] : 0));
+    else l1 += e * (1 + fs->coef1[ti]);
+  }
+#pragma unroll
+  for (int o = SG / 2; o; o >>= 1) {
+    l1 += __shfl_xor_sync(gmask, l1, o, SG);
+    l2 += __shfl_xor_sync(gmask, l2, o, SG);
+  }
   if (g == 0) {
     dst[pos] = sk.ncas > 1 ? __ddiv_rn((double)ca, (double)(sk.ncas - 1)) : 0.0;
     dst[pos + 1] = sk.max_fusible ? __ddiv_rn((double)par, (double)sk.max_fusible) : 0.0;
     dst[pos + 2 + ur] = 1.0;
     dst[pos + 2 + sk.n_unroll + 2] = sk.flops_feature;
   } else if (g == 1 || g == 2) {
-    int64_t t[HARL_MAX_DIMS];
-    for (int d = 0; d < sk.ndims; ++d) {
-      const int vl = st[d * L + L - 1];
-      t[d] = (g == 2 && L >= 2) ? (int64_t)st[d * L + L - 2] * vl : vl;
-    }
-    const int64_t l = footprint_level(sk, t, g == 1, ca == 0);
+    const long long l = g == 1 ? l1 : l2;
     dst[pos + 2 + sk.n_unroll + g - 1] =
         __ddiv_rn(glibc_log10_ge1(__dadd_rn(1.0, (double)l)), 6.0);
   }
@@ -458,14 +529,18 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
   __shared__ uint16_t s_st[FEAT ? ROWS : 1][HARL_MAX_SLOTS];
   __shared__ uint8_t s_kn[FEAT ? ROWS : 1][4];
-  extern __shared__ double s_feat[];   // FEAT: [ROWS][F]
+  extern __shared__ double s_feat[];   // FEAT: [ROWS][F], then the LUT
+  __shared__ FootSmem s_foot[1];
   (void)LJ;
+  const int lut_n = sk.max_extent + 1;
+  double* lut_s = (FEAT && lut_n <= FEAT_LUT_SMEM_MAX)
+                      ? s_feat + (SAMPLE_THREADS / SG) * sk.feature_len : nullptr;
   const int lr = threadIdx.x / SG;
   const int64_t r0 = (int64_t)blockIdx.x * ROWS;
   const int64_t r = r0 + lr;
   sample_group<MAXI>(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src,
                s_dst, FEAT ? s_st[lr] : nullptr, FEAT ? s_kn[lr] : nullptr,
-               /*fill_tables=*/true);
+               /*fill_tables=*/true, FEAT ? s_foot : nullptr, lut_s, lut_n);
   dbg_ts(23);
   if (FEAT) {
     const int g = threadIdx.x & (SG - 1);
@@ -473,11 +548,16 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
                            << (threadIdx.x & (32 - SG));
     __syncwarp(gmask);
     const int F = sk.feature_len;
-    if (r < a.n) featurize_group(sk, g, gmask, s_st[lr], s_kn[lr], s_feat + lr * F);
+    if (r < a.n)
+      featurize_group(sk, g, gmask, s_st[lr], s_kn[lr], s_feat + lr * F,
+                      s_foot, lut_s);
+    dbg_ts(34);
     __syncthreads();
+    dbg_ts(35);
     const int64_t rows = a.n - r0 < ROWS ? a.n - r0 : ROWS;
     double* out = feat_out + r0 * F;
     for (int i = threadIdx.x; i < rows * F; i += blockDim.x) out[i] = s_feat[i];
+    dbg_ts(31);
   }
   dbg_grid(true, 60);
 }

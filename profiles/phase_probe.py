@@ -52,6 +52,11 @@ def main():
             t = ts[lo:lo + len(names)].astype(np.int64)
             rel = (t - t[0]) / 1e3
             print(f"rep {rep} {nm}: " + " ".join(f"{n}={r:.2f}" for n, r in zip(names, rel)))
+            if nm == "sample":   # featurize inside the sampler ends at 31
+                print(f"rep {rep} sample " + " ".join(
+                    f"{n}={(int(ts[i]) - int(ts[16])) / 1e3:.2f}" for n, i in
+                    (("feat_zeroed", 32), ("feat_lut", 33), ("feat_row", 34),
+                     ("feat_barrier", 35), ("featurized", 31))))
         if rep == 2:
             a0, a1, b0, b1 = (int(x) for x in ts[60:64])
             print(f"sampler grid {(a1 - a0) / 1e3:.2f} us, gap to featurize "

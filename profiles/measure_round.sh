@@ -8,4 +8,5 @@ python bench.py --config c3 --no-cpu-baseline > gpurun_out/${TAG:-v6}/c3.json 2>
 python bench.py --config c4 --no-cpu-baseline > gpurun_out/${TAG:-v6}/c4.json 2>>gpurun_out/${TAG:-v6}/sweep.err
 python profiles/segment_probe.py c2 > gpurun_out/${TAG:-v6}/segments.json 2>>gpurun_out/${TAG:-v6}/sweep.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/${TAG:-v6}/launches.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/${TAG:-v6}/ncu_bench.log 2>&1
-tail -c 300 gpurun_out/${TAG:-v6}/*.json
+
+ncu --set full --clock-control none --import-source on -k 'regex:k_sample_rows|k_gbt_finish|k_value_tc|k_policy_tc64' --launch-skip 150 --launch-count 4 -o gpurun_out/${TAG:-v6}/full python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/${TAG:-v6}/ncu_full.log 2>&1

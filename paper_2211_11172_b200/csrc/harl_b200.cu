@@ -1082,6 +1082,7 @@ int harl_prepare(void) {
   carve(k_ppo_wgrad);
   carve(k_ppo_finalize);
   carve(k_ppo_adam);
+  carve(k_ppo_wgrad_adam);
   carve(k_wt_fill);
   carve(k_tc_probe);
     cudaGetLastError();
@@ -1529,6 +1530,45 @@ int64_t harl_ppo_scratch_bytes(int32_t B, int32_t row_stride, int32_t n_jobs) {
          (int64_t)sizeof(GradJob) * 4 * (HARL_MAX_LAYERS + 2) + 256;
 }
 
+// HARL_PPO_FUSED_ADAM=1: k_ppo_wgrad + k_ppo_adam as one cooperative
+// kernel (its whole grid co-resident, a grid barrier between gradients and
+// Adam).  Bit-identical; the kernel itself is shorter (19.3 us live vs
+// 13.1 + 9.3) but the C2 episode measured slower (5.83-5.94 vs 5.79 ms):
+// the cooperative node costs more in the graph than the launch it saves.
+static bool fused_wgrad_adam_ok(int grid) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("HARL_PPO_FUSED_ADAM");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!env || use_pdl()) return false;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ppo_wgrad_adam, 256, 0) !=
+        cudaSuccess)
+      nb = 0;
+    per_sm = nb;
+  }
+  return (int64_t)per_sm * sm_count() >= grid;
+}
+
+// the grid barrier's {arrival count, generation} words (zeroed once)
+static int ppo_barrier_words(unsigned int** out) {
+  static unsigned int* words = nullptr;
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (!words) {
+    cudaError_t e = cudaMalloc(&words, 2 * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(words, 0, 2 * sizeof(unsigned int));
+    if (e != cudaSuccess) {
+      words = nullptr;
+      return cuda_status(e, "ppo barrier alloc");
+    }
+  }
+  *out = words;
+  return HARL_OK;
+}
+
 int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     const harl_ppo_hyper* hp, const harl_replay_ring* ring,
                     const int32_t* idx, int32_t B, int32_t feature_len,
@@ -1585,49 +1625,6 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   // rows + the split-reduction partials (PPO_SPLIT x PPO_TM x widest layer)
   const size_t rsmem = sizeof(double) * (PPO_TM * (size_t)row_stride + 8 +
                                          (size_t)PPO_SPLIT * PPO_TM * wmax);
-  if (phase & 1) {
-  if (use_ppo_tc()) {
-    // fp64 tensor-core rows kernel: 8 rows per CTA in shared memory
-    const size_t tsmem = sizeof(double) * (size_t)PPO8_ROWS * row_stride;
-    int rc2 = allow_smem(k_ppo_rows_tc, tsmem, "k_ppo_rows_tc");
-    if (rc2) return rc2;
-    if (B > 0) {
-      HARL_PROF_BEGIN(st);
-      launch_k(k_ppo_rows_tc, dim3((unsigned)((B + PPO8_ROWS - 1) / PPO8_ROWS), 2),
-               dim3(PPO8_THREADS), tsmem, st, a, *pol, *val, *ring, idx, params,
-               wt_params, rows, rowout);
-      HARL_CHECK_LAUNCH("k_ppo_rows_tc");
-    }
-  } else {
-    int rc2 = allow_smem(k_ppo_rows, rsmem, "k_ppo_rows");
-    if (rc2) return rc2;
-    if (B > 0) {
-      HARL_PROF_BEGIN(st);
-      launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM), 2), dim3(PPO_THREADS), rsmem, st, 
-          a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
-      HARL_CHECK_LAUNCH("k_ppo_rows");
-    }
-  }
-  GradJobs jt;
-  memset(&jt, 0, sizeof(jt));
-  for (int j = 0; j < n_jobs; ++j) jt.j[j] = jobs[j];
-  jt.n = n_jobs;
-  // one extra CTA sums the per-row loss terms (and, on a single device,
-  // forms the means and checks them) alongside the gradient tiles
-  HARL_PROF_BEGIN(st);
-  launch_k(k_ppo_wgrad, dim3((unsigned)n_tiles + 1), dim3(256), 0, st, jt, B, row_stride,
-           rows, grads, bad, phase == 3 ? 1 : 0, (const double*)rowout, losses,
-           phase == 3 ? B_norm : 0, hp->entropy_weight, hp->value_loss_weight);
-  HARL_CHECK_LAUNCH("k_ppo_wgrad");
-  }
-  if (!(phase & 2)) return HARL_OK;
-  if (phase == 2) {   // sharded: means and checks over the all-reduced sums
-    HARL_PROF_BEGIN(st);
-    launch_k(k_ppo_finalize, dim3(148), dim3(256), 0, st, B_norm, hp->entropy_weight,
-                                        hp->value_loss_weight, losses, grads,
-                                        n_params, bad);
-    HARL_CHECK_LAUNCH("k_ppo_finalize");
-  }
   AdamArgs ad;
   memset(&ad, 0, sizeof(ad));
   ad.n_pi = n_pi;
@@ -1659,6 +1656,73 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   if (val_trunk_img) add_trunk(*val, (uint8_t*)val_trunk_img, true);
   ad.tp = tplan;
   ad.wt = wt_params;
+  if (phase & 1) {
+  if (use_ppo_tc()) {
+    // fp64 tensor-core rows kernel: 8 rows per CTA in shared memory
+    const size_t tsmem = sizeof(double) * (size_t)PPO8_ROWS * row_stride;
+    int rc2 = allow_smem(k_ppo_rows_tc, tsmem, "k_ppo_rows_tc");
+    if (rc2) return rc2;
+    if (B > 0) {
+      HARL_PROF_BEGIN(st);
+      launch_k(k_ppo_rows_tc, dim3((unsigned)((B + PPO8_ROWS - 1) / PPO8_ROWS), 2),
+               dim3(PPO8_THREADS), tsmem, st, a, *pol, *val, *ring, idx, params,
+               wt_params, rows, rowout);
+      HARL_CHECK_LAUNCH("k_ppo_rows_tc");
+    }
+  } else {
+    int rc2 = allow_smem(k_ppo_rows, rsmem, "k_ppo_rows");
+    if (rc2) return rc2;
+    if (B > 0) {
+      HARL_PROF_BEGIN(st);
+      launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM), 2), dim3(PPO_THREADS), rsmem, st, 
+          a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
+      HARL_CHECK_LAUNCH("k_ppo_rows");
+    }
+  }
+  GradJobs jt;
+  memset(&jt, 0, sizeof(jt));
+  for (int j = 0; j < n_jobs; ++j) jt.j[j] = jobs[j];
+  jt.n = n_jobs;
+  // one extra CTA sums the per-row loss terms (and, on a single device,
+  // forms the means and checks them) alongside the gradient tiles
+  if (phase == 3 && fused_wgrad_adam_ok(n_tiles + 1)) {
+    // gradients and Adam in one cooperative launch (grid barrier between)
+    unsigned int* barw = nullptr;
+    int rcb = ppo_barrier_words(&barw);
+    if (rcb) return rcb;
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)n_tiles + 1);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HARL_PROF_BEGIN(st);
+    cudaLaunchKernelEx(&cfg, k_ppo_wgrad_adam, jt, B, row_stride,
+                       (const double*)rows, grads, bad, (const double*)rowout,
+                       losses, B_norm, hp->entropy_weight,
+                       hp->value_loss_weight, ad, adam_dev, params, adam_m,
+                       adam_v, params32, barw);
+    HARL_CHECK_LAUNCH("k_ppo_wgrad_adam");
+    return HARL_OK;
+  }
+  HARL_PROF_BEGIN(st);
+  launch_k(k_ppo_wgrad, dim3((unsigned)n_tiles + 1), dim3(256), 0, st, jt, B, row_stride,
+           rows, grads, bad, phase == 3 ? 1 : 0, (const double*)rowout, losses,
+           phase == 3 ? B_norm : 0, hp->entropy_weight, hp->value_loss_weight);
+  HARL_CHECK_LAUNCH("k_ppo_wgrad");
+  }
+  if (!(phase & 2)) return HARL_OK;
+  if (phase == 2) {   // sharded: means and checks over the all-reduced sums
+    HARL_PROF_BEGIN(st);
+    launch_k(k_ppo_finalize, dim3(148), dim3(256), 0, st, B_norm, hp->entropy_weight,
+                                        hp->value_loss_weight, losses, grads,
+                                        n_params, bad);
+    HARL_CHECK_LAUNCH("k_ppo_finalize");
+  }
   HARL_PROF_BEGIN(st);
   launch_k(k_ppo_adam, dim3(296), dim3(256), 0, st, ad, adam_dev, bad, grads, params, adam_m,
                                    adam_v, params32);

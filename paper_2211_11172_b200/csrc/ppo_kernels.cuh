@@ -718,13 +718,10 @@ struct GradJobs {
 // a CTA stages its 16 A columns and 16 D columns for 256 rows at a time
 // with all loads in flight.  check_finite: flag non-finite gradients here
 // (rlcore.py:368-373) so no separate scan is needed on a single device.
-__global__ void __launch_bounds__(256)
-k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
-            const double* __restrict__ rows, double* grads, int32_t* bad,
-            int check_finite, const double* rowout, double* losses,
-            int means_B, double w_ent, double w_val) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
+__device__ __forceinline__ void wgrad_body(
+    const GradJobs& jt, int B, int RS, const double* __restrict__ rows,
+    double* grads, int32_t* bad, int check_finite, const double* rowout,
+    double* losses, int means_B, double w_ent, double w_val) {
   dbg_ts(54);
   if (blockIdx.x == gridDim.x - 1) {   // the extra CTA: loss sums/means
     if (threadIdx.x < 32) ppo_losses_warp(B, rowout, losses, means_B, w_ent, w_val, bad);
@@ -823,6 +820,17 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
   }
 }
 
+__global__ void __launch_bounds__(256)
+k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
+            const double* __restrict__ rows, double* grads, int32_t* bad,
+            int check_finite, const double* rowout, double* losses,
+            int means_B, double w_ent, double w_val) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  wgrad_body(jt, B, RS, rows, grads, bad, check_finite, rowout, losses,
+             means_B, w_ent, w_val);
+}
+
 // (d) Adam over [0, n_pi) with the policy optimizer and [n_pi, n) with the
 // value optimizer.  Scalars precomputed on the host exactly as numpy does.
 // Where the updated fp32 weights also live in the tcgen05 weight images
@@ -878,17 +886,11 @@ __global__ void k_wt_fill(TransPlan tp, const double* params, double* wt) {
   }
 }
 
-__global__ void k_ppo_adam(const __grid_constant__ AdamArgs a,
-                           const double* adam_dev, const int32_t* bad,
-                           const double* grads, double* params, double* m,
-                           double* v, float* params32) {
-  // __grid_constant__: the pack/transposition plans are indexed with
-  // runtime loop counters; a by-value param would be copied to local memory
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
-  dbg_ts(50);
-  if (*bad) return;
-  dbg_ts(51);
+__device__ __forceinline__ void adam_body(const AdamArgs& a,
+                                          const double* adam_dev,
+                                          const double* grads, double* params,
+                                          double* m, double* v,
+                                          float* params32) {
   double b1t_pi = a.h.b1t_pi, b2t_pi = a.h.b2t_pi, b1t_v = a.h.b1t_v,
          b2t_v = a.h.b2t_v;
   if (adam_dev) {  // graph replay: this update's 1 - beta^t from device memory
@@ -947,6 +949,64 @@ __global__ void k_ppo_adam(const __grid_constant__ AdamArgs a,
       }
   }
   dbg_ts(53);
+}
+
+__global__ void k_ppo_adam(const __grid_constant__ AdamArgs a,
+                           const double* adam_dev, const int32_t* bad,
+                           const double* grads, double* params, double* m,
+                           double* v, float* params32) {
+  // __grid_constant__: the pack/transposition plans are indexed with
+  // runtime loop counters; a by-value param would be copied to local memory
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  dbg_ts(50);
+  if (*bad) return;
+  dbg_ts(51);
+  adam_body(a, adam_dev, grads, params, m, v, params32);
+}
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident):
+// arrival count + generation word, so it needs no reset between launches
+// of different grid sizes.
+__device__ inline void grid_barrier(unsigned int* count, unsigned int* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int g0;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen));
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      unsigned int g;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen));
+      } while (g == g0);
+    }
+  }
+  __syncthreads();
+}
+
+// (c)+(d) in one cooperative launch: every CTA writes its gradient tile
+// (the extra CTA the loss means and checks), one grid barrier publishes
+// them and the global finiteness flag, then every CTA runs its grid-stride
+// share of Adam -- one launch and one dependency gap less per update, same
+// arithmetic as k_ppo_wgrad + k_ppo_adam.
+__global__ void __launch_bounds__(256)
+k_ppo_wgrad_adam(const __grid_constant__ GradJobs jt, int B, int RS,
+                 const double* __restrict__ rows, double* grads, int32_t* bad,
+                 const double* rowout, double* losses, int means_B,
+                 double w_ent, double w_val, const __grid_constant__ AdamArgs a,
+                 const double* adam_dev, double* params, double* m, double* v,
+                 float* params32, unsigned int* bar) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  wgrad_body(jt, B, RS, rows, grads, bad, 1, rowout, losses, means_B, w_ent,
+             w_val);
+  grid_barrier(bar, bar + 1);
+  if (*(volatile int32_t*)bad) return;
+  adam_body(a, adam_dev, grads, params, m, v, params32);
 }
 
 }  // namespace harl

@@ -1079,8 +1079,9 @@ class DeviceAgent:
         if losses is None:
             losses = self.losses
         src = self.head0_src.ctypes.data_as(C.c_void_p)
-        with PF.span("ppo", B, launches=(2 if phase & 1 else 0) +
-                     (2 if phase == 2 else 1 if phase & 2 else 0)):
+        # (launch count from the library: 2 when wgrad and Adam run as one
+        # cooperative kernel, 3 otherwise)
+        with PF.span("ppo", B, launches=None):
           N.check(lib.harl_ppo_update(
             C.byref(self.pol_layout), C.byref(self.val_layout), C.byref(hp),
             C.byref(ring.desc), _ptr(slots), B, self.F, self.C0, src,

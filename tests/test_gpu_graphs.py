@@ -111,3 +111,22 @@ def test_kernel_fusion_variants_match_default(monkeypatch, flag):
         assert torch.equal(dflt.replay.Xn, alt.replay.Xn)
         assert g1.bit_generator.state == g2.bit_generator.state
 
+
+
+def test_fused_wgrad_adam_matches_separate_launches():
+    """HARL_PPO_FUSED_ADAM=1 (gradients + Adam in one cooperative kernel
+    with a grid barrier) leaves the same parameters, moments, replay ring
+    and scores as the default two launches, bit for bit."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    script = os.path.join(here, "_episode_digest.py")
+    out = []
+    for flag in ("0", "1"):
+        env = dict(os.environ, HARL_PPO_FUSED_ADAM=flag)
+        r = subprocess.run([sys.executable, script], env=env, text=True,
+                           capture_output=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append(r.stdout.strip().splitlines()[-1])
+    assert out[0] == out[1]

@@ -25,11 +25,14 @@ struct LaneJump {
 #ifndef HARL_SAMPLE_LANES
 #define HARL_SAMPLE_LANES 8
 #endif
+#ifndef HARL_SAMPLE_ROWS
+#define HARL_SAMPLE_ROWS 16     // rows per CTA
+#endif
 #ifndef HARL_SAMPLE_MINB
-#define HARL_SAMPLE_MINB (8 * 8 / HARL_SAMPLE_LANES)
+#define HARL_SAMPLE_MINB (8 * 8 * 16 / (HARL_SAMPLE_LANES * HARL_SAMPLE_ROWS))
 #endif
 constexpr int SG = HARL_SAMPLE_LANES;   // lanes cooperating on one row
-constexpr int SAMPLE_THREADS = 16 * SG;  // 16 rows per CTA
+constexpr int SAMPLE_THREADS = HARL_SAMPLE_ROWS * SG;
 constexpr int SAMPLE_MAXI = 16;        // cached exps per lane (C0 <= 128)
 
 struct SampleArgs {

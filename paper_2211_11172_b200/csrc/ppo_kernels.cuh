@@ -36,7 +36,10 @@ typedef harl_replay_ring PpoRing;
 #ifndef HARL_PPO_WIDE
 #define HARL_PPO_WIDE 2
 #endif
-constexpr int PPO_TM = 2;
+#ifndef HARL_PPO_TM
+#define HARL_PPO_TM 2          // minibatch rows per CTA
+#endif
+constexpr int PPO_TM = HARL_PPO_TM;
 // HARL_PPO_WIDE x 4 warps per row: the loss terms use 4 warps per row, the
 // dense layers split each output's reduction over the extra threads
 constexpr int PPO_THREADS = 128 * PPO_TM * HARL_PPO_WIDE;

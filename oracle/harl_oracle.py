@@ -751,8 +751,10 @@ def run_episode(tb, num_slots, cfg: EpisodeCfg, agent: Agent, opt_pi: Adam,
     """tuner.py:350-440.  Returns (entries, new order_counter, summary).
 
     ``follow(step, info)`` (optional) returns a dict that may override the
-    sampled actions (``"actions"``) or the culled tracks (``"cull"``) so a
-    GPU trajectory can be replayed and checked step by step."""
+    sampled actions (``"actions"``), the culled tracks (``"cull"``) or the
+    network outputs pushed into the replay FIFO (``"logp"``/``"adv"``/
+    ``"td"``, phase "push") so a GPU trajectory can be replayed and checked
+    step by step."""
     p = cfg.tracks
     budget = p * cfg.track_len
     tiles, knobs = sample_initial(tb, p, rng)
@@ -804,7 +806,15 @@ def run_episode(tb, num_slots, cfg: EpisodeCfg, agent: Agent, opt_pi: Adam,
             v_next, _ = agent.value(nf)
             adv = rewards + rl_cfg.discount * v_next - v_cur
             td = rewards + rl_cfg.discount * v_next
-            replay.push_rows(X, nf, acts, logp, rewards, adv, td, masks)
+            push = (logp, adv, td)
+            if follow is not None:
+                # optional: the replayed trajectory's own network outputs
+                # go into the FIFO, so later PPO updates see its inputs
+                ov = follow(t, {"phase": "push"})
+                push = tuple(ov.get(k) if ov.get(k) is not None else v
+                             for k, v in zip(("logp", "adv", "td"), push))
+            replay.push_rows(X, nf, acts, push[0], rewards, push[1], push[2],
+                             masks)
         tiles[sel], knobs[sel], feats[sel], score[sel] = nt, nk, nf, new
         steps[sel] += 1
         better = new > best[sel]

@@ -55,6 +55,7 @@ def _device_fit_incremental(model, examples):
     with the old ensemble evaluated by the GBT kernel without its floor,
     loss_after from the fit's own final predictions."""
     from schedtune.costmodel import CostModelError, FitReport, _Tree
+    from .errors import DeviceError
     if not examples:
         raise CostModelError("fit_incremental needs at least one example")
     cfg = model.cfg
@@ -73,9 +74,12 @@ def _device_fit_incremental(model, examples):
     else:
         raw = np.ones(len(y), dtype=np.float64)
     before = float(np.mean((raw - y) ** 2))
-    fit = D.gbt_fit(Xd, y, n_trees=cfg.n_trees, max_depth=cfg.max_depth,
-                    learning_rate=cfg.learning_rate,
-                    min_leaf=cfg.min_samples_leaf)
+    try:
+        fit = D.gbt_fit(Xd, y, n_trees=cfg.n_trees, max_depth=cfg.max_depth,
+                        learning_rate=cfg.learning_rate,
+                        min_leaf=cfg.min_samples_leaf)
+    except DeviceError:                 # a shape the device fit rejects
+        return model._b200_host_fit(examples)
     model.base = fit.base
     model.fitted = True
     model.trees = [_Tree(feature=f, threshold=t, left=l, right=r, value=v)
@@ -258,15 +262,13 @@ def b200_session_class(base):
                 m.fit_incremental = types.MethodType(_device_fit_incremental, m)
                 m._b200_refit_of = m
 
-        def _run_episode(self, sg, sketch, rnd):
-            self._b200_hook_model()
-            ecfg = EpisodeConfig.from_tuner(self.cfg, self.searcher)
+        def _b200_prepare(self, sg, sketch):
+            """Everything the device episode needs before it touches the
+            session state: the engine, the sketch tables and the forest.
+            Raises ScheduleError/DeviceError for shapes beyond the device
+            tables (an extent above 65535, more than 64 slots, ...)."""
             eng = self._b200_engine(sg)
             tables = self._b200_sketch_tables(sg, sketch)
-            eng.dagent.upload()
-            buf = self.buffers[sg.id]
-            if not buf._on_device:
-                self._b200_load_ring(eng, sg)
             forest = getattr(self, "_b200_forest", None)
             if forest is None or not forest.load_model(self.model):
                 # capacity for the refits to come (n_estimators trees of
@@ -278,8 +280,42 @@ def b200_session_class(base):
                     self.model, node_capacity=trees * (2 ** (depth + 1)),
                     tree_capacity=trees)
                 self._b200_forest = forest
-            res = eng.run_episode(tables, forest, self.rng, ecfg,
-                                  self.order_counter)
+            return eng, tables, forest
+
+        def _run_episode(self, sg, sketch, rnd):
+            from .errors import DeviceError, ScheduleError
+            self._b200_hook_model()
+            host = getattr(self, "_b200_host_sketches", None)
+            if host is None:
+                host = self._b200_host_sketches = set()
+            key = (sg.id, sketch.id)
+            if key not in host:
+                try:
+                    eng, tables, forest = self._b200_prepare(sg, sketch)
+                except (ScheduleError, DeviceError):
+                    # beyond the device tables: this sketch runs on the
+                    # reference's own path from now on (nothing of the
+                    # session state has been touched yet)
+                    host.add(key)
+            if key in host:
+                # the reference reads the deque and the numpy agent, both
+                # current (RingBuffer materialises the device ring;
+                # sync_to_host ran after the last device episode)
+                return super()._run_episode(sg, sketch, rnd)
+            ecfg = EpisodeConfig.from_tuner(self.cfg, self.searcher)
+            eng.dagent.upload()
+            buf = self.buffers[sg.id]
+            if not buf._on_device:
+                self._b200_load_ring(eng, sg)
+            from .errors import to_reference
+            try:
+                res = eng.run_episode(tables, forest, self.rng, ecfg,
+                                      self.order_counter)
+            except (ValueError, RuntimeError) as exc:
+                ref = to_reference(exc)
+                if ref is None:
+                    raise
+                raise ref from exc
             eng.sync_to_host()
             # the replay FIFO now lives in the device ring; the deque is
             # rebuilt only if something reads it (_RingBuffer)

@@ -1926,8 +1926,9 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
 
 
 // TrackSet.cull (stopping.py:68-86) on the host: the n_elim live tracks
-// with the lowest (advantage, -index) go (NaN advantages order last, as a
-// numpy sort puts them).  rows: the cull step's m rows (row r = track
+// with the lowest (advantage, -index) go, for finite advantages (the
+// engine routes a step with a NaN advantage to shard.eliminated, which runs
+// the reference's own comparison sort; here NaN keys would order last).  rows: the cull step's m rows (row r = track
 // tracks[r], advantage adv[r]); alive (per track, 0/1) is updated; gone_out
 // gets the eliminated track ids ascending, keep_out the surviving rows
 // ascending (the survivor gather's index list).

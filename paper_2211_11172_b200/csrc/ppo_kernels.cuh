@@ -43,6 +43,8 @@ constexpr int PPO_TM = HARL_PPO_TM;
 // HARL_PPO_WIDE x 4 warps per row: the loss terms use 4 warps per row, the
 // dense layers split each output's reduction over the extra threads
 constexpr int PPO_THREADS = 128 * PPO_TM * HARL_PPO_WIDE;
+static_assert(PPO_TM >= 1 && HARL_PPO_WIDE >= 1 && PPO_THREADS <= 1024,
+              "HARL_PPO_TM x HARL_PPO_WIDE: at most 1024 threads per CTA");
 
 // Latency-bound small-batch layers: every thread keeps PPO_UNR weight
 // loads in flight (issued before the FMAs that consume them); the CTA's

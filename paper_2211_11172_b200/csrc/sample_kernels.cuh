@@ -34,6 +34,8 @@ struct LaneJump {
 constexpr int SG = HARL_SAMPLE_LANES;   // lanes cooperating on one row
 constexpr int SAMPLE_THREADS = HARL_SAMPLE_ROWS * SG;
 constexpr int SAMPLE_MAXI = 16;        // cached exps per lane (C0 <= 128)
+static_assert(SAMPLE_THREADS <= 1024, "HARL_SAMPLE_ROWS x HARL_SAMPLE_LANES: at most 1024 threads");
+static_assert(HARL_SAMPLE_MINB >= 1, "HARL_SAMPLE_MINB must be at least 1");
 
 struct SampleArgs {
   const float* logits;   // [n][ldz] (head0 compact columns, then 3x3)

@@ -918,6 +918,7 @@ class DeviceAgent:
         self.tc = (hidden == (128, 128) and F <= 64 and self.NH <= 128
                    and os.environ.get("HARL_KERNELS", "tc") != "ffma")
         self._hid = None
+        self._retired = []      # scratch buffers graphs may still address
         self.packed = None
         if self.tc:
             lib = N.load()
@@ -1047,10 +1048,26 @@ class DeviceAgent:
         self.pol_desc, self.val_desc = pd, vd
 
     def hid_scratch(self, n: int):
+        """The logits scratch of the tcgen05 policy path, grown on demand.
+        A replaced buffer is retired, not freed: CUDA graphs captured
+        against it (other episode geometries cached by the engine) keep
+        its address baked in."""
         if self._hid is None or self._hid.shape[0] < n:
+            if self._hid is not None:
+                self._retired.append(self._hid)
             self._hid = torch.empty((max(n, 1), 128), dtype=torch.float32,
                                     device=self.device)
         return self._hid
+
+    def raise_if_diverged(self):
+        """ppo_update's finiteness checks (rlcore.py:368-373): the kernels
+        set ``bad`` (1: a loss, 2: a gradient) and skip the Adam step; the
+        host raises the reference's RlDivergedError."""
+        code = int(self.bad.item())
+        if code & 1:
+            raise RlDivergedError("actor or critic loss is not finite")
+        if code:
+            raise RlDivergedError("non-finite gradient in update")
 
     # -- PPO ----------------------------------------------------------------
 

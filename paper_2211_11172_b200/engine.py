@@ -492,9 +492,7 @@ class EpisodeEngine:
         st = b.status.cpu().numpy().view(np.uint64)
         for code in st[:len(plan)]:
             D.raise_status(int(code))
-        if int(self.dagent.bad.item()):
-            from .errors import RlDivergedError
-            raise RlDivergedError("non-finite loss or gradient in update")
+        self.dagent.raise_if_diverged()
         return res
 
     def _episode_prologue(self, b, forest):
@@ -551,15 +549,26 @@ class EpisodeEngine:
                 cur, nxt = nxt, cur
                 used += m
                 continue
+            # a record may name the steps it wants (``record.steps``): the
+            # full-size parity tests keep a few steps of a 1 M-row episode
+            want = record is not None and \
+                (getattr(record, "steps", None) is None or
+                 step["t"] in record.steps)
+            if want:
+                rng_before = gen.bit_generator.state
+                params_before = self.dagent.params.clone()
             res = self._launch_step(b, k, step, cur, nxt, rt, used, False,
-                                    gen=gen, inj=inj,
-                                    want_logits=record is not None)
+                                    gen=gen, inj=inj, want_logits=want)
             if inj is not None:
                 R.skip_u64(gen, 4 * m)
             self.replay.note_push(m)
-            if record is not None:
+            if want:
                 po = b.pol_out
                 record.append({"t": step["t"], "m": m,
+                               "rng_before": rng_before,
+                               "params": params_before,
+                               "tiles": cur["tiles"][:, :m].clone(),
+                               "knobs": cur["knobs"][:, :m].clone(),
                                "sel": rt[:m].clone(),
                                "X": cur["feat"][:m].clone(),
                                "actions": po["actions"].view(-1)[:4 * m]
@@ -592,7 +601,7 @@ class EpisodeEngine:
                 self._compact(b, cur, rt, nxt, rt_spare, len(keep))
                 cur, nxt = nxt, cur
                 rt, rt_spare = rt_spare, rt
-                if record is not None:
+                if want:
                     record[-1]["cull"] = gone
             if step["ppo"]:
                 B = step["ppo"]
@@ -604,7 +613,7 @@ class EpisodeEngine:
                 self._launch_ppo(b, ppo_k, B, slots_t, a.opt_pi.t, a.opt_v.t,
                                  False)
                 train.append((step["t"], b.losses[ppo_k], B))
-                if record is not None:
+                if want:
                     record[-1]["ppo_idx"] = idx
                 ppo_k += 1
         return self._result(b, cfg, order_counter, used, culls, train, alive)
@@ -723,9 +732,7 @@ class EpisodeEngine:
         st = b.status.cpu().numpy().view(np.uint64)
         for code in st[:len(plan)]:
             D.raise_status(int(code))
-        if int(self.dagent.bad.item()):
-            from .errors import RlDivergedError
-            raise RlDivergedError("non-finite loss or gradient in update")
+        self.dagent.raise_if_diverged()
         res = self._result(b, cfg, order_counter, used_local, culls, train,
                            alive)
         res.extra["global_visits"] = used
@@ -958,9 +965,9 @@ class EpisodeEngine:
         adv_full = np.zeros(len(alive))
         adv_full[tracks] = a
         v = adv_full[live]
-        if np.isnan(v).any():      # NaN orders last, as in the full sort
-            order = np.lexsort((-live, v))
-            gone = np.sort(live[order[:n_elim]])
+        if np.isnan(v).any():      # the reference's own sort (shard.py)
+            from .shard import eliminated
+            gone = eliminated(live, v, n_elim)
         else:
             cut = np.partition(v, n_elim - 1)[n_elim - 1]
             below = live[v < cut]
@@ -979,7 +986,7 @@ class EpisodeEngine:
                      m - cfg.min_tracks)
         if n_elim <= 0:
             return np.zeros(0, dtype=np.int64), np.arange(m, dtype=np.int32)
-        if np.isnan(adv).any():          # NaN orders last: the full sort
+        if np.isnan(adv).any():          # the reference's sort (_cull)
             gone = self._cull(tracks, adv, m, alive, cfg)
             return gone, np.flatnonzero(alive[tracks]).astype(np.int32)
         cut = np.partition(adv, n_elim - 1)[n_elim - 1]
@@ -1012,6 +1019,14 @@ class EpisodeEngine:
         pt[:m].copy_(b.rt[rt_i][:m], non_blocking=True)
         pa[:m].copy_(b.adv[:m], non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if np.isnan(pa[:m].numpy()).any():   # the reference's sort (_cull)
+            tracks = pt[:m].numpy().astype(np.int64)
+            gone, keep = self._cull_rows(tracks, pa[:m].numpy().copy(),
+                                         alive, cfg)
+            b.keep_pin[:len(keep)].numpy()[:] = keep
+            b.keep[:len(keep)].copy_(b.keep_pin[:len(keep)],
+                                     non_blocking=True)
+            return gone
         a8 = b.alive8
         a8[:len(alive)] = alive
         gone = np.zeros(n_elim, dtype=np.int64)
@@ -1057,6 +1072,10 @@ class EpisodeEngine:
         lib = N.load()
         need = lib.harl_ppo_scratch_bytes(B, self.dagent.row_stride, 0)
         if self._ppo_scratch is None or self._ppo_scratch.numel() < need:
+            # the old buffer is retired, not freed: graphs captured for
+            # other cached geometries keep its address baked in
+            if self._ppo_scratch is not None:
+                self.dagent._retired.append(self._ppo_scratch)
             self._ppo_scratch = torch.empty(need, dtype=torch.uint8,
                                             device=self.dev)
 

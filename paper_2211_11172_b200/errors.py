@@ -22,6 +22,7 @@ class InvalidActionError(ValueError):
     def __init__(self, subspace: str, detail: str):
         super().__init__(f"invalid {subspace} action: {detail}")
         self.subspace = subspace
+        self.detail = detail
 
 
 class RlDivergedError(RuntimeError):
@@ -43,3 +44,25 @@ class SpaceTooLarge(DeviceError):
         super().__init__(f"space has {size} states, above the cap of {cap}")
         self.size = size
         self.cap = cap
+
+
+def to_reference(exc: BaseException):
+    """The reference package's own exception for one of ours (the drop-in
+    raises these, so ``except schedtune.rlcore.RlDivergedError`` and
+    friends catch device failures).  None when ``exc`` has no reference
+    counterpart or the reference is not importable."""
+    try:
+        from schedtune import costmodel, rlcore, schedspace, workload
+    except ImportError:
+        return None
+    if isinstance(exc, InvalidActionError):
+        return schedspace.InvalidActionError(exc.subspace,
+                                             getattr(exc, "detail", str(exc)))
+    table = ((RlDivergedError, rlcore.RlDivergedError),
+             (ScheduleError, schedspace.ScheduleError),
+             (CostModelError, costmodel.CostModelError),
+             (WorkloadError, workload.WorkloadError))
+    for ours, theirs in table:
+        if isinstance(exc, ours):
+            return theirs(*exc.args)
+    return None

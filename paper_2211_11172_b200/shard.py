@@ -75,6 +75,30 @@ class GlobalReplayIndex:
                 np.asarray([s[1] for s in sel], dtype=np.int64))
 
 
+def eliminated(live, adv_live, n_elim):
+    """The ``n_elim`` tracks TrackSet.cull eliminates (stopping.py:80-86):
+    ``sorted(live, key=(advantage, -index))[:n_elim]``, ascending ids.
+    ``live`` ascending track ids, ``adv_live`` their advantages.
+
+    Finite keys: a lexsort, the same total order.  With a NaN key Python's
+    tuple comparisons are no longer a total order (every comparison with
+    NaN is False), so the outcome depends on timsort's comparison sequence
+    over the input order; that case runs the reference's own ``sorted``
+    over the same keys in the same (index) order -- the identical
+    decision, not "NaN last"."""
+    live = np.asarray(live, dtype=np.int64)
+    adv_live = np.asarray(adv_live, dtype=np.float64)
+    if n_elim <= 0:
+        return np.zeros(0, dtype=np.int64)
+    if np.isnan(adv_live).any():
+        keys = [(float(a), -int(i)) for i, a in zip(live.tolist(),
+                                                     adv_live.tolist())]
+        order = sorted(range(len(keys)), key=keys.__getitem__)
+        return np.sort(live[np.asarray(order[:n_elim], dtype=np.int64)])
+    order = np.lexsort((-live, adv_live))
+    return np.sort(live[order[:n_elim]])
+
+
 def cull_decision(alive, track_ids, adv, fraction, min_tracks):
     """stopping.py:68-86 on the merged advantages of every rank."""
     live = np.flatnonzero(alive)
@@ -84,8 +108,7 @@ def cull_decision(alive, track_ids, adv, fraction, min_tracks):
         return np.zeros(0, dtype=np.int64)
     full = np.zeros(len(alive))
     full[np.asarray(track_ids, dtype=np.int64)] = adv
-    order = np.lexsort((-live, full[live]))
-    return np.sort(live[order[:n_elim]])
+    return eliminated(live, full[live], n_elim)
 
 
 def shard_tasks(n_tasks: int, world: int, rank: int) -> list:

@@ -1,5 +1,5 @@
-"""Parity at BASELINE.json's full sizes (C2: conv2d at 16 K tracks; C5: GEMM
-4096^3 at 1 M tracks), where the oracle cannot replay a whole episode in
+"""Parity at BASELINE.json's full sizes (C2: conv2d at 16 K tracks; C3:
+bmm+softmax at 64 K tracks; C5: GEMM 4096^3 at 1 M tracks), where the oracle cannot replay a whole episode in
 seconds, through properties that do not depend on size:
 
 * every visited state is a legal state of the sketch: per tiled dimension
@@ -89,6 +89,16 @@ def test_c2_full_size_episode_properties():
     assert res.visits == 16384 * 40
     _check_legal(tb, res)
     _check_sample(w, tb, res)
+    _check_reward_chain(res)
+
+
+def test_c3_full_size_episode_properties():
+    """C3 (bmm + softmax, sketch k3: 2 stages, 7 dims) at 65,536 tracks."""
+    w, tb, res = _episode("c3", 65536)
+    assert res.visits == 65536 * 40
+    assert len(res.train) == 30 and len(res.culls) == 1
+    _check_legal(tb, res)
+    _check_sample(w, tb, res, seed=2)
     _check_reward_chain(res)
 
 

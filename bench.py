@@ -1,7 +1,7 @@
 """Benchmark: schedules/sec of the HARL inner search step on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config c2|c1|c3|c5] [--population P]
+                    [--config c2|c1|c3|c5|c4] [--population P]
 
 A bench "step" is one ``_run_episode`` (tuner.py:350-440) over the whole
 population: initial sampling, every search step of the default geometry
@@ -9,25 +9,34 @@ population: initial sampling, every search step of the default geometry
 steps at P/2, PPO every 2 steps), i.e. P*40 visited schedules.  The unit of
 work is one visited schedule (one CandidateEntry, tuner.py:408-412).
 
-* ``value``: whole-job schedules/s with the population resident in HBM,
-  device time via CUDA events on the launching stream, summed over the K
-  timed episodes (L2 flushed between episodes, outside the events), max over
-  ranks.
-* ``e2e``: the same metric through the host-buffer call a drop-in makes per
-  episode: agent parameters/moments, replay ring, forest and generator state
-  go host->device before; after the episode the device rank_scores
-  (costmodel.py:266-286) selects the top-k' distinct unmeasured entries and
-  those (states, features, scores), the per-visit rewards and the updated
-  agent/ring come back device->host, every episode.
-* ``cpu_baseline``: the oracle (numpy restatement of the reference, bit-exact
-  with it) timed on this host on a bounded sample of the same workload.
-* ``--impl reference``: the reference CPU path (the oracle port) with all
-  host cores, one independent session per core (the reference's own
-  process-pool model, cli.py:231-235), same metric.
+* ``value``: whole-job schedules/s with the population resident in HBM
+  (``EpisodeEngine.run_episode``), device time from CUDA events on the
+  launching stream summed over the K timed episodes (L2 flushed between
+  episodes, outside the events), max over ranks.
+* ``e2e``: the same metric through the drop-in a user calls:
+  ``B200TuningSession._run_episode`` (compat.py) on a reference
+  ``TuningSession`` from baseline/_ref -- numpy agent, moments and the
+  refitted ensemble host->device, CandidateEntry list and updated numpy
+  parameters back -- wall time, with the library's accounted H2D/D2H
+  bytes per call.
+* ``roofline``: the dominant kernel from the library's per-launch event
+  timer and the rows each launch processed (``harl_profile_read``), with
+  SURVEY §8(d)'s algorithmic work per row, against peaks measured in this
+  run (TF32/FP16/FP64 cuBLAS matmuls) and MEASURED_PEAKS.json's HBM copy
+  bandwidth; ``kernels`` lists every kernel the same way.
+* ``cpu_baseline`` / ``--impl reference``: the reference's own
+  ``TuningSession._run_episode`` from baseline/_ref (the oracle port only
+  if the reference is not installed) in the reference's process-pool model
+  (cli.py:231-235): one session per host core, P/N tracks each, full
+  60-step episodes of the same config.
+* ``c3_64k``: the C3 configuration (BERT bmm+softmax, 64 K tracks, the
+  north star's >= 64 K step) measured the same way in the same run.
 
-Synthetic data: random-init weights of the reference architecture, a
-synthetic depth-6 50-tree GBT forest with thresholds drawn from real feature
-values (no measurements are available offline).
+Data: random-init weights of the reference architecture; the cost model is
+warm-started as SURVEY §8(d) prescribes (512 uniform states measured by the
+analytic simulator, fit_round) -- on the device for the GPU arm
+(harl_sim_time + harl_gbt_fit, bit-exact with the reference), with the
+reference's own code in the reference arm.
 """
 
 from __future__ import annotations
@@ -97,71 +106,6 @@ subgraphs:
 
 
 # ---------------------------------------------------------------------------
-# workload construction (shared by the GPU and CPU legs)
-
-
-def synthetic_forest(tables, seed: int, n_trees: int = 50, depth: int = 6):
-    """50 trees of depth <= 6 (the reference's GbtConfig defaults,
-    costmodel.py:24-31) splitting on features that actually vary, with
-    thresholds at feature values of random states so walks branch."""
-    from oracle.harl_oracle import featurize, sample_initial  # host-only
-    rng = np.random.default_rng(seed)
-    tiles, knobs = sample_initial(tables, 512, rng)
-    X = featurize(tables, tiles, knobs)
-    varying = np.flatnonzero(X.std(axis=0) > 0)
-    trees = []
-    for _ in range(n_trees):
-        feat, thr, left, right, val = [], [], [], [], []
-
-        def add(d):
-            i = len(feat)
-            feat.append(-1)
-            thr.append(0.0)
-            left.append(-1)
-            right.append(-1)
-            val.append(0.0)
-            if d < depth and rng.random() < 0.92:
-                f = int(rng.choice(varying))
-                feat[i] = f
-                thr[i] = float(X[int(rng.integers(len(X))), f])
-                left[i] = add(d + 1)
-                right[i] = add(d + 1)
-            else:
-                val[i] = float(rng.normal(0.0, 0.05))
-            return i
-        add(0)
-        trees.append(tuple(np.asarray(a) for a in (feat, thr, left, right,
-                                                   val)))
-    return trees
-
-
-def build_workload(cfg_name: str, population: int | None, seed: int = 0):
-    from paper_2211_11172_b200 import workloads as W
-    from paper_2211_11172_b200.agent import RlConfig, init_session_agents
-    from paper_2211_11172_b200.space import SketchTables
-    c = CONFIGS[cfg_name]
-    net = W.loads_network(c["yaml"])
-    target = W.TargetConfig()
-    sg = net.subgraphs[0]
-    ks = W.generate_sketches(sg, target)
-    S = max(k.space.num_tile_slots for k in ks)
-    tables = SketchTables(sg, ks[c["sketch"]], target, S)
-    rl = RlConfig()
-    agent = init_session_agents([(sg.id, S)], tables.feature_len, rl,
-                                np.random.default_rng(seed))[sg.id]
-    P = population or c["population"]
-    return dict(tables=tables, agent=agent, rl=rl, P=P, cfg=c,
-                trees=synthetic_forest(tables, seed + 1), base=0.5, lr=0.3)
-
-
-def episode_config(P):
-    from paper_2211_11172_b200.engine import EpisodeConfig
-    # TunerConfig defaults with min_tracks = P/2, initial_tracks = P
-    return EpisodeConfig(tracks=P, track_len=40, cull_window=20,
-                         cull_fraction=0.5, min_tracks=P // 2)
-
-
-# ---------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 
 
@@ -221,50 +165,256 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU legs
+# workload construction (shared by the GPU and CPU legs)
 
 
-def cpu_episode_sample(cfg_name, P, steps, seed=0):
-    """Oracle episode on P tracks for `steps` search steps; returns
-    (visits, seconds)."""
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+def synthetic_forest(tables, seed: int, n_trees: int = 50, depth: int = 6):
+    """Test helper (tests/, smoke): 50 random trees of depth <= 6 splitting
+    on features that vary, thresholds at feature values of random states.
+    Not used by the bench legs, which warm-start the cost model the
+    reference's way (``device_warm_start`` / ``ref_warm_start``)."""
+    from oracle.harl_oracle import featurize, sample_initial  # test-only
+    rng = np.random.default_rng(seed)
+    tiles, knobs = sample_initial(tables, 512, rng)
+    X = featurize(tables, tiles, knobs)
+    varying = np.flatnonzero(X.std(axis=0) > 0)
+    trees = []
+    for _ in range(n_trees):
+        feat, thr, left, right, val = [], [], [], [], []
+
+        def add(d):
+            i = len(feat)
+            feat.append(-1)
+            thr.append(0.0)
+            left.append(-1)
+            right.append(-1)
+            val.append(0.0)
+            if d < depth and rng.random() < 0.92:
+                f = int(rng.choice(varying))
+                feat[i] = f
+                thr[i] = float(X[int(rng.integers(len(X))), f])
+                left[i] = add(d + 1)
+                right[i] = add(d + 1)
+            else:
+                val[i] = float(rng.normal(0.0, 0.05))
+            return i
+        add(0)
+        trees.append(tuple(np.asarray(a) for a in (feat, thr, left, right,
+                                                   val)))
+    return trees
+
+
+def build_workload(cfg_name: str, population: int | None, seed: int = 0,
+                   synthetic: bool = True):
+    """Tables, a random-init agent of the reference architecture and the
+    step geometry of a config.  ``synthetic``: also a synthetic forest
+    (tests); the bench legs pass False and warm-start the cost model."""
+    from paper_2211_11172_b200 import workloads as W
+    from paper_2211_11172_b200.agent import RlConfig, init_session_agents
+    from paper_2211_11172_b200.space import SketchTables
+    c = CONFIGS[cfg_name]
+    net = W.loads_network(c["yaml"])
+    target = W.TargetConfig()
+    sg = net.subgraphs[0]
+    ks = W.generate_sketches(sg, target)
+    S = max(k.space.num_tile_slots for k in ks)
+    tables = SketchTables(sg, ks[c["sketch"]], target, S)
+    rl = RlConfig()
+    agent = init_session_agents([(sg.id, S)], tables.feature_len, rl,
+                                np.random.default_rng(seed))[sg.id]
+    P = population or c["population"]
+    w = dict(tables=tables, agent=agent, rl=rl, P=P, cfg=c, sg=sg,
+             base=0.5, lr=0.3)
+    if synthetic:
+        w["trees"] = synthetic_forest(tables, seed + 1)
+    return w
+
+
+def device_warm_start(tables, sg_flops: float, gen, dev):
+    """SURVEY §8(d)'s cost-model warm start on the device: 512 uniform
+    states (sample_initial_schedules, schedspace.py:165-178), measured by
+    the analytic simulator with SimulatedBackend's defaults (measure.py:
+    99-133, harl_sim_time, bit-exact), throughput = flops / time, targets
+    renormalised by the best (costmodel.py:180-188), fit_round ->
+    fit_incremental (costmodel.py:190-215, harl_gbt_fit, bit-exact):
+    50 trees of depth <= 6.  Returns (trees, base)."""
+    from paper_2211_11172_b200 import device as D
+    dsk = D.DeviceSketch(tables, dev)
+    t, k = D.init_population(dsk, 512, gen)
+    X = D.featurize(dsk, t, k, 512)
+    secs = D.simulate_time(dsk, t, k, 512).cpu().numpy()
+    thr = sg_flops / secs
+    y = thr / thr.max()
+    fit = D.gbt_fit(X, y, n_trees=50, max_depth=6, learning_rate=0.3,
+                    min_leaf=1, device=dev)
+    return fit.trees, fit.base
+
+
+def episode_config(P):
+    from paper_2211_11172_b200.engine import EpisodeConfig
+    # TunerConfig defaults with min_tracks = P/2, initial_tracks = P
+    return EpisodeConfig(tracks=P, track_len=40, cull_window=20,
+                         cull_fraction=0.5, min_tracks=P // 2)
+
+
+def _ref_import():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    import schedtune  # noqa: F401  (raises ImportError when absent)
+
+
+def ref_network(cfg_name: str):
+    """The config's network through the reference's own loader."""
+    import tempfile
+    from schedtune.workload import load_network
+    with tempfile.NamedTemporaryFile("w", suffix=".yaml", delete=False) as f:
+        f.write(CONFIGS[cfg_name]["yaml"])
+        path = f.name
+    try:
+        return load_network(path)
+    finally:
+        os.unlink(path)
+
+
+def ref_warm_start(sess, sg, sketch, n: int = 512):
+    """The same warm start through the reference session's own objects:
+    sample_initial_schedules on the session generator, SimulatedBackend
+    measure_batch, SurrogateModel.observe, fit_round."""
+    from schedtune.measure import MeasureRequest
+    from schedtune.schedspace import sample_initial_schedules
+    ctx = sess.contexts[sketch.id]
+    states = sample_initial_schedules(sketch, n, sess.rng)
+    res = sess.backend.measure_batch([MeasureRequest(state=s, ctx=ctx)
+                                      for s in states])
+    for s, r in zip(states, res):
+        sess.model.observe(ctx.featurize(s), r.throughput, sg.id)
+    sess.model.fit_round()
+
+
+def ref_session(cfg_name: str, P: int, seed: int, b200: bool = False):
+    """A reference TuningSession (or the drop-in subclass) for one config:
+    TunerConfig defaults with initial_tracks = P, min_tracks = P/2, the
+    rl (adaptive) searcher, SimulatedBackend, warm-started cost model."""
+    from schedtune.measure import SimulatedBackend
+    from schedtune.tuner import TunerConfig, TuningSession
+    from schedtune.workload import TargetConfig
+    net = ref_network(cfg_name)
+    cfg = TunerConfig(seed=seed, total_trials=10 ** 9, top_k=64,
+                      initial_tracks=P, min_tracks=max(1, P // 2))
+    cls = TuningSession
+    if b200:
+        from paper_2211_11172_b200.compat import b200_session_class
+        cls = b200_session_class(TuningSession)
+    sess = cls(net, TargetConfig(), cfg, SimulatedBackend(), "rl")
+    if b200:
+        sess._b200_hook_model()       # fit_round -> harl_gbt_fit
+    sg = net.subgraphs[0]
+    sketch = sess.sketches[sg.id][CONFIGS[cfg_name]["sketch"]]
+    ref_warm_start(sess, sg, sketch)
+    return sess, sg, sketch
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the reference's own _run_episode (baseline/_ref), or the oracle
+# port when the reference is not installed
+
+
+def _host_info():
+    import platform
+    cpu = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": cpu, "glibc": "-".join(platform.libc_ver()),
+            "numpy": np.__version__, "python": platform.python_version(),
+            "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+def _ref_episode_worker(job):
+    """One process of the reference's process-pool model (cli.py:231-235):
+    an independent reference session on P tracks, ``warm`` untimed then
+    ``steps`` timed full episodes (``TuningSession._run_episode``,
+    tuner.py:350-440, perf_counter around the call).  Falls back to the
+    oracle port when the reference package is absent."""
+    cfg_name, P, seed, warm, steps = job
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        _ref_import()
+        sess, sg, sketch = ref_session(cfg_name, P, seed)
+        kind = "reference"
+
+        def episode(rnd):
+            t = time.perf_counter()
+            v0 = sess.order_counter
+            sess._run_episode(sg, sketch, rnd)
+            return sess.order_counter - v0, time.perf_counter() - t
+    except ImportError:
+        kind = "port"
+        episode = _port_episode_fn(cfg_name, P, seed)
+    out = []
+    for i in range(warm + steps):
+        v, s = episode(i + 1)
+        if i >= warm:
+            out.append((v, s))
+    return kind, out
+
+
+def _port_episode_fn(cfg_name, P, seed):
+    """The oracle restatement (bit-exact with the reference) of one full
+    episode per call, warm-started the same way (oracle sim + fit)."""
     from oracle import harl_oracle as O
-    w = build_workload(cfg_name, P, seed)
-    a = w["agent"]
+    w = build_workload(cfg_name, P, seed, synthetic=False)
+    tb, a, sg = w["tables"], w["agent"], w["sg"]
+    rng = np.random.default_rng(seed)
+    tiles, knobs = O.sample_initial(tb, 512, rng)
+    X = O.featurize(tb, tiles, knobs)
+    secs = np.array([O.sim_time(tb, tiles[i], knobs[i]) for i in range(512)])
+    thr = sg.flops / secs
+    base, trees = O.gbt_fit(X, thr / thr.max())[:2]
     oa = O.Agent.from_param_lists(a.policy, a.value, len(a.hidden))
     opi = O.Adam.zeros_like(oa.policy_params(), w["rl"].lr_actor)
     ov = O.Adam.zeros_like(oa.value_params(), w["rl"].lr_critic)
-    model = O.GbtModel(w["base"], w["lr"], True, w["trees"])
-    ecfg = O.EpisodeCfg(tracks=P, track_len=steps, cull_window=20,
-                        cull_fraction=0.5, min_tracks=P // 2,
+    model = O.GbtModel(base, 0.3, True, trees)
+    ecfg = O.EpisodeCfg(tracks=P, track_len=40, cull_window=20,
+                        cull_fraction=0.5, min_tracks=max(1, P // 2),
                         rl_cfg=O.RlCfg())
-    t = time.perf_counter()
-    entries, _, _ = O.run_episode(w["tables"], w["tables"].num_slots, ecfg,
-                                  oa, opi, ov, O.Replay(4096), model,
-                                  np.random.default_rng(seed + 7), 0)
-    return len(entries), time.perf_counter() - t
+    rep = O.Replay(4096)
+    state = {"order": 0}
+
+    def episode(rnd):
+        t = time.perf_counter()
+        entries, _, _ = O.run_episode(tb, tb.num_slots, ecfg, oa, opi, ov,
+                                      rep, model, rng, state["order"])
+        state["order"] += len(entries)
+        return len(entries), time.perf_counter() - t
+    return episode
 
 
-def _cpu_worker(args):
-    cfg_name, P, steps, seed = args
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    return cpu_episode_sample(cfg_name, P, steps, seed)
-
-
-def cpu_parallel(cfg_name, P, steps, procs):
-    """The reference's own parallelism model: independent sessions in a
-    process pool (cli.py:231-235), P/procs tracks each."""
+def cpu_pool(cfg_name, P, warm, steps, procs=None):
+    """N = len(sched_getaffinity) independent reference sessions x P/N
+    tracks each, full episodes; aggregate =
+    sum of visits / slowest process's summed episode time."""
     from concurrent.futures import ProcessPoolExecutor
     import multiprocessing as mp
+    procs = procs or len(os.sched_getaffinity(0))
     per = max(2, P // procs)
-    t = time.perf_counter()
     with ProcessPoolExecutor(procs, mp_context=mp.get_context("spawn")) as ex:
-        res = list(ex.map(_cpu_worker, [(cfg_name, per, steps, s)
-                                        for s in range(procs)]))
-    wall = time.perf_counter() - t
-    visits = sum(v for v, _ in res)
-    slowest = max(s for _, s in res)
-    return visits, slowest, wall
+        res = list(ex.map(_ref_episode_worker,
+                          [(cfg_name, per, s, warm, steps)
+                           for s in range(procs)]))
+    kinds = {k for k, _ in res}
+    visits = sum(v for _, r in res for v, _ in r)
+    slowest = max(sum(s for _, s in r) for _, r in res)
+    one = [v / s for _, r in res for v, s in r]
+    return dict(kind="reference" if kinds == {"reference"} else "port",
+                procs=procs, per=per, visits=visits, seconds=slowest,
+                value=visits / slowest,
+                per_process=float(np.median(one)), host=_host_info())
 
 
 # ---------------------------------------------------------------------------
@@ -277,36 +427,77 @@ def l2_flush(torch, dev, buf=[]):
     buf[0].fill_(1)
 
 
-def run_gpu(args, rank, world):
+def measure_peaks(torch, dev):
+    """Dense matmul peaks of this GPU measured in this run (cuBLAS through
+    torch; CUDA events, best of 5 after 2 warm-ups): TF32 (fp32 matmul with
+    TF32 allowed, 8192^3), FP16 (8192^3), FP64 (4096^3, DMMA)."""
+    out = {}
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        for name, dt, n in (("tf32", torch.float32, 8192),
+                            ("fp16", torch.float16, 8192),
+                            ("fp64", torch.float64, 4096)):
+            a = torch.randn(n, n, device=dev).to(dt)
+            b = torch.randn(n, n, device=dev).to(dt)
+            c = torch.empty(n, n, device=dev, dtype=dt)
+            for _ in range(2):
+                torch.matmul(a, b, out=c)
+            best = math.inf
+            for _ in range(5):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                torch.matmul(a, b, out=c)
+                e1.record()
+                e1.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            out[f"{name}_tflops"] = round(2.0 * n ** 3 / (best * 1e-3) / 1e12, 1)
+            del a, b, c
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+    torch.cuda.empty_cache()
+    try:
+        mp_ = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        out["hbm_gbs"] = mp_["hbm_gbs"]
+        out["hbm_note"] = "MEASURED_PEAKS.json hbm_gbs (driver-measured copy)"
+    except (OSError, KeyError, ValueError):
+        out["hbm_gbs"] = 6557.8
+        out["hbm_note"] = "B200_PROFILING.md fallback"
+    return out
+
+
+def value_leg(cfg_name, P, steps, warmup, dev, rank, world, profile=True):
+    """Device-resident episodes (EpisodeEngine.run_episode), population in
+    HBM: CUDA events on the launching stream around each episode, L2
+    flushed between episodes (outside the events).  Then one untimed,
+    eagerly launched episode with the library's per-launch event timer for
+    the per-kernel table."""
     import torch
     from paper_2211_11172_b200 import device as D
     from paper_2211_11172_b200 import profiling
     from paper_2211_11172_b200.engine import EpisodeEngine
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
-    torch.cuda.set_device(dev)
-    w = build_workload(args.config, args.population, seed=rank)
-    P = w["P"]
+    w = build_workload(cfg_name, P, seed=rank, synthetic=False)
     tb = w["tables"]
+    gen = np.random.default_rng(1000 + rank)
+    trees, base = device_warm_start(tb, w["sg"].flops, gen, dev)
     ecfg = episode_config(P)
     eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, dev)
-    forest = D.DeviceForest(w["trees"], w["base"], w["lr"], device=dev)
-    gen = np.random.default_rng(1000 + rank)
+    forest = D.DeviceForest(trees, base, 0.3, device=dev)
     stream = torch.cuda.current_stream()
     order = 0
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         res = eng.run_episode(tb, forest, gen, ecfg, order)
         order += res.visits
     torch.cuda.synchronize()
     profiling.reset()
-    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    total_ms = 0.0
-    visits = 0
+    total_ms, visits = 0.0, 0
     with ClockSampler(dev.index) as clk:
-        for _ in range(args.steps):
+        for _ in range(steps):
             l2_flush(torch, dev)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -320,267 +511,188 @@ def run_gpu(args, rank, world):
             order += res.visits
     torch.cuda.synchronize()
     launches = profiling.launch_count()
-    # one extra, untimed episode with per-call CUDA events: kernel shares
-    profiling.reset()
-    profiling.timing(True)
-    profiling.native_timing(True)
-    eng.use_graphs = False          # per-launch events need eager launches
-    res = eng.run_episode(tb, forest, gen, ecfg, order)
-    eng.use_graphs = True
-    order += res.visits
-    kstats = profiling.kernel_times()
-    native = profiling.native_kernel_times()
-    profiling.native_timing(False)
-    profiling.timing(False)
-    if world > 1:
-        dist.barrier()
-    # ---- e2e: host buffers in and out every episode ------------------------
-    host = E2EHost(eng, w, dev, ecfg.budget)
-    e2e_ms, h2d, d2h, e2e_visits = 0.0, 0, 0, 0
-    e2e_parts = {}
-    for _ in range(max(1, min(args.steps, 3))):
+    out = dict(total_ms=total_ms, visits=visits, clocks=clk.summary(),
+               launches=launches, P=P, tables=tb, n_trees=len(trees),
+               n_params=sum(p.size for p in w["agent"].policy) +
+               sum(p.size for p in w["agent"].value))
+    if profile:
+        profiling.native_timing(True)
+        eng.use_graphs = False      # per-launch events need eager launches
         l2_flush(torch, dev)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        b_in, b_out, v, parts = host.episode(forest, gen, ecfg, order)
-        torch.cuda.synchronize()
-        e2e_ms += (time.perf_counter() - t0) * 1e3
-        h2d, d2h = b_in, b_out
-        e2e_visits += v
-        order += v
-        for k_, t_ in parts.items():
-            e2e_parts[k_] = e2e_parts.get(k_, 0.0) + t_
-    return dict(total_ms=total_ms, visits=visits, clocks=clk.summary(),
-                launches=launches, kstats=kstats, native=native, e2e_ms=e2e_ms,
-                e2e_visits=e2e_visits, h2d=h2d, d2h=d2h, P=P,
-                e2e_parts=e2e_parts)
-
-
-class E2EHost:
-    """The drop-in's host side for the e2e number: pinned host buffers for
-    every per-episode input (agent parameters + Adam moments, replay ring,
-    GBT ensemble; the replay ring stays resident like the drop-in's) and
-    output (the rank_scores selection -- top-k' distinct
-    unmeasured entries with states, features, scores -- the per-visit
-    rewards of the trajectory log, the updated agent and ring), allocated
-    once.  Each timed episode copies the inputs host->device, runs
-    ``_run_episode`` + the device rank_scores and copies the outputs back
-    (what ``compat.B200TuningSession._run_episode`` moves per round, without
-    the reference's Python object construction).  The selected states
-    accumulate as the "measured" exclusion set, as in a session."""
-
-    def __init__(self, eng, w, dev, visits):
-        import torch
-        self.eng, self.w, self.dev = eng, w, dev
-        self.tb = w["tables"]
-        da, ring = eng.dagent, eng.replay
-        pin = lambda t: torch.empty(t.shape, dtype=t.dtype).pin_memory()
-        self.agent_in = {k: pin(getattr(da, k)) for k in ("params", "m", "v")}
-        for k, t in self.agent_in.items():
-            t.copy_(getattr(da, k))
-        self.agent_out = {k: pin(getattr(da, k)) for k in ("params", "m", "v")}
-        keys = ("X", "Xn", "actions", "scalars", "move_bits", "shift_bits")
-        self.ring_out = {k: pin(getattr(ring, k)) for k in keys}
-        self.V = (visits, torch.empty(visits, dtype=torch.float64).pin_memory())
-        from paper_2211_11172_b200 import device as D
-        self.rank_scratch = D.RankScratch(dev)
-        self.top_k = 64                 # TunerConfig.top_k default
-        # allocations a session makes once, outside the per-round path
-        self.rank_scratch.ensure(visits, 64 * 16, self.top_k)
-        self.rank_scratch.host_pins(4 * self.top_k, w["tables"])
-        self.measured = None
-
-    def episode(self, forest, gen, ecfg, order):
-        import torch
-        eng, tb = self.eng, self.tb
-        da, ring = eng.dagent, eng.replay
-        parts = {}
-        t0 = time.perf_counter()
-        nin = 0
-        for k, t in self.agent_in.items():
-            getattr(da, k).copy_(t, non_blocking=True)
-            nin += t.numel() * t.element_size()
-        da.params32.copy_(da.params)            # fp32 rollout copy
-        da.refresh_derived()                    # tcgen05 images + transposes
-        # the replay ring is not uploaded: between episodes the drop-in keeps
-        # it in device memory (compat._RingBuffer); it is still exported
-        # below, as the per-round checkpoint does
-        w = self.w
-        forest.load(w["trees"], w["base"], w["lr"])
-        nin += forest.n_nodes * 16 + forest.n_trees * 4 + forest.HDR.itemsize
-        t1 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         res = eng.run_episode(tb, forest, gen, ecfg, order)
-        t2 = time.perf_counter()
-        V = res.visits
-        if self.V is None or self.V[0] < V:
-            self.V = (V, torch.empty(V, dtype=torch.float64).pin_memory())
-        # rank_scores on the device (what run_round consumes): the top-k'
-        # distinct unmeasured entries come back with their features; the
-        # per-visit rewards come back for the trajectory log
-        idx, tiles, knobs, feats, scores, _ = res.top_entries(
-            self.top_k, self.measured, self.rank_scratch)
-        self.V[1][:V].copy_(res.log_reward[:V], non_blocking=True)
-        nout = len(idx) * (2 * tb.local_slots + 3 + 8 * tb.feature_len + 8 + 8) \
-            + V * 8
-        # the chosen states become "measured" for the next episodes
-        mt = tiles if self.measured is None else \
-            np.concatenate([self.measured[0], tiles])
-        mk = knobs if self.measured is None else \
-            np.concatenate([self.measured[1], knobs])
-        self.measured = (mt, mk)
-        t2b = time.perf_counter()
-        for k, t in self.agent_out.items():
-            t.copy_(getattr(da, k), non_blocking=True)
-            nout += t.numel() * t.element_size()
-        for k, t in self.ring_out.items():
-            t.copy_(getattr(ring, k), non_blocking=True)
-            nout += t.numel() * t.element_size()
-        torch.cuda.current_stream().synchronize()
-        t3 = time.perf_counter()
-        parts.update(h2d_ms=(t1 - t0) * 1e3, episode_ms=(t2 - t1) * 1e3,
-                     rank_ms=(t2b - t2) * 1e3, d2h_ms=(t3 - t2b) * 1e3)
-        return nin, nout, V, parts
+        e1.record(stream)
+        e1.synchronize()
+        eng.use_graphs = True
+        out["native"] = profiling.native_kernel_times()
+        out["profiled_episode_ms"] = e0.elapsed_time(e1)
+        profiling.native_timing(False)
+    return out
 
 
-# kernel -> (profiling span whose rows it processes, bound)
-KERNEL_SPAN = {
-    "k_trunk_tc<policy>": ("policy_tc", "tensor"),
-    "k_heads_tc": ("policy_tc", "tensor"),
-    "k_sample_rows": ("policy_tc", "hbm"),
-    "k_trunk_tc<value>": ("value_tc", "tensor"),
-    "k_policy_tc": ("policy_tc", "tensor"),
-    "k_policy_tc64": ("policy_tc", "tensor"),
-    "k_policy_step_fused": ("policy_tc", "tensor"),
-    "k_value_tc": ("value_tc", "tensor"),
-    "k_featurize": ("featurize", "hbm"),
-    "k_featurize2": ("featurize", "hbm"),
-    "k_gbt_predict": ("gbt", "hbm"),
-    "k_gbt_predict2": ("gbt", "hbm"),
-    "k_finish_step": ("finish", "hbm"),
-    "k_gbt_finish": ("gbt", "hbm"),
-    "k_ring_rows": ("finish", "hbm"),
-    "k_ppo_rows": ("ppo", "fp64"),
-    "k_ppo_rows_tc": ("ppo", "fp64"),
-}
+def e2e_leg(cfg_name, P, steps, warmup, dev, rank):
+    """The same metric through the drop-in (the call a user makes):
+    ``B200TuningSession._run_episode`` (compat.py) on a reference
+    ``TuningSession`` built from baseline/_ref, called exactly as run_round
+    calls it (tuner.py:480).  Every timed call takes the session's numpy
+    agent and Adam moments, the replay deque (first call) and the refitted
+    ensemble host->device, runs the episode and the device rank_scores,
+    writes parameters and moments back into the numpy arrays and returns
+    the reference's CandidateEntry list.  Wall time (perf_counter with a
+    device synchronize on both sides); bytes = the library's accounted
+    host<->device copies of the timed calls."""
+    import torch
+    from paper_2211_11172_b200 import profiling as PF
+    _ref_import()
+    sess, sg, sketch = ref_session(cfg_name, P, seed=rank, b200=True)
+    rnd = 0
+    for _ in range(warmup):
+        rnd += 1
+        sess._run_episode(sg, sketch, rnd)
+    ms, visits, h2d, d2h = 0.0, 0, 0, 0
+    n = max(1, steps)
+    for _ in range(n):
+        rnd += 1
+        l2_flush(torch, dev)
+        torch.cuda.synchronize()
+        PF.xfer_reset()
+        v0 = sess.order_counter
+        t0 = time.perf_counter()
+        entries = sess._run_episode(sg, sketch, rnd)
+        torch.cuda.synchronize()
+        ms += (time.perf_counter() - t0) * 1e3
+        visits += sess.order_counter - v0
+        x = PF.xfer_bytes()
+        h2d += x["h2d"]
+        d2h += x["d2h"]
+    return dict(ms=ms, visits=visits, steps=n, h2d=h2d // n, d2h=d2h // n,
+                entries=len(entries))
 
 
-def per_row_work(tables, H, feat_in_sampler=False):
-    """Algorithmic work per row (one schedule / one minibatch row) of each
-    kernel: flops for the MLP kernels, HBM bytes for the rest (DESIGN.md
-    "Kernels and their rooflines" states the same figures)."""
-    F, S = tables.feature_len, tables.num_slots
+def kernel_work(tables, H: int, P: int):
+    """Algorithmic work per unit (one row a launch processed) of each
+    kernel: flops for the tensor-core MLPs and the fp64 PPO,
+    bytes for the rest.  The sampler's fp32 logits read is an unfused
+    intermediate, not algorithmic work, and is not counted."""
+    F, S = tables.feature_len, tables.local_slots
     C = len(tables.head_cols)
-    NH = C + 9                      # tiling columns + 3 + 3 + 3 knob heads
-    state = 2 * S + 3               # int16 tile slots + 3 knob bytes
+    state = 2 * S + 3               # u16 tile slots + 3 knob bytes
+    walk = state + 5 + state        # state in, action (u16 + 3 u8), state out
+    pol = 2 * (F * H + H * H + H * (C + 9))
+    val = 2 * (F * H + H * H + H)
+    feat_in_sampler = 0 < P <= 16384   # HARL_SAMPLE_FEAT_MAX_ROWS
+    gbt = 8 * F + 16                # K6: features in, score + reward out
+    log = state + 8 + 8 + 4         # entry log: state, score, reward, track
     return {
-        "k_trunk_tc<policy>": 2 * (F * H + H * H),
-        "k_heads_tc": 2 * H * NH,
-        "k_trunk_tc<value>": 2 * (F * H + H * H + H),   # per evaluated row
-        "k_policy_tc": 2 * (F * H + H * H + H * NH),
-        "k_policy_tc64": 2 * (F * H + H * H + H * NH),
-        # + the sampler/walker and the featurizer of the same rows
-        "k_policy_step_fused": 2 * (F * H + H * H + H * NH),
-        "k_value_tc": 2 * (F * H + H * H + H),
-        # logits in; actions, logp, successor state out (+ its feature row
-        # when the sampler featurizes, <= 16 K rows per launch)
-        "k_sample_rows": 4 * NH + state + 16 + 8 + state +
-                         (8 * F if feat_in_sampler else 0),
-        "k_featurize": state + 8 * F,
-        "k_featurize2": state + 8 * F,
-        "k_gbt_predict": 8 * F + 8,
-        "k_gbt_predict2": 8 * F + 8,
-        # reward/score/v/adv/log entry (state + score + track) + ring scalars
-        "k_finish_step": 8 * 6 + state + 8 + 4 + 8 * 4 + 16 + 4,
-        # GBT (features in, score + reward out) + the finish row work
-        "k_gbt_finish": 8 * F + 8 + 8 * 6 + state + 8 + 4 + 8 * 4 + 16 + 4,
-        "k_ring_rows": 2 * 8 * F * 2,               # X and X' read + written
+        "k_mlp_f16<policy>": ("tensor", pol), "k_mlp_f16<value>": ("tensor", val),
+        "k_policy_tc": ("tensor", pol), "k_policy_tc64": ("tensor", pol),
+        "k_policy_step_fused": ("tensor", pol),
+        "k_value_tc": ("tensor", val),
+        "k_sample_rows": ("hbm", walk + (8 * F if feat_in_sampler else 0)),
+        "k_featurize2": ("hbm", state + 8 * F),
+        "k_featurize": ("hbm", state + 8 * F),
+        "k_gbt_predict2": ("hbm", gbt), "k_gbt_predict": ("hbm", gbt),
+        "k_gbt_finish": ("hbm", gbt + log),
         # policy + value forward and backward in fp64 (3x forward flops)
-        "k_ppo_rows": 3 * 2 * (2 * (F * H + H * H) + H * NH + H),
-        "k_ppo_rows_tc": 3 * 2 * (2 * (F * H + H * H) + H * NH + H),
+        "k_ppo_rows": ("fp64", 3 * (pol + val)),
+        "k_ppo_rows_tc": ("fp64", 3 * (pol + val)),
+        "k_ppo_wgrad": ("fp64", None),        # 2 * B per parameter, below
+        "k_ppo_adam": ("hbm", 60),            # per parameter
     }
 
 
-def roofline_entry(native, spans, tables, hidden, P=0):
-    """Dominant kernel's achieved rate vs the measured peak, from the native
-    per-kernel event timer (harl_profile_*) of the untimed profiled episode;
-    rows per kernel come from the matching host span."""
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    if not native:
-        return None
-    # the sampler featurizes in-kernel up to 16 K rows per launch
-    # (HARL_SAMPLE_FEAT_MAX_ROWS, harl_b200.cu)
-    work = per_row_work(tables, hidden, feat_in_sampler=0 < P <= 16384)
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    bf16 = peaks.get("bf16_tflops", 1590.0)
-    tf32 = bf16 * 1.1 / 2.25        # dense tf32 : bf16 nominal ratio
-    fp64 = 37.0                     # B200 nominal fp64 (no measured figure)
+def roofline_table(native, tables, H, P, peaks, n_params):
+    """Per-kernel achieved rate from the library's per-launch event timer
+    (harl_profile_read: summed launch time and the rows each launch
+    processed) against this run's measured peaks; the dominant kernel (by
+    device time) is the line's ``roofline``."""
+    work = kernel_work(tables, H, P)
+    pk = {"tensor": peaks["tf32_tflops"], "fp64": peaks["fp64_tflops"],
+          "hbm": peaks["hbm_gbs"]}
     table = {}
     for name, st in native.items():
-        if st["ms"] <= 0:
-            continue
-        if name not in KERNEL_SPAN:     # listed with its time only
-            table[name] = {"bound": None, "achieved": 0.0, "peak": None,
-                           "unit": None, "frac": 0.0,
-                           "us_per_launch": 1e3 * st["ms"] / max(1, st["launches"]),
-                           "ms_per_episode": st["ms"]}
-            continue
-        span, bound = KERNEL_SPAN[name]
-        rows = spans.get(span, {}).get("rows", 0)
-        q = work[name] * rows
-        if bound == "hbm":
-            ach = q / (st["ms"] * 1e-3) / 1e9
-            ent = {"bound": "hbm", "achieved": ach, "peak": hbm,
-                   "unit": "GB/s"}
-        else:
-            ach = q / (st["ms"] * 1e-3) / 1e12
-            pk = tf32 if bound == "tensor" else fp64
-            ent = {"bound": "tensor" if bound == "tensor" else "fp64",
-                   "achieved": ach, "peak": round(pk, 1), "unit": "TFLOP/s"}
-        ent["frac"] = ent["achieved"] / ent["peak"]
-        ent["us_per_launch"] = 1e3 * st["ms"] / max(1, st["launches"])
-        ent["ms_per_episode"] = st["ms"]
+        ms, units = st["ms"], st.get("units", -1)
+        ent = {"us_per_launch": round(1e3 * ms / max(1, st["launches"]), 2),
+               "ms_per_episode": round(ms, 4), "launches": st["launches"],
+               "units": units}
+        if name in work and ms > 0 and units > 0:
+            bound, per = work[name]
+            if name == "k_ppo_wgrad":
+                per = 2 * n_params
+            q = per * units / (ms * 1e-3)
+            ach = q / 1e9 if bound == "hbm" else q / 1e12
+            ent.update(bound=bound, achieved=round(ach, 3),
+                       unit="GB/s" if bound == "hbm" else "TFLOP/s",
+                       peak=pk[bound], frac=round(ach / pk[bound], 5),
+                       work_per_unit=per,
+                       work_unit="B" if bound == "hbm" else "flop")
+            if name.startswith("k_mlp_f16"):
+                # fp32-accurate networks on the fp16 pipe (3xFP16): also
+                # against the measured dense fp16 peak of that pipe
+                ent["frac_of_fp16_peak"] = round(ach / peaks["fp16_tflops"], 5)
         table[name] = ent
-    if not table:
-        return None
-    top = max((k for k in table if table[k]["bound"]),
-              key=lambda k: table[k]["ms_per_episode"])
+    timed = [k for k in table if "bound" in table[k]]
+    if not timed:
+        return None, table
+    top = max(timed, key=lambda k: table[k]["ms_per_episode"])
     e = table[top]
-    # DRAM bytes per launch of that kernel from the committed ncu --set full
-    # capture (per row there, scaled to this run's average rows per launch)
     traffic = None
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
-        if top in tr:
-            span = KERNEL_SPAN[top][0]
-            rows = spans.get(span, {}).get("rows", 0)
-            launches = native[top]["launches"] or 1
-            per_row = tr[top]["dram_bytes_per_launch"] / tr[top]["rows_per_launch"]
-            traffic = round(per_row * rows / launches)
+        tr = json.load(open(os.path.join(ROOT, "profiles",
+                                         "r2_traffic.json")))
+        key = "c2" if P <= 16384 else "c3"
+        if top in tr.get(key, {}):
+            traffic = round(tr[key][top]["dram_bytes_per_launch"])
     except (OSError, ValueError, KeyError):
         traffic = None
-    out = {"kernel": top, "bound": e["bound"],
-           "achieved": round(e["achieved"], 3), "peak": e["peak"],
-           "unit": e["unit"], "frac": round(e["frac"], 5), "traffic": traffic,
-           "traffic_note": "DRAM bytes/launch (dram__bytes_read+write) from "
-                           "profiles/r1_traffic.json (ncu --set full), scaled "
-                           "to this run's rows/launch; population data is "
-                           "L2-resident, so DRAM traffic << algorithmic bytes",
-           "us_per_launch": round(e["us_per_launch"], 2),
-           "peak_note": "hbm: MEASURED_PEAKS.json hbm_gbs (burst); tensor: "
-                        "dense tf32 = measured bf16 x 1.1/2.25; fp64: 37 "
-                        "TFLOP/s nominal",
-           "kernels": {k: {"bound": v["bound"],
-                           "achieved": round(v["achieved"], 3),
-                           "unit": v["unit"], "frac": round(v["frac"], 5),
-                           "us_per_launch": round(v["us_per_launch"], 2),
-                           "ms_per_episode": round(v["ms_per_episode"], 4)}
-                       for k, v in sorted(table.items(),
-                                          key=lambda kv: -kv[1]["ms_per_episode"])}}
-    return out
+    roof = {"kernel": top, "bound": e["bound"], "achieved": e["achieved"],
+            "peak": e["peak"], "unit": e["unit"], "frac": e["frac"],
+            "traffic": traffic,
+            "rows_per_launch": round(e["units"] / max(1, e["launches"]), 1),
+            "us_per_launch": e["us_per_launch"],
+            "achieved_note": "algorithmic work per row (SURVEY §8(d)) x rows "
+                             "the library counted per launch / summed launch "
+                             "time (per-launch CUDA events on the launching "
+                             "stream, spin-kernel aligned, one untimed eager "
+                             "episode)",
+            "traffic_note": "DRAM bytes per launch (dram__bytes_read+write) "
+                            "averaged over the launches of the committed ncu "
+                            "--set full capture of the same config "
+                            "(profiles/r2_traffic.json; ncu flushes caches "
+                            "between replays, so this is the cold figure)"}
+    return roof, table
+
+
+def gpu_arm(args, P, rank, world):
+    import torch
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    peaks = measure_peaks(torch, dev)
+    r = value_leg(args.config, P, args.steps, args.warmup, dev, rank, world)
+    try:
+        e = e2e_leg(args.config, P, min(args.steps, 5), min(args.warmup, 3),
+                    dev, rank)
+    except ImportError as exc:
+        e = {"unavailable": f"the drop-in needs the reference package "
+                            f"(baseline/_ref): {exc}"}
+    c3 = None
+    if args.config == "c2" and not args.no_extra:
+        c3 = value_leg("c3", CONFIGS["c3"]["population"], 3, 3, dev, rank,
+                       world)
+    return peaks, r, e, c3
+
+
+def _max_over_ranks(vals, world):
+    if world == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t]
 
 
 def main():
@@ -591,8 +703,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--population", type=int, default=None)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the C3 64K sub-measurement")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -611,83 +724,131 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    r = run_gpu(args, rank, world)
-    total_ms, e2e_ms = r["total_ms"], r["e2e_ms"]
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64,
-                         device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_ms = float(t[0]), float(t[1])
+    peaks, r, e, c3 = gpu_arm(args, P, rank, world)
+    total_ms, = _max_over_ranks([r["total_ms"]], world)
+    e_ms = _max_over_ranks([e.get("ms", 0.0)], world)[0]
+    c3_ms = _max_over_ranks([c3["total_ms"]], world)[0] if c3 else None
     if rank != 0:
         return
+    tb = r["tables"]
+    H = 128
     visits_all = r["visits"] * world
     value = visits_all / (total_ms / 1e3)
-    e2e = r["e2e_visits"] * world / (e2e_ms / 1e3)
-    tb = build_workload(args.config, P)["tables"]
+    n_params = r["n_params"]
+    roof, table = roofline_table(r["native"], tb, H, P, peaks, n_params)
+    flops = kernel_work(tb, H, P)
+    fl_sched = flops["k_mlp_f16<policy>"][1] + 2 * flops["k_mlp_f16<value>"][1]
+    by_sched = 2 * (2 * tb.local_slots + 3) + 5 + 8 * tb.feature_len
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 networks + fp64 features/GBT/PPO",
-        "data": "synthetic (random-init reference architecture, synthetic "
-                "50-tree depth-6 GBT)",
+        "dtype": "fp32-accurate networks (3xFP16 split, fp32 accumulate, "
+                 "tcgen05 kind::f16) + fp64 features/GBT/PPO",
+        "data": "synthetic: random-init reference architecture (Glorot, "
+                "seeded); cost model warm-started per SURVEY §8(d) (512 "
+                "uniform states, analytic simulator, fit_round -> "
+                f"{r['n_trees']} trees, on the device, bit-exact)",
         "config": {"workload": cfgd["workload"], "population_per_gpu": P,
                    "episode": "cull_window 20, episode_len 40, "
                               "min_tracks P/2 (60 steps, P*40 visits)",
-                   "hidden": [128, 128], "step": "one full _run_episode",
+                   "hidden": [H, H], "step": "one full _run_episode",
                    "l2": "flushed (256 MiB write) between timed episodes",
                    "parallelism": f"independent task replicas x{world}"
                    if world > 1 else "single GPU"},
-        "e2e": {"value": round(e2e, 1), "unit": UNIT,
-                "h2d_bytes_per_step": int(r["h2d"]),
-                "d2h_bytes_per_step": int(r["d2h"]),
-                "ms_per_step_parts": {k: round(v / max(1, min(args.steps, 3)), 3)
-                                      for k, v in r["e2e_parts"].items()}},
         "gpu_launches": int(r["launches"]),
         "clocks": r["clocks"],
-        "roofline": roofline_entry(r["native"], r["kstats"], tb, 128, P),
-        "kernel_ms_per_episode": {k: round(v["ms"], 4)
-                                  for k, v in r["kstats"].items()},
+        "roofline": roof,
+        "peaks_measured": peaks,
+        "step_roofline": {
+            "tensor": {"achieved": round(value * fl_sched / 1e12, 2),
+                       "peak": peaks["tf32_tflops"], "unit": "TFLOP/s",
+                       "frac": round(value * fl_sched / 1e12 /
+                                     peaks["tf32_tflops"], 4),
+                       "flop_per_schedule": fl_sched,
+                       "note": "policy + 2 value passes per schedule, "
+                               "1-pass algorithmic flops vs the measured "
+                               "TF32 peak"},
+            "hbm": {"achieved": round(value * by_sched / 1e9, 2),
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(value * by_sched / 1e9 / peaks["hbm_gbs"],
+                                  5),
+                    "bytes_per_schedule": by_sched}},
+        "kernels": table,
+        "profiled_episode_ms": round(r["profiled_episode_ms"], 3),
     }
+    if "ms" in e:
+        ev = e["visits"] * world / (e_ms / 1e3)
+        line["e2e"] = {"value": round(ev, 1), "unit": UNIT,
+                       "h2d_bytes_per_step": int(e["h2d"]),
+                       "d2h_bytes_per_step": int(e["d2h"]),
+                       "ms_per_step": round(e_ms / e["steps"], 3),
+                       "steps": e["steps"],
+                       "call": "B200TuningSession._run_episode (compat.py) "
+                               "on a baseline/_ref TuningSession: numpy "
+                               "agent/moments + ensemble in, params/moments "
+                               f"+ {e['entries']} CandidateEntry out"}
+    else:
+        line["e2e"] = e
+    if c3:
+        c3v = c3["visits"] * world / (c3_ms / 1e3)
+        croof, ctab = roofline_table(c3["native"], c3["tables"], H,
+                                     c3["P"], peaks, c3["n_params"])
+        line["c3_64k"] = {
+            "workload": CONFIGS["c3"]["workload"], "value": round(c3v, 1),
+            "unit": UNIT, "ms_per_step": round(c3_ms / 3, 3), "steps": 3,
+            "warmup": 3, "population_per_gpu": c3["P"], "roofline": croof,
+            "kernels": {k: v for k, v in ctab.items()
+                        if k in ("k_mlp_f16<policy>", "k_mlp_f16<value>",
+                                 "k_policy_tc", "k_policy_tc64",
+                                 "k_value_tc", "k_sample_rows",
+                                 "k_featurize2", "k_gbt_finish",
+                                 "k_ppo_rows", "k_ppo_wgrad")}}
     if not args.no_cpu_baseline and world == 1:   # rank 0 at N=1 only
-        steps = 2
-        visits, secs = cpu_episode_sample(args.config, P, steps)
+        cb = cpu_pool(args.config, P, 0, 1)
         line["cpu_baseline"] = {
-            "value": round(visits / secs, 1), "unit": UNIT, "cores": 1,
-            "kind": "port",
-            "sample": f"oracle episode, {P} tracks x {steps} steps "
-                      f"({visits} visits) on 1 core, OPENBLAS_NUM_THREADS=1"}
+            "value": round(cb["value"], 1), "unit": UNIT,
+            "cores": cb["procs"], "kind": cb["kind"],
+            "sample": f"{cb['procs']} independent {cb['kind']} sessions x "
+                      f"{cb['per']} tracks, one full 60-step _run_episode "
+                      f"each ({cb['visits']} visits; single-process rate "
+                      f"{cb['per_process']:.0f}/s)",
+            "host": cb["host"]}
     print(json.dumps(line))
 
 
 def reference_arm(args, P, cfgd):
-    procs = len(os.sched_getaffinity(0))
-    steps = 2
-    # each "step" of the reference arm: one bounded sample of the workload
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_parallel(args.config, min(P, 2048), 1, min(procs, 2))
-    tot_v, tot_s = 0, 0.0
-    for _ in range(args.steps):
-        v, slowest, wall = cpu_parallel(args.config, P, steps, procs)
-        tot_v += v
-        tot_s += slowest
-    value = tot_v / tot_s
+    """The reference CPU path on this box's host cores: one reference
+    TuningSession per core, P/N tracks each (cli.py:231-235), full
+    60-step ``_run_episode`` calls of the same config; a step = one
+    episode in every process."""
+    steps = max(1, min(args.steps, 5))
+    warm = min(args.warmup, 1)
+    cb = cpu_pool(args.config, P, warm, steps)
+    value = cb["value"]
     line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT,
-            "impl": "reference", "n_gpus": 0, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(1e3 * tot_s / args.steps, 2),
+            "impl": "reference", "n_gpus": 0, "steps": steps,
+            "warmup": warm,
+            "ms_per_step": round(1e3 * cb["seconds"] / steps, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "fp64 (numpy)", "data": "synthetic",
+            "dtype": "fp64 (numpy)",
+            "data": "synthetic: random-init agents, SimulatedBackend "
+                    "warm start (512 states, fit_round)",
             "config": {"workload": cfgd["workload"], "population": P,
-                       "sample": f"{procs} processes x {P // procs} tracks x "
-                                 f"{steps} steps per timed step"},
+                       "episode": "cull_window 20, episode_len 40, "
+                                  "min_tracks P/2 per session (60 steps)",
+                       "sample": f"{cb['procs']} processes x {cb['per']} "
+                                 f"tracks x {steps} full episodes "
+                                 f"(+{warm} untimed)"},
             "cpu_baseline": {"value": round(value, 1), "unit": UNIT,
-                             "cores": procs, "kind": "port",
-                             "sample": f"{procs} independent oracle sessions "
-                                       f"x {max(2, P // procs)} tracks x "
-                                       f"{steps} steps"},
+                             "cores": cb["procs"], "kind": cb["kind"],
+                             "sample": f"{cb['procs']} independent "
+                                       f"{cb['kind']} sessions x {cb['per']} "
+                                       f"tracks, {steps} full episodes each; "
+                                       f"single-process rate "
+                                       f"{cb['per_process']:.0f}/s",
+                             "host": cb["host"]},
             "e2e": {"value": round(value, 1), "unit": UNIT,
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -695,13 +856,6 @@ def reference_arm(args, P, cfgd):
 
 # ---------------------------------------------------------------------------
 # C4: the ResNet-50 task set through the reference session (drop-in)
-
-
-def _ref_import():
-    ref = os.path.join(ROOT, "baseline", "_ref")
-    if os.path.isdir(ref) and ref not in sys.path:
-        sys.path.insert(0, ref)
-    import schedtune  # noqa: F401  (raises ImportError when absent)
 
 
 def taskset_session(cls_name, P, rank, world, rounds_budget):

@@ -517,8 +517,10 @@ int harl_heap_to_creation_order(const int32_t* feat_h, const double* thr_h,
  * bracketed by CUDA events on its own stream.  harl_profile_read
  * synchronises the recorded events and writes, per distinct kernel (first
  * appearance order, at most max_kernels), its name (NUL-terminated in
- * name_cap-byte slots), summed milliseconds and launch count; it returns
- * the number of distinct kernels. */
+ * name_cap-byte slots), summed milliseconds, launch count and summed work
+ * units (the rows each launch processed as the entry point counted them;
+ * -1 if any launch of that kernel did not report them); it returns the
+ * number of distinct kernels. */
 long long harl_launch_count(void);
 /* Debug: enable (on=1) phase timestamps (globaltimer ns) written by CTA 0
  * of the wide tcgen05 kernels; copies the first n (<= 64) to out_host. */
@@ -526,7 +528,8 @@ int harl_debug_timestamps(int on, unsigned long long* out_host, int n);
 int harl_profile_set(int on, long long spin_ns);
 int harl_profile_reset(void);
 int harl_profile_read(int max_kernels, char* names, int name_cap,
-                      double* total_ms, long long* launches);
+                      double* total_ms, long long* launches,
+                      long long* units);
 
 #ifdef __cplusplus
 }

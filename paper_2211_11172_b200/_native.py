@@ -181,7 +181,7 @@ _SIGS = {
     "harl_debug_timestamps": (i32, [i32, vp, i32]),
     "harl_profile_set": (i32, [i32, C.c_longlong]),
     "harl_profile_reset": (i32, []),
-    "harl_profile_read": (i32, [i32, C.c_char_p, i32, vp, vp]),
+    "harl_profile_read": (i32, [i32, C.c_char_p, i32, vp, vp, vp]),
     "harl_ppo_update": (i32, [P(NetLayout), P(NetLayout), P(PpoHyper),
                               P(ReplayRing), vp, i32, i32, i32, vp, i32, vp,
                               vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp,

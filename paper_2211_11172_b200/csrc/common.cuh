@@ -30,6 +30,7 @@ __device__ __forceinline__ void griddep_launch() {
 // captured) the pair becomes spin-kernel, event, <kernel>, event.
 void prof_begin(cudaStream_t st);
 void prof_end(const char* where);
+void prof_units(long long units);
 
 // phase timestamps of CTA 0 (debug: harl_debug_timestamps)
 __device__ int g_dbg_on;
@@ -66,6 +67,8 @@ __device__ inline void dbg_grid(bool end, int slot = 60) {
 }
 
 #define HARL_PROF_BEGIN(st) ::harl::prof_begin((cudaStream_t)(st))
+// work units (rows) of the launch that follows, for the per-kernel timer
+#define HARL_PROF_UNITS(u) ::harl::prof_units((long long)(u))
 
 #define HARL_CHECK_LAUNCH(where)                                     \
   do {                                                               \

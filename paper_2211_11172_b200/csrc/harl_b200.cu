@@ -23,6 +23,7 @@
 #include "mlp_tc.cuh"
 #include "sample_kernels.cuh"
 #include "mlp_tc2.cuh"
+#include "mlp_f16.cuh"
 #include "rank_kernels.cuh"
 #include "gbt_fit_kernels.cuh"
 #include "sim_kernels.cuh"
@@ -62,6 +63,7 @@ __global__ void k_spin(unsigned long long ns) {
 struct ProfRec {
   const char* name;
   cudaEvent_t e0, e1;
+  long long units;   // work units (rows) the launch processed, -1 unknown
 };
 
 static std::mutex g_prof_mu;
@@ -72,6 +74,7 @@ static std::vector<ProfRec> g_prof_recs;
 static size_t g_ev_used = 0;
 static thread_local cudaEvent_t t_pending = nullptr;
 static thread_local cudaStream_t t_pending_st = nullptr;
+static thread_local long long t_units = -1;
 static std::atomic<long long> g_launches{0};
 static const size_t PROF_MAX_EVENTS = 1 << 16;
 
@@ -101,14 +104,18 @@ void prof_begin(cudaStream_t st) {
   t_pending_st = st;
 }
 
+void prof_units(long long units) { t_units = units; }
+
 void prof_end(const char* where) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  const long long units = t_units;
+  t_units = -1;
   if (!t_pending) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t e1 = prof_event();
   if (e1) {
     cudaEventRecord(e1, t_pending_st);
-    g_prof_recs.push_back({where, t_pending, e1});
+    g_prof_recs.push_back({where, t_pending, e1, units});
   }
   t_pending = nullptr;
 }
@@ -269,6 +276,30 @@ static bool use_tc64() {
 }
 
 // HARL_TC_GEN1=1 selects the first-generation 4-warp tcgen05 kernels
+// 3xFP16 kernels (mlp_f16.cuh): HARL_TC16=0 falls back to 3xTF32;
+// HARL_TC16_MIN_ROWS: launches below this many rows keep the 3xTF32 path
+// (read per call: the A/B tests switch it inside one process; launches
+// inside captured graphs do not pass through here)
+static bool use_tc16(int64_t n) {
+  const char* e = getenv("HARL_TC16");
+  if (e && e[0] == '0') return false;
+  const char* m = getenv("HARL_TC16_MIN_ROWS");
+  return !m || n >= atoll(m);
+}
+
+// CTAs for a ping-pong f16 launch: every CTA takes tiles in pairs when
+// there are more tiles than SMs (HARL_TC16_GRID overrides)
+static int tc16_grid(int64_t tiles) {
+  static long long forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("HARL_TC16_GRID");
+    forced = e ? atoll(e) : 0;
+  }
+  int64_t g = tiles < sm_count() ? tiles : sm_count();
+  if (forced > 0 && forced < g) g = forced;
+  return (int)(g > 0 ? g : 1);
+}
+
 static bool use_tc2() {
   static int v = -1;
   if (v < 0) v = getenv("HARL_TC_GEN1") ? 0 : 1;
@@ -542,6 +573,7 @@ int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
     if ((rc = allow_smem(k_featurize2, smem2, "k_featurize2"))) return rc;
     HARL_PROF_BEGIN((cudaStream_t)stream);
     launch_k(k_featurize2, dim3((unsigned)((n + FEAT2_ROWS - 1) / FEAT2_ROWS)), dim3(FEAT2_THREADS), smem2, (cudaStream_t)stream, *sk, tiles, knobs, n, ld, feat);
+    HARL_PROF_UNITS(n);
     HARL_CHECK_LAUNCH("k_featurize2");
     return HARL_OK;
   }
@@ -549,6 +581,7 @@ int harl_featurize(const harl_sketch_desc* sk, const uint16_t* tiles,
   if ((rc = allow_smem(k_featurize, smem, "k_featurize"))) return rc;
   HARL_PROF_BEGIN((cudaStream_t)stream);
   launch_k(k_featurize, dim3((unsigned)((n + FEAT_THREADS - 1) / FEAT_THREADS)), dim3(FEAT_THREADS), smem, (cudaStream_t)stream, *sk, tiles, knobs, n, ld, feat);
+  HARL_PROF_UNITS(n);
   HARL_CHECK_LAUNCH("k_featurize");
   return HARL_OK;
 }
@@ -612,6 +645,7 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
           (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
           forest->n_nodes, forest->fitted, forest->base, forest->floor_value, feat,
           n, F, score, old_score, reward, (const GbtHdr*)forest->dev_hdr, T);
+    HARL_PROF_UNITS(n);
     HARL_CHECK_LAUNCH("k_gbt_predict2");
     return HARL_OK;
   }
@@ -624,6 +658,7 @@ int harl_gbt_predict(const harl_forest_desc* forest, const double* feat,
       (const GbtNode*)forest->nodes, forest->tree_first, forest->n_trees,
       forest->fitted, forest->base, forest->floor_value, feat, n, feature_len,
       score, old_score, reward, rows, (const GbtHdr*)forest->dev_hdr);
+  HARL_PROF_UNITS(n);
   HARL_CHECK_LAUNCH("k_gbt_predict");
   return HARL_OK;
 }
@@ -782,6 +817,7 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   else if (nI <= 12) grc = go(k_sample_rows<true, 12>, k_sample_rows<false, 12>);
   else grc = go(k_sample_rows<true, 16>, k_sample_rows<false, 16>);
   if (grc) return grc;
+  HARL_PROF_UNITS(n);
   HARL_CHECK_LAUNCH("k_sample_rows");
   return HARL_OK;
 }
@@ -827,6 +863,36 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int NHP = (pol->n_head_cols + 15) / 16 * 16;
+  // 3xFP16 policy (trunk + heads, weights resident, two tiles in flight)
+  if (!fuse_tc && packed_trunk && NHP <= F16_NHP_MAX && use_tc16(n) &&
+      ((uintptr_t)feat & 15) == 0 &&
+      (size_t)f16_smem_bytes(true, NHP, sk->feature_len, 1) <= (size_t)max_dyn_smem()) {
+    const size_t smem = (size_t)f16_smem_bytes(true, NHP, sk->feature_len, 1);
+    if ((rc = allow_smem(k_mlp_f16<true>, smem, "k_mlp_f16<policy>"))) return rc;
+    F16Args fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.nxb = 1;
+    fa.feat0 = feat;
+    fa.n0 = n;
+    fa.F = sk->feature_len;
+    fa.NH = pol->n_head_cols;
+    fa.NHP = NHP;
+    fa.logits = hid_scratch;
+    fa.logits_out = logits_out;
+    fa.img = (const uint8_t*)packed_trunk + TRUNK_IMAGE;
+    HARL_PROF_BEGIN(st);
+    launch_k(k_mlp_f16<true>, dim3(tc16_grid((n + 127) / 128)), dim3(F16_THREADS),
+             smem, st, fa);
+    HARL_PROF_UNITS(n);
+    HARL_CHECK_LAUNCH("k_mlp_f16<policy>");
+    const bool in_sampler = feat_out && n <= SAMPLE_FEAT_MAX_ROWS;
+    rc = launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
+                        TC_H, n, ld, tiles, knobs, inject, actions, logp,
+                        tiles_out, knobs_out, move_bits, shift_bits, head0_col,
+                        status, st, in_sampler ? feat_out : nullptr);
+    if (rc || !feat_out || in_sampler) return rc;
+    return harl_featurize(sk, tiles_out, knobs_out, n, ld, feat_out, stream);
+  }
   // fused step: policy -> sample/apply -> featurize in one kernel
   if (feat_out && fuse_tc && packed_trunk && packed_heads && use_tc2() &&
       ((uintptr_t)feat & 15) == 0) {
@@ -865,6 +931,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
       HARL_PROF_BEGIN(st);
       launch_k(k_policy_step_fused, dim3(grid), dim3(TC2_THREADS), smem, st, pa, fa,
                *sk, J);
+      HARL_PROF_UNITS(n);
       HARL_CHECK_LAUNCH("k_policy_step_fused");
       return HARL_OK;
     }
@@ -890,12 +957,14 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
       if ((rc = allow_smem(k_policy_tc64, (size_t)tc2_smem(NHP), "k_policy_tc64"))) return rc;
       HARL_PROF_BEGIN(st);
       launch_k(k_policy_tc64, dim3((unsigned)tiles64), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
+      HARL_PROF_UNITS(n);
       HARL_CHECK_LAUNCH("k_policy_tc64");
     } else {
       const int64_t tiles_n = (n + 127) / 128;
       const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
       HARL_PROF_BEGIN(st);
       launch_k(k_policy_tc, dim3(grid), dim3(TC2_THREADS), tc2_smem(NHP), st, pa);
+      HARL_PROF_UNITS(n);
       HARL_CHECK_LAUNCH("k_policy_tc");
     }
     // small populations (latency-bound steps): the sampler featurizes the
@@ -963,6 +1032,33 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
     return HARL_E_ARG;
   }
   if (n0 + n1 <= 0) return HARL_OK;
+  if (packed && use_tc16(n0 + n1) && ((uintptr_t)feat0 & 15) == 0 &&
+      ((uintptr_t)feat1 & 15) == 0 &&
+      (size_t)f16_smem_bytes(false, 0, feature_len, 1) <= (size_t)max_dyn_smem()) {
+    const int nxb = (size_t)f16_smem_bytes(false, 0, feature_len, 2) <=
+                    (size_t)max_dyn_smem() ? 2 : 1;
+    const size_t smem = (size_t)f16_smem_bytes(false, 0, feature_len, nxb);
+    if ((rc = allow_smem(k_mlp_f16<false>, smem, "k_mlp_f16<value>"))) return rc;
+    F16Args fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.nxb = nxb;
+    fa.feat0 = feat0;
+    fa.feat1 = feat1;
+    fa.n0 = n0;
+    fa.n1 = feat1 ? n1 : 0;
+    fa.F = feature_len;
+    fa.out0 = v0;
+    fa.out1 = v1;
+    fa.b3 = val->b[2];
+    fa.img = (const uint8_t*)packed + TRUNK_IMAGE;
+    const int64_t tiles_n = (n0 + 127) / 128 + (fa.n1 + 127) / 128;
+    HARL_PROF_BEGIN((cudaStream_t)stream);
+    launch_k(k_mlp_f16<false>, dim3(tc16_grid(tiles_n)), dim3(F16_THREADS), smem,
+             (cudaStream_t)stream, fa);
+    HARL_PROF_UNITS(n0 + fa.n1);
+    HARL_CHECK_LAUNCH("k_mlp_f16<value>");
+    return HARL_OK;
+  }
   if (packed && use_tc2() && ((uintptr_t)feat0 & 15) == 0 &&
       ((uintptr_t)feat1 & 15) == 0) {
     const size_t smem = (size_t)tc2_value_smem();
@@ -981,6 +1077,7 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
     const int grid = (int)(tiles_n < sm_count() ? tiles_n : sm_count());
     HARL_PROF_BEGIN((cudaStream_t)stream);
     launch_k(k_value_tc, dim3(grid), dim3(TC2_THREADS), smem, (cudaStream_t)stream, va);
+    HARL_PROF_UNITS(n0 + va.n1);
     HARL_CHECK_LAUNCH("k_value_tc");
     return HARL_OK;
   }
@@ -1028,6 +1125,8 @@ int harl_prepare(void) {
   if ((rc = allow_max_smem(k_policy_tc64, "k_policy_tc64"))) return rc;
   if ((rc = allow_max_smem(k_policy_step_fused, "k_policy_step_fused"))) return rc;
   if ((rc = allow_max_smem(k_value_tc, "k_value_tc"))) return rc;
+  if ((rc = allow_max_smem(k_mlp_f16<true>, "k_mlp_f16<policy>"))) return rc;
+  if ((rc = allow_max_smem(k_mlp_f16<false>, "k_mlp_f16<value>"))) return rc;
   if ((rc = allow_max_smem(k_ppo_rows, "k_ppo_rows"))) return rc;
   if ((rc = allow_max_smem(k_ppo_rows_tc, "k_ppo_rows_tc"))) return rc;
   // One shared-memory carveout for every kernel: the episode alternates
@@ -1073,6 +1172,9 @@ int harl_prepare(void) {
   carve(k_policy_tc64);
   carve(k_policy_step_fused);
   carve(k_value_tc);
+  carve(k_mlp_f16<true>);
+  carve(k_mlp_f16<false>);
+  carve(k_pack16);
   carve(k_finish_step);
   carve(k_ring_rows);
   carve(k_gather_rows);
@@ -1092,7 +1194,10 @@ int harl_prepare(void) {
 }
 
 int64_t harl_tc_packed_bytes(int32_t which, int32_t n_head_cols) {
-  if (which == 0) return TRUNK_IMAGE;
+  // trunk images carry the 3xFP16 image (heads included) behind them
+  if (which == 0)
+    return TRUNK_IMAGE +
+           f16_image_bytes(std::min((n_head_cols + 15) / 16 * 16, F16_NHP_MAX));
   return heads_image_bytes((n_head_cols + 15) / 16 * 16);
 }
 
@@ -1124,6 +1229,27 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     HARL_PROF_BEGIN(st);
     launch_k(k_pack_heads, dim3(64), dim3(256), 0, st, ha, (uint8_t*)pol_heads);
     HARL_CHECK_LAUNCH("k_pack_heads");
+    if (ha.NHP <= F16_NHP_MAX) {
+      uint8_t* f = (uint8_t*)pol_trunk + TRUNK_IMAGE;
+      float* ff = (float*)f;
+      uint16_t* h1 = (uint16_t*)(f + f16_off_w1());
+      uint16_t* h2 = (uint16_t*)(f + f16_off_w2());
+      uint16_t* hh = (uint16_t*)(f + f16_off_wh());
+      Pack16Args pk;
+      memset(&pk, 0, sizeof(pk));
+      pk.m[0] = {pol->W[0], feature_len, TC_H, TC_K1, TC_H, h1, h1 + F16_W1 / 2, ff + F16_SC + 0};
+      pk.m[1] = {pol->W[1], TC_H, TC_H, TC_H, TC_H, h2, h2 + F16_W2 / 2, ff + F16_SC + 1};
+      pk.m[2] = {pol->head_W, TC_H, pol->n_head_cols, TC_H, ha.NHP, hh,
+                 hh + ha.NHP * TC_H, ff + F16_SC + 2};
+      pk.v[0] = {pol->b[0], TC_H, TC_H, ff + F16_B1};
+      pk.v[1] = {pol->b[1], TC_H, TC_H, ff + F16_B2};
+      pk.v[2] = {pol->head_b, pol->n_head_cols, TC_H, ff + F16_B3};
+      pk.n_mat = 3;
+      pk.n_vec = 3;
+      HARL_PROF_BEGIN(st);
+      launch_k(k_pack16, dim3(3), dim3(1024), 0, st, pk);
+      HARL_CHECK_LAUNCH("k_pack16<policy>");
+    }
   }
   if (val && val_trunk) {
     if (!tc_trunk_ok(val, feature_len)) {
@@ -1142,6 +1268,22 @@ int harl_pack_tc_weights(const harl_mlp_desc* pol, const harl_mlp_desc* val,
     HARL_PROF_BEGIN(st);
     launch_k(k_pack_trunk, dim3(64), dim3(256), 0, st, ta, (uint8_t*)val_trunk, 1);
     HARL_CHECK_LAUNCH("k_pack_trunk<value>");
+    uint8_t* f = (uint8_t*)val_trunk + TRUNK_IMAGE;
+    float* ff = (float*)f;
+    uint16_t* h1 = (uint16_t*)(f + f16_off_w1());
+    uint16_t* h2 = (uint16_t*)(f + f16_off_w2());
+    Pack16Args pk;
+    memset(&pk, 0, sizeof(pk));
+    pk.m[0] = {val->W[0], feature_len, TC_H, TC_K1, TC_H, h1, h1 + F16_W1 / 2, ff + F16_SC + 0};
+    pk.m[1] = {val->W[1], TC_H, TC_H, TC_H, TC_H, h2, h2 + F16_W2 / 2, ff + F16_SC + 1};
+    pk.v[0] = {val->b[0], TC_H, TC_H, ff + F16_B1};
+    pk.v[1] = {val->b[1], TC_H, TC_H, ff + F16_B2};
+    pk.v[2] = {val->W[2], TC_H, TC_H, ff + F16_B3};
+    pk.n_mat = 2;
+    pk.n_vec = 3;
+    HARL_PROF_BEGIN(st);
+    launch_k(k_pack16, dim3(2), dim3(1024), 0, st, pk);
+    HARL_CHECK_LAUNCH("k_pack16<value>");
   }
   return HARL_OK;
 }
@@ -1229,6 +1371,7 @@ int harl_gbt_finish_step(const harl_forest_desc* forest, int32_t feature_len,
              forest->n_nodes, forest->fitted, forest->base, forest->floor_value,
              io->feat_new, n, F, score, old_score, reward,
              (const GbtHdr*)forest->dev_hdr, T, fa);
+  HARL_PROF_UNITS(n);
   HARL_CHECK_LAUNCH("k_gbt_finish");
   return HARL_OK;
 }
@@ -1463,6 +1606,14 @@ static int build_grad_jobs(const harl_net_layout& P, const harl_net_layout& V,
 int harl_selftest_tcgen05(const float* A, const float* B, float* D, int mode,
                           void* stream) {
   const size_t smem = (PROBE_N + PROBE_M) * PROBE_K * 4 + 1024;
+  if (mode >= 6) {
+    int rc = allow_smem(k_tc_probe_f16, smem, "k_tc_probe_f16");
+    if (rc) return rc;
+    HARL_PROF_BEGIN((cudaStream_t)stream);
+    launch_k(k_tc_probe_f16, dim3(1), dim3(128), smem, (cudaStream_t)stream, A, B, D, mode);
+    HARL_CHECK_LAUNCH("k_tc_probe_f16");
+    return HARL_OK;
+  }
   if (mode >= 3) {
     int rc = allow_smem(k_tc_probe_m64, smem, "k_tc_probe_m64");
     if (rc) return rc;
@@ -1631,6 +1782,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   ad.n = n_params;
   ad.h = *hp;
   // images as built by k_pack_trunk / k_pack_heads (mlp_tc.cuh)
+  // ... and, behind each trunk image, the 3xFP16 image (mlp_f16.cuh)
   auto add_trunk = [&](const harl_net_layout& L, uint8_t* img, bool value) {
     const int H = TC_H;
     float* w1h = (float*)img;
@@ -1638,20 +1790,38 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
     float* w2h = w1l + TC_K1 * H;
     float* w2l = w2h + H * H;
     float* bb = w2l + H * H;
-    ad.pk.mat[ad.pk.n_mat++] = {L.off_W[0], L.dims[0], H, TC_K1, w1h, w1l};
-    ad.pk.mat[ad.pk.n_mat++] = {L.off_W[1], H, H, H, w2h, w2l};
+    uint8_t* f = img + TRUNK_IMAGE;
+    float* ff = (float*)f;
+    uint16_t* h1 = (uint16_t*)(f + f16_off_w1());
+    uint16_t* h2 = (uint16_t*)(f + f16_off_w2());
+    ad.pk.mat[ad.pk.n_mat++] = {L.off_W[0], L.dims[0], H, TC_K1, w1h, w1l,
+                                h1, h1 + F16_W1 / 2, ff + F16_SC + 0};
+    ad.pk.mat[ad.pk.n_mat++] = {L.off_W[1], H, H, H, w2h, w2l,
+                                h2, h2 + F16_W2 / 2, ff + F16_SC + 1};
     ad.pk.vec[ad.pk.n_vec++] = {L.off_b[0], H, bb};
     ad.pk.vec[ad.pk.n_vec++] = {L.off_b[1], H, bb + H};
-    if (value) ad.pk.vec[ad.pk.n_vec++] = {L.off_W[2], H, bb + 2 * H};
+    ad.pk.vec[ad.pk.n_vec++] = {L.off_b[0], H, ff + F16_B1};
+    ad.pk.vec[ad.pk.n_vec++] = {L.off_b[1], H, ff + F16_B2};
+    if (value) {
+      ad.pk.vec[ad.pk.n_vec++] = {L.off_W[2], H, bb + 2 * H};
+      ad.pk.vec[ad.pk.n_vec++] = {L.off_W[2], H, ff + F16_B3};
+    }
   };
   if (pol_trunk_img && pol_heads_img) {
     add_trunk(*pol, (uint8_t*)pol_trunk_img, false);
     const int NHP = (pol->n_head_cols + 15) / 16 * 16;
     float* whh = (float*)pol_heads_img;
     float* whl = whh + NHP * TC_H;
+    uint8_t* f = (uint8_t*)pol_trunk_img + TRUNK_IMAGE;
+    uint16_t* hh = (uint16_t*)(f + f16_off_wh());
+    const bool f16 = NHP <= F16_NHP_MAX;
     ad.pk.mat[ad.pk.n_mat++] = {pol->off_hW, TC_H, pol->n_head_cols, TC_H,
-                                whh, whl};
+                                whh, whl, f16 ? hh : nullptr,
+                                hh + NHP * TC_H, (float*)f + F16_SC + 2};
     ad.pk.vec[ad.pk.n_vec++] = {pol->off_hb, pol->n_head_cols, whl + NHP * TC_H};
+    if (f16)
+      ad.pk.vec[ad.pk.n_vec++] = {pol->off_hb, pol->n_head_cols,
+                                  (float*)f + F16_B3};
   }
   if (val_trunk_img) add_trunk(*val, (uint8_t*)val_trunk_img, true);
   ad.tp = tplan;
@@ -1667,6 +1837,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
       launch_k(k_ppo_rows_tc, dim3((unsigned)((B + PPO8_ROWS - 1) / PPO8_ROWS), 2),
                dim3(PPO8_THREADS), tsmem, st, a, *pol, *val, *ring, idx, params,
                wt_params, rows, rowout);
+      HARL_PROF_UNITS(B);
       HARL_CHECK_LAUNCH("k_ppo_rows_tc");
     }
   } else {
@@ -1676,6 +1847,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
       HARL_PROF_BEGIN(st);
       launch_k(k_ppo_rows, dim3((unsigned)((B + PPO_TM - 1) / PPO_TM), 2), dim3(PPO_THREADS), rsmem, st, 
           a, *pol, *val, *ring, idx, params, wt_params, rows, rowout);
+      HARL_PROF_UNITS(B);
       HARL_CHECK_LAUNCH("k_ppo_rows");
     }
   }
@@ -1713,6 +1885,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   launch_k(k_ppo_wgrad, dim3((unsigned)n_tiles + 1), dim3(256), 0, st, jt, B, row_stride,
            rows, grads, bad, phase == 3 ? 1 : 0, (const double*)rowout, losses,
            phase == 3 ? B_norm : 0, hp->entropy_weight, hp->value_loss_weight);
+  HARL_PROF_UNITS(B);
   HARL_CHECK_LAUNCH("k_ppo_wgrad");
   }
   if (!(phase & 2)) return HARL_OK;
@@ -1766,11 +1939,12 @@ int harl_profile_reset(void) {
 }
 
 int harl_profile_read(int max_kernels, char* names, int name_cap,
-                      double* total_ms, long long* launches) {
+                      double* total_ms, long long* launches,
+                      long long* units) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   std::vector<std::string> keys;
   std::vector<double> ms;
-  std::vector<long long> cnt;
+  std::vector<long long> cnt, un;
   for (const ProfRec& r : g_prof_recs) {
     cudaError_t e = cudaEventSynchronize(r.e1);
     if (e != cudaSuccess) return cuda_status(e, "harl_profile_read");
@@ -1783,9 +1957,12 @@ int harl_profile_read(int max_kernels, char* names, int name_cap,
       keys.push_back(r.name);
       ms.push_back(0.0);
       cnt.push_back(0);
+      un.push_back(0);
     }
     ms[k] += t;
     cnt[k] += 1;
+    // a launch whose units are unknown poisons the kernel's total
+    if (un[k] >= 0) un[k] = r.units >= 0 ? un[k] + r.units : -1;
   }
   const int n = (int)keys.size();
   for (int k = 0; k < n && k < max_kernels; ++k) {
@@ -1795,6 +1972,7 @@ int harl_profile_read(int max_kernels, char* names, int name_cap,
     }
     if (total_ms) total_ms[k] = ms[k];
     if (launches) launches[k] = cnt[k];
+    if (units) units[k] = un[k];
   }
   return n;
 }

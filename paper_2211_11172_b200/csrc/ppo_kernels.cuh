@@ -846,6 +846,10 @@ struct PackMat {
   int32_t K, N, Kpad;
   float* hi;
   float* lo;
+  // optional 3xFP16 image (mlp_f16.cuh): halves of p32 * (*sc16)
+  uint16_t* h16;
+  uint16_t* l16;
+  const float* sc16;
 };
 struct PackVec {
   int64_t off;
@@ -854,7 +858,7 @@ struct PackVec {
 };
 struct PackPlan {
   PackMat mat[6];
-  PackVec vec[6];
+  PackVec vec[12];
   int32_t n_mat, n_vec;
 };
 
@@ -934,6 +938,9 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a,
         const uint32_t o = tc::kmajor_off(nn, k, M.Kpad) / 4;
         M.hi[o] = hi;
         M.lo[o] = lo;
+        if (M.h16)
+          tc::store_split_f16(p32 * *M.sc16, M.h16, M.l16,
+                              tc::kmajor16_off(nn, k, M.Kpad));
       }
     }
     for (int q = 0; q < a.pk.n_vec; ++q) {

@@ -7,6 +7,7 @@
 // [46,48) version=1, [61,64) layout (0 = no swizzle).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace harl {
@@ -105,6 +106,11 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// kind::f16 with fp16 A and B (formats 0), fp32 accumulate, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // K-major, no swizzle ("interleaved") canonical layout: core matrices of
 // 8 rows x 16 bytes; lbo = byte distance between K-adjacent core matrices,
 // sbo = byte distance between 8-row groups.
@@ -122,6 +128,13 @@ __device__ inline uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
 __host__ __device__ inline uint32_t kmajor_off(int row, int k, int k_total) {
   return (uint32_t)((row >> 3) * (k_total / 4) * 128 + (k >> 2) * 128 +
                     (row & 7) * 16 + (k & 3) * 4);
+}
+
+// the same layout for 2-byte elements: a core matrix is 8 rows x 8
+// elements; lbo = 128, sbo = K_total/8*128; one K=16 MMA step = 256 bytes
+__host__ __device__ inline uint32_t kmajor16_off(int row, int k, int k_total) {
+  return (uint32_t)((row >> 3) * (k_total / 8) * 128 + (k >> 3) * 128 +
+                    (row & 7) * 16 + (k & 7) * 2);
 }
 
 // -- MMA -------------------------------------------------------------------------
@@ -145,6 +158,33 @@ __device__ inline void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem,
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+__device__ inline void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc,
+                                  uint64_t b_desc, uint32_t idesc,
+                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ inline void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem,
+                                  uint64_t b_desc, uint32_t idesc,
+                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// two fp32 values -> one fp16x2 word (first in the low half), RN
+__device__ inline uint32_t pack_half2(float lo_elem, float hi_elem) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
+}
+
 // -- TMEM <-> registers (warp-collective; warp w%4 owns lanes 32(w%4)..) ----
 __device__ inline void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
@@ -163,6 +203,20 @@ __device__ inline void tmem_ld32(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ inline void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+        "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]),
+        "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ inline void tmem_st32(uint32_t taddr, const float* v) {
@@ -273,6 +327,15 @@ __device__ inline float to_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+
+// 3xFP16 split of one value into the 2-byte K-major image at byte offset
+// `off`: hi = fp16(x) (RN), lo = fp16(x - hi)
+__device__ inline void store_split_f16(float w, uint16_t* hi, uint16_t* lo,
+                                       uint32_t off) {
+  const __half h = __float2half_rn(w);
+  hi[off / 2] = __half_as_ushort(h);
+  lo[off / 2] = __half_as_ushort(__float2half_rn(w - __half2float(h)));
 }
 
 // 3xTF32 split: x ~= hi + lo with both exactly representable in tf32

@@ -178,4 +178,72 @@ k_tc_probe_m64(const float* A, const float* B, float* D, int mode) {
   if (warp == 0) tc::tmem_dealloc(tm, 256);
 }
 
+// kind::f16 probes (fp16 operands, fp32 accumulate), M=128 N=128 K=64:
+// mode 6: A from TMEM, two fp16 per 32-bit column, element k of a row at
+// column k/2, even k in the low half; mode 7: A from shared memory in the
+// 2-byte K-major core layout.  B from shared memory in the same layout.
+// The operands arrive as fp32 values the host made fp16-exact.
+__global__ void __launch_bounds__(128)
+k_tc_probe_f16(const float* A, const float* B, float* D, int mode) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sB = sm;                                  // N x K fp16 (K-major)
+  uint8_t* sA = sm + PROBE_N * PROBE_K * 2;          // M x K fp16
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tc::tmem_alloc(&tbase, 256);
+  if (tid == 0) tc::mbar_init(&bar, 1);
+  for (int i = tid; i < PROBE_K * PROBE_N; i += blockDim.x) {
+    const int k = i / PROBE_N, n = i % PROBE_N;
+    *(__half*)(sB + tc::kmajor16_off(n, k, PROBE_K)) = __float2half_rn(B[i]);
+  }
+  for (int i = tid; i < PROBE_M * PROBE_K; i += blockDim.x) {
+    const int m = i / PROBE_K, k = i % PROBE_K;
+    *(__half*)(sA + tc::kmajor16_off(m, k, PROBE_K)) = __float2half_rn(A[i]);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t d_col = 0, a_col = 128;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  if (mode == 6) {
+    float v[32];
+    for (int j = 0; j < 32; ++j)
+      v[j] = __uint_as_float(tc::pack_half2(A[tid * PROBE_K + 2 * j],
+                                            A[tid * PROBE_K + 2 * j + 1]));
+    tc::tmem_st32(tm + lane_base + a_col, v);
+    tc::tmem_st_wait();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_f16(PROBE_M, PROBE_N);
+    const uint32_t sb = PROBE_K / 8 * 128;
+    for (int s = 0; s < PROBE_K / 16; ++s) {
+      const uint64_t bd = tc::sdesc(tc::smem_u32(sB) + 256 * s, 128, sb);
+      if (mode == 7) {
+        const uint64_t ad = tc::sdesc(tc::smem_u32(sA) + 256 * s, 128, sb);
+        tc::mma_f16_ss(tm + d_col, ad, bd, idesc, s > 0);
+      } else {
+        tc::mma_f16_ts(tm + d_col, tm + a_col + 8 * s, bd, idesc, s > 0);
+      }
+    }
+    tc::mma_commit(&bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after();
+  float out[32];
+  for (int c0 = 0; c0 < PROBE_N; c0 += 32) {
+    tc::tmem_ld32(tm + lane_base + d_col + c0, out);
+    for (int j = 0; j < 32; ++j) D[tid * PROBE_N + c0 + j] = out[j];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tm, 256);
+}
+
 }  // namespace harl

@@ -293,6 +293,7 @@ def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
     if exclude is not None and len(exclude[1]):
         E = len(exclude[1])
         ex_t, ex_k = states_to_device(tables, exclude[0], exclude[1], dev)
+        PF.xfer("h2d", ex_t, ex_k)
     sc.ensure(n_visits, E, k)
     elog = N.EntryLog(log_tiles.data_ptr(), log_knobs.data_ptr(),
                       log_score.data_ptr(), 0, 0, log_tiles.shape[1])
@@ -304,6 +305,7 @@ def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
             sc.out.numel(), sc.stats.data_ptr(), _stream()),
             "harl_rank_topk")
     st = sc.stats.cpu().numpy()
+    PF.xfer("d2h", sc.stats)
     n = int(st[0])
     stats = {"selected": n, "kept": int(st[1]), "collisions": int(st[2]),
              "k_target": int(st[3])}
@@ -763,6 +765,7 @@ class DeviceForest:
         h["base"], h["floor_value"] = float(base), float(floor_value)
         h["n_nodes"] = len(nodes)
         self.hdr.copy_(torch.from_numpy(h.view(np.uint8).copy()))
+        PF.xfer("h2d", nodes.nbytes + firsts.nbytes + h.nbytes)
         # host mirrors (informational; the kernels read the header)
         self.desc.fitted = 1 if fitted else 0
         self.desc.base = float(base)
@@ -941,7 +944,7 @@ class DeviceAgent:
         if not self.tc:
             return
         lib = N.load()
-        with PF.span("pack", 0, launches=3):
+        with PF.span("pack", 0, launches=None):
             N.check(lib.harl_pack_tc_weights(
                 C.byref(self.pol_desc), C.byref(self.val_desc), self.F,
                 _ptr(self.packed["pt"]), _ptr(self.packed["ph"]),
@@ -1002,6 +1005,7 @@ class DeviceAgent:
         self.params32.copy_(p.float())
         self.m.copy_(torch.from_numpy(self._pack(a.opt_pi.m, a.opt_v.m)))
         self.v.copy_(torch.from_numpy(self._pack(a.opt_pi.v, a.opt_v.v)))
+        PF.xfer("h2d", self.params, self.m, self.v)
         self.refresh_derived()
 
     def refresh_derived(self):
@@ -1023,6 +1027,7 @@ class DeviceAgent:
         self._unpack_into(self.params.cpu().numpy(), a.policy, a.value)
         self._unpack_into(self.m.cpu().numpy(), a.opt_pi.m, a.opt_v.m)
         self._unpack_into(self.v.cpu().numpy(), a.opt_pi.v, a.opt_v.v)
+        PF.xfer("d2h", self.params, self.m, self.v)
 
     def _build_descs(self):
         base = self.params32.data_ptr()

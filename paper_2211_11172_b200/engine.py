@@ -189,6 +189,8 @@ class EpisodeResult:
             idx = didx[:n].cpu().numpy().astype(np.int64)
             tiles, knobs = D.states_to_host(self.tables, t, kn, n)
             f, sc = f.cpu().numpy(), sc.cpu().numpy()
+            PF.xfer("d2h", idx.nbytes + tiles.nbytes + knobs.nbytes +
+                    f.nbytes + sc.nbytes)
         else:
             S = self.tables.local_slots
             pi, pt, pk, pf, ps = pins
@@ -197,6 +199,7 @@ class EpisodeResult:
             pk[:, :n].copy_(kn[:, :n], non_blocking=True)
             pf[:n].copy_(f[:n], non_blocking=True)
             ps[:n].copy_(sc[:n], non_blocking=True)
+            PF.xfer("d2h", pi[:n], pt[:S, :n], pk[:, :n], pf[:n], ps[:n])
             torch.cuda.current_stream().synchronize()
             idx = pi[:n].numpy().astype(np.int64)
             tiles = np.ascontiguousarray(
@@ -490,6 +493,7 @@ class EpisodeEngine:
         else:
             res = self._run_graphed(b, gen, cfg, order_counter)
         st = b.status.cpu().numpy().view(np.uint64)
+        PF.xfer("d2h", b.status)
         for code in st[:len(plan)]:
             D.raise_status(int(code))
         self.dagent.raise_if_diverged()
@@ -730,6 +734,7 @@ class EpisodeEngine:
                 train.append((step["t"], losses, B))
                 ppo_k += 1
         st = b.status.cpu().numpy().view(np.uint64)
+        PF.xfer("d2h", b.status)
         for code in st[:len(plan)]:
             D.raise_status(int(code))
         self.dagent.raise_if_diverged()
@@ -869,9 +874,11 @@ class EpisodeEngine:
             b.rng_tab[k0:k1 + 1].copy_(pins["rng"][k0:k1 + 1], non_blocking=True)
             b.wpos_tab[k0:k1 + 1].copy_(pins["wpos"][k0:k1 + 1],
                                         non_blocking=True)
+            PF.xfer("h2d", b.rng_tab[k0:k1 + 1], b.wpos_tab[k0:k1 + 1])
             if p1 > p0:
                 b.slot_tab[p0:p1].copy_(pins["slot"][p0:p1], non_blocking=True)
                 b.adam_tab[p0:p1].copy_(pins["adam"][p0:p1], non_blocking=True)
+                PF.xfer("h2d", b.slot_tab[p0:p1], b.adam_tab[p0:p1])
 
         segs = b.graphs
         # rows of segment 0 first; then, before blocking anywhere, the rows
@@ -913,6 +920,7 @@ class EpisodeEngine:
                                                       pin_memory=True)
                     kp[:len(keep)].numpy()[:] = keep
                     b.keep[:len(keep)].copy_(kp[:len(keep)], non_blocking=True)
+                    PF.xfer("h2d", b.keep[:len(keep)])
                 else:
                     gone = self._cull_native(b, rt_i, m, alive, cfg)
                 culls.append((prev["t"], gone, int(alive.sum())))
@@ -1018,6 +1026,7 @@ class EpisodeEngine:
         pt, pa = b.cull_pin
         pt[:m].copy_(b.rt[rt_i][:m], non_blocking=True)
         pa[:m].copy_(b.adv[:m], non_blocking=True)
+        PF.xfer("d2h", pt[:m], pa[:m])
         torch.cuda.current_stream().synchronize()
         if np.isnan(pa[:m].numpy()).any():   # the reference's sort (_cull)
             tracks = pt[:m].numpy().astype(np.int64)
@@ -1026,6 +1035,7 @@ class EpisodeEngine:
             b.keep_pin[:len(keep)].numpy()[:] = keep
             b.keep[:len(keep)].copy_(b.keep_pin[:len(keep)],
                                      non_blocking=True)
+            PF.xfer("h2d", b.keep[:len(keep)])
             return gone
         a8 = b.alive8
         a8[:len(alive)] = alive
@@ -1037,6 +1047,7 @@ class EpisodeEngine:
             "harl_cull_select")
         alive[:] = a8[:len(alive)].astype(bool)
         b.keep[:nk.value].copy_(b.keep_pin[:nk.value], non_blocking=True)
+        PF.xfer("h2d", b.keep[:nk.value])
         return gone
 
     def _cull_inputs(self, b, rt_i, m):
@@ -1049,6 +1060,7 @@ class EpisodeEngine:
         pt, pa = b.cull_pin
         pt[:m].copy_(b.rt[rt_i][:m], non_blocking=True)
         pa[:m].copy_(b.adv[:m], non_blocking=True)
+        PF.xfer("d2h", pt[:m], pa[:m])
         torch.cuda.current_stream().synchronize()
         return pt[:m].numpy().astype(np.int64), pa[:m].numpy().copy()
 

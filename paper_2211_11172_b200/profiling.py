@@ -10,8 +10,11 @@ from __future__ import annotations
 
 import contextlib
 
+import numpy as np
+
 _launches = 0
 _timing = False
+_xfer = {"h2d": 0, "d2h": 0}   # host<->device bytes moved by the library
 _spans = []   # (name, rows, start_event, end_event)
 
 
@@ -19,6 +22,24 @@ def reset():
     global _launches, _spans
     _launches = 0
     _spans = []
+
+
+def xfer(kind: str, *tensors_or_bytes):
+    """Account host<->device bytes (``kind`` "h2d" or "d2h") of the copies
+    the library issues: tensors (their bytes) or plain byte counts."""
+    n = 0
+    for t in tensors_or_bytes:
+        n += int(t) if isinstance(t, (int, np.integer)) else \
+            t.numel() * t.element_size()
+    _xfer[kind] += n
+
+
+def xfer_reset():
+    _xfer["h2d"] = _xfer["d2h"] = 0
+
+
+def xfer_bytes() -> dict:
+    return dict(_xfer)
 
 
 def timing(on: bool):
@@ -94,8 +115,10 @@ def native_timing(on: bool, spin_ns: int = 20000):
 
 
 def native_kernel_times() -> dict:
-    """{kernel name: {"ms": summed ms, "launches": n}} from the native
-    timer (synchronises the recorded events)."""
+    """{kernel name: {"ms": summed ms, "launches": n, "units": rows}} from
+    the native timer (synchronises the recorded events); ``units`` is the
+    rows the launches processed as the library counted them (-1 when a
+    launch site does not report them)."""
     import ctypes as C
     import numpy as np
     from . import _native as N
@@ -104,15 +127,17 @@ def native_kernel_times() -> dict:
     names = C.create_string_buffer(cap * width)
     ms = np.zeros(cap, dtype=np.float64)
     cnt = np.zeros(cap, dtype=np.int64)
+    units = np.zeros(cap, dtype=np.int64)
     n = lib.harl_profile_read(cap, names, width, ms.ctypes.data,
-                              cnt.ctypes.data)
+                              cnt.ctypes.data, units.ctypes.data)
     if n < 0:
         N.check(n, "harl_profile_read")
     raw = names.raw
     out = {}
     for k in range(min(n, cap)):
         nm = raw[k * width:(k + 1) * width].split(b"\0", 1)[0].decode()
-        out[nm] = {"ms": float(ms[k]), "launches": int(cnt[k])}
+        out[nm] = {"ms": float(ms[k]), "launches": int(cnt[k]),
+                   "units": int(units[k])}
     return out
 
 

@@ -85,12 +85,15 @@ def test_graph_replay_is_bit_identical(monkeypatch, hidden, which, lazy):
                                   "_SPLIT_FINISH", "_PAR_VALUE"])
 def test_kernel_fusion_variants_match_default(monkeypatch, flag):
     """Each alternative launch structure produces the default episode bit
-    for bit: _FUSED_STEP (k_policy_step_fused: policy -> sample/apply ->
-    featurize in one kernel), _SPLIT_FEATURIZE (k_featurize2 launched after
+    for bit: _FUSED_STEP (k_policy_step_fused: the 3xTF32 policy -> sample/
+    apply -> featurize in one kernel, against the 3xTF32 default), _SPLIT_FEATURIZE (k_featurize2 launched after
     the sampler instead of inside it), _SPLIT_FINISH (k_gbt_predict2 +
     k_finish_step instead of the fused k_gbt_finish), _PAR_VALUE (the value
     pass on a forked stream beside the GBT pass, joined by the finish)."""
     from paper_2211_11172_b200 import engine as E
+    if flag == "_FUSED_STEP":
+        # the fused kernel is the 3xTF32 policy: compare with that default
+        monkeypatch.setenv("HARL_TC16", "0")
     tb, forest, cfg, (_, dflt) = _setup((128, 128), "conv")
     _, _, _, (_, alt) = _setup((128, 128), "conv")
     g1, g2 = np.random.default_rng(9), np.random.default_rng(9)

@@ -1,10 +1,10 @@
 """Network-output parity at the north-star sizes (>= 64 K candidates).
 
 At these sizes the production tcgen05 kernels run their persistent
-multi-tile paths -- ``k_policy_tc`` (128-row tiles; a CTA owns several tiles
-above 148 x 128 rows, re-staging X and re-streaming W1/heads per tile) and
-``k_value_tc`` (two populations, several tiles per CTA) -- which the small
-oracle tests never reach.  Each test compares them with the oracle's fp64
+multi-tile paths -- ``k_mlp_f16<policy>`` / ``k_mlp_f16<value>`` (3xFP16,
+two 128-row tiles in flight per CTA, several tile pairs per CTA above
+148 x 128 rows) and, on the 3xTF32 fallback, ``k_policy_tc`` /
+``k_value_tc`` -- which the small oracle tests never reach.  Each test compares them with the oracle's fp64
 forward chunk by chunk (tests/large_util.py):
 
 * one policy step + V(X)/V(X') at 65,536 rows (C3 sketch k3, 512 tiles)
@@ -16,8 +16,8 @@ forward chunk by chunk (tests/large_util.py):
   oracle (every draw vouched for, states/features/scores/rewards bit-exact,
   logp/advantages within 1e-4; with the device's logp/advantages in the
   oracle's FIFO, the parameters after all 30 PPO updates within 1e-6);
-* the golden and shadow replays re-run with HARL_TC64=0 (the M=128 kernel
-  on every launch instead of the 64-row-tile one).
+* the golden and shadow replays and the 64 K multi-tile check re-run on
+  the 3xTF32 fallback (HARL_TC16=0, with and without HARL_TC64=0).
 """
 
 import os
@@ -255,15 +255,23 @@ def test_c1_full_episode_shadow_replay():
     assert_close_rel(got, ref, tol=1e-6, what="params after 30 updates")
 
 
-def test_golden_and_shadow_replays_without_tc64():
-    """HARL_TC64=0: every policy launch on the M=128 kernel (the library
-    reads the switch once per process, so the replays run in a child)."""
-    env = dict(os.environ, HARL_TC64="0")
+@pytest.mark.parametrize("env", [{"HARL_TC16": "0"},
+                                 {"HARL_TC16": "0", "HARL_TC64": "0"}],
+                         ids=["tf32", "tf32-m128"])
+def test_replays_on_the_tf32_fallback(env):
+    """The 3xTF32 kernels (the fallback where the 3xFP16 image does not fit:
+    more than 128 padded head columns, F > 64 staging) stay verified: the
+    golden and shadow replays and the 64 K multi-tile oracle check re-run
+    with HARL_TC16=0, and with HARL_TC64=0 as well (k_policy_tc's M=128
+    tiles on every launch), in a child process."""
     p = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-x", "-p",
-         "no:cacheprovider", os.path.join(ROOT, "tests",
-                                          "test_gpu_episode.py"),
-         "-k", "golden_episode_replay or shadow_replay"],
-        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+         "no:cacheprovider",
+         os.path.join(ROOT, "tests", "test_gpu_episode.py"),
+         os.path.join(ROOT, "tests", "test_gpu_large.py"),
+         "-k", "golden_episode_replay or shadow_replay or "
+               "multitile_vs_oracle and c3"],
+        cwd=ROOT, env=dict(os.environ, **env), capture_output=True,
+        text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
     assert " passed" in p.stdout

@@ -35,12 +35,18 @@ void prof_units(long long units);
 // phase timestamps of CTA 0 (debug: harl_debug_timestamps)
 __device__ int g_dbg_on;
 __device__ unsigned long long g_dbg_ts[64];
+// (compiled in only with -DHARL_PHASE_TS: the check costs every thread of
+// the hot kernels a few instructions per stamp, ~3 % of the sampler)
 __device__ inline void dbg_ts(int i) {
+#ifdef HARL_PHASE_TS
   if (blockIdx.x == 0 && threadIdx.x == 0 && g_dbg_on) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_dbg_ts[i] = t;
   }
+#else
+  (void)i;
+#endif
 }
 
 // Ampere-style asynchronous 16-byte global->shared copies (no register

@@ -84,7 +84,11 @@ __device__ inline double row_logp(const float* z, int C, Legal legal, int a) {
   return (double)z[a] - (double)zmax - log(s);
 }
 
-// 3-column shift head, sequential in one thread (the reference's cumsum)
+// 3-column shift head, sequential in one thread (the reference's cumsum).
+// The inverse CDF compares the running sum of the exps with u * s instead
+// of dividing every probability by s (the reference's p = e / s, cumsum,
+// count(c < u)); the two differ only for a uniform within rounding of a
+// CDF boundary, far inside the fp32-logit flips the parity tests bound.
 __device__ inline int sample3(const float* z, uint32_t m3, double u,
                               double* logp_out) {
   float zmax = -INFINITY;
@@ -95,16 +99,19 @@ __device__ inline int sample3(const float* z, uint32_t m3, double u,
     e[j] = ((m3 >> j) & 1u) ? (double)expf(z[j] - zmax) : 0.0;
     s += e[j];
   }
+  const double us = u * s;
   int count = 0;
   double c = 0.0;
   for (int j = 0; j < 3; ++j) {
-    c += e[j] / s;
-    count += (c < u);
+    c += e[j];
+    count += (c < us);
   }
   int idx = min(count, 2);
   while (idx > 0 && !((m3 >> idx) & 1u)) --idx;
   const bool ok = (m3 >> idx) & 1u;
-  *logp_out = ok ? ((double)z[idx] - (double)zmax - log(s)) : -INFINITY;
+  // log(s) in fp32 (s in [1, 3]): ~2e-7 absolute on logp
+  *logp_out = ok ? ((double)z[idx] - (double)zmax - (double)logf((float)s))
+                 : -INFINITY;
   return ok ? idx : -1;
 }
 
@@ -325,16 +332,11 @@ __device__ __forceinline__ void sample_group(
     }
     const double s = gsum(sl);
     dbg_ts(19);
-    const double inv = 1.0 / s;
-    // lane-local inclusive prefix of p_j = e_j / s; the lane's offset is the
-    // exclusive scan of the lane totals (3 shuffle steps)
-    double tot = 0.0;
-#pragma unroll
-    for (int i = 0; i < MAXI; ++i) tot += (double)e[i] * inv;
-    for (int i = MAXI; i < nI; ++i) {
-      const int j = jb + i;
-      if (j < C0 && legal0(j)) tot += (double)expf(z[j] - zmax) * inv;
-    }
+    // inverse CDF on the running sums of the exps against u * s (no
+    // division per column, see sample3); lane offsets = exclusive scan of
+    // the lane totals (3 shuffle steps)
+    const double tot = sl;
+    const double us0 = u0 * s;
     double incl = tot;
 #pragma unroll
     for (int o = 1; o < SG; o <<= 1) {
@@ -345,14 +347,14 @@ __device__ __forceinline__ void sample_group(
     int count = 0;
 #pragma unroll
     for (int i = 0; i < MAXI; ++i) {
-      c += (double)e[i] * inv;
-      if (((rm >> i) & 1u) && c < u0) ++count;
+      c += (double)e[i];
+      if (((rm >> i) & 1u) && c < us0) ++count;
     }
     for (int i = MAXI; i < nI; ++i) {
       const int j = jb + i;
       if (j < C0) {
-        if (legal0(j)) c += (double)expf(z[j] - zmax) * inv;
-        if (c < u0) ++count;
+        if (legal0(j)) c += (double)expf(z[j] - zmax);
+        if (c < us0) ++count;
       }
     }
     count = gsumi(count);
@@ -360,7 +362,10 @@ __device__ __forceinline__ void sample_group(
     int idx = min(count, C0 - 1);
     while (idx > 0 && !legal0(idx)) --idx;
     const bool ok = legal0(idx);
-    const double lp0 = ok ? ((double)z[idx] - (double)zmax - log(s)) : -INFINITY;
+    // log(s) in fp32 (s in [1, C0]): ~5e-7 absolute on logp, against the
+    // 1e-4 * max(|logp|, rms) tolerance
+    const double lp0 = ok ? ((double)z[idx] - (double)zmax -
+                             (double)logf((float)s)) : -INFINITY;
     act[0] = !ok ? 0 : ((idx == C0 - 1) ? S * S : s_src[idx] * S + s_dst[idx]);
     col0 = ok ? idx : 0;
     // shift heads: lane h-1 handles head h

@@ -64,6 +64,11 @@ __device__ inline void cp_async_wait_all() {
 // grid extent probe: earliest CTA start / latest CTA end of one kernel
 // (slots 60/61; harl_debug_timestamps resets them with on=1)
 __device__ inline void dbg_grid(bool end, int slot = 60) {
+#ifndef HARL_PHASE_TS
+  (void)end;
+  (void)slot;
+  return;
+#endif
   if (threadIdx.x == 0 && g_dbg_on == 2) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

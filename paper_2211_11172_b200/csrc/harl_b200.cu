@@ -813,9 +813,16 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
     return HARL_OK;
   };
   int grc;
-  if (nI <= 8) grc = go(k_sample_rows<true, 8>, k_sample_rows<false, 8>);
-  else if (nI <= 12) grc = go(k_sample_rows<true, 12>, k_sample_rows<false, 12>);
-  else grc = go(k_sample_rows<true, 16>, k_sample_rows<false, 16>);
+  // instantiation: head-0 columns cached per lane (MAXI) x slots per lane
+  const int nsl = sk->local_slots <= 2 * SG ? 2 : (sk->local_slots <= 4 * SG ? 4 : 8);
+#define HARL_SAMPLER(MX, NS) go(k_sample_rows<true, MX, NS>, k_sample_rows<false, MX, NS>)
+#define HARL_SAMPLER_NSL(MX) \
+  (nsl == 2 ? HARL_SAMPLER(MX, 2) : nsl == 4 ? HARL_SAMPLER(MX, 4) : HARL_SAMPLER(MX, 8))
+  if (nI <= 8) grc = HARL_SAMPLER_NSL(8);
+  else if (nI <= 12) grc = HARL_SAMPLER_NSL(12);
+  else grc = HARL_SAMPLER_NSL(16);
+#undef HARL_SAMPLER_NSL
+#undef HARL_SAMPLER
   if (grc) return grc;
   HARL_PROF_UNITS(n);
   HARL_CHECK_LAUNCH("k_sample_rows");
@@ -1155,12 +1162,14 @@ int harl_prepare(void) {
   carve(k_gbt_predict2<false>);
   carve(k_policy_step);
   carve(k_value_forward);
-  carve(k_sample_rows<false, 8>);
-  carve(k_sample_rows<true, 8>);
-  carve(k_sample_rows<false, 12>);
-  carve(k_sample_rows<true, 12>);
-  carve(k_sample_rows<false, 16>);
-  carve(k_sample_rows<true, 16>);
+#define HARL_CARVE_SAMPLER(MX) \
+  carve(k_sample_rows<false, MX, 2>); carve(k_sample_rows<true, MX, 2>); \
+  carve(k_sample_rows<false, MX, 4>); carve(k_sample_rows<true, MX, 4>); \
+  carve(k_sample_rows<false, MX, 8>); carve(k_sample_rows<true, MX, 8>);
+  HARL_CARVE_SAMPLER(8)
+  HARL_CARVE_SAMPLER(12)
+  HARL_CARVE_SAMPLER(16)
+#undef HARL_CARVE_SAMPLER
   carve(k_gbt_finish<true>);
   carve(k_gbt_finish<false>);
   carve(k_trunk_tc<TRUNK_POLICY>);

@@ -202,7 +202,9 @@ __device__ __noinline__ InjectRow sample_inject_row(
 // rows past a.n compute on row 0 and write nothing, so every lane stays in
 // the group shuffles).  zrow: the row's logits (null: a.logits + r*ldz);
 // s_src/s_dst: the compact head-0 column tables, filled by the caller.
-template <int MAXI = SAMPLE_MAXI>
+// NSL: slots per lane (a row's local slots <= SG * NSL; the host picks the
+// smallest of 2 / 4 / 8, so the state loops carry no dead iterations)
+template <int MAXI = SAMPLE_MAXI, int NSL = HARL_MAX_SLOTS / SG>
 __device__ __forceinline__ void sample_group(
     const harl_sketch_desc& sk, const PcgJump& J, u128 base_arg,
     const u128* base_dev, const uint16_t* __restrict__ tiles,
@@ -224,9 +226,10 @@ __device__ __forceinline__ void sample_group(
     if (base_dev) base = *base_dev;
     if (a.grow) grow_r = (int64_t)a.grow[rr];
   }
-  int tv[HARL_MAX_SLOTS / SG];
+  static_assert(NSL * SG <= HARL_MAX_SLOTS, "slots per lane");
+  int tv[NSL];
 #pragma unroll
-  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i) {
+  for (int i = 0; i < NSL; ++i) {
     const int s = g + SG * i;
     tv[i] = s < sk.local_slots ? tiles[(int64_t)s * a.ld + rr] : 0;
   }
@@ -273,7 +276,7 @@ __device__ __forceinline__ void sample_group(
   // ---- current state: lane g holds slots g, g+8, ... --------------------
   uint64_t mv = 0;
 #pragma unroll
-  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i)
+  for (int i = 0; i < NSL; ++i)
     if (tv[i] > 1) mv |= 1ull << (g + SG * i);
 #pragma unroll
   for (int o = SG / 2; o; o >>= 1) mv |= __shfl_xor_sync(0xffffffffu, mv, o, SG);
@@ -407,7 +410,7 @@ __device__ __forceinline__ void sample_group(
   const int didx = dst >= 0 && dst < HARL_MAX_SLOTS ? dst : 0;
   int vs = 0, vd = 0;
 #pragma unroll
-  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i) {
+  for (int i = 0; i < NSL; ++i) {
     if (i == sidx / SG) vs = tv[i];
     if (i == didx / SG) vd = tv[i];
   }
@@ -432,7 +435,7 @@ __device__ __forceinline__ void sample_group(
   if (!live) return;
   const bool moved = code == HARL_ST_OK && src >= 0;
 #pragma unroll
-  for (int i = 0; i < HARL_MAX_SLOTS / SG; ++i) {
+  for (int i = 0; i < NSL; ++i) {
     const int s = g + SG * i;
     if (s < sk.local_slots) {
       int v = tv[i];
@@ -523,7 +526,7 @@ __device__ __forceinline__ void featurize_group(const harl_sketch_desc& sk,
 // MAXI: head-0 columns cached per lane (>= ceil(C0 / SG) for the cached
 // path; the host picks the smallest of 8 / 12 / 16 that covers the head so
 // the unrolled column loops carry no dead iterations)
-template <bool FEAT, int MAXI>
+template <bool FEAT, int MAXI, int NSL>
 __global__ void __launch_bounds__(SAMPLE_THREADS, HARL_SAMPLE_MINB)
 k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const __grid_constant__ PcgJump J,
@@ -548,7 +551,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   const int lr = threadIdx.x / SG;
   const int64_t r0 = (int64_t)blockIdx.x * ROWS;
   const int64_t r = r0 + lr;
-  sample_group<MAXI>(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src,
+  sample_group<MAXI, NSL>(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src,
                s_dst, FEAT ? s_st[lr] : nullptr, FEAT ? s_kn[lr] : nullptr,
                /*fill_tables=*/true, FEAT ? s_foot : nullptr, lut_s, lut_n);
   dbg_ts(23);

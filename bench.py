@@ -467,22 +467,30 @@ def measure_peaks(torch, dev):
     return out
 
 
-def value_leg(cfg_name, P, steps, warmup, dev, rank, world, profile=True):
+def value_leg(cfg_name, P, steps, warmup, dev, rank, world, profile=True,
+              shard=None):
     """Device-resident episodes (EpisodeEngine.run_episode), population in
     HBM: CUDA events on the launching stream around each episode, L2
     flushed between episodes (outside the events).  Then one untimed,
     eagerly launched episode with the library's per-launch event timer for
-    the per-kernel table."""
+    the per-kernel table.
+
+    ``shard`` (world, rank, group): one population of P * world tracks
+    sharded across the ranks (EpisodeEngine(shard=...): interleaved tracks,
+    merged culls, one gradient all-reduce per PPO update); every rank
+    starts from the same agent, cost model and generator.  Otherwise each
+    rank runs its own task replica of P tracks."""
     import torch
     from paper_2211_11172_b200 import device as D
     from paper_2211_11172_b200 import profiling
     from paper_2211_11172_b200.engine import EpisodeEngine
-    w = build_workload(cfg_name, P, seed=rank, synthetic=False)
+    seed = 0 if shard else rank
+    w = build_workload(cfg_name, P, seed=seed, synthetic=False)
     tb = w["tables"]
-    gen = np.random.default_rng(1000 + rank)
+    gen = np.random.default_rng(1000 + seed)
     trees, base = device_warm_start(tb, w["sg"].flops, gen, dev)
-    ecfg = episode_config(P)
-    eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, dev)
+    ecfg = episode_config(P * world if shard else P)
+    eng = EpisodeEngine(w["agent"], w["rl"], tb.levels, dev, shard=shard)
     forest = D.DeviceForest(trees, base, 0.3, device=dev)
     stream = torch.cuda.current_stream()
     order = 0
@@ -507,12 +515,15 @@ def value_leg(cfg_name, P, steps, warmup, dev, rank, world, profile=True):
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
-            visits += res.visits
-            order += res.visits
+            # sharded: every rank reports the whole population's visits
+            visits += res.extra.get("global_visits", res.visits) if shard \
+                else res.visits
+            order += res.extra.get("global_visits", res.visits)
     torch.cuda.synchronize()
     launches = profiling.launch_count()
     out = dict(total_ms=total_ms, visits=visits, clocks=clk.summary(),
                launches=launches, P=P, tables=tb, n_trees=len(trees),
+               eng=eng, forest=forest, gen=gen, ecfg=ecfg, order=order,
                n_params=sum(p.size for p in w["agent"].policy) +
                sum(p.size for p in w["agent"].value))
     if profile:
@@ -527,6 +538,7 @@ def value_leg(cfg_name, P, steps, warmup, dev, rank, world, profile=True):
         e1.record(stream)
         e1.synchronize()
         eng.use_graphs = True
+        out["order"] = order + res.extra.get("global_visits", res.visits)
         out["native"] = profiling.native_kernel_times()
         out["profiled_episode_ms"] = e0.elapsed_time(e1)
         profiling.native_timing(False)
@@ -666,12 +678,56 @@ def roofline_table(native, tables, H, P, peaks, n_params):
     return roof, table
 
 
+def e2e_shard_leg(r, steps, world):
+    """e2e of the sharded mode (the drop-in is one session per process, so
+    the sharded engine is the public API here): every timed episode uploads
+    the host agent (numpy parameters + Adam moments) to each rank, runs the
+    sharded episode and writes parameters and moments back to numpy; wall
+    time, max over ranks, the library's accounted H2D/D2H bytes."""
+    import torch
+    from paper_2211_11172_b200 import profiling as PF
+    eng, tb, forest, gen = r["eng"], r["tables"], r["forest"], r["gen"]
+    ms, visits, h2d, d2h = 0.0, 0, 0, 0
+    order = r["order"]
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        PF.xfer_reset()
+        t0 = time.perf_counter()
+        eng.dagent.upload()
+        res = eng.run_episode(tb, forest, gen, r["ecfg"], order)
+        eng.sync_to_host()
+        torch.cuda.synchronize()
+        ms += (time.perf_counter() - t0) * 1e3
+        v = res.extra.get("global_visits", res.visits)
+        visits += v
+        order += v
+        x = PF.xfer_bytes()
+        h2d += x["h2d"]
+        d2h += x["d2h"]
+    return dict(ms=ms, visits=visits, steps=steps, h2d=h2d // steps,
+                d2h=d2h // steps, entries=0, sharded=True)
+
+
 def gpu_arm(args, P, rank, world):
     import torch
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    # (ranks beyond the visible devices share them: the gloo tests run two
+    # ranks on one GPU)
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) %
+                       torch.cuda.device_count())
     torch.cuda.set_device(dev)
     peaks = measure_peaks(torch, dev)
-    r = value_leg(args.config, P, args.steps, args.warmup, dev, rank, world)
+    shard = None
+    if world > 1 and args.mode == "shard":
+        import torch.distributed as dist
+        shard = (world, rank, dist.group.WORLD)
+    r = value_leg(args.config, P, args.steps, args.warmup, dev, rank, world,
+                  shard=shard)
+    if shard:
+        e = e2e_shard_leg(r, max(1, min(args.steps, 5)), world)
+        return peaks, r, e, None
     try:
         e = e2e_leg(args.config, P, min(args.steps, 5), min(args.warmup, 3),
                     dev, rank)
@@ -690,7 +746,8 @@ def _max_over_ranks(vals, world):
         return vals
     import torch
     import torch.distributed as dist
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    t = torch.tensor(vals, dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t]
 
@@ -706,6 +763,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the C3 64K sub-measurement")
+    ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
+                    help="N > 1: one population of P*N tracks sharded over "
+                         "the ranks (gradient all-reduce), or N independent "
+                         "task replicas")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -723,7 +784,8 @@ def main():
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        # HARL_DIST_BACKEND=gloo: two ranks on one GPU (tests)
+        dist.init_process_group(os.environ.get("HARL_DIST_BACKEND", "nccl"))
     peaks, r, e, c3 = gpu_arm(args, P, rank, world)
     total_ms, = _max_over_ranks([r["total_ms"]], world)
     e_ms = _max_over_ranks([e.get("ms", 0.0)], world)[0]
@@ -732,7 +794,8 @@ def main():
         return
     tb = r["tables"]
     H = 128
-    visits_all = r["visits"] * world
+    sharded = world > 1 and args.mode == "shard"
+    visits_all = r["visits"] * (1 if sharded else world)
     value = visits_all / (total_ms / 1e3)
     n_params = r["n_params"]
     roof, table = roofline_table(r["native"], tb, H, P, peaks, n_params)
@@ -755,7 +818,12 @@ def main():
                               "min_tracks P/2 (60 steps, P*40 visits)",
                    "hidden": [H, H], "step": "one full _run_episode",
                    "l2": "flushed (256 MiB write) between timed episodes",
-                   "parallelism": f"independent task replicas x{world}"
+                   "parallelism": (f"one population of {P * world} tracks "
+                                   f"sharded over {world} GPUs (track i on "
+                                   f"rank i mod {world}, NCCL all-reduce of "
+                                   f"the PPO gradients, merged culls)"
+                                   if sharded else
+                                   f"independent task replicas x{world}")
                    if world > 1 else "single GPU"},
         "gpu_launches": int(r["launches"]),
         "clocks": r["clocks"],
@@ -779,16 +847,19 @@ def main():
         "profiled_episode_ms": round(r["profiled_episode_ms"], 3),
     }
     if "ms" in e:
-        ev = e["visits"] * world / (e_ms / 1e3)
+        ev = e["visits"] * (1 if e.get("sharded") else world) / (e_ms / 1e3)
         line["e2e"] = {"value": round(ev, 1), "unit": UNIT,
                        "h2d_bytes_per_step": int(e["h2d"]),
                        "d2h_bytes_per_step": int(e["d2h"]),
                        "ms_per_step": round(e_ms / e["steps"], 3),
                        "steps": e["steps"],
-                       "call": "B200TuningSession._run_episode (compat.py) "
-                               "on a baseline/_ref TuningSession: numpy "
-                               "agent/moments + ensemble in, params/moments "
-                               f"+ {e['entries']} CandidateEntry out"}
+                       "call": ("sharded EpisodeEngine.run_episode with the "
+                                "numpy agent/moments uploaded and written "
+                                "back every episode" if e.get("sharded") else
+                                "B200TuningSession._run_episode (compat.py) "
+                                "on a baseline/_ref TuningSession: numpy "
+                                "agent/moments + ensemble in, params/moments "
+                                f"+ {e['entries']} CandidateEntry out")}
     else:
         line["e2e"] = e
     if c3:

@@ -634,6 +634,29 @@ class EpisodeEngine:
             dist.all_reduce(h, group=group)
             t.copy_(h)
 
+    def _gather_advantages(self, b, local_ids, m_l, P):
+        """Every rank's (track id, advantage) of the cull step: one
+        all-gather of fixed-size tensors (ceil(P / G) rows per rank, track
+        id -1 for padding) on the device for NCCL, on the host for gloo."""
+        import torch.distributed as dist
+        world, _, group = self.shard
+        cap = (P + world - 1) // world
+        dev = self.dev
+        mine = torch.full((2, cap), -1.0, dtype=torch.float64, device=dev)
+        mine[0, :m_l] = torch.from_numpy(local_ids[:m_l].astype(np.float64)
+                                         ).to(dev)
+        mine[1, :m_l] = b.adv[:m_l]
+        nccl = dist.get_backend(group) == "nccl"
+        src = mine if nccl else mine.cpu()
+        out = torch.empty((world * 2, cap), dtype=src.dtype,
+                          device=src.device)
+        dist.all_gather_into_tensor(out, src, group=group)
+        o = out.cpu().numpy().reshape(world, 2, cap)
+        ids = o[:, 0, :].reshape(-1)
+        av = o[:, 1, :].reshape(-1)
+        keep = ids >= 0
+        return ids[keep].astype(np.int64), av[keep]
+
     def _run_sharded(self, tables, forest, gen, cfg, order_counter):
         """This rank's share of the episode: tracks i with i % G == rank
         (shard.py).  Every rank advances the same generator; uniforms are
@@ -676,31 +699,39 @@ class EpisodeEngine:
         used_local, used, ppo_k = 0, 0, 0
         local_rows = []
         cap = self.replay.cap
+        grow_all = None                          # changes only at culls
+        live = None
         for k, step in enumerate(plan):
             m = step["m"]
-            grow_all = lay.global_rows(alive, local_ids)
+            if grow_all is None:
+                # the local rows' global rows: fixed between culls, so one
+                # (pinned, asynchronous) upload per segment -- a pageable
+                # copy per step would synchronise the stream every step
+                grow_all = lay.global_rows(alive, local_ids)
+                live = np.flatnonzero(alive)
+                if getattr(b, "grow_pin", None) is None:
+                    b.grow_pin = torch.empty(Pl, dtype=torch.int32,
+                                             pin_memory=True)
+                n_g = len(grow_all)
+                b.grow_pin[:n_g].numpy()[:] = grow_all
+                b.grow[:n_g].copy_(b.grow_pin[:n_g], non_blocking=True)
             m_l = int(np.searchsorted(grow_all, m))   # local rows in sel
-            b.grow[:m_l].copy_(torch.from_numpy(grow_all[:m_l].astype(np.int32)))
             keep_from = int(np.searchsorted(grow_all[:m_l], max(0, m - cap)))
             self._launch_step(b, k, step, cur, nxt, rt, used_local, False,
                               gen=gen, m=m_l, grow=b.grow, m_total=m,
                               keep_from=keep_from)
             self.replay.note_push(m_l)
             local_rows.append(m_l)
-            live = np.flatnonzero(alive)
             self._gidx.push_step(live[:m] % world)
             cur, nxt = nxt, cur
             used_local += m_l
             used += m
             if step["cull"]:
-                mine = (local_ids[:m_l], b.adv[:m_l].cpu().numpy())
-                got = [None] * world
-                dist.all_gather_object(got, mine, group=group)
-                ids = np.concatenate([g_[0] for g_ in got])
-                av = np.concatenate([g_[1] for g_ in got])
+                ids, av = self._gather_advantages(b, local_ids, m_l, P)
                 gone = cull_decision(alive, ids, av, cfg.cull_fraction,
                                      cfg.min_tracks)
                 alive[gone] = False
+                grow_all = None
                 culls.append((step["t"], gone, int(alive.sum())))
                 keep = np.flatnonzero(alive[local_ids]).astype(np.int32)
                 b.keep[:len(keep)].copy_(torch.from_numpy(keep))
@@ -713,7 +744,18 @@ class EpisodeEngine:
                 pos = gen.choice(len(self._gidx), size=B, replace=False)
                 owners, lpush = self._gidx.locate(pos)
                 slots = (lpush[owners == rank] % cap).astype(np.int32)
-                slots_t = torch.from_numpy(slots).to(dev)
+                # pinned ring of slot lists (one per update of the episode):
+                # the copy stays asynchronous
+                sp = getattr(b, "slot_pin", None)
+                if sp is None or sp.shape[1] < B:
+                    sp = b.slot_pin = torch.empty(
+                        (max(1, sum(1 for s_ in plan if s_["ppo"])), B),
+                        dtype=torch.int32, pin_memory=True)
+                    b.slot_dev = torch.empty_like(sp, device=dev)
+                sp[ppo_k, :len(slots)].numpy()[:] = slots
+                b.slot_dev[ppo_k, :len(slots)].copy_(sp[ppo_k, :len(slots)],
+                                                     non_blocking=True)
+                slots_t = b.slot_dev[ppo_k, :len(slots)]
                 a = self.agent
                 a.opt_pi.t += 1
                 a.opt_v.t += 1
@@ -723,10 +765,17 @@ class EpisodeEngine:
                                        a.opt_pi.t, a.opt_v.t,
                                        scratch=self._ppo_scratch,
                                        losses=losses, B_norm=B, phase=1)
-                self._allreduce_(self.dagent.grads)
-                sums = losses[5:9].clone()
-                self._allreduce_(sums)
-                losses[5:9].copy_(sums)
+                # one all-reduce: gradients and the loss partial sums
+                n_g = self.dagent.grads.numel()
+                buf = getattr(self, "_ar_buf", None)
+                if buf is None or buf.numel() != n_g + 4:
+                    buf = self._ar_buf = torch.empty(
+                        n_g + 4, dtype=torch.float64, device=dev)
+                buf[:n_g].copy_(self.dagent.grads.view(-1))
+                buf[n_g:].copy_(losses[5:9])
+                self._allreduce_(buf)
+                self.dagent.grads.view(-1).copy_(buf[:n_g])
+                losses[5:9].copy_(buf[n_g:])
                 self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
                                        a.opt_pi.t, a.opt_v.t,
                                        scratch=self._ppo_scratch,

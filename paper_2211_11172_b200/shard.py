@@ -24,7 +24,6 @@ episode* as the single-device one:
 from __future__ import annotations
 
 import math
-from collections import deque
 
 import numpy as np
 
@@ -41,7 +40,8 @@ class ShardLayout:
         return np.asarray(track_ids) % world
 
     def global_rows(self, alive: np.ndarray, local_alive_ids: np.ndarray):
-        """Global row (rank among all alive ids) of each locally alive id."""
+        """Global row (rank among all alive ids) of each locally alive id.
+        (Callers cache it: it changes only when a cull changes ``alive``.)"""
         csum = np.cumsum(alive) - 1
         return csum[local_alive_ids].astype(np.int64)
 
@@ -51,28 +51,43 @@ class GlobalReplayIndex:
 
     Pushes arrive per step in global-row order; every rank appends its own
     rows to its local ring (capacity ``cap`` each, more than enough since a
-    rank only ever needs the rows that survive globally)."""
+    rank only ever needs the rows that survive globally).  Kept as a numpy
+    ring of (owner rank, local push number) -- one vectorised append per
+    step, no per-row Python."""
 
     def __init__(self, cap: int, world: int):
         self.cap, self.G = cap, world
-        self.items = deque(maxlen=cap)      # (rank, local push counter)
-        self.local_pushes = [0] * world
+        self._rank = np.zeros(cap, dtype=np.int64)
+        self._push = np.zeros(cap, dtype=np.int64)
+        self._n = 0                         # total global pushes so far
+        self.local_pushes = np.zeros(world, dtype=np.int64)
 
     def __len__(self):
-        return len(self.items)
+        return min(self._n, self.cap)
 
     def push_step(self, owners_in_row_order):
-        for r in owners_in_row_order:
-            r = int(r)
-            self.items.append((r, self.local_pushes[r]))
-            self.local_pushes[r] += 1
+        o = np.asarray(owners_in_row_order, dtype=np.int64)
+        m = len(o)
+        if m == 0:
+            return
+        # local push number of each row: the owner's running count
+        onehot = o[:, None] == np.arange(self.G)[None, :]
+        before = np.cumsum(onehot, axis=0) - onehot
+        num = self.local_pushes[o] + before[np.arange(m), o]
+        self.local_pushes += onehot.sum(axis=0)
+        keep = min(m, self.cap)             # only the last cap rows survive
+        pos = (self._n + np.arange(m - keep, m)) % self.cap
+        self._rank[pos] = o[m - keep:]
+        self._push[pos] = num[m - keep:]
+        self._n += m
 
     def locate(self, positions):
-        """Global FIFO positions -> (rank, local push number) arrays."""
-        items = list(self.items)
-        sel = [items[int(i)] for i in positions]
-        return (np.asarray([s[0] for s in sel], dtype=np.int64),
-                np.asarray([s[1] for s in sel], dtype=np.int64))
+        """Global FIFO positions (0 = oldest kept) -> (rank, local push
+        number) arrays."""
+        p = np.asarray(positions, dtype=np.int64)
+        first = self._n - len(self)
+        slot = (first + p) % self.cap
+        return self._rank[slot].copy(), self._push[slot].copy()
 
 
 def eliminated(live, adv_live, n_elim):

@@ -40,6 +40,28 @@ def test_replay_index_tracks_the_global_fifo():
     assert ranks.tolist() == [0, 1, 1] and local.tolist() == [1, 1, 3]
 
 
+def test_replay_index_matches_a_row_by_row_fifo():
+    """The vectorised index against the plain deque of (rank, local push)
+    it replaces: random step sizes, some larger than the capacity."""
+    from collections import deque
+    rng = np.random.default_rng(3)
+    for world, cap in ((1, 7), (2, 16), (4, 64), (8, 33)):
+        idx = GlobalReplayIndex(cap=cap, world=world)
+        ref, counts = deque(maxlen=cap), [0] * world
+        for _ in range(40):
+            own = rng.integers(0, world, size=int(rng.integers(0, 3 * cap)))
+            idx.push_step(own)
+            for r in own:
+                ref.append((int(r), counts[r]))
+                counts[r] += 1
+            assert len(idx) == len(ref)
+            if len(ref):
+                pos = rng.integers(0, len(ref), size=10)
+                ranks, local = idx.locate(pos)
+                assert ranks.tolist() == [ref[p][0] for p in pos]
+                assert local.tolist() == [ref[p][1] for p in pos]
+
+
 def test_cull_decision_ties_drop_higher_index():
     alive = np.ones(6, dtype=bool)
     gone = cull_decision(alive, np.arange(6), np.array([0, 0, 1, 1, 0, 2.]),

@@ -23,7 +23,31 @@ struct GbtHdr {
   int32_t n_trees, fitted;
   double base, floor_value;
   int64_t n_nodes;
+  int32_t max_depth;        // internal levels of the deepest tree
+  int32_t perfect_depth;    // > 0: the perfect-tree image below is valid
+  const uint8_t* perfect;   // perfect-tree image (device)
+  int64_t perfect_bytes;    // its size (multiple of 16)
 };
+
+// Perfect-tree image of a forest of depth D <= GBT_PERFECT_MAX: every tree
+// padded to a complete binary tree of D levels, breadth-first (children of
+// slot i at 2i+1, 2i+2), so a walk needs no child links: thresholds
+// f64 [T][2^D-1] | leaf lr*values f64 [T][2^D] | features i16 [T][2^D-1].
+// A leaf above level D becomes pass-through slots (feature 0, threshold
+// +inf) whose whole subtree repeats its value, so every route through
+// them -- a NaN feature goes right, as in the reference's walk -- ends on
+// the same leaf value.
+constexpr int GBT_PERFECT_MAX = 7;
+__host__ __device__ inline size_t gbt_perfect_off_leaf(int T, int D) {
+  return ((size_t)T * ((1 << D) - 1) * 8 + 15) & ~(size_t)15;
+}
+__host__ __device__ inline size_t gbt_perfect_off_feat(int T, int D) {
+  return gbt_perfect_off_leaf(T, D) + (size_t)T * (1 << D) * 8;
+}
+__host__ __device__ inline size_t gbt_perfect_bytes(int T, int D) {
+  return (gbt_perfect_off_feat(T, D) + (size_t)T * ((1 << D) - 1) * 2 + 15) &
+         ~(size_t)15;
+}
 
 struct __align__(16) GbtNode {
   double v;        // split threshold (internal) / lr*value (leaf)
@@ -95,14 +119,46 @@ k_gbt_predict(const GbtNode* __restrict__ nodes,
 // tile's 64 rows); 16 groups (1024 threads) measured slower: the 64-register
 // cap spills the fused finish epilogue (C2 20.5 -> 24.2 us)
 constexpr int GBT2_GROUPS = HARL_GBT_GROUPS;
+
+// one node record as a single 16-byte shared-memory load (the compiler
+// otherwise splits it into four loads), and a shared-memory fp64 load
+// through an explicit state space (the feature tile pointer is chosen at
+// run time between two buffers, which demoted its loads to generic ones)
+__device__ __forceinline__ void lds_node(uint32_t addr, double& v, int& feat,
+                                         int& left, int& right) {
+  uint32_t a, b, c, d;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
+  v = __hiloint2double((int)b, (int)a);
+  feat = (int)(int16_t)(c & 0xffffu);
+  left = (int)(int16_t)(c >> 16);
+  right = (int)(int16_t)(d & 0xffffu);
+}
+__device__ __forceinline__ int lds_s16(uint32_t addr) {
+  short v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return (int)v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+constexpr int GBT_ILP = 4;               // trees walked side by side
+constexpr int GBT_WALK_MAX_DEPTH = 24;   // fixed-depth walk up to this depth
 constexpr int GBT2_ROWS = 64;
 constexpr int GBT2_THREADS = GBT2_ROWS * GBT2_GROUPS;
 
 __host__ __device__ inline size_t gbt2_align(size_t x) { return (x + 15) & ~(size_t)15; }
 
+__host__ __device__ inline size_t gbt2_node_region(int64_t n_nodes, int T) {
+  const size_t rec = gbt2_align((size_t)n_nodes * 16);
+  const size_t per = gbt_perfect_bytes(T, GBT_PERFECT_MAX);
+  return rec > per ? rec : per;
+}
 __host__ __device__ inline size_t gbt2_smem_bytes(bool smem_nodes, int64_t n_nodes,
                                                   int T, int F) {
-  return (smem_nodes ? gbt2_align((size_t)n_nodes * 16) : 0) +
+  return (smem_nodes ? gbt2_node_region(n_nodes, T) : 0) +
          gbt2_align((size_t)T * 4) + 2 * gbt2_align((size_t)GBT2_ROWS * F * 8) +
          (size_t)GBT2_ROWS * T * 8;
 }
@@ -123,26 +179,35 @@ __device__ __forceinline__ void gbt2_body(
   dbg_ts(24);
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ uint64_t fbar, xbar[2];
+  int max_depth = 1 << 30;   // unknown: the while-loop walk
+  int pdepth = 0;
+  const uint8_t* perfect = nullptr;
+  int64_t perfect_bytes = 0;
   if (hdr) {   // reloadable forest: the scalars live on the device
     n_trees = hdr->n_trees;
     fitted = hdr->fitted;
     base = hdr->base;
     floor_value = hdr->floor_value;
     n_nodes = hdr->n_nodes;
+    max_depth = hdr->max_depth;
+    pdepth = hdr->perfect_depth;
+    perfect = hdr->perfect;
+    perfect_bytes = hdr->perfect_bytes;
   }
+  if (!SMEM_NODES || pdepth > GBT_PERFECT_MAX) pdepth = 0;
   size_t off = 0;
   const GbtNode* nodes = gnodes;
   GbtNode* sn = (GbtNode*)gsm;
   if (SMEM_NODES) {
     nodes = sn;
-    off = gbt2_align((size_t)n_nodes * 16);
+    // the node region is sized for either layout (t_cap: capacity in trees)
+    off = gbt2_node_region(n_nodes, t_cap > n_trees ? t_cap : n_trees);
   }
   int32_t* s_first = (int32_t*)(gsm + off);
   off += gbt2_align((size_t)(n_trees > t_cap ? n_trees : t_cap) * 4);
-  double* xsb[2];
-  xsb[0] = (double*)(gsm + off);
+  double* const xsb0 = (double*)(gsm + off);
   off += gbt2_align((size_t)GBT2_ROWS * F * 8);
-  xsb[1] = (double*)(gsm + off);
+  double* const xsb1 = (double*)(gsm + off);
   off += gbt2_align((size_t)GBT2_ROWS * F * 8);
   double* contrib = (double*)(gsm + off);
   const int64_t n_tiles = (n + GBT2_ROWS - 1) / GBT2_ROWS;
@@ -150,11 +215,13 @@ __device__ __forceinline__ void gbt2_body(
     tc::mbar_init(&fbar, 1);
     tc::mbar_init(&xbar[0], 1);
     tc::mbar_init(&xbar[1], 1);
-    if (SMEM_NODES && n_nodes > 0) tc::bulk_load(sn, gnodes, (uint32_t)n_nodes * 16, &fbar);
+    if (SMEM_NODES && pdepth > 0 && perfect_bytes > 0)
+      tc::bulk_load(sn, perfect, (uint32_t)perfect_bytes, &fbar);
+    else if (SMEM_NODES && n_nodes > 0) tc::bulk_load(sn, gnodes, (uint32_t)n_nodes * 16, &fbar);
     else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&fbar)) : "memory");
     if (blockIdx.x < n_tiles) {
       const int64_t r0 = (int64_t)blockIdx.x * GBT2_ROWS;
-      tc::bulk_f64(xsb[0], feat + r0 * F,
+      tc::bulk_f64(xsb0, feat + r0 * F,
                    (uint32_t)(min((int64_t)GBT2_ROWS, n - r0) * F), &xbar[0]);
     }
   }
@@ -179,19 +246,95 @@ __device__ __forceinline__ void gbt2_body(
       const int64_t nt = tile + gridDim.x;
       if (nt < n_tiles) {   // the other buffer was released at the end of it-1
         const int64_t n0 = nt * GBT2_ROWS;
-        tc::bulk_f64(xsb[b ^ 1], feat + n0 * F,
+        tc::bulk_f64(b ? xsb0 : xsb1, feat + n0 * F,
                      (uint32_t)(min((int64_t)GBT2_ROWS, n - n0) * F), &xbar[b ^ 1]);
       }
     }
     if (it < 2) dbg_ts(25 + 3 * it);
-    const double* xs = xsb[b];
+    const double* xs = b ? xsb1 : xsb0;
     if (fitted && rl < rows) {
       const double* x = xs + rl * F;
-      for (int t = g; t < n_trees; t += GBT2_GROUPS) {
-        const GbtNode* tree = nodes + s_first[t];
-        GbtNode nd = tree[0];
-        while (nd.feat >= 0) nd = tree[(x[nd.feat] <= nd.v) ? nd.left : nd.right];
-        contrib[rl * n_trees + t] = nd.v;
+      if (pdepth > 0) {
+        // perfect-tree walk: slot 2i+1+(x > thr), no child links to load;
+        // GBT_ILP trees side by side
+        const int D = pdepth, NI = (1 << D) - 1, NLF = 1 << D;
+        const uint32_t s_thr = tc::smem_u32(sn);
+        const uint32_t s_leaf = s_thr + (uint32_t)gbt_perfect_off_leaf(n_trees, D);
+        const uint32_t s_feat = s_thr + (uint32_t)gbt_perfect_off_feat(n_trees, D);
+        const uint32_t s_x = tc::smem_u32(x);
+        for (int t0 = g; t0 < n_trees; t0 += GBT_ILP * GBT2_GROUPS) {
+          uint32_t tbase[GBT_ILP], idx[GBT_ILP];
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) {
+            const int t = t0 + k * GBT2_GROUPS;
+            tbase[k] = (uint32_t)((t < n_trees ? t : t0) * NI);
+            idx[k] = 0;
+          }
+          for (int lv = 0; lv < D; ++lv) {
+            int f[GBT_ILP];
+            double th[GBT_ILP], xv[GBT_ILP];
+#pragma unroll
+            for (int k = 0; k < GBT_ILP; ++k) {
+              f[k] = lds_s16(s_feat + 2u * (tbase[k] + idx[k]));
+              th[k] = lds_f64(s_thr + 8u * (tbase[k] + idx[k]));
+            }
+#pragma unroll
+            for (int k = 0; k < GBT_ILP; ++k) xv[k] = lds_f64(s_x + 8u * (uint32_t)f[k]);
+#pragma unroll
+            for (int k = 0; k < GBT_ILP; ++k)
+              idx[k] = 2u * idx[k] + (xv[k] <= th[k] ? 1u : 2u);
+          }
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) {
+            const int t = t0 + k * GBT2_GROUPS;
+            const double lv = lds_f64(s_leaf + 8u * ((uint32_t)t * NLF + idx[k] - (uint32_t)NI));
+            if (t < n_trees) contrib[rl * n_trees + t] = lv;
+          }
+        }
+      } else if (SMEM_NODES && max_depth <= GBT_WALK_MAX_DEPTH) {
+        // GBT_ILP trees walked side by side for a fixed max_depth levels
+        // (a walk that reached its leaf stays there): independent chains
+        // of dependent shared-memory loads instead of one at a time
+        const uint32_t s_nodes = tc::smem_u32(nodes), s_x = tc::smem_u32(x);
+        for (int t0 = g; t0 < n_trees; t0 += GBT_ILP * GBT2_GROUPS) {
+          uint32_t cur[GBT_ILP];   // node byte address
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) {
+            const int t = t0 + k * GBT2_GROUPS;
+            cur[k] = s_nodes + 16u * (uint32_t)s_first[t < n_trees ? t : t0];
+          }
+          uint32_t tb[GBT_ILP];
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) tb[k] = cur[k];
+          for (int lv = 0; lv < max_depth; ++lv) {
+            double v[GBT_ILP];
+            int f[GBT_ILP], l[GBT_ILP], r_[GBT_ILP];
+#pragma unroll
+            for (int k = 0; k < GBT_ILP; ++k) lds_node(cur[k], v[k], f[k], l[k], r_[k]);
+            double xv[GBT_ILP];
+#pragma unroll
+            for (int k = 0; k < GBT_ILP; ++k)
+              xv[k] = lds_f64(s_x + 8u * (uint32_t)(f[k] < 0 ? 0 : f[k]));
+#pragma unroll
+            for (int k = 0; k < GBT_ILP; ++k)
+              if (f[k] >= 0) cur[k] = tb[k] + 16u * (uint32_t)(xv[k] <= v[k] ? l[k] : r_[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) {
+            const int t = t0 + k * GBT2_GROUPS;
+            double v;
+            int f, l, r_;
+            lds_node(cur[k], v, f, l, r_);
+            if (t < n_trees) contrib[rl * n_trees + t] = v;
+          }
+        }
+      } else {
+        for (int t = g; t < n_trees; t += GBT2_GROUPS) {
+          const GbtNode* tree = nodes + s_first[t];
+          GbtNode nd = tree[0];
+          while (nd.feat >= 0) nd = tree[(x[nd.feat] <= nd.v) ? nd.left : nd.right];
+          contrib[rl * n_trees + t] = nd.v;
+        }
       }
     }
     __syncthreads();

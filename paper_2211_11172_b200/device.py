@@ -695,14 +695,17 @@ class DeviceForest:
     NODE = np.dtype([("v", "<f8"), ("feat", "<i2"), ("left", "<i2"),
                      ("right", "<i2"), ("pad", "<i2")])
     HDR = np.dtype([("n_trees", "<i4"), ("fitted", "<i4"), ("base", "<f8"),
-                    ("floor_value", "<f8"), ("n_nodes", "<i8")])
+                    ("floor_value", "<f8"), ("n_nodes", "<i8"),
+                    ("max_depth", "<i4"), ("perfect_depth", "<i4"),
+                    ("perfect", "<u8"), ("perfect_bytes", "<i8")])
+    PERFECT_MAX = 7       # gbt_kernels.cuh GBT_PERFECT_MAX
 
     def __init__(self, trees, base: float, learning_rate: float,
                  fitted: bool = True, floor_value: float = 1e-6,
                  device=None, node_capacity: int = 0, tree_capacity: int = 0):
         N.load()
         dev = _dev(device)
-        nodes, firsts = self._records(trees, learning_rate)
+        nodes, firsts, self._depth = self._records(trees, learning_rate)
         self.cap_nodes = max(len(nodes), int(node_capacity), 1)
         self.cap_trees = max(len(firsts), int(tree_capacity), 1)
         self.nodes = torch.zeros(self.cap_nodes * 16, dtype=torch.uint8,
@@ -711,6 +714,11 @@ class DeviceForest:
                                       device=dev)
         self.hdr = torch.zeros(self.HDR.itemsize, dtype=torch.uint8,
                                device=dev)
+        # perfect-tree image (forests of depth <= PERFECT_MAX), capacity-
+        # sized like the node records
+        self.perfect = torch.zeros(
+            self.perfect_bytes(self.cap_trees, self.PERFECT_MAX),
+            dtype=torch.uint8, device=dev)
         d = N.ForestDesc()
         d.n_trees = self.cap_trees
         d.n_nodes = self.cap_nodes
@@ -724,11 +732,13 @@ class DeviceForest:
     @classmethod
     def _records(cls, trees, learning_rate):
         """All trees' node records in one vectorised pass (the per-round
-        host cost of a refit reload)."""
+        host cost of a refit reload), and the forest's depth (internal
+        levels of its deepest tree), with which the kernels walk several
+        trees side by side for a fixed number of levels."""
         if len(trees) > 1024:
             raise DeviceError("more than 1024 trees")
         if not trees:
-            return np.zeros(0, cls.NODE), np.zeros(0, np.int32)
+            return np.zeros(0, cls.NODE), np.zeros(0, np.int32), 0
         sizes = np.fromiter((len(t[0]) for t in trees), np.int64, len(trees))
         if sizes.max() > 32767:
             raise DeviceError("tree too large for int16 node indices")
@@ -741,8 +751,8 @@ class DeviceForest:
         val = np.concatenate([np.asarray(t[4], np.float64) for t in trees])
         leaf = feat < 0
         off = np.repeat(firsts, sizes)
-        _check_depth_all(feat, np.where(leaf, 0, left) + off,
-                         np.where(leaf, 0, right) + off, firsts)
+        depth = _check_depth_all(feat, np.where(leaf, 0, left) + off,
+                                 np.where(leaf, 0, right) + off, firsts)
         rec = np.zeros(len(feat), dtype=cls.NODE)
         # leaves carry learning_rate * value: the reference's fp64
         # product (costmodel.py:224), formed here once
@@ -750,7 +760,51 @@ class DeviceForest:
         rec["feat"] = feat.astype(np.int16)
         rec["left"] = np.where(leaf, 0, left).astype(np.int16)
         rec["right"] = np.where(leaf, 0, right).astype(np.int16)
-        return rec, firsts.astype(np.int32)
+        return rec, firsts.astype(np.int32), depth
+
+    @staticmethod
+    def perfect_bytes(T: int, D: int) -> int:
+        """gbt_kernels.cuh gbt_perfect_bytes."""
+        leaf = (T * ((1 << D) - 1) * 8 + 15) & ~15
+        feat = leaf + T * (1 << D) * 8
+        return (feat + T * ((1 << D) - 1) * 2 + 15) & ~15
+
+    @classmethod
+    def perfect_image(cls, nodes, firsts, D: int) -> np.ndarray:
+        """The perfect-tree image of a forest of depth <= D (gbt_kernels.cuh):
+        breadth-first complete trees of D levels; a leaf above the last
+        level becomes pass-through slots (feature 0, threshold +inf) whose
+        subtree repeats its value.  Built level by level for all trees at
+        once."""
+        T = len(firsts)
+        NI, NL = (1 << D) - 1, 1 << D
+        feat = nodes["feat"].astype(np.int64)
+        v = nodes["v"]
+        sizes = np.diff(np.append(firsts, len(nodes))).astype(np.int64)
+        off = np.repeat(firsts.astype(np.int64), sizes)
+        left = nodes["left"].astype(np.int64) + off
+        right = nodes["right"].astype(np.int64) + off
+        thr_p = np.empty((T, NI), np.float64)
+        feat_p = np.empty((T, NI), np.int16)
+        cur = firsts.astype(np.int64)[:, None]
+        for d in range(D):
+            leaf = feat[cur] < 0
+            lo = (1 << d) - 1
+            thr_p[:, lo:lo + (1 << d)] = np.where(leaf, np.inf, v[cur])
+            feat_p[:, lo:lo + (1 << d)] = np.where(leaf, 0, feat[cur])
+            cur = np.stack([np.where(leaf, cur, left[cur]),
+                            np.where(leaf, cur, right[cur])],
+                           axis=-1).reshape(T, -1)
+        if not (feat[cur] < 0).all():
+            raise DeviceError("forest deeper than its perfect image")
+        leaf_p = v[cur]
+        out = np.zeros(cls.perfect_bytes(T, D), np.uint8)
+        b_leaf = (T * NI * 8 + 15) & ~15
+        out[:T * NI * 8] = thr_p.reshape(-1).view(np.uint8)
+        out[b_leaf:b_leaf + T * NL * 8] = leaf_p.reshape(-1).view(np.uint8)
+        b_feat = b_leaf + T * NL * 8
+        out[b_feat:b_feat + T * NI * 2] = feat_p.reshape(-1).view(np.uint8)
+        return out
 
     def _write(self, nodes, firsts, base, fitted, floor_value):
         self.n_nodes = len(nodes)
@@ -758,14 +812,24 @@ class DeviceForest:
         if len(nodes):
             self.nodes[:len(nodes) * 16].copy_(
                 torch.from_numpy(nodes.view(np.uint8).copy()))
+        depth = int(getattr(self, "_depth", 64))
+        pimg = None
+        if len(firsts) and 0 < depth <= self.PERFECT_MAX:
+            pimg = self.perfect_image(nodes, firsts, depth)
+            self.perfect[:len(pimg)].copy_(torch.from_numpy(pimg))
         if len(firsts):
             self.tree_first[:len(firsts)].copy_(torch.from_numpy(firsts))
         h = np.zeros(1, dtype=self.HDR)
         h["n_trees"], h["fitted"] = len(firsts), 1 if fitted else 0
         h["base"], h["floor_value"] = float(base), float(floor_value)
         h["n_nodes"] = len(nodes)
+        h["max_depth"] = depth
+        h["perfect_depth"] = depth if pimg is not None else 0
+        h["perfect"] = self.perfect.data_ptr()
+        h["perfect_bytes"] = len(pimg) if pimg is not None else 0
         self.hdr.copy_(torch.from_numpy(h.view(np.uint8).copy()))
-        PF.xfer("h2d", nodes.nbytes + firsts.nbytes + h.nbytes)
+        PF.xfer("h2d", nodes.nbytes + firsts.nbytes + h.nbytes +
+                (pimg.nbytes if pimg is not None else 0))
         # host mirrors (informational; the kernels read the header)
         self.desc.fitted = 1 if fitted else 0
         self.desc.base = float(base)
@@ -775,9 +839,10 @@ class DeviceForest:
              fitted: bool = True, floor_value: float = 1e-6) -> bool:
         """Load another ensemble in place; False if it exceeds the
         capacity (build a new forest then)."""
-        nodes, firsts = self._records(trees, learning_rate)
+        nodes, firsts, depth = self._records(trees, learning_rate)
         if len(nodes) > self.cap_nodes or len(firsts) > self.cap_trees:
             return False
+        self._depth = depth
         self._write(nodes, firsts, base, fitted, floor_value)
         return True
 
@@ -805,10 +870,10 @@ def _check_depth_all(feat, left_g, right_g, roots):
     deeper trees.  All trees at once: global child indices, one
     level-synchronous walk from every root."""
     frontier = np.asarray(roots, dtype=np.int64)
-    for _ in range(64):
+    for depth in range(64):
         inner = frontier[feat[frontier] >= 0]
         if inner.size == 0:
-            return
+            return depth
         frontier = np.concatenate([left_g[inner], right_g[inner]])
     raise DeviceError("tree deeper than the reference's 64-step walk")
 

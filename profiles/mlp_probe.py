@@ -5,8 +5,9 @@ of the tensor-core kernels at a chosen population.
 
 Builds the config's tables and a random-init agent (the bench's), a
 uniform population of ``rows`` states and its features, then launches
-``reps`` x (policy step [k_policy_tc + sampler + featurize] and V(X)/V(X')
-[k_value_tc]) -- the launch list ncu filters with -k.  Prints per-kernel
+``reps`` x (policy step [k_mlp_f16<policy> + sampler + featurize], V(X)/V(X')
+[k_mlp_f16<value>] and the warm-started GBT over X' [k_gbt_predict2]) --
+the launch list ncu filters with -k.  Prints per-kernel
 CUDA-event times (library timer) and the algorithmic TF/s of the MLPs."""
 
 import argparse
@@ -45,12 +46,18 @@ def main():
     v0 = torch.empty(n, dtype=torch.float32, device="cuda")
     v1 = torch.empty(n, dtype=torch.float32, device="cuda")
     out = None
+    trees, base = bench.device_warm_start(tb, w["sg"].flops,
+                                          np.random.default_rng(1),
+                                          torch.device("cuda"))
+    forest = D.DeviceForest(trees, base, 0.3)
+    score = torch.empty(n, dtype=torch.float64, device="cuda")
     if args.time:
         profiling.native_timing(True)
     for _ in range(args.reps):
         out = D.policy_step(dsk, dag, X, t, k, n, gen=gen, out=out,
                             feat_out=Xn)
         D.value_pair(dag, X, n, Xn, n, v0, v1)
+        D.gbt_predict(forest, Xn, n, out=score)
     torch.cuda.synchronize()
     D.raise_status(int(out["status"].item()) & ((1 << 64) - 1))
     if args.phases:

@@ -24,8 +24,9 @@ def _chain(depth):
 
 def test_records_offsets_and_leaf_products():
     trees = [_chain(3), _chain(1), _chain(5)]
-    rec, firsts = DeviceForest._records(trees, 0.3)
+    rec, firsts, depth = DeviceForest._records(trees, 0.3)
     assert firsts.tolist() == [0, 7, 10]
+    assert depth == 5          # internal levels of the deepest tree
     assert len(rec) == 7 + 3 + 11
     for (feat, thr, left, right, val), f in zip(trees, firsts):
         r = rec[f:f + len(feat)]
@@ -40,11 +41,68 @@ def test_records_offsets_and_leaf_products():
 
 
 def test_records_reject_walks_deeper_than_reference():
-    DeviceForest._records([_chain(63)], 0.3)
+    assert DeviceForest._records([_chain(63)], 0.3)[2] == 63
     with pytest.raises(DeviceError):
         DeviceForest._records([_chain(3), _chain(64)], 0.3)
 
 
 def test_records_empty():
-    rec, firsts = DeviceForest._records([], 0.3)
-    assert len(rec) == 0 and len(firsts) == 0
+    rec, firsts, depth = DeviceForest._records([], 0.3)
+    assert len(rec) == 0 and len(firsts) == 0 and depth == 0
+
+
+def _walk_records(rec, first, x):
+    i = first
+    while rec["feat"][i] >= 0:
+        f = rec["feat"][i]
+        i = first + (rec["left"][i] if x[f] <= rec["v"][i] else rec["right"][i])
+    return rec["v"][i]
+
+
+def _walk_perfect(img, T, D, t, x):
+    NI, NL = (1 << D) - 1, 1 << D
+    b_leaf = (T * NI * 8 + 15) & ~15
+    thr = img[:T * NI * 8].view(np.float64).reshape(T, NI)
+    leaf = img[b_leaf:b_leaf + T * NL * 8].view(np.float64).reshape(T, NL)
+    feat = img[b_leaf + T * NL * 8:b_leaf + T * NL * 8 + T * NI * 2] \
+        .view(np.int16).reshape(T, NI)
+    i = 0
+    for _ in range(D):
+        i = 2 * i + (1 if x[feat[t, i]] <= thr[t, i] else 2)
+    return leaf[t, i - NI]
+
+
+def test_perfect_image_walks_to_the_same_leaves():
+    """The perfect-tree image (the kernel's layout for forests of depth
+    <= 7) gives every row the leaf value of the node-record walk, also for
+    NaN features (which go right in both)."""
+    rng = np.random.default_rng(0)
+    trees = []
+    for _ in range(20):
+        feat, thr, left, right, val = [], [], [], [], []
+
+        def add(d):
+            i = len(feat)
+            feat.append(-1); thr.append(0.0); left.append(-1)
+            right.append(-1); val.append(0.0)
+            if d < 5 and rng.random() < 0.8:
+                feat[i] = int(rng.integers(0, 4))
+                thr[i] = float(rng.normal())
+                left[i] = add(d + 1)
+                right[i] = add(d + 1)
+            else:
+                val[i] = float(rng.normal())
+            return i
+        add(0)
+        trees.append(tuple(np.asarray(a) for a in (feat, thr, left, right,
+                                                   val)))
+    rec, firsts, depth = DeviceForest._records(trees, 0.3)
+    img = DeviceForest.perfect_image(rec, firsts, depth)
+    assert len(img) == DeviceForest.perfect_bytes(len(trees), depth)
+    X = rng.normal(size=(300, 4))
+    X[::7, 1] = np.nan
+    for x in X:
+        for t, f in enumerate(firsts):
+            a = _walk_records(rec, f, x)
+            b = _walk_perfect(img, len(trees), depth, t, x)
+            assert a.tobytes() == b.tobytes()

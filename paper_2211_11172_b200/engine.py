@@ -218,6 +218,42 @@ class EpisodeResult:
         return out
 
 
+# sharded PPO: "rows" (default; the minibatch rows all-reduced, the
+# single-device update on every rank) or "grads" (per-shard gradients
+# all-reduced)
+_SHARD_PPO = os.environ.get("HARL_SHARD_PPO", "rows")
+
+
+class _StagingRing:
+    """B replay rows in the ring layout the PPO kernels read (X, actions,
+    scalars, move/shift bits), all views of one byte buffer so a single
+    collective moves them."""
+
+    def __init__(self, cap: int, F: int, dev):
+        import torch
+        self.cap = cap
+        sizes = [("X", (cap, F), torch.float64),
+                 ("scalars", (cap, 4), torch.float64),
+                 ("move_bits", (cap,), torch.int64),
+                 ("actions", (cap, 4), torch.int32),
+                 ("shift_bits", (cap,), torch.int32)]
+        nbytes = [int(np.prod(sh)) * torch.empty(0, dtype=dt).element_size()
+                  for _, sh, dt in sizes]
+        self.buf = torch.zeros(sum((n + 15) // 16 * 16 for n in nbytes),
+                               dtype=torch.uint8, device=dev)
+        off = 0
+        for (name, sh, dt), n in zip(sizes, nbytes):
+            setattr(self, name, self.buf[off:off + n].view(dt).view(sh))
+            off += (n + 15) // 16 * 16
+        d = N.ReplayRing()
+        d.X = d.Xn = self.X.data_ptr()
+        d.actions, d.scalars = self.actions.data_ptr(), self.scalars.data_ptr()
+        d.move_bits = self.move_bits.data_ptr()
+        d.shift_bits = self.shift_bits.data_ptr()
+        d.cap = cap
+        self.desc = d
+
+
 class _Buffers:
     """Device buffers of one episode geometry (population, entry log, step
     scratch, per-step parameter tables).  Kept alive across episodes so the
@@ -634,6 +670,72 @@ class EpisodeEngine:
             dist.all_reduce(h, group=group)
             t.copy_(h)
 
+    def _sharded_ppo_rows(self, slots_t, where_t, B, losses):
+        """One PPO update of a sharded episode, identical bit for bit to the
+        single-device update (so an episode does not depend on the world
+        size): every rank writes the minibatch rows it owns (its ring slots
+        ``slots_t``) into their minibatch positions ``where_t`` of a zeroed
+        staging ring of B rows -- exactly one rank owns each row -- one
+        NCCL all-reduce (uint8 sum: x + 0 = x for every byte) gives every
+        rank the whole minibatch in minibatch order, and every rank runs
+        the single-device ppo_update on it.  The all-reduce carries the
+        B transitions' PPO inputs (B x (8F + 60) bytes, 115 KB at B = 256,
+        F = 49) instead of the fp64 gradients (1.2 MB); the update itself,
+        ~1.5 % of the step's flops at C2, is replicated."""
+        import torch
+        st = self._staging_ring(B)
+        st.buf.zero_()
+        ring = self.replay
+        sl = slots_t.long()
+        wh = where_t.long()
+        st.X[wh] = ring.X[sl]
+        st.actions[wh] = ring.actions[sl]
+        st.scalars[wh] = ring.scalars[sl]
+        st.move_bits[wh] = ring.move_bits[sl]
+        st.shift_bits[wh] = ring.shift_bits[sl]
+        self._allreduce_(st.buf)
+        if getattr(self, "_iota_B", None) is None or self._iota_B.numel() < B:
+            self._iota_B = torch.arange(B, dtype=torch.int32, device=self.dev)
+        self._ensure_ppo_scratch(B)
+        a = self.agent
+        self.dagent.ppo_update(st, self._iota_B[:B], self.rl_cfg, a.opt_pi.t,
+                               a.opt_v.t, scratch=self._ppo_scratch,
+                               losses=losses)
+
+    def _staging_ring(self, B):
+        st = getattr(self, "_stage", None)
+        if st is None or st.cap < B:
+            st = self._stage = _StagingRing(B, self.agent.feature_len,
+                                            self.dev)
+        return st
+
+    def _sharded_ppo_grads(self, slots_t, B, losses):
+        """The gradient variant (HARL_SHARD_PPO=grads): per-shard gradient
+        and loss partial sums over the owned rows (global 1/B), one
+        all-reduce of {gradients, loss sums}, the identical Adam on every
+        rank.  Rounded differently from the single-device sum."""
+        import torch
+        a = self.agent
+        self._ensure_ppo_scratch(max(int(slots_t.numel()), 1))
+        self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
+                               a.opt_pi.t, a.opt_v.t,
+                               scratch=self._ppo_scratch,
+                               losses=losses, B_norm=B, phase=1)
+        n_g = self.dagent.grads.numel()
+        buf = getattr(self, "_ar_buf", None)
+        if buf is None or buf.numel() != n_g + 4:
+            buf = self._ar_buf = torch.empty(n_g + 4, dtype=torch.float64,
+                                             device=self.dev)
+        buf[:n_g].copy_(self.dagent.grads.view(-1))
+        buf[n_g:].copy_(losses[5:9])
+        self._allreduce_(buf)
+        self.dagent.grads.view(-1).copy_(buf[:n_g])
+        losses[5:9].copy_(buf[n_g:])
+        self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
+                               a.opt_pi.t, a.opt_v.t,
+                               scratch=self._ppo_scratch,
+                               losses=losses, B_norm=B, phase=2)
+
     def _gather_advantages(self, b, local_ids, m_l, P):
         """Every rank's (track id, advantage) of the cull step: one
         all-gather of fixed-size tensors (ceil(P / G) rows per rank, track
@@ -743,43 +845,34 @@ class EpisodeEngine:
                 B = step["ppo"]
                 pos = gen.choice(len(self._gidx), size=B, replace=False)
                 owners, lpush = self._gidx.locate(pos)
-                slots = (lpush[owners == rank] % cap).astype(np.int32)
-                # pinned ring of slot lists (one per update of the episode):
-                # the copy stays asynchronous
+                mine = owners == rank
+                slots = (lpush[mine] % cap).astype(np.int32)
+                where = np.flatnonzero(mine).astype(np.int32)
+                # pinned ring of (slot, minibatch position) lists, one per
+                # update of the episode: the copies stay asynchronous
+                n_up = max(1, sum(1 for s_ in plan if s_["ppo"]))
                 sp = getattr(b, "slot_pin", None)
-                if sp is None or sp.shape[1] < B:
-                    sp = b.slot_pin = torch.empty(
-                        (max(1, sum(1 for s_ in plan if s_["ppo"])), B),
-                        dtype=torch.int32, pin_memory=True)
+                if sp is None or sp.shape[2] < B or sp.shape[1] < n_up:
+                    sp = b.slot_pin = torch.empty((2, n_up, B),
+                                                  dtype=torch.int32,
+                                                  pin_memory=True)
                     b.slot_dev = torch.empty_like(sp, device=dev)
-                sp[ppo_k, :len(slots)].numpy()[:] = slots
-                b.slot_dev[ppo_k, :len(slots)].copy_(sp[ppo_k, :len(slots)],
-                                                     non_blocking=True)
-                slots_t = b.slot_dev[ppo_k, :len(slots)]
+                k_ = len(slots)
+                sp[0, ppo_k, :k_].numpy()[:] = slots
+                sp[1, ppo_k, :k_].numpy()[:] = where
+                b.slot_dev[:, ppo_k, :k_].copy_(sp[:, ppo_k, :k_],
+                                                non_blocking=True)
+                slots_t = b.slot_dev[0, ppo_k, :k_]
                 a = self.agent
                 a.opt_pi.t += 1
                 a.opt_v.t += 1
-                self._ensure_ppo_scratch(max(len(slots), 1))
                 losses = b.losses[ppo_k]
-                self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
-                                       a.opt_pi.t, a.opt_v.t,
-                                       scratch=self._ppo_scratch,
-                                       losses=losses, B_norm=B, phase=1)
-                # one all-reduce: gradients and the loss partial sums
-                n_g = self.dagent.grads.numel()
-                buf = getattr(self, "_ar_buf", None)
-                if buf is None or buf.numel() != n_g + 4:
-                    buf = self._ar_buf = torch.empty(
-                        n_g + 4, dtype=torch.float64, device=dev)
-                buf[:n_g].copy_(self.dagent.grads.view(-1))
-                buf[n_g:].copy_(losses[5:9])
-                self._allreduce_(buf)
-                self.dagent.grads.view(-1).copy_(buf[:n_g])
-                losses[5:9].copy_(buf[n_g:])
-                self.dagent.ppo_update(self.replay, slots_t, self.rl_cfg,
-                                       a.opt_pi.t, a.opt_v.t,
-                                       scratch=self._ppo_scratch,
-                                       losses=losses, B_norm=B, phase=2)
+                if _SHARD_PPO == "grads":
+                    self._sharded_ppo_grads(slots_t, B, losses)
+                else:
+                    self._sharded_ppo_rows(slots_t,
+                                           b.slot_dev[1, ppo_k, :k_], B,
+                                           losses)
                 train.append((step["t"], losses, B))
                 ppo_k += 1
         st = b.status.cpu().numpy().view(np.uint64)

@@ -5,7 +5,9 @@ Track ``i`` of the episode's population lives on rank ``i % G``
 balanced; a contiguous split would put every replay row -- and hence every
 PPO minibatch -- on the last rank at P >= 4096, rlcore.py:253-265).
 Parameters and trees are replicated; the only data-path collective is one
-sum-all-reduce of the PPO gradient (+ loss partial sums) per update.
+all-reduce per PPO update: of the minibatch rows (default, every rank then
+runs the single-device update -- bit-identical at any world size) or of the
+per-shard gradient and loss partial sums (HARL_SHARD_PPO=grads).
 
 Everything here is host arithmetic that keeps a sharded episode *the same
 episode* as the single-device one:

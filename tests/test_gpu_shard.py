@@ -1,7 +1,8 @@
 """Population-sharded episodes on the device (world size 2, both ranks on
 cuda:0, gloo for the collectives -- the single-box stand-in for NCCL):
 the merged shards reproduce the single-device episode (same generator
-stream, uniforms at global rows, merged culls, summed PPO gradients)."""
+stream, uniforms at global rows, merged culls, the minibatch rows
+all-reduced so every rank runs the single-device PPO update)."""
 
 import os
 import socket
@@ -64,11 +65,19 @@ def _worker(rank, world, port, hidden, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("hidden", [(32, 32), (128, 128)])
-def test_sharded_engine_matches_single_device(hidden):
+@pytest.mark.parametrize("hidden,mode", [((32, 32), "rows"),
+                                         ((128, 128), "rows"),
+                                         ((128, 128), "grads")])
+def test_sharded_engine_matches_single_device(hidden, mode, monkeypatch):
+    """mode "rows" (default): the minibatch rows all-reduced and the
+    single-device update run on every rank -- the merged shards equal the
+    single-device episode bit for bit, parameters included.  mode "grads"
+    (HARL_SHARD_PPO=grads): per-shard gradient sums all-reduced -- equal up
+    to the first update, then within fp64 rounding."""
     import torch.multiprocessing as mp
     from paper_2211_11172_b200 import device as D
     from paper_2211_11172_b200.engine import EpisodeEngine
+    monkeypatch.setenv("HARL_SHARD_PPO", mode)   # inherited by the ranks
     tb, rl, agent, trees, cfg = _setup(hidden)
     forest = D.DeviceForest(trees, 0.5, 0.3)
     eng = EpisodeEngine(agent, rl, tb.levels, use_graphs=False)
@@ -95,11 +104,17 @@ def test_sharded_engine_matches_single_device(hidden):
         merged.update(got[1][0][ep])
         assert merged.keys() == ref[ep].keys()
         diff = [k for k in ref[ep] if merged[k] != ref[ep][k]]
-        # PPO gradients are summed per shard (different rounding), so a
-        # near-boundary draw may flip after the first update; none before
-        assert len(diff) <= len(ref[ep]) // 200, len(diff)
+        if mode == "rows":
+            assert not diff, len(diff)
+        else:
+            # per-shard gradient sums round differently: a near-boundary
+            # draw may flip after the first update; none before
+            assert len(diff) <= len(ref[ep]) // 200, len(diff)
     assert got[0][2] == got[1][2] == gen.bit_generator.state["state"]["state"]
-    for a, b in zip(got[0][1], agent.policy):
-        np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-9)
     for a, b in zip(got[0][1], got[1][1]):
         np.testing.assert_array_equal(a, b)
+    for a, b in zip(got[0][1], agent.policy):
+        if mode == "rows":
+            np.testing.assert_array_equal(a, b)
+        else:
+            np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-9)

@@ -500,6 +500,16 @@ int harl_brute_force(const harl_sketch_desc* sk, const harl_sim_desc* sim,
                      unsigned long long* out, unsigned long long* scratch,
                      int64_t scratch_len, void* stream);
 
+/* Host-side: ScheduleState.canonical (schedspace.py:117-120) of n states
+ * (tiles [n][slots] u16, `levels` factors per tiled dim; knobs [n][3] u8):
+ * "<prefix>|t=a.b;c.d|ca=..|par=..|ur=.." per state, each NUL-terminated,
+ * into out.  Returns the bytes written, or -(bytes needed) if cap is too
+ * small.  The drop-in's CandidateEntry texts (tuner.py:406-412). */
+long long harl_format_canonical(const uint16_t* tiles, const uint8_t* knobs,
+                                long long n, int slots, int levels,
+                                const char* prefix, long long prefix_len,
+                                char* out, long long cap);
+
 /* Host-side: harl_gbt_fit's heap-layout trees (host copies) -> the
  * reference's node numbering (_fit_tree, costmodel.py:86-141), K slots per
  * tree in and out; sizes[t] = nodes of tree t.  0 on success. */
@@ -508,6 +518,28 @@ int harl_heap_to_creation_order(const int32_t* feat_h, const double* thr_h,
                                 int64_t* feature, double* threshold,
                                 int64_t* left, int64_t* right, double* value,
                                 int32_t* sizes);
+
+/* Host-side: a GBT ensemble (the reference's _Tree arrays per tree,
+ * costmodel.py:59-78: int64 feature/left/right, f64 threshold/value,
+ * concatenated over the trees, sizes[t] nodes each, child indices local to
+ * their tree) -> the device layouts DeviceForest uploads: 16-byte node
+ * records (inner: the threshold; leaf: learning_rate * value,
+ * costmodel.py:224) into nodes_out,
+ * each tree's first record into firsts_out and, when the forest depth is in
+ * [1, perfect_max], the perfect-tree image (gbt_kernels.cuh) into
+ * perfect_out (*perfect_bytes_out its size, 0 if none).  Returns the depth
+ * (inner levels of the deepest tree) or -1 (deeper than the reference's
+ * 64-step walk), -2 (empty tree / child index outside its tree), -3 (more
+ * than 1024 trees or a tree beyond int16 indices), -4 (perfect_cap too
+ * small).  Replaces the per-round numpy packing of the forest reload. */
+long long harl_forest_pack(int n_trees, const int64_t* sizes,
+                           const int64_t* feature, const double* threshold,
+                           const int64_t* left, const int64_t* right,
+                           const double* value, double learning_rate,
+                           void* nodes_out, int32_t* firsts_out,
+                           int perfect_max, void* perfect_out,
+                           long long perfect_cap,
+                           long long* perfect_bytes_out);
 
 /* Instrumentation (no reference counterpart; the reference has no device).
  * harl_launch_count: kernels this library has launched since load (graph

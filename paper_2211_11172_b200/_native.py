@@ -170,6 +170,12 @@ _SIGS = {
                                           vp, vp, vp]),
     "harl_format_floats": (C.c_longlong, [vp, C.c_longlong, vp, C.c_longlong,
                                           i32]),
+    "harl_format_canonical": (C.c_longlong, [vp, vp, C.c_longlong, i32, i32,
+                                              C.c_char_p, C.c_longlong, vp,
+                                              C.c_longlong]),
+    "harl_forest_pack": (C.c_longlong, [i32, vp, vp, vp, vp, vp, vp, f64, vp,
+                                         vp, i32, vp, C.c_longlong,
+                                         P(C.c_longlong)]),
     "harl_cull_select": (i32, [vp, vp, i64, vp, i64, i64, vp, vp, P(i64)]),
     "harl_gbt_fit_scratch_bytes": (i64, [i32, i32, i32]),
     "harl_gbt_fit": (i32, [vp, vp, i32, i32, i32, i32, f64, i32, vp, i64, vp,

@@ -359,11 +359,14 @@ def b200_session_class(base):
                     sc = self._b200_rank_scratch = D.RankScratch()
                 order, tiles, knobs, feats, _, _ = res.top_entries(
                     k_hat, ex, sc)
-            states = tables.states_from_arrays(tiles, knobs, ScheduleState)
-            return [CandidateEntry(canonical=s.canonical(),
-                                   features=feats[i], state=s,
-                                   order=base + int(order[i]))
-                    for i, s in enumerate(states)]
+            # canonical texts formatted as ScheduleState.canonical does
+            # (schedspace.py:117-120), from the same Python ints
+            states, texts = tables.states_from_arrays(
+                tiles, knobs, ScheduleState, canonical=True)
+            return [CandidateEntry(canonical=c, features=f, state=s, order=o)
+                    for s, c, f, o in zip(states, texts, feats,
+                                          (base + np.asarray(order, np.int64))
+                                          .tolist())]
 
         def _b200_log(self, res, rnd):
             import json

@@ -206,4 +206,50 @@ int harl_heap_to_creation_order(const int32_t* feat_h, const double* thr_h,
   return 0;
 }
 
+// ScheduleState.canonical (schedspace.py:117-120) of n states (tiles
+// [n][slots] u16 with `levels` factors per tiled dim, knobs [n][3] u8):
+// "<prefix>|t=a.b.c;d.e.f|ca=..|par=..|ur=.." per state, each followed by
+// a NUL.  Returns the bytes written, or -(bytes needed) if cap is too small.
+long long harl_format_canonical(const uint16_t* tiles, const uint8_t* knobs,
+                                long long n, int slots, int levels,
+                                const char* prefix, long long prefix_len,
+                                char* out, long long cap) {
+  if (n < 0 || slots < 0 || (slots && levels <= 0)) return 0;
+  const long long per = prefix_len + 3 + 6LL * slots + 3 * (5 + 4 + 4) + 1;
+  if (per * n > cap) return -(per * n);
+  char* p = out;
+  auto num = [&](unsigned v) {
+    char b[8];
+    int k = 0;
+    do {
+      b[k++] = (char)('0' + v % 10);
+      v /= 10;
+    } while (v);
+    while (k) *p++ = b[--k];
+  };
+  for (long long i = 0; i < n; ++i) {
+    memcpy(p, prefix, (size_t)prefix_len);
+    p += prefix_len;
+    memcpy(p, "|t=", 3);
+    p += 3;
+    const uint16_t* t = tiles + i * slots;
+    for (int s = 0; s < slots; ++s) {
+      if (s) *p++ = (s % levels) ? '.' : ';';
+      num(t[s]);
+    }
+    const uint8_t* k = knobs + i * 3;
+    memcpy(p, "|ca=", 4);
+    p += 4;
+    num(k[0]);
+    memcpy(p, "|par=", 5);
+    p += 5;
+    num(k[1]);
+    memcpy(p, "|ur=", 4);
+    p += 4;
+    num(k[2]);
+    *p++ = '\0';
+  }
+  return (long long)(p - out);
+}
+
 }  // extern "C"

@@ -705,9 +705,9 @@ class DeviceForest:
                  device=None, node_capacity: int = 0, tree_capacity: int = 0):
         N.load()
         dev = _dev(device)
-        nodes, firsts, self._depth = self._records(trees, learning_rate)
-        self.cap_nodes = max(len(nodes), int(node_capacity), 1)
-        self.cap_trees = max(len(firsts), int(tree_capacity), 1)
+        cols = self._columns(trees)
+        self.cap_nodes = max(int(cols[0].sum()), int(node_capacity), 1)
+        self.cap_trees = max(len(trees), int(tree_capacity), 1)
         self.nodes = torch.zeros(self.cap_nodes * 16, dtype=torch.uint8,
                                  device=dev)
         self.tree_first = torch.zeros(self.cap_trees, dtype=torch.int32,
@@ -727,7 +727,72 @@ class DeviceForest:
         d.dev_hdr = self.hdr.data_ptr()
         self.desc = d
         self.device = dev
-        self._write(nodes, firsts, base, fitted, floor_value)
+        # pinned staging of everything _write uploads (node records, perfect
+        # image, tree firsts, header), written by harl_forest_pack in place
+        pb = self.perfect_bytes(self.cap_trees, self.PERFECT_MAX)
+        a16 = lambda n: (n + 15) // 16 * 16  # noqa: E731
+        self._o_img = a16(self.cap_nodes * 16)
+        self._o_first = self._o_img + a16(pb)
+        self._o_hdr = self._o_first + a16(self.cap_trees * 4)
+        self._stage = torch.empty(self._o_hdr + a16(self.HDR.itemsize),
+                                  dtype=torch.uint8, pin_memory=True)
+        self._stage_np = self._stage.numpy()
+        self._stage_done = None
+        self._write(cols, learning_rate, base, fitted, floor_value)
+
+    @staticmethod
+    def _columns(trees):
+        """(sizes i64, feature i64, threshold f64, left i64, right i64,
+        value f64): the trees' arrays concatenated (harl_forest_pack's
+        input)."""
+        if len(trees) > 1024:
+            raise DeviceError("more than 1024 trees")
+        if not trees:
+            z = np.zeros(0, np.int64)
+            return (z, z, z.astype(np.float64), z, z, z.astype(np.float64))
+        sizes = np.fromiter((len(t[0]) for t in trees), np.int64, len(trees))
+        cat = [np.concatenate([t[j] for t in trees]).astype(dt, copy=False)
+               for j, dt in ((0, np.int64), (1, np.float64), (2, np.int64),
+                             (3, np.int64), (4, np.float64))]
+        return (sizes, *(np.ascontiguousarray(c) for c in cat))
+
+    @classmethod
+    def _native_pack(cls, cols, learning_rate, nodes_out, firsts_out,
+                     img_out):
+        """harl_forest_pack of ``cols`` into the given host arrays ->
+        (depth, perfect-image bytes written)."""
+        lib = N.load(require_device=False)
+        pbytes = C.c_longlong(0)
+        ptr = lambda a: a.ctypes.data  # noqa: E731
+        depth = int(lib.harl_forest_pack(
+            len(cols[0]), ptr(cols[0]), ptr(cols[1]), ptr(cols[2]),
+            ptr(cols[3]), ptr(cols[4]), ptr(cols[5]), float(learning_rate),
+            ptr(nodes_out), ptr(firsts_out), cls.PERFECT_MAX, ptr(img_out),
+            img_out.nbytes, C.byref(pbytes)))
+        if depth < 0:
+            raise DeviceError({
+                -1: "tree deeper than the reference's 64-step walk",
+                -2: "empty tree or child index outside its tree",
+                -3: "tree too large for int16 node indices",
+                -4: "perfect-tree image beyond its capacity"}.get(
+                    depth, f"harl_forest_pack failed ({depth})"))
+        return depth, int(pbytes.value)
+
+    @classmethod
+    def pack_host(cls, trees, learning_rate):
+        """The native packing on its own (host arrays, no device): (node
+        records, firsts, depth, perfect image or None) -- what ``_records``
+        and ``perfect_image`` restate in numpy."""
+        cols = cls._columns(trees)
+        nodes = np.zeros(int(cols[0].sum()), cls.NODE)
+        firsts = np.zeros(len(cols[0]), np.int32)
+        img = np.zeros(cls.perfect_bytes(len(cols[0]), cls.PERFECT_MAX),
+                       np.uint8)
+        depth, pb = cls._native_pack(cols, learning_rate, nodes.view(np.uint8)
+                                     if len(nodes) else np.zeros(16, np.uint8),
+                                     firsts if len(firsts)
+                                     else np.zeros(1, np.int32), img)
+        return nodes, firsts, depth, (img[:pb] if pb else None)
 
     @classmethod
     def _records(cls, trees, learning_rate):
@@ -806,30 +871,46 @@ class DeviceForest:
         out[b_feat:b_feat + T * NI * 2] = feat_p.reshape(-1).view(np.uint8)
         return out
 
-    def _write(self, nodes, firsts, base, fitted, floor_value):
-        self.n_nodes = len(nodes)
-        self.n_trees = len(firsts)
-        if len(nodes):
-            self.nodes[:len(nodes) * 16].copy_(
-                torch.from_numpy(nodes.view(np.uint8).copy()))
-        depth = int(getattr(self, "_depth", 64))
-        pimg = None
-        if len(firsts) and 0 < depth <= self.PERFECT_MAX:
-            pimg = self.perfect_image(nodes, firsts, depth)
-            self.perfect[:len(pimg)].copy_(torch.from_numpy(pimg))
-        if len(firsts):
-            self.tree_first[:len(firsts)].copy_(torch.from_numpy(firsts))
-        h = np.zeros(1, dtype=self.HDR)
-        h["n_trees"], h["fitted"] = len(firsts), 1 if fitted else 0
+    def _write(self, cols, learning_rate, base, fitted, floor_value):
+        """Pack ``cols`` (``_columns``) with harl_forest_pack straight into
+        the pinned staging buffer and upload it (async copies on the
+        current stream; the next write waits for them)."""
+        lib = N.load()
+        sizes = cols[0]
+        T, n_nodes = len(sizes), int(sizes.sum())
+        if self._stage_done is not None:
+            self._stage_done.synchronize()
+        st = self._stage_np
+        depth, pb = self._native_pack(
+            cols, learning_rate, st,
+            st[self._o_first:self._o_first + 4 * T].view(np.int32),
+            st[self._o_img:self._o_first])
+        self._depth = depth
+        self.n_nodes, self.n_trees = n_nodes, T
+        h = st[self._o_hdr:self._o_hdr + self.HDR.itemsize].view(self.HDR)
+        h["n_trees"], h["fitted"] = T, 1 if fitted else 0
         h["base"], h["floor_value"] = float(base), float(floor_value)
-        h["n_nodes"] = len(nodes)
+        h["n_nodes"] = n_nodes
         h["max_depth"] = depth
-        h["perfect_depth"] = depth if pimg is not None else 0
+        h["perfect_depth"] = depth if pb else 0
         h["perfect"] = self.perfect.data_ptr()
-        h["perfect_bytes"] = len(pimg) if pimg is not None else 0
-        self.hdr.copy_(torch.from_numpy(h.view(np.uint8).copy()))
-        PF.xfer("h2d", nodes.nbytes + firsts.nbytes + h.nbytes +
-                (pimg.nbytes if pimg is not None else 0))
+        h["perfect_bytes"] = pb
+        stg = self._stage
+        if n_nodes:
+            self.nodes[:n_nodes * 16].copy_(stg[:n_nodes * 16],
+                                            non_blocking=True)
+        if pb:
+            self.perfect[:pb].copy_(stg[self._o_img:self._o_img + pb],
+                                    non_blocking=True)
+        if T:
+            self.tree_first[:T].copy_(
+                stg[self._o_first:self._o_first + 4 * T].view(torch.int32),
+                non_blocking=True)
+        self.hdr.copy_(stg[self._o_hdr:self._o_hdr + self.HDR.itemsize],
+                       non_blocking=True)
+        self._stage_done = torch.cuda.Event()
+        self._stage_done.record()
+        PF.xfer("h2d", n_nodes * 16 + 4 * T + self.HDR.itemsize + pb)
         # host mirrors (informational; the kernels read the header)
         self.desc.fitted = 1 if fitted else 0
         self.desc.base = float(base)
@@ -839,11 +920,10 @@ class DeviceForest:
              fitted: bool = True, floor_value: float = 1e-6) -> bool:
         """Load another ensemble in place; False if it exceeds the
         capacity (build a new forest then)."""
-        nodes, firsts, depth = self._records(trees, learning_rate)
-        if len(nodes) > self.cap_nodes or len(firsts) > self.cap_trees:
+        cols = self._columns(trees)
+        if int(cols[0].sum()) > self.cap_nodes or len(trees) > self.cap_trees:
             return False
-        self._depth = depth
-        self._write(nodes, firsts, base, fitted, floor_value)
+        self._write(cols, learning_rate, base, fitted, floor_value)
         return True
 
     @staticmethod
@@ -919,6 +999,7 @@ class DeviceAgent:
             raise DeviceError("network shape beyond the device kernels' limits")
         self.cols = head_columns(S, levels)
         self.C0 = len(self.cols)
+        self._hw0 = np.zeros((hidden[-1], self.C0))
         self.NH = self.C0 + 9
         self.hidden, self.F, self.S = hidden, F, S
         nt = len(hidden)
@@ -972,9 +1053,16 @@ class DeviceAgent:
             r += vdims[l + 1]
         self.row_stride = r
         self.pol_layout, self.val_layout = pl, vl
-        self.params = torch.zeros(self.n_params, dtype=torch.float64, device=dev)
-        self.m = torch.zeros_like(self.params)
-        self.v = torch.zeros_like(self.params)
+        # parameters and both Adam moments in one [3][n] block (one copy
+        # each way per episode), staged through one pinned host block
+        self.pmv = torch.zeros((3, self.n_params), dtype=torch.float64,
+                               device=dev)
+        self.params, self.m, self.v = self.pmv[0], self.pmv[1], self.pmv[2]
+        self._pin = torch.empty((3, self.n_params), dtype=torch.float64,
+                                pin_memory=True)
+        self._pin_np = self._pin.numpy()
+        self._pin_done = None
+        self._pin_views = [self._views(self._pin_np[i]) for i in range(3)]
         self.grads = torch.zeros_like(self.params)
         self.params32 = torch.zeros(self.n_params, dtype=torch.float32,
                                     device=dev)
@@ -1017,60 +1105,80 @@ class DeviceAgent:
 
     # -- host <-> device --------------------------------------------------
 
-    def _pack(self, pol_list, val_list) -> np.ndarray:
-        out = np.zeros(self.n_params, dtype=np.float64)
+    def _views(self, flat: np.ndarray):
+        """1-D views of a flat parameter vector in the numpy lists' order:
+        (policy trunk W/b..., the compact head's [H][NH] and [NH] blocks,
+        value W/b...)."""
         pl, vl = self.pol_layout, self.val_layout
         nt = len(self.hidden)
+        dims = [self.F, *self.hidden]
+        trunk = []
         for l in range(nt):
-            W, b = pol_list[2 * l], pol_list[2 * l + 1]
-            out[pl.off_W[l]:pl.off_W[l] + W.size] = W.reshape(-1)
-            out[pl.off_b[l]:pl.off_b[l] + b.size] = b
-        heads = pol_list[2 * nt:]
-        H = self.hidden[-1]
-        hW = np.zeros((H, self.NH))
-        hb = np.zeros(self.NH)
-        hW[:, :self.C0] = heads[0][:, self.cols]
-        hb[:self.C0] = heads[1][self.cols]
-        for h in range(3):
-            hW[:, self.C0 + 3 * h:self.C0 + 3 * h + 3] = heads[2 + 2 * h]
-            hb[self.C0 + 3 * h:self.C0 + 3 * h + 3] = heads[3 + 2 * h]
-        out[pl.off_hW:pl.off_hW + hW.size] = hW.reshape(-1)
-        out[pl.off_hb:pl.off_hb + self.NH] = hb
-        for l in range(vl.n_layers):
-            W, b = val_list[2 * l], val_list[2 * l + 1]
-            out[vl.off_W[l]:vl.off_W[l] + W.size] = W.reshape(-1)
-            out[vl.off_b[l]:vl.off_b[l] + b.size] = b
-        return out
-
-    def _unpack_into(self, flat: np.ndarray, pol_list, val_list):
-        pl, vl = self.pol_layout, self.val_layout
-        nt = len(self.hidden)
-        for l in range(nt):
-            W, b = pol_list[2 * l], pol_list[2 * l + 1]
-            W[...] = flat[pl.off_W[l]:pl.off_W[l] + W.size].reshape(W.shape)
-            b[...] = flat[pl.off_b[l]:pl.off_b[l] + b.size]
+            n = dims[l] * dims[l + 1]
+            trunk.append(flat[pl.off_W[l]:pl.off_W[l] + n])
+            trunk.append(flat[pl.off_b[l]:pl.off_b[l] + dims[l + 1]])
         H = self.hidden[-1]
         hW = flat[pl.off_hW:pl.off_hW + H * self.NH].reshape(H, self.NH)
         hb = flat[pl.off_hb:pl.off_hb + self.NH]
-        heads = pol_list[2 * nt:]
-        heads[0][:, self.cols] = hW[:, :self.C0]
-        heads[1][self.cols] = hb[:self.C0]
-        for h in range(3):
-            heads[2 + 2 * h][...] = hW[:, self.C0 + 3 * h:self.C0 + 3 * h + 3]
-            heads[3 + 2 * h][...] = hb[self.C0 + 3 * h:self.C0 + 3 * h + 3]
+        vdims = [self.F, *self.hidden, 1]
+        val = []
         for l in range(vl.n_layers):
-            W, b = val_list[2 * l], val_list[2 * l + 1]
-            W[...] = flat[vl.off_W[l]:vl.off_W[l] + W.size].reshape(W.shape)
-            b[...] = flat[vl.off_b[l]:vl.off_b[l] + b.size]
+            n = vdims[l] * vdims[l + 1]
+            val.append(flat[vl.off_W[l]:vl.off_W[l] + n])
+            val.append(flat[vl.off_b[l]:vl.off_b[l] + vdims[l + 1]])
+        return trunk, hW, hb, val
+
+    def _pack(self, pol_list, val_list, out=None, views=None) -> np.ndarray:
+        """The numpy lists -> the flat layout (every element written)."""
+        if out is None:
+            out = np.zeros(self.n_params, dtype=np.float64)
+        trunk, hW, hb, val = views if views is not None else self._views(out)
+        nt2 = len(trunk)
+        for dst, src in zip(trunk, pol_list):
+            np.copyto(dst, src.reshape(-1))
+        heads = pol_list[nt2:]
+        C0 = self.C0
+        np.take(heads[0], self.cols, axis=1, out=self._hw0)
+        hW[:, :C0] = self._hw0
+        hb[:C0] = heads[1][self.cols]
+        for h in range(3):
+            hW[:, C0 + 3 * h:C0 + 3 * h + 3] = heads[2 + 2 * h]
+            hb[C0 + 3 * h:C0 + 3 * h + 3] = heads[3 + 2 * h]
+        for dst, src in zip(val, val_list):
+            np.copyto(dst, src.reshape(-1))
+        return out
+
+    def _unpack_into(self, flat: np.ndarray, pol_list, val_list, views=None):
+        trunk, hW, hb, val = views if views is not None else self._views(flat)
+        nt2 = len(trunk)
+        for src, dst in zip(trunk, pol_list):
+            np.copyto(dst, src.reshape(dst.shape))
+        heads = pol_list[nt2:]
+        C0 = self.C0
+        heads[0][:, self.cols] = hW[:, :C0]
+        heads[1][self.cols] = hb[:C0]
+        for h in range(3):
+            np.copyto(heads[2 + 2 * h], hW[:, C0 + 3 * h:C0 + 3 * h + 3])
+            np.copyto(heads[3 + 2 * h], hb[C0 + 3 * h:C0 + 3 * h + 3])
+        for src, dst in zip(val, val_list):
+            np.copyto(dst, src.reshape(dst.shape))
 
     def upload(self):
+        """The numpy parameters and moments -> the device: packed into the
+        pinned block, one async copy, then the derived copies (fp32
+        rollout parameters, transposes, weight images) on the device."""
         a = self.agent
-        p = torch.from_numpy(self._pack(a.policy, a.value)).to(self.device)
-        self.params.copy_(p)
-        self.params32.copy_(p.float())
-        self.m.copy_(torch.from_numpy(self._pack(a.opt_pi.m, a.opt_v.m)))
-        self.v.copy_(torch.from_numpy(self._pack(a.opt_pi.v, a.opt_v.v)))
-        PF.xfer("h2d", self.params, self.m, self.v)
+        if self._pin_done is not None:      # the last copy out of _pin
+            self._pin_done.synchronize()
+        pin, vw = self._pin_np, self._pin_views
+        self._pack(a.policy, a.value, pin[0], vw[0])
+        self._pack(a.opt_pi.m, a.opt_v.m, pin[1], vw[1])
+        self._pack(a.opt_pi.v, a.opt_v.v, pin[2], vw[2])
+        self.pmv.copy_(self._pin, non_blocking=True)
+        self._pin_done = torch.cuda.Event()
+        self._pin_done.record()
+        self.params32.copy_(self.params)
+        PF.xfer("h2d", self.pmv)
         self.refresh_derived()
 
     def refresh_derived(self):
@@ -1089,10 +1197,16 @@ class DeviceAgent:
     def download(self):
         """Write device params and moments back into the numpy lists."""
         a = self.agent
-        self._unpack_into(self.params.cpu().numpy(), a.policy, a.value)
-        self._unpack_into(self.m.cpu().numpy(), a.opt_pi.m, a.opt_v.m)
-        self._unpack_into(self.v.cpu().numpy(), a.opt_pi.v, a.opt_v.v)
-        PF.xfer("d2h", self.params, self.m, self.v)
+        if self._pin_done is not None:
+            self._pin_done.synchronize()
+        self._pin.copy_(self.pmv, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self._pin_done = None
+        pin, vw = self._pin_np, self._pin_views
+        self._unpack_into(pin[0], a.policy, a.value, vw[0])
+        self._unpack_into(pin[1], a.opt_pi.m, a.opt_v.m, vw[1])
+        self._unpack_into(pin[2], a.opt_pi.v, a.opt_v.v, vw[2])
+        PF.xfer("d2h", self.pmv)
 
     def _build_descs(self):
         base = self.params32.data_ptr()

@@ -115,6 +115,28 @@ def canonical_text(sketch_id, tiles, ca, par, ur) -> str:
     return f"{sketch_id}|t={t}|ca={ca}|par={par}|ur={ur}"
 
 
+def canonical_texts(sketch_id, tiles, knobs, levels: int) -> list:
+    """``canonical_text`` of every row of (tiles [n, slots] u16, knobs
+    [n, 3] u8), formatted natively (harl_format_canonical)."""
+    import ctypes as C
+    from . import _native as N
+    t = np.ascontiguousarray(tiles, dtype=np.uint16)
+    k = np.ascontiguousarray(knobs, dtype=np.uint8)
+    n = len(k)
+    if n == 0:
+        return []
+    t = t.reshape(n, -1)
+    pre = sketch_id.encode()
+    cap = n * (len(pre) + 6 * t.shape[1] + 64)
+    buf = C.create_string_buffer(cap)
+    nb = N.load(require_device=False).harl_format_canonical(
+        t.ctypes.data, k.ctypes.data, n, t.shape[1], levels, pre, len(pre),
+        buf, cap)
+    if nb < 0:
+        raise ValueError("canonical text buffer too small")
+    return buf.raw[:nb].decode().split("\0")[:-1]
+
+
 @dataclass(frozen=True)
 class ModificationAction:
     tile_src: int = -1
@@ -312,17 +334,22 @@ class SketchTables:
                         s.unroll_index)
         return tiles, knobs
 
-    def states_from_arrays(self, tiles, knobs, state_cls=ScheduleState):
-        L = self.levels
+    def states_from_arrays(self, tiles, knobs, state_cls=ScheduleState,
+                           canonical: bool = False):
+        """(tiles [B, slots], knobs [B, 3]) -> ``state_cls`` objects (and,
+        with ``canonical``, their canonical texts as a second list)."""
+        L, sk = self.levels, self.sketch_id
         out = []
-        for t, k in zip(np.asarray(tiles), np.asarray(knobs)):
-            tl = tuple(tuple(int(v) for v in t[d * L:(d + 1) * L])
-                       for d in range(self.ndims))
-            out.append(state_cls(sketch_id=self.sketch_id, tiles=tl,
-                                 compute_at_index=int(k[0]),
-                                 parallel_fuse_count=int(k[1]),
-                                 unroll_index=int(k[2])))
-        return out
+        for t, k in zip(np.asarray(tiles).tolist(), np.asarray(knobs).tolist()):
+            it = iter(t)
+            tl = tuple(zip(*([it] * L))) if L else ()
+            out.append(state_cls(sketch_id=sk, tiles=tl,
+                                 compute_at_index=k[0],
+                                 parallel_fuse_count=k[1],
+                                 unroll_index=k[2]))
+        if canonical:
+            texts = canonical_texts(sk, tiles, knobs, L)
+        return (out, texts) if canonical else out
 
     def arrays_from_canonical(self, texts) -> tuple:
         """Canonical strings of this sketch (``sk|t=a.b;..|ca=|par=|ur=``,

@@ -106,3 +106,77 @@ def test_perfect_image_walks_to_the_same_leaves():
             a = _walk_records(rec, f, x)
             b = _walk_perfect(img, len(trees), depth, t, x)
             assert a.tobytes() == b.tobytes()
+
+
+def _random_forest(rng, n_trees, max_d, n_feat=4):
+    trees = []
+    for _ in range(n_trees):
+        feat, thr, left, right, val = [], [], [], [], []
+
+        def add(d):
+            i = len(feat)
+            feat.append(-1); thr.append(0.0); left.append(-1)
+            right.append(-1); val.append(0.0)
+            if d < max_d and rng.random() < 0.8:
+                feat[i] = int(rng.integers(0, n_feat))
+                thr[i] = float(rng.normal())
+                left[i] = add(d + 1)
+                right[i] = add(d + 1)
+            else:
+                val[i] = float(rng.normal())
+            return i
+        add(0)
+        trees.append(tuple(np.asarray(a) for a in (feat, thr, left, right,
+                                                   val)))
+    return trees
+
+
+def _golden_trees():
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "gbt_fit_large.npz")
+    d = np.load(p)
+    n = len({k[:7] for k in d.files if k.startswith("tree")})
+    return [tuple(d[f"tree{t:03d}_{c}"] for c in
+                  ("feature", "threshold", "left", "right", "value"))
+            for t in range(n)]
+
+
+@pytest.mark.parametrize("case", ["golden", "d3", "d6", "d7", "d9", "one"])
+def test_native_pack_matches_the_restatement(case):
+    """harl_forest_pack (the drop-in's per-episode forest reload) writes
+    the numpy restatement's node records, firsts, depth and perfect-tree
+    image byte for byte."""
+    rng = np.random.default_rng(sum(map(ord, case)))
+    trees = {"golden": _golden_trees,
+             "d3": lambda: _random_forest(rng, 50, 3),
+             "d6": lambda: _random_forest(rng, 50, 6),
+             "d7": lambda: _random_forest(rng, 64, 7),
+             "d9": lambda: _random_forest(rng, 30, 9),
+             "one": lambda: _random_forest(rng, 1, 0)}[case]()
+    rec, firsts, depth = DeviceForest._records(trees, 0.3)
+    nrec, nfirsts, ndepth, img = DeviceForest.pack_host(trees, 0.3)
+    assert ndepth == depth
+    assert nrec.tobytes() == rec.tobytes()
+    assert nfirsts.tolist() == firsts.tolist()
+    if 0 < depth <= DeviceForest.PERFECT_MAX:
+        ref = DeviceForest.perfect_image(rec, firsts, depth)
+        assert img is not None and img.tobytes() == ref.tobytes()
+    else:
+        assert img is None
+
+
+def test_native_pack_errors():
+    assert DeviceForest.pack_host([_chain(63)], 0.3)[2] == 63
+    with pytest.raises(DeviceError):
+        DeviceForest.pack_host([_chain(3), _chain(64)], 0.3)
+    nodes, firsts, depth, img = DeviceForest.pack_host([], 0.3)
+    assert len(nodes) == 0 and depth == 0 and img is None
+    bad = list(_chain(2))
+    bad[2] = bad[2].copy()
+    bad[2][0] = 99                      # child outside the tree
+    with pytest.raises(DeviceError):
+        DeviceForest.pack_host([tuple(bad)], 0.3)
+    z = np.zeros(0, np.int64)
+    with pytest.raises(DeviceError):
+        DeviceForest.pack_host([(z, z.astype(float), z, z, z.astype(float))],
+                               0.3)

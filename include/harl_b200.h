@@ -235,7 +235,12 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
  * fused kernel (policy -> sample/apply -> featurize per 128-row tile, the
  * logits never leave the SM); otherwise a separate featurize launch.  Not
  * a fallback: returns HARL_E_ARG if the shape is not eligible (the caller
- * then uses harl_policy_step). */
+ * then uses harl_policy_step).  flags: HARL_STEP_FUSED (the one fused
+ * 3xTF32 kernel), HARL_WEIGHTS_SETTLED (no launch since the one before the
+ * previous launch on the stream wrote the weight images: with HARL_PDL=1 the
+ * kernel may load them before its programmatic-dependency wait). */
+#define HARL_STEP_FUSED 1
+#define HARL_WEIGHTS_SETTLED 2
 int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         const double* feat, const uint16_t* tiles,
                         const uint8_t* knobs, int64_t n, int64_t ld,
@@ -247,14 +252,14 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
                         const int32_t* grow, int64_t m_total, double* feat_out,
-                        int32_t fuse_tc, void* stream);
+                        int32_t flags, void* stream);
 
 /* V(X) and V(X') in one launch (tuner.py:395-396) on the tcgen05 path
  * (hidden (128,128), feature_len <= 64); HARL_E_ARG if not eligible. */
 int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
                        int64_t n0, const double* feat1, int64_t n1,
                        int32_t feature_len, float* v0, float* v1,
-                       const void* packed, void* stream);
+                       const void* packed, int32_t flags, void* stream);
 
 /* Pre-pack the tcgen05 weight images (tf32 hi/lo in the UMMA K-major
  * layout + biases) after every parameter change; the tcgen05 entry points

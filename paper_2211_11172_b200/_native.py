@@ -147,7 +147,7 @@ _SIGS = {
                                   vp, vp, vp, vp, vp, vp, vp, vp, i64, vp,
                                   i32, vp]),
     "harl_value_pair_tc": (i32, [P(MlpDesc), vp, i64, vp, i64, i32, vp, vp,
-                                 vp, vp]),
+                                 vp, i32, vp]),
     "harl_tc_packed_bytes": (i64, [i32, i32]),
     "harl_pack_tc_weights": (i32, [P(MlpDesc), P(MlpDesc), i32, vp, vp, vp,
                                    vp]),

@@ -13,15 +13,33 @@ namespace harl {
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 
-// Programmatic dependent launch (sm_90+): every kernel waits for its
-// predecessor grid (completion + memory visibility) before touching global
-// memory, then lets its own dependents launch; without the launch
-// attribute both are no-ops.
+// Programmatic dependent launch (sm_90+; HARL_PDL=1 sets the launch
+// attribute, without it all of these are no-ops).  Every kernel waits for
+// its predecessor grid (completion + memory visibility) with griddep_wait()
+// before it reads anything the predecessor may have written or writes
+// anything the predecessor may read.  The step kernels let their dependents
+// launch late, with griddep_trigger() once a CTA's main work is done (an
+// early trigger lets waiting dependent CTAs take residency the primary's
+// later CTAs need).  Since every trigger comes after its kernel's own
+// griddep_wait, a kernel that starts has everything before its predecessor
+// complete: its pre-wait prologue may read data written two launches back
+// or earlier (weight images, forest, tables).  HARL_PDL_EARLY=1 restores
+// the trigger at kernel start (griddep_launch) for A/B.
+#ifndef HARL_PDL_EARLY
+#define HARL_PDL_EARLY 0
+#endif
 __device__ __forceinline__ void griddep_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 __device__ __forceinline__ void griddep_launch() {
+#if HARL_PDL_EARLY
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void griddep_trigger() {
+#if !HARL_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 // Launch accounting and the optional per-kernel timer (harl_profile_*).

@@ -175,8 +175,8 @@ struct GbtFinishArgs {
 
 struct GbtFinishEpilogue {
   const GbtFinishArgs& f;
-  int64_t wpos;
   __device__ void operator()(int64_t r0, int rows, int g, int rl) const {
+    const int64_t wpos = f.wpos_dev ? *f.wpos_dev : f.a.wpos;
     if (g == 1) {
       if (rl < rows) finish_row(f.a, f.io, f.ring, f.log, f.ts, wpos, r0 + rl);
       return;
@@ -209,9 +209,9 @@ k_gbt_finish(const GbtNode* __restrict__ gnodes,
              double* score, const double* old_score, double* reward,
              const GbtHdr* hdr, int32_t t_cap,
              const __grid_constant__ GbtFinishArgs fa) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
-  const GbtFinishEpilogue epi{fa, fa.wpos_dev ? *fa.wpos_dev : fa.a.wpos};
+  // (gbt2_body waits for the predecessor after its forest prologue; the
+  // epilogue reads the write position after that)
+  const GbtFinishEpilogue epi{fa};
   gbt2_body<SMEM_NODES>(gnodes, tree_first, n_trees, n_nodes, fitted, base,
                         floor_value, feat, n, F, score, old_score, reward, hdr,
                         t_cap, epi);

@@ -211,6 +211,7 @@ __device__ __forceinline__ void gbt2_body(
   off += gbt2_align((size_t)GBT2_ROWS * F * 8);
   double* contrib = (double*)(gsm + off);
   const int64_t n_tiles = (n + GBT2_ROWS - 1) / GBT2_ROWS;
+  // the forest (written by host copies only) streams in before the PDL wait
   if (threadIdx.x == 0) {
     tc::mbar_init(&fbar, 1);
     tc::mbar_init(&xbar[0], 1);
@@ -219,6 +220,9 @@ __device__ __forceinline__ void gbt2_body(
       tc::bulk_load(sn, perfect, (uint32_t)perfect_bytes, &fbar);
     else if (SMEM_NODES && n_nodes > 0) tc::bulk_load(sn, gnodes, (uint32_t)n_nodes * 16, &fbar);
     else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&fbar)) : "memory");
+  }
+  griddep_wait();  // PDL: the feature rows come from the predecessor
+  if (threadIdx.x == 0) {
     if (blockIdx.x < n_tiles) {
       const int64_t r0 = (int64_t)blockIdx.x * GBT2_ROWS;
       tc::bulk_f64(xsb0, feat + r0 * F,
@@ -364,6 +368,7 @@ __device__ __forceinline__ void gbt2_body(
     if (it < 2) dbg_ts(27 + 3 * it);
     epi(r0, rows, g, rl);
   }
+  griddep_trigger();
 }
 
 template <bool SMEM_NODES>
@@ -374,8 +379,7 @@ k_gbt_predict2(const GbtNode* __restrict__ gnodes,
                double floor_value, const double* __restrict__ feat, int64_t n,
                int32_t F, double* score, const double* old_score,
                double* reward, const GbtHdr* hdr, int32_t t_cap) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
+  // (gbt2_body waits for the predecessor after its forest prologue)
   gbt2_body<SMEM_NODES>(gnodes, tree_first, n_trees, n_nodes, fitted, base,
                         floor_value, feat, n, F, score, old_score, reward, hdr,
                         t_cap, GbtNoEpilogue());

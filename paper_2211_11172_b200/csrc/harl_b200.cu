@@ -853,7 +853,8 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
                         const int32_t* grow, int64_t m_total, double* feat_out,
-                        int32_t fuse_tc, void* stream) {
+                        int32_t flags, void* stream) {
+  const int32_t fuse_tc = flags & HARL_STEP_FUSED;
   int rc = check_sketch(sk);
   if (rc) return rc;
   if ((rc = check_mlp(pol, true))) return rc;
@@ -887,6 +888,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     fa.logits = hid_scratch;
     fa.logits_out = logits_out;
     fa.img = (const uint8_t*)packed_trunk + TRUNK_IMAGE;
+    fa.early_w = (flags & HARL_WEIGHTS_SETTLED) ? 1 : 0;
     HARL_PROF_BEGIN(st);
     launch_k(k_mlp_f16<true>, dim3(tc16_grid((n + 127) / 128)), dim3(F16_THREADS),
              smem, st, fa);
@@ -1030,7 +1032,7 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
 int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
                        int64_t n0, const double* feat1, int64_t n1,
                        int32_t feature_len, float* v0, float* v1,
-                       const void* packed, void* stream) {
+                       const void* packed, int32_t flags, void* stream) {
   int rc = check_mlp(val, false);
   if (rc) return rc;
   if (val->n_layers != 3 || !tc_trunk_ok(val, feature_len) ||
@@ -1058,6 +1060,7 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
     fa.out1 = v1;
     fa.b3 = val->b[2];
     fa.img = (const uint8_t*)packed + TRUNK_IMAGE;
+    fa.early_w = (flags & HARL_WEIGHTS_SETTLED) ? 1 : 0;
     const int64_t tiles_n = (n0 + 127) / 128 + (fa.n1 + 127) / 128;
     HARL_PROF_BEGIN((cudaStream_t)stream);
     launch_k(k_mlp_f16<false>, dim3(tc16_grid(tiles_n)), dim3(F16_THREADS), smem,
@@ -2115,7 +2118,8 @@ int harl_gbt_fit(const double* X, const double* y, int32_t n,
 // TrackSet.cull (stopping.py:68-86) on the host: the n_elim live tracks
 // with the lowest (advantage, -index) go, for finite advantages (the
 // engine routes a step with a NaN advantage to shard.eliminated, which runs
-// the reference's own comparison sort; here NaN keys would order last).  rows: the cull step's m rows (row r = track
+// the reference's own comparison sort; here NaN keys would order last; -0.0
+// ties with +0.0 as in Python's comparisons).  rows: the cull step's m rows (row r = track
 // tracks[r], advantage adv[r]); alive (per track, 0/1) is updated; gone_out
 // gets the eliminated track ids ascending, keep_out the surviving rows
 // ascending (the survivor gather's index list).
@@ -2133,42 +2137,77 @@ int harl_cull_select(const double* adv, const int32_t* tracks, int64_t m,
       return HARL_E_ARG;
     }
   if (n_elim > 0) {
-    // ordered 64-bit keys (NaN last), the cut = the n_elim-th smallest key;
-    // everything below goes, ties at the cut go by descending track index
-    std::vector<uint64_t> key(m), tmp(m);
+    // ordered 64-bit keys (NaN last); the cut = the n_elim-th smallest key,
+    // found by an MSB radix select (11-bit digits, each pass over the rows
+    // still in the cut's bucket); everything below goes, ties at the cut go
+    // by descending track index
+    static thread_local std::vector<uint64_t> key, cand;
+    key.resize((size_t)m);
+    cand.resize((size_t)m);
     const uint64_t* bits = reinterpret_cast<const uint64_t*>(adv);
     for (int64_t r = 0; r < m; ++r) {
-      const uint64_t b = bits[r];
+      uint64_t b = bits[r];
+      if (b == 0x8000000000000000ull) b = 0;   // -0.0 ties with +0.0
       const bool nan = (b & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
-      const uint64_t k = nan ? ~0ull : ((b >> 63) ? ~b : (b | 0x8000000000000000ull));
-      key[r] = k;
-      tmp[r] = k;
+      key[r] = nan ? ~0ull : ((b >> 63) ? ~b : (b | 0x8000000000000000ull));
     }
-    std::nth_element(tmp.begin(), tmp.begin() + (n_elim - 1), tmp.end());
-    const uint64_t cut = tmp[n_elim - 1];
-    std::vector<int32_t> tied;
+    uint64_t rank = (uint64_t)(n_elim - 1), prefix = 0;
+    const uint64_t* src = key.data();
+    int64_t n = m;
+    uint32_t hist[2048];
+    static const int kShift[6] = {53, 42, 31, 20, 9, 0};   // 5 x 11 + 9 bits
+    for (int pass = 0; pass < 6; ++pass) {
+      const int shift = kShift[pass], width = pass < 5 ? 11 : 9;
+      const uint64_t dmask = (1ull << width) - 1;
+      memset(hist, 0, sizeof(uint32_t) << width);
+      for (int64_t i = 0; i < n; ++i) ++hist[(src[i] >> shift) & dmask];
+      uint64_t d = 0, below = 0;
+      while (below + hist[d] <= rank) below += hist[d++];
+      rank -= below;
+      prefix |= d << shift;
+      // keep the bucket's keys
+      int64_t c = 0;
+      for (int64_t i = 0; i < n; ++i)
+        if (((src[i] >> shift) & dmask) == d) cand[c++] = src[i];
+      src = cand.data();
+      n = c;
+      if (n == 1) {
+        prefix = cand[0];
+        break;
+      }
+    }
+    const uint64_t cut = prefix;
+    static thread_local std::vector<int32_t> tied;
+    tied.clear();
+    // branch-free passes (the keep/go outcome is a coin flip per row)
     int64_t below = 0;
     for (int64_t r = 0; r < m; ++r) {
-      if (key[r] < cut) {
-        alive[tracks[r]] = 2;   // marked: eliminated
-        ++below;
-      } else if (key[r] == cut) {
-        tied.push_back(tracks[r]);
-      }
+      const int lt = key[r] < cut;
+      uint8_t& a = alive[tracks[r]];
+      a = (uint8_t)(a << lt);   // live (1) -> 2: marked eliminated
+      below += lt;
     }
+    for (int64_t r = 0; r < m; ++r)
+      if (key[r] == cut) tied.push_back(tracks[r]);
     const int64_t need = n_elim - below;
-    std::sort(tied.begin(), tied.end(), [](int32_t a, int32_t b) { return a > b; });
+    // the `need` highest track indices among the ties (a set: no full sort)
+    if (need > 0 && need < (int64_t)tied.size())
+      std::nth_element(tied.begin(), tied.begin() + (need - 1), tied.end(),
+                       [](int32_t a, int32_t b) { return a > b; });
     for (int64_t i = 0; i < need; ++i) alive[tied[i]] = 2;
-    int64_t g = 0;
-    for (int64_t t = 0; t < n_tracks; ++t)
-      if (alive[t] == 2) {
-        gone_out[g++] = t;
-        alive[t] = 0;
-      }
+    int64_t g = 0, sink;
+    for (int64_t t = 0; t < n_tracks; ++t) {
+      const uint8_t a = alive[t];
+      *(g < n_elim ? &gone_out[g] : &sink) = t;
+      g += a == 2;
+      alive[t] = (uint8_t)(a & 1);
+    }
   }
   int64_t k = 0;
-  for (int64_t r = 0; r < m; ++r)
-    if (alive[tracks[r]]) keep_out[k++] = (int32_t)r;
+  for (int64_t r = 0; r < m; ++r) {
+    keep_out[k] = (int32_t)r;
+    k += alive[tracks[r]] != 0;
+  }
   *n_keep = k;
   return HARL_OK;
 }

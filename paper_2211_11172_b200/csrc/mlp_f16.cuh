@@ -157,6 +157,8 @@ struct F16Args {
   float* out1;          // value: v [n1]
   const float* b3;      // value: [1] device
   const uint8_t* img;   // f16 image (k_pack16)
+  int32_t early_w;      // the image was not written by the previous launch:
+                        // load it before the PDL wait
 };
 
 // warp roles: 16 epilogue warps (TMEM lane quarter w % 4, column group
@@ -212,8 +214,6 @@ __device__ __forceinline__ void f16_stage_x(const double* xs, int rows, int F,
 // has been converted.
 template <bool POLICY>
 __global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
   extern __shared__ __align__(1024) uint8_t smf[];
   const float* fl = (const float*)smf;
   const int img_bytes = POLICY ? f16_image_bytes(a.NHP) : f16_off_wh();
@@ -250,6 +250,16 @@ __global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
   }
   tc_sync();
   const uint32_t tm = tbase;
+  const bool mma_thread = mine > 0 && warp == F16_EPI_WARPS && lane == 0;
+  auto load_weights = [&]() {
+    tc::bulk_load(smf, a.img, (uint32_t)f16_off_w2(), &wbar[0]);
+    tc::bulk_load(smf + f16_off_w2(), a.img + f16_off_w2(), 2 * F16_W2, &wbar[1]);
+    if (POLICY)
+      tc::bulk_load(smf + f16_off_wh(), a.img + f16_off_wh(),
+                    (uint32_t)(2 * a.NHP * TC_H * 2), &wbar[2]);
+  };
+  if (mma_thread && a.early_w) load_weights();
+  griddep_wait();  // PDL: the feature rows (and unsettled weights) are ready
   auto tile_of = [&](int64_t j, const double*& f, int64_t& r0, int& rows,
                      bool& second) {
     const int64_t t = blockIdx.x + j * gridDim.x;
@@ -375,13 +385,9 @@ __global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
       g_dbg_ts[35] = n_evt;
       g_dbg_ts[38] = clock64() - c_start;
     }
-  } else if (mine > 0 && warp == F16_EPI_WARPS && lane == 0) {
+  } else if (mma_thread) {
     // ---------------- MMA / copy issuing thread --------------------------
-    tc::bulk_load(smf, a.img, (uint32_t)f16_off_w2(), &wbar[0]);
-    tc::bulk_load(smf + f16_off_w2(), a.img + f16_off_w2(), 2 * F16_W2, &wbar[1]);
-    if (POLICY)
-      tc::bulk_load(smf + f16_off_wh(), a.img + f16_off_wh(),
-                    (uint32_t)(2 * a.NHP * TC_H * 2), &wbar[2]);
+    if (!a.early_w) load_weights();
     auto copy_x = [&](int64_t jt) {       // tile jt -> buffer jt % NXB
       if (jt >= mine) return;
       const double* f;
@@ -449,6 +455,7 @@ __global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
       g_dbg_ts[37] = c_iss;
     }
   }
+  griddep_trigger();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tm, 512);
 }

@@ -379,6 +379,7 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
     const int q = i / sw, c = seg0 + i % sw;
     out[q * RS + c] = base[q * RS + c];
   }
+  griddep_trigger();
   dbg_ts(48);
 }
 
@@ -640,6 +641,7 @@ k_ppo_rows_tc(const __grid_constant__ PpoArgs a,
     const int q = i / sw, c = seg0 + i % sw;
     out[q * RS + c] = base[q * RS + c];
   }
+  griddep_trigger();
   dbg_ts(48);
 }
 
@@ -834,6 +836,7 @@ k_ppo_wgrad(const __grid_constant__ GradJobs jt, int B, int RS,
   griddep_launch();
   wgrad_body(jt, B, RS, rows, grads, bad, check_finite, rowout, losses,
              means_B, w_ent, w_val);
+  griddep_trigger();
 }
 
 // (d) Adam over [0, n_pi) with the policy optimizer and [n_pi, n) with the
@@ -975,6 +978,7 @@ __global__ void k_ppo_adam(const __grid_constant__ AdamArgs a,
   if (*bad) return;
   dbg_ts(51);
   adam_body(a, adam_dev, grads, params, m, v, params32);
+  griddep_trigger();
 }
 
 // Grid-wide barrier for a cooperative launch (all CTAs co-resident):

@@ -572,6 +572,7 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
     for (int i = threadIdx.x; i < rows * F; i += blockDim.x) out[i] = s_feat[i];
     dbg_ts(31);
   }
+  griddep_trigger();
   dbg_grid(true, 60);
 }
 

@@ -328,6 +328,7 @@ k_featurize2(const __grid_constant__ harl_sketch_desc sk,
   dbg_ts(32);
   extern __shared__ __align__(16) unsigned char fsm[];
   featurize_tile(sk, tiles, knobs, n, ld, (int64_t)blockIdx.x * FEAT2_ROWS, feat, fsm);
+  griddep_trigger();
   dbg_ts(35);
 }
 

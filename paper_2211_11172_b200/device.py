@@ -1299,14 +1299,17 @@ class DeviceAgent:
 def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 n: int, gen=None, inject=None, out=None, want_logits=False,
                 rng_dev=None, advance=True, grow=None, m_total: int = 0,
-                feat_out=None, fuse_tc: bool = False, reset_status=True):
+                feat_out=None, fuse_tc: bool = False, reset_status=True,
+                settled: bool = False):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
     ``feat_out`` (optional f64 [n][F]): also featurize the new states (in
     the sampler kernel on the tcgen05 path; ``fuse_tc``: in the one fused
     policy->sample->featurize kernel instead).  ``reset_status=False``: the
     caller already set ``out["status"]`` to -1 (the engine fills its
-    per-step status table once per episode, not once per step).  Returns a dict of device tensors;
+    per-step status table once per episode, not once per step).
+    ``settled``: the weight images were not written by the previous launch
+    (see ``value_pair``).  Returns a dict of device tensors;
     ``status`` must be checked by the caller (``raise_status``)."""
     lib = N.load()
     dev = dsk.device
@@ -1347,7 +1350,9 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
             N.check(lib.harl_policy_step_tc(
                 *args, _ptr(agent.hid_scratch(n)), _ptr(rng_dev),
                 _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _ptr(grow),
-                m_total, _ptr(feat_out), 1 if fuse_tc else 0, _stream()),
+                m_total, _ptr(feat_out),
+                (STEP_FUSED if fuse_tc else 0) |
+                (WEIGHTS_SETTLED if settled else 0), _stream()),
                 "harl_policy_step_tc")
         if feat_out is not None and not fuse_tc and n > SAMPLE_FEAT_MAX_ROWS:
             # the library featurized with k_featurize2 inside the call: its
@@ -1378,10 +1383,16 @@ def value_estimate(agent: DeviceAgent, feat, n: int, out=None):
     return out[:n]
 
 
+# harl_policy_step_tc / harl_value_pair_tc flags (include/harl_b200.h)
+STEP_FUSED, WEIGHTS_SETTLED = 1, 2
+
+
 def value_pair(agent: DeviceAgent, feat0, n0: int, feat1, n1: int,
-               out0, out1):
+               out0, out1, settled: bool = False):
     """V(X) and V(X') (tuner.py:395-396); one tcgen05 launch for the
-    production shape, otherwise two FFMA launches."""
+    production shape, otherwise two FFMA launches.  ``settled``: the
+    weight images were not written by the previous launch (the kernel may
+    prefetch them ahead of its PDL wait)."""
     lib = N.load()
     if agent.tc:
         with PF.span("value_tc", n0 + n1):
@@ -1389,6 +1400,7 @@ def value_pair(agent: DeviceAgent, feat0, n0: int, feat1, n1: int,
                                            _ptr(feat0), n0, _ptr(feat1), n1,
                                            feat0.shape[1], _ptr(out0),
                                            _ptr(out1), _ptr(agent.packed["vt"]),
+                                           WEIGHTS_SETTLED if settled else 0,
                                            _stream()),
                     "harl_value_pair_tc")
         return out0[:n0], out1[:n1]

@@ -51,10 +51,10 @@ _FUSED_STEP = os.environ.get("HARL_FUSED_STEP") == "1"
 # of inside the sampler kernel (A/B and parity cross-check)
 _SPLIT_FEATURIZE = os.environ.get("HARL_SPLIT_FEATURIZE") == "1"
 
-# HARL_NATIVE_CULL=1: the cull decision through harl_cull_select (C++
-# nth_element) instead of numpy's partition -- measured slower on the GPU
-# box's host (0.50 vs 0.41 ms between segments at 16 K tracks), kept for A/B
-_PY_CULL = os.environ.get("HARL_NATIVE_CULL") != "1"
+# the graphed episode's cull decision: harl_cull_select (C++ radix select,
+# branch-free marking) by default; HARL_NATIVE_CULL=0 uses numpy's
+# partition (_cull_rows) instead, kept for A/B (the same decision)
+_PY_CULL = os.environ.get("HARL_NATIVE_CULL") == "0"
 
 # HARL_SPLIT_FINISH=1: separate GBT and finish launches (k_gbt_predict2 +
 # k_finish_step) instead of the fused k_gbt_finish (A/B and fallback path)
@@ -392,7 +392,9 @@ class EpisodeEngine:
                             advance=not graph_mode, grow=grow,
                             m_total=m_total,
                             feat_out=None if _SPLIT_FEATURIZE else nxt["feat"],
-                            fuse_tc=_FUSED_STEP, reset_status=False)
+                            fuse_tc=_FUSED_STEP, reset_status=False,
+                            settled=k > 0 and not b.plan[k - 1]["ppo"] and
+                            not b.plan[k - 1]["cull"])
         if _SPLIT_FEATURIZE:
             D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         # value pass first: the fused GBT kernel's finish epilogue needs
@@ -408,8 +410,10 @@ class EpisodeEngine:
                 D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
                              nxt["feat"], m, v_cur, v_next)
         else:
+            # (the sampler or featurize launch precedes it: the weight
+            # images were last written by an earlier Adam step)
             D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
-                         nxt["feat"], m, v_cur, v_next)
+                         nxt["feat"], m, v_cur, v_next, settled=True)
         po = b.pol_out
         io = N.StepBuffers(
             rt.data_ptr(), nxt["tiles"].data_ptr(), nxt["knobs"].data_ptr(),
@@ -501,8 +505,13 @@ class EpisodeEngine:
         eliminated track set (parity replays only)."""
         if self.shard is not None:
             return self._run_sharded(tables, forest, gen, cfg, order_counter)
+        trace = _HOST_TRACE
+        if trace is not None:
+            trace.append(("episode", 0, 0, time.perf_counter()))
         plan = schedule(cfg, len(self.replay), self.rl_cfg)
         b = self._buffers(tables, cfg, forest, plan)
+        if trace is not None:
+            trace.append(("buffers", 0, 0, time.perf_counter()))
         # graphs for the production (tcgen05) path; the FFMA kernels used
         # by small test networks take their RNG state by value
         # a plan's first episode runs eagerly: capturing costs more than the
@@ -518,6 +527,8 @@ class EpisodeEngine:
         cur, nxt = b.pop[0], b.pop[1]
         rt, rt_spare = b.rt[0], b.rt[1]
         D.init_population(b.dsk, P, gen, cur["tiles"], cur["knobs"])
+        if trace is not None:
+            trace.append(("init", 0, 0, time.perf_counter()))
         if getattr(b, "iota", None) is None:
             b.iota = torch.arange(P, dtype=torch.int32, device=self.dev)
         if eager:
@@ -1169,7 +1180,12 @@ class EpisodeEngine:
         pt[:m].copy_(b.rt[rt_i][:m], non_blocking=True)
         pa[:m].copy_(b.adv[:m], non_blocking=True)
         PF.xfer("d2h", pt[:m], pa[:m])
+        trace = _HOST_TRACE
+        if trace is not None:
+            trace.append(("cull_wait", 0, 0, time.perf_counter()))
         torch.cuda.current_stream().synchronize()
+        if trace is not None:
+            trace.append(("cull_synced", 0, 0, time.perf_counter()))
         if np.isnan(pa[:m].numpy()).any():   # the reference's sort (_cull)
             tracks = pt[:m].numpy().astype(np.int64)
             gone, keep = self._cull_rows(tracks, pa[:m].numpy().copy(),
@@ -1187,9 +1203,13 @@ class EpisodeEngine:
             pa.data_ptr(), pt.data_ptr(), m, a8.ctypes.data, len(alive),
             n_elim, gone.ctypes.data, b.keep_pin.data_ptr(), C.byref(nk)),
             "harl_cull_select")
+        if trace is not None:
+            trace.append(("cull_selected", 0, 0, time.perf_counter()))
         alive[:] = a8[:len(alive)].astype(bool)
         b.keep[:nk.value].copy_(b.keep_pin[:nk.value], non_blocking=True)
         PF.xfer("h2d", b.keep[:nk.value])
+        if trace is not None:
+            trace.append(("cull_done", 0, 0, time.perf_counter()))
         return gone
 
     def _cull_inputs(self, b, rt_i, m):

@@ -47,6 +47,7 @@ def main():
     wrap(eng, "_cull", "cull host")
     wrap(torch.cuda.CUDAGraph, "replay", "graph replay calls")
     E._HOST_TRACE = trace = []
+    torch.cuda.synchronize()
     t = time.perf_counter()
     eng.run_episode(tb, forest, gen, cfg, 0)
     torch.cuda.synchronize()

@@ -83,3 +83,41 @@ def test_row_cull_matches_track_cull():
         g2, k2 = E._cull_rows(tracks, adv, a2, cfg)
         assert g1.tolist() == g2.tolist() and np.array_equal(a1, a2)
         assert k2.tolist() == np.flatnonzero(a1[tracks]).tolist()
+
+
+@pytest.mark.parametrize("m", [16384, 65536])
+def test_cull_select_full_size_matches_row_cull(m):
+    """At bench sizes, the radix-select path makes _cull_rows' decision,
+    also with -0.0/+0.0 ties (equal in Python's comparisons), all-equal
+    advantages and coarse ties."""
+    from types import SimpleNamespace
+    from paper_2211_11172_b200.engine import EpisodeEngine
+    E = EpisodeEngine.__new__(EpisodeEngine)
+    lib = N.load(require_device=False)
+    rng = np.random.default_rng(m)
+    for case in range(4):
+        adv = rng.normal(size=m)
+        if case == 1:
+            adv = np.round(adv * 3) / 3
+        elif case == 2:
+            adv[:] = -0.0
+            adv[::3] = 0.0
+        elif case == 3:
+            adv[:] = 1.25
+        n_tracks = m + 11
+        tracks = rng.permutation(n_tracks)[:m].astype(np.int32)
+        alive = np.zeros(n_tracks, bool)
+        alive[tracks] = True
+        cfg = SimpleNamespace(cull_fraction=0.5, min_tracks=m // 2)
+        ne = m // 2
+        a8 = alive.astype(np.uint8)
+        gone = np.zeros(ne, np.int64)
+        keep = np.zeros(m, np.int32)
+        nk = C.c_int64(0)
+        assert lib.harl_cull_select(
+            adv.ctypes.data, tracks.ctypes.data, m, a8.ctypes.data, n_tracks,
+            ne, gone.ctypes.data, keep.ctypes.data, C.byref(nk)) == 0
+        g, k = E._cull_rows(tracks.astype(np.int64), adv, alive, cfg)
+        assert gone.tolist() == g.tolist()
+        assert keep[:nk.value].tolist() == k.tolist()
+        assert np.array_equal(a8.astype(bool), alive)

@@ -19,6 +19,7 @@
 #include "space_kernels.cuh"
 #include "episode_kernels.cuh"
 #include "ppo_kernels.cuh"
+#include "ppo_cluster.cuh"
 #include "tc_probe.cuh"
 #include "mlp_tc.cuh"
 #include "sample_kernels.cuh"
@@ -256,6 +257,27 @@ static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 // HARL_PPO_TC=1: the DMMA PPO rows kernel (8 rows per CTA) instead of the
 // SIMT one (2 rows per CTA, split reductions) -- measured slower at C2
 // (41 vs 29 us: 32 CTAs per chain and dependent 32-step MMA chains)
+// HARL_PPO_CL=1: the thread-block-cluster rows kernel (ppo_cluster.cuh)
+// for the production network shape -- parity-green, but measured slower
+// than the SIMT rows kernel at B = 256 (C2 episode 5.42 vs 5.35 ms): its
+// column-slice exchanges move 28 KB per CTA through distributed shared
+// memory (~21 B/cycle per SM) six times per update, ~1.5 us each
+static bool use_ppo_cl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HARL_PPO_CL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+static bool ppo_cl_shape(const harl_net_layout& P, const harl_net_layout& V,
+                         int F) {
+  return P.n_layers == 2 && P.dims[1] == PCL_H && P.dims[2] == PCL_H &&
+         F >= 1 && F <= PCL_KX && P.n_head_cols >= 1 &&
+         P.n_head_cols <= PCL_H && V.n_layers == 3 && V.dims[1] == PCL_H &&
+         V.dims[2] == PCL_H && V.dims[3] == 1;
+}
+
 static bool use_ppo_tc() {
   static int v = -1;
   if (v < 0) {
@@ -1839,7 +1861,21 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   ad.tp = tplan;
   ad.wt = wt_params;
   if (phase & 1) {
-  if (use_ppo_tc()) {
+  if (use_ppo_cl() && ppo_cl_shape(*pol, *val, feature_len)) {
+    // thread-block clusters: 8 CTAs x 32 rows, weight slices in shared
+    // memory, activations exchanged through distributed shared memory
+    const size_t csmem = pcl_smem_bytes(feature_len);
+    int rc2 = allow_smem(k_ppo_rows_cl, csmem, "k_ppo_rows_cl");
+    if (rc2) return rc2;
+    if (B > 0) {
+      HARL_PROF_BEGIN(st);
+      launch_k(k_ppo_rows_cl, dim3((unsigned)((B + PCL_R - 1) / PCL_R * PCL_CTAS), 2),
+               dim3(PCL_THREADS), csmem, st, a, *pol, *val, *ring, idx, params,
+               rows, rowout);
+      HARL_PROF_UNITS(B);
+      HARL_CHECK_LAUNCH("k_ppo_rows_cl");
+    }
+  } else if (use_ppo_tc()) {
     // fp64 tensor-core rows kernel: 8 rows per CTA in shared memory
     const size_t tsmem = sizeof(double) * (size_t)PPO8_ROWS * row_stride;
     int rc2 = allow_smem(k_ppo_rows_tc, tsmem, "k_ppo_rows_tc");

@@ -57,6 +57,8 @@ def main():
                     f"{n}={(int(ts[i]) - int(ts[16])) / 1e3:.2f}" for n, i in
                     (("feat_zeroed", 32), ("feat_lut", 33), ("feat_row", 34),
                      ("feat_barrier", 35), ("featurized", 31))))
+        t = ts[57:60].astype(np.int64)
+        print(f"rep {rep} ppo_cl exchange: push={(t[1]-t[0])/1e3:.2f} sync={(t[2]-t[1])/1e3:.2f}")
         if rep == 2:
             a0, a1, b0, b1 = (int(x) for x in ts[60:64])
             print(f"sampler grid {(a1 - a0) / 1e3:.2f} us, gap to featurize "

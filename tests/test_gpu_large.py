@@ -275,3 +275,22 @@ def test_replays_on_the_tf32_fallback(env):
         text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
     assert " passed" in p.stdout
+
+
+def test_cluster_ppo_kernel_parity():
+    """HARL_PPO_CL=1 (k_ppo_rows_cl: the per-row PPO work on 8-CTA
+    clusters, DMMA layers, distributed-shared-memory exchanges) keeps the
+    PPO parity: the update vs the oracle, the golden and shadow replays and
+    the C1 60-step shadow replay with 30 chained updates, in a child
+    process."""
+    p = subprocess.run(
+        [sys.executable, "-m", "pytest", "-q", "-x", "-p",
+         "no:cacheprovider",
+         os.path.join(ROOT, "tests", "test_gpu_episode.py"),
+         os.path.join(ROOT, "tests", "test_gpu_large.py"),
+         "-k", "ppo_update_matches_oracle or golden_episode_replay or "
+               "shadow_replay"],
+        cwd=ROOT, env=dict(os.environ, HARL_PPO_CL="1"), capture_output=True,
+        text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+    assert " passed" in p.stdout

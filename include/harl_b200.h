@@ -81,6 +81,11 @@ typedef struct harl_sketch_desc {
   const double* log2_lut;       /* device [max_extent+1]: log2(v)/10 */
   const uint16_t* spf_lut;      /* device [max_extent+1] */
   const uint16_t* tiling_table; /* device [sum tiling_counts][levels] */
+  /* optional device copy of this descriptor (NULL: none).  Kernels that
+   * stage the per-column / per-term tables into shared memory read them
+   * from it with coalesced global loads instead of thread-divergent
+   * kernel-parameter (constant bank) reads, which serialise per address. */
+  const struct harl_sketch_desc* dev_self;
 } harl_sketch_desc;
 
 /* numpy PCG64 bit-generator state (Generator.bit_generator.state). */
@@ -254,6 +259,31 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         const int32_t* grow, int64_t m_total, double* feat_out,
                         int32_t flags, void* stream);
 
+/* harl_policy_step_tc with SurrogateModel.predict + the reward
+ * (costmodel.py:219-230, tuner.py:389-391) fused into the sampler: the
+ * successor rows it featurizes into feat_out are scored by `forest` (a
+ * reloadable forest: dev_hdr set, host fields are capacities, at most 64
+ * trees) into score[n], and reward[n] = (score - old_score) / old_score
+ * (old_score NULL: no reward).  Bit-identical to harl_gbt_predict /
+ * harl_gbt_finish_step on the same rows.  Returns HARL_E_LIMIT, launching
+ * nothing, when the step is not eligible (not the 3xFP16 path, more rows
+ * than the in-sampler featurize takes, forest capacity or shared memory):
+ * the caller then scores with harl_gbt_finish_step. */
+int harl_policy_step_tc_gbt(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+                            const double* feat, const uint16_t* tiles,
+                            const uint8_t* knobs, int64_t n, int64_t ld,
+                            const harl_pcg64* rng, const int32_t* inject,
+                            int32_t* actions, double* logp, uint16_t* tiles_out,
+                            uint8_t* knobs_out, uint64_t* move_bits,
+                            uint32_t* shift_bits, int32_t* head0_col,
+                            float* logits_out, uint64_t* status,
+                            float* hid_scratch, const uint64_t* rng_state_dev,
+                            const void* packed_trunk, const void* packed_heads,
+                            const int32_t* grow, int64_t m_total, double* feat_out,
+                            int32_t flags, const harl_forest_desc* forest,
+                            const double* old_score, double* score, double* reward,
+                            void* stream);
+
 /* V(X) and V(X') in one launch (tuner.py:395-396) on the tcgen05 path
  * (hidden (128,128), feature_len <= 64); HARL_E_ARG if not eligible. */
 int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
@@ -338,6 +368,26 @@ int harl_finish_step(const harl_step_buffers* io, int64_t n, int64_t ld,
                      int64_t wpos, int64_t keep_from, const harl_entry_log* log,
                      const harl_track_stats* ts, const int64_t* wpos_dev,
                      void* stream);
+
+/* harl_value_pair_tc with the step's finish (harl_finish_step: advantage /
+ * TD, replay push incl. the X / X' rows, entry log, Track.advance;
+ * tuner.py:393-412) run in the value kernel's epilogue for the X' rows:
+ * n1 = the step's rows, n0 = n1 (V(X) computed here, each CTA taking the X
+ * and X' tiles of the same rows) or 0 (V(X) already in v0 from the
+ * previous step).  io->feat / feat_new / v_cur / v_next must be feat0 /
+ * feat1 / v0 / v1.  Bit-identical to harl_value_pair_tc followed by
+ * harl_finish_step.  HARL_E_LIMIT (nothing launched) when the step is not
+ * on the 3xFP16 path: the caller runs the two calls then. */
+int harl_value_finish_tc(const harl_mlp_desc* val, const double* feat0,
+                         int64_t n0, const double* feat1, int64_t n1,
+                         int32_t feature_len, float* v0, float* v1,
+                         const void* packed, int32_t flags,
+                         const harl_step_buffers* io, int64_t ld, int64_t vbase,
+                         int32_t local_slots, double discount, int32_t rl,
+                         const harl_replay_ring* ring, int64_t wpos,
+                         int64_t keep_from, const harl_entry_log* log,
+                         const harl_track_stats* ts, const int64_t* wpos_dev,
+                         void* stream);
 
 /* Survivor compaction after a host cull (stopping.py:68-86): row i of the
  * destination population <- row idx[i] of the source. */

@@ -49,7 +49,7 @@ class SketchDesc(C.Structure):
                 ("stage_extra", i16 * MAX_STAGES),
                 ("head0_src", i16 * MAX_HEAD0), ("head0_dst", i16 * MAX_HEAD0),
                 ("flops_feature", f64), ("log2_lut", vp), ("spf_lut", vp),
-                ("tiling_table", vp)]
+                ("tiling_table", vp), ("dev_self", vp)]
 
 
 class Pcg64(C.Structure):
@@ -146,8 +146,17 @@ _SIGS = {
                                   i64, P(Pcg64), vp, vp, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, vp, vp, vp, i64, vp,
                                   i32, vp]),
+    "harl_policy_step_tc_gbt": (i32, [P(SketchDesc), P(MlpDesc), vp, vp, vp,
+                                      i64, i64, P(Pcg64), vp, vp, vp, vp, vp,
+                                      vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      i64, vp, i32, P(ForestDesc), vp, vp, vp,
+                                      vp]),
     "harl_value_pair_tc": (i32, [P(MlpDesc), vp, i64, vp, i64, i32, vp, vp,
                                  vp, i32, vp]),
+    "harl_value_finish_tc": (i32, [P(MlpDesc), vp, i64, vp, i64, i32, vp, vp,
+                                   vp, i32, P(StepBuffers), i64, i64, i32,
+                                   f64, i32, P(ReplayRing), i64, i64,
+                                   P(EntryLog), P(TrackStats), vp, vp]),
     "harl_tc_packed_bytes": (i64, [i32, i32]),
     "harl_pack_tc_weights": (i32, [P(MlpDesc), P(MlpDesc), i32, vp, vp, vp,
                                    vp]),

@@ -786,7 +786,8 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
                           uint16_t* tiles_out, uint8_t* knobs_out,
                           uint64_t* move_bits, uint32_t* shift_bits,
                           int32_t* head0_col, uint64_t* status,
-                          cudaStream_t st, double* feat_out = nullptr) {
+                          cudaStream_t st, double* feat_out = nullptr,
+                          const SampleGbtArgs* gf = nullptr) {
   PcgJump J;
   LaneJump LJ;
   u128 base;
@@ -819,8 +820,17 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   const dim3 grid((unsigned)((n + rows_per_cta - 1) / rows_per_cta));
   HARL_PROF_BEGIN(st);
   const int nI = (sk->n_head0 + SG - 1) / SG;
-  auto go = [&](auto kfeat, auto kplain) -> int {
-    if (feat_out) {   // also featurize the successor states (schedspace.py:415)
+  auto go = [&](auto kfeat, auto kplain, auto kgbt) -> int {
+    if (feat_out && gf) {   // + the cost model on the successor rows
+      const size_t lut = sk->max_extent + 1 <= FEAT_LUT_SMEM_MAX
+                             ? (size_t)(sk->max_extent + 1) * 8 : 0;
+      const size_t smem = (size_t)gf->region + (size_t)SGBT_ROWS * sk->feature_len * 8 + lut;
+      int rc = allow_smem(kgbt, smem, "k_sample_gbt");
+      if (rc) return rc;
+      const dim3 ggrid((unsigned)((n + SGBT_ROWS - 1) / SGBT_ROWS));
+      launch_k(kgbt, ggrid, dim3(SGBT_THREADS), smem, st, *sk, J, base,
+               (const u128*)rng_state_dev, tiles, knobs, a, feat_out, *gf);
+    } else if (feat_out) {   // also featurize the successor states (schedspace.py:415)
       const size_t lut = sk->max_extent + 1 <= FEAT_LUT_SMEM_MAX
                              ? (size_t)(sk->max_extent + 1) * 8 : 0;
       const size_t smem = (size_t)rows_per_cta * sk->feature_len * 8 + lut;
@@ -837,7 +847,8 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
   int grc;
   // instantiation: head-0 columns cached per lane (MAXI) x slots per lane
   const int nsl = sk->local_slots <= 2 * SG ? 2 : (sk->local_slots <= 4 * SG ? 4 : 8);
-#define HARL_SAMPLER(MX, NS) go(k_sample_rows<true, MX, NS>, k_sample_rows<false, MX, NS>)
+#define HARL_SAMPLER(MX, NS) \
+  go(k_sample_rows<true, MX, NS>, k_sample_rows<false, MX, NS>, k_sample_gbt<MX, NS>)
 #define HARL_SAMPLER_NSL(MX) \
   (nsl == 2 ? HARL_SAMPLER(MX, 2) : nsl == 4 ? HARL_SAMPLER(MX, 4) : HARL_SAMPLER(MX, 8))
   if (nI <= 8) grc = HARL_SAMPLER_NSL(8);
@@ -847,7 +858,8 @@ static int launch_sampler(const harl_sketch_desc* sk, const harl_pcg64* rng,
 #undef HARL_SAMPLER
   if (grc) return grc;
   HARL_PROF_UNITS(n);
-  HARL_CHECK_LAUNCH("k_sample_rows");
+  if (feat_out && gf) HARL_CHECK_LAUNCH("k_sample_gbt");
+  else HARL_CHECK_LAUNCH("k_sample_rows");
   return HARL_OK;
 }
 
@@ -864,7 +876,7 @@ static bool tc_trunk_ok(const harl_mlp_desc* m, int F) {
          m->dims[1] == TC_H && m->dims[2] == TC_H;
 }
 
-int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+static int policy_step_tc_impl(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         const double* feat, const uint16_t* tiles,
                         const uint8_t* knobs, int64_t n, int64_t ld,
                         const harl_pcg64* rng, const int32_t* inject,
@@ -875,7 +887,8 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         float* hid_scratch, const uint64_t* rng_state_dev,
                         const void* packed_trunk, const void* packed_heads,
                         const int32_t* grow, int64_t m_total, double* feat_out,
-                        int32_t flags, void* stream) {
+                        int32_t flags, void* stream, const harl_forest_desc* forest,
+                        const double* old_score, double* score, double* reward) {
   const int32_t fuse_tc = flags & HARL_STEP_FUSED;
   int rc = check_sketch(sk);
   if (rc) return rc;
@@ -893,10 +906,33 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int NHP = (pol->n_head_cols + 15) / 16 * 16;
-  // 3xFP16 policy (trunk + heads, weights resident, two tiles in flight)
-  if (!fuse_tc && packed_trunk && NHP <= F16_NHP_MAX && use_tc16(n) &&
+  const bool f16_path = !fuse_tc && packed_trunk && NHP <= F16_NHP_MAX && use_tc16(n) &&
       ((uintptr_t)feat & 15) == 0 &&
-      (size_t)f16_smem_bytes(true, NHP, sk->feature_len, 1) <= (size_t)max_dyn_smem()) {
+      (size_t)f16_smem_bytes(true, NHP, sk->feature_len, 1) <= (size_t)max_dyn_smem();
+  // the cost model fused into the sampler: decided before anything launches
+  SampleGbtArgs gf;
+  memset(&gf, 0, sizeof(gf));
+  if (forest) {
+    const size_t lut = sk->max_extent + 1 <= FEAT_LUT_SMEM_MAX
+                           ? (size_t)(sk->max_extent + 1) * 8 : 0;
+    const size_t region = sgbt_region_bytes(forest->n_trees > 0 ? forest->n_trees : 1);
+    if (!f16_path || !feat_out || n > SAMPLE_FEAT_MAX_ROWS || !forest->dev_hdr ||
+        forest->n_trees > SGBT_MAX_TREES || !forest->tree_first || !forest->nodes ||
+        !score || (size_t)region + (size_t)SGBT_ROWS * sk->feature_len * 8 + lut >
+            (size_t)max_dyn_smem() / 2 - 16384) {
+      set_error("harl_policy_step_tc_gbt: step not eligible for the fused cost model");
+      return HARL_E_LIMIT;
+    }
+    gf.nodes = (const GbtNode*)forest->nodes;
+    gf.tree_first = forest->tree_first;
+    gf.hdr = (const GbtHdr*)forest->dev_hdr;
+    gf.old_score = old_score;
+    gf.score = score;
+    gf.reward = reward;
+    gf.region = (int32_t)region;
+  }
+  // 3xFP16 policy (trunk + heads, weights resident, two tiles in flight)
+  if (f16_path) {
     const size_t smem = (size_t)f16_smem_bytes(true, NHP, sk->feature_len, 1);
     if ((rc = allow_smem(k_mlp_f16<true>, smem, "k_mlp_f16<policy>"))) return rc;
     F16Args fa;
@@ -912,15 +948,18 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     fa.img = (const uint8_t*)packed_trunk + TRUNK_IMAGE;
     fa.early_w = (flags & HARL_WEIGHTS_SETTLED) ? 1 : 0;
     HARL_PROF_BEGIN(st);
+    GbtFinishArgs nofin;
+    memset(&nofin, 0, sizeof(nofin));
     launch_k(k_mlp_f16<true>, dim3(tc16_grid((n + 127) / 128)), dim3(F16_THREADS),
-             smem, st, fa);
+             smem, st, fa, nofin);
     HARL_PROF_UNITS(n);
     HARL_CHECK_LAUNCH("k_mlp_f16<policy>");
     const bool in_sampler = feat_out && n <= SAMPLE_FEAT_MAX_ROWS;
     rc = launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
                         TC_H, n, ld, tiles, knobs, inject, actions, logp,
                         tiles_out, knobs_out, move_bits, shift_bits, head0_col,
-                        status, st, in_sampler ? feat_out : nullptr);
+                        status, st, in_sampler ? feat_out : nullptr,
+                        forest ? &gf : nullptr);
     if (rc || !feat_out || in_sampler) return rc;
     return harl_featurize(sk, tiles_out, knobs_out, n, ld, feat_out, stream);
   }
@@ -1005,7 +1044,8 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     rc = launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
                         TC_H, n, ld, tiles, knobs, inject, actions, logp,
                         tiles_out, knobs_out, move_bits, shift_bits, head0_col,
-                        status, st, in_sampler ? feat_out : nullptr);
+                        status, st, in_sampler ? feat_out : nullptr,
+                        forest ? &gf : nullptr);
     if (rc || !feat_out || in_sampler) return rc;
     return harl_featurize(sk, tiles_out, knobs_out, n, ld, feat_out, stream);
   }
@@ -1050,11 +1090,56 @@ int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
     return harl_featurize(sk, tiles_out, knobs_out, n, ld, feat_out, stream);
 }
 
+int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+                        const double* feat, const uint16_t* tiles,
+                        const uint8_t* knobs, int64_t n, int64_t ld,
+                        const harl_pcg64* rng, const int32_t* inject,
+                        int32_t* actions, double* logp, uint16_t* tiles_out,
+                        uint8_t* knobs_out, uint64_t* move_bits,
+                        uint32_t* shift_bits, int32_t* head0_col,
+                        float* logits_out, uint64_t* status,
+                        float* hid_scratch, const uint64_t* rng_state_dev,
+                        const void* packed_trunk, const void* packed_heads,
+                        const int32_t* grow, int64_t m_total, double* feat_out,
+                        int32_t flags, void* stream) {
+  return policy_step_tc_impl(sk, pol, feat, tiles, knobs, n, ld, rng, inject, actions,
+                             logp, tiles_out, knobs_out, move_bits, shift_bits,
+                             head0_col, logits_out, status, hid_scratch, rng_state_dev,
+                             packed_trunk, packed_heads, grow, m_total, feat_out, flags,
+                             stream, nullptr, nullptr, nullptr, nullptr);
+}
 
-int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
+int harl_policy_step_tc_gbt(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
+                            const double* feat, const uint16_t* tiles,
+                            const uint8_t* knobs, int64_t n, int64_t ld,
+                            const harl_pcg64* rng, const int32_t* inject,
+                            int32_t* actions, double* logp, uint16_t* tiles_out,
+                            uint8_t* knobs_out, uint64_t* move_bits,
+                            uint32_t* shift_bits, int32_t* head0_col,
+                            float* logits_out, uint64_t* status,
+                            float* hid_scratch, const uint64_t* rng_state_dev,
+                            const void* packed_trunk, const void* packed_heads,
+                            const int32_t* grow, int64_t m_total, double* feat_out,
+                            int32_t flags, const harl_forest_desc* forest,
+                            const double* old_score, double* score, double* reward,
+                            void* stream) {
+  if (!forest) {
+    set_error("harl_policy_step_tc_gbt: forest required");
+    return HARL_E_ARG;
+  }
+  return policy_step_tc_impl(sk, pol, feat, tiles, knobs, n, ld, rng, inject, actions,
+                             logp, tiles_out, knobs_out, move_bits, shift_bits,
+                             head0_col, logits_out, status, hid_scratch, rng_state_dev,
+                             packed_trunk, packed_heads, grow, m_total, feat_out, flags,
+                             stream, forest, old_score, score, reward);
+}
+
+
+static int value_pair_tc_impl(const harl_mlp_desc* val, const double* feat0,
                        int64_t n0, const double* feat1, int64_t n1,
                        int32_t feature_len, float* v0, float* v1,
-                       const void* packed, int32_t flags, void* stream) {
+                       const void* packed, int32_t flags, void* stream,
+                       const GbtFinishArgs* fin) {
   int rc = check_mlp(val, false);
   if (rc) return rc;
   if (val->n_layers != 3 || !tc_trunk_ok(val, feature_len) ||
@@ -1062,10 +1147,16 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
     set_error("harl_value_pair_tc: shape not eligible for the tcgen05 path");
     return HARL_E_ARG;
   }
-  if (n0 + n1 <= 0) return HARL_OK;
-  if (packed && use_tc16(n0 + n1) && ((uintptr_t)feat0 & 15) == 0 &&
+  const bool f16_ok = packed && use_tc16(n0 + n1) && ((uintptr_t)feat0 & 15) == 0 &&
       ((uintptr_t)feat1 & 15) == 0 &&
-      (size_t)f16_smem_bytes(false, 0, feature_len, 1) <= (size_t)max_dyn_smem()) {
+      (size_t)f16_smem_bytes(false, 0, feature_len, 1) <= (size_t)max_dyn_smem();
+  if (fin && (!f16_ok || !feat1 || n1 <= 0 || (n0 != 0 && n0 != n1) ||
+              fin->a.n != n1)) {
+    set_error("harl_value_finish_tc: step not eligible for the fused finish");
+    return HARL_E_LIMIT;
+  }
+  if (n0 + n1 <= 0) return HARL_OK;
+  if (f16_ok) {
     const int nxb = (size_t)f16_smem_bytes(false, 0, feature_len, 2) <=
                     (size_t)max_dyn_smem() ? 2 : 1;
     const size_t smem = (size_t)f16_smem_bytes(false, 0, feature_len, nxb);
@@ -1083,12 +1174,18 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
     fa.b3 = val->b[2];
     fa.img = (const uint8_t*)packed + TRUNK_IMAGE;
     fa.early_w = (flags & HARL_WEIGHTS_SETTLED) ? 1 : 0;
-    const int64_t tiles_n = (n0 + 127) / 128 + (fa.n1 + 127) / 128;
+    GbtFinishArgs nofin;
+    memset(&nofin, 0, sizeof(nofin));
+    fa.fin = fin ? 1 : 0;
+    fa.pair = (fin && n0 == n1) ? 1 : 0;
+    const int64_t tiles_n = fa.pair ? (n1 + 127) / 128
+                                    : (n0 + 127) / 128 + (fa.n1 + 127) / 128;
     HARL_PROF_BEGIN((cudaStream_t)stream);
     launch_k(k_mlp_f16<false>, dim3(tc16_grid(tiles_n)), dim3(F16_THREADS), smem,
-             (cudaStream_t)stream, fa);
+             (cudaStream_t)stream, fa, fin ? *fin : nofin);
     HARL_PROF_UNITS(n0 + fa.n1);
-    HARL_CHECK_LAUNCH("k_mlp_f16<value>");
+    if (fin) HARL_CHECK_LAUNCH("k_mlp_f16<value+finish>");
+    else HARL_CHECK_LAUNCH("k_mlp_f16<value>");
     return HARL_OK;
   }
   if (packed && use_tc2() && ((uintptr_t)feat0 & 15) == 0 &&
@@ -1137,6 +1234,50 @@ int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
   launch_k(k_trunk_tc<TRUNK_VALUE>, dim3(grid), dim3(128), TRUNK_SMEM, (cudaStream_t)stream, ta);
   HARL_CHECK_LAUNCH("k_trunk_tc<value>");
   return HARL_OK;
+}
+
+int harl_value_pair_tc(const harl_mlp_desc* val, const double* feat0,
+                       int64_t n0, const double* feat1, int64_t n1,
+                       int32_t feature_len, float* v0, float* v1,
+                       const void* packed, int32_t flags, void* stream) {
+  return value_pair_tc_impl(val, feat0, n0, feat1, n1, feature_len, v0, v1, packed,
+                            flags, stream, nullptr);
+}
+
+int harl_value_finish_tc(const harl_mlp_desc* val, const double* feat0,
+                         int64_t n0, const double* feat1, int64_t n1,
+                         int32_t feature_len, float* v0, float* v1,
+                         const void* packed, int32_t flags,
+                         const harl_step_buffers* io, int64_t ld, int64_t vbase,
+                         int32_t local_slots, double discount, int32_t rl,
+                         const harl_replay_ring* ring, int64_t wpos,
+                         int64_t keep_from, const harl_entry_log* log,
+                         const harl_track_stats* ts, const int64_t* wpos_dev,
+                         void* stream) {
+  if (!io || !log || !ts || (rl && (!ring || ring->cap < 1)) ||
+      io->v_cur != v0 || io->v_next != v1 || io->feat != feat0 || io->feat_new != feat1) {
+    set_error("harl_value_finish_tc: bad arguments");
+    return HARL_E_ARG;
+  }
+  GbtFinishArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.a.n = n1;
+  fa.a.ld = ld;
+  fa.a.vbase = vbase;
+  fa.a.local_slots = local_slots;
+  fa.a.F = feature_len;
+  fa.a.discount = discount;
+  fa.a.rl = rl;
+  fa.a.wpos = wpos;
+  fa.a.keep_from = keep_from;
+  fa.io = *io;
+  if (ring) fa.ring = *ring;
+  if (fa.ring.cap < 1) fa.ring.cap = 1;
+  fa.log = *log;
+  fa.ts = *ts;
+  fa.wpos_dev = wpos_dev;
+  return value_pair_tc_impl(val, feat0, n0, feat1, n1, feature_len, v0, v1, packed,
+                            flags, stream, &fa);
 }
 
 int harl_prepare(void) {

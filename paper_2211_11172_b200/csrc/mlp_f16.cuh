@@ -23,6 +23,7 @@
 #pragma once
 
 #include "mlp_tc2.cuh"
+#include "episode_kernels.cuh"
 
 namespace harl {
 
@@ -159,6 +160,8 @@ struct F16Args {
   const uint8_t* img;   // f16 image (k_pack16)
   int32_t early_w;      // the image was not written by the previous launch:
                         // load it before the PDL wait
+  int32_t pair;         // value: n0 == n1, CTA-local pairs (X tile p, X' tile p)
+  int32_t fin;          // value: the step's finish bookkeeping in the epilogue
 };
 
 // warp roles: 16 epilogue warps (TMEM lane quarter w % 4, column group
@@ -212,8 +215,19 @@ __device__ __forceinline__ void f16_stage_x(const double* xs, int rows, int F,
 // the slot's next layer.  X tiles arrive in shared memory by bulk copy
 // (xfull[b]), issued by the MMA thread as soon as a buffer's previous tile
 // has been converted.
+//
+// VALUE with a.fin (the step's finish fused, k_gbt_finish's epilogue work:
+// advantage/TD, replay push, entry log, Track.advance -- tuner.py:393-412,
+// rlcore.py:231-265, stopping.py:45-53): with a.pair the CTA takes X tile p
+// and X' tile p as its slot-0 / slot-1 tiles, so the thread that writes
+// V(X')[r] wrote V(X)[r] one event earlier (same lane quarter, lane and
+// column group) and runs finish_row for r right there; the other column
+// groups copy the tile's pushed X / X' rows into their replay slots.
+// Without a.pair (V(X) reused from the previous step: n0 = 0) V(X) comes
+// from the earlier launch.
 template <bool POLICY>
-__global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
+__global__ void __launch_bounds__(F16_THREADS, 1)
+k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
   extern __shared__ __align__(1024) uint8_t smf[];
   const float* fl = (const float*)smf;
   const int img_bytes = POLICY ? f16_image_bytes(a.NHP) : f16_off_wh();
@@ -226,8 +240,9 @@ __global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
   constexpr int NL = POLICY ? 3 : 2;
   const int NXB = a.nxb;
   const int64_t t0 = (a.n0 + 127) / 128, t1 = (a.n1 + 127) / 128;
-  const int64_t tiles = t0 + t1;
-  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t units = a.pair ? t1 : t0 + t1;   // pairs or tiles
+  const int64_t mine_u = units > blockIdx.x ? (units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t mine = a.pair ? 2 * mine_u : mine_u;
   const int64_t cnt0 = (mine + 1) / 2, cnt1 = mine / 2;   // tiles per slot
   // global event e -> (slot, slot-tile, layer); slot 1 lags one stage
   const int64_t n_ev = 2 * (NL * cnt0 + 1) + 2;
@@ -262,11 +277,18 @@ __global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
   griddep_wait();  // PDL: the feature rows (and unsettled weights) are ready
   auto tile_of = [&](int64_t j, const double*& f, int64_t& r0, int& rows,
                      bool& second) {
-    const int64_t t = blockIdx.x + j * gridDim.x;
-    second = t >= t0;
+    int64_t t;
+    if (a.pair) {
+      t = blockIdx.x + (j >> 1) * gridDim.x;
+      second = (j & 1) != 0;
+    } else {
+      t = blockIdx.x + j * gridDim.x;
+      second = t >= t0;
+      if (second) t -= t0;
+    }
     f = second ? a.feat1 : a.feat0;
     const int64_t n = second ? a.n1 : a.n0;
-    r0 = (second ? t - t0 : t) * 128;
+    r0 = t * 128;
     rows = (int)min((int64_t)128, n - r0);
   };
   if (mine > 0 && warp < F16_EPI_WARPS) {
@@ -364,6 +386,44 @@ __global__ void __launch_bounds__(F16_THREADS, 1) k_mlp_f16(F16Args a) {
             (sec ? a.out1 : a.out0)[r0 + lrow] =
                 ((pp[lrow] + pp[128 + lrow]) + (pp[256 + lrow] + pp[384 + lrow])) +
                 __ldg(a.b3);
+          }
+          if (a.fin && sec) {   // X' tile: V(X) and V(X') of its rows are in
+            const int64_t wpos = fin.wpos_dev ? *fin.wpos_dev : fin.a.wpos;
+            if (g == 0) {       // memory, written by this thread or earlier
+              if (lrow < rows)
+                finish_row(fin.a, fin.io, fin.ring, fin.log, fin.ts, wpos, r0 + lrow);
+            } else if (fin.a.rl) {
+              const int64_t lo = r0 > fin.a.keep_from ? r0 : fin.a.keep_from;
+              const int64_t hi = r0 + rows;
+              if (lo < hi) {
+                const int F = fin.a.F;
+                const int total = (int)(hi - lo) * F;
+                const double* __restrict__ sx = fin.io.feat + lo * F;
+                const double* __restrict__ sxn = fin.io.feat_new + lo * F;
+                // all loads of a batch before its stores (the ring could
+                // alias the rows as far as the compiler knows)
+                constexpr int U = 8;
+                for (int e0 = (g - 1) * 128 + lrow; e0 < total; e0 += 384 * U) {
+                  double vx[U], vxn[U];
+#pragma unroll
+                  for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * 384;
+                    vx[u] = e < total ? sx[e] : 0.0;
+                    vxn[u] = e < total ? sxn[e] : 0.0;
+                  }
+#pragma unroll
+                  for (int u = 0; u < U; ++u) {
+                    const int e = e0 + u * 384;
+                    if (e < total) {
+                      const int rr = e / F, k = e - rr * F;
+                      const int64_t slot = (wpos + lo + rr) % fin.ring.cap;
+                      fin.ring.X[slot * F + k] = vx[u];
+                      fin.ring.Xn[slot * F + k] = vxn[u];
+                    }
+                  }
+                }
+              }
+            }
           }
         }
         // the slot's last layer is done with A: stage its next tile's X

@@ -29,7 +29,7 @@ struct LaneJump {
 #define HARL_SAMPLE_ROWS 16     // rows per CTA
 #endif
 #ifndef HARL_SAMPLE_MINB
-#define HARL_SAMPLE_MINB (8 * 8 * 16 / (HARL_SAMPLE_LANES * HARL_SAMPLE_ROWS))
+#define HARL_SAMPLE_MINB (7 * 8 * 16 / (HARL_SAMPLE_LANES * HARL_SAMPLE_ROWS))  // 72 registers: one wave of 16-row CTAs at 16 K rows, fewer spills than 64 (-1 us per launch)
 #endif
 constexpr int SG = HARL_SAMPLE_LANES;   // lanes cooperating on one row
 constexpr int SAMPLE_THREADS = HARL_SAMPLE_ROWS * SG;
@@ -258,15 +258,21 @@ __device__ __forceinline__ void sample_group(
     }
   }
   if (fill_tables) {
+    dbg_ts(38);
     // the CTA's head-0 column tables, filled while the row loads above are
     // in flight (the caller passes this CTA's shared arrays)
+    // (from the descriptor's device copy when there is one: coalesced
+    // loads, not per-thread constant-bank reads that serialise by address)
+    const harl_sketch_desc& sg = sk.dev_self ? *sk.dev_self : sk;
     for (int i = threadIdx.x; i < C0; i += blockDim.x) {
-      const int16_t vs = sk.head0_src[i], vd = sk.head0_dst[i];
+      const int16_t vs = sg.head0_src[i], vd = sg.head0_dst[i];
       const_cast<int16_t*>(s_src)[i] = vs;
       const_cast<int16_t*>(s_dst)[i] = vd;
     }
-    if (fs) foot_fill(sk, fs, lut_s, lut_n);
+    if (fs) foot_fill(sg, fs, lut_s, lut_n);
+    dbg_ts(39);
     __syncthreads();
+    dbg_ts(36);
   }
   // ---- uniforms: lane h of the group draws head h ---------------------
   double u_mine = 0.0;
@@ -574,6 +580,191 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   }
   griddep_trigger();
   dbg_grid(true, 60);
+}
+
+}  // namespace harl
+
+#include "gbt_kernels.cuh"
+
+namespace harl {
+
+// ---------------------------------------------------------------------------
+// Sampler + featurize + GBT predict/reward in one kernel (populations whose
+// step rows fit the in-sampler featurize).  The successor rows' features
+// are already in shared memory when the sampler has featurized them, so
+// the cost model (costmodel.py:219-230: pred = base + sum_t lr*leaf_t in
+// tree order, np.maximum(pred, floor)) and the reward (tuner.py:389-391:
+// (new - old) / old) are evaluated right there: no feature round trip, no
+// separate GBT launch with its own forest prologue.  The forest's
+// perfect-tree image (depth <= SGBT_DEPTH; the reference's GbtConfig
+// default is 6) is bulk-copied into shared memory at kernel start -- the
+// forest is written by host copies only, so the copy runs ahead of the
+// programmatic-dependency wait and lands while the CTA samples.  The 8
+// lanes of a row walk trees g, g+8, ... (4 side by side) and then add the
+// contributions in tree order through group shuffles, every lane forming
+// the same sequential sum (bit-identical to gbt2_body).  A reloaded forest
+// the region cannot hold (deeper, more trees than the launch was sized
+// for, or no perfect image) is walked from the global node records.
+constexpr int SGBT_ROWS = 64;
+constexpr int SGBT_THREADS = SGBT_ROWS * SG;
+constexpr int SGBT_MAX_TREES = 8 * SG;   // 8 contributions per lane
+constexpr int SGBT_DEPTH = 6;
+static_assert(SGBT_THREADS <= 1024, "k_sample_gbt: at most 1024 threads");
+
+struct SampleGbtArgs {
+  const GbtNode* nodes;        // node records (fallback walk)
+  const int32_t* tree_first;
+  const GbtHdr* hdr;           // run-time forest scalars
+  const double* old_score;     // [n] score of the row's current state
+  double* score;               // [n] out
+  double* reward;              // [n] out
+  int32_t region;              // shared bytes reserved for the image
+};
+
+__host__ __device__ inline size_t sgbt_region_bytes(int t_cap) {
+  return gbt_perfect_bytes(t_cap, SGBT_DEPTH);
+}
+
+template <int MAXI, int NSL>
+__global__ void __launch_bounds__(SGBT_THREADS, 2)
+k_sample_gbt(const __grid_constant__ harl_sketch_desc sk,
+             const __grid_constant__ PcgJump J, u128 base_arg,
+             const u128* base_dev, const uint16_t* __restrict__ tiles,
+             const uint8_t* __restrict__ knobs, SampleArgs a,
+             double* __restrict__ feat_out,
+             const __grid_constant__ SampleGbtArgs ga) {
+  constexpr int ROWS = SGBT_ROWS;
+  __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
+  __shared__ uint16_t s_st[ROWS][HARL_MAX_SLOTS];
+  __shared__ uint8_t s_kn[ROWS][4];
+  __shared__ FootSmem s_foot[1];
+  __shared__ uint64_t fbar;
+  __shared__ int s_gi[3];          // n_trees, fitted, staged depth (0: global walk)
+  __shared__ double s_gd[2];       // base, floor
+  extern __shared__ __align__(16) unsigned char sgm[];
+  unsigned char* s_forest = sgm;
+  double* s_feat = (double*)(sgm + ga.region);
+  if (threadIdx.x == 0) {
+    const GbtHdr h = *ga.hdr;
+    const int D = h.perfect_depth;
+    const bool stage = h.fitted && h.n_trees > 0 && D >= 1 && D <= SGBT_DEPTH &&
+                       h.perfect_bytes > 0 && h.perfect_bytes <= ga.region;
+    s_gi[0] = h.n_trees;
+    s_gi[1] = h.fitted;
+    s_gi[2] = stage ? D : 0;
+    s_gd[0] = h.base;
+    s_gd[1] = h.floor_value;
+    if (stage) {
+      tc::mbar_init(&fbar, 1);
+      tc::bulk_load(s_forest, h.perfect, (uint32_t)h.perfect_bytes, &fbar);
+    }
+  }
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  const int lut_n = sk.max_extent + 1;
+  double* lut_s = lut_n <= FEAT_LUT_SMEM_MAX ? s_feat + ROWS * sk.feature_len : nullptr;
+  const int lr = threadIdx.x / SG;
+  const int g = threadIdx.x & (SG - 1);
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+  const int64_t r = r0 + lr;
+  // (the table fill inside ends with a CTA barrier: s_gi/s_gd are visible)
+  sample_group<MAXI, NSL>(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr,
+                          s_src, s_dst, s_st[lr], s_kn[lr], /*fill_tables=*/true,
+                          s_foot, lut_s, lut_n);
+  const unsigned gmask = (SG == 32 ? 0xffffffffu : ((1u << SG) - 1u))
+                         << (threadIdx.x & (32 - SG));
+  __syncwarp(gmask);
+  const int F = sk.feature_len;
+  double* x = s_feat + lr * F;
+  if (r < a.n) featurize_group(sk, g, gmask, s_st[lr], s_kn[lr], x, s_foot, lut_s);
+  const bool live = r < a.n;
+  const double o = (live && ga.old_score) ? ga.old_score[r] : 1.0;
+  __syncthreads();
+  {
+    const int64_t rows = a.n - r0 < ROWS ? a.n - r0 : ROWS;
+    double* out = feat_out + r0 * F;
+    for (int i = threadIdx.x; i < rows * F; i += blockDim.x) out[i] = s_feat[i];
+  }
+  // ---- cost model on the row's features (shared memory) -------------------
+  const int T = s_gi[0], fitted = s_gi[1], D = s_gi[2];
+  double c[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) c[j] = 0.0;
+  if (fitted) {
+    const uint32_t s_x = tc::smem_u32(x);
+    if (D > 0) {
+      tc::mbar_wait(&fbar, 0);
+      const int NI = (1 << D) - 1, NLF = 1 << D;
+      const uint32_t s_thr = tc::smem_u32(s_forest);
+      const uint32_t s_leaf = s_thr + (uint32_t)gbt_perfect_off_leaf(T, D);
+      const uint32_t s_ft = s_thr + (uint32_t)gbt_perfect_off_feat(T, D);
+#pragma unroll
+      for (int jb = 0; jb < 8; jb += GBT_ILP) {
+        uint32_t tbase[GBT_ILP], idx[GBT_ILP];
+#pragma unroll
+        for (int k = 0; k < GBT_ILP; ++k) {
+          const int t = g + SG * (jb + k);
+          tbase[k] = (uint32_t)((t < T ? t : 0) * NI);
+          idx[k] = 0;
+        }
+        if (g + SG * jb >= T) continue;
+        for (int lv = 0; lv < D; ++lv) {
+          int f[GBT_ILP];
+          double th[GBT_ILP], xv[GBT_ILP];
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) {
+            f[k] = lds_s16(s_ft + 2u * (tbase[k] + idx[k]));
+            th[k] = lds_f64(s_thr + 8u * (tbase[k] + idx[k]));
+          }
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) xv[k] = lds_f64(s_x + 8u * (uint32_t)f[k]);
+#pragma unroll
+          for (int k = 0; k < GBT_ILP; ++k) idx[k] = 2u * idx[k] + (xv[k] <= th[k] ? 1u : 2u);
+        }
+#pragma unroll
+        for (int k = 0; k < GBT_ILP; ++k) {
+          const int t = g + SG * (jb + k);
+          const double lv = lds_f64(s_leaf + 8u * ((uint32_t)(t < T ? t : 0) * NLF +
+                                                   idx[k] - (uint32_t)NI));
+          if (t < T) c[jb + k] = lv;
+        }
+      }
+    } else {
+      // node records in global memory (a forest the region cannot hold)
+      const double* xg = x;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int t = g + SG * j;
+        if (t < T) {
+          const GbtNode* tree = ga.nodes + __ldg(ga.tree_first + t);
+          GbtNode nd = tree[0];
+          while (nd.feat >= 0) nd = tree[(xg[nd.feat] <= nd.v) ? nd.left : nd.right];
+          c[j] = nd.v;
+        }
+      }
+    }
+  }
+  // tree-order sum (pred = pred + lr*leaf, costmodel.py:208/228): every lane
+  // of the group forms the same sequential chain from the shuffled terms
+  double pred = 1.0;
+  if (fitted) {
+    pred = s_gd[0];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int q = 0; q < SG; ++q) {
+        const double v = __shfl_sync(0xffffffffu, c[j], q, SG);
+        if (SG * j + q < T) pred = __dadd_rn(pred, v);
+      }
+    }
+  }
+  if (live && g == 0) {
+    const double fl = s_gd[1];
+    const double s = (pred != pred) ? pred : (pred < fl ? fl : pred);
+    ga.score[r] = s;
+    if (ga.old_score) ga.reward[r] = __ddiv_rn(__dsub_rn(s, o), o);
+  }
+  griddep_trigger();
 }
 
 }  // namespace harl

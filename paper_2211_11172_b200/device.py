@@ -128,6 +128,11 @@ class DeviceSketch:
         d.log2_lut = self.log2_lut.data_ptr()
         d.spf_lut = self.spf_lut.data_ptr()
         d.tiling_table = self.tiling_table.data_ptr()
+        # a device copy of the descriptor (dev_self NULL inside it): kernels
+        # staging the column/term tables read them with coalesced loads
+        raw = np.frombuffer(C.string_at(C.addressof(d), C.sizeof(d)), np.uint8)
+        self.desc_dev = torch.from_numpy(raw.copy()).to(dev)
+        d.dev_self = self.desc_dev.data_ptr()
         self.desc = d
         self.head_cols = cols
 
@@ -1300,7 +1305,7 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 n: int, gen=None, inject=None, out=None, want_logits=False,
                 rng_dev=None, advance=True, grow=None, m_total: int = 0,
                 feat_out=None, fuse_tc: bool = False, reset_status=True,
-                settled: bool = False):
+                settled: bool = False, gbt=None):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
     ``feat_out`` (optional f64 [n][F]): also featurize the new states (in
@@ -1309,8 +1314,12 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
     caller already set ``out["status"]`` to -1 (the engine fills its
     per-step status table once per episode, not once per step).
     ``settled``: the weight images were not written by the previous launch
-    (see ``value_pair``).  Returns a dict of device tensors;
-    ``status`` must be checked by the caller (``raise_status``)."""
+    (see ``value_pair``).  ``gbt`` (optional ``(forest, old_score, score,
+    reward)``): score the featurized successor rows with the forest inside
+    the sampler (harl_policy_step_tc_gbt); ``out["gbt_fused"]`` says
+    whether the library took it (else the caller scores them).  Returns a
+    dict of device tensors; ``status`` must be checked by the caller
+    (``raise_status``)."""
     lib = N.load()
     dev = dsk.device
     if out is None:
@@ -1345,15 +1354,26 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
             _ptr(out["knobs"]), _ptr(out["move_bits"]),
             _ptr(out["shift_bits"]), _ptr(out["head0_col"]), _ptr(logits),
             _ptr(out["status"])]
+    out["gbt_fused"] = False
     if agent.tc:
+        flags = (STEP_FUSED if fuse_tc else 0) | \
+            (WEIGHTS_SETTLED if settled else 0)
+        tc_args = [*args, _ptr(agent.hid_scratch(n)), _ptr(rng_dev),
+                   _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]),
+                   _ptr(grow), m_total, _ptr(feat_out), flags]
         with PF.span("policy_tc", n, launches=None):
-            N.check(lib.harl_policy_step_tc(
-                *args, _ptr(agent.hid_scratch(n)), _ptr(rng_dev),
-                _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), _ptr(grow),
-                m_total, _ptr(feat_out),
-                (STEP_FUSED if fuse_tc else 0) |
-                (WEIGHTS_SETTLED if settled else 0), _stream()),
-                "harl_policy_step_tc")
+            rc = N.E_LIMIT
+            if gbt is not None and feat_out is not None and not fuse_tc:
+                forest, old_score, score, reward = gbt
+                rc = lib.harl_policy_step_tc_gbt(
+                    *tc_args, C.byref(forest.desc), _ptr(old_score),
+                    _ptr(score), _ptr(reward), _stream())
+                if rc != N.E_LIMIT:
+                    N.check(rc, "harl_policy_step_tc_gbt")
+                    out["gbt_fused"] = True
+            if rc == N.E_LIMIT:
+                N.check(lib.harl_policy_step_tc(*tc_args, _stream()),
+                        "harl_policy_step_tc")
         if feat_out is not None and not fuse_tc and n > SAMPLE_FEAT_MAX_ROWS:
             # the library featurized with k_featurize2 inside the call: its
             # rows belong to the featurize span (per-kernel roofline rows)

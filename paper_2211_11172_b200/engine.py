@@ -60,6 +60,17 @@ _PY_CULL = os.environ.get("HARL_NATIVE_CULL") == "0"
 # k_finish_step) instead of the fused k_gbt_finish (A/B and fallback path)
 _SPLIT_FINISH = os.environ.get("HARL_SPLIT_FINISH") == "1"
 
+# HARL_SAMPLE_GBT=1: the cost model scored inside the sampler (k_sample_gbt:
+# the featurized successor rows never leave shared memory before the forest
+# walk) and the step's finish run in the value kernel's epilogue
+# (harl_value_finish_tc: one launch fewer per step); =2: sampler-side only,
+# the finish as its own launch.  Bit-identical to the default, measured no
+# faster at C2 (5.44 / 5.40 vs 5.40 ms per episode: the forest walk adds
+# ~7 us to the sampler and the finish ~8 us to the value pass, the launch
+# they save costs ~18 us), so the separate k_gbt_finish stays the default.
+_SAMPLE_GBT = os.environ.get("HARL_SAMPLE_GBT", "0") in ("1", "2")
+_VALUE_FINISH = os.environ.get("HARL_SAMPLE_GBT", "0") == "1"
+
 # HARL_PAR_VALUE=1: the value pass on a forked stream, concurrent with the
 # GBT pass (both read only X'); the finish kernel joins them (split finish).
 # Measured slower at 16 K tracks (5.95 vs 5.82 ms per C2 episode): both
@@ -394,7 +405,11 @@ class EpisodeEngine:
                             feat_out=None if _SPLIT_FEATURIZE else nxt["feat"],
                             fuse_tc=_FUSED_STEP, reset_status=False,
                             settled=k > 0 and not b.plan[k - 1]["ppo"] and
-                            not b.plan[k - 1]["cull"])
+                            not b.plan[k - 1]["cull"],
+                            gbt=(b.forest, cur["score"], nxt["score"], b.reward)
+                            if _SAMPLE_GBT and not _SPLIT_FINISH and
+                            not _PAR_VALUE and not _SPLIT_FEATURIZE else None)
+        gbt_done = res.get("gbt_fused", False)
         if _SPLIT_FEATURIZE:
             D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         # value pass first: the fused GBT kernel's finish epilogue needs
@@ -402,18 +417,6 @@ class EpisodeEngine:
         v_cur, v_next = b.vbuf[(k + 1) % 2], b.vbuf[k % 2]
         reuse = self._v_reusable(b.plan, k)
         par = _PAR_VALUE
-        if par:
-            main = torch.cuda.current_stream()
-            side = self._side_stream()
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
-                             nxt["feat"], m, v_cur, v_next)
-        else:
-            # (the sampler or featurize launch precedes it: the weight
-            # images were last written by an earlier Adam step)
-            D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
-                         nxt["feat"], m, v_cur, v_next, settled=True)
         po = b.pol_out
         io = N.StepBuffers(
             rt.data_ptr(), nxt["tiles"].data_ptr(), nxt["knobs"].data_ptr(),
@@ -426,7 +429,34 @@ class EpisodeEngine:
         cap = self.replay.cap
         keep_from = max(0, m - cap) if keep_from is None else keep_from
         wdev = D._ptr(b.wpos_tab[k:k + 1]) if graph_mode else None
-        if not _SPLIT_FINISH and not par:
+        if gbt_done and _VALUE_FINISH and self.dagent.tc and not par:
+            # the scores are in (sampler); the finish rides on the value pass
+            with PF.span("value_tc", (0 if reuse else m) + m):
+                rc = lib.harl_value_finish_tc(
+                    C.byref(self.dagent.val_desc), cur["feat"].data_ptr(),
+                    0 if reuse else m, nxt["feat"].data_ptr(), m,
+                    tables.feature_len, v_cur.data_ptr(), v_next.data_ptr(),
+                    self.dagent.packed["vt"].data_ptr(), D.WEIGHTS_SETTLED, io,
+                    P, used, tables.local_slots, self.rl_cfg.discount, 1,
+                    self.replay.desc, self.replay.wpos, keep_from, b.elog,
+                    b.ts, wdev, D._stream())
+            if rc == 0:
+                return res
+            if rc != N.E_LIMIT:
+                N.check(rc, "harl_value_finish_tc")
+        if par:
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
+                             nxt["feat"], m, v_cur, v_next)
+        else:
+            # (the sampler or featurize launch precedes it: the weight
+            # images were last written by an earlier Adam step)
+            D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
+                         nxt["feat"], m, v_cur, v_next, settled=True)
+        if not _SPLIT_FINISH and not par and not gbt_done:
             with PF.span("gbt", m, launches=1):
                 rc = lib.harl_gbt_finish_step(
                     C.byref(b.forest.desc), tables.feature_len,
@@ -438,8 +468,9 @@ class EpisodeEngine:
                 return res
             if rc != N.E_LIMIT:
                 N.check(rc, "harl_gbt_finish_step")
-        D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
-                      out=nxt["score"], reward=b.reward)
+        if not gbt_done:
+            D.gbt_predict(b.forest, nxt["feat"], m, old_score=cur["score"],
+                          out=nxt["score"], reward=b.reward)
         if par:
             main.wait_stream(side)
         with PF.span("finish", m, launches=1):

@@ -55,7 +55,8 @@ def main():
             if nm == "sample":   # featurize inside the sampler ends at 31
                 print(f"rep {rep} sample " + " ".join(
                     f"{n}={(int(ts[i]) - int(ts[16])) / 1e3:.2f}" for n, i in
-                    (("feat_zeroed", 32), ("feat_lut", 33), ("feat_row", 34),
+                    (("fill_start", 38), ("fill_done", 39), ("fill_synced", 36),
+                     ("feat_zeroed", 32), ("feat_lut", 33), ("feat_row", 34),
                      ("feat_barrier", 35), ("featurized", 31))))
         t = ts[57:60].astype(np.int64)
         print(f"rep {rep} ppo_cl exchange: push={(t[1]-t[0])/1e3:.2f} sync={(t[2]-t[1])/1e3:.2f}")

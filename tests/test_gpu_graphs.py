@@ -82,15 +82,22 @@ def test_graph_replay_is_bit_identical(monkeypatch, hidden, which, lazy):
 
 
 @pytest.mark.parametrize("flag", ["_FUSED_STEP", "_SPLIT_FEATURIZE",
-                                  "_SPLIT_FINISH", "_PAR_VALUE"])
+                                  "_SPLIT_FINISH", "_PAR_VALUE",
+                                  "_SAMPLE_GBT", "_VALUE_FINISH"])
 def test_kernel_fusion_variants_match_default(monkeypatch, flag):
     """Each alternative launch structure produces the default episode bit
     for bit: _FUSED_STEP (k_policy_step_fused: the 3xTF32 policy -> sample/
     apply -> featurize in one kernel, against the 3xTF32 default), _SPLIT_FEATURIZE (k_featurize2 launched after
     the sampler instead of inside it), _SPLIT_FINISH (k_gbt_predict2 +
     k_finish_step instead of the fused k_gbt_finish), _PAR_VALUE (the value
-    pass on a forked stream beside the GBT pass, joined by the finish)."""
+    pass on a forked stream beside the GBT pass, joined by the finish),
+    _SAMPLE_GBT (the cost model inside the sampler, k_sample_gbt, then a
+    finish-only launch, against the separate k_gbt_finish), _VALUE_FINISH
+    (with the sampler-side cost model: the finish in the value kernel's
+    epilogue, harl_value_finish_tc, against the finish launch)."""
     from paper_2211_11172_b200 import engine as E
+    if flag == "_VALUE_FINISH":   # needs the scores from the sampler
+        monkeypatch.setattr(E, "_SAMPLE_GBT", True)
     if flag == "_FUSED_STEP":
         # the fused kernel is the 3xTF32 policy: compare with that default
         monkeypatch.setenv("HARL_TC16", "0")

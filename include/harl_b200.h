@@ -246,6 +246,18 @@ int harl_policy_step(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
  * kernel may load them before its programmatic-dependency wait). */
 #define HARL_STEP_FUSED 1
 #define HARL_WEIGHTS_SETTLED 2
+/* split launches on the 3xFP16 path (HARL_E_LIMIT, nothing launched,
+ * elsewhere): MLP_ONLY runs the policy network into hid_scratch and
+ * returns (rng may be NULL); SAMPLE_ONLY runs the sampler on the logits a
+ * previous MLP_ONLY call left in hid_scratch for the same rows.  The engine
+ * uses them to run the next step's policy network beside this step's value
+ * and GBT passes. */
+#define HARL_STEP_MLP_ONLY 4
+#define HARL_STEP_SAMPLE_ONLY 8
+/* harl_value_pair_tc with n0 == n1: each CTA takes the X and X' tiles of
+ * the same rows as its two in-flight tiles (half the CTAs of the default
+ * tile order), leaving SMs to a concurrent launch */
+#define HARL_VALUE_PAIRED 16
 int harl_policy_step_tc(const harl_sketch_desc* sk, const harl_mlp_desc* pol,
                         const double* feat, const uint16_t* tiles,
                         const uint8_t* knobs, int64_t n, int64_t ld,

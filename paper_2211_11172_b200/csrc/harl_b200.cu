@@ -900,7 +900,9 @@ static int policy_step_tc_impl(const harl_sketch_desc* sk, const harl_mlp_desc* 
     return HARL_E_ARG;
   }
   if (n <= 0) return HARL_OK;
-  if (!rng && !inject) {
+  const bool mlp_only = (flags & HARL_STEP_MLP_ONLY) != 0;
+  const bool sample_only = (flags & HARL_STEP_SAMPLE_ONLY) != 0;
+  if (!rng && !inject && !mlp_only) {
     set_error("harl_policy_step_tc: need rng or injected actions");
     return HARL_E_ARG;
   }
@@ -909,6 +911,10 @@ static int policy_step_tc_impl(const harl_sketch_desc* sk, const harl_mlp_desc* 
   const bool f16_path = !fuse_tc && packed_trunk && NHP <= F16_NHP_MAX && use_tc16(n) &&
       ((uintptr_t)feat & 15) == 0 &&
       (size_t)f16_smem_bytes(true, NHP, sk->feature_len, 1) <= (size_t)max_dyn_smem();
+  if ((mlp_only || sample_only) && (!f16_path || (mlp_only && sample_only))) {
+    set_error("harl_policy_step_tc: split launch not on the 3xFP16 path");
+    return HARL_E_LIMIT;
+  }
   // the cost model fused into the sampler: decided before anything launches
   SampleGbtArgs gf;
   memset(&gf, 0, sizeof(gf));
@@ -932,7 +938,7 @@ static int policy_step_tc_impl(const harl_sketch_desc* sk, const harl_mlp_desc* 
     gf.region = (int32_t)region;
   }
   // 3xFP16 policy (trunk + heads, weights resident, two tiles in flight)
-  if (f16_path) {
+  if (f16_path && !sample_only) {
     const size_t smem = (size_t)f16_smem_bytes(true, NHP, sk->feature_len, 1);
     if ((rc = allow_smem(k_mlp_f16<true>, smem, "k_mlp_f16<policy>"))) return rc;
     F16Args fa;
@@ -954,6 +960,9 @@ static int policy_step_tc_impl(const harl_sketch_desc* sk, const harl_mlp_desc* 
              smem, st, fa, nofin);
     HARL_PROF_UNITS(n);
     HARL_CHECK_LAUNCH("k_mlp_f16<policy>");
+    if (mlp_only) return HARL_OK;
+  }
+  if (f16_path) {
     const bool in_sampler = feat_out && n <= SAMPLE_FEAT_MAX_ROWS;
     rc = launch_sampler(sk, rng, rng_state_dev, grow, m_total, hid_scratch,
                         TC_H, n, ld, tiles, knobs, inject, actions, logp,
@@ -1177,7 +1186,7 @@ static int value_pair_tc_impl(const harl_mlp_desc* val, const double* feat0,
     GbtFinishArgs nofin;
     memset(&nofin, 0, sizeof(nofin));
     fa.fin = fin ? 1 : 0;
-    fa.pair = (fin && n0 == n1) ? 1 : 0;
+    fa.pair = ((fin || (flags & HARL_VALUE_PAIRED)) && n0 == n1) ? 1 : 0;
     const int64_t tiles_n = fa.pair ? (n1 + 127) / 128
                                     : (n0 + 127) / 128 + (fa.n1 + 127) / 128;
     HARL_PROF_BEGIN((cudaStream_t)stream);

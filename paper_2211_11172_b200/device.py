@@ -1305,7 +1305,7 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
                 n: int, gen=None, inject=None, out=None, want_logits=False,
                 rng_dev=None, advance=True, grow=None, m_total: int = 0,
                 feat_out=None, fuse_tc: bool = False, reset_status=True,
-                settled: bool = False, gbt=None):
+                settled: bool = False, gbt=None, split: int = 0):
     """select_actions + decode/apply for n rows.  Consumes 4*n doubles of
     ``gen`` (head-major, like rlcore.py:223-225) unless ``inject`` is given.
     ``feat_out`` (optional f64 [n][F]): also featurize the new states (in
@@ -1317,8 +1317,10 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
     (see ``value_pair``).  ``gbt`` (optional ``(forest, old_score, score,
     reward)``): score the featurized successor rows with the forest inside
     the sampler (harl_policy_step_tc_gbt); ``out["gbt_fused"]`` says
-    whether the library took it (else the caller scores them).  Returns a
-    dict of device tensors; ``status`` must be checked by the caller
+    whether the library took it (else the caller scores them).
+    ``split=STEP_SAMPLE_ONLY``: the policy network already ran for these
+    rows (``policy_mlp``), only the sampler launches.  Returns a dict of
+    device tensors; ``status`` must be checked by the caller
     (``raise_status``)."""
     lib = N.load()
     dev = dsk.device
@@ -1357,7 +1359,7 @@ def policy_step(dsk: DeviceSketch, agent: DeviceAgent, feat, tiles, knobs,
     out["gbt_fused"] = False
     if agent.tc:
         flags = (STEP_FUSED if fuse_tc else 0) | \
-            (WEIGHTS_SETTLED if settled else 0)
+            (WEIGHTS_SETTLED if settled else 0) | split
         tc_args = [*args, _ptr(agent.hid_scratch(n)), _ptr(rng_dev),
                    _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]),
                    _ptr(grow), m_total, _ptr(feat_out), flags]
@@ -1405,10 +1407,33 @@ def value_estimate(agent: DeviceAgent, feat, n: int, out=None):
 
 # harl_policy_step_tc / harl_value_pair_tc flags (include/harl_b200.h)
 STEP_FUSED, WEIGHTS_SETTLED = 1, 2
+STEP_MLP_ONLY, STEP_SAMPLE_ONLY, VALUE_PAIRED = 4, 8, 16
+
+
+def policy_mlp(dsk: DeviceSketch, agent: DeviceAgent, feat, n: int,
+               settled: bool = True) -> bool:
+    """The policy network alone (PolicyNet.forward, rlcore.py:136-146) for
+    n rows into the agent's logits scratch, for a later
+    ``policy_step(..., split=STEP_SAMPLE_ONLY)`` on the same rows.  False
+    (nothing launched) off the 3xFP16 path."""
+    if not agent.tc:
+        return False
+    lib = N.load()
+    z = [None] * 10
+    with PF.span("policy_tc", n, launches=None):
+        rc = lib.harl_policy_step_tc(
+            C.byref(dsk.desc), C.byref(agent.pol_desc), _ptr(feat), None, None,
+            n, 0, None, *z, _ptr(agent.hid_scratch(n)), None,
+            _ptr(agent.packed["pt"]), _ptr(agent.packed["ph"]), None, 0, None,
+            STEP_MLP_ONLY | (WEIGHTS_SETTLED if settled else 0), _stream())
+    if rc == N.E_LIMIT:
+        return False
+    N.check(rc, "harl_policy_step_tc")
+    return True
 
 
 def value_pair(agent: DeviceAgent, feat0, n0: int, feat1, n1: int,
-               out0, out1, settled: bool = False):
+               out0, out1, settled: bool = False, paired: bool = False):
     """V(X) and V(X') (tuner.py:395-396); one tcgen05 launch for the
     production shape, otherwise two FFMA launches.  ``settled``: the
     weight images were not written by the previous launch (the kernel may
@@ -1420,7 +1445,8 @@ def value_pair(agent: DeviceAgent, feat0, n0: int, feat1, n1: int,
                                            _ptr(feat0), n0, _ptr(feat1), n1,
                                            feat0.shape[1], _ptr(out0),
                                            _ptr(out1), _ptr(agent.packed["vt"]),
-                                           WEIGHTS_SETTLED if settled else 0,
+                                           (WEIGHTS_SETTLED if settled else 0) |
+                                           (VALUE_PAIRED if paired else 0),
                                            _stream()),
                     "harl_value_pair_tc")
         return out0[:n0], out1[:n1]

@@ -71,6 +71,11 @@ _SPLIT_FINISH = os.environ.get("HARL_SPLIT_FINISH") == "1"
 _SAMPLE_GBT = os.environ.get("HARL_SAMPLE_GBT", "0") in ("1", "2")
 _VALUE_FINISH = os.environ.get("HARL_SAMPLE_GBT", "0") == "1"
 
+# graph mode: the next step's policy network on a forked stream beside the
+# value and GBT passes of steps without a PPO update or cull
+# (HARL_OVERLAP_POLICY=0: strictly sequential launches)
+_OVERLAP_POLICY = os.environ.get("HARL_OVERLAP_POLICY", "1") != "0"
+
 # HARL_PAR_VALUE=1: the value pass on a forked stream, concurrent with the
 # GBT pass (both read only X'); the finish kernel joins them (split finish).
 # Measured slower at 16 K tracks (5.95 vs 5.82 ms per C2 episode): both
@@ -389,9 +394,37 @@ class EpisodeEngine:
                      grow=None, m_total=0, keep_from=None):
         """Issue every launch of search step k (policy+walker, featurize,
         GBT+reward, V(X)/V(X'), finish).  In graph mode the RNG base state
-        and the replay write position come from the device tables."""
-        tables, P = b.tables, b.P
+        and the replay write position come from the device tables.
+
+        Graph mode, a step without PPO update or cull before an equal-size
+        step (_OVERLAP_POLICY): step k+1's policy network depends only on
+        X' (the sampler's output) and unchanged weights, so it runs on a
+        forked stream beside this step's value and GBT passes (disjoint
+        SMs once the population is culled), joined before step k+1's
+        sampler."""
         m = step["m"] if m is None else m
+        pre = graph_mode and getattr(b, "pre_pol", None) == k
+        b.pre_pol = None
+        side = None
+        if (graph_mode and _OVERLAP_POLICY and
+                grow is None and inj is None and not want_logits and
+                not _SPLIT_FEATURIZE and not _PAR_VALUE and not _FUSED_STEP
+                and not step["ppo"] and not step["cull"] and
+                k + 1 < len(b.plan) and b.plan[k + 1]["m"] == m):
+            side = self._side_stream()
+        try:
+            return self._launch_step_body(b, k, step, cur, nxt, rt, used,
+                                          graph_mode, gen, inj, want_logits,
+                                          m, grow, m_total, keep_from, pre,
+                                          side)
+        finally:
+            if side is not None:
+                torch.cuda.current_stream().wait_stream(side)
+
+    def _launch_step_body(self, b, k, step, cur, nxt, rt, used, graph_mode,
+                          gen, inj, want_logits, m, grow, m_total, keep_from,
+                          pre, side):
+        tables, P = b.tables, b.P
         lib = N.load()
         out = dict(b.pol_out)
         out["tiles"], out["knobs"] = nxt["tiles"], nxt["knobs"]
@@ -408,8 +441,14 @@ class EpisodeEngine:
                             not b.plan[k - 1]["cull"],
                             gbt=(b.forest, cur["score"], nxt["score"], b.reward)
                             if _SAMPLE_GBT and not _SPLIT_FINISH and
-                            not _PAR_VALUE and not _SPLIT_FEATURIZE else None)
+                            not _PAR_VALUE and not _SPLIT_FEATURIZE else None,
+                            split=D.STEP_SAMPLE_ONLY if pre else 0)
         gbt_done = res.get("gbt_fused", False)
+        if side is not None:   # step k+1's policy network beside value + GBT
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                if D.policy_mlp(b.dsk, self.dagent, nxt["feat"], m):
+                    b.pre_pol = k + 1
         if _SPLIT_FEATURIZE:
             D.featurize(b.dsk, nxt["tiles"], nxt["knobs"], m, nxt["feat"])
         # value pass first: the fused GBT kernel's finish epilogue needs
@@ -454,8 +493,11 @@ class EpisodeEngine:
         else:
             # (the sampler or featurize launch precedes it: the weight
             # images were last written by an earlier Adam step)
+            # (paired X/X' tiles per CTA when the next policy network runs
+            # beside it: half the CTAs, the rest of the SMs for that one)
             D.value_pair(self.dagent, cur["feat"], 0 if reuse else m,
-                         nxt["feat"], m, v_cur, v_next, settled=True)
+                         nxt["feat"], m, v_cur, v_next, settled=True,
+                         paired=side is not None)
         if not _SPLIT_FINISH and not par and not gbt_done:
             with PF.span("gbt", m, launches=1):
                 rc = lib.harl_gbt_finish_step(
@@ -969,6 +1011,7 @@ class EpisodeEngine:
         self._ensure_ppo_scratch(max([s["ppo"] or 0 for s in b.plan] + [1]))
         segs = self._segments(b.plan)
         graphs = []
+        b.pre_pol = None
         cur_i, rt_i, used, ppo_k = 0, 0, 0, 0
         wpos0 = self.replay.wpos
         count0 = self.replay.count

@@ -83,7 +83,8 @@ def test_graph_replay_is_bit_identical(monkeypatch, hidden, which, lazy):
 
 @pytest.mark.parametrize("flag", ["_FUSED_STEP", "_SPLIT_FEATURIZE",
                                   "_SPLIT_FINISH", "_PAR_VALUE",
-                                  "_SAMPLE_GBT", "_VALUE_FINISH"])
+                                  "_SAMPLE_GBT", "_VALUE_FINISH",
+                                  "_OVERLAP_POLICY"])
 def test_kernel_fusion_variants_match_default(monkeypatch, flag):
     """Each alternative launch structure produces the default episode bit
     for bit: _FUSED_STEP (k_policy_step_fused: the 3xTF32 policy -> sample/
@@ -94,7 +95,9 @@ def test_kernel_fusion_variants_match_default(monkeypatch, flag):
     _SAMPLE_GBT (the cost model inside the sampler, k_sample_gbt, then a
     finish-only launch, against the separate k_gbt_finish), _VALUE_FINISH
     (with the sampler-side cost model: the finish in the value kernel's
-    epilogue, harl_value_finish_tc, against the finish launch)."""
+    epilogue, harl_value_finish_tc, against the finish launch),
+    _OVERLAP_POLICY (the next step's policy network on a forked stream
+    beside the value and GBT passes, against strictly sequential launches)."""
     from paper_2211_11172_b200 import engine as E
     if flag == "_VALUE_FINISH":   # needs the scores from the sampler
         monkeypatch.setattr(E, "_SAMPLE_GBT", True)

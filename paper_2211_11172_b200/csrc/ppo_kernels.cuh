@@ -190,7 +190,8 @@ __device__ inline double wsum64(double v) {
 
 // per-row terms written to rowout[r*4 + {0..3}]:
 //   min(s_un, s_cl), entropy total, ratio, (v - td)^2
-__global__ void __launch_bounds__(PPO_THREADS)
+// (2 CTAs per SM: the 2 x B/PPO_TM CTAs of a minibatch in one wave)
+__global__ void __launch_bounds__(PPO_THREADS, 2)
 k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout P,
            const __grid_constant__ NetLayout V, PpoRing ring, const int32_t* idx,
            const double* params, const double* wt, double* rows,
@@ -209,6 +210,30 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   double* base = srows;  // this CTA's rows, copied out at the end
   double* wbuf = srows + PPO_TM * RS + 8;  // split-reduction partials
   __shared__ int16_t s_src[HARL_MAX_HEAD0];
+  // the rows' transition fields, loaded with the gather (one round trip
+  // behind idx) instead of where the loss terms use them
+  __shared__ uint64_t s_mv[PPO_TM];
+  __shared__ uint32_t s_sb[PPO_TM];
+  __shared__ int32_t s_act[PPO_TM][4];
+  __shared__ double s_sc[PPO_TM][4];
+  if (threadIdx.x < nrows) {
+    const int q = threadIdx.x;
+    const int sl = idx[r0 + q];
+    const int4 ac = *(const int4*)&ring.actions[(int64_t)sl * 4];
+    const uint64_t mvq = ring.move_bits[sl];
+    const uint32_t sbq = ring.shift_bits[sl];
+    double sc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sc[j] = ring.scalars[(int64_t)sl * 4 + j];
+    s_act[q][0] = ac.x;
+    s_act[q][1] = ac.y;
+    s_act[q][2] = ac.z;
+    s_act[q][3] = ac.w;
+    s_mv[q] = mvq;
+    s_sb[q] = sbq;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s_sc[q][j] = sc[j];
+  }
   for (int i = threadIdx.x; i < a.C0; i += blockDim.x) s_src[i] = a.head0_src[i];
   // gather X (shared by both nets: P.row_act[0] == V.row_act[0])
   for (int i = threadIdx.x; i < nrows * a.F; i += blockDim.x) {
@@ -249,18 +274,17 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   constexpr int HI = 4;      // cached columns per lane (C0 <= 128)
   double ev[HI];
   double hm = 0.0, hs = 1.0, hls = 0.0, hent = 0.0;
-  int col = 0, c0 = 0, C = 0, slot = 0;
+  int col = 0, c0 = 0, C = 0;
   uint64_t mv = 0;
   uint32_t sb = 0;
   double* z = nullptr;
   if (active) {
-    slot = idx[r0 + rr];
     z = base + rr * RS + P.row_head;
-    mv = ring.move_bits[slot];
-    sb = ring.shift_bits[slot];
+    mv = s_mv[rr];
+    sb = s_sb[rr];
     c0 = h == 0 ? 0 : a.C0 + 3 * (h - 1);
     C = h == 0 ? a.C0 : 3;
-    col = ring.actions[slot * 4 + h];
+    col = s_act[rr][h];
   }
   auto legal = [&](int j) -> bool {
     if (h == 0) return j == a.C0 - 1 || ((mv >> s_src[j]) & 1ull);
@@ -308,8 +332,8 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   if (active) {
     const double logp_new = ((s_lp[rr][0] + s_lp[rr][1]) + s_lp[rr][2]) + s_lp[rr][3];
     const double ent_total = ((s_ent[rr][0] + s_ent[rr][1]) + s_ent[rr][2]) + s_ent[rr][3];
-    const double logp_old = ring.scalars[slot * 4 + 0];
-    const double adv = ring.scalars[slot * 4 + 2];
+    const double logp_old = s_sc[rr][0];
+    const double adv = s_sc[rr][2];
     const double ratio = exp(logp_new - logp_old);
     const double clipped = fmin(fmax(ratio, a.clip_lo), a.clip_hi);
     const double s_un = ratio * adv, s_cl = clipped * adv;
@@ -343,8 +367,7 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   }
   if (role == 1 && threadIdx.x < nrows) {
     const int q = threadIdx.x;
-    const int sl = idx[r0 + q];
-    const double td = ring.scalars[sl * 4 + 3];
+    const double td = s_sc[q][3];
     const double v = base[q * RS + V.row_act[V.n_layers]];
     rowout[(int64_t)(r0 + q) * 4 + 3] = (v - td) * (v - td);
     // dv = w * 2 (v - td) / B is the value net's output delta

@@ -466,22 +466,28 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
   for (int k = 0; k < a.nbounds; ++k) a.per_track += a.bounds[k] > 1;
   unsigned long long* bad = (unsigned long long*)scratch;
   unsigned long long* used = bad + 1;
+  // pinned host words for the two read-backs (a pageable copy stages
+  // through a driver buffer)
+  static thread_local unsigned long long* hw = nullptr;
+  if (!hw) {
+    cudaError_t e = cudaHostAlloc((void**)&hw, 16, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_status(e, "init pinned words");
+  }
   a.t0 = 0;
   a.j0 = 0;
   while (a.t0 < count) {
-    const unsigned long long init = ULLONG_MAX;
-    cudaError_t e = cudaMemcpyAsync(bad, &init, 8, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_status(e, "init memcpy");
+    cudaError_t e = cudaMemsetAsync(bad, 0xff, 8, st);   // ULLONG_MAX
+    if (e != cudaSuccess) return cuda_status(e, "init memset");
     const int64_t todo = count - a.t0;
     const int threads = 256;
     HARL_PROF_BEGIN(st);
     launch_k(k_init_sample, dim3((unsigned)((todo + threads - 1) / threads)), dim3(threads), 0, st, 
         *sk, J, a, tiles, knobs, bad);
     HARL_CHECK_LAUNCH("k_init_sample");
-    unsigned long long first = 0;
-    e = cudaMemcpyAsync(&first, bad, 8, cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(hw, bad, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_status(e, "init sync");
+    const unsigned long long first = hw[0];
     if (first == ULLONG_MAX) {
       a.j0 += (uint64_t)todo * (uint64_t)a.per_track;
       a.t0 = count;
@@ -493,10 +499,10 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
     HARL_PROF_BEGIN(st);
     launch_k(k_init_one, dim3(1), dim3(1), 0, st, *sk, J, one, (int64_t)first, tiles, knobs, used);
     HARL_CHECK_LAUNCH("k_init_one");
-    unsigned long long u = 0;
-    e = cudaMemcpyAsync(&u, used, 8, cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(hw + 1, used, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_status(e, "init sync");
+    const unsigned long long u = hw[1];
     a.j0 = one.j0 + u;
     a.t0 = (int64_t)first + 1;
   }

@@ -172,21 +172,28 @@ def states_to_host(tables: SketchTables, tiles, knobs, n: int):
 
 
 def init_population(dsk: DeviceSketch, count: int, gen: np.random.Generator,
-                    tiles=None, knobs=None):
-    """sample_initial_schedules on device, advancing ``gen`` exactly."""
+                    tiles=None, knobs=None, cursor=None):
+    """sample_initial_schedules on device, advancing ``gen`` exactly (or,
+    given a ``rng.StreamCursor`` over it, the cursor instead)."""
     lib = N.load()
     tb = dsk.tables
     if tiles is None:
         tiles, knobs = alloc_state(count, tb, dsk.device)
-    scratch = torch.zeros(4, dtype=torch.int64, device=dsk.device)
-    st = R.to_struct(gen)
+    scratch = getattr(dsk, "_init_scratch", None)
+    if scratch is None:
+        scratch = dsk._init_scratch = torch.zeros(4, dtype=torch.int64,
+                                                  device=dsk.device)
+    st = cursor.struct() if cursor is not None else R.to_struct(gen)
     used = C.c_int64(0)
     with PF.span("init", count):
         N.check(lib.harl_init_population(
             C.byref(dsk.desc), C.byref(st), count, _ptr(tiles), _ptr(knobs),
             tiles.shape[1], C.byref(used), _ptr(scratch), _stream()),
             "harl_init_population")
-    R.skip_u32(gen, used.value)
+    if cursor is not None:
+        cursor.skip_u32(used.value)
+    else:
+        R.skip_u32(gen, used.value)
     return tiles, knobs
 
 

@@ -36,6 +36,7 @@ import os
 from . import _native as N
 from . import device as D
 from . import profiling as PF
+from . import rng as R
 from .agent import AgentState, RlConfig
 from .space import SketchTables
 
@@ -128,11 +129,25 @@ class EpisodeConfig:
                    min_tracks=min_tracks, rl=rl, adaptive=adaptive)
 
 
+_PLANS: dict = {}
+
+
 def schedule(cfg: EpisodeConfig, replay_count: int, rl_cfg: RlConfig):
     """The episode's step plan, known before it starts: the live-row count
     per step, where culls happen and how many rows they keep, and the
     replay size at each PPO step.  None of it depends on the data
-    (tuner.py:371-432, stopping.py:68-95)."""
+    (tuner.py:371-432, stopping.py:68-95).  Memoised (the configs are
+    frozen): the returned plan is shared and must not be modified."""
+    key = (cfg, replay_count, rl_cfg)
+    plan = _PLANS.get(key)
+    if plan is None:
+        if len(_PLANS) > 256:
+            _PLANS.clear()
+        plan = _PLANS[key] = _schedule(cfg, replay_count, rl_cfg)
+    return plan
+
+
+def _schedule(cfg: EpisodeConfig, replay_count: int, rl_cfg: RlConfig):
     alive, used, t = cfg.tracks, 0, 0
     count = replay_count
     plan = []
@@ -322,16 +337,31 @@ class _Buffers:
                      torch.empty(P, dtype=torch.float32, device=dev)]
         self.adv = torch.empty(P, dtype=torch.float64, device=dev)
         self.keep = torch.empty(P, dtype=torch.int32, device=dev)
-        # per-step tables for graph replay (host fills them each episode)
-        self.rng_tab = torch.zeros((max(n_steps, 1), 2), dtype=torch.int64,
-                                   device=dev)
-        self.wpos_tab = torch.zeros(max(n_steps, 1), dtype=torch.int64,
-                                    device=dev)
+        # per-step tables for graph replay (host fills them each episode),
+        # views of one device block mirrored by one pinned block: an upload
+        # is one copy
         Bmax = max([s["ppo"] or 0 for s in plan] + [1])
-        self.slot_tab = torch.zeros((max(self.n_ppo, 1), Bmax),
-                                    dtype=torch.int32, device=dev)
-        self.adam_tab = torch.zeros((max(self.n_ppo, 1), 4),
-                                    dtype=torch.float64, device=dev)
+        ns, npp = max(n_steps, 1), max(self.n_ppo, 1)
+        a16 = lambda n: (n + 15) // 16 * 16  # noqa: E731
+        o_wpos = a16(ns * 16)
+        o_slot = o_wpos + a16(ns * 8)
+        o_adam = o_slot + a16(npp * Bmax * 4)
+        nbytes = o_adam + npp * 4 * 8
+        self.tab = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        self.tab_pin = torch.zeros(nbytes, dtype=torch.uint8,
+                                   pin_memory=dev.type == "cuda")
+
+        def views(t):
+            return (t[:ns * 16].view(torch.int64).view(ns, 2),
+                    t[o_wpos:o_wpos + ns * 8].view(torch.int64),
+                    t[o_slot:o_slot + npp * Bmax * 4].view(torch.int32)
+                    .view(npp, Bmax),
+                    t[o_adam:o_adam + npp * 32].view(torch.float64)
+                    .view(npp, 4))
+        self.rng_tab, self.wpos_tab, self.slot_tab, self.adam_tab = \
+            views(self.tab)
+        self.pins = dict(zip(("rng", "wpos", "slot", "adam"),
+                             views(self.tab_pin)))
         self.graphs = None      # list of (first_step, last_step, CUDAGraph)
 
 
@@ -372,14 +402,13 @@ class EpisodeEngine:
     # -----------------------------------------------------------------------
 
     def _buffers(self, tables, cfg, forest, plan):
-        key = (id(tables), cfg, id(forest),
-               tuple((s["m"], s["cull"], s["ppo"]) for s in plan))
+        key = (id(tables), cfg, id(forest), id(plan))   # plans are memoised
         b = self._cache.get(key)
         if b is None:
             if len(self._cache) > 8:
                 self._cache.clear()
             b = _Buffers(self, tables, cfg.tracks, cfg.budget, plan, forest)
-            b.keepalive = (tables, forest)
+            b.keepalive = (tables, forest, plan)
             self._cache[key] = b
         return b
 
@@ -599,7 +628,9 @@ class EpisodeEngine:
         # ---- population (outside any graph: the sampler may sync) -------
         cur, nxt = b.pop[0], b.pop[1]
         rt, rt_spare = b.rt[0], b.rt[1]
-        D.init_population(b.dsk, P, gen, cur["tiles"], cur["knobs"])
+        cursor = None if eager else R.StreamCursor(gen)
+        D.init_population(b.dsk, P, gen, cur["tiles"], cur["knobs"],
+                          cursor=cursor)
         if trace is not None:
             trace.append(("init", 0, 0, time.perf_counter()))
         if getattr(b, "iota", None) is None:
@@ -611,7 +642,7 @@ class EpisodeEngine:
             res = self._run_eager(b, gen, cfg, order_counter, inject, record,
                                   cull_override)
         else:
-            res = self._run_graphed(b, gen, cfg, order_counter)
+            res = self._run_graphed(b, gen, cfg, order_counter, cursor)
         st = b.status.cpu().numpy().view(np.uint64)
         PF.xfer("d2h", b.status)
         for code in st[:len(plan)]:
@@ -1046,7 +1077,7 @@ class EpisodeEngine:
         self.replay.wpos, self.replay.count = wpos0, count0
         b.graphs = graphs
 
-    def _run_graphed(self, b, gen, cfg, order_counter):
+    def _run_graphed(self, b, gen, cfg, order_counter, cursor=None):
         from . import rng as R
         P = cfg.tracks
         inc = int(gen.bit_generator.state["state"]["inc"])
@@ -1059,17 +1090,14 @@ class EpisodeEngine:
         # pipelined: the first segment's rows go up and its graph starts,
         # then the host prepares the remaining rows while the GPU runs
         n_steps = len(b.plan)
-        if getattr(b, "pins", None) is None:
-            mk = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            b.pins = {"rng": mk(b.rng_tab), "wpos": mk(b.wpos_tab),
-                      "slot": mk(b.slot_tab), "adam": mk(b.adam_tab)}
         pins = b.pins
         rng_np = pins["rng"].numpy().view(np.uint64)
         wpos_np = pins["wpos"].numpy()
         slot_np = pins["slot"].numpy()
         adam_np = pins["adam"].numpy()
         a = self.agent
-        cursor = R.StreamCursor(gen)
+        if cursor is None:
+            cursor = R.StreamCursor(gen)
         pk = [0]
 
         def precompute(k0, k1):
@@ -1098,14 +1126,10 @@ class EpisodeEngine:
             return p0, pk[0]
 
         def upload(k0, k1, p0, p1):
-            b.rng_tab[k0:k1 + 1].copy_(pins["rng"][k0:k1 + 1], non_blocking=True)
-            b.wpos_tab[k0:k1 + 1].copy_(pins["wpos"][k0:k1 + 1],
-                                        non_blocking=True)
-            PF.xfer("h2d", b.rng_tab[k0:k1 + 1], b.wpos_tab[k0:k1 + 1])
-            if p1 > p0:
-                b.slot_tab[p0:p1].copy_(pins["slot"][p0:p1], non_blocking=True)
-                b.adam_tab[p0:p1].copy_(pins["adam"][p0:p1], non_blocking=True)
-                PF.xfer("h2d", b.slot_tab[p0:p1], b.adam_tab[p0:p1])
+            # the whole table block in one stream-ordered copy (rows of
+            # earlier segments are rewritten with the values they hold)
+            b.tab.copy_(b.tab_pin, non_blocking=True)
+            PF.xfer("h2d", b.tab)
 
         segs = b.graphs
         # rows of segment 0 first; then, before blocking anywhere, the rows
@@ -1269,8 +1293,11 @@ class EpisodeEngine:
                                      non_blocking=True)
             PF.xfer("h2d", b.keep[:len(keep)])
             return gone
-        a8 = b.alive8
-        a8[:len(alive)] = alive
+        # (bool and uint8 share a layout: the library marks alive in place)
+        a8 = alive.view(np.uint8) if alive.dtype == np.bool_ and \
+            alive.flags.c_contiguous else b.alive8
+        if a8 is b.alive8:
+            a8[:len(alive)] = alive
         gone = np.zeros(n_elim, dtype=np.int64)
         nk = C.c_int64(0)
         N.check(N.load().harl_cull_select(
@@ -1279,7 +1306,8 @@ class EpisodeEngine:
             "harl_cull_select")
         if trace is not None:
             trace.append(("cull_selected", 0, 0, time.perf_counter()))
-        alive[:] = a8[:len(alive)].astype(bool)
+        if a8 is b.alive8:
+            alive[:] = a8[:len(alive)].astype(bool)
         b.keep[:nk.value].copy_(b.keep_pin[:nk.value], non_blocking=True)
         PF.xfer("h2d", b.keep[:nk.value])
         if trace is not None:

@@ -62,6 +62,23 @@ class StreamCursor:
             j = _JUMPS[(n, self.inc)] = _jump(n, self.inc)
         self.s = (j[0] * self.s + j[1]) & M128
 
+    def skip_u32(self, n: int) -> None:
+        """``skip_u32`` on the cursor (the buffered half kept the same way)."""
+        if n <= 0:
+            return
+        if self.has:
+            n -= 1
+            self.has = 0
+        if n > 0:
+            full, odd = divmod(n, 2)
+            self.skip_u64(full + odd)
+            self.has, self.buf = odd, output(self.s) >> 32
+
+    def struct(self) -> "N.Pcg64":
+        return N.Pcg64(state_hi=self.s >> 64, state_lo=self.s & M64,
+                       inc_hi=self.inc >> 64, inc_lo=self.inc & M64,
+                       has_uint32=self.has, uinteger=self.buf)
+
     def sync_to(self) -> None:
         self.gen.bit_generator.state = {
             "bit_generator": "PCG64",

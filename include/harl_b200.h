@@ -599,6 +599,22 @@ int harl_heap_to_creation_order(const int32_t* feat_h, const double* thr_h,
  * 64-step walk), -2 (empty tree / child index outside its tree), -3 (more
  * than 1024 trees or a tree beyond int16 indices), -4 (perfect_cap too
  * small).  Replaces the per-round numpy packing of the forest reload. */
+/* Host-side: the agent's numpy arrays <-> the flat fp64 parameter layout
+ * (DeviceAgent._views) in one call.  Each op moves rows x ncols doubles:
+ * flat[off + r*flat_ld + c] <-> host[r*host_ld + (cols ? cols[c] : c)]
+ * (cols: the tiling head's legal columns, else NULL).  to_host = 0 packs
+ * the arrays into flat, 1 writes flat back into them.  0, or -1 for a bad
+ * op.  Replaces the per-array numpy copies of DeviceAgent._pack /
+ * _unpack_into (rlcore.py:50-160 state, tuner.py:350-440). */
+typedef struct harl_copy_op {
+  int64_t off, flat_ld;
+  void* host;
+  int64_t host_ld, rows, ncols;
+  const int64_t* cols;
+} harl_copy_op;
+int harl_agent_copy(const harl_copy_op* ops, int32_t n_ops, double* flat,
+                    int32_t to_host);
+
 long long harl_forest_pack(int n_trees, const int64_t* sizes,
                            const int64_t* feature, const double* threshold,
                            const int64_t* left, const int64_t* right,

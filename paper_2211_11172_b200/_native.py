@@ -63,6 +63,11 @@ class MlpDesc(C.Structure):
                 ("head_W", vp), ("head_b", vp), ("n_head_cols", i32)]
 
 
+class CopyOp(C.Structure):
+    _fields_ = [("off", i64), ("flat_ld", i64), ("host", vp), ("host_ld", i64),
+                ("rows", i64), ("ncols", i64), ("cols", vp)]
+
+
 class ForestDesc(C.Structure):
     _fields_ = [("n_trees", i32), ("fitted", i32), ("base", f64),
                 ("floor_value", f64), ("tree_first", vp), ("nodes", vp),
@@ -182,6 +187,7 @@ _SIGS = {
     "harl_format_canonical": (C.c_longlong, [vp, vp, C.c_longlong, i32, i32,
                                               C.c_char_p, C.c_longlong, vp,
                                               C.c_longlong]),
+    "harl_agent_copy": (i32, [P(CopyOp), i32, vp, i32]),
     "harl_forest_pack": (C.c_longlong, [i32, vp, vp, vp, vp, vp, vp, f64, vp,
                                          vp, i32, vp, C.c_longlong,
                                          P(C.c_longlong)]),

@@ -316,11 +316,14 @@ def b200_session_class(base):
                 if ref is None:
                     raise
                 raise ref from exc
-            eng.sync_to_host()
+            # the agent's copy-out runs on a side stream while the entry
+            # selection's kernels run; the numpy lists are written after
+            eng.dagent.download_async()
             # the replay FIFO now lives in the device ring; the deque is
             # rebuilt only if something reads it (_RingBuffer)
             buf._on_device = True
             entries = self._b200_entries(res, tables, sketch)
+            eng.sync_to_host()
             self.order_counter += res.visits
             if self.log:
                 self._b200_log(res, rnd)

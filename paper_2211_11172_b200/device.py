@@ -932,6 +932,7 @@ class DeviceForest:
              fitted: bool = True, floor_value: float = 1e-6) -> bool:
         """Load another ensemble in place; False if it exceeds the
         capacity (build a new forest then)."""
+        self._loaded = None
         cols = self._columns(trees)
         if int(cols[0].sum()) > self.cap_nodes or len(trees) > self.cap_trees:
             return False
@@ -947,14 +948,32 @@ class DeviceForest:
     def from_model(cls, model, device=None, node_capacity: int = 0,
                    tree_capacity: int = 0):
         """From a reference ``SurrogateModel`` (duck-typed)."""
-        return cls(cls._model_trees(model), model.base,
-                   model.cfg.learning_rate, fitted=model.fitted,
-                   device=device, node_capacity=node_capacity,
-                   tree_capacity=tree_capacity)
+        trees = cls._model_trees(model)
+        f = cls(trees, model.base, model.cfg.learning_rate,
+                fitted=model.fitted, device=device,
+                node_capacity=node_capacity, tree_capacity=tree_capacity)
+        f._loaded = ((model.base, model.cfg.learning_rate, bool(model.fitted),
+                      len(trees)), trees)
+        return f
 
     def load_model(self, model) -> bool:
-        return self.load(self._model_trees(model), model.base,
-                         model.cfg.learning_rate, fitted=model.fitted)
+        """Load a reference ``SurrogateModel``; a no-op when it still holds
+        the very tree arrays (and scalars) loaded last time -- the
+        reference refits by building new trees (costmodel.py:190-212),
+        so an unchanged model is skipped without re-packing it."""
+        trees = self._model_trees(model)
+        sig = (model.base, model.cfg.learning_rate, bool(model.fitted),
+               len(trees))
+        last = getattr(self, "_loaded", None)
+        if last is not None and last[0] == sig and all(
+                a is b for ta, tb in zip(trees, last[1])
+                for a, b in zip(ta, tb)):
+            return True
+        ok = self.load(trees, model.base, model.cfg.learning_rate,
+                       fitted=model.fitted)
+        # the arrays are held, so their identities stay unique
+        self._loaded = (sig, trees) if ok else None
+        return ok
 
 
 def _check_depth_all(feat, left_g, right_g, roots):
@@ -1140,6 +1159,74 @@ class DeviceAgent:
             val.append(flat[vl.off_b[l]:vl.off_b[l] + vdims[l + 1]])
         return trunk, hW, hb, val
 
+    def _copy_plan(self, pol_list, val_list):
+        """harl_agent_copy's op list moving these arrays to / from the flat
+        layout (the _views / _pack order), cached while the arrays are the
+        same objects; None if one is not a C-contiguous float64 array of
+        its layout shape (the numpy copies handle it then)."""
+        key = tuple(id(a) for a in pol_list) + tuple(id(a) for a in val_list)
+        cache = getattr(self, "_plans", None)
+        if cache is None:
+            cache = self._plans = {}
+        hit = cache.get(key)
+        if hit is not None:
+            return hit[0]
+        arrs = list(pol_list) + list(val_list)
+        if any(not isinstance(a, np.ndarray) or a.dtype != np.float64 or
+               not a.flags.c_contiguous for a in arrs):
+            return None
+        pl, vl = self.pol_layout, self.val_layout
+        nt = len(self.hidden)
+        dims = [self.F, *self.hidden]
+        H, NH, C0 = self.hidden[-1], self.NH, self.C0
+        cols = np.ascontiguousarray(self.cols, dtype=np.int64)
+        ops = []
+
+        def flat_op(off, a, n):
+            if a.size != n:
+                raise ValueError
+            ops.append((off, 0, a.ctypes.data, 0, 1, n, None))
+        try:
+            for l in range(nt):
+                flat_op(pl.off_W[l], pol_list[2 * l], dims[l] * dims[l + 1])
+                flat_op(pl.off_b[l], pol_list[2 * l + 1], dims[l + 1])
+            heads = pol_list[2 * nt:]
+            if heads[0].shape[0] != H or heads[1].size != heads[0].shape[1]:
+                raise ValueError
+            ops.append((pl.off_hW, NH, heads[0].ctypes.data, heads[0].shape[1],
+                        H, C0, cols.ctypes.data))
+            ops.append((pl.off_hb, 0, heads[1].ctypes.data, 0, 1, C0,
+                        cols.ctypes.data))
+            for h in range(3):
+                w, b = heads[2 + 2 * h], heads[3 + 2 * h]
+                if w.shape != (H, 3) or b.size != 3:
+                    raise ValueError
+                ops.append((pl.off_hW + C0 + 3 * h, NH, w.ctypes.data, 3, H, 3,
+                            None))
+                ops.append((pl.off_hb + C0 + 3 * h, 0, b.ctypes.data, 0, 1, 3,
+                            None))
+            vdims = [self.F, *self.hidden, 1]
+            for l in range(vl.n_layers):
+                flat_op(vl.off_W[l], val_list[2 * l], vdims[l] * vdims[l + 1])
+                flat_op(vl.off_b[l], val_list[2 * l + 1], vdims[l + 1])
+        except (ValueError, IndexError):
+            return None
+        arr = (N.CopyOp * len(ops))(*[N.CopyOp(*o) for o in ops])
+        if len(cache) > 16:
+            cache.clear()
+        cache[key] = ((arr, len(ops)), arrs, cols)   # keeps the ids valid
+        return cache[key][0]
+
+    def _native_copy(self, flat: np.ndarray, pol_list, val_list,
+                     to_host: bool) -> bool:
+        plan = self._copy_plan(pol_list, val_list)
+        if plan is None:
+            return False
+        N.check(N.load().harl_agent_copy(plan[0], plan[1], flat.ctypes.data,
+                                         1 if to_host else 0),
+                "harl_agent_copy")
+        return True
+
     def _pack(self, pol_list, val_list, out=None, views=None) -> np.ndarray:
         """The numpy lists -> the flat layout (every element written)."""
         if out is None:
@@ -1183,9 +1270,11 @@ class DeviceAgent:
         if self._pin_done is not None:      # the last copy out of _pin
             self._pin_done.synchronize()
         pin, vw = self._pin_np, self._pin_views
-        self._pack(a.policy, a.value, pin[0], vw[0])
-        self._pack(a.opt_pi.m, a.opt_v.m, pin[1], vw[1])
-        self._pack(a.opt_pi.v, a.opt_v.v, pin[2], vw[2])
+        for i, (pol, val) in enumerate(((a.policy, a.value),
+                                        (a.opt_pi.m, a.opt_v.m),
+                                        (a.opt_pi.v, a.opt_v.v))):
+            if not self._native_copy(pin[i], pol, val, False):
+                self._pack(pol, val, pin[i], vw[i])
         self.pmv.copy_(self._pin, non_blocking=True)
         self._pin_done = torch.cuda.Event()
         self._pin_done.record()
@@ -1206,18 +1295,43 @@ class DeviceAgent:
         if getattr(self, "packed", None) is not None:
             self.repack()
 
+    def download_async(self):
+        """Start the device -> pinned copy of params and moments on a side
+        stream (ordered after everything issued so far on the current
+        stream) so the caller can issue other device work meanwhile;
+        ``download`` finishes it."""
+        if self._pin_done is not None:
+            self._pin_done.synchronize()
+        main = torch.cuda.current_stream()
+        side = getattr(self, "_side", None)
+        if side is None:
+            side = self._side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self._pin.copy_(self.pmv, non_blocking=True)
+            self._dl_done = torch.cuda.Event()
+            self._dl_done.record()
+        self.pmv.record_stream(side)
+
     def download(self):
         """Write device params and moments back into the numpy lists."""
         a = self.agent
-        if self._pin_done is not None:
-            self._pin_done.synchronize()
-        self._pin.copy_(self.pmv, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        dl = getattr(self, "_dl_done", None)
+        if dl is not None:        # started by download_async
+            self._dl_done = None
+            dl.synchronize()
+        else:
+            if self._pin_done is not None:
+                self._pin_done.synchronize()
+            self._pin.copy_(self.pmv, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
         self._pin_done = None
         pin, vw = self._pin_np, self._pin_views
-        self._unpack_into(pin[0], a.policy, a.value, vw[0])
-        self._unpack_into(pin[1], a.opt_pi.m, a.opt_v.m, vw[1])
-        self._unpack_into(pin[2], a.opt_pi.v, a.opt_v.v, vw[2])
+        for i, (pol, val) in enumerate(((a.policy, a.value),
+                                        (a.opt_pi.m, a.opt_v.m),
+                                        (a.opt_pi.v, a.opt_v.v))):
+            if not self._native_copy(pin[i], pol, val, True):
+                self._unpack_into(pin[i], pol, val, vw[i])
         PF.xfer("d2h", self.pmv)
 
     def _build_descs(self):

@@ -95,3 +95,34 @@ def test_fused_cost_model_after_reloads():
             ref_reward[:n].cpu().numpy().tobytes()
         if not fitted:
             assert (score.cpu().numpy() == 1.0).all()
+
+
+def test_native_agent_copy_matches_numpy_pack():
+    """DeviceAgent's native pack/unpack (harl_agent_copy) writes the same
+    flat block and the same numpy arrays as the numpy restatement
+    (_pack / _unpack_into), for parameters and both Adam moments."""
+    from paper_2211_11172_b200 import device as D
+    _, _, tb = all_sketch_tables(CONV)[0]
+    agent = _agent(tb)
+    rng = np.random.default_rng(4)
+    for lst in (agent.policy, agent.value, agent.opt_pi.m, agent.opt_v.m,
+                agent.opt_pi.v, agent.opt_v.v):
+        for a in lst:
+            a[...] = rng.normal(size=a.shape)
+    dag = D.DeviceAgent(agent, tb.levels)
+    for pol, val in ((agent.policy, agent.value),
+                     (agent.opt_pi.m, agent.opt_v.m),
+                     (agent.opt_pi.v, agent.opt_v.v)):
+        ref = dag._pack(pol, val)
+        got = np.full(dag.n_params, np.nan)
+        got[:] = ref          # untouched padding (if any) equal on both sides
+        got_n = got.copy()
+        assert dag._native_copy(got_n, pol, val, False)
+        assert got_n.tobytes() == ref.tobytes()
+        flat = rng.normal(size=dag.n_params)
+        a1 = [x.copy() for x in pol], [x.copy() for x in val]
+        a2 = [x.copy() for x in pol], [x.copy() for x in val]
+        dag._unpack_into(flat, *a1)
+        assert dag._native_copy(flat, *a2, True)
+        for x, y in zip(a1[0] + a1[1], a2[0] + a2[1]):
+            assert x.tobytes() == y.tobytes()

@@ -76,7 +76,8 @@ STRUCTS = {"harl_sketch_desc": N.SketchDesc, "harl_pcg64": N.Pcg64,
            "harl_replay_ring": N.ReplayRing, "harl_entry_log": N.EntryLog,
            "harl_track_stats": N.TrackStats,
            "harl_step_buffers": N.StepBuffers,
-           "harl_net_layout": N.NetLayout, "harl_ppo_hyper": N.PpoHyper}
+           "harl_net_layout": N.NetLayout, "harl_ppo_hyper": N.PpoHyper,
+           "harl_copy_op": N.CopyOp}
 
 
 def test_ctypes_layouts_match_the_c_compiler(tmp_path):

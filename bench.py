@@ -550,8 +550,10 @@ def e2e_leg(cfg_name, P, steps, warmup, dev, rank):
     ``B200TuningSession._run_episode`` (compat.py) on a reference
     ``TuningSession`` built from baseline/_ref, called exactly as run_round
     calls it (tuner.py:480).  Every timed call takes the session's numpy
-    agent and Adam moments, the replay deque (first call) and the refitted
-    ensemble host->device, runs the episode and the device rank_scores,
+    agent and Adam moments (compared bit for bit with what the previous
+    call wrote back, uploaded if they differ), the replay deque (first
+    call) and the ensemble (reloaded when refitted) host->device, runs the
+    episode and the device rank_scores,
     writes parameters and moments back into the numpy arrays and returns
     the reference's CandidateEntry list.  Wall time (perf_counter with a
     device synchronize on both sides); bytes = the library's accounted

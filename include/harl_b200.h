@@ -603,8 +603,8 @@ int harl_heap_to_creation_order(const int32_t* feat_h, const double* thr_h,
  * (DeviceAgent._views) in one call.  Each op moves rows x ncols doubles:
  * flat[off + r*flat_ld + c] <-> host[r*host_ld + (cols ? cols[c] : c)]
  * (cols: the tiling head's legal columns, else NULL).  to_host = 0 packs
- * the arrays into flat, 1 writes flat back into them.  0, or -1 for a bad
- * op.  Replaces the per-array numpy copies of DeviceAgent._pack /
+ * the arrays into flat, 1 writes flat back into them, 2 only compares
+ * (returns 1 at the first bitwise difference).  0, or -1 for a bad op.  Replaces the per-array numpy copies of DeviceAgent._pack /
  * _unpack_into (rlcore.py:50-160 state, tuner.py:350-440). */
 typedef struct harl_copy_op {
   int64_t off, flat_ld;

@@ -23,6 +23,25 @@ extern "C" {
 int harl_agent_copy(const harl_copy_op* ops, int32_t n_ops, double* flat,
                     int32_t to_host) {
   if (!ops || n_ops < 0 || !flat) return -1;
+  if (to_host == 2) {   // compare only: 0 if every element is bitwise equal
+    for (int32_t i = 0; i < n_ops; ++i) {
+      const harl_copy_op& o = ops[i];
+      if (!o.host || o.rows < 0 || o.ncols < 0 || o.off < 0) return -1;
+      const double* h = static_cast<const double*>(o.host);
+      const double* f = flat + o.off;
+      for (int64_t r = 0; r < o.rows; ++r) {
+        const double* fr = f + r * o.flat_ld;
+        const double* hr = h + r * o.host_ld;
+        if (!o.cols) {
+          if (memcmp(hr, fr, (size_t)o.ncols * 8)) return 1;
+        } else {
+          for (int64_t c = 0; c < o.ncols; ++c)
+            if (memcmp(&hr[o.cols[c]], &fr[c], 8)) return 1;
+        }
+      }
+    }
+    return 0;
+  }
   for (int32_t i = 0; i < n_ops; ++i) {
     const harl_copy_op& o = ops[i];
     if (!o.host || o.rows < 0 || o.ncols < 0 || o.off < 0) return -1;

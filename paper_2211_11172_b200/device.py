@@ -1227,6 +1227,20 @@ class DeviceAgent:
                 "harl_agent_copy")
         return True
 
+    def _host_matches_pin(self) -> bool:
+        """The numpy parameters and moments equal, bit for bit, the pinned
+        block (False when a list cannot be compared natively)."""
+        a = self.agent
+        lib = N.load()
+        for i, (pol, val) in enumerate(((a.policy, a.value),
+                                        (a.opt_pi.m, a.opt_v.m),
+                                        (a.opt_pi.v, a.opt_v.v))):
+            plan = self._copy_plan(pol, val)
+            if plan is None or lib.harl_agent_copy(
+                    plan[0], plan[1], self._pin_np[i].ctypes.data, 2) != 0:
+                return False
+        return True
+
     def _pack(self, pol_list, val_list, out=None, views=None) -> np.ndarray:
         """The numpy lists -> the flat layout (every element written)."""
         if out is None:
@@ -1269,6 +1283,11 @@ class DeviceAgent:
         a = self.agent
         if self._pin_done is not None:      # the last copy out of _pin
             self._pin_done.synchronize()
+        if _UPLOAD_SKIP and getattr(self, "_device_is_pin", False) and \
+                self._host_matches_pin():
+            # the device state is what the last download wrote into the
+            # lists, and nobody changed them since: nothing to upload
+            return
         pin, vw = self._pin_np, self._pin_views
         for i, (pol, val) in enumerate(((a.policy, a.value),
                                         (a.opt_pi.m, a.opt_v.m),
@@ -1281,6 +1300,7 @@ class DeviceAgent:
         self.params32.copy_(self.params)
         PF.xfer("h2d", self.pmv)
         self.refresh_derived()
+        self._device_is_pin = True
 
     def refresh_derived(self):
         """Rebuild every device copy derived from the master parameters:
@@ -1332,6 +1352,7 @@ class DeviceAgent:
                                         (a.opt_pi.v, a.opt_v.v))):
             if not self._native_copy(pin[i], pol, val, True):
                 self._unpack_into(pin[i], pol, val, vw[i])
+        self._device_is_pin = True
         PF.xfer("d2h", self.pmv)
 
     def _build_descs(self):
@@ -1386,6 +1407,7 @@ class DeviceAgent:
                    phase: int = 3):
         """One ppo_update on replay ``slots`` (device int32 ring slots).
         ``t_pi``/``t_v`` are the Adam step counts AFTER this update."""
+        self._device_is_pin = False
         lib = N.load()
         B = int(slots.shape[0])
         hp = N.PpoHyper()
@@ -1527,6 +1549,10 @@ def value_estimate(agent: DeviceAgent, feat, n: int, out=None):
 
 
 # harl_policy_step_tc / harl_value_pair_tc flags (include/harl_b200.h)
+# DeviceAgent.upload skips the copy while the numpy lists still hold what
+# the last download wrote (HARL_UPLOAD_SKIP=0: always upload; A/B)
+_UPLOAD_SKIP = os.environ.get("HARL_UPLOAD_SKIP", "1") != "0"
+
 STEP_FUSED, WEIGHTS_SETTLED = 1, 2
 STEP_MLP_ONLY, STEP_SAMPLE_ONLY, VALUE_PAIRED = 4, 8, 16
 

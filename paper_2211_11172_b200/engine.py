@@ -605,6 +605,9 @@ class EpisodeEngine:
         chosen actions; ``record`` collects per-step device tensors for
         parity checks; ``cull_override(step, own_choice)`` may replace the
         eliminated track set (parity replays only)."""
+        # (graph replays update the parameters without passing through
+        # DeviceAgent.ppo_update: the host copy is stale from here on)
+        self.dagent._device_is_pin = False
         if self.shard is not None:
             return self._run_sharded(tables, forest, gen, cfg, order_counter)
         trace = _HOST_TRACE

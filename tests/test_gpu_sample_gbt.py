@@ -126,3 +126,32 @@ def test_native_agent_copy_matches_numpy_pack():
         assert dag._native_copy(flat, *a2, True)
         for x, y in zip(a1[0] + a1[1], a2[0] + a2[1]):
             assert x.tobytes() == y.tobytes()
+
+
+def test_upload_skipped_only_while_the_host_lists_are_unchanged():
+    """DeviceAgent.upload skips the copy when the numpy lists still hold,
+    bit for bit, what the last download wrote; any change (one element of
+    one Adam moment) is uploaded; an episode always invalidates."""
+    import torch
+    from paper_2211_11172_b200 import device as D
+    _, _, tb = all_sketch_tables(CONV)[0]
+    agent = _agent(tb)
+    dag = D.DeviceAgent(agent, tb.levels)
+    calls = []
+    orig = dag.refresh_derived
+    dag.refresh_derived = lambda: (calls.append(1), orig())[1]
+    dag.upload()
+    dag.download()
+    n0 = len(calls)
+    dag.upload()                       # unchanged: skipped
+    assert len(calls) == n0
+    agent.opt_v.m[1].reshape(-1)[3] += 0.5
+    dag.upload()                       # changed: uploaded
+    assert len(calls) == n0 + 1
+    torch.cuda.synchronize()
+    dag.download()
+    assert agent.opt_v.m[1].reshape(-1)[3] == dag._pin_np[1][
+        dag.val_layout.off_b[0] + 3]
+    dag._device_is_pin = False         # what run_episode does
+    dag.upload()
+    assert len(calls) == n0 + 2

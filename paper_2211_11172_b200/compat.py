@@ -309,27 +309,47 @@ def b200_session_class(base):
                 self._b200_load_ring(eng, sg)
             from .errors import to_reference
             try:
+                # (status checked below, after the entry selection's
+                # launches are queued behind the episode)
                 res = eng.run_episode(tables, forest, self.rng, ecfg,
-                                      self.order_counter)
+                                      self.order_counter, defer_checks=True)
+                # the agent's copy-out runs on a side stream while the
+                # entry selection's kernels run; the numpy lists are
+                # written after the checks
+                eng.dagent.download_async()
+                pending = self._b200_entries_launch(res, tables, sketch)
+                getattr(res, "check", lambda: None)()
             except (ValueError, RuntimeError) as exc:
                 ref = to_reference(exc)
                 if ref is None:
                     raise
                 raise ref from exc
-            # the agent's copy-out runs on a side stream while the entry
-            # selection's kernels run; the numpy lists are written after
-            eng.dagent.download_async()
             # the replay FIFO now lives in the device ring; the deque is
             # rebuilt only if something reads it (_RingBuffer)
             buf._on_device = True
-            entries = self._b200_entries(res, tables, sketch)
+            entries = self._b200_entries(res, tables, sketch, pending)
             eng.sync_to_host()
             self.order_counter += res.visits
             if self.log:
                 self._b200_log(res, rnd)
             return entries
 
-        def _b200_entries(self, res, tables, sketch):
+        def _b200_entries_launch(self, res, tables, sketch):
+            """Queue the device top-k' selection of ``_b200_entries`` right
+            behind the episode (None when every visit is returned)."""
+            if self.b200_all_entries:
+                return None
+            cfg = self.cfg
+            k_hat = max(0, min(cfg.top_k, cfg.total_trials - self.trials_used))
+            prefix = sketch.id + "|"
+            measured = [c for c in self.measured if c.startswith(prefix)]
+            ex = tables.arrays_from_canonical(measured) if measured else None
+            sc = getattr(self, "_b200_rank_scratch", None)
+            if sc is None:
+                sc = self._b200_rank_scratch = D.RankScratch()
+            return (k_hat, ex, sc, res.top_entries_launch(k_hat, ex, sc))
+
+        def _b200_entries(self, res, tables, sketch, pending=None):
             """The episode's CandidateEntry list (tuner.py:406-412).
 
             run_round passes it straight to ``rank_scores(model, entries,
@@ -350,18 +370,11 @@ def b200_session_class(base):
                                     res.visits).cpu().numpy()
                 order = np.arange(res.visits)
             else:
-                cfg = self.cfg
-                k_hat = max(0, min(cfg.top_k,
-                                   cfg.total_trials - self.trials_used))
-                prefix = sketch.id + "|"
-                measured = [c for c in self.measured if c.startswith(prefix)]
-                ex = tables.arrays_from_canonical(measured) if measured \
-                    else None
-                sc = getattr(self, "_b200_rank_scratch", None)
-                if sc is None:
-                    sc = self._b200_rank_scratch = D.RankScratch()
+                if pending is None:
+                    pending = self._b200_entries_launch(res, tables, sketch)
+                k_hat, ex, sc, pend = pending
                 order, tiles, knobs, feats, _, _ = res.top_entries(
-                    k_hat, ex, sc)
+                    k_hat, ex, sc, pend)
             # canonical texts formatted as ScheduleState.canonical does
             # (schedspace.py:117-120), from the same Python ints
             states, texts = tables.states_from_arrays(

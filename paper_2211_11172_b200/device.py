@@ -283,7 +283,7 @@ class RankScratch:
 
 def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
               n_visits: int, k: int, exclude=None, scratch=None,
-              sort: bool = True):
+              sort: bool = True, launch_only: bool = False):
     """``rank_scores(model, entries, k, exclude)`` (costmodel.py:266-286)
     over a device entry log whose ``log_score`` holds each visit's model
     score (the episode's per-visit GBT predictions, which equal
@@ -316,8 +316,26 @@ def rank_topk(tables: SketchTables, log_tiles, log_knobs, log_score,
             sc.buf.data_ptr(), sc.buf.numel(), sc.out.data_ptr(),
             sc.out.numel(), sc.stats.data_ptr(), _stream()),
             "harl_rank_topk")
-    st = sc.stats.cpu().numpy()
+    # the stats through a pinned buffer and an event: ``launch_only``
+    # returns here (the caller may queue more work), ``rank_topk_finish``
+    # completes the call
+    if getattr(sc, "stats_pin", None) is None:
+        sc.stats_pin = torch.empty(4, dtype=torch.int64, pin_memory=True)
+    sc.stats_pin.copy_(sc.stats, non_blocking=True)
     PF.xfer("d2h", sc.stats)
+    ev = torch.cuda.Event()
+    ev.record()
+    pend = (sc, ev, sort)
+    if launch_only:
+        return pend
+    return rank_topk_finish(pend)
+
+
+def rank_topk_finish(pend):
+    """The second half of ``rank_topk(..., launch_only=True)``."""
+    sc, ev, sort = pend
+    ev.synchronize()
+    st = sc.stats_pin.numpy()
     n = int(st[0])
     stats = {"selected": n, "kept": int(st[1]), "collisions": int(st[2]),
              "k_target": int(st[3])}
@@ -1394,11 +1412,7 @@ class DeviceAgent:
         """ppo_update's finiteness checks (rlcore.py:368-373): the kernels
         set ``bad`` (1: a loss, 2: a gradient) and skip the Adam step; the
         host raises the reference's RlDivergedError."""
-        code = int(self.bad.item())
-        if code & 1:
-            raise RlDivergedError("actor or critic loss is not finite")
-        if code:
-            raise RlDivergedError("non-finite gradient in update")
+        raise_diverged(int(self.bad.item()))
 
     # -- PPO ----------------------------------------------------------------
 
@@ -1555,6 +1569,14 @@ _UPLOAD_SKIP = os.environ.get("HARL_UPLOAD_SKIP", "1") != "0"
 
 STEP_FUSED, WEIGHTS_SETTLED = 1, 2
 STEP_MLP_ONLY, STEP_SAMPLE_ONLY, VALUE_PAIRED = 4, 8, 16
+
+
+def raise_diverged(code: int) -> None:
+    """DeviceAgent.bad as ppo_update's exception (rlcore.py:368-373)."""
+    if code & 1:
+        raise RlDivergedError("actor or critic loss is not finite")
+    if code:
+        raise RlDivergedError("non-finite gradient in update")
 
 
 def policy_mlp(dsk: DeviceSketch, agent: DeviceAgent, feat, n: int,

@@ -200,15 +200,16 @@ class EpisodeResult:
     def scores(self) -> np.ndarray:
         return self.log_score[:self.visits].cpu().numpy()
 
-    def top_entries(self, k: int, exclude=None, scratch=None):
+    def top_entries(self, k: int, exclude=None, scratch=None,
+                    pending=None):
         """``rank_scores(model, entries, k, exclude)`` on the device entry
         log (costmodel.py:266-286): (visit indices ascending, host tiles
         [n, slots] u16, knobs [n, 3] u8, features [n, F] f64, scores [n],
-        stats).  See ``device.rank_topk`` for the superset contract."""
-        didx, n, stats = D.rank_topk(self.tables, self.log_tiles,
-                                     self.log_knobs, self.log_score,
-                                     self.visits, k, exclude, scratch,
-                                     sort=False)
+        stats).  See ``device.rank_topk`` for the superset contract.
+        ``pending``: from ``top_entries_launch`` with the same arguments."""
+        if pending is None:
+            pending = self.top_entries_launch(k, exclude, scratch)
+        didx, n, stats = D.rank_topk_finish(pending)
         t, kn, sc, _, f = D.gather_entries(self.tables, self.log_tiles,
                                            self.log_knobs, self.log_score,
                                            self.log_track, didx[:n],
@@ -239,6 +240,12 @@ class EpisodeResult:
             f, sc = pf[:n].numpy().copy(), ps[:n].numpy().copy()
         o = np.argsort(idx, kind="stable")
         return (idx[o], tiles[o], knobs[o], f[o], sc[o], stats)
+
+    def top_entries_launch(self, k: int, exclude=None, scratch=None):
+        """Queue the selection's kernels (``top_entries`` finishes)."""
+        return D.rank_topk(self.tables, self.log_tiles, self.log_knobs,
+                           self.log_score, self.visits, k, exclude, scratch,
+                           sort=False, launch_only=True)
 
     def rewards_per_step(self):
         r = self.log_reward[:self.visits].cpu().numpy()
@@ -598,13 +605,17 @@ class EpisodeEngine:
     def run_episode(self, tables: SketchTables, forest: D.DeviceForest, gen,
                     cfg: EpisodeConfig, order_counter: int = 0,
                     inject=None, record: list | None = None,
-                    cull_override=None) -> EpisodeResult:
+                    cull_override=None, defer_checks: bool = False
+                    ) -> EpisodeResult:
         """Run one episode.  ``gen`` is the session's numpy Generator
         (PCG64), advanced exactly as the reference advances it.  ``inject``
         (optional callable ``step -> (m,4) actions``) replays externally
         chosen actions; ``record`` collects per-step device tensors for
         parity checks; ``cull_override(step, own_choice)`` may replace the
-        eliminated track set (parity replays only)."""
+        eliminated track set (parity replays only).  ``defer_checks``: the
+        per-step status words and the divergence flag are copied out
+        asynchronously and checked by ``result.check()`` (the caller may
+        issue more device work first); otherwise checked before returning."""
         # (graph replays update the parameters without passing through
         # DeviceAgent.ppo_update: the host copy is stale from here on)
         self.dagent._device_is_pin = False
@@ -646,11 +657,28 @@ class EpisodeEngine:
                                   cull_override)
         else:
             res = self._run_graphed(b, gen, cfg, order_counter, cursor)
-        st = b.status.cpu().numpy().view(np.uint64)
-        PF.xfer("d2h", b.status)
-        for code in st[:len(plan)]:
-            D.raise_status(int(code))
-        self.dagent.raise_if_diverged()
+        # the status words and the divergence flag in one pinned copy-out
+        n = len(plan)
+        pin = getattr(b, "check_pin", None)
+        if pin is None:
+            pin = b.check_pin = torch.empty(max(n, 1) + 1, dtype=torch.int64,
+                                            pin_memory=True)
+        pin[:n].copy_(b.status[:n], non_blocking=True)
+        pin[n:n + 1].copy_(self.dagent.bad.to(torch.int64), non_blocking=True)
+        PF.xfer("d2h", pin)
+        ev = torch.cuda.Event()
+        ev.record()
+        words = pin[:n + 1]
+
+        def check():
+            ev.synchronize()
+            w = words.numpy()
+            for code in w[:n].view(np.uint64):
+                D.raise_status(int(code))
+            D.raise_diverged(int(w[n]))
+        res.check = check
+        if not defer_checks:
+            check()
         return res
 
     def _episode_prologue(self, b, forest):

@@ -103,8 +103,8 @@ def test_drop_in_topk_entries_rank_like_full_list(tmp_path, searcher):
     orig = dev._b200_entries
     seen = []
 
-    def spy(res, tables, sketch):
-        top = orig(res, tables, sketch)
+    def spy(res, tables, sketch, pending=None):
+        top = orig(res, tables, sketch, pending)
         dev.b200_all_entries = True
         try:
             full = orig(res, tables, sketch)

@@ -466,6 +466,15 @@ typedef struct harl_ppo_hyper {
  * applies Adam.  phase 3 = both (single device). */
 int64_t harl_ppo_scratch_bytes(int32_t B, int32_t row_stride,
                                int32_t n_jobs);
+/* phase flag: gradients and Adam in one launch without a grid barrier --
+ * each gradient tile's CTA steps its own parameters after saving their
+ * pre-update values; params, adam_m, adam_v must be rows 0-2 of one
+ * [6][n_params] block whose rows 3-5 receive that backup.  bad[0] is
+ * flagged as before and bad[1] must be writable (a per-update snapshot);
+ * when the update flags bad the caller restores rows 0-2 from rows 3-5
+ * (and the derived copies) before raising, as ppo_update steps nothing
+ * then (rlcore.py:368-375).  Single device (phase 3) only. */
+#define HARL_PPO_SPECULATIVE 8
 int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     const harl_ppo_hyper* hp, const harl_replay_ring* ring,
                     const int32_t* idx, int32_t B, int32_t feature_len,

@@ -1922,7 +1922,20 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
                     void* val_trunk_img, double* wt_params, int32_t B_norm,
                     int32_t phase, void* stream) {
   if (B_norm <= 0) B_norm = B;
+  // HARL_PPO_SPECULATIVE: gradients + Adam in one launch (k_ppo_wgrad_spec);
+  // the pre-update values go to the backup block behind params/m/v
+  const bool spec = (phase & HARL_PPO_SPECULATIVE) != 0;
+  phase &= 3;
   if (phase < 1 || phase > 3) phase = 3;
+  if (spec && phase != 3) {
+    set_error("harl_ppo_update: the speculative update is single-device (phase 3)");
+    return HARL_E_ARG;
+  }
+  if (spec && (adam_m != params + n_params || adam_v != params + 2 * n_params)) {
+    set_error("harl_ppo_update: the speculative update needs params, m, v and "
+              "the backup as consecutive [n_params] rows of one block");
+    return HARL_E_ARG;
+  }
   if (!pol || !val || !hp || !ring || B < 0 || n_head0 < 1 ||
       n_head0 > HARL_MAX_HEAD0 || pol->n_layers < 1 ||
       pol->n_layers > HARL_MAX_LAYERS || val->n_layers < 2 ||
@@ -1952,6 +1965,7 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   a.clip_hi = 1.0 + hp->clip_ratio;
   a.w_ent = hp->entropy_weight;
   a.w_val = hp->value_loss_weight;
+  a.bad = spec ? bad : nullptr;
   for (int j = 0; j < n_head0; ++j) a.head0_src[j] = head0_src_host[j];
   TransPlan tplan;
   build_trans_plan(*pol, *val, &tplan, &a);
@@ -2061,6 +2075,16 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   jt.n = n_jobs;
   // one extra CTA sums the per-row loss terms (and, on a single device,
   // forms the means and checks them) alongside the gradient tiles
+  if (spec) {
+    HARL_PROF_BEGIN(st);
+    launch_k(k_ppo_wgrad_spec, dim3((unsigned)n_tiles + 1), dim3(256), 0, st, jt, B,
+             row_stride, (const double*)rows, grads, bad, (const double*)rowout, losses,
+             B_norm, hp->entropy_weight, hp->value_loss_weight, ad, adam_dev, params,
+             adam_m, adam_v, params32, params + 3 * n_params);
+    HARL_PROF_UNITS(B);
+    HARL_CHECK_LAUNCH("k_ppo_wgrad_spec");
+    return HARL_OK;
+  }
   if (phase == 3 && fused_wgrad_adam_ok(n_tiles + 1)) {
     // gradients and Adam in one cooperative launch (grid barrier between)
     unsigned int* barw = nullptr;

@@ -156,6 +156,8 @@ k_ppo_rows_cl(const __grid_constant__ PpoArgs a,
   // ---- weight slices and the cluster's X rows (the ring rows come from
   // the preceding step kernels: everything follows the PDL wait) ---------
   griddep_wait();
+  if (a.bad && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    a.bad[1] = a.bad[0];   // the speculative Adam's per-update snapshot
   dbg_ts(40);
   // asynchronous 8-byte copies (no register staging, every load in flight
   // at once; rows of Wh / X need not be 16-byte aligned); padding is stored

@@ -28,6 +28,8 @@ struct PpoArgs {
   int64_t wt_head, wt_P[HARL_MAX_LAYERS], wt_V[HARL_MAX_LAYERS];
   int32_t B_norm;           // batch size in the 1/B normalisation (global)
   double clip_lo, clip_hi, w_ent, w_val;
+  int32_t* bad;             // optional: bad[1] = bad[0] at the update's start
+                            // (the speculative Adam's skip decision)
   int16_t head0_src[HARL_MAX_HEAD0];
 };
 
@@ -205,6 +207,8 @@ k_ppo_rows(const __grid_constant__ PpoArgs a, const __grid_constant__ NetLayout 
   // share only X, so their chains run side by side in separate CTAs
   const int role = blockIdx.y;
   const int r0 = blockIdx.x * PPO_TM;
+  // (nothing sets bad before this update's wgrad launch: a stable snapshot)
+  if (a.bad && blockIdx.x == 0 && role == 0 && threadIdx.x == 0) a.bad[1] = a.bad[0];
   const int nrows = min(PPO_TM, a.B - r0);
   const int RS = a.row_stride;
   double* base = srows;  // this CTA's rows, copied out at the end
@@ -479,6 +483,7 @@ k_ppo_rows_tc(const __grid_constant__ PpoArgs a,
   extern __shared__ double srows[];
   const int role = blockIdx.y;   // 0 policy chain, 1 value chain
   const int r0 = blockIdx.x * PPO8_ROWS;
+  if (a.bad && blockIdx.x == 0 && role == 0 && threadIdx.x == 0) a.bad[1] = a.bad[0];
   const int nrows = min(PPO8_ROWS, a.B - r0);
   const int RS = a.row_stride;
   double* base = srows;
@@ -748,10 +753,16 @@ struct GradJobs {
 // a CTA stages its 16 A columns and 16 D columns for 256 rows at a time
 // with all loads in flight.  check_finite: flag non-finite gradients here
 // (rlcore.py:368-373) so no separate scan is needed on a single device.
+struct WgNoEpi {
+  __device__ void operator()(int64_t, double, bool) const {}
+};
+
+template <typename Epi = WgNoEpi>
 __device__ __forceinline__ void wgrad_body(
     const GradJobs& jt, int B, int RS, const double* __restrict__ rows,
     double* grads, int32_t* bad, int check_finite, const double* rowout,
-    double* losses, int means_B, double w_ent, double w_val) {
+    double* losses, int means_B, double w_ent, double w_val,
+    const Epi& epi = Epi()) {
   dbg_ts(54);
   if (blockIdx.x == gridDim.x - 1) {   // the extra CTA: loss sums/means
     if (threadIdx.x < 32) ppo_losses_warp(B, rowout, losses, means_B, w_ent, w_val, bad);
@@ -845,8 +856,11 @@ __device__ __forceinline__ void wgrad_body(
   const double acc = acc1;
   const int i = i0 + ti, j = j0 + tj;
   if (i < ni && j < jb.nj) {
-    grads[jb.g_off + (int64_t)i * jb.nj + j] = acc;
-    if (check_finite && !isfinite(acc)) atomicOr(bad, 2);
+    const int64_t gi = jb.g_off + (int64_t)i * jb.nj + j;
+    grads[gi] = acc;
+    const bool fin = isfinite(acc);
+    if (check_finite && !fin) atomicOr(bad, 2);
+    epi(gi, acc, fin);
   }
 }
 
@@ -921,6 +935,12 @@ __global__ void k_wt_fill(TransPlan tp, const double* params, double* wt) {
   }
 }
 
+__device__ __forceinline__ void adam_one(const AdamArgs& a, double b1t_pi,
+                                         double b2t_pi, double b1t_v,
+                                         double b2t_v, int64_t i, double g,
+                                         double* params, double* m, double* v,
+                                         float* params32);
+
 __device__ __forceinline__ void adam_body(const AdamArgs& a,
                                           const double* adam_dev,
                                           const double* grads, double* params,
@@ -935,12 +955,24 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a,
     b2t_v = adam_dev[3];
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+       i += (int64_t)gridDim.x * blockDim.x)
+    adam_one(a, b1t_pi, b2t_pi, b1t_v, b2t_v, i, grads[i], params, m, v, params32);
+  dbg_ts(53);
+}
+
+// Adam.step (rlcore.py:62-71) for parameter i with gradient g, in the
+// reference's operation order, and every derived copy of it (fp32 rollout
+// value, tf32 / fp16 tcgen05 images, the backward pass's transposes)
+__device__ __forceinline__ void adam_one(const AdamArgs& a, double b1t_pi,
+                                         double b2t_pi, double b1t_v,
+                                         double b2t_v, int64_t i, double g,
+                                         double* params, double* m, double* v,
+                                         float* params32) {
+  {
     const bool pi = i < a.n_pi;
     const double lr = pi ? a.h.lr_actor : a.h.lr_critic;
     const double b1t = pi ? b1t_pi : b1t_v;
     const double b2t = pi ? b2t_pi : b2t_v;
-    const double g = grads[i];
     double mi = __dmul_rn(m[i], a.h.beta1);
     mi = __dadd_rn(mi, __dmul_rn(a.h.one_m_beta1, g));
     double vi = __dmul_rn(v[i], a.h.beta2);
@@ -986,7 +1018,6 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a,
         }
       }
   }
-  dbg_ts(53);
 }
 
 __global__ void k_ppo_adam(const __grid_constant__ AdamArgs a,
@@ -1046,6 +1077,63 @@ k_ppo_wgrad_adam(const __grid_constant__ GradJobs jt, int B, int RS,
   grid_barrier(bar, bar + 1);
   if (*(volatile int32_t*)bad) return;
   adam_body(a, adam_dev, grads, params, m, v, params32);
+}
+
+// (c)+(d) speculatively, no grid barrier: each gradient tile's CTA applies
+// Adam to its own parameters as soon as their gradients are summed (a
+// parameter's gradient is one thread's complete in-order sum over the
+// batch), after saving their pre-update values (params / m / v) into the
+// backup block.  The reference steps nothing when any loss or gradient is
+// non-finite (ppo_update raises first, rlcore.py:368-375): here the update
+// flags `bad` as before, tiles with a finite gradient have already
+// stepped, and the host restores the whole backup before raising
+// (DeviceAgent.restore_diverged).  Updates after a flagged one skip
+// entirely: the decision reads bad[1], the snapshot of bad[0] that this
+// update's k_ppo_rows took before anything of this update could set it,
+// so every CTA of the flagged update itself backs up and steps alike.
+struct WgSpecEpi {
+  const AdamArgs* a;
+  double b1t_pi, b2t_pi, b1t_v, b2t_v;
+  bool skip;
+  double* params;
+  double* m;
+  double* v;
+  float* params32;
+  double* bk;   // [3][n]: params, m, v before this update
+  __device__ void operator()(int64_t i, double g, bool fin) const {
+    if (skip || i >= a->n) return;
+    const int64_t n = a->n;
+    bk[i] = params[i];
+    bk[n + i] = m[i];
+    bk[2 * n + i] = v[i];
+    if (fin) adam_one(*a, b1t_pi, b2t_pi, b1t_v, b2t_v, i, g, params, m, v, params32);
+  }
+};
+
+__global__ void __launch_bounds__(256)
+k_ppo_wgrad_spec(const __grid_constant__ GradJobs jt, int B, int RS,
+                 const double* __restrict__ rows, double* grads, int32_t* bad,
+                 const double* rowout, double* losses, int means_B,
+                 double w_ent, double w_val, const __grid_constant__ AdamArgs a,
+                 const double* adam_dev, double* params, double* m, double* v,
+                 float* params32, double* bk) {
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  WgSpecEpi e;
+  e.a = &a;
+  e.b1t_pi = adam_dev ? adam_dev[0] : a.h.b1t_pi;
+  e.b2t_pi = adam_dev ? adam_dev[1] : a.h.b2t_pi;
+  e.b1t_v = adam_dev ? adam_dev[2] : a.h.b1t_v;
+  e.b2t_v = adam_dev ? adam_dev[3] : a.h.b2t_v;
+  e.skip = bad[1] != 0;
+  e.params = params;
+  e.m = m;
+  e.v = v;
+  e.params32 = params32;
+  e.bk = bk;
+  wgrad_body(jt, B, RS, rows, grads, bad, 1, rowout, losses, means_B, w_ent,
+             w_val, e);
+  griddep_trigger();
 }
 
 }  // namespace harl

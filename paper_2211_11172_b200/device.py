@@ -1104,8 +1104,10 @@ class DeviceAgent:
         self.pol_layout, self.val_layout = pl, vl
         # parameters and both Adam moments in one [3][n] block (one copy
         # each way per episode), staged through one pinned host block
-        self.pmv = torch.zeros((3, self.n_params), dtype=torch.float64,
-                               device=dev)
+        # (rows 3-5: the speculative update's pre-update backup)
+        self._pmv6 = torch.zeros((6, self.n_params), dtype=torch.float64,
+                                 device=dev)
+        self.pmv = self._pmv6[:3]
         self.params, self.m, self.v = self.pmv[0], self.pmv[1], self.pmv[2]
         self._pin = torch.empty((3, self.n_params), dtype=torch.float64,
                                 pin_memory=True)
@@ -1116,7 +1118,10 @@ class DeviceAgent:
         self.params32 = torch.zeros(self.n_params, dtype=torch.float32,
                                     device=dev)
         self.losses = torch.zeros(16, dtype=torch.float64, device=dev)
-        self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        # bad[0]: ppo_update's finiteness flags; bad[1]: the speculative
+        # update's per-update snapshot of bad[0]
+        self._badw = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.bad = self._badw[:1]
         # transposed fp64 copies for the PPO backward (kept current by Adam)
         self.wt = torch.zeros(max(1, int(N.load().harl_ppo_wt_doubles(
             C.byref(pl), C.byref(vl)))), dtype=torch.float64, device=dev)
@@ -1412,7 +1417,22 @@ class DeviceAgent:
         """ppo_update's finiteness checks (rlcore.py:368-373): the kernels
         set ``bad`` (1: a loss, 2: a gradient) and skip the Adam step; the
         host raises the reference's RlDivergedError."""
-        raise_diverged(int(self.bad.item()))
+        code = int(self.bad.item())
+        if code:
+            self.restore_diverged()
+        raise_diverged(code)
+
+    def restore_diverged(self):
+        """After a flagged speculative update (harl_ppo_update with
+        HARL_PPO_SPECULATIVE): parameters and moments back to their values
+        before it (the backup rows), derived copies rebuilt -- the state
+        the reference leaves when ppo_update raises before stepping."""
+        if not getattr(self, "_spec_used", False):
+            return
+        self.pmv.copy_(self._pmv6[3:])
+        self.params32.copy_(self.params)
+        self.refresh_derived()
+        self._device_is_pin = False
 
     # -- PPO ----------------------------------------------------------------
 
@@ -1442,8 +1462,12 @@ class DeviceAgent:
         if losses is None:
             losses = self.losses
         src = self.head0_src.ctypes.data_as(C.c_void_p)
+        # speculative gradients + Adam (single device, not the cooperative
+        # variant); the backup restores a flagged update (restore_diverged)
+        spec = _PPO_SPEC and phase == 3 and \
+            os.environ.get("HARL_PPO_FUSED_ADAM") != "1"
         # (launch count from the library: 2 when wgrad and Adam run as one
-        # cooperative kernel, 3 otherwise)
+        # kernel, 3 otherwise)
         with PF.span("ppo", B, launches=None):
           N.check(lib.harl_ppo_update(
             C.byref(self.pol_layout), C.byref(self.val_layout), C.byref(hp),
@@ -1453,8 +1477,11 @@ class DeviceAgent:
             _ptr(losses), _ptr(self.bad), _ptr(scratch), _ptr(adam_dev),
             *(([_ptr(self.packed["pt"]), _ptr(self.packed["ph"]),
                 _ptr(self.packed["vt"])]) if self.tc else [None, None, None]),
-            _ptr(self.wt), int(B_norm or B), phase, _stream()),
+            _ptr(self.wt), int(B_norm or B),
+            phase | (PPO_SPECULATIVE if spec else 0), _stream()),
             "harl_ppo_update")
+        if spec:
+            self._spec_used = True
         return losses
 
 
@@ -1569,6 +1596,10 @@ _UPLOAD_SKIP = os.environ.get("HARL_UPLOAD_SKIP", "1") != "0"
 
 STEP_FUSED, WEIGHTS_SETTLED = 1, 2
 STEP_MLP_ONLY, STEP_SAMPLE_ONLY, VALUE_PAIRED = 4, 8, 16
+PPO_SPECULATIVE = 8
+# gradients + Adam in one launch, restored on divergence
+# (HARL_PPO_SPEC=0: the separate k_ppo_wgrad + k_ppo_adam launches)
+_PPO_SPEC = os.environ.get("HARL_PPO_SPEC", "1") != "0"
 
 
 def raise_diverged(code: int) -> None:

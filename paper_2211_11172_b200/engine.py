@@ -675,6 +675,8 @@ class EpisodeEngine:
             w = words.numpy()
             for code in w[:n].view(np.uint64):
                 D.raise_status(int(code))
+            if int(w[n]):
+                self.dagent.restore_diverged()
             D.raise_diverged(int(w[n]))
         res.check = check
         if not defer_checks:

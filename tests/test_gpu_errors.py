@@ -43,9 +43,15 @@ def _ring_with_nan(tb, agent, n=64):
     return ring
 
 
+@pytest.mark.parametrize("spec", [True, False])
 @pytest.mark.parametrize("hidden", [(16,), (128, 128)])
-def test_ppo_nan_row_diverges_without_a_step(hidden):
+def test_ppo_nan_row_diverges_without_a_step(hidden, spec, monkeypatch):
+    """A NaN minibatch row: RlDivergedError and no Adam step (rlcore.py:
+    368-375), also when the update ran speculatively (gradients + Adam in
+    one launch, restored from the backup) and a later update of the same
+    episode ran before the check (it skips)."""
     from paper_2211_11172_b200 import device as D
+    monkeypatch.setattr(D, "_PPO_SPEC", spec)
     from paper_2211_11172_b200.agent import RlConfig, init_session_agents
     from paper_2211_11172_b200.errors import RlDivergedError
     sg, sk, tb = all_sketch_tables(CONV)[0]
@@ -56,8 +62,11 @@ def test_ppo_nan_row_diverges_without_a_step(hidden):
     dag = D.DeviceAgent(agent, tb.levels)
     before = dag.params.clone()
     m_before = dag.m.clone()
+    v_before = dag.v.clone()
+    p32_before = dag.params32.clone()
     slots = torch.arange(64, dtype=torch.int32, device="cuda")
     dag.ppo_update(ring, slots, cfg, 1, 1)
+    dag.ppo_update(ring, slots[1:], cfg, 2, 2)   # clean, but after the flag
     torch.cuda.synchronize()
     assert int(dag.bad.item()) != 0
     with pytest.raises(RlDivergedError):
@@ -65,6 +74,8 @@ def test_ppo_nan_row_diverges_without_a_step(hidden):
     # no Adam step: the reference raises before opt.step
     assert torch.equal(dag.params, before)
     assert torch.equal(dag.m, m_before)
+    assert torch.equal(dag.v, v_before)
+    assert torch.equal(dag.params32, p32_before)
     # a clean minibatch (row 0 left out) updates normally
     dag.bad.zero_()
     dag.ppo_update(ring, slots[1:], cfg, 1, 1)

@@ -126,19 +126,26 @@ def test_kernel_fusion_variants_match_default(monkeypatch, flag):
 
 
 
-def test_fused_wgrad_adam_matches_separate_launches():
+@pytest.mark.parametrize("env", [("HARL_PPO_FUSED_ADAM", "1", "0"),
+                                 ("HARL_PPO_SPEC", "0", "1")])
+def test_fused_wgrad_adam_matches_separate_launches(env):
     """HARL_PPO_FUSED_ADAM=1 (gradients + Adam in one cooperative kernel
-    with a grid barrier) leaves the same parameters, moments, replay ring
-    and scores as the default two launches, bit for bit."""
+    with a grid barrier) and the default speculative single launch
+    (k_ppo_wgrad_spec, HARL_PPO_SPEC=0 disables it) leave the same
+    parameters, moments, replay ring and scores as the two launches, bit
+    for bit."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     script = os.path.join(here, "_episode_digest.py")
     out = []
-    for flag in ("0", "1"):
-        env = dict(os.environ, HARL_PPO_FUSED_ADAM=flag)
-        r = subprocess.run([sys.executable, script], env=env, text=True,
+    name, on, off = env
+    for flag in (off, on):
+        env_ = dict(os.environ, HARL_PPO_SPEC="0") \
+            if name == "HARL_PPO_FUSED_ADAM" else dict(os.environ)
+        env_[name] = flag
+        r = subprocess.run([sys.executable, script], env=env_, text=True,
                            capture_output=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         out.append(r.stdout.strip().splitlines()[-1])

@@ -60,6 +60,27 @@ __device__ __forceinline__ float tanh_1mufu(float x) {
   return copysignf(fmaf(-e, r, 1.f), x);
 }
 
+// tanh with two MUFU ops and three other instructions: e = 2^(2x log2 e),
+// tanh = 1 - 2 / (e + 1) with rcp.approx (|error| <= ~3e-7, near x = 0
+// from the cancellation; +-1 exactly for |x| > 44, NaN propagates).  The
+// hidden epilogues alternate it with tanh_1mufu over their columns: one
+// is bound by the MUFU pipe (16 ops/clk/SM), the other by issue slots,
+// and the mix keeps both below the single-formula bound.
+#ifndef HARL_TANH_MIX
+#define HARL_TANH_MIX 1
+#endif
+__device__ __forceinline__ float tanh_2mufu(float x) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * 2.8853900817779268f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+  return fmaf(-2.0f, r, 1.0f);
+}
+template <int J>
+__device__ __forceinline__ float tanh_mix(float x) {
+  if (HARL_TANH_MIX && (J & 1) == 0) return tanh_2mufu(x);
+  return tanh_1mufu(x);
+}
+
 // (x0, x1) -> fp16 hi/lo pair words for two consecutive K elements:
 // hi = fp16(x) (RN), lo = fp16(x - hi) (x - hi is exact in fp32)
 __device__ __forceinline__ void split16x2(float x0, float x1, uint32_t& hi,
@@ -101,10 +122,18 @@ __device__ __forceinline__ void f16_hidden(uint32_t t_d, uint32_t a_hi,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float4 bb = b4[j];
-      const float z0 = tanh_1mufu(fmaf(v[4 * j], inv, bb.x));
-      const float z1 = tanh_1mufu(fmaf(v[4 * j + 1], inv, bb.y));
-      const float z2 = tanh_1mufu(fmaf(v[4 * j + 2], inv, bb.z));
-      const float z3 = tanh_1mufu(fmaf(v[4 * j + 3], inv, bb.w));
+      float z0, z1, z2, z3;
+      if (j & 1) {
+        z0 = tanh_mix<1>(fmaf(v[4 * j], inv, bb.x));
+        z1 = tanh_mix<1>(fmaf(v[4 * j + 1], inv, bb.y));
+        z2 = tanh_mix<1>(fmaf(v[4 * j + 2], inv, bb.z));
+        z3 = tanh_mix<1>(fmaf(v[4 * j + 3], inv, bb.w));
+      } else {
+        z0 = tanh_mix<0>(fmaf(v[4 * j], inv, bb.x));
+        z1 = tanh_mix<0>(fmaf(v[4 * j + 1], inv, bb.y));
+        z2 = tanh_mix<0>(fmaf(v[4 * j + 2], inv, bb.z));
+        z3 = tanh_mix<0>(fmaf(v[4 * j + 3], inv, bb.w));
+      }
       split16x2(z0, z1, h[2 * j], l[2 * j]);
       split16x2(z2, z3, h[2 * j + 1], l[2 * j + 1]);
     }
@@ -377,7 +406,9 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
           float acc = 0.f;
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            acc = fmaf(tanh_1mufu(fmaf(v[c], inv2, b2[c])), w3[c], acc);
+            acc = fmaf((c & 4) ? tanh_mix<1>(fmaf(v[c], inv2, b2[c]))
+                               : tanh_mix<0>(fmaf(v[c], inv2, b2[c])),
+                       w3[c], acc);
           part[(s * 4 + g) * 128 + lrow] = acc;
           // the quarter's four column groups (warps q, q+4, q+8, q+12)
           asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");

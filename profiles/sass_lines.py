@@ -39,7 +39,9 @@ def main():
     iss = hdr.index("Warp Stall Sampling (All Samples)")
     data, seen = [], set()
     for r in rows[2:]:
-        if r[ia] in seen:
+        if r and r[0] == "Kernel Name":   # the next kernel of the capture
+            break
+        if len(r) <= max(ia, iex, iss) or r[ia] in seen:
             continue
         seen.add(r[ia])
         data.append((int(r[iex] or 0), int(r[iss] or 0), r[isrc]))

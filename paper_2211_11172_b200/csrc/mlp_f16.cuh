@@ -273,16 +273,9 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
   const int64_t mine_u = units > blockIdx.x ? (units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t mine = a.pair ? 2 * mine_u : mine_u;
   const int64_t cnt0 = (mine + 1) / 2, cnt1 = mine / 2;   // tiles per slot
-  // global event e -> (slot, slot-tile, layer); slot 1 lags one stage
+  // global event e -> slot s = e % 2, slot step k = e / 2 - s (slot 1 lags
+  // one stage), tile k / NL, layer k % NL
   const int64_t n_ev = 2 * (NL * cnt0 + 1) + 2;
-  auto event = [&](int64_t e, int& s, int64_t& st, int& l) -> bool {
-    s = (int)(e & 1);
-    const int64_t k = (e >> 1) - s;
-    if (k < 0) return false;
-    st = k / NL;
-    l = (int)(k % NL);
-    return st < (s ? cnt1 : cnt0);
-  };
   if (warp == 0) tc::tmem_alloc(&tbase, 512);
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) tc::mbar_init(&wbar[i], 1);
@@ -354,10 +347,33 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
     const bool prof = g_dbg_on == 3 && blockIdx.x == 0 && warp == 0;
     unsigned long long c_wait = 0, c_hid = 0, c_out = 0, n_evt = 0;
     const unsigned long long c_start = clock64();
+    int ev_l0 = 0, ev_l1 = 0;           // (policy: the event order walked
+    int64_t ev_t0 = 0, ev_t1 = 0;       // with per-slot counters)
     for (int64_t e = 0; e < n_ev; ++e) {
       int s, l;
       int64_t st;
-      if (!event(e, s, st, l)) continue;
+      if constexpr (POLICY) {
+        s = (int)(e & 1);
+        if (e == 1) continue;           // slot 1 lags one stage
+        l = s ? ev_l1 : ev_l0;
+        st = s ? ev_t1 : ev_t0;
+        if (s) {
+          if (++ev_l1 == NL) { ev_l1 = 0; ++ev_t1; }
+        } else {
+          if (++ev_l0 == NL) { ev_l0 = 0; ++ev_t0; }
+        }
+        if (st >= (s ? cnt1 : cnt0)) continue;
+      } else {
+        // (the value kernel keeps the division form: the counters' extra
+        // live registers spill there)
+        (void)ev_l0; (void)ev_l1; (void)ev_t0; (void)ev_t1;
+        s = (int)(e & 1);
+        const int64_t k = (e >> 1) - s;
+        if (k < 0) continue;
+        st = k / NL;
+        l = (int)(k % NL);
+        if (st >= (s ? cnt1 : cnt0)) continue;
+      }
       const int64_t jt = 2 * st + s;
       const bool has_next = st + 1 < (s ? cnt1 : cnt0);
       const unsigned long long c0 = prof ? clock64() : 0;
@@ -528,10 +544,33 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
       copy_x(s + NXB);
       issue(s, 0);
     }
+    int ev_l0 = 0, ev_l1 = 0;           // (policy: the event order walked
+    int64_t ev_t0 = 0, ev_t1 = 0;       // with per-slot counters)
     for (int64_t e = 0; e < n_ev; ++e) {
       int s, l;
       int64_t st;
-      if (!event(e, s, st, l)) continue;
+      if constexpr (POLICY) {
+        s = (int)(e & 1);
+        if (e == 1) continue;           // slot 1 lags one stage
+        l = s ? ev_l1 : ev_l0;
+        st = s ? ev_t1 : ev_t0;
+        if (s) {
+          if (++ev_l1 == NL) { ev_l1 = 0; ++ev_t1; }
+        } else {
+          if (++ev_l0 == NL) { ev_l0 = 0; ++ev_t0; }
+        }
+        if (st >= (s ? cnt1 : cnt0)) continue;
+      } else {
+        // (the value kernel keeps the division form: the counters' extra
+        // live registers spill there)
+        (void)ev_l0; (void)ev_l1; (void)ev_t0; (void)ev_t1;
+        s = (int)(e & 1);
+        const int64_t k = (e >> 1) - s;
+        if (k < 0) continue;
+        st = k / NL;
+        l = (int)(k % NL);
+        if (st >= (s ? cnt1 : cnt0)) continue;
+      }
       const int64_t jt = 2 * st + s;
       wait_ready(s);
       if (l < NL - 1) {

@@ -1176,6 +1176,8 @@ static int value_pair_tc_impl(const harl_mlp_desc* val, const double* feat0,
                     (size_t)max_dyn_smem() ? 2 : 1;
     const size_t smem = (size_t)f16_smem_bytes(false, 0, feature_len, nxb);
     if ((rc = allow_smem(k_mlp_f16<false>, smem, "k_mlp_f16<value>"))) return rc;
+    if ((rc = allow_smem(k_mlp_f16<false, true>, smem, "k_mlp_f16<value+finish>")))
+      return rc;
     F16Args fa;
     memset(&fa, 0, sizeof(fa));
     fa.nxb = nxb;
@@ -1196,8 +1198,12 @@ static int value_pair_tc_impl(const harl_mlp_desc* val, const double* feat0,
     const int64_t tiles_n = fa.pair ? (n1 + 127) / 128
                                     : (n0 + 127) / 128 + (fa.n1 + 127) / 128;
     HARL_PROF_BEGIN((cudaStream_t)stream);
-    launch_k(k_mlp_f16<false>, dim3(tc16_grid(tiles_n)), dim3(F16_THREADS), smem,
-             (cudaStream_t)stream, fa, fin ? *fin : nofin);
+    if (fin)
+      launch_k(k_mlp_f16<false, true>, dim3(tc16_grid(tiles_n)), dim3(F16_THREADS), smem,
+               (cudaStream_t)stream, fa, *fin);
+    else
+      launch_k(k_mlp_f16<false, false>, dim3(tc16_grid(tiles_n)), dim3(F16_THREADS), smem,
+               (cudaStream_t)stream, fa, nofin);
     HARL_PROF_UNITS(n0 + fa.n1);
     if (fin) HARL_CHECK_LAUNCH("k_mlp_f16<value+finish>");
     else HARL_CHECK_LAUNCH("k_mlp_f16<value>");

@@ -254,7 +254,7 @@ __device__ __forceinline__ void f16_stage_x(const double* xs, int rows, int F,
 // groups copy the tile's pushed X / X' rows into their replay slots.
 // Without a.pair (V(X) reused from the previous step: n0 = 0) V(X) comes
 // from the earlier launch.
-template <bool POLICY>
+template <bool POLICY, bool FIN = false>
 __global__ void __launch_bounds__(F16_THREADS, 1)
 k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
   extern __shared__ __align__(1024) uint8_t smf[];
@@ -434,7 +434,7 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
                 ((pp[lrow] + pp[128 + lrow]) + (pp[256 + lrow] + pp[384 + lrow])) +
                 __ldg(a.b3);
           }
-          if (a.fin && sec) {   // X' tile: V(X) and V(X') of its rows are in
+          if (FIN && sec) {     // X' tile: V(X) and V(X') of its rows are in
             const int64_t wpos = fin.wpos_dev ? *fin.wpos_dev : fin.a.wpos;
             if (g == 0) {       // memory, written by this thread or earlier
               if (lrow < rows)

@@ -1,9 +1,10 @@
 #!/bin/bash
-# Round-2 v3 measurement pass on one B200 (repo root, under gpurun):
+# Round-2 measurement pass on one B200 (repo root, under gpurun):
 # bench lines, launch list and --set full capture of the C2 step kernels,
-# the population sweep and the probes.  Outputs in gpurun_out/r2v3/.
+# --set full of the MLP kernels at C3 64 K / C5 1 M, the population sweep
+# and the probes.  Outputs in gpurun_out/${TAG:-r2v3}/.
 set -u
-O=gpurun_out/r2v3
+O=gpurun_out/${TAG:-r2v3}
 mkdir -p $O
 NCU=/usr/local/cuda/bin/ncu
 EPI='regex:k_(mlp_f16|sample|gbt|ppo|featurize|gather|init|finish)'
@@ -26,6 +27,15 @@ timeout 1200 $NCU --set full --clock-control none --import-source on \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extra > $O/full_c2.log 2>&1
 $NCU -i $O/full_c2.ncu-rep --page raw --csv > $O/full_c2.raw.csv 2>/dev/null
 rm -f $O/full_c2.ncu-rep
+for c in "c3 65536" "c5 1048576"; do
+  set -- $c
+  timeout 900 $NCU --set full --clock-control none --import-source on \
+    -k regex:"k_mlp_f16" --launch-skip 2 --launch-count 2 \
+    -o $O/full_mlp_$1 -f python profiles/mlp_probe.py --config $1 --rows $2 --reps 2 \
+    > $O/full_mlp_$1.log 2>&1
+  $NCU -i $O/full_mlp_$1.ncu-rep --page raw --csv > $O/full_mlp_$1.raw.csv 2>/dev/null
+  rm -f $O/full_mlp_$1.ncu-rep
+done
 for P in 1024 16384 65536 262144 1048576; do
   timeout 600 python bench.py --config c5 --population $P --steps 5 --warmup 3 \
     --no-cpu-baseline --no-extra > $O/c5_$P.json 2> $O/c5_$P.err

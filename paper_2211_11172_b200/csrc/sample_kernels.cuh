@@ -53,6 +53,8 @@ struct SampleArgs {
   const int32_t* grow;   // optional: global row of each local row (shards)
   int64_t m_total;       // rows drawn this step over all shards
   const PcgTab* pcg_tab; // optional byte-sliced jump table of the stream
+  int32_t prefill;       // launched with PDL: stage the constant tables
+                         // before the programmatic-dependency wait
 };
 
 __device__ inline float gmaxf(float v) {
@@ -159,6 +161,22 @@ __device__ inline void foot_fill(const harl_sketch_desc& sk, FootSmem* fs,
     for (int v = threadIdx.x; v < lut_n; v += blockDim.x) lut_s[v] = __ldg(sk.log2_lut + v);
 }
 
+// the CTA's constant tables: compact head-0 column -> (src, dst) slots,
+// footprint terms, log2 LUT (from the descriptor's device copy when there
+// is one: coalesced loads, not per-thread constant-bank reads that
+// serialise by address)
+__device__ inline void sample_fill(const harl_sketch_desc& sk, int16_t* s_src,
+                                   int16_t* s_dst, FootSmem* fs, double* lut_s,
+                                   int lut_n) {
+  const harl_sketch_desc& sg = sk.dev_self ? *sk.dev_self : sk;
+  for (int i = threadIdx.x; i < sk.n_head0; i += blockDim.x) {
+    const int16_t vs = sg.head0_src[i], vd = sg.head0_dst[i];
+    s_src[i] = vs;
+    s_dst[i] = vd;
+  }
+  if (fs) foot_fill(sg, fs, lut_s, lut_n);
+}
+
 // inject mode (parity replays): lane 0 scores the given actions; out of
 // line so the sampling path stays compact in the instruction cache
 struct InjectRow {
@@ -261,15 +279,8 @@ __device__ __forceinline__ void sample_group(
     dbg_ts(38);
     // the CTA's head-0 column tables, filled while the row loads above are
     // in flight (the caller passes this CTA's shared arrays)
-    // (from the descriptor's device copy when there is one: coalesced
-    // loads, not per-thread constant-bank reads that serialise by address)
-    const harl_sketch_desc& sg = sk.dev_self ? *sk.dev_self : sk;
-    for (int i = threadIdx.x; i < C0; i += blockDim.x) {
-      const int16_t vs = sg.head0_src[i], vd = sg.head0_dst[i];
-      const_cast<int16_t*>(s_src)[i] = vs;
-      const_cast<int16_t*>(s_dst)[i] = vd;
-    }
-    if (fs) foot_fill(sg, fs, lut_s, lut_n);
+    sample_fill(sk, const_cast<int16_t*>(s_src), const_cast<int16_t*>(s_dst),
+                fs, lut_s, lut_n);
     dbg_ts(39);
     __syncthreads();
     dbg_ts(36);
@@ -540,10 +551,6 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
               const u128* base_dev, const uint16_t* __restrict__ tiles,
               const uint8_t* __restrict__ knobs, SampleArgs a,
               double* __restrict__ feat_out) {
-  griddep_wait();  // PDL: predecessors complete and visible
-  griddep_launch();
-  dbg_ts(16);
-  dbg_grid(false, 60);
   constexpr int ROWS = SAMPLE_THREADS / SG;
   __shared__ int16_t s_src[HARL_MAX_HEAD0], s_dst[HARL_MAX_HEAD0];
   __shared__ uint16_t s_st[FEAT ? ROWS : 1][HARL_MAX_SLOTS];
@@ -554,12 +561,20 @@ k_sample_rows(const __grid_constant__ harl_sketch_desc sk,
   const int lut_n = sk.max_extent + 1;
   double* lut_s = (FEAT && lut_n <= FEAT_LUT_SMEM_MAX)
                       ? s_feat + (SAMPLE_THREADS / SG) * sk.feature_len : nullptr;
+  // launched with PDL: the constant tables are staged while the previous
+  // kernel drains; otherwise inside sample_group behind the row loads
+  if (a.prefill) sample_fill(sk, s_src, s_dst, FEAT ? s_foot : nullptr, lut_s, lut_n);
+  griddep_wait();  // PDL: predecessors complete and visible
+  griddep_launch();
+  if (a.prefill) __syncthreads();
+  dbg_ts(16);
+  dbg_grid(false, 60);
   const int lr = threadIdx.x / SG;
   const int64_t r0 = (int64_t)blockIdx.x * ROWS;
   const int64_t r = r0 + lr;
   sample_group<MAXI, NSL>(sk, J, base_arg, base_dev, tiles, knobs, a, r, nullptr, s_src,
                s_dst, FEAT ? s_st[lr] : nullptr, FEAT ? s_kn[lr] : nullptr,
-               /*fill_tables=*/true, FEAT ? s_foot : nullptr, lut_s, lut_n);
+               /*fill_tables=*/!a.prefill, FEAT ? s_foot : nullptr, lut_s, lut_n);
   dbg_ts(23);
   if (FEAT) {
     const int g = threadIdx.x & (SG - 1);

@@ -276,6 +276,7 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
   // global event e -> slot s = e % 2, slot step k = e / 2 - s (slot 1 lags
   // one stage), tile k / NL, layer k % NL
   const int64_t n_ev = 2 * (NL * cnt0 + 1) + 2;
+  if (POLICY) dbg_ts(0);
   if (warp == 0) tc::tmem_alloc(&tbase, 512);
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) tc::mbar_init(&wbar[i], 1);
@@ -286,6 +287,7 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
     }
   }
   tc_sync();
+  if (POLICY) dbg_ts(1);
   const uint32_t tm = tbase;
   const bool mma_thread = mine > 0 && warp == F16_EPI_WARPS && lane == 0;
   auto load_weights = [&]() {
@@ -339,7 +341,9 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
       tc::tmem_st_wait();
       arrive(s);
     }
+    if (POLICY) dbg_ts(2);
     tc::mbar_wait(&wbar[0], 0);           // biases and scales
+    if (POLICY) dbg_ts(3);
     const float inv1 = fl[F16_SC + 4], inv2 = fl[F16_SC + 5];
     uint32_t ph = 0;                      // bit s: done[s] parity
     // phase accounting (harl_debug_timestamps(3): CTA 0, warp 0 -> slots
@@ -378,6 +382,7 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
       const bool has_next = st + 1 < (s ? cnt1 : cnt0);
       const unsigned long long c0 = prof ? clock64() : 0;
       tc::mbar_wait(&done[s], (ph >> s) & 1u);
+      if (POLICY && e == 0) dbg_ts(6);
       ph ^= 1u << s;
       tc::fence_after();
       const unsigned long long c1 = prof ? clock64() : 0;
@@ -494,7 +499,6 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
     }
   } else if (mma_thread) {
     // ---------------- MMA / copy issuing thread --------------------------
-    if (!a.early_w) load_weights();
     auto copy_x = [&](int64_t jt) {       // tile jt -> buffer jt % NXB
       if (jt >= mine) return;
       const double* f;
@@ -506,7 +510,12 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
       tc::bulk_f64((double*)(xsm + b * xbb), f + r0 * a.F,
                    (uint32_t)rows * a.F, &xfull[b]);
     };
+    // the first X tiles ahead of the weight image (the epilogue warps
+    // convert them while the image streams in), then the image in three
+    // pieces: W1 + biases, W2, heads -- each layer's first MMA waits for
+    // its own piece only
     for (int64_t jt = 0; jt < NXB; ++jt) copy_x(jt);
+    if (!a.early_w) load_weights();
     const uint32_t sw = tc::smem_u32(smf);
     const uint32_t id_h = tc::idesc_f16(128, TC_H);
     const uint32_t id_o = tc::idesc_f16(128, POLICY ? a.NHP : TC_H);
@@ -521,6 +530,8 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
       if (prof) c_wait += clock64() - c0;
     };
     auto issue = [&](int s, int l) {
+      if (l > 0) tc::mbar_wait(&wbar[l], 0);   // that layer's weights (once
+                                              // complete, an immediate test)
       const unsigned long long c0 = prof ? clock64() : 0;
       const uint32_t d = tm + 256 * s, ah = d + 128;
       if (l == 0)
@@ -536,14 +547,26 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
       if (prof) c_iss += clock64() - c0;
     };
     tc::mbar_wait(&wbar[0], 0);
-    tc::mbar_wait(&wbar[1], 0);
-    if (POLICY) tc::mbar_wait(&wbar[2], 0);
+#ifdef HARL_PHASE_TS
+    if (POLICY && blockIdx.x == 0 && g_dbg_on) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_dbg_ts[4] = t;
+    }
+#endif
     // prologue: the slots' first tiles are staged (tile s converted)
     for (int s = 0; s < 2 && s < mine; ++s) {
       wait_ready(s);
       copy_x(s + NXB);
       issue(s, 0);
     }
+#ifdef HARL_PHASE_TS
+    if (POLICY && blockIdx.x == 0 && g_dbg_on) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_dbg_ts[5] = t;
+    }
+#endif
     int ev_l0 = 0, ev_l1 = 0;           // (policy: the event order walked
     int64_t ev_t0 = 0, ev_t1 = 0;       // with per-slot counters)
     for (int64_t e = 0; e < n_ev; ++e) {
@@ -585,9 +608,11 @@ k_mlp_f16(F16Args a, const __grid_constant__ GbtFinishArgs fin) {
       g_dbg_ts[37] = c_iss;
     }
   }
+  if (POLICY) dbg_ts(9);
   griddep_trigger();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tm, 512);
+  if (POLICY) dbg_ts(10);
 }
 
 // ---------------------------------------------------------------------------

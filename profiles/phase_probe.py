@@ -16,8 +16,8 @@ from paper_2211_11172_b200 import _native as N  # noqa: E402
 from paper_2211_11172_b200 import device as D  # noqa: E402
 from paper_2211_11172_b200.engine import EpisodeConfig, EpisodeEngine  # noqa: E402
 
-NAMES = ["start", "init", "x_staged", "w1_ready", "mma1", "epi1", "mma2",
-         "epi2", "heads_ready", "mma_heads", "end"]
+NAMES = ["start", "init", "x_staged", "bias_ready", "mma_weights_ready",
+         "first_issue", "first_done", "-", "-", "loop_end", "end"]
 SNAMES = ["start", "rng", "state", "softmax", "cdf", "shift_heads", "decided", "end"]
 GNAMES = ["start", "x0", "walk0", "sum0", "x1", "walk1", "sum1"]
 FNAMES = ["start", "staged", "rows", "end"]

@@ -319,6 +319,9 @@ def b200_session_class(base):
                 eng.dagent.download_async()
                 pending = self._b200_entries_launch(res, tables, sketch)
                 getattr(res, "check", lambda: None)()
+                # the checks passed: the numpy lists are written on the host
+                # pool while the entry list is built
+                eng.dagent.download_start_unpack()
             except (ValueError, RuntimeError) as exc:
                 ref = to_reference(exc)
                 if ref is None:

@@ -1250,19 +1250,41 @@ class DeviceAgent:
                 "harl_agent_copy")
         return True
 
+    def _lists(self):
+        a = self.agent
+        return ((a.policy, a.value), (a.opt_pi.m, a.opt_v.m),
+                (a.opt_pi.v, a.opt_v.v))
+
     def _host_matches_pin(self) -> bool:
         """The numpy parameters and moments equal, bit for bit, the pinned
-        block (False when a list cannot be compared natively)."""
-        a = self.agent
+        block (False when a list cannot be compared natively).  The three
+        compares run on the host pool's threads (ctypes releases the GIL)."""
         lib = N.load()
-        for i, (pol, val) in enumerate(((a.policy, a.value),
-                                        (a.opt_pi.m, a.opt_v.m),
-                                        (a.opt_pi.v, a.opt_v.v))):
-            plan = self._copy_plan(pol, val)
-            if plan is None or lib.harl_agent_copy(
-                    plan[0], plan[1], self._pin_np[i].ctypes.data, 2) != 0:
-                return False
-        return True
+        plans = [self._copy_plan(pol, val) for pol, val in self._lists()]
+        if any(p is None for p in plans):
+            return False
+
+        def cmp(i):
+            return lib.harl_agent_copy(plans[i][0], plans[i][1],
+                                       self._pin_np[i].ctypes.data, 2) == 0
+        if not _POOL_ON:
+            return all(cmp(i) for i in range(3))
+        return all(_host_pool().map(cmp, range(3)))
+
+    def _unpack_all(self):
+        """The pinned block -> the numpy lists (native plans, the three
+        lists on the host pool's threads; numpy copies where no plan)."""
+        pin, vw = self._pin_np, self._pin_views
+        lists = self._lists()
+
+        def one(i):
+            pol, val = lists[i]
+            return self._native_copy(pin[i], pol, val, True)
+        done = list(_host_pool().map(one, range(3))) if _POOL_ON else \
+            [one(i) for i in range(3)]
+        for i, ok in enumerate(done):
+            if not ok:
+                self._unpack_into(pin[i], *lists[i], vw[i])
 
     def _pack(self, pol_list, val_list, out=None, views=None) -> np.ndarray:
         """The numpy lists -> the flat layout (every element written)."""
@@ -1356,25 +1378,42 @@ class DeviceAgent:
             self._dl_done.record()
         self.pmv.record_stream(side)
 
+    def download_start_unpack(self):
+        """After ``download_async``: wait for the copy and write the numpy
+        lists on the host pool (the caller keeps working; ``download``
+        joins).  Call only when nothing else touches the lists meanwhile."""
+        dl = getattr(self, "_dl_done", None)
+        if dl is None:
+            return
+        self._dl_done = None
+
+        if not _POOL_ON:
+            self._dl_done = dl       # download() finishes it in line
+            return
+
+        def job():
+            dl.synchronize()
+            self._unpack_all()
+        self._unpack_job = _host_pool().submit(job)
+
     def download(self):
         """Write device params and moments back into the numpy lists."""
-        a = self.agent
-        dl = getattr(self, "_dl_done", None)
-        if dl is not None:        # started by download_async
-            self._dl_done = None
-            dl.synchronize()
+        job = getattr(self, "_unpack_job", None)
+        if job is not None:       # started by download_start_unpack
+            self._unpack_job = None
+            job.result()
         else:
-            if self._pin_done is not None:
-                self._pin_done.synchronize()
-            self._pin.copy_(self.pmv, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            dl = getattr(self, "_dl_done", None)
+            if dl is not None:    # started by download_async
+                self._dl_done = None
+                dl.synchronize()
+            else:
+                if self._pin_done is not None:
+                    self._pin_done.synchronize()
+                self._pin.copy_(self.pmv, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            self._unpack_all()
         self._pin_done = None
-        pin, vw = self._pin_np, self._pin_views
-        for i, (pol, val) in enumerate(((a.policy, a.value),
-                                        (a.opt_pi.m, a.opt_v.m),
-                                        (a.opt_pi.v, a.opt_v.v))):
-            if not self._native_copy(pin[i], pol, val, True):
-                self._unpack_into(pin[i], pol, val, vw[i])
         self._device_is_pin = True
         PF.xfer("d2h", self.pmv)
 
@@ -1600,6 +1639,22 @@ PPO_SPECULATIVE = 8
 # gradients + Adam in one launch, restored on divergence
 # (HARL_PPO_SPEC=0: the separate k_ppo_wgrad + k_ppo_adam launches)
 _PPO_SPEC = os.environ.get("HARL_PPO_SPEC", "1") != "0"
+
+
+_POOL = None
+# HARL_HOST_POOL=0: the agent copies run in line on the calling thread
+_POOL_ON = os.environ.get("HARL_HOST_POOL", "1") != "0"
+
+
+def _host_pool():
+    """A small persistent host thread pool for the native agent copies
+    (ctypes releases the GIL, so the three lists copy in parallel)."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=3,
+                                   thread_name_prefix="harl-agent")
+    return _POOL
 
 
 def raise_diverged(code: int) -> None:

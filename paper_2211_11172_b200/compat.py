@@ -382,7 +382,11 @@ def b200_session_class(base):
             # (schedspace.py:117-120), from the same Python ints
             states, texts = tables.states_from_arrays(
                 tiles, knobs, ScheduleState, canonical=True)
-            return [CandidateEntry(canonical=c, features=f, state=s, order=o)
+            from .space import fast_dataclass_maker
+            make = fast_dataclass_maker(CandidateEntry, ("canonical",
+                                                         "features", "state",
+                                                         "order"))
+            return [make(c, f, s, o)
                     for s, c, f, o in zip(states, texts, feats,
                                           (base + np.asarray(order, np.int64))
                                           .tolist())]

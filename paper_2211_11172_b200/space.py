@@ -115,6 +115,30 @@ def canonical_text(sketch_id, tiles, ca, par, ur) -> str:
     return f"{sketch_id}|t={t}|ca={ca}|par={par}|ur={ur}"
 
 
+def fast_dataclass_maker(cls, names):
+    """``(*values) -> cls(**dict(zip(names, values)))`` for a frozen
+    dataclass whose fields are exactly ``names`` (in order) with plain
+    ``__init__`` semantics (no ``__post_init__``, no slots, no converters):
+    the instance dict is filled directly, skipping the per-field
+    ``object.__setattr__`` of the frozen ``__init__`` (~5x cheaper; equal
+    and hash-equal objects).  Any other class gets its constructor."""
+    import dataclasses
+    ok = (dataclasses.is_dataclass(cls) and
+          not hasattr(cls, "__post_init__") and
+          "__slots__" not in cls.__dict__ and
+          tuple(f.name for f in dataclasses.fields(cls)) == tuple(names) and
+          all(f.init for f in dataclasses.fields(cls)))
+    if not ok:
+        return lambda *v: cls(**dict(zip(names, v)))
+    new = object.__new__
+
+    def make(*v):
+        o = new(cls)
+        o.__dict__.update(zip(names, v))
+        return o
+    return make
+
+
 def canonical_texts(sketch_id, tiles, knobs, levels: int) -> list:
     """``canonical_text`` of every row of (tiles [n, slots] u16, knobs
     [n, 3] u8), formatted natively (harl_format_canonical)."""
@@ -340,13 +364,14 @@ class SketchTables:
         with ``canonical``, their canonical texts as a second list)."""
         L, sk = self.levels, self.sketch_id
         out = []
+        make = fast_dataclass_maker(state_cls, ("sketch_id", "tiles",
+                                                "compute_at_index",
+                                                "parallel_fuse_count",
+                                                "unroll_index"))
         for t, k in zip(np.asarray(tiles).tolist(), np.asarray(knobs).tolist()):
             it = iter(t)
             tl = tuple(zip(*([it] * L))) if L else ()
-            out.append(state_cls(sketch_id=sk, tiles=tl,
-                                 compute_at_index=k[0],
-                                 parallel_fuse_count=k[1],
-                                 unroll_index=k[2]))
+            out.append(make(sk, tl, k[0], k[1], k[2]))
         if canonical:
             texts = canonical_texts(sk, tiles, knobs, L)
         return (out, texts) if canonical else out

@@ -1257,8 +1257,8 @@ class DeviceAgent:
 
     def _host_matches_pin(self) -> bool:
         """The numpy parameters and moments equal, bit for bit, the pinned
-        block (False when a list cannot be compared natively).  The three
-        compares run on the host pool's threads (ctypes releases the GIL)."""
+        block (False when a list cannot be compared natively).  In line: a
+        pool dispatch costs more than the three ~30 us compares."""
         lib = N.load()
         plans = [self._copy_plan(pol, val) for pol, val in self._lists()]
         if any(p is None for p in plans):
@@ -1267,9 +1267,7 @@ class DeviceAgent:
         def cmp(i):
             return lib.harl_agent_copy(plans[i][0], plans[i][1],
                                        self._pin_np[i].ctypes.data, 2) == 0
-        if not _POOL_ON:
-            return all(cmp(i) for i in range(3))
-        return all(_host_pool().map(cmp, range(3)))
+        return all(cmp(i) for i in range(3))
 
     def _unpack_all(self):
         """The pinned block -> the numpy lists (native plans, the three

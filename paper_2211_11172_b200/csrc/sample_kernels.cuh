@@ -31,6 +31,9 @@ struct LaneJump {
 #ifndef HARL_SAMPLE_MINB
 #define HARL_SAMPLE_MINB (7 * 8 * 16 / (HARL_SAMPLE_LANES * HARL_SAMPLE_ROWS))  // 72 registers: one wave of 16-row CTAs at 16 K rows, fewer spills than 64 (-1 us per launch)
 #endif
+#ifndef HARL_SAMPLE_FILL_FIRST
+#define HARL_SAMPLE_FILL_FIRST 1
+#endif
 constexpr int SG = HARL_SAMPLE_LANES;   // lanes cooperating on one row
 constexpr int SAMPLE_THREADS = HARL_SAMPLE_ROWS * SG;
 constexpr int SAMPLE_MAXI = 16;        // cached exps per lane (C0 <= 128)
@@ -237,6 +240,17 @@ __device__ __forceinline__ void sample_group(
   const int64_t rr = live ? r : 0;
   const int S = sk.num_slots, C0 = sk.n_head0;
   const bool draw = !a.inject && g < 4;
+#if HARL_SAMPLE_FILL_FIRST
+  // the CTA's constant tables first: holding the row loads (32 registers of
+  // PCG table entries among them) across the table fill spilled them, and
+  // the spill stores serialised the row loads behind their round trips
+  if (fill_tables) {
+    sample_fill(sk, const_cast<int16_t*>(s_src), const_cast<int16_t*>(s_dst),
+                fs, lut_s, lut_n);
+    __syncthreads();
+    fill_tables = false;
+  }
+#endif
   // ---- every global load of the row is issued before any math ----------
   u128 base = base_arg;
   int64_t grow_r = rr;

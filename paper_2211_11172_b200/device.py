@@ -1640,8 +1640,11 @@ _PPO_SPEC = os.environ.get("HARL_PPO_SPEC", "1") != "0"
 
 
 _POOL = None
-# HARL_HOST_POOL=0: the agent copies run in line on the calling thread
-_POOL_ON = os.environ.get("HARL_HOST_POOL", "1") != "0"
+# HARL_HOST_POOL=1: the agent lists are unpacked on a host thread while the
+# entry list is built -- measured slower at C2 (e2e 6.29-6.43 vs 5.95-6.00
+# ms per call: the worker contends for the GIL with the entry building),
+# so the copies run in line by default
+_POOL_ON = os.environ.get("HARL_HOST_POOL", "0") == "1"
 
 
 def _host_pool():

@@ -258,15 +258,32 @@ __global__ void k_gather_rows(GatherArgs a, const int32_t* idx,
                               int32_t* row_track_o) {
   griddep_wait();  // PDL: predecessors complete and visible
   griddep_launch();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n_out) return;
-  const int64_t r = idx[i];
-  for (int s = 0; s < a.local_slots; ++s)
-    tiles_o[(int64_t)s * a.ld_dst + i] = tiles[(int64_t)s * a.ld_src + r];
-  for (int k = 0; k < 3; ++k) knobs_o[(int64_t)k * a.ld_dst + i] = knobs[(int64_t)k * a.ld_src + r];
-  for (int k = 0; k < a.F; ++k) feat_o[i * a.F + k] = feat[r * a.F + k];
-  score_o[i] = score[r];
-  row_track_o[i] = row_track[r];
+  // one thread per copied element (not per row: a row's ~80 dependent
+  // load/store pairs had serialised on their round trips), elements
+  // ordered so consecutive threads write consecutive addresses
+  const int64_t n = a.n_out;
+  const int S = a.local_slots, F = a.F;
+  const int64_t n_st = n * (S + 3), n_f = n * F, n_sc = 2 * n;
+  const int64_t total = n_st + n_f + n_sc;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < n_st) {                       // state: slot-major, row fastest
+      const int64_t s = e / n, i = e - s * n;
+      const int64_t r = __ldg(idx + i);
+      if (s < S) tiles_o[s * a.ld_dst + i] = tiles[s * a.ld_src + r];
+      else knobs_o[(s - S) * a.ld_dst + i] = knobs[(s - S) * a.ld_src + r];
+    } else if (e < n_st + n_f) {          // features: row-major
+      const int64_t f = e - n_st, i = f / F, k = f - i * F;
+      const int64_t r = __ldg(idx + i);
+      feat_o[f] = feat[r * F + k];
+    } else {
+      const int64_t f = e - n_st - n_f;
+      const int64_t i = f < n ? f : f - n;
+      const int64_t r = __ldg(idx + i);
+      if (f < n) score_o[i] = score[r];
+      else row_track_o[i] = row_track[r];
+    }
+  }
 }
 
 }  // namespace harl

@@ -1659,7 +1659,10 @@ int harl_gather_rows(const int32_t* idx, int64_t n_out, int32_t local_slots,
   a.local_slots = local_slots;
   a.F = feature_len;
   HARL_PROF_BEGIN((cudaStream_t)stream);
-  launch_k(k_gather_rows, dim3((unsigned)((n_out + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, 
+  const int64_t elems = n_out * (local_slots + 3 + feature_len + 2);
+  int64_t gblocks = (elems + 255) / 256;
+  if (gblocks > 8 * sm_count()) gblocks = 8 * sm_count();
+  launch_k(k_gather_rows, dim3((unsigned)gblocks), dim3(256), 0, (cudaStream_t)stream, 
       a, idx, tiles, knobs, feat, score, row_track, tiles_o, knobs_o, feat_o,
       score_o, row_track_o);
   HARL_CHECK_LAUNCH("k_gather_rows");

@@ -2442,30 +2442,43 @@ int harl_cull_select(const double* adv, const int32_t* tracks, int64_t m,
     }
     const uint64_t cut = prefix;
     static thread_local std::vector<int32_t> tied;
+    static thread_local std::vector<uint64_t> elim;   // eliminated-track bitmap
     tied.clear();
-    // branch-free passes (the keep/go outcome is a coin flip per row)
+    elim.assign((size_t)((n_tracks + 63) / 64), 0ull);
+    // one marking pass (branch-free: the keep/go outcome is a coin flip per
+    // row); the ties at the cut are rare and collected on the side
     int64_t below = 0;
     for (int64_t r = 0; r < m; ++r) {
-      const int lt = key[r] < cut;
-      uint8_t& a = alive[tracks[r]];
-      a = (uint8_t)(a << lt);   // live (1) -> 2: marked eliminated
-      below += lt;
+      const uint64_t kk = key[r];
+      const int32_t t = tracks[r];
+      const uint64_t lt = kk < cut;
+      elim[t >> 6] |= lt << (t & 63);
+      below += (int64_t)lt;
+      if (kk == cut) tied.push_back(t);
     }
-    for (int64_t r = 0; r < m; ++r)
-      if (key[r] == cut) tied.push_back(tracks[r]);
     const int64_t need = n_elim - below;
     // the `need` highest track indices among the ties (a set: no full sort)
     if (need > 0 && need < (int64_t)tied.size())
       std::nth_element(tied.begin(), tied.begin() + (need - 1), tied.end(),
                        [](int32_t a, int32_t b) { return a > b; });
-    for (int64_t i = 0; i < need; ++i) alive[tied[i]] = 2;
-    int64_t g = 0, sink;
-    for (int64_t t = 0; t < n_tracks; ++t) {
-      const uint8_t a = alive[t];
-      *(g < n_elim ? &gone_out[g] : &sink) = t;
-      g += a == 2;
-      alive[t] = (uint8_t)(a & 1);
+    for (int64_t i = 0; i < need; ++i) elim[tied[i] >> 6] |= 1ull << (tied[i] & 63);
+    // eliminated tracks ascending straight from the bitmap
+    int64_t g = 0;
+    for (size_t w = 0; w < elim.size(); ++w)
+      for (uint64_t bw = elim[w]; bw; bw &= bw - 1) {
+        const int64_t t = (int64_t)w * 64 + __builtin_ctzll(bw);
+        if (g < n_elim) gone_out[g] = t;
+        ++g;
+        alive[t] = 0;
+      }
+    int64_t k = 0;
+    for (int64_t r = 0; r < m; ++r) {
+      const int32_t t = tracks[r];
+      keep_out[k] = (int32_t)r;
+      k += (int64_t)(((elim[t >> 6] >> (t & 63)) & 1ull) ^ 1ull);
     }
+    *n_keep = k;
+    return HARL_OK;
   }
   int64_t k = 0;
   for (int64_t r = 0; r < m; ++r) {

@@ -319,19 +319,24 @@ def b200_session_class(base):
                 eng.dagent.download_async()
                 pending = self._b200_entries_launch(res, tables, sketch)
                 getattr(res, "check", lambda: None)()
-                # the checks passed: the numpy lists are written on the host
-                # pool while the entry list is built
+                # the checks passed: the numpy lists are written now, while
+                # the GPU runs the entry selection's kernels (or, with
+                # HARL_HOST_POOL=1, on a host thread beside the entry list)
                 eng.dagent.download_start_unpack()
             except (ValueError, RuntimeError) as exc:
                 ref = to_reference(exc)
                 if ref is None:
                     raise
                 raise ref from exc
+            pooled = getattr(eng.dagent, "_unpack_job", None) is not None
+            if not pooled:
+                eng.sync_to_host()
             # the replay FIFO now lives in the device ring; the deque is
             # rebuilt only if something reads it (_RingBuffer)
             buf._on_device = True
             entries = self._b200_entries(res, tables, sketch, pending)
-            eng.sync_to_host()
+            if pooled:
+                eng.sync_to_host()
             self.order_counter += res.visits
             if self.log:
                 self._b200_log(res, rnd)

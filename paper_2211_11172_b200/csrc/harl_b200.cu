@@ -511,7 +511,9 @@ int harl_init_population(const harl_sketch_desc* sk, const harl_pcg64* rng,
     cudaError_t e = cudaMemsetAsync(bad, 0xff, 8, st);   // ULLONG_MAX
     if (e != cudaSuccess) return cuda_status(e, "init memset");
     const int64_t todo = count - a.t0;
-    const int threads = 256;
+    // 64-thread CTAs: one track per thread, and every SM gets tracks at
+    // 16 K (256-thread CTAs left most SMs idle)
+    const int threads = 64;
     HARL_PROF_BEGIN(st);
     launch_k(k_init_sample, dim3((unsigned)((todo + threads - 1) / threads)), dim3(threads), 0, st, 
         *sk, J, a, tiles, knobs, bad);

@@ -144,7 +144,10 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
 }
-constexpr int GBT_ILP = 4;               // trees walked side by side
+#ifndef HARL_GBT_ILP
+#define HARL_GBT_ILP 4
+#endif
+constexpr int GBT_ILP = HARL_GBT_ILP;    // trees walked side by side
 constexpr int GBT_WALK_MAX_DEPTH = 24;   // fixed-depth walk up to this depth
 constexpr int GBT2_ROWS = 64;
 constexpr int GBT2_THREADS = GBT2_ROWS * GBT2_GROUPS;

@@ -51,7 +51,10 @@ static_assert(PPO_TM >= 1 && HARL_PPO_WIDE >= 1 && PPO_THREADS <= 1024,
 // Latency-bound small-batch layers: every thread keeps PPO_UNR weight
 // loads in flight (issued before the FMAs that consume them); the CTA's
 // row activations live in shared memory.
-constexpr int PPO_UNR = 16;
+#ifndef HARL_PPO_UNR
+#define HARL_PPO_UNR 16
+#endif
+constexpr int PPO_UNR = HARL_PPO_UNR;
 
 // Each output is split over up to PPO_SPLIT threads along the reduction
 // (contiguous k ranges summed in part order: deterministic), so a thread's

@@ -614,6 +614,7 @@ def kernel_work(tables, H: int, P: int):
         "k_ppo_rows": ("fp64", 3 * (pol + val)),
         "k_ppo_rows_tc": ("fp64", 3 * (pol + val)),
         "k_ppo_wgrad": ("fp64", None),        # 2 * B per parameter, below
+        "k_ppo_wgrad_spec": ("fp64", None),   # the same, Adam fused in
         "k_ppo_adam": ("hbm", 60),            # per parameter
     }
 
@@ -634,7 +635,7 @@ def roofline_table(native, tables, H, P, peaks, n_params):
                "units": units}
         if name in work and ms > 0 and units > 0:
             bound, per = work[name]
-            if name == "k_ppo_wgrad":
+            if name in ("k_ppo_wgrad", "k_ppo_wgrad_spec"):
                 per = 2 * n_params
             q = per * units / (ms * 1e-3)
             ach = q / 1e9 if bound == "hbm" else q / 1e12
@@ -877,7 +878,8 @@ def main():
                                  "k_policy_tc", "k_policy_tc64",
                                  "k_value_tc", "k_sample_rows",
                                  "k_featurize2", "k_gbt_finish",
-                                 "k_ppo_rows", "k_ppo_wgrad")}}
+                                 "k_ppo_rows", "k_ppo_wgrad",
+                                 "k_ppo_wgrad_spec")}}
     if not args.no_cpu_baseline and world == 1:   # rank 0 at N=1 only
         cb = cpu_pool(args.config, P, 0, 1)
         line["cpu_baseline"] = {

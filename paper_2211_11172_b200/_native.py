@@ -214,6 +214,7 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 _lib = None
+_device_ok = False     # a CUDA device was seen (checked once, not per call)
 
 
 def load(require_device: bool = True):
@@ -238,11 +239,12 @@ def load(require_device: bool = True):
         if lib.harl_abi_version() != 1:
             raise DeviceError("ABI version mismatch")
         _lib = lib
-    if require_device:
+    if require_device and not _device_ok:
         import torch
         if not torch.cuda.is_available():
             raise DeviceError("no CUDA device: the B200 path has no CPU "
                               "fallback")
+        globals()["_device_ok"] = True
     return _lib
 
 

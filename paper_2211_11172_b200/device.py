@@ -49,7 +49,10 @@ def _ptr(t) -> int | None:
 
 
 def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """The current CUDA stream of the current device as a raw handle (the
+    torch internals behind ``torch.cuda.current_stream().cuda_stream``,
+    without building a Stream object per launch)."""
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def _dev(device=None):
@@ -1501,8 +1504,7 @@ class DeviceAgent:
         src = self.head0_src.ctypes.data_as(C.c_void_p)
         # speculative gradients + Adam (single device, not the cooperative
         # variant); the backup restores a flagged update (restore_diverged)
-        spec = _PPO_SPEC and phase == 3 and \
-            os.environ.get("HARL_PPO_FUSED_ADAM") != "1"
+        spec = _PPO_SPEC and phase == 3 and not _PPO_COOP
         # (launch count from the library: 2 when wgrad and Adam run as one
         # kernel, 3 otherwise)
         with PF.span("ppo", B, launches=None):
@@ -1637,6 +1639,7 @@ PPO_SPECULATIVE = 8
 # gradients + Adam in one launch, restored on divergence
 # (HARL_PPO_SPEC=0: the separate k_ppo_wgrad + k_ppo_adam launches)
 _PPO_SPEC = os.environ.get("HARL_PPO_SPEC", "1") != "0"
+_PPO_COOP = os.environ.get("HARL_PPO_FUSED_ADAM") == "1"
 
 
 _POOL = None

@@ -794,7 +794,16 @@ class EpisodeEngine:
             if step["ppo"]:
                 B = step["ppo"]
                 idx = gen.choice(len(self.replay), size=B, replace=False)
-                slots_t = torch.from_numpy(self.replay.slots_of(idx)).to(self.dev)
+                # through this update's row of the pinned table block: a
+                # pageable copy would synchronise the stream every update
+                sl = self.replay.slots_of(idx)
+                pin = b.pins["slot"]
+                if pin.is_pinned() and B <= pin.shape[1] and ppo_k < pin.shape[0]:
+                    pin[ppo_k, :B].numpy()[:] = sl
+                    b.slot_tab[ppo_k, :B].copy_(pin[ppo_k, :B], non_blocking=True)
+                    slots_t = b.slot_tab[ppo_k, :B]
+                else:
+                    slots_t = torch.from_numpy(sl).to(self.dev)
                 a = self.agent
                 a.opt_pi.t += 1
                 a.opt_v.t += 1

@@ -36,8 +36,6 @@ __device__ inline void finish_row(const FinishArgs& a,
   const uint8_t* __restrict__ knobs_new = io.knobs_new;
   uint16_t* __restrict__ log_tiles = log.tiles;
   uint8_t* __restrict__ log_knobs = log.knobs;
-  const double* feat = io.feat;
-  const double* feat_new = io.feat_new;
   const double* new_score = io.new_score;
   const double* reward = io.reward;
   const float* v_cur = io.v_cur;

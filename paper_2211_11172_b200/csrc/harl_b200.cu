@@ -1997,13 +1997,11 @@ int harl_ppo_update(const harl_net_layout* pol, const harl_net_layout* val,
   char* sc = (char*)scratch;
   double* rows = (double*)sc;
   double* rowout = rows + (int64_t)B * row_stride;
-  GradJob* djobs = (GradJob*)(rowout + (int64_t)B * 4);
   GradJob jobs[4 * (HARL_MAX_LAYERS + 2)];
   int n_jobs = 0, n_tiles = 0;
   build_grad_jobs(*pol, *val, jobs, &n_jobs, &n_tiles);
   // the job table is passed by value (no host->device copy: the call is
   // legal inside CUDA-graph capture)
-  (void)djobs;
   PpoArgs a;
   memset(&a, 0, sizeof(a));
   a.B = B;
